@@ -1,0 +1,176 @@
+/*
+ * nld_b200.h -- C-ABI of the B200-native ANOVA-Laplacian hot path.
+ *
+ * This is the drop-in boundary for the reference package `nldenoise`
+ * (/root/reference/pkg/src/nldenoise).  The reference is in-process Python,
+ * so its "FFI" is its Python call surface; each entry point below replaces
+ * one reference interface (file:line cited) and is bound by the Python shim
+ * `paper_2407_06834_b200/_lib.py` through ctypes.
+ *
+ * Conventions
+ *  - every function returns an int status: NLD_OK or one of NLD_ERR_*;
+ *    nld_last_error() returns a thread-local message for the last failure.
+ *    The codes map one-to-one onto the reference exception classes
+ *    (errors.py:4-45).
+ *  - vectors and features are DEVICE pointers (fp64) unless stated;
+ *    `stream` is a cudaStream_t (NULL = legacy default stream).
+ *  - batched right-hand sides are row-major [nrhs][n] with leading
+ *    dimension `ld` (>= n).
+ *  - no torch types cross this boundary.
+ */
+#ifndef NLD_B200_H
+#define NLD_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NLD_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define NLD_API __attribute__((visibility("default")))
+#else
+#define NLD_API
+#endif
+
+/* status codes -> reference exceptions (errors.py) */
+#define NLD_OK 0
+#define NLD_ERR_DIMENSION 1   /* DimensionMismatchError (errors.py:24)      */
+#define NLD_ERR_SCALING 2     /* ScalingOverflowError  (errors.py:28-29)    */
+#define NLD_ERR_WINDOW 3      /* WindowSizeError       (errors.py:32-33)    */
+#define NLD_ERR_DENSE_LIMIT 4 /* DenseLimitError       (errors.py:36-37)    */
+#define NLD_ERR_BREAKDOWN 5   /* SolverBreakdownError  (errors.py:40-41)    */
+#define NLD_ERR_VALUE 6       /* ValueError                                 */
+#define NLD_ERR_CUDA 7        /* RuntimeError: CUDA failure / no device     */
+
+/* operator kinds for nld_op_apply */
+#define NLD_APPLY_GAMMA 0          /* Gamma v            kernel.py:118-127   */
+#define NLD_APPLY_GAMMA_SQUARED 1  /* squared subkernels kernel.py:129-140   */
+#define NLD_APPLY_SYSTEM 2         /* lam v + mu(eta v - Gamma v) linops.py:48-50 */
+#define NLD_APPLY_LAPLACIAN 3      /* eta v - Gamma v    linops.py:43-46     */
+#define NLD_APPLY_WINDOW_SUM 4     /* sum_l G_l v (unit diagonal kept)       */
+
+/* preconditioners for nld_cg_solve (linops.py:447-454) */
+#define NLD_PREC_NONE 0
+#define NLD_PREC_JACOBI 1
+#define NLD_PREC_L2 2
+
+typedef struct nld_operator nld_operator;
+
+/* NFFT / fast-summation parameters, FastsumPlan.build (transform.py:273-283).
+ * n_expansion <= 0 selects the reference's adaptive expansion_degree
+ * (transform.py:254-258); mode 0 = "fast", 1 = "exact" (kernel.py:28-29). */
+typedef struct {
+  int32_t n_expansion;
+  int32_t cutoff;
+  double oversampling;
+  double rmax;
+  double truncation_eps;
+  int32_t mode;
+  int32_t reserved;
+  int64_t dense_limit;
+} nld_params;
+
+/* per-window plan summary (FastsumPlan fields, transform.py:261-270) */
+typedef struct {
+  int32_t dim;
+  int32_t bandwidth;      /* N_d                                   */
+  int32_t grid;           /* oversampled n = 2 ceil(os N_d / 2)    */
+  int32_t cutoff;
+  double center[3];
+  double scale;
+  double sig_scaled;
+  int32_t box_lo[3];      /* support box of the spread grid        */
+  int32_t box_w[3];
+  int64_t n_cells;        /* occupied stencil cells                */
+  int64_t n_subproblems;  /* work items of <= P nodes of one cell  */
+  int64_t n_edge;         /* nodes with 2m+1 nonzero weights       */
+} nld_window_info;
+
+/* per-call stage timings (CUDA events), last nld_op_apply */
+typedef struct {
+  float spread_ms;
+  float assemble_ms;
+  float conv_ms;
+  float gather_ms;
+  float epilogue_ms;
+  float total_ms;
+  int32_t launches;
+  int32_t reserved;
+} nld_stats;
+
+NLD_API const char* nld_last_error(void);
+NLD_API int nld_abi_version(void);
+
+/* AnovaOperator.__init__ + lazy _build_plans (kernel.py:28-77,
+ * transform.py:272-320).  features_dev: (n, n_features) row-major fp64 on the
+ * device; windows given as CSR on the HOST: window w uses feature columns
+ * window_index[window_offset[w] .. window_offset[w+1]).  Plans, node tables,
+ * the cell sort and the subproblem lists are built here and owned by the
+ * handle; the features are copied per window as the reference does
+ * (kernel.py:73). */
+NLD_API int nld_op_create(const double* features_dev, int64_t n, int32_t n_features,
+                  const int32_t* window_index, const int32_t* window_offset,
+                  int32_t n_windows, double sigma, const nld_params* params,
+                  void* stream, nld_operator** out);
+NLD_API int nld_op_destroy(nld_operator* op);
+
+/* One fused product per right-hand side (kernel.py:79-93, linops.py:43-50).
+ * coef: per-rhs (lam, mu) pairs for NLD_APPLY_SYSTEM, ignored otherwise.
+ * NLD_APPLY_SYSTEM/LAPLACIAN use the cached degree (nld_op_degree). */
+NLD_API int nld_op_apply(nld_operator* op, int32_t kind, const double* v, double* out,
+                 int32_t nrhs, int64_t ld, const double* coef_host,
+                 void* stream);
+
+/* eta = Gamma 1 (kernel.py:142-146), cached on the device; squared != 0
+ * gives degree_squared (kernel.py:148-154).  eta_out may be NULL (just
+ * build the cache) or a device buffer of n doubles. */
+NLD_API int nld_op_degree(nld_operator* op, int32_t squared, double* eta_out,
+                  void* stream);
+
+/* dense kernel matrix with zero diagonal, (n, n) row-major device buffer
+ * (kernel.py:156-158); NLD_ERR_DENSE_LIMIT above params.dense_limit. */
+NLD_API int nld_op_assemble_dense(nld_operator* op, int32_t squared, double* out,
+                          void* stream);
+
+NLD_API int nld_op_window_info(const nld_operator* op, int32_t window,
+                       nld_window_info* out);
+NLD_API int nld_op_stats(const nld_operator* op, nld_stats* out);
+NLD_API int nld_op_set_timing(nld_operator* op, int32_t enabled);
+
+/* deflated_solve / plain_solve (linops.py:263-319) on nrhs systems
+ * A_r = lam_r I + mu_r (diag eta - Gamma) sharing every Gamma application.
+ * f, u: device [nrhs][ld].  lam/mu/iterations/relres/converged are HOST
+ * arrays of nrhs; history (HOST, may be NULL) is [nrhs][history_cap] and
+ * receives residual_history (linops.py:184-190), padded with NaN.
+ * deflate != 0 -> deflated_solve (constant eigenvector split off),
+ * 0 -> plain_solve. */
+NLD_API int nld_cg_solve(nld_operator* op, const double* f, double* u, int32_t nrhs,
+                 int64_t ld, const double* lam, const double* mu,
+                 int32_t precond, int32_t deflate, double tol, int32_t maxit,
+                 int32_t warm_start, int32_t* iterations, double* relres,
+                 int32_t* converged, double* history, int32_t history_cap,
+                 void* stream);
+
+/* DeflatingBasis.apply / apply_adjoint (linops.py:134-176) for a device
+ * vector v of length n (v[0] != 0): out = U x or U^T x. */
+NLD_API int nld_basis_apply(const double* v, const double* x, double* out, int64_t n,
+                    int32_t adjoint, void* stream);
+
+/* scs_up / scs_down (linops.py:114-131) on device vectors. */
+NLD_API int nld_scs(const double* x, double* out, int64_t n, int32_t down,
+            void* stream);
+
+/* small device vector kernels used by the generic pcg (linops.py:193-244):
+ * out = a x + b y;   dots[k] = <x_k, y_k> for k < count (HOST result). */
+NLD_API int nld_axpby(double a, const double* x, double b, const double* y,
+              double* out, int64_t n, void* stream);
+NLD_API int nld_dot(const double* x, const double* y, int64_t n, double* result,
+            void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NLD_B200_H */

@@ -1,0 +1,820 @@
+// One application of the ANOVA kernel: per window spread -> fused separable
+// convolution (FFT, x kernel coefficients, FFT) -> gather, summed over
+// windows with the degree/diagonal epilogue fused into one pass.
+//
+// Reference path (one window): gauss_transform_fast (transform.py:323-333)
+//   = nfft_adjoint (spread _kernels.py:48-88, ifftn, crop, deconvolve)
+//   x kernel_coeffs
+//   nfft (deconvolve, embed, fftn, gather _kernels.py:91-136);
+// summed over windows in AnovaOperator._fast_apply (kernel.py:79-93) and
+// shifted in ShiftedSystem.apply (linops.py:43-50).
+//
+// B200 design:
+//  * spread: one CTA per subproblem (<= 512 nodes of ONE stencil cell, sorted
+//    once at plan build).  Threads own (a,b) pairs of the (2m)^3 block and
+//    accumulate the c-axis in registers; node weights are staged in shared
+//    memory and read by broadcast.  No atomics: each subproblem writes its
+//    partial block, and `assemble` sums blocks per grid point in a fixed
+//    order (deterministic).
+//  * conv: the grid operation FFT -> x E_k -> FFT is exactly a separable
+//    circulant convolution with a complex 1-D kernel K (the unpaired -M/2
+//    frequency makes it complex); it runs pruned to the support box.
+//  * gather: one CTA per subproblem; the (2m)^3 grid block of its cell sits in
+//    shared memory, each thread owns a node and contracts a -> b -> c.
+#include <algorithm>
+
+#include "nld_internal.cuh"
+
+namespace nld {
+
+namespace {
+
+constexpr int kThreads = 128;
+constexpr int kChunk = 128;
+
+template <int D, int MC>
+struct Geo {
+  static constexpr int S = 2 * MC;
+  static constexpr int SA = (D == 3) ? S : 1;
+  static constexpr int SB = (D >= 2) ? S : 1;
+  static constexpr int SC = S;
+  static constexpr int PAIRS = SA * SB;
+  static constexpr int R = (PAIRS + 31) / 32;
+  static constexpr int TEAM_RAW = (PAIRS + R - 1) / R;
+  static constexpr int TEAM = TEAM_RAW <= 1 ? 1 : TEAM_RAW <= 2 ? 2 : TEAM_RAW <= 4 ? 4
+                              : TEAM_RAW <= 8 ? 8 : TEAM_RAW <= 16 ? 16 : 32;
+  static constexpr int NTEAM = kThreads / TEAM;
+  static constexpr int ROW = S * D;                    // global row (doubles)
+  static constexpr int SROW_RAW = D * S + 1;            // [C][B][A'] + v slot
+  static constexpr int SROW = (SROW_RAW % 2) ? SROW_RAW + 1 : SROW_RAW;
+  static constexpr int BLK = SA * SB * SC;
+  static constexpr int NWARP = kThreads / 32;
+  static constexpr int SMEM_STAGE = kChunk * SROW + kChunk;
+  static constexpr int SMEM_RED = NWARP * BLK;
+  static constexpr int SMEM = SMEM_STAGE > SMEM_RED ? SMEM_STAGE : SMEM_RED;
+};
+
+__device__ __forceinline__ int wrap_pos(int p, int w) {
+  // box coordinate after a stencil offset; only exceeds [0,w) in wrap mode
+  if (p >= w) p -= w;
+  if (p < 0) p += w;
+  return p;
+}
+
+template <int D>
+__device__ __forceinline__ int64_t box_flat(const WinDev& wd, const int* p) {
+  int64_t f = 0;
+  for (int s = 0; s < D; ++s) f = f * wd.box_w[s] + p[s];
+  return f;
+}
+
+// ---- spread ---------------------------------------------------------------
+
+template <int D, int MC>
+__global__ void __launch_bounds__(kThreads)
+k_spread(const SubDev* __restrict__ subs, const WinDev* __restrict__ wins,
+         const double* __restrict__ rows, const int32_t* __restrict__ pix,
+         const double* __restrict__ v, int64_t ldv, double* __restrict__ blocks,
+         int64_t blk_ld) {
+  using G = Geo<D, MC>;
+  extern __shared__ double sm[];
+  double* sv = sm + kChunk * G::SROW;
+  const SubDev sd = subs[blockIdx.x];
+  const int rhs = blockIdx.y;
+  const WinDev wd = wins[sd.win];
+  const double* __restrict__ vr = v + rhs * ldv;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int tl = lane & (G::TEAM - 1);
+  const int team = tid / G::TEAM;
+
+  int pa[G::R], pb[G::R];
+  bool pok[G::R];
+#pragma unroll
+  for (int r = 0; r < G::R; ++r) {
+    int p = tl + G::TEAM * r;
+    pok[r] = p < G::PAIRS;
+    pa[r] = pok[r] ? p / G::SB : 0;
+    pb[r] = pok[r] ? p % G::SB : 0;
+  }
+  double acc[G::R][G::SC];
+#pragma unroll
+  for (int r = 0; r < G::R; ++r)
+#pragma unroll
+    for (int c = 0; c < G::SC; ++c) acc[r][c] = 0.0;
+
+  const int64_t local = sd.start - wd.node_off;
+  const double* __restrict__ rw = rows + wd.row_off + local * G::ROW;
+  const int32_t* __restrict__ pw = pix + sd.start;
+
+  for (int c0 = 0; c0 < sd.count; c0 += kChunk) {
+    const int cn = min(kChunk, sd.count - c0);
+    __syncthreads();
+    for (int e = tid; e < cn; e += kThreads) sv[e] = vr[pw[c0 + e]];
+    __syncthreads();
+    // stage rows: dim s -> smem segment (D-1-s)*S; dim 0 of a 3-D window is
+    // pre-multiplied by v; lower-dimensional windows keep v in slot D*S.
+    for (int e = tid; e < cn * G::ROW; e += kThreads) {
+      const int pt = e / G::ROW;
+      const int k = e - pt * G::ROW;
+      const int s = k / G::S;
+      const int i = k - s * G::S;
+      double val = rw[(int64_t)(c0 + pt) * G::ROW + k];
+      if (D == 3 && s == 0) val *= sv[pt];
+      sm[pt * G::SROW + (D - 1 - s) * G::S + i] = val;
+    }
+    if (D < 3)
+      for (int e = tid; e < cn; e += kThreads) sm[e * G::SROW + D * G::S] = sv[e];
+    __syncthreads();
+    for (int pt = team; pt < cn; pt += G::NTEAM) {
+      const double* row = sm + pt * G::SROW;
+      double cw[G::SC];
+#pragma unroll
+      for (int c = 0; c < G::SC; c += 2) {
+        double2 t = *reinterpret_cast<const double2*>(row + c);
+        cw[c] = t.x;
+        cw[c + 1] = t.y;
+      }
+#pragma unroll
+      for (int r = 0; r < G::R; ++r) {
+        double ab;
+        if (D == 3) ab = row[2 * G::S + pa[r]] * row[G::S + pb[r]];
+        else if (D == 2) ab = row[2 * G::S] * row[G::S + pb[r]];
+        else ab = row[G::S];
+#pragma unroll
+        for (int c = 0; c < G::SC; ++c) acc[r][c] = fma(ab, cw[c], acc[r][c]);
+      }
+    }
+  }
+  // reduce the teams of a warp, then the warps of the CTA
+#pragma unroll
+  for (int off = G::TEAM; off < 32; off <<= 1)
+#pragma unroll
+    for (int r = 0; r < G::R; ++r)
+#pragma unroll
+      for (int c = 0; c < G::SC; ++c)
+        acc[r][c] += __shfl_xor_sync(0xffffffffu, acc[r][c], off);
+  __syncthreads();
+  const int warp = tid >> 5;
+  if (lane < G::TEAM) {
+#pragma unroll
+    for (int r = 0; r < G::R; ++r)
+      if (pok[r]) {
+        const int p = tl + G::TEAM * r;
+#pragma unroll
+        for (int c = 0; c < G::SC; ++c) sm[warp * G::BLK + p * G::SC + c] = acc[r][c];
+      }
+  }
+  __syncthreads();
+  double* __restrict__ out = blocks + rhs * blk_ld + sd.block;
+  for (int e = tid; e < G::BLK; e += kThreads) {
+    double s = sm[e];
+#pragma unroll
+    for (int w = 1; w < G::NWARP; ++w) s += sm[w * G::BLK + e];
+    out[e] = s;
+  }
+}
+
+// ---- assemble: grid point <- sum of the blocks of the cells covering it -----
+
+__global__ void k_assemble(const WinDev* __restrict__ wins, int L,
+                           const int32_t* __restrict__ cellmap,
+                           const CellDev* __restrict__ cells,
+                           const double* __restrict__ blocks, int64_t blk_ld,
+                           double* __restrict__ grid, int64_t grid_ld) {
+  const int w = blockIdx.y;
+  const int rhs = blockIdx.z;
+  const WinDev wd = wins[w];
+  const double* __restrict__ bl = blocks + rhs * blk_ld;
+  double* __restrict__ g = grid + rhs * grid_ld + wd.grid_off;
+  const int S = wd.S;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < wd.box_size;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    if (!wd.fast) {
+      g[e] = 0.0;
+      continue;
+    }
+    int t[3] = {0, 0, 0};
+    int64_t rem = e;
+    for (int s = wd.d - 1; s >= 0; --s) {
+      t[s] = (int)(rem % wd.box_w[s]);
+      rem /= wd.box_w[s];
+    }
+    double sum = 0.0;
+    const int o0n = wd.d == 3 ? S : 1;
+    const int o1n = wd.d >= 2 ? S : 1;
+    for (int o0 = 0; o0 < o0n; ++o0)
+      for (int o1 = 0; o1 < o1n; ++o1)
+        for (int o2 = 0; o2 < S; ++o2) {
+          // offsets along dims (d-3+..): map (o0,o1,o2) onto the window dims
+          int off[3];
+          if (wd.d == 3) { off[0] = o0; off[1] = o1; off[2] = o2; }
+          else if (wd.d == 2) { off[0] = o1; off[1] = o2; off[2] = 0; }
+          else { off[0] = o2; off[1] = 0; off[2] = 0; }
+          int c[3];
+          bool ok = true;
+          for (int s = 0; s < wd.d; ++s) {
+            int cc = t[s] - off[s];
+            if (cc < 0) {
+              if (wd.wrap) cc += wd.box_w[s];
+              else ok = false;
+            }
+            c[s] = cc;
+          }
+          if (!ok) continue;
+          int64_t key = 0;
+          for (int s = 0; s < wd.d; ++s) key = key * wd.box_w[s] + c[s];
+          int cell = cellmap[wd.cellmap_off + key];
+          if (cell < 0) continue;
+          const CellDev cd = cells[cell];
+          int64_t inner = 0;
+          for (int s = 0; s < wd.d; ++s) inner = inner * S + off[s];
+          for (int q = 0; q < cd.nsub; ++q) sum += bl[cd.block0 + (int64_t)q * cd.blk + inner];
+        }
+    g[e] = sum;
+  }
+}
+
+// ---- edge nodes: the i = 0 / i = 2m+1 stencil slices (rare) ---------------
+
+__device__ __forceinline__ bool edge_combo(const EdgeDev& ed, int d, int W, int S,
+                                           int lin, int* ii, double* wprod) {
+  // decode lin into per-dim offsets 0..W-1; reject the principal part
+  bool principal = true;
+  double w = 1.0;
+  for (int s = d - 1; s >= 0; --s) {
+    ii[s] = lin % W;
+    lin /= W;
+    if (ii[s] < 1 || ii[s] > S) principal = false;
+    w *= ed.w[s][ii[s]];
+  }
+  *wprod = w;
+  return !principal && w != 0.0;
+}
+
+__global__ void k_spread_edges(const EdgeDev* __restrict__ edges, int64_t ne,
+                               const WinDev* __restrict__ wins,
+                               const double* __restrict__ v, int64_t ldv,
+                               double* __restrict__ grid, int64_t grid_ld) {
+  const int rhs = blockIdx.y;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < ne;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const EdgeDev& ed = edges[k];
+    const WinDev wd = wins[ed.win];
+    const double val = v[rhs * ldv + ed.pix];
+    const int W = wd.S + 2;
+    int total = 1;
+    for (int s = 0; s < wd.d; ++s) total *= W;
+    for (int lin = 0; lin < total; ++lin) {
+      int ii[3];
+      double wp;
+      if (!edge_combo(ed, wd.d, W, wd.S, lin, ii, &wp)) continue;
+      int p[3];
+      for (int s = 0; s < wd.d; ++s) p[s] = wrap_pos(ed.cc[s] + ii[s] - 1, wd.box_w[s]);
+      int64_t f = 0;
+      for (int s = 0; s < wd.d; ++s) f = f * wd.box_w[s] + p[s];
+      atomicAdd(grid + rhs * grid_ld + wd.grid_off + f, val * wp);
+    }
+  }
+}
+
+__global__ void k_gather_edges(const EdgeDev* __restrict__ edges, int64_t ne,
+                               const WinDev* __restrict__ wins,
+                               const double* __restrict__ grid, int64_t grid_ld,
+                               double* __restrict__ wout, int64_t N, int L) {
+  const int rhs = blockIdx.y;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < ne;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const EdgeDev& ed = edges[k];
+    const WinDev wd = wins[ed.win];
+    const int W = wd.S + 2;
+    int total = 1;
+    for (int s = 0; s < wd.d; ++s) total *= W;
+    double y = 0.0;
+    for (int lin = 0; lin < total; ++lin) {
+      int ii[3];
+      double wp;
+      if (!edge_combo(ed, wd.d, W, wd.S, lin, ii, &wp)) continue;
+      int p[3];
+      for (int s = 0; s < wd.d; ++s) p[s] = wrap_pos(ed.cc[s] + ii[s] - 1, wd.box_w[s]);
+      int64_t f = 0;
+      for (int s = 0; s < wd.d; ++s) f = f * wd.box_w[s] + p[s];
+      y += grid[rhs * grid_ld + wd.grid_off + f] * wp;
+    }
+    wout[((int64_t)rhs * L + ed.win) * N + ed.pix] += y;
+  }
+}
+
+// ---- generic path (cutoffs without a templated kernel) --------------------
+
+__global__ void k_spread_generic(const WinDev* __restrict__ wins, int w,
+                                 const double* __restrict__ rows,
+                                 const int32_t* __restrict__ pix,
+                                 const int32_t* __restrict__ key,
+                                 const double* __restrict__ v, int64_t ldv,
+                                 double* __restrict__ grid, int64_t grid_ld, int64_t N) {
+  const int rhs = blockIdx.y;
+  const WinDev wd = wins[w];
+  const int S = wd.S, d = wd.d;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < N;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const double* row = rows + wd.row_off + e * (int64_t)S * d;
+    const double val = v[rhs * ldv + pix[wd.node_off + e]];
+    int cc[3] = {0, 0, 0};
+    int rem = key[wd.node_off + e];
+    for (int s = d - 1; s >= 0; --s) {
+      cc[s] = rem % wd.box_w[s];
+      rem /= wd.box_w[s];
+    }
+    int total = 1;
+    for (int s = 0; s < d; ++s) total *= S;
+    for (int lin = 0; lin < total; ++lin) {
+      int l = lin;
+      double wp = val;
+      int64_t f = 0;
+      int ii[3];
+      for (int s = d - 1; s >= 0; --s) {
+        ii[s] = l % S;
+        l /= S;
+      }
+      for (int s = 0; s < d; ++s) {
+        wp *= row[s * S + ii[s]];
+        f = f * wd.box_w[s] + wrap_pos(cc[s] + ii[s], wd.box_w[s]);
+      }
+      atomicAdd(grid + rhs * grid_ld + wd.grid_off + f, wp);
+    }
+  }
+}
+
+__global__ void k_gather_generic(const WinDev* __restrict__ wins, int w, int L,
+                                 const double* __restrict__ rows,
+                                 const int32_t* __restrict__ pix,
+                                 const int32_t* __restrict__ key,
+                                 const double* __restrict__ grid, int64_t grid_ld,
+                                 double* __restrict__ wout, int64_t N) {
+  const int rhs = blockIdx.y;
+  const WinDev wd = wins[w];
+  const int S = wd.S, d = wd.d;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < N;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const double* row = rows + wd.row_off + e * (int64_t)S * d;
+    int cc[3] = {0, 0, 0};
+    int rem = key[wd.node_off + e];
+    for (int s = d - 1; s >= 0; --s) {
+      cc[s] = rem % wd.box_w[s];
+      rem /= wd.box_w[s];
+    }
+    int total = 1;
+    for (int s = 0; s < d; ++s) total *= S;
+    double y = 0.0;
+    for (int lin = 0; lin < total; ++lin) {
+      int l = lin;
+      double wp = 1.0;
+      int64_t f = 0;
+      int ii[3];
+      for (int s = d - 1; s >= 0; --s) {
+        ii[s] = l % S;
+        l /= S;
+      }
+      for (int s = 0; s < d; ++s) {
+        wp *= row[s * S + ii[s]];
+        f = f * wd.box_w[s] + wrap_pos(cc[s] + ii[s], wd.box_w[s]);
+      }
+      y += grid[rhs * grid_ld + wd.grid_off + f] * wp;
+    }
+    wout[((int64_t)rhs * L + w) * N + pix[wd.node_off + e]] = y;
+  }
+}
+
+// ---- separable convolution pass --------------------------------------------
+
+__global__ void k_conv(const WinDev* __restrict__ wins, int pass,
+                       const double2* __restrict__ K,
+                       const double* __restrict__ gin, const double2* __restrict__ cin,
+                       double2* __restrict__ cout, double* __restrict__ gout,
+                       int64_t grid_ld) {
+  const int w = blockIdx.y;
+  const int rhs = blockIdx.z;
+  const WinDev wd = wins[w];
+  if (pass >= wd.d) return;
+  const int axis = wd.d - 1 - pass;
+  const bool first = pass == 0;
+  const bool last = pass == wd.d - 1;
+  const double2* __restrict__ kw = K + wd.kern_off;
+  const int n = wd.n;
+  int64_t stride = 1;
+  for (int s = wd.d - 1; s > axis; --s) stride *= wd.box_w[s];
+  const int wa = wd.box_w[axis];
+  const int64_t base = rhs * grid_ld + wd.grid_off;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < wd.box_size;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int t = (int)((e / stride) % wa);
+    const int64_t line = e - (int64_t)t * stride;
+    double re = 0.0, im = 0.0;
+    for (int s = 0; s < wa; ++s) {
+      int dl = (s - t) % n;
+      if (dl < 0) dl += n;
+      const double2 k = kw[dl];
+      const int64_t src = base + line + (int64_t)s * stride;
+      if (first) {
+        const double g = gin[src];
+        re = fma(k.x, g, re);
+        im = fma(k.y, g, im);
+      } else {
+        const double2 x = cin[src];
+        re = fma(k.x, x.x, re);
+        re = fma(-k.y, x.y, re);
+        im = fma(k.x, x.y, im);
+        im = fma(k.y, x.x, im);
+      }
+    }
+    if (last) gout[base + e] = re;
+    else cout[base + e] = make_double2(re, im);
+  }
+}
+
+// ---- gather -------------------------------------------------------------
+
+template <int D, int MC>
+__global__ void __launch_bounds__(kThreads)
+k_gather(const SubDev* __restrict__ subs, const CellDev* __restrict__ cells,
+         const WinDev* __restrict__ wins, const double* __restrict__ rows,
+         const int32_t* __restrict__ pix, const double* __restrict__ grid,
+         int64_t grid_ld, double* __restrict__ wout, int64_t N, int L) {
+  using G = Geo<D, MC>;
+  __shared__ double gb[G::BLK];
+  const SubDev sd = subs[blockIdx.x];
+  const int rhs = blockIdx.y;
+  const CellDev cd = cells[sd.cell];
+  const WinDev wd = wins[sd.win];
+  const double* __restrict__ g = grid + rhs * grid_ld + wd.grid_off;
+  for (int e = threadIdx.x; e < G::BLK; e += kThreads) {
+    int off[3];
+    off[0] = e / (G::SB * G::SC);
+    off[1] = (e / G::SC) % G::SB;
+    off[2] = e % G::SC;
+    int p[3];
+    // block dims (a,b,c) -> window dims
+    if (D == 3) {
+      for (int s = 0; s < 3; ++s) p[s] = wrap_pos(cd.cc[s] + off[s], wd.box_w[s]);
+    } else if (D == 2) {
+      p[0] = wrap_pos(cd.cc[0] + off[1], wd.box_w[0]);
+      p[1] = wrap_pos(cd.cc[1] + off[2], wd.box_w[1]);
+    } else {
+      p[0] = wrap_pos(cd.cc[0] + off[2], wd.box_w[0]);
+    }
+    gb[e] = g[box_flat<D>(wd, p)];
+  }
+  __syncthreads();
+  const int64_t local = sd.start - wd.node_off;
+  const double* __restrict__ rw = rows + wd.row_off + local * G::ROW;
+  double* __restrict__ out = wout + ((int64_t)rhs * L + sd.win) * N;
+  for (int j = threadIdx.x; j < sd.count; j += kThreads) {
+    double wrow[G::ROW];
+    const double2* src = reinterpret_cast<const double2*>(rw + (int64_t)j * G::ROW);
+#pragma unroll
+    for (int k = 0; k < G::ROW / 2; ++k) {
+      double2 t = __ldg(src + k);
+      wrow[2 * k] = t.x;
+      wrow[2 * k + 1] = t.y;
+    }
+    // wrow: [dim0 S][dim1 S][dim2 S]; block order [a][b][c] = dims (0,1,2)
+    double y = 0.0;
+#pragma unroll
+    for (int a = 0; a < G::SA; ++a) {
+      double ua = 0.0;
+#pragma unroll
+      for (int b = 0; b < G::SB; ++b) {
+        const double* gr = gb + (a * G::SB + b) * G::SC;
+        double t = 0.0;
+#pragma unroll
+        for (int c = 0; c < G::SC; c += 2) {
+          double2 gg = *reinterpret_cast<const double2*>(gr + c);
+          t = fma(gg.x, wrow[(D - 1) * G::S + c], t);
+          t = fma(gg.y, wrow[(D - 1) * G::S + c + 1], t);
+        }
+        if (D >= 2) ua = fma(t, wrow[(D - 2) * G::S + b], ua);
+        else ua = t;
+      }
+      if (D == 3) y = fma(ua, wrow[a], y);
+      else y = ua;
+    }
+    out[pix[sd.start + j]] = y;
+  }
+}
+
+// ---- epilogue: window sum + diagonal/degree terms (kernel.py:86-93,
+//      linops.py:43-50) ---------------------------------------------------
+
+__global__ void k_epilogue(int kind, int L, int64_t N, const double* __restrict__ v,
+                           int64_t ldv, const double* __restrict__ wsum, int direct,
+                           double* __restrict__ out, int64_t ldo,
+                           const double* __restrict__ eta,
+                           const double* __restrict__ coef) {
+  const int rhs = blockIdx.y;
+  const double lam = coef ? coef[2 * rhs] : 0.0;
+  const double mu = coef ? coef[2 * rhs + 1] : 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double x = v[rhs * ldv + i];
+    double gam;
+    if (direct) {
+      gam = wsum[rhs * N + i];
+    } else {
+      double s = 0.0;
+      for (int w = 0; w < L; ++w) s += wsum[((int64_t)rhs * L + w) * N + i];
+      if (kind == NLD_APPLY_WINDOW_SUM) {
+        out[rhs * ldo + i] = s;
+        continue;
+      }
+      gam = (s - (double)L * x) / (double)L;
+    }
+    double y;
+    if (kind == NLD_APPLY_SYSTEM) y = lam * x + mu * (eta[i] * x - gam);
+    else if (kind == NLD_APPLY_LAPLACIAN) y = eta[i] * x - gam;
+    else y = gam;
+    out[rhs * ldo + i] = y;
+  }
+}
+
+// ---- dense exact mode (kernel.py:97-114, _kernels.py:205-227) -------------
+
+__global__ void k_dense_apply(const double* __restrict__ F, int64_t N, int D,
+                              const int* __restrict__ widx, const int* __restrict__ woff,
+                              int L, double inv_s2, const double* __restrict__ v,
+                              int64_t ldv, double* __restrict__ out) {
+  const int rhs = blockIdx.y;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int64_t j = 0; j < N; ++j) {
+      if (j == i) continue;
+      double gsum = 0.0;
+      for (int w = 0; w < L; ++w) {
+        double r2 = 0.0;
+        for (int k = woff[w]; k < woff[w + 1]; ++k) {
+          double diff = F[i * D + widx[k]] - F[j * D + widx[k]];
+          r2 += diff * diff;
+        }
+        gsum += exp(-inv_s2 * r2);
+      }
+      acc += (gsum / (double)L) * v[rhs * ldv + j];
+    }
+    out[rhs * N + i] = acc;
+  }
+}
+
+__global__ void k_dense_assemble(const double* __restrict__ F, int64_t N, int D,
+                                 const int* __restrict__ widx, const int* __restrict__ woff,
+                                 int L, double inv_s2, double* __restrict__ out) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < N * N;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / N, j = e % N;
+    double gsum = 0.0;
+    if (i != j) {
+      for (int w = 0; w < L; ++w) {
+        double r2 = 0.0;
+        for (int k = woff[w]; k < woff[w + 1]; ++k) {
+          double diff = F[i * D + widx[k]] - F[j * D + widx[k]];
+          r2 += diff * diff;
+        }
+        gsum += exp(-inv_s2 * r2);
+      }
+    }
+    out[e] = gsum / (double)L;
+  }
+}
+
+int grid_blocks(int64_t n, int threads, int cap = 148 * 8) {
+  int64_t b = (n + threads - 1) / threads;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(b, cap));
+}
+
+template <int D, int MC>
+void launch_spread(const PlanSet& ps, const Workspace& ws, const double* v, int64_t ldv,
+                   int nrhs, cudaStream_t st) {
+  using G = Geo<D, MC>;
+  if (ps.n_subs[D] == 0) return;
+  size_t smem = sizeof(double) * G::SMEM;
+  static bool attr = false;
+  if (!attr) {
+    NLD_CUDA(cudaFuncSetAttribute(k_spread<D, MC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem));
+    attr = true;
+  }
+  dim3 grid((unsigned)ps.n_subs[D], nrhs);
+  k_spread<D, MC><<<grid, kThreads, smem, st>>>(ps.subs[D], ps.wdev, ps.rows, ps.pix, v, ldv,
+                                                ws.blocks, ps.blocks_total);
+  NLD_CUDA(cudaGetLastError());
+}
+
+template <int D, int MC>
+void launch_gather(const PlanSet& ps, const Workspace& ws, int64_t N, int L, int nrhs,
+                   cudaStream_t st) {
+  if (ps.n_subs[D] == 0) return;
+  dim3 grid((unsigned)ps.n_subs[D], nrhs);
+  k_gather<D, MC><<<grid, kThreads, 0, st>>>(ps.subs[D], ps.cells, ps.wdev, ps.rows, ps.pix,
+                                             ws.grid_out, ps.grid_total, ws.wout, N, L);
+  NLD_CUDA(cudaGetLastError());
+}
+
+template <int MC>
+void spread_all(const PlanSet& ps, const Workspace& ws, const double* v, int64_t ldv,
+                int nrhs, cudaStream_t st) {
+  launch_spread<1, MC>(ps, ws, v, ldv, nrhs, st);
+  launch_spread<2, MC>(ps, ws, v, ldv, nrhs, st);
+  launch_spread<3, MC>(ps, ws, v, ldv, nrhs, st);
+}
+
+template <int MC>
+void gather_all(const PlanSet& ps, const Workspace& ws, int64_t N, int L, int nrhs,
+                cudaStream_t st) {
+  launch_gather<1, MC>(ps, ws, N, L, nrhs, st);
+  launch_gather<2, MC>(ps, ws, N, L, nrhs, st);
+  launch_gather<3, MC>(ps, ws, N, L, nrhs, st);
+}
+
+struct EvScope {
+  nld_operator* op;
+  cudaStream_t st;
+  int idx = 0;
+  EvScope(nld_operator* o, cudaStream_t s) : op(o), st(s) {}
+  void mark() {
+    if (op->timing && op->events) cudaEventRecord(op->ev[idx++], st);
+  }
+};
+
+}  // namespace
+
+void ensure_workspace(nld_operator* op, const PlanSet& ps, int nrhs) {
+  Workspace& ws = op->ws;
+  if (ws.nrhs_cap >= nrhs && ws.grid_total >= ps.grid_total &&
+      ws.blocks_total >= ps.blocks_total)
+    return;
+  free_workspace(ws);
+  int cap = std::max(nrhs, 1);
+  int64_t gt = std::max(ps.grid_total, std::max(op->sets[0].grid_total, op->sets[1].grid_total));
+  int64_t bt = std::max(ps.blocks_total, std::max(op->sets[0].blocks_total, op->sets[1].blocks_total));
+  NLD_CUDA(cudaMalloc(&ws.blocks, sizeof(double) * std::max<int64_t>(1, bt) * cap));
+  NLD_CUDA(cudaMalloc(&ws.grid_in, sizeof(double) * std::max<int64_t>(1, gt) * cap));
+  NLD_CUDA(cudaMalloc(&ws.grid_out, sizeof(double) * std::max<int64_t>(1, gt) * cap));
+  NLD_CUDA(cudaMalloc(&ws.cbuf0, sizeof(double2) * std::max<int64_t>(1, gt) * cap));
+  NLD_CUDA(cudaMalloc(&ws.cbuf1, sizeof(double2) * std::max<int64_t>(1, gt) * cap));
+  NLD_CUDA(cudaMalloc(&ws.wout, sizeof(double) * std::max<int64_t>(1, op->N * op->L) * cap));
+  NLD_CUDA(cudaMalloc(&ws.coef, sizeof(double) * 2 * cap));
+  ws.nrhs_cap = cap;
+  ws.grid_total = gt;
+  ws.blocks_total = bt;
+}
+
+void free_workspace(Workspace& ws) {
+  cudaFree(ws.blocks);
+  cudaFree(ws.grid_in);
+  cudaFree(ws.grid_out);
+  cudaFree(ws.cbuf0);
+  cudaFree(ws.cbuf1);
+  cudaFree(ws.wout);
+  cudaFree(ws.coef);
+  ws = Workspace();
+}
+
+void apply_op(nld_operator* op, int which, int kind, const double* v, double* out,
+              int nrhs, int64_t ld, const double* coef_dev, const double* eta,
+              cudaStream_t st) {
+  const PlanSet& ps = op->sets[which];
+  ensure_workspace(op, ps, nrhs);
+  Workspace& ws = op->ws;
+  const int64_t N = op->N;
+  const int L = op->L;
+  const int m = op->params.cutoff;
+  EvScope ev(op, st);
+  ev.mark();
+  // 1. spread (block path)
+  switch (m) {
+    case 3: spread_all<3>(ps, ws, v, ld, nrhs, st); break;
+    case 4: spread_all<4>(ps, ws, v, ld, nrhs, st); break;
+    case 5: spread_all<5>(ps, ws, v, ld, nrhs, st); break;
+    default: break;
+  }
+  ev.mark();
+  // 2. assemble the support boxes
+  {
+    int64_t maxbox = 1;
+    for (const auto& w : ps.wdev_h) maxbox = std::max(maxbox, w.box_size);
+    dim3 grid(grid_blocks(maxbox, 128, 512), L, nrhs);
+    k_assemble<<<grid, 128, 0, st>>>(ps.wdev, L, ps.cellmap, ps.cells, ws.blocks,
+                                     ps.blocks_total, ws.grid_in, ps.grid_total);
+    NLD_CUDA(cudaGetLastError());
+  }
+  // generic windows + edge nodes (atomics on top of the assembled boxes)
+  for (int w = 0; w < L; ++w) {
+    if (ps.wdev_h[w].fast) continue;
+    dim3 grid(grid_blocks(N, 256), nrhs);
+    k_spread_generic<<<grid, 256, 0, st>>>(ps.wdev, w, ps.rows, ps.pix, ps.key, v, ld,
+                                           ws.grid_in, ps.grid_total, N);
+    NLD_CUDA(cudaGetLastError());
+  }
+  if (ps.n_edges) {
+    dim3 grid(grid_blocks(ps.n_edges, 128), nrhs);
+    k_spread_edges<<<grid, 128, 0, st>>>(ps.edges, ps.n_edges, ps.wdev, v, ld, ws.grid_in,
+                                         ps.grid_total);
+    NLD_CUDA(cudaGetLastError());
+  }
+  ev.mark();
+  // 3. separable convolution, one pass per axis
+  {
+    int maxd = 0;
+    int64_t maxbox = 1;
+    for (const auto& w : ps.wdev_h) {
+      maxd = std::max(maxd, w.d);
+      maxbox = std::max(maxbox, w.box_size);
+    }
+    for (int pass = 0; pass < maxd; ++pass) {
+      dim3 grid(grid_blocks(maxbox, 128, 1024), L, nrhs);
+      const double2* cin = (pass % 2 == 1) ? ws.cbuf0 : ws.cbuf1;
+      double2* cout = (pass % 2 == 0) ? ws.cbuf0 : ws.cbuf1;
+      k_conv<<<grid, 128, 0, st>>>(ps.wdev, pass, ps.K, ws.grid_in, cin, cout, ws.grid_out,
+                                   ps.grid_total);
+      NLD_CUDA(cudaGetLastError());
+    }
+  }
+  ev.mark();
+  // 4. gather
+  switch (m) {
+    case 3: gather_all<3>(ps, ws, N, L, nrhs, st); break;
+    case 4: gather_all<4>(ps, ws, N, L, nrhs, st); break;
+    case 5: gather_all<5>(ps, ws, N, L, nrhs, st); break;
+    default: break;
+  }
+  for (int w = 0; w < L; ++w) {
+    if (ps.wdev_h[w].fast) continue;
+    dim3 grid(grid_blocks(N, 256), nrhs);
+    k_gather_generic<<<grid, 256, 0, st>>>(ps.wdev, w, L, ps.rows, ps.pix, ps.key,
+                                           ws.grid_out, ps.grid_total, ws.wout, N);
+    NLD_CUDA(cudaGetLastError());
+  }
+  if (ps.n_edges) {
+    dim3 grid(grid_blocks(ps.n_edges, 128), nrhs);
+    k_gather_edges<<<grid, 128, 0, st>>>(ps.edges, ps.n_edges, ps.wdev, ws.grid_out,
+                                         ps.grid_total, ws.wout, N, L);
+    NLD_CUDA(cudaGetLastError());
+  }
+  ev.mark();
+  // 5. epilogue
+  {
+    dim3 grid(grid_blocks(N, 256, 148 * 16), nrhs);
+    k_epilogue<<<grid, 256, 0, st>>>(kind, L, N, v, ld, ws.wout, 0, out, ld, eta, coef_dev);
+    NLD_CUDA(cudaGetLastError());
+  }
+  ev.mark();
+}
+
+static void dense_tables(nld_operator* op, int** widx, int** woff, cudaStream_t st) {
+  NLD_CUDA(cudaMallocAsync(widx, sizeof(int) * op->win_index.size(), st));
+  NLD_CUDA(cudaMallocAsync(woff, sizeof(int) * op->win_offset.size(), st));
+  NLD_CUDA(cudaMemcpyAsync(*widx, op->win_index.data(), sizeof(int) * op->win_index.size(),
+                           cudaMemcpyHostToDevice, st));
+  NLD_CUDA(cudaMemcpyAsync(*woff, op->win_offset.data(), sizeof(int) * op->win_offset.size(),
+                           cudaMemcpyHostToDevice, st));
+}
+
+void dense_apply(nld_operator* op, int which, int kind, const double* v, double* out,
+                 int nrhs, int64_t ld, const double* coef_dev, const double* eta,
+                 cudaStream_t st) {
+  if (op->N > op->params.dense_limit)
+    throw Error(NLD_ERR_DENSE_LIMIT, "dense assembly of " + std::to_string(op->N) +
+                                         " nodes exceeds the limit " +
+                                         std::to_string(op->params.dense_limit));
+  int *widx = nullptr, *woff = nullptr;
+  dense_tables(op, &widx, &woff, st);
+  double* gam = nullptr;
+  NLD_CUDA(cudaMallocAsync(&gam, sizeof(double) * op->N * nrhs, st));
+  double inv = (which ? 2.0 : 1.0) / (op->sigma * op->sigma);
+  dim3 grid(grid_blocks(op->N, 128), nrhs);
+  k_dense_apply<<<grid, 128, 0, st>>>(op->feats, op->N, op->D, widx, woff, op->L, inv, v, ld,
+                                      gam);
+  NLD_CUDA(cudaGetLastError());
+  dim3 g2(grid_blocks(op->N, 256), nrhs);
+  k_epilogue<<<g2, 256, 0, st>>>(kind, op->L, op->N, v, ld, gam, 1, out, ld, eta, coef_dev);
+  NLD_CUDA(cudaGetLastError());
+  cudaFreeAsync(gam, st);
+  cudaFreeAsync(widx, st);
+  cudaFreeAsync(woff, st);
+}
+
+void dense_assemble(nld_operator* op, int which, double* out, cudaStream_t st) {
+  if (op->N > op->params.dense_limit)
+    throw Error(NLD_ERR_DENSE_LIMIT, "dense assembly of " + std::to_string(op->N) +
+                                         " nodes exceeds the limit " +
+                                         std::to_string(op->params.dense_limit));
+  int *widx = nullptr, *woff = nullptr;
+  dense_tables(op, &widx, &woff, st);
+  double inv = (which ? 2.0 : 1.0) / (op->sigma * op->sigma);
+  k_dense_assemble<<<grid_blocks(op->N * op->N, 256, 148 * 32), 256, 0, st>>>(
+      op->feats, op->N, op->D, widx, woff, op->L, inv, out);
+  NLD_CUDA(cudaGetLastError());
+  cudaFreeAsync(widx, st);
+  cudaFreeAsync(woff, st);
+}
+
+}  // namespace nld

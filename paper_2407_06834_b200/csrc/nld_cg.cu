@@ -1,0 +1,664 @@
+// Device-resident deflated / plain PCG around the fused system matvec,
+// plus the small vector kernels behind DeflatingBasis and the generic pcg.
+//
+// Reference: pcg (linops.py:193-244), _projected_prec (:252-260),
+// deflated_solve (:263-300), plain_solve (:303-319), scs_up/scs_down
+// (:114-131), DeflatingBasis (:134-176).
+//
+// deflated_solve runs CG on the tail block of U^T A U, U the orthogonal basis
+// whose first column is 1/sqrt(n).  With x = U[0; y] this is CG in pixel space
+// on the complement of 1 with the operator Pi A Pi, the preconditioner
+// z = Pi(D^-1 r) and the right-hand side Pi(lam f), Pi = I - 11^T/n, and
+// u = mean(f) 1 + x.  U is orthogonal, so every inner product, norm,
+// step length and stopping decision is the same quantity as in the reference
+// (hard part 4).  The projections need one mean per product
+// instead of the two O(n) prefix scans per product of the literal form.
+//
+// Reductions are two-stage with a fixed block count and a fixed summation
+// order, so results are run-to-run deterministic.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <limits>
+#include <vector>
+
+#include "nld_internal.cuh"
+
+namespace nld {
+
+namespace {
+
+constexpr int kRB = 296;   // reduction blocks (2 per SM)
+constexpr int kRT = 256;
+constexpr int kMaxK = 4;
+
+struct RhsScal {
+  double alpha, mq, mz, beta, lam, mu, mf;
+  int active;
+  int pad;
+};
+
+enum RedMode { RED_SUM = 0, RED_PQ = 1, RED_UPDATE = 2, RED_PREC = 3, RED_RESID = 4,
+               RED_NORM2 = 5 };
+
+struct CgPtr {
+  double* x;
+  double* r;
+  double* p;
+  double* q;
+  double* b;
+  double* t;
+  const double* f;
+  const double* eta;
+  const double* eta2;
+  int64_t N;
+  int64_t ldf;
+  int L;
+  int prec;
+  int deflate;
+};
+
+__device__ __forceinline__ double dinv_at(const CgPtr& c, const RhsScal& s, int64_t i) {
+  if (c.prec == NLD_PREC_JACOBI) return 1.0 / (s.lam + s.mu * c.eta[i]);
+  if (c.prec == NLD_PREC_L2) {
+    const double pa = s.lam + s.mu * c.eta[i];
+    const double row_sq = c.eta2[i] / (double)(c.L * c.L);
+    return 1.0 / sqrt(s.mu * s.mu * row_sq + pa * pa);
+  }
+  return 1.0;
+}
+
+template <int K>
+__device__ __forceinline__ void block_store(double (&v)[K], double* part) {
+  __shared__ double sh[K][kRT];
+#pragma unroll
+  for (int k = 0; k < K; ++k) sh[k][threadIdx.x] = v[k];
+  __syncthreads();
+  for (int off = kRT / 2; off > 0; off >>= 1) {
+    if (threadIdx.x < off)
+#pragma unroll
+      for (int k = 0; k < K; ++k) sh[k][threadIdx.x] += sh[k][threadIdx.x + off];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0)
+#pragma unroll
+    for (int k = 0; k < K; ++k) part[k] = sh[k][0];
+}
+
+// vecA: generic input for RED_SUM / RED_NORM2 ([rhs][lda])
+template <int MODE>
+__global__ void __launch_bounds__(kRT)
+k_cg_reduce(CgPtr c, const RhsScal* __restrict__ sc, const double* __restrict__ vecA,
+            int64_t lda, double* __restrict__ part) {
+  const int rhs = blockIdx.y;
+  const RhsScal s = sc[rhs];
+  const int64_t N = c.N;
+  const int64_t o = rhs * N;
+  double acc[kMaxK] = {0.0, 0.0, 0.0, 0.0};
+  for (int64_t i = blockIdx.x * (int64_t)kRT + threadIdx.x; i < N;
+       i += (int64_t)gridDim.x * kRT) {
+    if (MODE == RED_SUM) {
+      acc[0] += vecA[rhs * lda + i];
+    } else if (MODE == RED_NORM2) {
+      const double a = vecA[rhs * lda + i];
+      acc[0] += a * a;
+    } else if (MODE == RED_PQ) {
+      const double p = c.p[o + i], q = c.q[o + i];
+      acc[0] += q;
+      acc[1] += p * q;
+      acc[2] += p;
+    } else if (MODE == RED_UPDATE || MODE == RED_PREC) {
+      double r = c.r[o + i];
+      if (MODE == RED_UPDATE && s.active) {
+        c.x[o + i] += s.alpha * c.p[o + i];
+        r -= s.alpha * (c.q[o + i] - s.mq);
+        c.r[o + i] = r;
+      }
+      const double zt = dinv_at(c, s, i) * r;
+      acc[0] += r * r;
+      acc[1] += zt;
+      acc[2] += r * zt;
+      acc[3] += r;
+    } else if (MODE == RED_RESID) {
+      const double e = c.b[o + i] - (c.t[o + i] - s.mq);
+      acc[0] += e * e;
+    }
+  }
+  double* pp = part + ((int64_t)rhs * gridDim.x + blockIdx.x) * kMaxK;
+  block_store<kMaxK>(acc, pp);
+}
+
+__global__ void k_final(const double* __restrict__ part, int nblk, double* __restrict__ out) {
+  // one thread per (rhs, k): sequential sum over blocks -> deterministic
+  const int rhs = blockIdx.x;
+  const int k = threadIdx.x;
+  if (k >= kMaxK) return;
+  double s = 0.0;
+  for (int b = 0; b < nblk; ++b) s += part[((int64_t)rhs * nblk + b) * kMaxK + k];
+  out[rhs * kMaxK + k] = s;
+}
+
+__global__ void k_cg_setup(CgPtr c, const RhsScal* __restrict__ sc, int warm) {
+  const int rhs = blockIdx.y;
+  const RhsScal s = sc[rhs];
+  const int64_t o = rhs * c.N;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < c.N;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double f = c.f[rhs * c.ldf + i];
+    const double g = c.deflate ? f - s.mf : f;
+    c.b[o + i] = s.lam * g;
+    c.x[o + i] = warm ? g : 0.0;
+  }
+}
+
+__global__ void k_cg_resid0(CgPtr c, const RhsScal* __restrict__ sc, int warm) {
+  // r = b - Pi A x0 (warm) or r = b (x0 = 0; A 0 == 0 exactly)
+  const int rhs = blockIdx.y;
+  const RhsScal s = sc[rhs];
+  const int64_t o = rhs * c.N;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < c.N;
+       i += (int64_t)gridDim.x * blockDim.x)
+    c.r[o + i] = warm ? c.b[o + i] - (c.q[o + i] - s.mq) : c.b[o + i];
+}
+
+__global__ void k_cg_direction(CgPtr c, const RhsScal* __restrict__ sc, int first) {
+  // z = Pi(D^-1 r) (or r), p = z + beta p
+  const int rhs = blockIdx.y;
+  const RhsScal s = sc[rhs];
+  if (!s.active) return;
+  const int64_t o = rhs * c.N;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < c.N;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double r = c.r[o + i];
+    const double z = (c.prec == NLD_PREC_NONE) ? r : dinv_at(c, s, i) * r - s.mz;
+    c.p[o + i] = first ? z : z + s.beta * c.p[o + i];
+  }
+}
+
+__global__ void k_cg_finish(CgPtr c, const RhsScal* __restrict__ sc, double* __restrict__ u,
+                            int64_t ldu) {
+  const int rhs = blockIdx.y;
+  const RhsScal s = sc[rhs];
+  const int64_t o = rhs * c.N;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < c.N;
+       i += (int64_t)gridDim.x * blockDim.x)
+    u[rhs * ldu + i] = c.deflate ? s.mf + c.x[o + i] : c.x[o + i];
+}
+
+int eblocks(int64_t n) {
+  int64_t b = (n + 255) / 256;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(b, 148 * 8));
+}
+
+struct Reducer {
+  double* part = nullptr;
+  double* out = nullptr;
+  std::vector<double> host;
+  int nrhs;
+  int nblk;
+  cudaStream_t st;
+  Reducer(int nr, int64_t N, cudaStream_t s) : nrhs(nr), st(s) {
+    nblk = (int)std::max<int64_t>(1, std::min<int64_t>(kRB, (N + kRT - 1) / kRT));
+    NLD_CUDA(cudaMallocAsync(&part, sizeof(double) * nr * nblk * kMaxK, st));
+    NLD_CUDA(cudaMallocAsync(&out, sizeof(double) * nr * kMaxK, st));
+    host.resize((size_t)nr * kMaxK);
+  }
+  ~Reducer() {
+    cudaFreeAsync(part, st);
+    cudaFreeAsync(out, st);
+  }
+  template <int MODE>
+  const std::vector<double>& run(const CgPtr& c, const RhsScal* sc,
+                                 const double* vecA = nullptr, int64_t lda = 0) {
+    dim3 grid(nblk, nrhs);
+    k_cg_reduce<MODE><<<grid, kRT, 0, st>>>(c, sc, vecA, lda, part);
+    NLD_CUDA(cudaGetLastError());
+    k_final<<<nrhs, 32, 0, st>>>(part, nblk, out);
+    NLD_CUDA(cudaMemcpyAsync(host.data(), out, sizeof(double) * nrhs * kMaxK,
+                             cudaMemcpyDeviceToHost, st));
+    NLD_CUDA(cudaStreamSynchronize(st));
+    return host;
+  }
+};
+
+// ---- generic vector kernels ---------------------------------------------
+
+__global__ void k_axpby(double a, const double* __restrict__ x, double b,
+                        const double* __restrict__ y, double* __restrict__ out, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = a * x[i] + b * y[i];
+}
+
+__global__ void k_dot_part(const double* __restrict__ x, const double* __restrict__ y,
+                           int64_t n, double* __restrict__ part) {
+  double acc[kMaxK] = {0.0, 0.0, 0.0, 0.0};
+  for (int64_t i = blockIdx.x * (int64_t)kRT + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * kRT)
+    acc[0] += x[i] * y[i];
+  block_store<kMaxK>(acc, part + blockIdx.x * kMaxK);
+}
+
+__global__ void k_reverse(const double* __restrict__ x, double* __restrict__ out, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = x[n - 1 - i];
+}
+
+// scs_up: out_i = x_0 + sum_{j>i} x_j; rev = inclusive scan of reversed x
+__global__ void k_scs_up(const double* __restrict__ x, const double* __restrict__ rev,
+                         double* __restrict__ out, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    // suffix sum from i+1 = rev[n-2-i]
+    out[i] = (i < n - 1) ? x[0] + rev[n - 2 - i] : x[0];
+  }
+}
+
+// scs_down: out_0 = total, out_i = cumsum_{i-1}
+__global__ void k_scs_down(const double* __restrict__ cs, double* __restrict__ out, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (i == 0) ? cs[n - 1] : cs[i - 1];
+}
+
+__global__ void k_sq(const double* __restrict__ v, double* __restrict__ out, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = v[i] * v[i];
+}
+
+__global__ void k_mul(const double* __restrict__ a, const double* __restrict__ b,
+                      double* __restrict__ out, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = a[i] * b[i];
+}
+
+// U x pieces: pre = sqrt(cumsum v^2); y0 = x0/norm, y_i = b_i v_i x_i
+__global__ void k_basis_y(const double* __restrict__ v, const double* __restrict__ pre2,
+                          const double* __restrict__ x, double* __restrict__ y, int64_t n) {
+  const double norm = sqrt(pre2[n - 1]);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (i == 0) {
+      y[0] = x[0] / norm;
+    } else {
+      const double pm = sqrt(pre2[i - 1]), pi = sqrt(pre2[i]);
+      const double b = 1.0 / (pm * pi);
+      y[i] = b * v[i] * x[i];
+    }
+  }
+}
+
+__global__ void k_basis_out(const double* __restrict__ v, const double* __restrict__ pre2,
+                            const double* __restrict__ x, const double* __restrict__ s,
+                            double* __restrict__ out, int64_t n, int adjoint) {
+  const double norm = sqrt(pre2[n - 1]);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (!adjoint) {
+      // out = v * scs_up(y); out[1:] -= a * x[1:]
+      double o = v[i] * s[i];
+      if (i > 0) {
+        const double a = sqrt(pre2[i - 1]) / sqrt(pre2[i]);
+        o -= a * x[i];
+      }
+      out[i] = o;
+    } else {
+      // out0 = s0 / norm; out_i = b v_i s_i - a x_i
+      if (i == 0) {
+        out[0] = s[0] / norm;
+      } else {
+        const double pm = sqrt(pre2[i - 1]), pi = sqrt(pre2[i]);
+        const double a = pm / pi;
+        const double b = 1.0 / (pm * pi);
+        out[i] = b * v[i] * s[i] - a * x[i];
+      }
+    }
+  }
+}
+
+void inclusive_scan(const double* in, double* out, int64_t n, cudaStream_t st) {
+  size_t bytes = 0;
+  cub::DeviceScan::InclusiveSum(nullptr, bytes, in, out, (int)n, st);
+  void* tmp = nullptr;
+  NLD_CUDA(cudaMallocAsync(&tmp, bytes ? bytes : 1, st));
+  NLD_CUDA(cub::DeviceScan::InclusiveSum(tmp, bytes, in, out, (int)n, st));
+  cudaFreeAsync(tmp, st);
+}
+
+}  // namespace
+
+void dev_axpby(double a, const double* x, double b, const double* y, double* out, int64_t n,
+               cudaStream_t st) {
+  k_axpby<<<eblocks(n), 256, 0, st>>>(a, x, b, y, out, n);
+  NLD_CUDA(cudaGetLastError());
+}
+
+double dev_dot(const double* x, const double* y, int64_t n, cudaStream_t st) {
+  int nblk = (int)std::max<int64_t>(1, std::min<int64_t>(kRB, (n + kRT - 1) / kRT));
+  double *part = nullptr, *out = nullptr;
+  NLD_CUDA(cudaMallocAsync(&part, sizeof(double) * nblk * kMaxK, st));
+  NLD_CUDA(cudaMallocAsync(&out, sizeof(double) * kMaxK, st));
+  k_dot_part<<<nblk, kRT, 0, st>>>(x, y, n, part);
+  k_final<<<1, 32, 0, st>>>(part, nblk, out);
+  double h[kMaxK];
+  NLD_CUDA(cudaMemcpyAsync(h, out, sizeof(double) * kMaxK, cudaMemcpyDeviceToHost, st));
+  cudaFreeAsync(part, st);
+  cudaFreeAsync(out, st);
+  NLD_CUDA(cudaStreamSynchronize(st));
+  return h[0];
+}
+
+void dev_scs(const double* x, double* out, int64_t n, int down, cudaStream_t st) {
+  double* tmp = nullptr;
+  double* tmp2 = nullptr;
+  NLD_CUDA(cudaMallocAsync(&tmp, sizeof(double) * n, st));
+  if (down) {
+    inclusive_scan(x, tmp, n, st);
+    k_scs_down<<<eblocks(n), 256, 0, st>>>(tmp, out, n);
+  } else {
+    NLD_CUDA(cudaMallocAsync(&tmp2, sizeof(double) * n, st));
+    k_reverse<<<eblocks(n), 256, 0, st>>>(x, tmp2, n);
+    inclusive_scan(tmp2, tmp, n, st);
+    k_scs_up<<<eblocks(n), 256, 0, st>>>(x, tmp, out, n);
+    cudaFreeAsync(tmp2, st);
+  }
+  NLD_CUDA(cudaGetLastError());
+  cudaFreeAsync(tmp, st);
+}
+
+void dev_basis(const double* v, const double* x, double* out, int64_t n, int adjoint,
+               cudaStream_t st) {
+  double *sq = nullptr, *pre2 = nullptr, *y = nullptr, *s = nullptr;
+  NLD_CUDA(cudaMallocAsync(&sq, sizeof(double) * n, st));
+  NLD_CUDA(cudaMallocAsync(&pre2, sizeof(double) * n, st));
+  NLD_CUDA(cudaMallocAsync(&y, sizeof(double) * n, st));
+  NLD_CUDA(cudaMallocAsync(&s, sizeof(double) * n, st));
+  k_sq<<<eblocks(n), 256, 0, st>>>(v, sq, n);
+  inclusive_scan(sq, pre2, n, st);
+  if (!adjoint) {
+    k_basis_y<<<eblocks(n), 256, 0, st>>>(v, pre2, x, y, n);
+    dev_scs(y, s, n, 0, st);
+  } else {
+    k_mul<<<eblocks(n), 256, 0, st>>>(v, x, y, n);
+    dev_scs(y, s, n, 1, st);
+  }
+  k_basis_out<<<eblocks(n), 256, 0, st>>>(v, pre2, x, s, out, n, adjoint);
+  NLD_CUDA(cudaGetLastError());
+  cudaFreeAsync(sq, st);
+  cudaFreeAsync(pre2, st);
+  cudaFreeAsync(y, st);
+  cudaFreeAsync(s, st);
+}
+
+void cg_solve(nld_operator* op, const double* f, double* u, int nrhs, int64_t ld,
+              const double* lam, const double* mu, int prec, int deflate, double tol,
+              int maxit, int warm, int* iters, double* relres, int* conv, double* hist,
+              int hist_cap, cudaStream_t st) {
+  const int64_t N = op->N;
+  if (deflate && N < 2) throw Error(NLD_ERR_DIMENSION, "basis needs at least two entries");
+  for (int r = 0; r < nrhs; ++r)
+    if (!(lam[r] > 0) || !(mu[r] > 0))
+      throw Error(NLD_ERR_VALUE, "shift lambda and weight mu must be positive");
+  // degree vectors (ShiftedSystem.__init__ caches eta, linops.py:37)
+  auto degree = [&](int which) -> const double* {
+    if (!op->eta[which]) {
+      NLD_CUDA(cudaMalloc(&op->eta[which], sizeof(double) * N));
+      double* ones = nullptr;
+      NLD_CUDA(cudaMallocAsync(&ones, sizeof(double) * N, st));
+      std::vector<double> h(N, 1.0);
+      NLD_CUDA(cudaMemcpyAsync(ones, h.data(), sizeof(double) * N, cudaMemcpyHostToDevice, st));
+      if (op->params.mode == 1) dense_apply(op, which, NLD_APPLY_GAMMA, ones, op->eta[which], 1, N, nullptr, nullptr, st);
+      else apply_op(op, which, NLD_APPLY_GAMMA, ones, op->eta[which], 1, N, nullptr, nullptr, st);
+      NLD_CUDA(cudaStreamSynchronize(st));
+      cudaFreeAsync(ones, st);
+    }
+    return op->eta[which];
+  };
+  if (op->params.mode != 1 && !op->built[0]) {
+    build_planset(op, 0, st);
+    op->built[0] = true;
+  }
+  const double* eta = degree(0);
+  double* eta2 = nullptr;
+  if (prec == NLD_PREC_L2) {
+    if (op->params.mode != 1 && !op->built[1]) {
+      build_planset(op, 1, st);
+      op->built[1] = true;
+    }
+    degree(1);
+    // degree_squared = apply_squared(1) * L (kernel.py:148-154)
+    NLD_CUDA(cudaMallocAsync(&eta2, sizeof(double) * N, st));
+    dev_axpby((double)op->L, op->eta[1], 0.0, op->eta[1], eta2, N, st);
+  }
+
+  const int64_t V = N * nrhs;
+  CgPtr c{};
+  NLD_CUDA(cudaMallocAsync(&c.x, sizeof(double) * V, st));
+  NLD_CUDA(cudaMallocAsync(&c.r, sizeof(double) * V, st));
+  NLD_CUDA(cudaMallocAsync(&c.p, sizeof(double) * V, st));
+  NLD_CUDA(cudaMallocAsync(&c.q, sizeof(double) * V, st));
+  NLD_CUDA(cudaMallocAsync(&c.b, sizeof(double) * V, st));
+  NLD_CUDA(cudaMallocAsync(&c.t, sizeof(double) * V, st));
+  c.f = f;
+  c.eta = eta;
+  c.eta2 = eta2;
+  c.N = N;
+  c.ldf = ld;
+  c.L = op->L;
+  c.prec = prec;
+  c.deflate = deflate;
+  RhsScal* scd = nullptr;
+  double* coef = nullptr;
+  NLD_CUDA(cudaMallocAsync(&scd, sizeof(RhsScal) * nrhs, st));
+  NLD_CUDA(cudaMallocAsync(&coef, sizeof(double) * 2 * nrhs, st));
+  std::vector<RhsScal> sc(nrhs);
+  std::vector<double> hcoef(2 * nrhs);
+  for (int r = 0; r < nrhs; ++r) {
+    sc[r] = RhsScal{0, 0, 0, 0, lam[r], mu[r], 0, 1, 0};
+    hcoef[2 * r] = lam[r];
+    hcoef[2 * r + 1] = mu[r];
+  }
+  NLD_CUDA(cudaMemcpyAsync(coef, hcoef.data(), sizeof(double) * 2 * nrhs,
+                           cudaMemcpyHostToDevice, st));
+  auto push = [&]() {
+    NLD_CUDA(cudaMemcpyAsync(scd, sc.data(), sizeof(RhsScal) * nrhs, cudaMemcpyHostToDevice,
+                             st));
+  };
+  auto matvec = [&](const double* in, double* out) {
+    if (op->params.mode == 1) dense_apply(op, 0, NLD_APPLY_SYSTEM, in, out, nrhs, N, coef, eta, st);
+    else apply_op(op, 0, NLD_APPLY_SYSTEM, in, out, nrhs, N, coef, eta, st);
+  };
+  const double dN = (double)N;
+  Reducer red(nrhs, N, st);
+  dim3 eg(eblocks(N), nrhs);
+
+  std::vector<std::vector<double>> H(nrhs);
+  std::vector<double> bnorm(nrhs, 0.0), rz(nrhs, 0.0);
+  std::vector<int> it(nrhs, 0), done(nrhs, 0);
+  for (int r = 0; r < nrhs; ++r) {
+    iters[r] = 0;
+    relres[r] = 0.0;
+    conv[r] = 0;
+  }
+
+  // mean of f (deflation: x_first = g0 carries the mean, linops.py:278-279)
+  push();
+  {
+    const auto& h = red.run<RED_SUM>(c, scd, f, ld);
+    for (int r = 0; r < nrhs; ++r) sc[r].mf = deflate ? h[r * kMaxK] / dN : 0.0;
+  }
+  push();
+  k_cg_setup<<<eg, 256, 0, st>>>(c, scd, warm);
+  if (warm) {
+    matvec(c.x, c.q);
+    if (deflate) {
+      const auto& h = red.run<RED_SUM>(c, scd, c.q, N);
+      for (int r = 0; r < nrhs; ++r) sc[r].mq = h[r * kMaxK] / dN;
+    }
+    push();
+  }
+  k_cg_resid0<<<eg, 256, 0, st>>>(c, scd, warm);
+  NLD_CUDA(cudaGetLastError());
+  std::vector<double> nb(nrhs), nr(nrhs);
+  {
+    const auto& h = red.run<RED_NORM2>(c, scd, c.b, N);
+    for (int r = 0; r < nrhs; ++r) nb[r] = std::sqrt(h[r * kMaxK]);
+  }
+  {
+    const auto& h = red.run<RED_PREC>(c, scd);
+    for (int r = 0; r < nrhs; ++r) {
+      nr[r] = std::sqrt(h[r * kMaxK]);
+      if (nb[r] == 0.0 && !warm) {
+        done[r] = 1;
+        conv[r] = 1;
+        H[r] = {0.0};
+        continue;
+      }
+      bnorm[r] = std::max(nb[r], nr[r]);
+      if (bnorm[r] == 0.0) {
+        done[r] = 1;
+        conv[r] = 1;
+        H[r] = {0.0};
+        continue;
+      }
+      H[r] = {nr[r] / bnorm[r]};
+      if (maxit <= 0) {
+        done[r] = 1;
+        conv[r] = 0;
+        relres[r] = H[r][0];
+        continue;
+      }
+      const double mz = (deflate && prec != NLD_PREC_NONE) ? h[r * kMaxK + 1] / dN : 0.0;
+      sc[r].mz = mz;
+      rz[r] = h[r * kMaxK + 2] - mz * h[r * kMaxK + 3];
+      sc[r].beta = 0.0;
+    }
+  }
+  for (int r = 0; r < nrhs; ++r) sc[r].active = done[r] ? 0 : 1;
+  push();
+  k_cg_direction<<<eg, 256, 0, st>>>(c, scd, 1);
+  NLD_CUDA(cudaGetLastError());
+
+  auto any_active = [&]() {
+    for (int r = 0; r < nrhs; ++r)
+      if (!done[r]) return true;
+    return false;
+  };
+  // explicit residual || b - Pi A x || for the flagged rhs
+  auto true_residual = [&](std::vector<double>& out) {
+    matvec(c.x, c.t);
+    if (deflate) {
+      const auto& h = red.run<RED_SUM>(c, scd, c.t, N);
+      for (int r = 0; r < nrhs; ++r) sc[r].mq = h[r * kMaxK] / dN;
+    } else {
+      for (int r = 0; r < nrhs; ++r) sc[r].mq = 0.0;
+    }
+    push();
+    const auto& h = red.run<RED_RESID>(c, scd);
+    out.resize(nrhs);
+    for (int r = 0; r < nrhs; ++r) out[r] = std::sqrt(h[r * kMaxK]) / (bnorm[r] > 0 ? bnorm[r] : 1.0);
+  };
+
+  std::vector<double> truer;
+  while (any_active()) {
+    matvec(c.p, c.q);
+    const auto& hpq = red.run<RED_PQ>(c, scd);
+    for (int r = 0; r < nrhs; ++r) {
+      if (done[r]) continue;
+      const double mq = deflate ? hpq[r * kMaxK] / dN : 0.0;
+      const double pap = hpq[r * kMaxK + 1] - mq * hpq[r * kMaxK + 2];
+      if (!std::isfinite(pap) || pap <= 0.0)
+        throw Error(NLD_ERR_BREAKDOWN, "indefinite or non-finite curvature at iteration " +
+                                           std::to_string(it[r]));
+      sc[r].mq = mq;
+      sc[r].alpha = rz[r] / pap;
+    }
+    push();
+    const auto& hu = red.run<RED_UPDATE>(c, scd);
+    std::vector<int> check(nrhs, 0);
+    bool need_true = false;
+    std::vector<double> hsave(hu.begin(), hu.end());
+    for (int r = 0; r < nrhs; ++r) {
+      if (done[r]) continue;
+      it[r] += 1;
+      const double rel = std::sqrt(hsave[r * kMaxK]) / bnorm[r];
+      H[r].push_back(rel);
+      if (rel <= tol) {
+        check[r] = 1;
+        need_true = true;
+      }
+    }
+    if (need_true) {
+      true_residual(truer);
+      for (int r = 0; r < nrhs; ++r) {
+        if (!check[r]) continue;
+        H[r].back() = truer[r];
+        if (truer[r] <= tol) {
+          done[r] = 1;
+          conv[r] = 1;
+          relres[r] = truer[r];
+        }
+      }
+    }
+    // next direction for the still-active rhs
+    std::vector<int> hit_max(nrhs, 0);
+    for (int r = 0; r < nrhs; ++r) {
+      if (done[r]) {
+        sc[r].active = 0;
+        continue;
+      }
+      const double mz = (deflate && prec != NLD_PREC_NONE) ? hsave[r * kMaxK + 1] / dN : 0.0;
+      const double rzn = hsave[r * kMaxK + 2] - mz * hsave[r * kMaxK + 3];
+      if (!std::isfinite(rzn))
+        throw Error(NLD_ERR_BREAKDOWN, "non-finite residual inner product");
+      sc[r].mz = mz;
+      sc[r].beta = rzn / rz[r];
+      rz[r] = rzn;
+      sc[r].active = 1;
+      if (it[r] >= maxit) hit_max[r] = 1;
+    }
+    push();
+    k_cg_direction<<<eg, 256, 0, st>>>(c, scd, 0);
+    NLD_CUDA(cudaGetLastError());
+    bool any_max = false;
+    for (int r = 0; r < nrhs; ++r) any_max |= hit_max[r] != 0;
+    if (any_max) {
+      true_residual(truer);
+      for (int r = 0; r < nrhs; ++r) {
+        if (!hit_max[r]) continue;
+        done[r] = 1;
+        relres[r] = truer[r];
+        conv[r] = truer[r] <= tol;
+        sc[r].active = 0;
+      }
+      push();
+    }
+  }
+  k_cg_finish<<<eg, 256, 0, st>>>(c, scd, u, ld);
+  NLD_CUDA(cudaGetLastError());
+  NLD_CUDA(cudaStreamSynchronize(st));
+  for (int r = 0; r < nrhs; ++r) {
+    iters[r] = it[r];
+    if (hist && hist_cap > 0) {
+      for (int k = 0; k < hist_cap; ++k)
+        hist[(int64_t)r * hist_cap + k] =
+            k < (int)H[r].size() ? H[r][k] : std::numeric_limits<double>::quiet_NaN();
+    }
+  }
+  cudaFreeAsync(c.x, st);
+  cudaFreeAsync(c.r, st);
+  cudaFreeAsync(c.p, st);
+  cudaFreeAsync(c.q, st);
+  cudaFreeAsync(c.b, st);
+  cudaFreeAsync(c.t, st);
+  cudaFreeAsync(scd, st);
+  cudaFreeAsync(coef, st);
+  if (eta2) cudaFreeAsync(eta2, st);
+  NLD_CUDA(cudaStreamSynchronize(st));
+}
+
+}  // namespace nld

@@ -1,0 +1,202 @@
+// Internal declarations shared by the nld_b200 translation units.
+//
+// Data layout in HBM (one operator, one plan set = one Gaussian width):
+//   rows    : per window, the sorted node table.  Node e of window w has a
+//             row of S*d fp64 principal Kaiser-Bessel weights (S = 2m, the
+//             stencil offsets i = 1..2m of node_tables, transform.py:147-170),
+//             dimension-major: [w_dim0(S)][w_dim1(S)][w_dim2(S)].
+//   pix     : per window, int32 original pixel of sorted node e.
+//   key     : per window, int32 flattened cell coordinate (sort key).
+//   cells   : occupied stencil cells (all windows), with their subproblems.
+//   subs    : work items: <= kSubMax nodes of one cell (grouped by dim).
+//   grids   : per window the support box of the oversampled grid, real fp64,
+//             [nrhs][sum of box sizes].
+//   K       : per window the separable convolution kernel K(delta),
+//             delta = 0..n-1, complex fp64 (FFT -> x coeffs -> FFT, fused).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/nld_b200.h"
+
+namespace nld {
+
+constexpr int kSubMax = 512;   // nodes per subproblem
+constexpr int kMaxDim = 3;
+
+struct Status {
+  int code = NLD_OK;
+  std::string msg;
+};
+
+void set_error(int code, const std::string& msg);
+int fail(int code, const std::string& msg);
+
+#define NLD_CUDA(call)                                                     \
+  do {                                                                     \
+    cudaError_t _e = (call);                                               \
+    if (_e != cudaSuccess) {                                               \
+      throw ::nld::Error(NLD_ERR_CUDA, std::string(#call) + ": " +         \
+                                           cudaGetErrorString(_e));        \
+    }                                                                      \
+  } while (0)
+
+struct Error {
+  int code;
+  std::string msg;
+  Error(int c, std::string m) : code(c), msg(std::move(m)) {}
+};
+
+// Device-visible description of one window of one plan set.
+struct WinDev {
+  int d;             // window dimension 1..3
+  int n;             // oversampled grid size per dimension
+  int S;             // 2m principal stencil width
+  int wrap;          // 1: box is the whole torus (positions mod n)
+  int box_w[3];      // support box extents (unused dims = 1)
+  int box_lo[3];
+  int64_t box_size;  // prod box_w
+  int64_t grid_off;  // offset of this window's box in a per-rhs grid buffer
+  int64_t kern_off;  // offset (complex entries) into the K table
+  int64_t cellmap_off;
+  int64_t node_off;  // offset (nodes) into pix/key of this window = w*N
+  int64_t row_off;   // offset (doubles) into rows
+  int fast;          // 1: block path (templated kernels), 0: generic path
+  int pad;
+};
+
+struct SubDev {
+  int64_t start;     // absolute node index (w*N + sorted position)
+  int64_t block;     // offset (doubles) of its partial block in the scratch
+  int32_t count;
+  int32_t cell;      // global cell index
+  int32_t win;
+  int32_t pad;
+};
+
+struct CellDev {
+  int32_t cc[3];     // cell coordinate in box units (first principal point)
+  int32_t win;
+  int64_t block0;    // offset (doubles) of its first subproblem block
+  int32_t nsub;
+  int32_t blk;       // block size S^d
+};
+
+struct EdgeDev {     // node with a nonzero weight at i = 0 or i = 2m+1
+  int32_t pix;
+  int32_t win;
+  int32_t cc[3];
+  int32_t pad;
+  double w[3][18];   // full width W = 2m+2 weights, m <= 8
+};
+
+// Host-side plan of one window.
+struct WinPlan {
+  int d = 0;
+  int cols[3] = {0, 0, 0};
+  double center[3] = {0, 0, 0};
+  double scale = 1.0, sig_scaled = 0.0;
+  int M = 0, n = 0, m = 0;
+  double b = 0.0;
+  int box_lo[3] = {0, 0, 0}, box_w[3] = {1, 1, 1};
+  int wrap = 0;
+  int64_t n_cells = 0, n_subs = 0, n_edge = 0;
+};
+
+// One Gaussian width (sigbar = 1/sigma^2 or 2/sigma^2) with its tables.
+struct PlanSet {
+  double sigbar = 0.0;
+  std::vector<WinPlan> win;
+  std::vector<WinDev> wdev_h;
+  WinDev* wdev = nullptr;        // device copy
+  double* rows = nullptr;
+  int32_t* pix = nullptr;
+  int32_t* key = nullptr;
+  int32_t* cellmap = nullptr;
+  double2* K = nullptr;
+  CellDev* cells = nullptr;
+  int64_t n_cells = 0;
+  SubDev* subs[kMaxDim + 1] = {nullptr, nullptr, nullptr, nullptr};
+  int64_t n_subs[kMaxDim + 1] = {0, 0, 0, 0};
+  int64_t blocks_total = 0;      // doubles per rhs of block scratch
+  EdgeDev* edges = nullptr;
+  int64_t n_edges = 0;
+  int64_t grid_total = 0;        // sum of box sizes
+  int64_t generic_nodes = 0;     // nodes in windows on the generic path
+  int shares_tables_with = -1;   // index of the plan set whose tables we use
+  bool owns_tables = true;
+};
+
+struct Workspace {
+  int nrhs_cap = 0;
+  double* blocks = nullptr;      // [nrhs][blocks_total]
+  double* grid_in = nullptr;     // [nrhs][grid_total]
+  double* grid_out = nullptr;
+  double2* cbuf0 = nullptr;
+  double2* cbuf1 = nullptr;
+  double* wout = nullptr;        // [nrhs][L][N] per-window gathers
+  double* coef = nullptr;        // [nrhs][2]
+  int64_t grid_total = 0, blocks_total = 0;
+};
+
+}  // namespace nld
+
+struct nld_operator {
+  int64_t N = 0;
+  int D = 0;
+  int L = 0;
+  double sigma = 0.0;
+  nld_params params{};
+  int device = 0;
+  double* feats = nullptr;       // not owned (only used at plan build)
+  std::vector<int> win_index, win_offset;
+  nld::PlanSet sets[2];          // [0] sigbar, [1] squared
+  bool built[2] = {false, false};
+  double* eta[2] = {nullptr, nullptr};
+  nld::Workspace ws;
+  double* dense[2] = {nullptr, nullptr};
+  int timing = 0;
+  nld_stats stats{};
+  cudaEvent_t ev[6] = {};
+  bool events = false;
+};
+
+namespace nld {
+
+void build_planset(nld_operator* op, int which, cudaStream_t st);
+void free_planset(PlanSet& ps);
+void ensure_workspace(nld_operator* op, const PlanSet& ps, int nrhs);
+void free_workspace(Workspace& ws);
+
+// one fused operator application (all windows, nrhs right-hand sides)
+void apply_op(nld_operator* op, int which, int kind, const double* v,
+              double* out, int nrhs, int64_t ld, const double* coef_dev,
+              const double* eta, cudaStream_t st);
+
+void dense_apply(nld_operator* op, int which, int kind, const double* v,
+                 double* out, int nrhs, int64_t ld, const double* coef_dev,
+                 const double* eta, cudaStream_t st);
+void dense_assemble(nld_operator* op, int which, double* out, cudaStream_t st);
+
+void cg_solve(nld_operator* op, const double* f, double* u, int nrhs,
+              int64_t ld, const double* lam, const double* mu, int prec,
+              int deflate, double tol, int maxit, int warm, int* iters,
+              double* relres, int* conv, double* hist, int hist_cap,
+              cudaStream_t st);
+
+// vector helpers (nld_vec.cu)
+void dev_axpby(double a, const double* x, double b, const double* y,
+               double* out, int64_t n, cudaStream_t st);
+double dev_dot(const double* x, const double* y, int64_t n, cudaStream_t st);
+void dev_scs(const double* x, double* out, int64_t n, int down,
+             cudaStream_t st);
+void dev_basis(const double* v, const double* x, double* out, int64_t n,
+               int adjoint, cudaStream_t st);
+
+int64_t expansion_degree(double sig_scaled, double eps);
+
+}  // namespace nld

@@ -1,0 +1,285 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the reference.
+
+Expected values are the REAL reference's outputs (tests/golden, made by
+tests/golden/make_golden.py) or the pinned CPU oracle at sizes it finishes in
+seconds.  Tolerances (north star): 1e-10 relative l2 for the fp64 matvec
+against the reference's own fast summation; the reference's NFFT error bound
+against the dense kernel sum at config 0; CG to 1e-8 relative within +-1
+iteration.
+"""
+
+import os
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from conftest import GOLDEN  # noqa: E402
+
+import paper_2407_06834_b200 as nld  # noqa: E402
+from oracle import nfft_oracle as O  # noqa: E402
+from paper_2407_06834_b200 import synth  # noqa: E402
+
+PIN = dict(n_expansion=synth.N_EXPANSION, cutoff=synth.CUTOFF,
+           oversampling=synth.OVERSAMPLING)
+MATVEC_TOL = 1e-10
+CG_TOL_U = 1e-8
+
+
+def rel(a, b):
+    a = np.asarray(a)
+    b = np.asarray(b)
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+def have(name):
+    return os.path.exists(os.path.join(GOLDEN, f"{name}.npz"))
+
+
+_OPS = {}
+
+
+def operator(name):
+    if name not in _OPS:
+        feats, wins, f = synth.make_problem(name)
+        _OPS[name] = (nld.AnovaOperator(feats, wins, synth.SIGMA, **PIN),
+                      feats, wins, f)
+    return _OPS[name]
+
+
+# ---------------------------------------------------------------- config 0/1
+
+@pytest.mark.parametrize("name", ["c0", "c1"])
+def test_matvec_matches_reference(golden, name):
+    g = golden(name)
+    op, feats, _, _ = operator(name)
+    v = synth.random_vector(op.n)
+    assert rel(op.apply(v), g["gv"]) < MATVEC_TOL
+    assert rel(op.degree(), g["eta"]) < MATVEC_TOL
+    info = op.window_info(0)
+    assert info["scale"] == float(g["scales"][0])
+    assert info["bandwidth"] == 32 and info["grid"] == 64
+    system = nld.ShiftedSystem(op, 1.0, float(g["mu"]))
+    av = system.apply(v)
+    if "av" in g:
+        assert rel(av, g["av"]) < MATVEC_TOL
+        assert rel(op.apply_squared(v), g["g2v"]) < MATVEC_TOL
+    # the fused epilogue equals the composition of the reference's formulas
+    want = 1.0 * v + float(g["mu"]) * (g["eta"] * v - g["gv"])
+    assert rel(av, want) < MATVEC_TOL
+
+
+def test_config0_against_dense_kernel_sum(golden):
+    g = golden("c0")
+    op, feats, wins, _ = operator("c0")
+    v = synth.random_vector(op.n)
+    fast = op.apply(v)
+    # within the reference's own NFFT error (2.8e-6 rel l2)
+    ref_err = rel(g["gv"], g["gv_dense"])
+    assert rel(fast, g["gv_dense"]) < 1.5 * ref_err
+    exact = nld.AnovaOperator(feats, wins, synth.SIGMA, mode="exact")
+    assert rel(exact.apply(v), g["gv_dense"]) < 1e-12
+
+
+@pytest.mark.parametrize("name", ["c0", "c1"])
+def test_deflated_cg_matches_reference(golden, name):
+    g = golden(name)
+    op, _, _, f = operator(name)
+    system = nld.ShiftedSystem(op, 1.0, float(g["mu"]))
+    res = nld.deflated_solve(system, f[:, 0], prec="jacobi", tol=synth.CG_TOL,
+                             maxit=200)
+    assert res.converged
+    assert abs(res.iterations - int(g["iters"])) <= 1
+    assert rel(res.x, g["u"]) < CG_TOL_U
+    if res.iterations == int(g["iters"]):
+        np.testing.assert_allclose(res.residual_history, g["history"],
+                                   rtol=1e-6)
+    # deflation preserves the mean (test_linops.py:182-185)
+    assert abs(res.x.mean() - f[:, 0].mean()) < 1e-8
+
+
+# ------------------------------------------------ large configs (subsampled)
+
+@pytest.mark.parametrize("name", ["c2", "c3", "c4"])
+def test_large_config_matvec_subsample(golden, name):
+    if not have(name):
+        pytest.skip(f"no golden for {name}")
+    g = golden(name)
+    op, feats, _, _ = operator(name)
+    v = synth.random_vector(op.n)
+    idx = g["idx"]
+    vt = torch.from_numpy(v).cuda()
+    gv = op.apply(vt)
+    eta = op.degree_device()
+    system = nld.ShiftedSystem(op, 1.0, float(g["mu"]))
+    av = system.apply(vt)
+    g2v = op.apply_squared(vt)
+    for key, vec in (("gv", gv), ("eta", eta), ("av", av), ("g2v", g2v)):
+        h = vec.cpu().numpy()
+        assert rel(h[idx], g[key + "_idx"]) < MATVEC_TOL, key
+        assert abs(np.linalg.norm(h) / float(g[key + "_norm"]) - 1) < MATVEC_TOL
+    _OPS.pop(name, None)
+
+
+# ------------------------------------------------ reference-default plans
+
+def test_default_parameters(golden):
+    """m=5, adaptive N_d (66/70/42 -> grids 132/140/84), exact mode, CG."""
+    g = golden("default_params")
+    wins = [np.arange(0, 3), np.arange(3, 6), np.arange(6, 7)]
+    op = nld.AnovaOperator(g["feats"], wins, 40.0)
+    assert rel(op.apply(g["v"]), g["gv"]) < MATVEC_TOL
+    assert [op.window_info(w)["bandwidth"] for w in range(3)] == list(g["nd"])
+    assert rel(op.apply_squared(g["v"]), g["g2v"]) < MATVEC_TOL
+    assert rel(op.degree(), g["eta"]) < MATVEC_TOL
+    exact = nld.AnovaOperator(g["feats"], wins, 40.0, mode="exact")
+    assert rel(exact.apply(g["v"]), g["gv_exact"]) < 1e-12
+    system = nld.ShiftedSystem(op, 1e-2, 1e-2)
+    res = nld.deflated_solve(system, g["f"], prec="jacobi", tol=1e-10,
+                             maxit=300)
+    assert abs(res.iterations - int(g["iters"])) <= 1
+    assert rel(res.x, g["u"]) < CG_TOL_U
+    res = nld.deflated_solve(system, g["f"], prec="l2", tol=1e-10, maxit=300)
+    assert abs(res.iterations - int(g["iters_l2"])) <= 1
+    assert rel(res.x, g["u_l2"]) < CG_TOL_U
+    res = nld.plain_solve(system, g["f"], prec="none", tol=1e-10, maxit=300)
+    assert abs(res.iterations - int(g["iters_plain"])) <= 1
+    assert rel(res.x, g["u_plain"]) < CG_TOL_U
+
+
+@pytest.mark.parametrize("d", [1, 2, 3])
+def test_fast_gauss_transform(golden, d):
+    """gauss_transform_fast on 400 nodes in [0,255]^d (test_transform.py:142-151)."""
+    g = golden("default_params")
+    pts, alpha = g[f"fgt{d}_pts"], g[f"fgt{d}_alpha"]
+    op = nld.AnovaOperator(pts, [np.arange(d)], 40.0)
+    assert rel(op.window_sum(alpha), g[f"fgt{d}_out"]) < MATVEC_TOL
+    assert op.window_info(0)["bandwidth"] == int(g[f"fgt{d}_nd"])
+
+
+def test_edge_nodes(golden):
+    """Nodes on grid lines carry 2m+1 nonzero weights (transform.py:168)."""
+    g = golden("edge_nodes")
+    op = nld.AnovaOperator(g["feats"], [np.arange(3), np.array([3])], 0.1,
+                           **PIN)
+    assert rel(op.apply(g["v"]), g["gv"]) < MATVEC_TOL
+    assert rel(op.degree(), g["eta"]) < MATVEC_TOL
+    assert op.window_info(0)["n_edge"] > 0
+    assert op.window_info(0)["scale"] == 1.0
+
+
+# ------------------------------------------------ other cutoffs (generic path)
+
+@pytest.mark.parametrize("cutoff", [2, 3, 4, 5, 6])
+def test_cutoffs_against_oracle(cutoff):
+    rng = np.random.default_rng(cutoff)
+    feats = rng.uniform(-1, 1, size=(700, 5))
+    wins = [np.arange(0, 3), np.arange(3, 5)]
+    v = rng.standard_normal(700)
+    kw = dict(n_expansion=16, cutoff=cutoff, oversampling=2.0)
+    op = nld.AnovaOperator(feats, wins, 0.5, **kw)
+    ref = O.AnovaOracle(feats, wins, 0.5, **kw)
+    assert rel(op.apply(v), ref.apply(v)) < MATVEC_TOL
+
+
+# ------------------------------------------------ size-independent properties
+
+def test_properties_full_size():
+    op, _, _, _ = operator("c2")
+    rng = np.random.default_rng(5)
+    u = torch.from_numpy(rng.standard_normal(op.n)).cuda()
+    w = torch.from_numpy(rng.standard_normal(op.n)).cuda()
+    gu, gw = op.apply(u), op.apply(w)
+    # linearity
+    comb = op.apply(2.0 * u - 3.0 * w)
+    assert rel(comb.cpu(), (2.0 * gu - 3.0 * gw).cpu()) < 1e-12
+    # near-symmetry of the fast operator (test_kernel.py:136-144)
+    lhs = float(u @ gw)
+    rhs = float(gu @ w)
+    assert abs(lhs - rhs) <= 1e-4 * max(abs(lhs), 1.0)
+    # L 1 = 0 and A 1 = lam 1 (test_linops.py:262-269)
+    system = nld.ShiftedSystem(op, 0.5, 1e-3)
+    ones = torch.ones(op.n, dtype=torch.float64, device="cuda")
+    assert float((system.apply(ones) - 0.5).abs().max()) < 1e-8
+    # batched = stacked single products
+    both = op.apply(torch.stack([u, w]))
+    assert rel(both[0].cpu(), gu.cpu()) < 1e-15
+    assert rel(both[1].cpu(), gw.cpu()) < 1e-15
+    # determinism
+    assert torch.equal(op.apply(u), gu)
+
+
+def test_batched_alpha_sweep_matches_single_solves(golden):
+    g = golden("c1")
+    op, _, _, f = operator("c1")
+    eta = op.degree()
+    alphas = synth.alpha_sweep(float(eta.mean()), 4)
+    batch = nld.deflated_solve_batched(op, f[:, 0], 1.0, alphas,
+                                       tol=synth.CG_TOL, maxit=200)
+    for a, res in zip(alphas, batch):
+        single = nld.deflated_solve(nld.ShiftedSystem(op, 1.0, a), f[:, 0],
+                                    tol=synth.CG_TOL, maxit=200)
+        assert res.iterations == single.iterations
+        assert rel(res.x, single.x) < 1e-12
+
+
+# ------------------------------------------------ basis / pcg / errors
+
+def test_deflating_basis_against_oracle():
+    rng = np.random.default_rng(2)
+    for n in (2, 30, 301, 5000):
+        v = rng.standard_normal(n)
+        v[0] += np.sign(v[0]) + 0.1
+        x = rng.standard_normal(n)
+        ob = O.Basis(v)
+        b = nld.DeflatingBasis(v)
+        assert np.abs(b.apply(x) - ob.apply(x)).max() < 1e-11
+        assert np.abs(b.apply_adjoint(x) - ob.apply_adjoint(x)).max() < 1e-11
+        assert np.abs(b.apply_adjoint(b.apply(x)) - x).max() < 1e-11
+    x = np.array([2.0, 3.0, 5.0, 7.0])
+    assert np.array_equal(nld.scs_up(x), [17.0, 14.0, 9.0, 2.0])
+    assert np.array_equal(nld.scs_down(x), [17.0, 2.0, 5.0, 10.0])
+    with pytest.raises(ValueError):
+        nld.DeflatingBasis(np.array([0.0, 1.0, 2.0]))
+
+
+def test_generic_pcg():
+    rng = np.random.default_rng(3)
+    m = rng.standard_normal((30, 30))
+    a = m @ m.T + 30 * np.eye(30)
+    b = rng.standard_normal(30)
+    res = nld.pcg(lambda x: a @ x, b, tol=1e-12, maxit=200)
+    assert res.converged
+    assert np.abs(res.x - np.linalg.solve(a, b)).max() < 1e-9
+    d = np.array([1.0, 4.0, 9.0])
+    res = nld.pcg(lambda x: d * x, np.ones(3), prec=lambda r: r / d,
+                  tol=1e-14, maxit=10)
+    assert res.converged and res.iterations == 1
+    with pytest.raises(nld.SolverBreakdownError):
+        nld.pcg(lambda x: np.diag([1.0, -1.0]) @ x, np.array([1.0, 1.0]),
+                maxit=10)
+
+
+def test_solver_edge_cases(golden):
+    op, _, _, f = operator("c0")
+    system = nld.ShiftedSystem(op, 1.0, 1e-3)
+    res = nld.deflated_solve(system, f[:, 0], maxit=0)
+    assert not res.converged and res.iterations == 0
+    # zero right-hand side (test_linops.py:162-164)
+    res = nld.deflated_solve(system, np.zeros(op.n))
+    assert res.converged and res.iterations == 0
+    assert res.relative_residual == 0.0 and np.abs(res.x).max() == 0.0
+    with pytest.raises(ValueError):
+        nld.deflated_solve(system, f[:, 0], prec="ilu")
+    with pytest.raises(nld.DimensionMismatchError):
+        op.apply(np.ones(3))
+
+
+def test_dense_limit():
+    rng = np.random.default_rng(0)
+    op = nld.AnovaOperator(rng.random((6000, 3)), [np.arange(3)], 40.0,
+                           mode="exact")
+    with pytest.raises(nld.DenseLimitError):
+        op.apply(np.ones(6000))

@@ -1,0 +1,88 @@
+"""CPU: host-side validation, error mapping and input generation."""
+
+import numpy as np
+import pytest
+
+import paper_2407_06834_b200 as nld
+from paper_2407_06834_b200 import _lib, synth
+
+
+class TestValidation:
+    """Same exceptions, same order as kernel.py:30-48 / linops.py:31-37."""
+
+    def test_wide_window_rejected(self):
+        with pytest.raises(nld.WindowSizeError):
+            nld.AnovaOperator(np.zeros((5, 4)), [np.arange(4)], 1.0)
+
+    def test_window_index_out_of_range(self):
+        with pytest.raises(nld.DimensionMismatchError):
+            nld.AnovaOperator(np.zeros((5, 2)), [np.array([2])], 1.0)
+
+    def test_bad_sigma(self):
+        with pytest.raises(ValueError):
+            nld.AnovaOperator(np.zeros((5, 2)), [np.arange(2)], 0.0)
+
+    def test_empty_features_rejected(self):
+        with pytest.raises(nld.DimensionMismatchError):
+            nld.AnovaOperator(np.zeros((0, 3)), [np.arange(3)], 1.0)
+
+    def test_features_must_be_2d(self):
+        with pytest.raises(nld.DimensionMismatchError):
+            nld.AnovaOperator(np.zeros(5), [np.arange(1)], 1.0)
+
+    def test_no_windows(self):
+        with pytest.raises(ValueError):
+            nld.AnovaOperator(np.zeros((5, 2)), [], 1.0)
+
+    def test_unknown_mode(self):
+        with pytest.raises(ValueError):
+            nld.AnovaOperator(np.zeros((5, 2)), [np.arange(2)], 1.0,
+                              mode="approx")
+
+    def test_odd_expansion(self):
+        with pytest.raises(ValueError):
+            nld.AnovaOperator(np.zeros((5, 2)), [np.arange(2)], 1.0,
+                              n_expansion=31)
+
+    def test_errors_share_the_reference_hierarchy(self):
+        for exc in (nld.DimensionMismatchError, nld.ScalingOverflowError,
+                    nld.WindowSizeError, nld.DenseLimitError,
+                    nld.SolverBreakdownError):
+            assert issubclass(exc, nld.NldenoiseError)
+
+
+def test_status_codes_map_to_reference_exceptions():
+    for code, exc in [(_lib.ERR_DIMENSION, nld.DimensionMismatchError),
+                      (_lib.ERR_SCALING, nld.ScalingOverflowError),
+                      (_lib.ERR_WINDOW, nld.WindowSizeError),
+                      (_lib.ERR_DENSE_LIMIT, nld.DenseLimitError),
+                      (_lib.ERR_BREAKDOWN, nld.SolverBreakdownError),
+                      (_lib.ERR_VALUE, ValueError)]:
+        with pytest.raises(exc):
+            _lib.check(code)
+    _lib.check(0)
+
+
+@pytest.mark.parametrize("name,n,d,nwin", [("c0", 4096, 9, 3),
+                                           ("c2", 1048576, 25, 9),
+                                           ("c3", 262144, 27, 9)])
+def test_generator_shapes(name, n, d, nwin):
+    feats, wins, f = synth.make_problem(name)
+    assert feats.shape == (n, d) and len(wins) == nwin
+    assert feats.min() >= -0.2 and feats.max() <= 0.2
+    assert f.min() >= 0.0 and f.max() <= 1.0
+    sizes = [w.size for w in wins]
+    assert sizes[:-1] == [3] * (nwin - 1) and sizes[-1] in (1, 3)
+    # windows cover the features once, in row-major patch order
+    assert np.array_equal(np.concatenate(wins), np.arange(d))
+
+
+def test_generator_is_deterministic():
+    a = synth.make_problem("c0")[0]
+    b = synth.make_problem("c0")[0]
+    assert np.array_equal(a, b)
+
+
+def test_alpha_sweep():
+    al = synth.alpha_sweep(100.0, 16)
+    assert al.size == 16 and np.isclose(al[0], 0.01) and np.isclose(al[-1], 1.0)
