@@ -1,0 +1,407 @@
+"""Benchmark: ANOVA-Laplacian matvecs/s (fp64) + CG denoise solve time.
+
+One *step* is one batched fused system matvec  y_r = v_r + a_r (eta v_r -
+Gamma v_r)  for the config-4 alpha sweep (16 right-hand sides sharing every
+Gamma application; BASELINE.json configs[4], 4096x4096, N = 16,777,216,
+3 windows of 3 features, M = 32, m = 4, fp64).  Matvecs count per right-hand
+side.  Inputs are device resident (2.1 GB of vectors + 9.7 GB of node tables,
+far larger than the 126 MB L2, so no explicit flush).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+`--impl reference` times the reference's CPU algorithm (the C+numpy port in
+oracle/, all host threads) on a bounded sample of the same workload and
+prints the same metric.  The driver launches N > 1 under torchrun; this round
+the multi-GPU path runs N independent replicas.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "ANOVA-Laplacian matvecs/s (fp64)"
+UNIT = "matvec/s"
+SAMPLE_NODES = 1 << 20        # CPU baseline: pixels [0, 2^20) of the config
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c4")
+    ap.add_argument("--nrhs", type=int, default=0, help="0: config default")
+    ap.add_argument("--no-cg", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# --------------------------------------------------------------------------
+# CPU baseline (reference algorithm, C + numpy port, all host threads)
+# --------------------------------------------------------------------------
+
+def cpu_sample(cfg_name, steps=2, warmup=1):
+    from oracle.cpu_port import CpuPort
+    from paper_2407_06834_b200 import synth
+
+    feats, wins, _ = synth.make_problem(cfg_name)
+    n_full = feats.shape[0]
+    ns = min(SAMPLE_NODES, n_full)
+    sub = np.ascontiguousarray(feats[:ns])
+    port = CpuPort(sub, wins, synth.SIGMA, n_expansion=synth.N_EXPANSION,
+                   cutoff=synth.CUTOFF, oversampling=synth.OVERSAMPLING)
+    eta = port.degree()
+    mu = synth.ALPHA_SCALE / float(eta.mean())
+    v = synth.random_vector(ns)
+    for _ in range(warmup):
+        port.system_apply(v, 1.0, mu)
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        port.system_apply(v, 1.0, mu)
+        times.append(time.perf_counter() - t0)
+    scale = ns / n_full
+    best = min(times)
+    return {
+        "value": scale / best,
+        "unit": UNIT,
+        "cores": port.nthreads,
+        "kind": "port",
+        "sample": (f"{cfg_name} pixels [0,{ns}) of {n_full} (all {len(wins)} "
+                   f"windows, M=32, m=4), one single-RHS ShiftedSystem.apply "
+                   f"per step on {port.nthreads} host threads (C restatement of "
+                   f"_kernels.py spread/gather + numpy pocketfft), best of "
+                   f"{steps} after {warmup} warm-up; scaled by {ns}/{n_full}"),
+        "sample_seconds": best,
+        "host_cpus": os.cpu_count(),
+        "times_s": times,
+    }
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return
+    res = cpu_sample(args.config, steps=max(1, args.steps), warmup=max(0, args.warmup))
+    line = {
+        "metric": METRIC, "value": res["value"], "unit": UNIT,
+        "impl": "reference", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * res["sample_seconds"],
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.config} fused system matvec (cpu sample)",
+                   "n_nodes": int(4096 * 4096 if args.config == "c4" else 0)},
+        "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind",
+                                             "sample")},
+        "e2e": {"value": res["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------
+# clocks during the timed region
+# --------------------------------------------------------------------------
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,"
+              "clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index),
+                 f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                out, _ = self.proc.communicate()
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown",
+                 "sw_power_cap"]
+        for ln in getattr(self, "lines", []):
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[3:7]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [],
+                    "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------
+# our arm
+# --------------------------------------------------------------------------
+
+def ncu_traffic(kernel_tag):
+    """dram bytes per launch of the dominant kernel from the committed
+    `ncu --set full` summary (profiles/ncu_summary.json), if present."""
+    path = os.path.join(REPO, "profiles", "ncu_summary.json")
+    try:
+        with open(path) as fh:
+            data = json.load(fh)
+        ent = data.get("kernels", {}).get(kernel_tag)
+        return None if ent is None else ent.get("dram_bytes_per_launch")
+    except (OSError, ValueError):
+        return None
+
+
+def run_ours(args, world, rank, local):
+    import torch
+
+    import paper_2407_06834_b200 as nld
+    from paper_2407_06834_b200 import _lib, synth
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+        pg = dist
+    cfg = synth.CONFIGS[args.config]
+    nrhs = args.nrhs or cfg.n_alpha
+    feats, wins, f_img = synth.make_problem(args.config)
+    n = feats.shape[0]
+    feat_t = torch.from_numpy(feats).to(dev)
+    t_setup = time.perf_counter()
+    op = nld.AnovaOperator(feat_t, wins, synth.SIGMA,
+                           n_expansion=synth.N_EXPANSION, cutoff=synth.CUTOFF,
+                           oversampling=synth.OVERSAMPLING)
+    eta = op.degree_device()
+    torch.cuda.synchronize()
+    t_setup = time.perf_counter() - t_setup
+    mean_eta = float(eta.mean())
+    alphas = synth.alpha_sweep(mean_eta, nrhs)
+    coef = np.stack([np.ones(nrhs), alphas], axis=1).ravel()
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1234 + rank)
+    V = torch.randn((nrhs, n), dtype=torch.float64, device=dev, generator=gen)
+    Y = torch.empty_like(V)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        op.apply_device(V, _lib.APPLY_SYSTEM, nrhs, coef, out=Y)
+
+    # fp64 FMA peak on this GPU (roofline denominator)
+    import ctypes
+    tf, pms = ctypes.c_double(), ctypes.c_double()
+    _lib.check(_lib.lib.nld_probe_fp64(1 << 16, 0, ctypes.byref(tf), ctypes.byref(pms),
+                                       ctypes.c_void_p(stream.cuda_stream)))
+    fp64_peak = tf.value
+
+    for _ in range(max(args.warmup, 0)):
+        step()
+    torch.cuda.synchronize()
+    op.set_timing(True)
+    stage = {"spread_ms": 0.0, "assemble_ms": 0.0, "conv_ms": 0.0,
+             "gather_ms": 0.0, "epilogue_ms": 0.0}
+    launches = 0
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    if pg:
+        pg.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+            st = op.stats()
+            for k in stage:
+                stage[k] += st[k]
+            launches += st["launches"]
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    if pg:
+        pg.barrier()
+    op.set_timing(False)
+    elapsed_ms = ev0.elapsed_time(ev1)
+    if pg:
+        t = torch.tensor([elapsed_ms], device=dev)
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        elapsed_ms = float(t.item())
+    ms_step = elapsed_ms / max(args.steps, 1)
+    value = world * nrhs * args.steps / (elapsed_ms * 1e-3)
+
+    # e2e through the public API: pinned host inputs -> device -> result back
+    e2e_steps = max(1, min(args.e2e_steps, args.steps))
+    Vh = torch.empty((nrhs, n), dtype=torch.float64, pin_memory=True)
+    Vh.copy_(V.cpu())
+    Yh = torch.empty((nrhs, n), dtype=torch.float64, pin_memory=True)
+    Vd = torch.empty_like(V)
+    Yd = torch.empty_like(V)
+    torch.cuda.synchronize()
+    if pg:
+        pg.barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        Vd.copy_(Vh, non_blocking=True)
+        op.apply_device(Vd, _lib.APPLY_SYSTEM, nrhs, coef, out=Yd)
+        Yh.copy_(Yd, non_blocking=True)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1)
+    if pg:
+        t = torch.tensor([e2e_ms], device=dev)
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e_val = world * nrhs * e2e_steps / (e2e_ms * 1e-3)
+    del Vh, Yh, Vd, Yd
+
+    # roofline of the dominant kernel (stage timings are CUDA events on the
+    # launching stream, summed over the timed region)
+    info = [op.window_info(w) for w in range(len(wins))]
+    sum_d = sum(i["dim"] for i in info)
+    flops_pt = sum(2 * (2 * synth.CUTOFF) ** i["dim"] for i in info)  # FMA=2
+    dominant = "gather" if stage["gather_ms"] >= stage["spread_ms"] else "spread"
+    dom_ms = stage[dominant + "_ms"] / max(args.steps, 1)
+    # minimal algorithmic bytes of one launch: raw coordinates
+    # (8 B per window dimension) + one fp64 vector per right-hand side
+    alg_bytes = n * (8 * sum_d + 8 * nrhs)
+    alg_flops = n * nrhs * flops_pt
+    hbm_peak = 6458.4
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as fh:
+            hbm_peak = float(json.load(fh)["hbm_gbs"])
+        peak_src = "MEASURED_PEAKS.json"
+    except (OSError, ValueError, KeyError):
+        peak_src = "fallback"
+    achieved = alg_bytes / (dom_ms * 1e-3) / 1e9
+    tag = f"k_{dominant}<3,4>"
+    roofline = {
+        "bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+        "frac": achieved / hbm_peak, "traffic": ncu_traffic(tag),
+        "kernel": tag, "kernel_ms": dom_ms, "peak_source": f"{peak_src} hbm_gbs",
+        "bytes_model": ("minimal: N*(8*sum_l d_l + 8*nrhs) per launch "
+                        "(coordinates + one vector per rhs; SURVEY §8d)"),
+        "fp64": {"achieved_tflops": alg_flops / (dom_ms * 1e-3) / 1e12,
+                 "peak_tflops": fp64_peak,
+                 "frac": alg_flops / (dom_ms * 1e-3) / 1e12 / fp64_peak,
+                 "peak_source": "nld_probe_fp64 DFMA loop, this GPU, this run",
+                 "flops_model": "N*nrhs*sum_l 2*(2m)^d_l per launch"},
+        "stage_share": {k: v / max(elapsed_ms, 1e-9) for k, v in stage.items()},
+    }
+
+    # CG denoise solve (deflated Jacobi, tol 1e-6) over the alpha sweep
+    cg = None
+    if not args.no_cg:
+        f = torch.from_numpy(np.ascontiguousarray(f_img[:, 0])).to(dev)
+        torch.cuda.synchronize()
+        c0 = torch.cuda.Event(enable_timing=True)
+        c1 = torch.cuda.Event(enable_timing=True)
+        c0.record(stream)
+        res = nld.deflated_solve_batched(op, f, 1.0, alphas, prec="jacobi",
+                                         tol=synth.CG_TOL, maxit=200)
+        c1.record(stream)
+        torch.cuda.synchronize()
+        its = [r.iterations for r in res]
+        cg = {"solve_ms": c0.elapsed_time(c1), "nrhs": nrhs,
+              "iterations": its, "converged": all(r.converged for r in res),
+              "relres_max": max(r.relative_residual for r in res),
+              "tol": synth.CG_TOL, "prec": "jacobi (deflated)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            cpu = cpu_sample(args.config)
+            cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        except Exception as exc:  # the baseline must not sink the bench line
+            cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "port",
+                   "sample": f"unavailable: {exc}"}
+    if cg is not None and cpu is not None and cpu.get("value"):
+        nmv = sum(cg["iterations"]) + 2 * nrhs
+        cg["cpu_extrapolated_s"] = nmv / cpu["value"]
+        cg["cpu_extrapolation"] = ("reference matvecs (iterations + 2 per alpha) "
+                                   "x sampled CPU matvec time")
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True,
+            "scaling": "weak" if world > 1 else "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": (f"{args.config}: batched fused system matvec "
+                                    f"y = v + a_k(eta v - Gamma v), {nrhs} rhs"),
+                       "n_nodes": n, "windows": [len(w) for w in wins],
+                       "nrhs": nrhs, "bandwidth": synth.N_EXPANSION,
+                       "cutoff": synth.CUTOFF, "grid": 64,
+                       "parallelism": f"replicas{world}" if world > 1 else "single",
+                       "l2": "inputs larger than L2 (no flush)",
+                       "setup_s": t_setup},
+            "roofline": roofline, "cpu_baseline": cpu,
+            "e2e": {"value": e2e_val, "unit": UNIT,
+                    "h2d_bytes_per_step": int(nrhs * n * 8),
+                    "d2h_bytes_per_step": int(nrhs * n * 8),
+                    "steps": e2e_steps},
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+            "cg": cg,
+        }
+        print(json.dumps(line), flush=True)
+    if pg:
+        pg.destroy_process_group()
+
+
+def main():
+    args = parse()
+    world, rank, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+    else:
+        run_ours(args, world, rank, local)
+
+
+if __name__ == "__main__":
+    main()

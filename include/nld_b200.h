@@ -170,6 +170,12 @@ NLD_API int nld_axpby(double a, const double* x, double b, const double* y,
 NLD_API int nld_dot(const double* x, const double* y, int64_t n, double* result,
             void* stream);
 
+/* fp64 FMA throughput probe (the roofline denominator of the FMA-bound
+ * spread/gather kernels): 8 independent DFMA chains per thread, `iters`
+ * steps, `blocks` x 256 threads (<= 0: 8 per SM).  HOST outputs. */
+NLD_API int nld_probe_fp64(int64_t iters, int32_t blocks, double* tflops,
+                           double* ms, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -689,6 +689,8 @@ void apply_op(nld_operator* op, int which, int kind, const double* v, double* ou
   const int m = op->params.cutoff;
   EvScope ev(op, st);
   ev.mark();
+  int launches = 0;
+  for (int g = 1; g <= kMaxDim; ++g) launches += ps.n_subs[g] ? 2 : 0;  // spread + gather
   // 1. spread (block path)
   switch (m) {
     case 3: spread_all<3>(ps, ws, v, ld, nrhs, st); break;
@@ -767,6 +769,16 @@ void apply_op(nld_operator* op, int which, int kind, const double* v, double* ou
     NLD_CUDA(cudaGetLastError());
   }
   ev.mark();
+  {
+    int maxd = 0, generic = 0;
+    for (const auto& w : ps.wdev_h) {
+      maxd = std::max(maxd, w.d);
+      generic += w.fast ? 0 : 2;
+    }
+    launches += 1 /*assemble*/ + maxd /*conv*/ + 1 /*epilogue*/ + generic +
+                (ps.n_edges ? 2 : 0);
+  }
+  op->stats.launches = launches;
 }
 
 static void dense_tables(nld_operator* op, int** widx, int** woff, cudaStream_t st) {

@@ -1,0 +1,58 @@
+// fp64 FMA throughput probe: the roofline denominator for the spread/gather
+// kernels, which are fp64-FMA bound (SURVEY.md §7 hard part 1).
+// MEASURED_PEAKS.json carries HBM and bf16 only, so bench.py measures the
+// sustained DFMA rate on the same box, in the same run.
+#include "nld_internal.cuh"
+
+namespace {
+
+constexpr int kChains = 8;
+
+__global__ void __launch_bounds__(256) k_dfma(double* out, int64_t iters, double a, double b) {
+  double x[kChains];
+#pragma unroll
+  for (int c = 0; c < kChains; ++c) x[c] = threadIdx.x * 1e-7 + c;
+  for (int64_t i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int c = 0; c < kChains; ++c) x[c] = fma(x[c], a, b);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int c = 0; c < kChains; ++c) s += x[c];
+  if (s == 12345.678) out[0] = s;  // keep the chains alive
+}
+
+}  // namespace
+
+extern "C" NLD_API int nld_probe_fp64(int64_t iters, int32_t blocks, double* tflops,
+                                      double* ms, void* stream) {
+  try {
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    int dev = 0;
+    NLD_CUDA(cudaGetDevice(&dev));
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (blocks <= 0) blocks = sms * 8;
+    double* out = nullptr;
+    NLD_CUDA(cudaMallocAsync(&out, sizeof(double), st));
+    cudaEvent_t e0, e1;
+    NLD_CUDA(cudaEventCreate(&e0));
+    NLD_CUDA(cudaEventCreate(&e1));
+    k_dfma<<<blocks, 256, 0, st>>>(out, iters / 8, 0.999999, 1e-9);  // warm-up
+    NLD_CUDA(cudaEventRecord(e0, st));
+    k_dfma<<<blocks, 256, 0, st>>>(out, iters, 0.999999, 1e-9);
+    NLD_CUDA(cudaEventRecord(e1, st));
+    NLD_CUDA(cudaEventSynchronize(e1));
+    float t = 0.f;
+    cudaEventElapsedTime(&t, e0, e1);
+    const double flops = 2.0 * kChains * (double)iters * blocks * 256.0;
+    *ms = t;
+    *tflops = flops / (t * 1e-3) / 1e12;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFreeAsync(out, st);
+    return NLD_OK;
+  } catch (const nld::Error& e) {
+    return nld::fail(e.code, e.msg);
+  }
+}

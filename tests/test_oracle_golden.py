@@ -114,3 +114,15 @@ def test_known_answers():
     assert np.allclose(O.ndft(c, np.array([0.25])), [-1j], atol=1e-14)
     assert np.allclose(O.gauss_direct([0.0, 1.0], [0.0], [1.0, 1.0], 1.0),
                        [1.0 + np.exp(-1.0)], atol=1e-14)
+
+
+def test_cpu_port_matches_reference(golden):
+    from oracle.cpu_port import CpuPort
+    g = golden("c0")
+    feats, wins, _ = synth.make_problem("c0")
+    v = synth.random_vector(feats.shape[0])
+    port = CpuPort(feats, wins, synth.SIGMA, **PIN)
+    assert rel(port.apply(v), g["gv"]) < 1e-12
+    assert rel(port.system_apply(v, 1.0, float(g["mu"])), g["av"]) < 1e-12
+    one = CpuPort(feats, wins, synth.SIGMA, nthreads=1, **PIN)
+    assert rel(one.apply(v), g["gv"]) < 1e-12
