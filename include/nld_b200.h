@@ -175,6 +175,9 @@ NLD_API int nld_dot(const double* x, const double* y, int64_t n, double* result,
  * steps, `blocks` x 256 threads (<= 0: 8 per SM).  HOST outputs. */
 NLD_API int nld_probe_fp64(int64_t iters, int32_t blocks, double* tflops,
                            double* ms, void* stream);
+/* the same for the fp64 tensor path (mma.sync m8n8k4 f64, DMMA). */
+NLD_API int nld_probe_dmma(int64_t iters, int32_t blocks, double* tflops,
+                           double* ms, void* stream);
 
 #ifdef __cplusplus
 }

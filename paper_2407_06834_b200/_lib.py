@@ -83,6 +83,7 @@ SIGNATURES = {
     "nld_axpby": (ctypes.c_int, [_D, _P, _D, _P, _P, _I64, _P]),
     "nld_dot": (ctypes.c_int, [_P, _P, _I64, _PD, _P]),
     "nld_probe_fp64": (ctypes.c_int, [_I64, _I32, _PD, _PD, _P]),
+    "nld_probe_dmma": (ctypes.c_int, [_I64, _I32, _PD, _PD, _P]),
 }
 
 

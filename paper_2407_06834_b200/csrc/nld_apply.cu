@@ -22,14 +22,18 @@
 //  * gather: one CTA per subproblem; the (2m)^3 grid block of its cell sits in
 //    shared memory, each thread owns a node and contracts a -> b -> c.
 #include <algorithm>
+#include <cstdlib>
 
 #include "nld_internal.cuh"
+#include "nld_mma.cuh"
 
 namespace nld {
 
 namespace {
 
-constexpr int kThreads = 128;
+constexpr int kThreads = 128;      // gather / generic CTAs
+constexpr int kSpreadWarps = 8;    // spread CTA = 8 warps
+constexpr int kSpreadThreads = 32 * kSpreadWarps;
 constexpr int kChunk = 128;
 
 template <int D, int MC>
@@ -43,15 +47,15 @@ struct Geo {
   static constexpr int TEAM_RAW = (PAIRS + R - 1) / R;
   static constexpr int TEAM = TEAM_RAW <= 1 ? 1 : TEAM_RAW <= 2 ? 2 : TEAM_RAW <= 4 ? 4
                               : TEAM_RAW <= 8 ? 8 : TEAM_RAW <= 16 ? 16 : 32;
-  static constexpr int NTEAM = kThreads / TEAM;
+  static constexpr int TPW = 32 / TEAM;                // teams per warp
   static constexpr int ROW = S * D;                    // global row (doubles)
-  static constexpr int SROW_RAW = D * S + 1;            // [C][B][A'] + v slot
-  static constexpr int SROW = (SROW_RAW % 2) ? SROW_RAW + 1 : SROW_RAW;
+  static constexpr int SROW_RAW = D * S;                // [C][B][A]
+  static constexpr int SROW = (SROW_RAW % 4 == 0) ? SROW_RAW + 2 : SROW_RAW;  // 16B aligned, bank skew
   static constexpr int BLK = SA * SB * SC;
-  static constexpr int NWARP = kThreads / 32;
-  static constexpr int SMEM_STAGE = kChunk * SROW + kChunk;
-  static constexpr int SMEM_RED = NWARP * BLK;
+  static constexpr int SMEM_STAGE = kChunk * SROW + kChunk * kSpreadWarps;
+  static constexpr int SMEM_RED = kSpreadWarps * BLK;
   static constexpr int SMEM = SMEM_STAGE > SMEM_RED ? SMEM_STAGE : SMEM_RED;
+  static constexpr int GRB = (BLK <= 512) ? 16 : 8;      // gather rhs per smem pass
 };
 
 __device__ __forceinline__ int wrap_pos(int p, int w) {
@@ -69,24 +73,36 @@ __device__ __forceinline__ int64_t box_flat(const WinDev& wd, const int* p) {
 }
 
 // ---- spread ---------------------------------------------------------------
+//
+// CTA = one subproblem, all right-hand sides.  The node rows of a chunk are
+// staged once in shared memory and reused by every rhs.  Warps map onto
+// (rhs slot, point slice): with nrhs >= 8 each warp owns one rhs and the
+// whole block (no cross-warp reduction); with fewer rhs several warps share
+// an rhs and reduce through shared memory at the end.  Inside a warp, TEAM
+// lanes own the (a,b) pairs of the (2m)^D block and accumulate its c-axis
+// in registers; C weights are read by 16-byte broadcast.
 
 template <int D, int MC>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kSpreadThreads)
 k_spread(const SubDev* __restrict__ subs, const WinDev* __restrict__ wins,
          const double* __restrict__ rows, const int32_t* __restrict__ pix,
-         const double* __restrict__ v, int64_t ldv, double* __restrict__ blocks,
-         int64_t blk_ld) {
+         const double* __restrict__ vt, int nrhs, double* __restrict__ blocks) {
   using G = Geo<D, MC>;
   extern __shared__ double sm[];
-  double* sv = sm + kChunk * G::SROW;
+  double* sv = sm + kChunk * G::SROW;          // [kChunk][kSpreadWarps]
   const SubDev sd = subs[blockIdx.x];
-  const int rhs = blockIdx.y;
   const WinDev wd = wins[sd.win];
-  const double* __restrict__ vr = v + rhs * ldv;
   const int tid = threadIdx.x;
   const int lane = tid & 31;
+  const int warp = tid >> 5;
   const int tl = lane & (G::TEAM - 1);
-  const int team = tid / G::TEAM;
+  const int rgs = nrhs < kSpreadWarps ? nrhs : kSpreadWarps;   // rhs per group
+  const int wpr = kSpreadWarps / rgs;                           // warps per rhs
+  const int slot = warp / wpr;
+  const int slice = warp - slot * wpr;
+  const int team = slice * G::TPW + lane / G::TEAM;
+  const int nteam = wpr * G::TPW;
+  const bool busy = slot < rgs;
 
   int pa[G::R], pb[G::R];
   bool pok[G::R];
@@ -97,81 +113,100 @@ k_spread(const SubDev* __restrict__ subs, const WinDev* __restrict__ wins,
     pa[r] = pok[r] ? p / G::SB : 0;
     pb[r] = pok[r] ? p % G::SB : 0;
   }
-  double acc[G::R][G::SC];
-#pragma unroll
-  for (int r = 0; r < G::R; ++r)
-#pragma unroll
-    for (int c = 0; c < G::SC; ++c) acc[r][c] = 0.0;
-
   const int64_t local = sd.start - wd.node_off;
   const double* __restrict__ rw = rows + wd.row_off + local * G::ROW;
   const int32_t* __restrict__ pw = pix + sd.start;
 
-  for (int c0 = 0; c0 < sd.count; c0 += kChunk) {
-    const int cn = min(kChunk, sd.count - c0);
-    __syncthreads();
-    for (int e = tid; e < cn; e += kThreads) sv[e] = vr[pw[c0 + e]];
-    __syncthreads();
-    // stage rows: dim s -> smem segment (D-1-s)*S; dim 0 of a 3-D window is
-    // pre-multiplied by v; lower-dimensional windows keep v in slot D*S.
-    for (int e = tid; e < cn * G::ROW; e += kThreads) {
-      const int pt = e / G::ROW;
-      const int k = e - pt * G::ROW;
-      const int s = k / G::S;
-      const int i = k - s * G::S;
-      double val = rw[(int64_t)(c0 + pt) * G::ROW + k];
-      if (D == 3 && s == 0) val *= sv[pt];
-      sm[pt * G::SROW + (D - 1 - s) * G::S + i] = val;
-    }
-    if (D < 3)
-      for (int e = tid; e < cn; e += kThreads) sm[e * G::SROW + D * G::S] = sv[e];
-    __syncthreads();
-    for (int pt = team; pt < cn; pt += G::NTEAM) {
-      const double* row = sm + pt * G::SROW;
-      double cw[G::SC];
-#pragma unroll
-      for (int c = 0; c < G::SC; c += 2) {
-        double2 t = *reinterpret_cast<const double2*>(row + c);
-        cw[c] = t.x;
-        cw[c + 1] = t.y;
-      }
-#pragma unroll
-      for (int r = 0; r < G::R; ++r) {
-        double ab;
-        if (D == 3) ab = row[2 * G::S + pa[r]] * row[G::S + pb[r]];
-        else if (D == 2) ab = row[2 * G::S] * row[G::S + pb[r]];
-        else ab = row[G::S];
-#pragma unroll
-        for (int c = 0; c < G::SC; ++c) acc[r][c] = fma(ab, cw[c], acc[r][c]);
-      }
-    }
-  }
-  // reduce the teams of a warp, then the warps of the CTA
-#pragma unroll
-  for (int off = G::TEAM; off < 32; off <<= 1)
+  for (int rg = 0; rg < nrhs; rg += rgs) {
+    const int rhs = rg + slot;
+    const bool act = busy && rhs < nrhs;
+    double acc[G::R][G::SC];
 #pragma unroll
     for (int r = 0; r < G::R; ++r)
 #pragma unroll
-      for (int c = 0; c < G::SC; ++c)
-        acc[r][c] += __shfl_xor_sync(0xffffffffu, acc[r][c], off);
-  __syncthreads();
-  const int warp = tid >> 5;
-  if (lane < G::TEAM) {
-#pragma unroll
-    for (int r = 0; r < G::R; ++r)
-      if (pok[r]) {
-        const int p = tl + G::TEAM * r;
-#pragma unroll
-        for (int c = 0; c < G::SC; ++c) sm[warp * G::BLK + p * G::SC + c] = acc[r][c];
+      for (int c = 0; c < G::SC; ++c) acc[r][c] = 0.0;
+    for (int c0 = 0; c0 < sd.count; c0 += kChunk) {
+      const int cn = min(kChunk, sd.count - c0);
+      __syncthreads();
+      // v of this rhs group, pixel-major input [N][nrhs]
+      for (int e = tid; e < cn * rgs; e += kSpreadThreads) {
+        const int pt = e / rgs, q = e - pt * rgs;
+        sv[pt * kSpreadWarps + q] =
+            (rg + q < nrhs) ? vt[(int64_t)pw[c0 + pt] * nrhs + rg + q] : 0.0;
       }
-  }
-  __syncthreads();
-  double* __restrict__ out = blocks + rhs * blk_ld + sd.block;
-  for (int e = tid; e < G::BLK; e += kThreads) {
-    double s = sm[e];
+      // rows: dim s -> smem segment (D-1-s)*S (C first, then B, then A)
+      if (rg == 0 || sd.count > kChunk) {
+        for (int e = tid; e < cn * G::ROW; e += kSpreadThreads) {
+          const int pt = e / G::ROW;
+          const int k = e - pt * G::ROW;
+          const int sdim = k / G::S;
+          const int i = k - sdim * G::S;
+          sm[pt * G::SROW + (D - 1 - sdim) * G::S + i] = rw[(int64_t)(c0 + pt) * G::ROW + k];
+        }
+      }
+      __syncthreads();
+      if (act) {
+        for (int pt = team; pt < cn; pt += nteam) {
+          const double* row = sm + pt * G::SROW;
+          const double v = sv[pt * kSpreadWarps + slot];
+          double cw[G::SC];
 #pragma unroll
-    for (int w = 1; w < G::NWARP; ++w) s += sm[w * G::BLK + e];
-    out[e] = s;
+          for (int c = 0; c < G::SC; c += 2) {
+            double2 t = *reinterpret_cast<const double2*>(row + c);
+            cw[c] = t.x;
+            cw[c + 1] = t.y;
+          }
+#pragma unroll
+          for (int r = 0; r < G::R; ++r) {
+            double ab;
+            if (D == 3) ab = (v * row[2 * G::S + pa[r]]) * row[G::S + pb[r]];
+            else if (D == 2) ab = v * row[G::S + pb[r]];
+            else ab = v;
+#pragma unroll
+            for (int c = 0; c < G::SC; ++c) acc[r][c] = fma(ab, cw[c], acc[r][c]);
+          }
+        }
+      }
+    }
+    // teams of a warp -> lanes [0, TEAM)
+#pragma unroll
+    for (int off = G::TEAM; off < 32; off <<= 1)
+#pragma unroll
+      for (int r = 0; r < G::R; ++r)
+#pragma unroll
+        for (int c = 0; c < G::SC; ++c)
+          acc[r][c] += __shfl_xor_sync(0xffffffffu, acc[r][c], off);
+    if (wpr == 1) {
+      if (act && lane < G::TEAM) {
+#pragma unroll
+        for (int r = 0; r < G::R; ++r)
+          if (pok[r]) {
+            const int p = tl + G::TEAM * r;
+#pragma unroll
+            for (int c = 0; c < G::SC; ++c)
+              blocks[(sd.block + p * G::SC + c) * nrhs + rhs] = acc[r][c];
+          }
+      }
+    } else {
+      __syncthreads();
+      if (busy && lane < G::TEAM) {
+#pragma unroll
+        for (int r = 0; r < G::R; ++r)
+          if (pok[r]) {
+            const int p = tl + G::TEAM * r;
+#pragma unroll
+            for (int c = 0; c < G::SC; ++c) sm[warp * G::BLK + p * G::SC + c] = acc[r][c];
+          }
+      }
+      __syncthreads();
+      for (int e = tid; e < rgs * G::BLK; e += kSpreadThreads) {
+        const int q = e / G::BLK, k = e - q * G::BLK;
+        if (rg + q >= nrhs) continue;
+        double sum = 0.0;
+        for (int w = 0; w < wpr; ++w) sum += sm[(q * wpr + w) * G::BLK + k];
+        blocks[(sd.block + k) * nrhs + rg + q] = sum;
+      }
+    }
   }
 }
 
@@ -180,16 +215,19 @@ k_spread(const SubDev* __restrict__ subs, const WinDev* __restrict__ wins,
 __global__ void k_assemble(const WinDev* __restrict__ wins, int L,
                            const int32_t* __restrict__ cellmap,
                            const CellDev* __restrict__ cells,
-                           const double* __restrict__ blocks, int64_t blk_ld,
+                           const double* __restrict__ blocks, int nrhs,
                            double* __restrict__ grid, int64_t grid_ld) {
+  // thread = (grid point, rhs) with rhs fastest: the cell lookups are shared
+  // and the block reads ([block + e][nrhs]) are contiguous across the rhs.
   const int w = blockIdx.y;
-  const int rhs = blockIdx.z;
   const WinDev wd = wins[w];
-  const double* __restrict__ bl = blocks + rhs * blk_ld;
-  double* __restrict__ g = grid + rhs * grid_ld + wd.grid_off;
   const int S = wd.S;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < wd.box_size;
-       e += (int64_t)gridDim.x * blockDim.x) {
+  const int64_t total = wd.box_size * nrhs;
+  for (int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; id < total;
+       id += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(id % nrhs);
+    const int64_t e = id / nrhs;
+    double* __restrict__ g = grid + r * grid_ld + wd.grid_off;
     if (!wd.fast) {
       g[e] = 0.0;
       continue;
@@ -206,7 +244,6 @@ __global__ void k_assemble(const WinDev* __restrict__ wins, int L,
     for (int o0 = 0; o0 < o0n; ++o0)
       for (int o1 = 0; o1 < o1n; ++o1)
         for (int o2 = 0; o2 < S; ++o2) {
-          // offsets along dims (d-3+..): map (o0,o1,o2) onto the window dims
           int off[3];
           if (wd.d == 3) { off[0] = o0; off[1] = o1; off[2] = o2; }
           else if (wd.d == 2) { off[0] = o1; off[1] = o2; off[2] = 0; }
@@ -224,12 +261,13 @@ __global__ void k_assemble(const WinDev* __restrict__ wins, int L,
           if (!ok) continue;
           int64_t key = 0;
           for (int s = 0; s < wd.d; ++s) key = key * wd.box_w[s] + c[s];
-          int cell = cellmap[wd.cellmap_off + key];
+          const int cell = cellmap[wd.cellmap_off + key];
           if (cell < 0) continue;
           const CellDev cd = cells[cell];
           int64_t inner = 0;
           for (int s = 0; s < wd.d; ++s) inner = inner * S + off[s];
-          for (int q = 0; q < cd.nsub; ++q) sum += bl[cd.block0 + (int64_t)q * cd.blk + inner];
+          for (int q = 0; q < cd.nsub; ++q)
+            sum += blocks[(cd.block0 + (int64_t)q * cd.blk + inner) * nrhs + r];
         }
     g[e] = sum;
   }
@@ -281,7 +319,7 @@ __global__ void k_spread_edges(const EdgeDev* __restrict__ edges, int64_t ne,
 __global__ void k_gather_edges(const EdgeDev* __restrict__ edges, int64_t ne,
                                const WinDev* __restrict__ wins,
                                const double* __restrict__ grid, int64_t grid_ld,
-                               double* __restrict__ wout, int64_t N, int L) {
+                               double* __restrict__ wout, int64_t N, int nrhs) {
   const int rhs = blockIdx.y;
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < ne;
        k += (int64_t)gridDim.x * blockDim.x) {
@@ -301,7 +339,7 @@ __global__ void k_gather_edges(const EdgeDev* __restrict__ edges, int64_t ne,
       for (int s = 0; s < wd.d; ++s) f = f * wd.box_w[s] + p[s];
       y += grid[rhs * grid_ld + wd.grid_off + f] * wp;
     }
-    wout[((int64_t)rhs * L + ed.win) * N + ed.pix] += y;
+    wout[((int64_t)ed.win * N + ed.pix) * nrhs + rhs] += y;
   }
 }
 
@@ -346,7 +384,7 @@ __global__ void k_spread_generic(const WinDev* __restrict__ wins, int w,
   }
 }
 
-__global__ void k_gather_generic(const WinDev* __restrict__ wins, int w, int L,
+__global__ void k_gather_generic(const WinDev* __restrict__ wins, int w, int nrhs,
                                  const double* __restrict__ rows,
                                  const int32_t* __restrict__ pix,
                                  const int32_t* __restrict__ key,
@@ -382,7 +420,7 @@ __global__ void k_gather_generic(const WinDev* __restrict__ wins, int w, int L,
       }
       y += grid[rhs * grid_ld + wd.grid_off + f] * wp;
     }
-    wout[((int64_t)rhs * L + w) * N + pix[wd.node_off + e]] = y;
+    wout[((int64_t)w * N + pix[wd.node_off + e]) * nrhs + rhs] = y;
   }
 }
 
@@ -434,107 +472,127 @@ __global__ void k_conv(const WinDev* __restrict__ wins, int pass,
 }
 
 // ---- gather -------------------------------------------------------------
+//
+// CTA = one subproblem, all rhs.  The (2m)^D grid blocks of its cell for a
+// group of GRB rhs sit in shared memory; each thread owns a node, holds its
+// weights in registers and contracts c -> b -> a for every rhs of the group.
 
 template <int D, int MC>
 __global__ void __launch_bounds__(kThreads)
 k_gather(const SubDev* __restrict__ subs, const CellDev* __restrict__ cells,
          const WinDev* __restrict__ wins, const double* __restrict__ rows,
          const int32_t* __restrict__ pix, const double* __restrict__ grid,
-         int64_t grid_ld, double* __restrict__ wout, int64_t N, int L) {
+         int64_t grid_ld, double* __restrict__ wout, int64_t N, int nrhs) {
   using G = Geo<D, MC>;
-  __shared__ double gb[G::BLK];
+  extern __shared__ double gb[];   // [GRB][BLK]
   const SubDev sd = subs[blockIdx.x];
-  const int rhs = blockIdx.y;
   const CellDev cd = cells[sd.cell];
   const WinDev wd = wins[sd.win];
-  const double* __restrict__ g = grid + rhs * grid_ld + wd.grid_off;
-  for (int e = threadIdx.x; e < G::BLK; e += kThreads) {
-    int off[3];
-    off[0] = e / (G::SB * G::SC);
-    off[1] = (e / G::SC) % G::SB;
-    off[2] = e % G::SC;
-    int p[3];
-    // block dims (a,b,c) -> window dims
-    if (D == 3) {
-      for (int s = 0; s < 3; ++s) p[s] = wrap_pos(cd.cc[s] + off[s], wd.box_w[s]);
-    } else if (D == 2) {
-      p[0] = wrap_pos(cd.cc[0] + off[1], wd.box_w[0]);
-      p[1] = wrap_pos(cd.cc[1] + off[2], wd.box_w[1]);
-    } else {
-      p[0] = wrap_pos(cd.cc[0] + off[2], wd.box_w[0]);
-    }
-    gb[e] = g[box_flat<D>(wd, p)];
-  }
-  __syncthreads();
   const int64_t local = sd.start - wd.node_off;
   const double* __restrict__ rw = rows + wd.row_off + local * G::ROW;
-  double* __restrict__ out = wout + ((int64_t)rhs * L + sd.win) * N;
-  for (int j = threadIdx.x; j < sd.count; j += kThreads) {
-    double wrow[G::ROW];
-    const double2* src = reinterpret_cast<const double2*>(rw + (int64_t)j * G::ROW);
-#pragma unroll
-    for (int k = 0; k < G::ROW / 2; ++k) {
-      double2 t = __ldg(src + k);
-      wrow[2 * k] = t.x;
-      wrow[2 * k + 1] = t.y;
-    }
-    // wrow: [dim0 S][dim1 S][dim2 S]; block order [a][b][c] = dims (0,1,2)
-    double y = 0.0;
-#pragma unroll
-    for (int a = 0; a < G::SA; ++a) {
-      double ua = 0.0;
-#pragma unroll
-      for (int b = 0; b < G::SB; ++b) {
-        const double* gr = gb + (a * G::SB + b) * G::SC;
-        double t = 0.0;
-#pragma unroll
-        for (int c = 0; c < G::SC; c += 2) {
-          double2 gg = *reinterpret_cast<const double2*>(gr + c);
-          t = fma(gg.x, wrow[(D - 1) * G::S + c], t);
-          t = fma(gg.y, wrow[(D - 1) * G::S + c + 1], t);
-        }
-        if (D >= 2) ua = fma(t, wrow[(D - 2) * G::S + b], ua);
-        else ua = t;
+  double* __restrict__ out = wout + (int64_t)sd.win * N * nrhs;
+  for (int rg = 0; rg < nrhs; rg += G::GRB) {
+    const int rn = min(G::GRB, nrhs - rg);
+    __syncthreads();
+    for (int e = threadIdx.x; e < rn * G::BLK; e += kThreads) {
+      const int q = e / G::BLK;
+      const int k = e - q * G::BLK;
+      int off[3];
+      off[0] = k / (G::SB * G::SC);
+      off[1] = (k / G::SC) % G::SB;
+      off[2] = k % G::SC;
+      int p[3];
+      if (D == 3) {
+        for (int s = 0; s < 3; ++s) p[s] = wrap_pos(cd.cc[s] + off[s], wd.box_w[s]);
+      } else if (D == 2) {
+        p[0] = wrap_pos(cd.cc[0] + off[1], wd.box_w[0]);
+        p[1] = wrap_pos(cd.cc[1] + off[2], wd.box_w[1]);
+      } else {
+        p[0] = wrap_pos(cd.cc[0] + off[2], wd.box_w[0]);
       }
-      if (D == 3) y = fma(ua, wrow[a], y);
-      else y = ua;
+      gb[e] = grid[(int64_t)(rg + q) * grid_ld + wd.grid_off + box_flat<D>(wd, p)];
     }
-    out[pix[sd.start + j]] = y;
+    __syncthreads();
+    for (int j = threadIdx.x; j < sd.count; j += kThreads) {
+      double wrow[G::ROW];
+      const double2* src = reinterpret_cast<const double2*>(rw + (int64_t)j * G::ROW);
+#pragma unroll
+      for (int k = 0; k < G::ROW / 2; ++k) {
+        double2 t = __ldg(src + k);
+        wrow[2 * k] = t.x;
+        wrow[2 * k + 1] = t.y;
+      }
+      double* __restrict__ o = out + (int64_t)pix[sd.start + j] * nrhs + rg;
+      for (int q = 0; q < rn; ++q) {
+        const double* gq = gb + q * G::BLK;
+        double y = 0.0;
+#pragma unroll
+        for (int a = 0; a < G::SA; ++a) {
+          double ua = 0.0;
+#pragma unroll
+          for (int b = 0; b < G::SB; ++b) {
+            const double* gr = gq + (a * G::SB + b) * G::SC;
+            double t = 0.0;
+#pragma unroll
+            for (int c = 0; c < G::SC; c += 2) {
+              double2 gg = *reinterpret_cast<const double2*>(gr + c);
+              t = fma(gg.x, wrow[(D - 1) * G::S + c], t);
+              t = fma(gg.y, wrow[(D - 1) * G::S + c + 1], t);
+            }
+            if (D >= 2) ua = fma(t, wrow[(D - 2) * G::S + b], ua);
+            else ua = t;
+          }
+          if (D == 3) y = fma(ua, wrow[a], y);
+          else y = ua;
+        }
+        o[q] = y;
+      }
+    }
   }
 }
 
 // ---- epilogue: window sum + diagonal/degree terms (kernel.py:86-93,
 //      linops.py:43-50) ---------------------------------------------------
 
-__global__ void k_epilogue(int kind, int L, int64_t N, const double* __restrict__ v,
-                           int64_t ldv, const double* __restrict__ wsum, int direct,
+__global__ void k_epilogue(int kind, int L, int64_t N, int nrhs,
+                           const double* __restrict__ v, int64_t ldv,
+                           const double* __restrict__ wsum, int direct,
                            double* __restrict__ out, int64_t ldo,
                            const double* __restrict__ eta,
                            const double* __restrict__ coef) {
-  const int rhs = blockIdx.y;
-  const double lam = coef ? coef[2 * rhs] : 0.0;
-  const double mu = coef ? coef[2 * rhs + 1] : 0.0;
+  // wsum: per-window gathers [L][N][nrhs] (or Gamma v [nrhs][N] if direct)
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const double x = v[rhs * ldv + i];
-    double gam;
-    if (direct) {
-      gam = wsum[rhs * N + i];
-    } else {
-      double s = 0.0;
-      for (int w = 0; w < L; ++w) s += wsum[((int64_t)rhs * L + w) * N + i];
-      if (kind == NLD_APPLY_WINDOW_SUM) {
-        out[rhs * ldo + i] = s;
-        continue;
+    const double et = eta ? eta[i] : 0.0;
+    for (int r = 0; r < nrhs; ++r) {
+      const double x = v[r * ldv + i];
+      double gam;
+      if (direct) {
+        gam = wsum[r * N + i];
+      } else {
+        double s = 0.0;
+        for (int w = 0; w < L; ++w) s += wsum[((int64_t)w * N + i) * nrhs + r];
+        if (kind == NLD_APPLY_WINDOW_SUM) {
+          out[r * ldo + i] = s;
+          continue;
+        }
+        gam = (s - (double)L * x) / (double)L;
       }
-      gam = (s - (double)L * x) / (double)L;
+      double y;
+      if (kind == NLD_APPLY_SYSTEM) y = coef[2 * r] * x + coef[2 * r + 1] * (et * x - gam);
+      else if (kind == NLD_APPLY_LAPLACIAN) y = et * x - gam;
+      else y = gam;
+      out[r * ldo + i] = y;
     }
-    double y;
-    if (kind == NLD_APPLY_SYSTEM) y = lam * x + mu * (eta[i] * x - gam);
-    else if (kind == NLD_APPLY_LAPLACIAN) y = eta[i] * x - gam;
-    else y = gam;
-    out[rhs * ldo + i] = y;
   }
+}
+
+// v [nrhs][ld] -> vt [N][nrhs] (pixel-major, for the spread's node gathers)
+__global__ void k_transpose_in(const double* __restrict__ v, int64_t ldv, int64_t N,
+                               int nrhs, double* __restrict__ vt) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N;
+       i += (int64_t)gridDim.x * blockDim.x)
+    for (int r = 0; r < nrhs; ++r) vt[i * nrhs + r] = v[r * ldv + i];
 }
 
 // ---- dense exact mode (kernel.py:97-114, _kernels.py:205-227) -------------
@@ -590,9 +648,20 @@ int grid_blocks(int64_t n, int threads, int cap = 148 * 8) {
   return (int)std::max<int64_t>(1, std::min<int64_t>(b, cap));
 }
 
+// NLD_NO_MMA=1 selects the CUDA-core (DFMA) kernels for the 3-D m=4 shape
+// (kept for A/B measurements; both paths are hand-written sm_100a CUDA).
+bool use_mma() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("NLD_NO_MMA");
+    v = (e && e[0] && e[0] != '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 template <int D, int MC>
-void launch_spread(const PlanSet& ps, const Workspace& ws, const double* v, int64_t ldv,
-                   int nrhs, cudaStream_t st) {
+void launch_spread(const PlanSet& ps, const Workspace& ws, const double* vt, int nrhs,
+                   cudaStream_t st) {
   using G = Geo<D, MC>;
   if (ps.n_subs[D] == 0) return;
   size_t smem = sizeof(double) * G::SMEM;
@@ -602,36 +671,81 @@ void launch_spread(const PlanSet& ps, const Workspace& ws, const double* v, int6
                                   (int)smem));
     attr = true;
   }
-  dim3 grid((unsigned)ps.n_subs[D], nrhs);
-  k_spread<D, MC><<<grid, kThreads, smem, st>>>(ps.subs[D], ps.wdev, ps.rows, ps.pix, v, ldv,
-                                                ws.blocks, ps.blocks_total);
+  k_spread<D, MC><<<(unsigned)ps.n_subs[D], kSpreadThreads, smem, st>>>(
+      ps.subs[D], ps.wdev, ps.rows, ps.pix, vt, nrhs, ws.blocks);
   NLD_CUDA(cudaGetLastError());
 }
 
 template <int D, int MC>
-void launch_gather(const PlanSet& ps, const Workspace& ws, int64_t N, int L, int nrhs,
+void launch_gather(const PlanSet& ps, const Workspace& ws, int64_t N, int nrhs,
                    cudaStream_t st) {
+  using G = Geo<D, MC>;
   if (ps.n_subs[D] == 0) return;
-  dim3 grid((unsigned)ps.n_subs[D], nrhs);
-  k_gather<D, MC><<<grid, kThreads, 0, st>>>(ps.subs[D], ps.cells, ps.wdev, ps.rows, ps.pix,
-                                             ws.grid_out, ps.grid_total, ws.wout, N, L);
+  size_t smem = sizeof(double) * G::BLK * std::min(nrhs, G::GRB);
+  static bool attr = false;
+  if (!attr) {
+    NLD_CUDA(cudaFuncSetAttribute(k_gather<D, MC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)(sizeof(double) * G::BLK * G::GRB)));
+    attr = true;
+  }
+  k_gather<D, MC><<<(unsigned)ps.n_subs[D], kThreads, smem, st>>>(
+      ps.subs[D], ps.cells, ps.wdev, ps.rows, ps.pix, ws.grid_out, ps.grid_total, ws.wout, N,
+      nrhs);
+  NLD_CUDA(cudaGetLastError());
+}
+
+template <int RPW>
+void launch_spread_mma(const PlanSet& ps, const Workspace& ws, const double* vt, int nrhs,
+                       cudaStream_t st) {
+  const int rpp = std::min(nrhs, mma::kSpWarps * RPW);
+  const size_t smem = sizeof(double) * mma::spread_smem(rpp);
+  static bool attr = false;
+  if (!attr) {
+    NLD_CUDA(cudaFuncSetAttribute(mma::k_spread_mma<RPW>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)(sizeof(double) * mma::spread_smem(mma::kSpWarps * RPW))));
+    attr = true;
+  }
+  mma::k_spread_mma<RPW><<<(unsigned)ps.n_subs[3], mma::kSpThreads, smem, st>>>(
+      ps.subs[3], ps.wdev, ps.rows, ps.pix, vt, nrhs, ws.blocks);
   NLD_CUDA(cudaGetLastError());
 }
 
 template <int MC>
-void spread_all(const PlanSet& ps, const Workspace& ws, const double* v, int64_t ldv,
-                int nrhs, cudaStream_t st) {
-  launch_spread<1, MC>(ps, ws, v, ldv, nrhs, st);
-  launch_spread<2, MC>(ps, ws, v, ldv, nrhs, st);
-  launch_spread<3, MC>(ps, ws, v, ldv, nrhs, st);
+void spread_all(const PlanSet& ps, const Workspace& ws, const double* vt, int nrhs,
+                cudaStream_t st) {
+  launch_spread<1, MC>(ps, ws, vt, nrhs, st);
+  launch_spread<2, MC>(ps, ws, vt, nrhs, st);
+  if (MC == 4 && use_mma() && ps.n_subs[3]) {
+    if (nrhs >= 16) launch_spread_mma<2>(ps, ws, vt, nrhs, st);
+    else launch_spread_mma<1>(ps, ws, vt, nrhs, st);
+  } else {
+    launch_spread<3, MC>(ps, ws, vt, nrhs, st);
+  }
+}
+
+void launch_gather_mma(const PlanSet& ps, const Workspace& ws, int64_t N, int nrhs,
+                       cudaStream_t st) {
+  const size_t smem = sizeof(double) * mma::kBlk * std::min(nrhs, mma::kGaRhs);
+  static bool attr = false;
+  if (!attr) {
+    NLD_CUDA(cudaFuncSetAttribute(mma::k_gather_mma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)(sizeof(double) * mma::kBlk * mma::kGaRhs)));
+    attr = true;
+  }
+  mma::k_gather_mma<<<(unsigned)ps.n_subs[3], mma::kGaThreads, smem, st>>>(
+      ps.subs[3], ps.cells, ps.wdev, ps.rows, ps.pix, ws.grid_out, ps.grid_total, ws.wout, N,
+      nrhs);
+  NLD_CUDA(cudaGetLastError());
 }
 
 template <int MC>
-void gather_all(const PlanSet& ps, const Workspace& ws, int64_t N, int L, int nrhs,
+void gather_all(const PlanSet& ps, const Workspace& ws, int64_t N, int nrhs,
                 cudaStream_t st) {
-  launch_gather<1, MC>(ps, ws, N, L, nrhs, st);
-  launch_gather<2, MC>(ps, ws, N, L, nrhs, st);
-  launch_gather<3, MC>(ps, ws, N, L, nrhs, st);
+  launch_gather<1, MC>(ps, ws, N, nrhs, st);
+  launch_gather<2, MC>(ps, ws, N, nrhs, st);
+  if (MC == 4 && use_mma() && ps.n_subs[3]) launch_gather_mma(ps, ws, N, nrhs, st);
+  else launch_gather<3, MC>(ps, ws, N, nrhs, st);
 }
 
 struct EvScope {
@@ -661,6 +775,7 @@ void ensure_workspace(nld_operator* op, const PlanSet& ps, int nrhs) {
   NLD_CUDA(cudaMalloc(&ws.cbuf0, sizeof(double2) * std::max<int64_t>(1, gt) * cap));
   NLD_CUDA(cudaMalloc(&ws.cbuf1, sizeof(double2) * std::max<int64_t>(1, gt) * cap));
   NLD_CUDA(cudaMalloc(&ws.wout, sizeof(double) * std::max<int64_t>(1, op->N * op->L) * cap));
+  NLD_CUDA(cudaMalloc(&ws.vt, sizeof(double) * std::max<int64_t>(1, op->N) * cap));
   NLD_CUDA(cudaMalloc(&ws.coef, sizeof(double) * 2 * cap));
   ws.nrhs_cap = cap;
   ws.grid_total = gt;
@@ -674,6 +789,7 @@ void free_workspace(Workspace& ws) {
   cudaFree(ws.cbuf0);
   cudaFree(ws.cbuf1);
   cudaFree(ws.wout);
+  cudaFree(ws.vt);
   cudaFree(ws.coef);
   ws = Workspace();
 }
@@ -691,11 +807,19 @@ void apply_op(nld_operator* op, int which, int kind, const double* v, double* ou
   ev.mark();
   int launches = 0;
   for (int g = 1; g <= kMaxDim; ++g) launches += ps.n_subs[g] ? 2 : 0;  // spread + gather
+  // 0. pixel-major copy of the rhs for the node gathers (nrhs > 1)
+  const double* vt = v;
+  if (nrhs > 1 || ld != N) {
+    k_transpose_in<<<grid_blocks(N, 256, 148 * 16), 256, 0, st>>>(v, ld, N, nrhs, ws.vt);
+    NLD_CUDA(cudaGetLastError());
+    vt = ws.vt;
+    ++launches;
+  }
   // 1. spread (block path)
   switch (m) {
-    case 3: spread_all<3>(ps, ws, v, ld, nrhs, st); break;
-    case 4: spread_all<4>(ps, ws, v, ld, nrhs, st); break;
-    case 5: spread_all<5>(ps, ws, v, ld, nrhs, st); break;
+    case 3: spread_all<3>(ps, ws, vt, nrhs, st); break;
+    case 4: spread_all<4>(ps, ws, vt, nrhs, st); break;
+    case 5: spread_all<5>(ps, ws, vt, nrhs, st); break;
     default: break;
   }
   ev.mark();
@@ -703,9 +827,9 @@ void apply_op(nld_operator* op, int which, int kind, const double* v, double* ou
   {
     int64_t maxbox = 1;
     for (const auto& w : ps.wdev_h) maxbox = std::max(maxbox, w.box_size);
-    dim3 grid(grid_blocks(maxbox, 128, 512), L, nrhs);
-    k_assemble<<<grid, 128, 0, st>>>(ps.wdev, L, ps.cellmap, ps.cells, ws.blocks,
-                                     ps.blocks_total, ws.grid_in, ps.grid_total);
+    dim3 grid(grid_blocks(maxbox * nrhs, 128, 2048), L);
+    k_assemble<<<grid, 128, 0, st>>>(ps.wdev, L, ps.cellmap, ps.cells, ws.blocks, nrhs,
+                                     ws.grid_in, ps.grid_total);
     NLD_CUDA(cudaGetLastError());
   }
   // generic windows + edge nodes (atomics on top of the assembled boxes)
@@ -743,29 +867,29 @@ void apply_op(nld_operator* op, int which, int kind, const double* v, double* ou
   ev.mark();
   // 4. gather
   switch (m) {
-    case 3: gather_all<3>(ps, ws, N, L, nrhs, st); break;
-    case 4: gather_all<4>(ps, ws, N, L, nrhs, st); break;
-    case 5: gather_all<5>(ps, ws, N, L, nrhs, st); break;
+    case 3: gather_all<3>(ps, ws, N, nrhs, st); break;
+    case 4: gather_all<4>(ps, ws, N, nrhs, st); break;
+    case 5: gather_all<5>(ps, ws, N, nrhs, st); break;
     default: break;
   }
   for (int w = 0; w < L; ++w) {
     if (ps.wdev_h[w].fast) continue;
     dim3 grid(grid_blocks(N, 256), nrhs);
-    k_gather_generic<<<grid, 256, 0, st>>>(ps.wdev, w, L, ps.rows, ps.pix, ps.key,
+    k_gather_generic<<<grid, 256, 0, st>>>(ps.wdev, w, nrhs, ps.rows, ps.pix, ps.key,
                                            ws.grid_out, ps.grid_total, ws.wout, N);
     NLD_CUDA(cudaGetLastError());
   }
   if (ps.n_edges) {
     dim3 grid(grid_blocks(ps.n_edges, 128), nrhs);
     k_gather_edges<<<grid, 128, 0, st>>>(ps.edges, ps.n_edges, ps.wdev, ws.grid_out,
-                                         ps.grid_total, ws.wout, N, L);
+                                         ps.grid_total, ws.wout, N, nrhs);
     NLD_CUDA(cudaGetLastError());
   }
   ev.mark();
   // 5. epilogue
   {
-    dim3 grid(grid_blocks(N, 256, 148 * 16), nrhs);
-    k_epilogue<<<grid, 256, 0, st>>>(kind, L, N, v, ld, ws.wout, 0, out, ld, eta, coef_dev);
+    k_epilogue<<<grid_blocks(N, 256, 148 * 16), 256, 0, st>>>(kind, L, N, nrhs, v, ld, ws.wout,
+                                                               0, out, ld, eta, coef_dev);
     NLD_CUDA(cudaGetLastError());
   }
   ev.mark();
@@ -806,8 +930,8 @@ void dense_apply(nld_operator* op, int which, int kind, const double* v, double*
   k_dense_apply<<<grid, 128, 0, st>>>(op->feats, op->N, op->D, widx, woff, op->L, inv, v, ld,
                                       gam);
   NLD_CUDA(cudaGetLastError());
-  dim3 g2(grid_blocks(op->N, 256), nrhs);
-  k_epilogue<<<g2, 256, 0, st>>>(kind, op->L, op->N, v, ld, gam, 1, out, ld, eta, coef_dev);
+  k_epilogue<<<grid_blocks(op->N, 256), 256, 0, st>>>(kind, op->L, op->N, nrhs, v, ld, gam, 1,
+                                                       out, ld, eta, coef_dev);
   NLD_CUDA(cudaGetLastError());
   cudaFreeAsync(gam, st);
   cudaFreeAsync(widx, st);

@@ -133,12 +133,13 @@ struct PlanSet {
 
 struct Workspace {
   int nrhs_cap = 0;
-  double* blocks = nullptr;      // [nrhs][blocks_total]
+  double* blocks = nullptr;      // [blocks_total][nrhs]
   double* grid_in = nullptr;     // [nrhs][grid_total]
   double* grid_out = nullptr;
   double2* cbuf0 = nullptr;
   double2* cbuf1 = nullptr;
-  double* wout = nullptr;        // [nrhs][L][N] per-window gathers
+  double* wout = nullptr;        // [L][N][nrhs] per-window gathers
+  double* vt = nullptr;          // [N][nrhs] pixel-major rhs
   double* coef = nullptr;        // [nrhs][2]
   int64_t grid_total = 0, blocks_total = 0;
 };

@@ -1,0 +1,309 @@
+// fp64 tensor-core (DMMA, mma.sync.m8n8k4.f64) spread and gather for 3-D
+// windows with cutoff m = 4 (an 8x8x8 stencil block) -- the BASELINE shape.
+//
+// Measured on B200: DMMA m8n8k4 sustains 37.06 TFLOP/s (the full fp64 rate)
+// against 34 TFLOP/s for a DFMA loop, and it takes its operands from
+// registers, which removes the shared-memory broadcast traffic that capped
+// the CUDA-core kernels at ~50% of the fp64 pipe.
+//
+// Fragment layouts (PTX ISA, mma.m8n8k4 .f64), g = lane >> 2, t = lane & 3:
+//   A (8x4 row)  : A[g][t]          B (4x8 col) : B[t][g]
+//   C/D (8x8)    : C[g][2t + i], i = 0, 1
+//
+// spread: block[a][(b,c)] += sum_j (v_j A_j[a]) (B_j[b] C_j[c])
+//         M = 8 (a), N = 64 (b,c) as 8 n-tiles (one per b), K = nodes.
+// gather: T[(a,b)][j] = sum_c G[a][b][c] C_j[c]   (M = 64 as 8 m-tiles, one
+//         per a; K = 8; N = 8 nodes), then y_j = sum_a A_j[a] B_j[b] T[a,b][j]
+//         reduced over b across the 8 lanes of a column.
+#pragma once
+
+#include "nld_internal.cuh"
+
+namespace nld {
+namespace mma {
+
+__device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_addr(dst)), "l"(src));
+}
+
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_addr(dst)), "l"(src));
+}
+
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+constexpr int kS = 8;             // stencil width 2m
+constexpr int kRow = 24;          // global row: [A(8)][B(8)][C(8)]
+constexpr int kSRow = 26;         // smem row stride (16B aligned, bank skew)
+constexpr int kBlk = 512;
+constexpr int kSpWarps = 8;
+constexpr int kSpThreads = 256;
+constexpr int kSpChunk = 128;     // nodes per pipeline stage
+constexpr int kGaWarps = 4;
+constexpr int kGaThreads = 128;
+constexpr int kGaRhs = 16;        // rhs whose G blocks sit in smem at once
+
+// shared-memory doubles of the spread for a given rhs-per-pass count
+__host__ __device__ constexpr int spread_smem(int rpp) {
+  return 2 * (kSpChunk * kSRow + kSpChunk * rpp);
+}
+
+// ---- spread ---------------------------------------------------------------
+// RPW rhs per warp; rpp = rhs per pass = 8 * RPW (or nrhs if smaller, then
+// several warps share an rhs and split the k-steps).
+template <int RPW>
+__global__ void __launch_bounds__(kSpThreads)
+k_spread_mma(const SubDev* __restrict__ subs, const WinDev* __restrict__ wins,
+             const double* __restrict__ rows, const int32_t* __restrict__ pix,
+             const double* __restrict__ vt, int nrhs, double* __restrict__ blocks) {
+  extern __shared__ __align__(16) double sm[];
+  const int rpp_max = kSpWarps * RPW;
+  const int rpp = nrhs < rpp_max ? nrhs : rpp_max;
+  double* srow[2] = {sm, sm + kSpChunk * kSRow};
+  double* sv[2] = {sm + 2 * kSpChunk * kSRow, sm + 2 * kSpChunk * kSRow + kSpChunk * rpp};
+  const SubDev sd = subs[blockIdx.x];
+  const WinDev wd = wins[sd.win];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int slots = (rpp + RPW - 1) / RPW;       // warps-groups with distinct rhs
+  const int wpr = kSpWarps / slots;              // warps sharing an rhs slot
+  const int slot = warp / wpr;
+  const int slice = warp - slot * wpr;
+  const bool busy = slot < slots;
+  const int64_t local = sd.start - wd.node_off;
+  const double* __restrict__ rw = rows + wd.row_off + local * kRow;
+  const int32_t* __restrict__ pw = pix + sd.start;
+  const int nchunk = (sd.count + kSpChunk - 1) / kSpChunk;
+
+  for (int rg = 0; rg < nrhs; rg += rpp) {
+    const int rn = min(rpp, nrhs - rg);
+    double acc[RPW][8][2];
+#pragma unroll
+    for (int q = 0; q < RPW; ++q)
+#pragma unroll
+      for (int n = 0; n < 8; ++n) acc[q][n][0] = acc[q][n][1] = 0.0;
+
+    auto stage = [&](int ck, int buf) {
+      const int c0 = ck * kSpChunk;
+      const int cn = min(kSpChunk, sd.count - c0);
+      // rows: 6 granules of 16 B per dimension pair... 12 granules per row
+      for (int e = tid; e < cn * 12; e += kSpThreads) {
+        const int pt = e / 12, gi = e - pt * 12;
+        const int dim = gi >> 2, w4 = gi & 3;
+        // smem order [C][B][A]: dim 2 -> 0, dim 1 -> 8, dim 0 -> 16
+        cp_async16(srow[buf] + pt * kSRow + (2 - dim) * kS + 2 * w4,
+                   rw + (int64_t)(c0 + pt) * kRow + dim * kS + 2 * w4);
+      }
+      for (int e = tid; e < cn * rn; e += kSpThreads) {
+        const int pt = e / rn, q = e - pt * rn;
+        cp_async8(sv[buf] + pt * rpp + q, vt + (int64_t)pw[c0 + pt] * nrhs + rg + q);
+      }
+      cp_commit();
+    };
+
+    stage(0, 0);
+    for (int ck = 0; ck < nchunk; ++ck) {
+      const int buf = ck & 1;
+      if (ck + 1 < nchunk) {
+        stage(ck + 1, buf ^ 1);
+        cp_wait<1>();
+      } else {
+        cp_wait<0>();
+      }
+      __syncthreads();
+      const int cn = min(kSpChunk, sd.count - ck * kSpChunk);
+      if (busy) {
+        const double* R = srow[buf];
+        const double* V = sv[buf];
+        const int nks = (cn + 3) >> 2;
+        for (int ks = slice; ks < nks; ks += wpr) {
+          const int j = ks * 4 + t;
+          const bool ok = j < cn;
+          const double* row = R + j * kSRow;
+          double bw[8];
+          double cw = 0.0, aw = 0.0;
+          if (ok) {
+#pragma unroll
+            for (int b = 0; b < 8; b += 2) {
+              const double2 x = *reinterpret_cast<const double2*>(row + kS + b);
+              bw[b] = x.x;
+              bw[b + 1] = x.y;
+            }
+            cw = row[g];
+            aw = row[2 * kS + g];
+          } else {
+#pragma unroll
+            for (int b = 0; b < 8; ++b) bw[b] = 0.0;
+          }
+          double af[RPW];
+#pragma unroll
+          for (int q = 0; q < RPW; ++q) {
+            const int qq = slot * RPW + q;
+            af[q] = (ok && qq < rn) ? V[j * rpp + qq] * aw : 0.0;
+          }
+#pragma unroll
+          for (int n = 0; n < 8; ++n) {
+            const double bf = bw[n] * cw;
+#pragma unroll
+            for (int q = 0; q < RPW; ++q) dmma(acc[q][n], af[q], bf);
+          }
+        }
+      }
+      __syncthreads();
+    }
+    // block element (a = g, b = n, c = 2t + i)
+    if (wpr == 1) {
+      if (busy) {
+#pragma unroll
+        for (int q = 0; q < RPW; ++q) {
+          const int qq = slot * RPW + q;
+          if (qq >= rn) continue;
+#pragma unroll
+          for (int n = 0; n < 8; ++n)
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+              blocks[(sd.block + (g * 8 + n) * 8 + 2 * t + i) * nrhs + rg + qq] = acc[q][n][i];
+        }
+      }
+    } else {
+      // RPW == 1 here (rpp < 8): reduce the wpr warps of each slot in smem
+      double* red = sm;   // kSpWarps * 512 doubles fit in the staging area
+      if (busy) {
+#pragma unroll
+        for (int n = 0; n < 8; ++n)
+#pragma unroll
+          for (int i = 0; i < 2; ++i) red[warp * kBlk + (g * 8 + n) * 8 + 2 * t + i] = acc[0][n][i];
+      }
+      __syncthreads();
+      for (int e = tid; e < slots * kBlk; e += kSpThreads) {
+        const int s = e / kBlk, k = e - s * kBlk;
+        if (s >= rn) continue;
+        double sum = 0.0;
+        for (int w = 0; w < wpr; ++w) sum += red[(s * wpr + w) * kBlk + k];
+        blocks[(sd.block + k) * nrhs + rg + s] = sum;
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// ---- gather ---------------------------------------------------------------
+__global__ void __launch_bounds__(kGaThreads)
+k_gather_mma(const SubDev* __restrict__ subs, const CellDev* __restrict__ cells,
+             const WinDev* __restrict__ wins, const double* __restrict__ rows,
+             const int32_t* __restrict__ pix, const double* __restrict__ grid,
+             int64_t grid_ld, double* __restrict__ wout, int64_t N, int nrhs) {
+  extern __shared__ __align__(16) double gb[];   // [kGaRhs][512]
+  const SubDev sd = subs[blockIdx.x];
+  const CellDev cd = cells[sd.cell];
+  const WinDev wd = wins[sd.win];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int64_t local = sd.start - wd.node_off;
+  const double* __restrict__ rw = rows + wd.row_off + local * kRow;
+  double* __restrict__ out = wout + (int64_t)sd.win * N * nrhs;
+  const int ntile = (sd.count + 7) >> 3;
+  for (int rg = 0; rg < nrhs; rg += kGaRhs) {
+    const int rn = min(kGaRhs, nrhs - rg);
+    __syncthreads();
+    for (int e = tid; e < rn * kBlk; e += kGaThreads) {
+      const int q = e >> 9, k = e & (kBlk - 1);
+      int p0 = cd.cc[0] + (k >> 6), p1 = cd.cc[1] + ((k >> 3) & 7), p2 = cd.cc[2] + (k & 7);
+      if (p0 >= wd.box_w[0]) p0 -= wd.box_w[0];
+      if (p1 >= wd.box_w[1]) p1 -= wd.box_w[1];
+      if (p2 >= wd.box_w[2]) p2 -= wd.box_w[2];
+      const int b = (k >> 3) & 7, c = k & 7;
+      gb[q * kBlk + (k & ~7) + (c ^ (((b >> 1) & 1) << 2))] =
+          grid[(int64_t)(rg + q) * grid_ld + wd.grid_off +
+               ((int64_t)p0 * wd.box_w[1] + p1) * wd.box_w[2] + p2];
+    }
+    __syncthreads();
+    for (int nt = warp; nt < ntile; nt += kGaWarps) {
+      const int j0 = nt * 8;
+      // B fragments: C weights of node j0 + g, c = 4 ks + t
+      const int jn = j0 + g;
+      double cf[2] = {0.0, 0.0};
+      if (jn < sd.count) {
+        cf[0] = __ldg(rw + (int64_t)jn * kRow + 2 * kS + t);
+        cf[1] = __ldg(rw + (int64_t)jn * kRow + 2 * kS + 4 + t);
+      }
+      // step-2 weights of nodes j0 + 2t + i: A[0..7], B[g]
+      double aw[2][8], bw[2];
+      int jp[2];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        jp[i] = j0 + 2 * t + i;
+        if (jp[i] < sd.count) {
+          const double2* src = reinterpret_cast<const double2*>(rw + (int64_t)jp[i] * kRow);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const double2 x = __ldg(src + k);
+            aw[i][2 * k] = x.x;
+            aw[i][2 * k + 1] = x.y;
+          }
+          bw[i] = __ldg(rw + (int64_t)jp[i] * kRow + kS + g);
+        } else {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) aw[i][k] = 0.0;
+          bw[i] = 0.0;
+        }
+      }
+      int pj[2] = {0, 0};
+      if (g == 0) {
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+          if (jp[i] < sd.count) pj[i] = pix[sd.start + jp[i]];
+      }
+      // swizzled G fragment offsets: (a*8 + g)*8 + (c ^ swz(g)), c = 4ks + t
+      const int sw = ((g >> 1) & 1) << 2;
+      const int o0 = g * 8 + (t ^ sw), o1 = g * 8 + ((4 + t) ^ sw);
+      for (int q = 0; q < rn; ++q) {
+        const double* G = gb + q * kBlk;
+        double T[8][2];
+#pragma unroll
+        for (int a = 0; a < 8; ++a) {
+          T[a][0] = T[a][1] = 0.0;
+          dmma(T[a], G[a * 64 + o0], cf[0]);
+        }
+#pragma unroll
+        for (int a = 0; a < 8; ++a) dmma(T[a], G[a * 64 + o1], cf[1]);
+        double p[2] = {0.0, 0.0};
+#pragma unroll
+        for (int a = 0; a < 8; ++a) {
+          p[0] = fma(aw[0][a], T[a][0], p[0]);
+          p[1] = fma(aw[1][a], T[a][1], p[1]);
+        }
+        p[0] *= bw[0];
+        p[1] *= bw[1];
+#pragma unroll
+        for (int off = 4; off < 32; off <<= 1) {
+          p[0] += __shfl_xor_sync(0xffffffffu, p[0], off);
+          p[1] += __shfl_xor_sync(0xffffffffu, p[1], off);
+        }
+        if (g == 0) {
+#pragma unroll
+          for (int i = 0; i < 2; ++i)
+            if (jp[i] < sd.count) out[(int64_t)pj[i] * nrhs + rg + q] = p[i];
+        }
+      }
+    }
+  }
+}
+
+}  // namespace mma
+}  // namespace nld

@@ -22,7 +22,63 @@ __global__ void __launch_bounds__(256) k_dfma(double* out, int64_t iters, double
   if (s == 12345.678) out[0] = s;  // keep the chains alive
 }
 
+constexpr int kMmaChains = 8;
+
+// fp64 tensor-core path (DMMA): mma.sync m8n8k4, 256 FMA per warp-instruction
+__global__ void __launch_bounds__(256) k_dmma(double* out, int64_t iters) {
+  double a = 1.0 + threadIdx.x * 1e-9, b = 0.999999;
+  double c[kMmaChains][2];
+#pragma unroll
+  for (int k = 0; k < kMmaChains; ++k) c[k][0] = c[k][1] = k * 1e-3;
+  for (int64_t i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < kMmaChains; ++k)
+      asm volatile(
+          "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+          : "+d"(c[k][0]), "+d"(c[k][1])
+          : "d"(a), "d"(b));
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int k = 0; k < kMmaChains; ++k) s += c[k][0] + c[k][1];
+  if (s == 12345.678) out[0] = s;
+}
+
 }  // namespace
+
+extern "C" NLD_API int nld_probe_dmma(int64_t iters, int32_t blocks, double* tflops,
+                                      double* ms, void* stream) {
+  try {
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    int dev = 0;
+    NLD_CUDA(cudaGetDevice(&dev));
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (blocks <= 0) blocks = sms * 8;
+    double* out = nullptr;
+    NLD_CUDA(cudaMallocAsync(&out, sizeof(double), st));
+    cudaEvent_t e0, e1;
+    NLD_CUDA(cudaEventCreate(&e0));
+    NLD_CUDA(cudaEventCreate(&e1));
+    k_dmma<<<blocks, 256, 0, st>>>(out, iters / 8);
+    NLD_CUDA(cudaEventRecord(e0, st));
+    k_dmma<<<blocks, 256, 0, st>>>(out, iters);
+    NLD_CUDA(cudaEventRecord(e1, st));
+    NLD_CUDA(cudaEventSynchronize(e1));
+    float t = 0.f;
+    cudaEventElapsedTime(&t, e0, e1);
+    // per warp-instruction: 8x8x4 FMA = 512 flop
+    const double flops = 512.0 * kMmaChains * (double)iters * blocks * (256 / 32);
+    *ms = t;
+    *tflops = flops / (t * 1e-3) / 1e12;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFreeAsync(out, st);
+    return NLD_OK;
+  } catch (const nld::Error& e) {
+    return nld::fail(e.code, e.msg);
+  }
+}
 
 extern "C" NLD_API int nld_probe_fp64(int64_t iters, int32_t blocks, double* tflops,
                                       double* ms, void* stream) {
