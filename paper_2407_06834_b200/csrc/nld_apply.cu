@@ -213,16 +213,20 @@ k_spread(const SubDev* __restrict__ subs, const WinDev* __restrict__ wins,
 // ---- assemble: grid point <- sum of the blocks of the cells covering it -----
 
 __global__ void k_assemble(const WinDev* __restrict__ wins, int L,
-                           const int32_t* __restrict__ cellmap,
-                           const CellDev* __restrict__ cells,
+                           const int2* __restrict__ cellinfo,
                            const double* __restrict__ blocks, int nrhs,
                            double* __restrict__ grid, int64_t grid_ld) {
   // thread = (grid point, rhs) with rhs fastest: the cell lookups are shared
-  // and the block reads ([block + e][nrhs]) are contiguous across the rhs.
+  // across the rhs and the block reads ([block + e][nrhs]) are contiguous.
+  // Cells covering the point are visited in a fixed order (deterministic).
   const int w = blockIdx.y;
   const WinDev wd = wins[w];
   const int S = wd.S;
+  const int d = wd.d;
   const int64_t total = wd.box_size * nrhs;
+  const int2* __restrict__ ci = cellinfo + wd.cellmap_off;
+  const int on0 = d == 3 ? S : 1, on1 = d >= 2 ? S : 1;
+  const int blk = on0 * on1 * S;
   for (int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; id < total;
        id += (int64_t)gridDim.x * blockDim.x) {
     const int r = (int)(id % nrhs);
@@ -232,43 +236,54 @@ __global__ void k_assemble(const WinDev* __restrict__ wins, int L,
       g[e] = 0.0;
       continue;
     }
-    int t[3] = {0, 0, 0};
+    // point coordinates mapped onto (t0, t1, t2) with unused leading dims 0
+    int t[3] = {0, 0, 0}, bw[3] = {1, 1, 1};
     int64_t rem = e;
-    for (int s = wd.d - 1; s >= 0; --s) {
-      t[s] = (int)(rem % wd.box_w[s]);
-      rem /= wd.box_w[s];
+    for (int s = 2; s >= 3 - d; --s) {
+      bw[s] = wd.box_w[s - (3 - d)];
+      t[s] = (int)(rem % bw[s]);
+      rem /= bw[s];
     }
     double sum = 0.0;
-    const int o0n = wd.d == 3 ? S : 1;
-    const int o1n = wd.d >= 2 ? S : 1;
-    for (int o0 = 0; o0 < o0n; ++o0)
-      for (int o1 = 0; o1 < o1n; ++o1)
-        for (int o2 = 0; o2 < S; ++o2) {
-          int off[3];
-          if (wd.d == 3) { off[0] = o0; off[1] = o1; off[2] = o2; }
-          else if (wd.d == 2) { off[0] = o1; off[1] = o2; off[2] = 0; }
-          else { off[0] = o2; off[1] = 0; off[2] = 0; }
-          int c[3];
-          bool ok = true;
-          for (int s = 0; s < wd.d; ++s) {
-            int cc = t[s] - off[s];
-            if (cc < 0) {
-              if (wd.wrap) cc += wd.box_w[s];
-              else ok = false;
-            }
-            c[s] = cc;
-          }
-          if (!ok) continue;
-          int64_t key = 0;
-          for (int s = 0; s < wd.d; ++s) key = key * wd.box_w[s] + c[s];
-          const int cell = cellmap[wd.cellmap_off + key];
-          if (cell < 0) continue;
-          const CellDev cd = cells[cell];
-          int64_t inner = 0;
-          for (int s = 0; s < wd.d; ++s) inner = inner * S + off[s];
-          for (int q = 0; q < cd.nsub; ++q)
-            sum += blocks[(cd.block0 + (int64_t)q * cd.blk + inner) * nrhs + r];
+    for (int o0 = 0; o0 < on0; ++o0) {
+      int c0 = t[0] - o0;
+      if (c0 < 0) {
+        if (!wd.wrap) break;
+        c0 += bw[0];
+      }
+      for (int o1 = 0; o1 < on1; ++o1) {
+        int c1 = t[1] - o1;
+        if (c1 < 0) {
+          if (!wd.wrap) break;
+          c1 += bw[1];
         }
+        const int64_t rowkey = ((int64_t)c0 * bw[1] + c1) * bw[2];
+        const int inner01 = (o0 * on1 + o1) * S;
+        if (S == 8 && !wd.wrap && t[2] >= 7) {
+          // common case: all 8 candidates in range; batch the lookups
+          int2 info[8];
+#pragma unroll
+          for (int o2 = 0; o2 < 8; ++o2) info[o2] = ci[rowkey + t[2] - o2];
+#pragma unroll
+          for (int o2 = 0; o2 < 8; ++o2) {
+            const int2 c = info[o2];
+            for (int q = 0; q < c.y; ++q)
+              sum += blocks[((int64_t)c.x + (int64_t)q * blk + inner01 + o2) * nrhs + r];
+          }
+        } else {
+          for (int o2 = 0; o2 < S; ++o2) {
+            int c2 = t[2] - o2;
+            if (c2 < 0) {
+              if (!wd.wrap) break;
+              c2 += bw[2];
+            }
+            const int2 c = ci[rowkey + c2];
+            for (int q = 0; q < c.y; ++q)
+              sum += blocks[((int64_t)c.x + (int64_t)q * blk + inner01 + o2) * nrhs + r];
+          }
+        }
+      }
+    }
     g[e] = sum;
   }
 }
@@ -554,24 +569,40 @@ k_gather(const SubDev* __restrict__ subs, const CellDev* __restrict__ cells,
 // ---- epilogue: window sum + diagonal/degree terms (kernel.py:86-93,
 //      linops.py:43-50) ---------------------------------------------------
 
-__global__ void k_epilogue(int kind, int L, int64_t N, int nrhs,
-                           const double* __restrict__ v, int64_t ldv,
-                           const double* __restrict__ wsum, int direct,
-                           double* __restrict__ out, int64_t ldo,
-                           const double* __restrict__ eta,
-                           const double* __restrict__ coef) {
-  // wsum: per-window gathers [L][N][nrhs] (or Gamma v [nrhs][N] if direct)
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const double et = eta ? eta[i] : 0.0;
-    for (int r = 0; r < nrhs; ++r) {
+constexpr int kTileP = 128;    // pixels per epilogue / transpose tile
+
+// Epilogue (kernel.py:86-93, linops.py:43-50): per pixel tile, sum the
+// per-window gathers [L][N][nrhs] (coalesced, rhs fastest), then switch to an
+// rhs-major layout in shared memory so v, eta and the output [nrhs][ld] are
+// read and written coalesced.
+__global__ void __launch_bounds__(256)
+k_epilogue(int kind, int L, int64_t N, int nrhs, const double* __restrict__ v, int64_t ldv,
+           const double* __restrict__ wsum, int direct, double* __restrict__ out,
+           int64_t ldo, const double* __restrict__ eta, const double* __restrict__ coef) {
+  extern __shared__ double tile[];   // [kTileP][nrhs + 1]
+  const int ld_t = nrhs + 1;
+  const int64_t ntiles = (N + kTileP - 1) / kTileP;
+  for (int64_t tl = blockIdx.x; tl < ntiles; tl += gridDim.x) {
+    const int64_t i0 = tl * kTileP;
+    const int np = (int)min((int64_t)kTileP, N - i0);
+    if (!direct) {
+      for (int e = threadIdx.x; e < np * nrhs; e += blockDim.x) {
+        const int p = e / nrhs, r = e - p * nrhs;
+        double s = 0.0;
+        for (int w = 0; w < L; ++w) s += wsum[((int64_t)w * N + i0) * nrhs + e];
+        tile[p * ld_t + r] = s;
+      }
+      __syncthreads();
+    }
+    for (int e = threadIdx.x; e < np * nrhs; e += blockDim.x) {
+      const int r = e / np, p = e - r * np;
+      const int64_t i = i0 + p;
       const double x = v[r * ldv + i];
       double gam;
       if (direct) {
         gam = wsum[r * N + i];
       } else {
-        double s = 0.0;
-        for (int w = 0; w < L; ++w) s += wsum[((int64_t)w * N + i) * nrhs + r];
+        const double s = tile[p * ld_t + r];
         if (kind == NLD_APPLY_WINDOW_SUM) {
           out[r * ldo + i] = s;
           continue;
@@ -579,20 +610,36 @@ __global__ void k_epilogue(int kind, int L, int64_t N, int nrhs,
         gam = (s - (double)L * x) / (double)L;
       }
       double y;
-      if (kind == NLD_APPLY_SYSTEM) y = coef[2 * r] * x + coef[2 * r + 1] * (et * x - gam);
-      else if (kind == NLD_APPLY_LAPLACIAN) y = et * x - gam;
+      if (kind == NLD_APPLY_SYSTEM) y = coef[2 * r] * x + coef[2 * r + 1] * (eta[i] * x - gam);
+      else if (kind == NLD_APPLY_LAPLACIAN) y = eta[i] * x - gam;
       else y = gam;
       out[r * ldo + i] = y;
     }
+    __syncthreads();
   }
 }
 
 // v [nrhs][ld] -> vt [N][nrhs] (pixel-major, for the spread's node gathers)
-__global__ void k_transpose_in(const double* __restrict__ v, int64_t ldv, int64_t N,
-                               int nrhs, double* __restrict__ vt) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N;
-       i += (int64_t)gridDim.x * blockDim.x)
-    for (int r = 0; r < nrhs; ++r) vt[i * nrhs + r] = v[r * ldv + i];
+__global__ void __launch_bounds__(256)
+k_transpose_in(const double* __restrict__ v, int64_t ldv, int64_t N, int nrhs,
+               double* __restrict__ vt) {
+  extern __shared__ double tile[];   // [kTileP][nrhs + 1]
+  const int ld_t = nrhs + 1;
+  const int64_t ntiles = (N + kTileP - 1) / kTileP;
+  for (int64_t tl = blockIdx.x; tl < ntiles; tl += gridDim.x) {
+    const int64_t i0 = tl * kTileP;
+    const int np = (int)min((int64_t)kTileP, N - i0);
+    for (int e = threadIdx.x; e < np * nrhs; e += blockDim.x) {
+      const int r = e / np, p = e - r * np;
+      tile[p * ld_t + r] = v[r * ldv + i0 + p];
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < np * nrhs; e += blockDim.x) {
+      const int p = e / nrhs, r = e - p * nrhs;
+      vt[i0 * nrhs + e] = tile[p * ld_t + r];
+    }
+    __syncthreads();
+  }
 }
 
 // ---- dense exact mode (kernel.py:97-114, _kernels.py:205-227) -------------
@@ -810,7 +857,8 @@ void apply_op(nld_operator* op, int which, int kind, const double* v, double* ou
   // 0. pixel-major copy of the rhs for the node gathers (nrhs > 1)
   const double* vt = v;
   if (nrhs > 1 || ld != N) {
-    k_transpose_in<<<grid_blocks(N, 256, 148 * 16), 256, 0, st>>>(v, ld, N, nrhs, ws.vt);
+    k_transpose_in<<<grid_blocks(N, kTileP, 148 * 16), 256,
+                     sizeof(double) * kTileP * (nrhs + 1), st>>>(v, ld, N, nrhs, ws.vt);
     NLD_CUDA(cudaGetLastError());
     vt = ws.vt;
     ++launches;
@@ -828,8 +876,8 @@ void apply_op(nld_operator* op, int which, int kind, const double* v, double* ou
     int64_t maxbox = 1;
     for (const auto& w : ps.wdev_h) maxbox = std::max(maxbox, w.box_size);
     dim3 grid(grid_blocks(maxbox * nrhs, 128, 2048), L);
-    k_assemble<<<grid, 128, 0, st>>>(ps.wdev, L, ps.cellmap, ps.cells, ws.blocks, nrhs,
-                                     ws.grid_in, ps.grid_total);
+    k_assemble<<<grid, 128, 0, st>>>(ps.wdev, L, ps.cellinfo, ws.blocks, nrhs, ws.grid_in,
+                                     ps.grid_total);
     NLD_CUDA(cudaGetLastError());
   }
   // generic windows + edge nodes (atomics on top of the assembled boxes)
@@ -888,8 +936,9 @@ void apply_op(nld_operator* op, int which, int kind, const double* v, double* ou
   ev.mark();
   // 5. epilogue
   {
-    k_epilogue<<<grid_blocks(N, 256, 148 * 16), 256, 0, st>>>(kind, L, N, nrhs, v, ld, ws.wout,
-                                                               0, out, ld, eta, coef_dev);
+    k_epilogue<<<grid_blocks(N, kTileP, 148 * 16), 256,
+                 sizeof(double) * kTileP * (nrhs + 1), st>>>(kind, L, N, nrhs, v, ld, ws.wout,
+                                                             0, out, ld, eta, coef_dev);
     NLD_CUDA(cudaGetLastError());
   }
   ev.mark();
@@ -930,8 +979,8 @@ void dense_apply(nld_operator* op, int which, int kind, const double* v, double*
   k_dense_apply<<<grid, 128, 0, st>>>(op->feats, op->N, op->D, widx, woff, op->L, inv, v, ld,
                                       gam);
   NLD_CUDA(cudaGetLastError());
-  k_epilogue<<<grid_blocks(op->N, 256), 256, 0, st>>>(kind, op->L, op->N, nrhs, v, ld, gam, 1,
-                                                       out, ld, eta, coef_dev);
+  k_epilogue<<<grid_blocks(op->N, kTileP), 256, sizeof(double) * kTileP * (nrhs + 1), st>>>(
+      kind, op->L, op->N, nrhs, v, ld, gam, 1, out, ld, eta, coef_dev);
   NLD_CUDA(cudaGetLastError());
   cudaFreeAsync(gam, st);
   cudaFreeAsync(widx, st);

@@ -25,7 +25,7 @@
 
 namespace nld {
 
-constexpr int kSubMax = 512;   // nodes per subproblem
+constexpr int kSubMax = 2048;  // nodes per subproblem
 constexpr int kMaxDim = 3;
 
 struct Status {
@@ -117,6 +117,7 @@ struct PlanSet {
   int32_t* pix = nullptr;
   int32_t* key = nullptr;
   int32_t* cellmap = nullptr;
+  int2* cellinfo = nullptr;      // per box key: (block offset / blk, nsub)
   double2* K = nullptr;
   CellDev* cells = nullptr;
   int64_t n_cells = 0;

@@ -49,13 +49,13 @@ __device__ __forceinline__ void cp_wait() {
 
 constexpr int kS = 8;             // stencil width 2m
 constexpr int kRow = 24;          // global row: [A(8)][B(8)][C(8)]
-constexpr int kSRow = 26;         // smem row stride (16B aligned, bank skew)
+constexpr int kSRow = 28;         // smem row stride: 16B aligned, conflict-free row[g]
 constexpr int kBlk = 512;
 constexpr int kSpWarps = 8;
 constexpr int kSpThreads = 256;
 constexpr int kSpChunk = 128;     // nodes per pipeline stage
-constexpr int kGaWarps = 4;
-constexpr int kGaThreads = 128;
+constexpr int kGaWarps = 8;
+constexpr int kGaThreads = 256;
 constexpr int kGaRhs = 16;        // rhs whose G blocks sit in smem at once
 
 // shared-memory doubles of the spread for a given rhs-per-pass count
@@ -67,7 +67,7 @@ __host__ __device__ constexpr int spread_smem(int rpp) {
 // RPW rhs per warp; rpp = rhs per pass = 8 * RPW (or nrhs if smaller, then
 // several warps share an rhs and split the k-steps).
 template <int RPW>
-__global__ void __launch_bounds__(kSpThreads)
+__global__ void __launch_bounds__(kSpThreads, 2)
 k_spread_mma(const SubDev* __restrict__ subs, const WinDev* __restrict__ wins,
              const double* __restrict__ rows, const int32_t* __restrict__ pix,
              const double* __restrict__ vt, int nrhs, double* __restrict__ blocks) {
@@ -131,6 +131,7 @@ k_spread_mma(const SubDev* __restrict__ subs, const WinDev* __restrict__ wins,
         const double* R = srow[buf];
         const double* V = sv[buf];
         const int nks = (cn + 3) >> 2;
+#pragma unroll 2
         for (int ks = slice; ks < nks; ks += wpr) {
           const int j = ks * 4 + t;
           const bool ok = j < cn;
@@ -203,6 +204,12 @@ k_spread_mma(const SubDev* __restrict__ subs, const WinDev* __restrict__ wins,
 }
 
 // ---- gather ---------------------------------------------------------------
+// Khatri-Rao form: T[a][j] = sum_{(b,c)} G[a][(b,c)] (B_j (x) C_j)[(b,c)]
+// (M = 8 rows a, K = 64, N = 8 nodes), then y_j = sum_a A_j[a] T[a][j]
+// reduced over a across the 8 lanes of a column.  The (B (x) C) fragments
+// depend only on the nodes, so they are formed once per 8-node tile and
+// reused for every right-hand side; the G fragments come from shared memory
+// (XOR-swizzled: element (a, kk) at a*64 + (kk ^ 4a), conflict-free).
 __global__ void __launch_bounds__(kGaThreads)
 k_gather_mma(const SubDev* __restrict__ subs, const CellDev* __restrict__ cells,
              const WinDev* __restrict__ wins, const double* __restrict__ rows,
@@ -223,73 +230,59 @@ k_gather_mma(const SubDev* __restrict__ subs, const CellDev* __restrict__ cells,
     __syncthreads();
     for (int e = tid; e < rn * kBlk; e += kGaThreads) {
       const int q = e >> 9, k = e & (kBlk - 1);
-      int p0 = cd.cc[0] + (k >> 6), p1 = cd.cc[1] + ((k >> 3) & 7), p2 = cd.cc[2] + (k & 7);
+      const int a = k >> 6, kk = k & 63;
+      int p0 = cd.cc[0] + a, p1 = cd.cc[1] + (kk >> 3), p2 = cd.cc[2] + (kk & 7);
       if (p0 >= wd.box_w[0]) p0 -= wd.box_w[0];
       if (p1 >= wd.box_w[1]) p1 -= wd.box_w[1];
       if (p2 >= wd.box_w[2]) p2 -= wd.box_w[2];
-      const int b = (k >> 3) & 7, c = k & 7;
-      gb[q * kBlk + (k & ~7) + (c ^ (((b >> 1) & 1) << 2))] =
+      gb[q * kBlk + a * 64 + (kk ^ (4 * a))] =
           grid[(int64_t)(rg + q) * grid_ld + wd.grid_off +
                ((int64_t)p0 * wd.box_w[1] + p1) * wd.box_w[2] + p2];
     }
     __syncthreads();
     for (int nt = warp; nt < ntile; nt += kGaWarps) {
       const int j0 = nt * 8;
-      // B fragments: C weights of node j0 + g, c = 4 ks + t
+      // (B (x) C) fragments of node j0 + g: k = 4 ks + t -> (b = ks/2, c = 4(ks&1) + t)
       const int jn = j0 + g;
-      double cf[2] = {0.0, 0.0};
+      double bf[16];
       if (jn < sd.count) {
-        cf[0] = __ldg(rw + (int64_t)jn * kRow + 2 * kS + t);
-        cf[1] = __ldg(rw + (int64_t)jn * kRow + 2 * kS + 4 + t);
+        const double* r = rw + (int64_t)jn * kRow;
+        double bw[8];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const double2 x = __ldg(reinterpret_cast<const double2*>(r + kS) + k);
+          bw[2 * k] = x.x;
+          bw[2 * k + 1] = x.y;
+        }
+        const double c0 = __ldg(r + 2 * kS + t), c1 = __ldg(r + 2 * kS + 4 + t);
+#pragma unroll
+        for (int ks = 0; ks < 16; ++ks) bf[ks] = bw[ks >> 1] * ((ks & 1) ? c1 : c0);
+      } else {
+#pragma unroll
+        for (int ks = 0; ks < 16; ++ks) bf[ks] = 0.0;
       }
-      // step-2 weights of nodes j0 + 2t + i: A[0..7], B[g]
-      double aw[2][8], bw[2];
-      int jp[2];
+      // A weight of the two output nodes j0 + 2t + i at row a = g
+      double aw[2];
+      int jp[2], pj[2] = {0, 0};
 #pragma unroll
       for (int i = 0; i < 2; ++i) {
         jp[i] = j0 + 2 * t + i;
-        if (jp[i] < sd.count) {
-          const double2* src = reinterpret_cast<const double2*>(rw + (int64_t)jp[i] * kRow);
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const double2 x = __ldg(src + k);
-            aw[i][2 * k] = x.x;
-            aw[i][2 * k + 1] = x.y;
-          }
-          bw[i] = __ldg(rw + (int64_t)jp[i] * kRow + kS + g);
-        } else {
-#pragma unroll
-          for (int k = 0; k < 8; ++k) aw[i][k] = 0.0;
-          bw[i] = 0.0;
-        }
+        const bool ok = jp[i] < sd.count;
+        aw[i] = ok ? __ldg(rw + (int64_t)jp[i] * kRow + g) : 0.0;
+        if (ok && g == 0) pj[i] = pix[sd.start + jp[i]];
       }
-      int pj[2] = {0, 0};
-      if (g == 0) {
+      const int gsw = 4 * g;
+      for (int q = 0; q < rn; ++q) {
+        const double* G = gb + q * kBlk + g * 64;
+        double acc[4][2];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[c][0] = acc[c][1] = 0.0;
+#pragma unroll
+        for (int ks = 0; ks < 16; ++ks) dmma(acc[ks & 3], G[(4 * ks + t) ^ gsw], bf[ks]);
+        double p[2];
 #pragma unroll
         for (int i = 0; i < 2; ++i)
-          if (jp[i] < sd.count) pj[i] = pix[sd.start + jp[i]];
-      }
-      // swizzled G fragment offsets: (a*8 + g)*8 + (c ^ swz(g)), c = 4ks + t
-      const int sw = ((g >> 1) & 1) << 2;
-      const int o0 = g * 8 + (t ^ sw), o1 = g * 8 + ((4 + t) ^ sw);
-      for (int q = 0; q < rn; ++q) {
-        const double* G = gb + q * kBlk;
-        double T[8][2];
-#pragma unroll
-        for (int a = 0; a < 8; ++a) {
-          T[a][0] = T[a][1] = 0.0;
-          dmma(T[a], G[a * 64 + o0], cf[0]);
-        }
-#pragma unroll
-        for (int a = 0; a < 8; ++a) dmma(T[a], G[a * 64 + o1], cf[1]);
-        double p[2] = {0.0, 0.0};
-#pragma unroll
-        for (int a = 0; a < 8; ++a) {
-          p[0] = fma(aw[0][a], T[a][0], p[0]);
-          p[1] = fma(aw[1][a], T[a][1], p[1]);
-        }
-        p[0] *= bw[0];
-        p[1] *= bw[1];
+          p[i] = aw[i] * ((acc[0][i] + acc[1][i]) + (acc[2][i] + acc[3][i]));
 #pragma unroll
         for (int off = 4; off < 32; off <<= 1) {
           p[0] += __shfl_xor_sync(0xffffffffu, p[0], off);

@@ -310,6 +310,15 @@ __global__ void k_cells(const int32_t* __restrict__ ukeys,
   }
 }
 
+__global__ void k_cellinfo(const int32_t* __restrict__ cellmap, const CellDev* __restrict__ cells,
+                           int64_t n, int2* __restrict__ info) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int c = cellmap[k];
+    info[k] = c < 0 ? make_int2(0, 0) : make_int2((int)cells[c].block0, cells[c].nsub);
+  }
+}
+
 __global__ void k_nsub(const int32_t* __restrict__ counts, int ncell,
                        int32_t* __restrict__ nsub) {
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < ncell;
@@ -485,6 +494,7 @@ void build_planset(nld_operator* op, int which, cudaStream_t st) {
     ps.pix = other->pix;
     ps.key = other->key;
     ps.cellmap = other->cellmap;
+    ps.cellinfo = other->cellinfo;
     ps.cells = other->cells;
     ps.n_cells = other->n_cells;
     for (int g = 0; g <= kMaxDim; ++g) {
@@ -774,6 +784,12 @@ void build_planset(nld_operator* op, int which, cudaStream_t st) {
   }
   ps.blocks_total = block_total;
   ps.grid_total = grid_total;
+  if (block_total >= (int64_t)INT32_MAX)
+    throw Error(NLD_ERR_VALUE, "too many subproblem blocks for 32-bit offsets");
+  ps.cellinfo = dalloc<int2>(cellmap_total);
+  k_cellinfo<<<blocks_for(cellmap_total), 256, 0, st>>>(ps.cellmap, ps.cells, cellmap_total,
+                                                        ps.cellinfo);
+  NLD_CUDA(cudaGetLastError());
   NLD_CUDA(cudaMalloc(&ps.wdev, sizeof(WinDev) * L));
   NLD_CUDA(cudaMemcpyAsync(ps.wdev, ps.wdev_h.data(), sizeof(WinDev) * L,
                            cudaMemcpyHostToDevice, st));
@@ -788,6 +804,7 @@ void free_planset(PlanSet& ps) {
     cudaFree(ps.pix);
     cudaFree(ps.key);
     cudaFree(ps.cellmap);
+    cudaFree(ps.cellinfo);
     cudaFree(ps.cells);
     for (int g = 0; g <= kMaxDim; ++g) cudaFree(ps.subs[g]);
     cudaFree(ps.edges);
