@@ -569,40 +569,85 @@ k_gather(const SubDev* __restrict__ subs, const CellDev* __restrict__ cells,
 // ---- epilogue: window sum + diagonal/degree terms (kernel.py:86-93,
 //      linops.py:43-50) ---------------------------------------------------
 
-constexpr int kTileP = 128;    // pixels per epilogue / transpose tile
+constexpr int kTileP = 128;    // pixels per transpose tile
+constexpr int kEpiElems = 2048;  // (pixel, rhs) elements per epilogue tile
+constexpr int kEpiThreads = 256;
+constexpr int kEpiPer = kEpiElems / kEpiThreads;
 
-// Epilogue (kernel.py:86-93, linops.py:43-50): per pixel tile, sum the
-// per-window gathers [L][N][nrhs] (coalesced, rhs fastest), then switch to an
-// rhs-major layout in shared memory so v, eta and the output [nrhs][ld] are
-// read and written coalesced.
-__global__ void __launch_bounds__(256)
-k_epilogue(int kind, int L, int64_t N, int nrhs, const double* __restrict__ v, int64_t ldv,
-           const double* __restrict__ wsum, int direct, double* __restrict__ out,
-           int64_t ldo, const double* __restrict__ eta, const double* __restrict__ coef) {
-  extern __shared__ double tile[];   // [kTileP][nrhs + 1]
-  const int ld_t = nrhs + 1;
-  const int64_t ntiles = (N + kTileP - 1) / kTileP;
+// Epilogue (kernel.py:86-93, linops.py:43-50) for power-of-two nrhs: a tile
+// of TP = 2048/nrhs pixels; the per-window gathers [L][N][nrhs] are read
+// coalesced (rhs fastest, 8 independent loads per thread per window), summed,
+// transposed through shared memory, and v, eta and the output [nrhs][ld] are
+// then accessed rhs-major, also coalesced.
+__global__ void __launch_bounds__(kEpiThreads)
+k_epilogue_tiled(int kind, int L, int64_t N, int lg_nrhs, const double* __restrict__ v,
+                 int64_t ldv, const double* __restrict__ wsum, double* __restrict__ out,
+                 int64_t ldo, const double* __restrict__ eta, const double* __restrict__ coef) {
+  __shared__ double tile[kEpiElems + kEpiElems / 16];
+  const int nrhs = 1 << lg_nrhs;
+  const int lg_tp = 11 - lg_nrhs;           // TP = 2048 / nrhs
+  const int TP = 1 << lg_tp;
+  const int64_t ntiles = (N + TP - 1) / TP;
+  const int tid = threadIdx.x;
   for (int64_t tl = blockIdx.x; tl < ntiles; tl += gridDim.x) {
-    const int64_t i0 = tl * kTileP;
-    const int np = (int)min((int64_t)kTileP, N - i0);
-    if (!direct) {
-      for (int e = threadIdx.x; e < np * nrhs; e += blockDim.x) {
-        const int p = e / nrhs, r = e - p * nrhs;
-        double s = 0.0;
-        for (int w = 0; w < L; ++w) s += wsum[((int64_t)w * N + i0) * nrhs + e];
-        tile[p * ld_t + r] = s;
+    const int64_t i0 = tl * TP;
+    const int cnt = (int)min((int64_t)TP, N - i0) << lg_nrhs;
+    double s[kEpiPer];
+#pragma unroll
+    for (int k = 0; k < kEpiPer; ++k) s[k] = 0.0;
+    for (int w = 0; w < L; ++w) {
+      const double* __restrict__ src = wsum + ((int64_t)w * N + i0) * nrhs;
+#pragma unroll
+      for (int k = 0; k < kEpiPer; ++k) {
+        const int e = tid + k * kEpiThreads;
+        if (e < cnt) s[k] += src[e];
       }
-      __syncthreads();
     }
-    for (int e = threadIdx.x; e < np * nrhs; e += blockDim.x) {
-      const int r = e / np, p = e - r * np;
+#pragma unroll
+    for (int k = 0; k < kEpiPer; ++k) {
+      const int e = tid + k * kEpiThreads;     // e = p * nrhs + r
+      const int p = e >> lg_nrhs, r = e & (nrhs - 1);
+      tile[r * (TP + 8) + p] = s[k];           // rhs-major, padded rows
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kEpiPer; ++k) {
+      const int e = tid + k * kEpiThreads;     // e = r * TP + p
+      const int r = e >> lg_tp, p = e & (TP - 1);
       const int64_t i = i0 + p;
+      if (i >= N) continue;
+      const double x = v[r * ldv + i];
+      const double sum = tile[r * (TP + 8) + p];
+      double y;
+      if (kind == NLD_APPLY_WINDOW_SUM) {
+        y = sum;
+      } else {
+        const double gam = (sum - (double)L * x) / (double)L;
+        if (kind == NLD_APPLY_SYSTEM) y = coef[2 * r] * x + coef[2 * r + 1] * (eta[i] * x - gam);
+        else if (kind == NLD_APPLY_LAPLACIAN) y = eta[i] * x - gam;
+        else y = gam;
+      }
+      out[r * ldo + i] = y;
+    }
+    __syncthreads();
+  }
+}
+
+// generic epilogue (any nrhs; also the dense path where wsum is Gamma v)
+__global__ void k_epilogue(int kind, int L, int64_t N, int nrhs, const double* __restrict__ v,
+                           int64_t ldv, const double* __restrict__ wsum, int direct,
+                           double* __restrict__ out, int64_t ldo,
+                           const double* __restrict__ eta, const double* __restrict__ coef) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    for (int r = 0; r < nrhs; ++r) {
       const double x = v[r * ldv + i];
       double gam;
       if (direct) {
         gam = wsum[r * N + i];
       } else {
-        const double s = tile[p * ld_t + r];
+        double s = 0.0;
+        for (int w = 0; w < L; ++w) s += wsum[((int64_t)w * N + i) * nrhs + r];
         if (kind == NLD_APPLY_WINDOW_SUM) {
           out[r * ldo + i] = s;
           continue;
@@ -615,7 +660,6 @@ k_epilogue(int kind, int L, int64_t N, int nrhs, const double* __restrict__ v, i
       else y = gam;
       out[r * ldo + i] = y;
     }
-    __syncthreads();
   }
 }
 
@@ -936,9 +980,17 @@ void apply_op(nld_operator* op, int which, int kind, const double* v, double* ou
   ev.mark();
   // 5. epilogue
   {
-    k_epilogue<<<grid_blocks(N, kTileP, 148 * 16), 256,
-                 sizeof(double) * kTileP * (nrhs + 1), st>>>(kind, L, N, nrhs, v, ld, ws.wout,
-                                                             0, out, ld, eta, coef_dev);
+    int lg = -1;
+    for (int k = 0; k <= 11; ++k)
+      if ((1 << k) == nrhs) lg = k;
+    if (lg >= 0) {
+      const int tp = 2048 >> lg;
+      k_epilogue_tiled<<<grid_blocks(N, tp, 148 * 8), kEpiThreads, 0, st>>>(
+          kind, L, N, lg, v, ld, ws.wout, out, ld, eta, coef_dev);
+    } else {
+      k_epilogue<<<grid_blocks(N, 256, 148 * 16), 256, 0, st>>>(kind, L, N, nrhs, v, ld, ws.wout,
+                                                                 0, out, ld, eta, coef_dev);
+    }
     NLD_CUDA(cudaGetLastError());
   }
   ev.mark();
@@ -979,8 +1031,8 @@ void dense_apply(nld_operator* op, int which, int kind, const double* v, double*
   k_dense_apply<<<grid, 128, 0, st>>>(op->feats, op->N, op->D, widx, woff, op->L, inv, v, ld,
                                       gam);
   NLD_CUDA(cudaGetLastError());
-  k_epilogue<<<grid_blocks(op->N, kTileP), 256, sizeof(double) * kTileP * (nrhs + 1), st>>>(
-      kind, op->L, op->N, nrhs, v, ld, gam, 1, out, ld, eta, coef_dev);
+  k_epilogue<<<grid_blocks(op->N, 256), 256, 0, st>>>(kind, op->L, op->N, nrhs, v, ld, gam, 1,
+                                                       out, ld, eta, coef_dev);
   NLD_CUDA(cudaGetLastError());
   cudaFreeAsync(gam, st);
   cudaFreeAsync(widx, st);

@@ -210,7 +210,7 @@ k_spread_mma(const SubDev* __restrict__ subs, const WinDev* __restrict__ wins,
 // depend only on the nodes, so they are formed once per 8-node tile and
 // reused for every right-hand side; the G fragments come from shared memory
 // (XOR-swizzled: element (a, kk) at a*64 + (kk ^ 4a), conflict-free).
-__global__ void __launch_bounds__(kGaThreads)
+__global__ void __launch_bounds__(kGaThreads, 2)
 k_gather_mma(const SubDev* __restrict__ subs, const CellDev* __restrict__ cells,
              const WinDev* __restrict__ wins, const double* __restrict__ rows,
              const int32_t* __restrict__ pix, const double* __restrict__ grid,
@@ -272,13 +272,7 @@ k_gather_mma(const SubDev* __restrict__ subs, const CellDev* __restrict__ cells,
         if (ok && g == 0) pj[i] = pix[sd.start + jp[i]];
       }
       const int gsw = 4 * g;
-      for (int q = 0; q < rn; ++q) {
-        const double* G = gb + q * kBlk + g * 64;
-        double acc[4][2];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) acc[c][0] = acc[c][1] = 0.0;
-#pragma unroll
-        for (int ks = 0; ks < 16; ++ks) dmma(acc[ks & 3], G[(4 * ks + t) ^ gsw], bf[ks]);
+      auto finish = [&](const double (&acc)[4][2], int q) {
         double p[2];
 #pragma unroll
         for (int i = 0; i < 2; ++i)
@@ -293,6 +287,32 @@ k_gather_mma(const SubDev* __restrict__ subs, const CellDev* __restrict__ cells,
           for (int i = 0; i < 2; ++i)
             if (jp[i] < sd.count) out[(int64_t)pj[i] * nrhs + rg + q] = p[i];
         }
+      };
+      int q = 0;
+      // two right-hand sides per pass: 8 independent DMMA chains in flight
+      for (; q + 1 < rn; q += 2) {
+        const double* G0 = gb + q * kBlk + g * 64;
+        const double* G1 = G0 + kBlk;
+        double a0[4][2], a1[4][2];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) a0[c][0] = a0[c][1] = a1[c][0] = a1[c][1] = 0.0;
+#pragma unroll
+        for (int ks = 0; ks < 16; ++ks) {
+          const int o = (4 * ks + t) ^ gsw;
+          dmma(a0[ks & 3], G0[o], bf[ks]);
+          dmma(a1[ks & 3], G1[o], bf[ks]);
+        }
+        finish(a0, q);
+        finish(a1, q + 1);
+      }
+      if (q < rn) {
+        const double* G0 = gb + q * kBlk + g * 64;
+        double a0[4][2];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) a0[c][0] = a0[c][1] = 0.0;
+#pragma unroll
+        for (int ks = 0; ks < 16; ++ks) dmma(a0[ks & 3], G0[(4 * ks + t) ^ gsw], bf[ks]);
+        finish(a0, q);
       }
     }
   }
