@@ -59,6 +59,14 @@ extern "C" {
 
 typedef struct nld_operator nld_operator;
 
+/* Collective hook for pixel sharding.  The library calls it at
+ * the plan-build reductions (torus bbox / radius / support box), once per
+ * product for the per-window grid sum, and for the CG scalars.
+ * dtype: 0 f64, 1 i32; op: 0 sum, 1 min, 2 max; on_device: buf is a device
+ * pointer ordered on `stream` (else a host pointer).  Returns 0 on success. */
+typedef int (*nld_allreduce_fn)(void* ctx, void* buf, int64_t count, int32_t dtype,
+                                int32_t op, int32_t on_device, void* stream);
+
 /* NFFT / fast-summation parameters, FastsumPlan.build (transform.py:273-283).
  * n_expansion <= 0 selects the reference's adaptive expansion_degree
  * (transform.py:254-258); mode 0 = "fast", 1 = "exact" (kernel.py:28-29). */
@@ -116,6 +124,11 @@ NLD_API int nld_op_create(const double* features_dev, int64_t n, int32_t n_featu
                   int32_t n_windows, double sigma, const nld_params* params,
                   void* stream, nld_operator** out);
 NLD_API int nld_op_destroy(nld_operator* op);
+
+/* Make `op` one shard of a pixel-sharded operator: its nodes are a slice of
+ * global_n nodes.  Must be called before the first product (plan build). */
+NLD_API int nld_op_set_comm(nld_operator* op, nld_allreduce_fn fn, void* ctx,
+                            int64_t global_n);
 
 /* One fused product per right-hand side (kernel.py:79-93, linops.py:43-50).
  * coef: per-rhs (lam, mu) pairs for NLD_APPLY_SYSTEM, ignored otherwise.

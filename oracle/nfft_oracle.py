@@ -199,7 +199,10 @@ class WindowPlan:
     """
 
     def __init__(self, pts, sigbar, n_expansion=None, cutoff=CUTOFF_DEFAULT,
-                 oversampling=2.0, rmax=RMAX_DEFAULT, eps=TRUNC_EPS_DEFAULT):
+                 oversampling=2.0, rmax=RMAX_DEFAULT, eps=TRUNC_EPS_DEFAULT,
+                 center=None, scale=None):
+        # center/scale overrides: a shard of a larger point set uses the
+        # global torus map (sharding tests only)
         if sigbar <= 0:
             raise ValueError("shape parameter must be positive")
         p = np.asarray(pts, np.float64)
@@ -207,10 +210,14 @@ class WindowPlan:
         if p.shape[0] == 0:
             raise ValueError("empty point set")
         self.d = p.shape[1]
-        lo, hi = p.min(axis=0), p.max(axis=0)
-        self.center = 0.5 * (lo + hi)
-        radius = float(np.sqrt(((p - self.center) ** 2).sum(axis=1).max()))
-        self.scale = rmax / max(radius, 1e-30)
+        if center is None:
+            lo, hi = p.min(axis=0), p.max(axis=0)
+            self.center = 0.5 * (lo + hi)
+            radius = float(np.sqrt(((p - self.center) ** 2).sum(axis=1).max()))
+            self.scale = rmax / max(radius, 1e-30)
+        else:
+            self.center = np.asarray(center, np.float64)
+            self.scale = float(scale)
         self.sig_scaled = sigbar / (self.scale * self.scale)
         if n_expansion is None:
             n_expansion = expansion_degree(self.sig_scaled, eps)

@@ -59,6 +59,11 @@ class Stats(ctypes.Structure):
 
 _P = ctypes.c_void_p
 _I32, _I64, _D = ctypes.c_int32, ctypes.c_int64, ctypes.c_double
+
+# int (*)(ctx, buf, count, dtype, op, on_device, stream)  (nld_allreduce_fn)
+ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
+                                ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
+                                ctypes.c_int32, ctypes.c_void_p)
 _PI32 = ctypes.POINTER(ctypes.c_int32)
 _PD = ctypes.POINTER(ctypes.c_double)
 
@@ -69,6 +74,7 @@ SIGNATURES = {
                                      ctypes.POINTER(Params), _P,
                                      ctypes.POINTER(_P)]),
     "nld_op_destroy": (ctypes.c_int, [_P]),
+    "nld_op_set_comm": (ctypes.c_int, [_P, ALLREDUCE_FN, _P, _I64]),
     "nld_op_apply": (ctypes.c_int, [_P, _I32, _P, _P, _I32, _I64, _PD, _P]),
     "nld_op_degree": (ctypes.c_int, [_P, _I32, _P, _P]),
     "nld_op_assemble_dense": (ctypes.c_int, [_P, _I32, _P, _P]),

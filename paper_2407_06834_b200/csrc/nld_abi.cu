@@ -22,13 +22,23 @@ int fail(int code, const std::string& msg) {
   return code;
 }
 
+void comm_host(nld_operator* op, void* buf, int64_t count, int dtype, int red) {
+  if (!op->comm || count <= 0) return;
+  if (op->comm(op->comm_ctx, buf, count, dtype, red, 0, nullptr) != 0)
+    throw Error(NLD_ERR_CUDA, "allreduce callback failed (host buffer)");
+}
+
+void comm_device(nld_operator* op, double* buf, int64_t count, cudaStream_t st) {
+  if (!op->comm || count <= 0) return;
+  if (op->comm(op->comm_ctx, buf, count, RED_F64, RED_OP_SUM, 1, st) != 0)
+    throw Error(NLD_ERR_CUDA, "allreduce callback failed (device buffer)");
+}
+
 }  // namespace nld
 
 using nld::Error;
 
 namespace {
-
-std::mutex g_build_mutex;
 
 // select the device that owns `ptr` (torch may have set another device on the
 // calling thread; this library's runtime keeps its own current device)
@@ -60,7 +70,7 @@ int guarded(F&& fn) {
 }
 
 void ensure_built(nld_operator* op, int which, cudaStream_t st) {
-  std::lock_guard<std::mutex> lk(g_build_mutex);
+  std::lock_guard<std::mutex> lk(op->build_mu);
   if (op->params.mode == 1 || op->built[which]) return;
   nld::build_planset(op, which, st);
   op->built[which] = true;
@@ -132,6 +142,7 @@ int nld_op_create(const double* features_dev, int64_t n, int32_t n_features,
     try {
       NLD_CUDA(cudaGetDevice(&op->device));
       op->N = n;
+      op->N_global = n;
       op->D = n_features;
       op->L = n_windows;
       op->sigma = sigma;
@@ -165,6 +176,20 @@ int nld_op_destroy(nld_operator* op) {
     if (op->events)
       for (auto& e : op->ev) cudaEventDestroy(e);
     delete op;
+  });
+}
+
+int nld_op_set_comm(nld_operator* op, nld_allreduce_fn fn, void* ctx, int64_t global_n) {
+  return guarded([&] {
+    if (!op) throw Error(NLD_ERR_VALUE, "null operator");
+    if (op->built[0] || op->built[1])
+      throw Error(NLD_ERR_VALUE, "set_comm must precede the first product");
+    if (global_n < op->N) throw Error(NLD_ERR_DIMENSION, "global_n smaller than local n");
+    if (op->params.mode == 1 && fn)
+      throw Error(NLD_ERR_VALUE, "exact mode cannot be sharded");
+    op->comm = fn;
+    op->comm_ctx = ctx;
+    op->N_global = global_n;
   });
 }
 

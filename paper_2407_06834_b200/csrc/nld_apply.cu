@@ -938,6 +938,8 @@ void apply_op(nld_operator* op, int which, int kind, const double* v, double* ou
                                          ps.grid_total);
     NLD_CUDA(cudaGetLastError());
   }
+  // pixel shards: sum the support-box grids of every rank
+  comm_device(op, ws.grid_in, ps.grid_total * nrhs, st);
   ev.mark();
   // 3. separable convolution, one pass per axis
   {

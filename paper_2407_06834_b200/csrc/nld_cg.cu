@@ -192,13 +192,14 @@ int eblocks(int64_t n) {
 }
 
 struct Reducer {
+  nld_operator* op = nullptr;
   double* part = nullptr;
   double* out = nullptr;
   std::vector<double> host;
   int nrhs;
   int nblk;
   cudaStream_t st;
-  Reducer(int nr, int64_t N, cudaStream_t s) : nrhs(nr), st(s) {
+  Reducer(nld_operator* o, int nr, int64_t N, cudaStream_t s) : op(o), nrhs(nr), st(s) {
     nblk = (int)std::max<int64_t>(1, std::min<int64_t>(kRB, (N + kRT - 1) / kRT));
     NLD_CUDA(cudaMallocAsync(&part, sizeof(double) * nr * nblk * kMaxK, st));
     NLD_CUDA(cudaMallocAsync(&out, sizeof(double) * nr * kMaxK, st));
@@ -218,6 +219,7 @@ struct Reducer {
     NLD_CUDA(cudaMemcpyAsync(host.data(), out, sizeof(double) * nrhs * kMaxK,
                              cudaMemcpyDeviceToHost, st));
     NLD_CUDA(cudaStreamSynchronize(st));
+    comm_host(op, host.data(), (int64_t)nrhs * kMaxK, RED_F64, RED_OP_SUM);
     return host;
   }
 };
@@ -399,7 +401,8 @@ void cg_solve(nld_operator* op, const double* f, double* u, int nrhs, int64_t ld
               int maxit, int warm, int* iters, double* relres, int* conv, double* hist,
               int hist_cap, cudaStream_t st) {
   const int64_t N = op->N;
-  if (deflate && N < 2) throw Error(NLD_ERR_DIMENSION, "basis needs at least two entries");
+  if (deflate && op->N_global < 2)
+    throw Error(NLD_ERR_DIMENSION, "basis needs at least two entries");
   for (int r = 0; r < nrhs; ++r)
     if (!(lam[r] > 0) || !(mu[r] > 0))
       throw Error(NLD_ERR_VALUE, "shift lambda and weight mu must be positive");
@@ -472,8 +475,8 @@ void cg_solve(nld_operator* op, const double* f, double* u, int nrhs, int64_t ld
     if (op->params.mode == 1) dense_apply(op, 0, NLD_APPLY_SYSTEM, in, out, nrhs, N, coef, eta, st);
     else apply_op(op, 0, NLD_APPLY_SYSTEM, in, out, nrhs, N, coef, eta, st);
   };
-  const double dN = (double)N;
-  Reducer red(nrhs, N, st);
+  const double dN = (double)op->N_global;
+  Reducer red(op, nrhs, N, st);
   dim3 eg(eblocks(N), nrhs);
 
   std::vector<std::vector<double>> H(nrhs);

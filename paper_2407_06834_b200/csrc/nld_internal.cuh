@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -148,7 +149,10 @@ struct Workspace {
 }  // namespace nld
 
 struct nld_operator {
-  int64_t N = 0;
+  int64_t N = 0;                 // local nodes (this shard)
+  int64_t N_global = 0;          // all shards
+  nld_allreduce_fn comm = nullptr;
+  void* comm_ctx = nullptr;
   int D = 0;
   int L = 0;
   double sigma = 0.0;
@@ -165,6 +169,8 @@ struct nld_operator {
   nld_stats stats{};
   cudaEvent_t ev[6] = {};
   bool events = false;
+  std::mutex build_mu;           // lazy plan build (per operator: shards may
+                                 // build concurrently in one process)
 };
 
 namespace nld {
@@ -200,5 +206,11 @@ void dev_basis(const double* v, const double* x, double* out, int64_t n,
                int adjoint, cudaStream_t st);
 
 int64_t expansion_degree(double sig_scaled, double eps);
+
+// collective helpers (no-ops without a comm hook)
+enum { RED_F64 = 0, RED_I32 = 1 };
+enum { RED_OP_SUM = 0, RED_OP_MIN = 1, RED_OP_MAX = 2 };
+void comm_host(nld_operator* op, void* buf, int64_t count, int dtype, int red);
+void comm_device(nld_operator* op, double* buf, int64_t count, cudaStream_t st);
 
 }  // namespace nld

@@ -420,16 +420,17 @@ void build_planset(nld_operator* op, int which, cudaStream_t st) {
     NLD_CUDA(cudaMemcpyAsync(hpart.data(), part.p, sizeof(double) * nb * 6,
                              cudaMemcpyDeviceToHost, st));
     NLD_CUDA(cudaStreamSynchronize(st));
-    double lo[3], hi[3];
+    double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
     for (int s = 0; s < wp.d; ++s) {
-      lo[s] = INFINITY;
-      hi[s] = -INFINITY;
       for (int k = 0; k < nb; ++k) {
         lo[s] = std::min(lo[s], hpart[k * 6 + s]);
         hi[s] = std::max(hi[s], hpart[k * 6 + 3 + s]);
       }
-      wp.center[s] = 0.5 * (lo[s] + hi[s]);
     }
+    // global bounding box across pixel shards (transform.py:292-293)
+    comm_host(op, lo, wp.d, RED_F64, RED_OP_MIN);
+    comm_host(op, hi, wp.d, RED_F64, RED_OP_MAX);
+    for (int s = 0; s < wp.d; ++s) wp.center[s] = 0.5 * (lo[s] + hi[s]);
     k_radius2<<<nb, kRedThreads, 0, st>>>(
         op->feats, N, op->D, cols, wp.d,
         make_double3(wp.center[0], wp.center[1], wp.center[2]), part.as<double>());
@@ -438,6 +439,7 @@ void build_planset(nld_operator* op, int which, cudaStream_t st) {
     NLD_CUDA(cudaStreamSynchronize(st));
     double r2 = 0.0;
     for (int k = 0; k < nb; ++k) r2 = std::max(r2, hpart[k]);
+    comm_host(op, &r2, 1, RED_F64, RED_OP_MAX);
     double radius = std::sqrt(r2);
     wp.scale = P.rmax / std::max(radius, 1e-30);
     wp.sig_scaled = ps.sigbar / (wp.scale * wp.scale);
@@ -572,6 +574,10 @@ void build_planset(nld_operator* op, int which, cudaStream_t st) {
     int hf[8];
     NLD_CUDA(cudaMemcpyAsync(hf, flags.p, sizeof(int) * 8, cudaMemcpyDeviceToHost, st));
     NLD_CUDA(cudaStreamSynchronize(st));
+    // global support box and overflow flag across shards
+    comm_host(op, hf, 1, RED_I32, RED_OP_MAX);
+    comm_host(op, hf + 1, 3, RED_I32, RED_OP_MIN);
+    comm_host(op, hf + 4, 3, RED_I32, RED_OP_MAX);
     if (hf[0]) throw Error(NLD_ERR_SCALING, "scaled nodes leave the torus [-1/2, 1/2)^d");
     BoxDev bx;
     bx.d = wp.d;

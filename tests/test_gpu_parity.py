@@ -283,3 +283,90 @@ def test_dense_limit():
                            mode="exact")
     with pytest.raises(nld.DenseLimitError):
         op.apply(np.ones(6000))
+
+
+# ------------------------------------------------ pixel sharding (emulated)
+
+def test_sharded_ranks_match_single_gpu(golden):
+    """2 ranks as host threads on one GPU (sharding.ThreadComm): the sharded
+    matvec, degree and batched CG equal the unsharded operator's."""
+    import threading
+
+    from paper_2407_06834_b200 import sharding as S
+    g = golden("c1")
+    full, feats, wins, f = operator("c1")
+    n = feats.shape[0]
+    v = synth.random_vector(n)
+    want_gv = full.apply(v)
+    want_eta = full.degree()
+    mus = [float(g["mu"]), 3.0 * float(g["mu"])]
+    want_cg = nld.deflated_solve_batched(full, f[:, 0], 1.0, mus,
+                                         tol=synth.CG_TOL, maxit=200)
+    world = 2
+    comm = S.ThreadComm(world, device=torch.device("cuda", 0))
+    out, errs = {}, []
+
+    def rank_main(rank):
+        try:
+            lo, hi = S.shard_range(n, rank, world)
+            op = nld.AnovaOperator(torch.from_numpy(feats[lo:hi]).cuda(), wins,
+                                   synth.SIGMA, **PIN)
+            S.attach(op, comm, rank, n)
+            gv = op.apply(v[lo:hi])
+            eta = op.degree().cpu().numpy()
+            res = nld.deflated_solve_batched(op, f[lo:hi, 0], 1.0, mus,
+                                             tol=synth.CG_TOL, maxit=200)
+            out[rank] = (gv, eta, res, op.window_info(0))
+        except Exception as exc:  # pragma: no cover - reported below
+            errs.append(exc)
+            comm.barrier.abort()
+
+    threads = [threading.Thread(target=rank_main, args=(r,)) for r in range(world)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join(timeout=600)
+    assert not errs, errs
+    gv = np.concatenate([out[r][0] for r in range(world)])
+    eta = np.concatenate([out[r][1] for r in range(world)])
+    assert rel(gv, want_gv) < 1e-12
+    assert rel(eta, want_eta) < 1e-12
+    assert out[0][3]["scale"] == full.window_info(0)["scale"]
+    assert out[0][3]["box_w"] == full.window_info(0)["box_w"]
+    for k in range(len(mus)):
+        its = {out[r][2][k].iterations for r in range(world)}
+        assert its == {want_cg[k].iterations}
+        x = np.concatenate([out[r][2][k].x for r in range(world)])
+        assert rel(x, want_cg[k].x) < 1e-10
+
+
+def test_torchcomm_nccl_single_rank(golden):
+    """The NCCL hook path (zero-copy CAI views, ExternalStream ordering) with a
+    one-rank process group gives the unsharded result bit for bit."""
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_2407_06834_b200 import sharding as S
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}",
+                            rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        full, feats, wins, f = operator("c0")
+        op = nld.AnovaOperator(torch.from_numpy(feats).cuda(), wins, synth.SIGMA,
+                               **PIN)
+        S.attach(op, S.TorchComm(device=torch.device("cuda", 0)), 0, op.n)
+        v = synth.random_vector(op.n)
+        assert np.array_equal(op.apply(v), full.apply(v))
+        r1 = nld.deflated_solve_batched(op, f[:, 0], 1.0, [0.01, 0.02],
+                                        tol=synth.CG_TOL)
+        r0 = nld.deflated_solve_batched(full, f[:, 0], 1.0, [0.01, 0.02],
+                                        tol=synth.CG_TOL)
+        for a, b in zip(r0, r1):
+            assert a.iterations == b.iterations
+            assert np.array_equal(a.x, b.x)
+    finally:
+        dist.destroy_process_group()
