@@ -331,7 +331,7 @@ def run_ours(args, world, rank, local):
     except (OSError, ValueError, KeyError):
         peak_src = "fallback"
     achieved = alg_bytes / (dom_ms * 1e-3) / 1e9
-    tag = f"k_{dominant}<3,4>"
+    tag = "k_gather_mma" if dominant == "gather" else "k_spread_mma"
     roofline = {
         "bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
         "frac": achieved / hbm_peak, "traffic": ncu_traffic(tag),

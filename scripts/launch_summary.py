@@ -1,0 +1,31 @@
+"""Summarise an `ncu --metrics gpu__time_duration.sum` launch list (CSV)."""
+import csv
+import json
+import sys
+from collections import OrderedDict
+
+rows = [r for r in csv.reader(l for l in open(sys.argv[1]) if l.startswith('"'))]
+hdr = rows[0]
+ik, iv, iu = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
+seq = []
+for r in rows[1:]:
+    name = r[ik].split("(")[0].replace("nld::", "").replace("<unnamed>::", "")
+    name = name.replace("mma::", "").replace("void ", "")
+    ns = float(r[iv]) * {"ns": 1, "us": 1e3, "usecond": 1e3, "ms": 1e6, "msecond": 1e6}.get(r[iu], 1)
+    seq.append((name, ns / 1e6))
+# one steady-state matvec step: the last k_transpose_in .. k_epilogue_tiled run
+ends = [i for i, (n, _) in enumerate(seq) if n.startswith("k_epilogue")]
+starts = [i for i, (n, _) in enumerate(seq) if n.startswith("k_transpose_in")]
+step = []
+if ends and starts:
+    e = ends[-1]
+    s = max(i for i in starts if i < e)
+    step = seq[s:e + 1]
+agg = OrderedDict()
+for n, ms in step:
+    agg[n] = agg.get(n, 0.0) + ms
+tot = sum(agg.values())
+out = {"launches_total": len(seq), "step_launches": len(step),
+       "step_ms_serialized": tot,
+       "step_share": {k: {"ms": v, "share": v / tot} for k, v in agg.items()}}
+print(json.dumps(out, indent=1))
