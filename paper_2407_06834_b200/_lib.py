@@ -13,7 +13,8 @@ import os
 from . import errors
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libnld_b200.so")
+# NLD_LIB selects an alternative build of the same library (A/B experiments)
+LIB_PATH = os.environ.get("NLD_LIB") or os.path.join(_HERE, "libnld_b200.so")
 
 NLD_OK = 0
 ERR_DIMENSION, ERR_SCALING, ERR_WINDOW, ERR_DENSE_LIMIT = 1, 2, 3, 4

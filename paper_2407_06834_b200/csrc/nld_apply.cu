@@ -579,7 +579,7 @@ constexpr int kEpiPer = kEpiElems / kEpiThreads;
 // coalesced (rhs fastest, 8 independent loads per thread per window), summed,
 // transposed through shared memory, and v, eta and the output [nrhs][ld] are
 // then accessed rhs-major, also coalesced.
-__global__ void __launch_bounds__(kEpiThreads)
+__global__ void __launch_bounds__(kEpiThreads, NLD_EPI_MINB)
 k_epilogue_tiled(int kind, int L, int64_t N, int lg_nrhs, const double* __restrict__ v,
                  int64_t ldv, const double* __restrict__ wsum, double* __restrict__ out,
                  int64_t ldo, const double* __restrict__ eta, const double* __restrict__ coef) {
@@ -808,8 +808,11 @@ void spread_all(const PlanSet& ps, const Workspace& ws, const double* vt, int nr
   launch_spread<1, MC>(ps, ws, vt, nrhs, st);
   launch_spread<2, MC>(ps, ws, vt, nrhs, st);
   if (MC == 4 && use_mma() && ps.n_subs[3]) {
-    if (nrhs >= 16) launch_spread_mma<2>(ps, ws, vt, nrhs, st);
-    else launch_spread_mma<1>(ps, ws, vt, nrhs, st);
+    if (nrhs >= 16) {
+      launch_spread_mma<2>(ps, ws, vt, nrhs, st);
+    } else {
+      launch_spread_mma<1>(ps, ws, vt, nrhs, st);
+    }
   } else {
     launch_spread<3, MC>(ps, ws, vt, nrhs, st);
   }
@@ -824,9 +827,22 @@ void launch_gather_mma(const PlanSet& ps, const Workspace& ws, int64_t N, int nr
                                   (int)(sizeof(double) * mma::kBlk * mma::kGaRhs)));
     attr = true;
   }
-  mma::k_gather_mma<<<(unsigned)ps.n_subs[3], mma::kGaThreads, smem, st>>>(
-      ps.subs[3], ps.cells, ps.wdev, ps.rows, ps.pix, ws.grid_out, ps.grid_total, ws.wout, N,
-      nrhs);
+  if (nrhs >= 8) {
+    const size_t smem16 = sizeof(double) * 16 * mma::kGRow;
+    static bool attr16 = false;
+    if (!attr16) {
+      NLD_CUDA(cudaFuncSetAttribute(mma::k_gather_mma16,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem16));
+      attr16 = true;
+    }
+    mma::k_gather_mma16<<<(unsigned)ps.n_subs[3], mma::kGaThreads, smem16, st>>>(
+        ps.subs[3], ps.cells, ps.wdev, ps.rows, ps.pix, ws.grid_out, ps.grid_total, ws.wout, N,
+        nrhs);
+  } else {
+    mma::k_gather_mma<<<(unsigned)ps.n_subs[3], mma::kGaThreads, smem, st>>>(
+        ps.subs[3], ps.cells, ps.wdev, ps.rows, ps.pix, ws.grid_out, ps.grid_total, ws.wout, N,
+        nrhs);
+  }
   NLD_CUDA(cudaGetLastError());
 }
 

@@ -19,6 +19,16 @@
 
 #include "nld_internal.cuh"
 
+#ifndef NLD_SPREAD_UNROLL
+#define NLD_SPREAD_UNROLL 2
+#endif
+#ifndef NLD_SPREAD_MINB
+#define NLD_SPREAD_MINB 2
+#endif
+#ifndef NLD_EPI_MINB
+#define NLD_EPI_MINB 4
+#endif
+
 namespace nld {
 namespace mma {
 
@@ -47,6 +57,7 @@ __device__ __forceinline__ void cp_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
+constexpr int kSpUnroll = NLD_SPREAD_UNROLL;
 constexpr int kS = 8;             // stencil width 2m
 constexpr int kRow = 24;          // global row: [A(8)][B(8)][C(8)]
 constexpr int kSRow = 28;         // smem row stride: 16B aligned, conflict-free row[g]
@@ -67,15 +78,16 @@ __host__ __device__ constexpr int spread_smem(int rpp) {
 // RPW rhs per warp; rpp = rhs per pass = 8 * RPW (or nrhs if smaller, then
 // several warps share an rhs and split the k-steps).
 template <int RPW>
-__global__ void __launch_bounds__(kSpThreads, 2)
+__global__ void __launch_bounds__(kSpThreads, NLD_SPREAD_MINB)
 k_spread_mma(const SubDev* __restrict__ subs, const WinDev* __restrict__ wins,
              const double* __restrict__ rows, const int32_t* __restrict__ pix,
              const double* __restrict__ vt, int nrhs, double* __restrict__ blocks) {
   extern __shared__ __align__(16) double sm[];
   const int rpp_max = kSpWarps * RPW;
   const int rpp = nrhs < rpp_max ? nrhs : rpp_max;
-  double* srow[2] = {sm, sm + kSpChunk * kSRow};
-  double* sv[2] = {sm + 2 * kSpChunk * kSRow, sm + 2 * kSpChunk * kSRow + kSpChunk * rpp};
+  const int rowbuf = kSpChunk * kSRow;                // doubles per row buffer
+  const int vbuf = kSpChunk * rpp;                     // doubles per v buffer
+  double* const sv0 = sm + 2 * rowbuf;
   const SubDev sd = subs[blockIdx.x];
   const WinDev wd = wins[sd.win];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -106,13 +118,19 @@ k_spread_mma(const SubDev* __restrict__ subs, const WinDev* __restrict__ wins,
         const int pt = e / 12, gi = e - pt * 12;
         const int dim = gi >> 2, w4 = gi & 3;
         // smem order [C][B][A]: dim 2 -> 0, dim 1 -> 8, dim 0 -> 16
-        cp_async16(srow[buf] + pt * kSRow + (2 - dim) * kS + 2 * w4,
+        cp_async16(sm + buf * rowbuf + pt * kSRow + (2 - dim) * kS + 2 * w4,
                    rw + (int64_t)(c0 + pt) * kRow + dim * kS + 2 * w4);
       }
       for (int e = tid; e < cn * rn; e += kSpThreads) {
         const int pt = e / rn, q = e - pt * rn;
-        cp_async8(sv[buf] + pt * rpp + q, vt + (int64_t)pw[c0 + pt] * nrhs + rg + q);
+        cp_async8(sv0 + buf * vbuf + pt * rpp + q, vt + (int64_t)pw[c0 + pt] * nrhs + rg + q);
       }
+      // zero-pad to a multiple of 4 nodes so the k-step loop needs no bounds test
+      const int cpad = (cn + 3) & ~3;
+      for (int e = tid; e < (cpad - cn) * kSRow; e += kSpThreads)
+        sm[buf * rowbuf + cn * kSRow + e] = 0.0;
+      for (int e = tid; e < (cpad - cn) * rpp; e += kSpThreads)
+        sv0[buf * vbuf + cn * rpp + e] = 0.0;
       cp_commit();
     };
 
@@ -128,35 +146,26 @@ k_spread_mma(const SubDev* __restrict__ subs, const WinDev* __restrict__ wins,
       __syncthreads();
       const int cn = min(kSpChunk, sd.count - ck * kSpChunk);
       if (busy) {
-        const double* R = srow[buf];
-        const double* V = sv[buf];
+        const double* R = sm + buf * rowbuf;
+        const double* V = sv0 + buf * vbuf;
         const int nks = (cn + 3) >> 2;
-#pragma unroll 2
+        const int q0 = slot * RPW;
+#pragma unroll kSpUnroll
         for (int ks = slice; ks < nks; ks += wpr) {
           const int j = ks * 4 + t;
-          const bool ok = j < cn;
           const double* row = R + j * kSRow;
           double bw[8];
-          double cw = 0.0, aw = 0.0;
-          if (ok) {
 #pragma unroll
-            for (int b = 0; b < 8; b += 2) {
-              const double2 x = *reinterpret_cast<const double2*>(row + kS + b);
-              bw[b] = x.x;
-              bw[b + 1] = x.y;
-            }
-            cw = row[g];
-            aw = row[2 * kS + g];
-          } else {
-#pragma unroll
-            for (int b = 0; b < 8; ++b) bw[b] = 0.0;
+          for (int b = 0; b < 8; b += 2) {
+            const double2 x = *reinterpret_cast<const double2*>(row + kS + b);
+            bw[b] = x.x;
+            bw[b + 1] = x.y;
           }
+          const double cw = row[g];
+          const double aw = row[2 * kS + g];
           double af[RPW];
 #pragma unroll
-          for (int q = 0; q < RPW; ++q) {
-            const int qq = slot * RPW + q;
-            af[q] = (ok && qq < rn) ? V[j * rpp + qq] * aw : 0.0;
-          }
+          for (int q = 0; q < RPW; ++q) af[q] = V[j * rpp + q0 + q] * aw;
 #pragma unroll
           for (int n = 0; n < 8; ++n) {
             const double bf = bw[n] * cw;
@@ -313,6 +322,107 @@ k_gather_mma(const SubDev* __restrict__ subs, const CellDev* __restrict__ cells,
 #pragma unroll
         for (int ks = 0; ks < 16; ++ks) dmma(a0[ks & 3], G0[(4 * ks + t) ^ gsw], bf[ks]);
         finish(a0, q);
+      }
+    }
+  }
+}
+
+// ---- gather, right-hand sides as the M dimension (nrhs >= 8) -------------
+// D[r][j] = sum_{k=(a,b,c)} G_r[k] W_j[k],  W_j = A_j (x) B_j (x) C_j.
+// M = 16 rhs (2 m-tiles), N = 8 nodes, K = 512 (128 k-steps).  The W
+// fragment W[k = 64a + 4ks + t][node j0 + g] = A[a] * (B (x) C)[4ks + t] costs
+// one DMUL and feeds one DMMA per m-tile; the result is already the output
+// (no cross-lane reduction).  G rows are padded to 516 doubles so the 8 rhs
+// rows of a fragment hit distinct banks.
+constexpr int kGRow = 516;
+
+__global__ void __launch_bounds__(kGaThreads, 2)
+k_gather_mma16(const SubDev* __restrict__ subs, const CellDev* __restrict__ cells,
+               const WinDev* __restrict__ wins, const double* __restrict__ rows,
+               const int32_t* __restrict__ pix, const double* __restrict__ grid,
+               int64_t grid_ld, double* __restrict__ wout, int64_t N, int nrhs) {
+  extern __shared__ __align__(16) double gb[];   // [16][kGRow]
+  const SubDev sd = subs[blockIdx.x];
+  const CellDev cd = cells[sd.cell];
+  const WinDev wd = wins[sd.win];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int64_t local = sd.start - wd.node_off;
+  const double* __restrict__ rw = rows + wd.row_off + local * kRow;
+  double* __restrict__ out = wout + (int64_t)sd.win * N * nrhs;
+  const int ntile = (sd.count + 7) >> 3;
+  for (int rg = 0; rg < nrhs; rg += 16) {
+    const int rn = min(16, nrhs - rg);
+    __syncthreads();
+    for (int e = tid; e < 16 * kBlk; e += kGaThreads) {
+      const int q = e >> 9, k = e & (kBlk - 1);
+      double val = 0.0;
+      if (q < rn) {
+        int p0 = cd.cc[0] + (k >> 6), p1 = cd.cc[1] + ((k >> 3) & 7), p2 = cd.cc[2] + (k & 7);
+        if (p0 >= wd.box_w[0]) p0 -= wd.box_w[0];
+        if (p1 >= wd.box_w[1]) p1 -= wd.box_w[1];
+        if (p2 >= wd.box_w[2]) p2 -= wd.box_w[2];
+        val = grid[(int64_t)(rg + q) * grid_ld + wd.grid_off +
+                   ((int64_t)p0 * wd.box_w[1] + p1) * wd.box_w[2] + p2];
+      }
+      gb[q * kGRow + k] = val;
+    }
+    __syncthreads();
+    const double* G0 = gb + g * kGRow + t;
+    const double* G1 = G0 + 8 * kGRow;
+    const bool two = rn > 8;
+    for (int nt = warp; nt < ntile; nt += kGaWarps) {
+      const int j0 = nt * 8;
+      const int jn = j0 + g;
+      double bc[16], aw[8];
+      if (jn < sd.count) {
+        const double* r = rw + (int64_t)jn * kRow;
+        double bw[8];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const double2 x = __ldg(reinterpret_cast<const double2*>(r) + k);
+          aw[2 * k] = x.x;
+          aw[2 * k + 1] = x.y;
+          const double2 y = __ldg(reinterpret_cast<const double2*>(r + kS) + k);
+          bw[2 * k] = y.x;
+          bw[2 * k + 1] = y.y;
+        }
+        const double c0 = __ldg(r + 2 * kS + t), c1 = __ldg(r + 2 * kS + 4 + t);
+#pragma unroll
+        for (int ks = 0; ks < 16; ++ks) bc[ks] = bw[ks >> 1] * ((ks & 1) ? c1 : c0);
+      } else {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) aw[k] = 0.0;
+#pragma unroll
+        for (int ks = 0; ks < 16; ++ks) bc[ks] = 0.0;
+      }
+      double acc[2][4][2];
+#pragma unroll
+      for (int m = 0; m < 2; ++m)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[m][c][0] = acc[m][c][1] = 0.0;
+#pragma unroll
+      for (int a = 0; a < 8; ++a) {
+        const double wa = aw[a];
+#pragma unroll
+        for (int ks = 0; ks < 16; ++ks) {
+          const double w = bc[ks] * wa;
+          const int k = a * 64 + 4 * ks;
+          dmma(acc[0][ks & 3], G0[k], w);
+          if (two) dmma(acc[1][ks & 3], G1[k], w);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int j = j0 + 2 * t + i;
+        if (j >= sd.count) continue;
+        double* o = out + (int64_t)pix[sd.start + j] * nrhs + rg;
+#pragma unroll
+        for (int m = 0; m < 2; ++m) {
+          const int r = m * 8 + g;
+          if (r < rn)
+            o[r] = (acc[m][0][i] + acc[m][1][i]) + (acc[m][2][i] + acc[m][3][i]);
+        }
       }
     }
   }
