@@ -212,79 +212,87 @@ k_spread(const SubDev* __restrict__ subs, const WinDev* __restrict__ wins,
 
 // ---- assemble: grid point <- sum of the blocks of the cells covering it -----
 
-__global__ void k_assemble(const WinDev* __restrict__ wins, int L,
-                           const int2* __restrict__ cellinfo,
-                           const double* __restrict__ blocks, int nrhs,
-                           double* __restrict__ grid, int64_t grid_ld) {
-  // thread = (grid point, rhs) with rhs fastest: the cell lookups are shared
-  // across the rhs and the block reads ([block + e][nrhs]) are contiguous.
-  // Cells covering the point are visited in a fixed order (deterministic).
+// Assemble: grid point <- sum of the partial blocks of the cells covering it.
+// 8 lanes share one (grid point, rhs) and split the outermost offset axis;
+// their partial sums are combined by a fixed xor tree (deterministic, no
+// atomics).  Lane layout: lane = 8 * item + slice.
+__global__ void __launch_bounds__(256, 4)
+k_assemble(const WinDev* __restrict__ wins, int L, const int2* __restrict__ cellinfo,
+           const double* __restrict__ blocks, int nrhs, double* __restrict__ grid,
+           int64_t grid_ld) {
   const int w = blockIdx.y;
   const WinDev wd = wins[w];
   const int S = wd.S;
   const int d = wd.d;
-  const int64_t total = wd.box_size * nrhs;
   const int2* __restrict__ ci = cellinfo + wd.cellmap_off;
   const int on0 = d == 3 ? S : 1, on1 = d >= 2 ? S : 1;
   const int blk = on0 * on1 * S;
-  for (int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; id < total;
-       id += (int64_t)gridDim.x * blockDim.x) {
-    const int r = (int)(id % nrhs);
-    const int64_t e = id / nrhs;
-    double* __restrict__ g = grid + r * grid_ld + wd.grid_off;
-    if (!wd.fast) {
-      g[e] = 0.0;
-      continue;
-    }
-    // point coordinates mapped onto (t0, t1, t2) with unused leading dims 0
-    int t[3] = {0, 0, 0}, bw[3] = {1, 1, 1};
-    int64_t rem = e;
-    for (int s = 2; s >= 3 - d; --s) {
-      bw[s] = wd.box_w[s - (3 - d)];
-      t[s] = (int)(rem % bw[s]);
-      rem /= bw[s];
-    }
+  const int slice = threadIdx.x & 7;
+  const int64_t total = wd.box_size * nrhs;
+  const int64_t items_per_block = blockDim.x >> 3;
+  for (int64_t base = blockIdx.x * items_per_block; base < total;
+       base += (int64_t)gridDim.x * items_per_block) {
+    const int64_t id = base + (threadIdx.x >> 3);
+    const bool live = id < total;
+    const int r = live ? (int)(id % nrhs) : 0;
+    const int64_t e = live ? id / nrhs : 0;
     double sum = 0.0;
-    for (int o0 = 0; o0 < on0; ++o0) {
-      int c0 = t[0] - o0;
-      if (c0 < 0) {
-        if (!wd.wrap) break;
-        c0 += bw[0];
+    if (live && wd.fast) {
+      // point coordinates on (t0, t1, t2), unused leading dims 0
+      int t0 = 0, t1 = 0, t2, bw1 = 1, bw2;
+      if (d == 3) {
+        bw2 = wd.box_w[2];
+        bw1 = wd.box_w[1];
+        t2 = (int)(e % bw2);
+        t1 = (int)((e / bw2) % bw1);
+        t0 = (int)(e / ((int64_t)bw2 * bw1));
+      } else if (d == 2) {
+        bw2 = wd.box_w[1];
+        bw1 = wd.box_w[0];
+        t2 = (int)(e % bw2);
+        t1 = (int)(e / bw2);
+      } else {
+        bw2 = wd.box_w[0];
+        t2 = (int)e;
       }
-      for (int o1 = 0; o1 < on1; ++o1) {
-        int c1 = t[1] - o1;
-        if (c1 < 0) {
-          if (!wd.wrap) break;
-          c1 += bw[1];
-        }
-        const int64_t rowkey = ((int64_t)c0 * bw[1] + c1) * bw[2];
-        const int inner01 = (o0 * on1 + o1) * S;
-        if (S == 8 && !wd.wrap && t[2] >= 7) {
-          // common case: all 8 candidates in range; batch the lookups
-          int2 info[8];
-#pragma unroll
-          for (int o2 = 0; o2 < 8; ++o2) info[o2] = ci[rowkey + t[2] - o2];
-#pragma unroll
-          for (int o2 = 0; o2 < 8; ++o2) {
-            const int2 c = info[o2];
-            for (int q = 0; q < c.y; ++q)
-              sum += blocks[((int64_t)c.x + (int64_t)q * blk + inner01 + o2) * nrhs + r];
+      const int bw0 = d == 3 ? wd.box_w[0] : 1;
+      // the split axis: o0 for d = 3, o1 for d = 2, o2 for d = 1
+      for (int sp = slice; sp < S; sp += 8) {
+        const int o0s = d == 3 ? sp : 0, o0e = d == 3 ? sp + 1 : 1;
+        for (int o0 = o0s; o0 < o0e; ++o0) {
+          int c0 = t0 - o0;
+          if (c0 < 0) {
+            if (!wd.wrap) continue;
+            c0 += bw0;
           }
-        } else {
-          for (int o2 = 0; o2 < S; ++o2) {
-            int c2 = t[2] - o2;
-            if (c2 < 0) {
-              if (!wd.wrap) break;
-              c2 += bw[2];
+          const int o1s = d == 2 ? sp : 0, o1e = d == 3 ? on1 : (d == 2 ? sp + 1 : 1);
+          for (int o1 = o1s; o1 < o1e; ++o1) {
+            int c1 = t1 - o1;
+            if (c1 < 0) {
+              if (!wd.wrap) continue;
+              c1 += bw1;
             }
-            const int2 c = ci[rowkey + c2];
-            for (int q = 0; q < c.y; ++q)
-              sum += blocks[((int64_t)c.x + (int64_t)q * blk + inner01 + o2) * nrhs + r];
+            const int64_t rowkey = ((int64_t)c0 * bw1 + c1) * bw2;
+            const int inner01 = (o0 * on1 + o1) * S;
+            const int o2s = d == 1 ? sp : 0, o2e = d == 1 ? sp + 1 : S;
+            for (int o2 = o2s; o2 < o2e; ++o2) {
+              int c2 = t2 - o2;
+              if (c2 < 0) {
+                if (!wd.wrap) break;
+                c2 += bw2;
+              }
+              const int2 c = ci[rowkey + c2];
+              for (int q = 0; q < c.y; ++q)
+                sum += blocks[((int64_t)c.x + (int64_t)q * blk + inner01 + o2) * nrhs + r];
+            }
           }
         }
       }
     }
-    g[e] = sum;
+    sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+    sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+    sum += __shfl_xor_sync(0xffffffffu, sum, 4);
+    if (live && slice == 0) grid[r * grid_ld + wd.grid_off + e] = sum;
   }
 }
 
@@ -935,8 +943,8 @@ void apply_op(nld_operator* op, int which, int kind, const double* v, double* ou
   {
     int64_t maxbox = 1;
     for (const auto& w : ps.wdev_h) maxbox = std::max(maxbox, w.box_size);
-    dim3 grid(grid_blocks(maxbox * nrhs, 128, 2048), L);
-    k_assemble<<<grid, 128, 0, st>>>(ps.wdev, L, ps.cellinfo, ws.blocks, nrhs, ws.grid_in,
+    dim3 grid(grid_blocks(maxbox * nrhs, 32, 148 * 16), L);
+    k_assemble<<<grid, 256, 0, st>>>(ps.wdev, L, ps.cellinfo, ws.blocks, nrhs, ws.grid_in,
                                      ps.grid_total);
     NLD_CUDA(cudaGetLastError());
   }
