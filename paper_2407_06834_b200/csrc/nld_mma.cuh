@@ -249,37 +249,42 @@ k_gather_mma(const SubDev* __restrict__ subs, const CellDev* __restrict__ cells,
                ((int64_t)p0 * wd.box_w[1] + p1) * wd.box_w[2] + p2];
     }
     __syncthreads();
-    for (int nt = warp; nt < ntile; nt += kGaWarps) {
+    struct Tile {
+      double bw[8], c0, c1, aw[2];
+      int pj[2];
+    };
+    auto load_tile = [&](Tile& T, int nt) {
       const int j0 = nt * 8;
-      // (B (x) C) fragments of node j0 + g: k = 4 ks + t -> (b = ks/2, c = 4(ks&1) + t)
       const int jn = j0 + g;
-      double bf[16];
-      if (jn < sd.count) {
-        const double* r = rw + (int64_t)jn * kRow;
-        double bw[8];
+      const bool okn = jn < sd.count;
+      const double* r = rw + (int64_t)(okn ? jn : 0) * kRow;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const double2 x = __ldg(reinterpret_cast<const double2*>(r + kS) + k);
-          bw[2 * k] = x.x;
-          bw[2 * k + 1] = x.y;
-        }
-        const double c0 = __ldg(r + 2 * kS + t), c1 = __ldg(r + 2 * kS + 4 + t);
-#pragma unroll
-        for (int ks = 0; ks < 16; ++ks) bf[ks] = bw[ks >> 1] * ((ks & 1) ? c1 : c0);
-      } else {
-#pragma unroll
-        for (int ks = 0; ks < 16; ++ks) bf[ks] = 0.0;
+      for (int k = 0; k < 4; ++k) {
+        const double2 x = __ldg(reinterpret_cast<const double2*>(r + kS) + k);
+        T.bw[2 * k] = okn ? x.x : 0.0;
+        T.bw[2 * k + 1] = okn ? x.y : 0.0;
       }
-      // A weight of the two output nodes j0 + 2t + i at row a = g
-      double aw[2];
-      int jp[2], pj[2] = {0, 0};
+      T.c0 = __ldg(r + 2 * kS + t);
+      T.c1 = __ldg(r + 2 * kS + 4 + t);
 #pragma unroll
       for (int i = 0; i < 2; ++i) {
-        jp[i] = j0 + 2 * t + i;
-        const bool ok = jp[i] < sd.count;
-        aw[i] = ok ? __ldg(rw + (int64_t)jp[i] * kRow + g) : 0.0;
-        if (ok && g == 0) pj[i] = pix[sd.start + jp[i]];
+        const int j = j0 + 2 * t + i;
+        const bool ok = j < sd.count;
+        T.aw[i] = ok ? __ldg(rw + (int64_t)j * kRow + g) : 0.0;
+        T.pj[i] = (ok && g == 0) ? __ldg(pix + sd.start + j) : 0;
       }
+    };
+    Tile cur, nxt;
+    if (warp < ntile) load_tile(cur, warp);
+    for (int nt = warp; nt < ntile; nt += kGaWarps) {
+      if (nt + kGaWarps < ntile) load_tile(nxt, nt + kGaWarps);
+      const int j0 = nt * 8;
+      double bf[16];
+#pragma unroll
+      for (int ks = 0; ks < 16; ++ks) bf[ks] = cur.bw[ks >> 1] * ((ks & 1) ? cur.c1 : cur.c0);
+      const double aw[2] = {cur.aw[0], cur.aw[1]};
+      int jp[2] = {j0 + 2 * t, j0 + 2 * t + 1};
+      const int pj[2] = {cur.pj[0], cur.pj[1]};
       const int gsw = 4 * g;
       auto finish = [&](const double (&acc)[4][2], int q) {
         double p[2];
@@ -323,6 +328,7 @@ k_gather_mma(const SubDev* __restrict__ subs, const CellDev* __restrict__ cells,
         for (int ks = 0; ks < 16; ++ks) dmma(a0[ks & 3], G0[(4 * ks + t) ^ gsw], bf[ks]);
         finish(a0, q);
       }
+      cur = nxt;
     }
   }
 }
