@@ -191,6 +191,9 @@ NLD_API int nld_probe_fp64(int64_t iters, int32_t blocks, double* tflops,
 /* the same for the fp64 tensor path (mma.sync m8n8k4 f64, DMMA). */
 NLD_API int nld_probe_dmma(int64_t iters, int32_t blocks, double* tflops,
                            double* ms, void* stream);
+/* half the warps DMMA, half DFMA: do the two fp64 paths share resources? */
+NLD_API int nld_probe_mixed(int64_t iters_mma, int64_t iters_fma, double* tflops,
+                            double* ms, void* stream);
 
 #ifdef __cplusplus
 }

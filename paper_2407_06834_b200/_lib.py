@@ -91,6 +91,7 @@ SIGNATURES = {
     "nld_dot": (ctypes.c_int, [_P, _P, _I64, _PD, _P]),
     "nld_probe_fp64": (ctypes.c_int, [_I64, _I32, _PD, _PD, _P]),
     "nld_probe_dmma": (ctypes.c_int, [_I64, _I32, _PD, _PD, _P]),
+    "nld_probe_mixed": (ctypes.c_int, [_I64, _I64, _PD, _PD, _P]),
 }
 
 
