@@ -183,6 +183,42 @@ NLD_API int nld_axpby(double a, const double* x, double b, const double* y,
 NLD_API int nld_dot(const double* x, const double* y, int64_t n, double* result,
             void* stream);
 
+/* ---- general transforms (transform.py:74-333) ------------------------------
+ * An NFFT plan is an nld_operator in raw-torus mode over n nodes of dimension d
+ * (device, row-major) mapped by (p - center) * scale (center may be NULL = 0;
+ * check_torus != 0 raises NLD_ERR_SCALING if a mapped node leaves
+ * [-1/2, 1/2)^d as map_to_torus does, transform.py:310-317).  Bandwidth M is
+ * the same in every dimension (even); the grid is n = 2 ceil(os M / 2).
+ * Complex arrays are interleaved (re, im) fp64, coefficients C-order over
+ * k = -M/2 .. M/2-1 per dimension.  Destroy with nld_op_destroy. */
+NLD_API int nld_nfft_create(const double* nodes_dev, int64_t n, int32_t d,
+                            int32_t bandwidth, double oversampling, int32_t cutoff,
+                            const double* center, double scale, int32_t check_torus,
+                            void* stream, nld_operator** out);
+/* nfft_adjoint (transform.py:215-223): coeffs = deconv(ifftn(spread(values))
+ * * prod(nos)), optionally times a real multiplier (kernel coefficients). */
+NLD_API int nld_nfft_adjoint(nld_operator* plan, const double* values, double* coeffs,
+                             const double* mult, void* stream);
+/* nfft (transform.py:200-212): values = gather(fftn(embed(deconv(coeffs)))). */
+NLD_API int nld_nfft_trafo(nld_operator* plan, const double* coeffs, double* values,
+                           void* stream);
+/* ndft / ndft_adjoint (transform.py:74-102), exact O(n M^d). */
+NLD_API int nld_ndft(const double* nodes, int64_t n, int32_t d, int32_t bandwidth,
+                     const double* in, double* out, int32_t adjoint, void* stream);
+/* gauss_transform_direct (transform.py:231-244), exact. */
+NLD_API int nld_gauss_direct(const double* targets, int64_t nt, const double* sources,
+                             int64_t ns, int32_t d, const double* alpha, double sigbar,
+                             double* out, void* stream);
+/* FastsumPlan.build pieces (transform.py:292-307): bounding-box centre and
+ * scale (HOST outputs), and kernel_coeffs (device, M^d real). */
+NLD_API int nld_fastsum_geometry(const double* points, int64_t n, int32_t d, double rmax,
+                                 double* center_host, double* scale_host, void* stream);
+NLD_API int nld_gauss_coeffs(int32_t bandwidth, int32_t d, double sig_scaled, double* out,
+                             void* stream);
+/* NfftPlan.window_factors (transform.py:140-145), HOST output of M values. */
+NLD_API int nld_window_factors(int32_t bandwidth, int32_t grid, int32_t cutoff,
+                               double* out_host);
+
 /* fp64 FMA throughput probe (the roofline denominator of the FMA-bound
  * spread/gather kernels): 8 independent DFMA chains per thread, `iters`
  * steps, `blocks` x 256 threads (<= 0: 8 per SM).  HOST outputs. */

@@ -14,6 +14,9 @@ from .kernel import AnovaOperator
 from .linops import (DeflatingBasis, ShiftedSystem, SolveResult,
                      deflated_solve, deflated_solve_batched, pcg, plain_solve,
                      scs_down, scs_up)
+from .transform import (FastsumPlan, NfftPlan, NodeSet, expansion_degree,
+                        gauss_transform_direct, gauss_transform_fast, ndft,
+                        ndft_adjoint, nfft, nfft_adjoint)
 
 __version__ = "0.1.0"
 
@@ -23,4 +26,7 @@ __all__ = [
     "ScalingOverflowError", "ShiftedSystem", "SolveResult",
     "SolverBreakdownError", "WindowSizeError", "deflated_solve",
     "deflated_solve_batched", "pcg", "plain_solve", "scs_down", "scs_up",
+    "FastsumPlan", "NfftPlan", "NodeSet", "expansion_degree",
+    "gauss_transform_direct", "gauss_transform_fast", "ndft", "ndft_adjoint",
+    "nfft", "nfft_adjoint",
 ]

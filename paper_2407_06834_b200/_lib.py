@@ -89,6 +89,15 @@ SIGNATURES = {
     "nld_scs": (ctypes.c_int, [_P, _P, _I64, _I32, _P]),
     "nld_axpby": (ctypes.c_int, [_D, _P, _D, _P, _P, _I64, _P]),
     "nld_dot": (ctypes.c_int, [_P, _P, _I64, _PD, _P]),
+    "nld_nfft_create": (ctypes.c_int, [_P, _I64, _I32, _I32, _D, _I32, _PD, _D, _I32, _P,
+                                       ctypes.POINTER(_P)]),
+    "nld_nfft_adjoint": (ctypes.c_int, [_P, _P, _P, _P, _P]),
+    "nld_nfft_trafo": (ctypes.c_int, [_P, _P, _P, _P]),
+    "nld_ndft": (ctypes.c_int, [_P, _I64, _I32, _I32, _P, _P, _I32, _P]),
+    "nld_gauss_direct": (ctypes.c_int, [_P, _I64, _P, _I64, _I32, _P, _D, _P, _P]),
+    "nld_fastsum_geometry": (ctypes.c_int, [_P, _I64, _I32, _D, _PD, _PD, _P]),
+    "nld_gauss_coeffs": (ctypes.c_int, [_I32, _I32, _D, _P, _P]),
+    "nld_window_factors": (ctypes.c_int, [_I32, _I32, _I32, _PD]),
     "nld_probe_fp64": (ctypes.c_int, [_I64, _I32, _PD, _PD, _P]),
     "nld_probe_dmma": (ctypes.c_int, [_I64, _I32, _PD, _PD, _P]),
     "nld_probe_mixed": (ctypes.c_int, [_I64, _I64, _PD, _PD, _P]),

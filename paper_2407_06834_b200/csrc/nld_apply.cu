@@ -315,14 +315,14 @@ __device__ __forceinline__ bool edge_combo(const EdgeDev& ed, int d, int W, int 
 
 __global__ void k_spread_edges(const EdgeDev* __restrict__ edges, int64_t ne,
                                const WinDev* __restrict__ wins,
-                               const double* __restrict__ v, int64_t ldv,
+                               const double* __restrict__ vt, int nrhs,
                                double* __restrict__ grid, int64_t grid_ld) {
   const int rhs = blockIdx.y;
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < ne;
        k += (int64_t)gridDim.x * blockDim.x) {
     const EdgeDev& ed = edges[k];
     const WinDev wd = wins[ed.win];
-    const double val = v[rhs * ldv + ed.pix];
+    const double val = vt[(int64_t)ed.pix * nrhs + rhs];
     const int W = wd.S + 2;
     int total = 1;
     for (int s = 0; s < wd.d; ++s) total *= W;
@@ -372,7 +372,7 @@ __global__ void k_spread_generic(const WinDev* __restrict__ wins, int w,
                                  const double* __restrict__ rows,
                                  const int32_t* __restrict__ pix,
                                  const int32_t* __restrict__ key,
-                                 const double* __restrict__ v, int64_t ldv,
+                                 const double* __restrict__ vt, int nrhs,
                                  double* __restrict__ grid, int64_t grid_ld, int64_t N) {
   const int rhs = blockIdx.y;
   const WinDev wd = wins[w];
@@ -380,7 +380,7 @@ __global__ void k_spread_generic(const WinDev* __restrict__ wins, int w,
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < N;
        e += (int64_t)gridDim.x * blockDim.x) {
     const double* row = rows + wd.row_off + e * (int64_t)S * d;
-    const double val = v[rhs * ldv + pix[wd.node_off + e]];
+    const double val = vt[(int64_t)pix[wd.node_off + e] * nrhs + rhs];
     int cc[3] = {0, 0, 0};
     int rem = key[wd.node_off + e];
     for (int s = d - 1; s >= 0; --s) {
@@ -909,6 +909,88 @@ void free_workspace(Workspace& ws) {
   ws = Workspace();
 }
 
+// spread of all windows into the support boxes ws.grid_in [nrhs][grid_total]
+// (block path + assemble + generic/edge atomics + the shard allreduce).
+// vt: right-hand sides pixel-major [N][nrhs].
+static int spread_stage_impl(nld_operator* op, const PlanSet& ps, const double* vt, int nrhs,
+                             cudaStream_t st, EvScope* ev) {
+  Workspace& ws = op->ws;
+  const int64_t N = op->N;
+  const int L = (int)ps.wdev_h.size();
+  int launches = 0;
+  switch (op->params.cutoff) {
+    case 3: spread_all<3>(ps, ws, vt, nrhs, st); break;
+    case 4: spread_all<4>(ps, ws, vt, nrhs, st); break;
+    case 5: spread_all<5>(ps, ws, vt, nrhs, st); break;
+    default: break;
+  }
+  for (int g = 1; g <= kMaxDim; ++g) launches += ps.n_subs[g] ? 1 : 0;
+  if (ev) ev->mark();
+  {
+    int64_t maxbox = 1;
+    for (const auto& w : ps.wdev_h) maxbox = std::max(maxbox, w.box_size);
+    dim3 grid(grid_blocks(maxbox * nrhs, 32, 148 * 16), L);
+    k_assemble<<<grid, 256, 0, st>>>(ps.wdev, L, ps.cellinfo, ws.blocks, nrhs, ws.grid_in,
+                                     ps.grid_total);
+    NLD_CUDA(cudaGetLastError());
+    ++launches;
+  }
+  for (int w = 0; w < L; ++w) {
+    if (ps.wdev_h[w].fast) continue;
+    dim3 grid(grid_blocks(N, 256), nrhs);
+    k_spread_generic<<<grid, 256, 0, st>>>(ps.wdev, w, ps.rows, ps.pix, ps.key, vt, nrhs,
+                                           ws.grid_in, ps.grid_total, N);
+    NLD_CUDA(cudaGetLastError());
+    ++launches;
+  }
+  if (ps.n_edges) {
+    dim3 grid(grid_blocks(ps.n_edges, 128), nrhs);
+    k_spread_edges<<<grid, 128, 0, st>>>(ps.edges, ps.n_edges, ps.wdev, vt, nrhs, ws.grid_in,
+                                         ps.grid_total);
+    NLD_CUDA(cudaGetLastError());
+    ++launches;
+  }
+  // pixel shards: sum the support-box grids of every rank (SURVEY §8e)
+  comm_device(op, ws.grid_in, ps.grid_total * nrhs, st);
+  return launches;
+}
+
+int spread_stage(nld_operator* op, const PlanSet& ps, const double* vt, int nrhs,
+                 cudaStream_t st) {
+  return spread_stage_impl(op, ps, vt, nrhs, st, nullptr);
+}
+
+// gather of all windows from ws.grid_out into ws.wout [L][N][nrhs]
+int gather_stage(nld_operator* op, const PlanSet& ps, int nrhs, cudaStream_t st) {
+  Workspace& ws = op->ws;
+  const int64_t N = op->N;
+  const int L = (int)ps.wdev_h.size();
+  int launches = 0;
+  switch (op->params.cutoff) {
+    case 3: gather_all<3>(ps, ws, N, nrhs, st); break;
+    case 4: gather_all<4>(ps, ws, N, nrhs, st); break;
+    case 5: gather_all<5>(ps, ws, N, nrhs, st); break;
+    default: break;
+  }
+  for (int g = 1; g <= kMaxDim; ++g) launches += ps.n_subs[g] ? 1 : 0;
+  for (int w = 0; w < L; ++w) {
+    if (ps.wdev_h[w].fast) continue;
+    dim3 grid(grid_blocks(N, 256), nrhs);
+    k_gather_generic<<<grid, 256, 0, st>>>(ps.wdev, w, nrhs, ps.rows, ps.pix, ps.key,
+                                           ws.grid_out, ps.grid_total, ws.wout, N);
+    NLD_CUDA(cudaGetLastError());
+    ++launches;
+  }
+  if (ps.n_edges) {
+    dim3 grid(grid_blocks(ps.n_edges, 128), nrhs);
+    k_gather_edges<<<grid, 128, 0, st>>>(ps.edges, ps.n_edges, ps.wdev, ws.grid_out,
+                                         ps.grid_total, ws.wout, N, nrhs);
+    NLD_CUDA(cudaGetLastError());
+    ++launches;
+  }
+  return launches;
+}
+
 void apply_op(nld_operator* op, int which, int kind, const double* v, double* out,
               int nrhs, int64_t ld, const double* coef_dev, const double* eta,
               cudaStream_t st) {
@@ -917,12 +999,10 @@ void apply_op(nld_operator* op, int which, int kind, const double* v, double* ou
   Workspace& ws = op->ws;
   const int64_t N = op->N;
   const int L = op->L;
-  const int m = op->params.cutoff;
   EvScope ev(op, st);
   ev.mark();
   int launches = 0;
-  for (int g = 1; g <= kMaxDim; ++g) launches += ps.n_subs[g] ? 2 : 0;  // spread + gather
-  // 0. pixel-major copy of the rhs for the node gathers (nrhs > 1)
+  // 0. pixel-major copy of the rhs for the node gathers
   const double* vt = v;
   if (nrhs > 1 || ld != N) {
     k_transpose_in<<<grid_blocks(N, kTileP, 148 * 16), 256,
@@ -931,39 +1011,8 @@ void apply_op(nld_operator* op, int which, int kind, const double* v, double* ou
     vt = ws.vt;
     ++launches;
   }
-  // 1. spread (block path)
-  switch (m) {
-    case 3: spread_all<3>(ps, ws, vt, nrhs, st); break;
-    case 4: spread_all<4>(ps, ws, vt, nrhs, st); break;
-    case 5: spread_all<5>(ps, ws, vt, nrhs, st); break;
-    default: break;
-  }
-  ev.mark();
-  // 2. assemble the support boxes
-  {
-    int64_t maxbox = 1;
-    for (const auto& w : ps.wdev_h) maxbox = std::max(maxbox, w.box_size);
-    dim3 grid(grid_blocks(maxbox * nrhs, 32, 148 * 16), L);
-    k_assemble<<<grid, 256, 0, st>>>(ps.wdev, L, ps.cellinfo, ws.blocks, nrhs, ws.grid_in,
-                                     ps.grid_total);
-    NLD_CUDA(cudaGetLastError());
-  }
-  // generic windows + edge nodes (atomics on top of the assembled boxes)
-  for (int w = 0; w < L; ++w) {
-    if (ps.wdev_h[w].fast) continue;
-    dim3 grid(grid_blocks(N, 256), nrhs);
-    k_spread_generic<<<grid, 256, 0, st>>>(ps.wdev, w, ps.rows, ps.pix, ps.key, v, ld,
-                                           ws.grid_in, ps.grid_total, N);
-    NLD_CUDA(cudaGetLastError());
-  }
-  if (ps.n_edges) {
-    dim3 grid(grid_blocks(ps.n_edges, 128), nrhs);
-    k_spread_edges<<<grid, 128, 0, st>>>(ps.edges, ps.n_edges, ps.wdev, v, ld, ws.grid_in,
-                                         ps.grid_total);
-    NLD_CUDA(cudaGetLastError());
-  }
-  // pixel shards: sum the support-box grids of every rank (SURVEY §8e)
-  comm_device(op, ws.grid_in, ps.grid_total * nrhs, st);
+  // 1-2. spread + assemble (+ shard allreduce)
+  launches += spread_stage_impl(op, ps, vt, nrhs, st, &ev);
   ev.mark();
   // 3. separable convolution, one pass per axis
   {
@@ -980,29 +1029,12 @@ void apply_op(nld_operator* op, int which, int kind, const double* v, double* ou
       k_conv<<<grid, 128, 0, st>>>(ps.wdev, pass, ps.K, ws.grid_in, cin, cout, ws.grid_out,
                                    ps.grid_total);
       NLD_CUDA(cudaGetLastError());
+      ++launches;
     }
   }
   ev.mark();
   // 4. gather
-  switch (m) {
-    case 3: gather_all<3>(ps, ws, N, nrhs, st); break;
-    case 4: gather_all<4>(ps, ws, N, nrhs, st); break;
-    case 5: gather_all<5>(ps, ws, N, nrhs, st); break;
-    default: break;
-  }
-  for (int w = 0; w < L; ++w) {
-    if (ps.wdev_h[w].fast) continue;
-    dim3 grid(grid_blocks(N, 256), nrhs);
-    k_gather_generic<<<grid, 256, 0, st>>>(ps.wdev, w, nrhs, ps.rows, ps.pix, ps.key,
-                                           ws.grid_out, ps.grid_total, ws.wout, N);
-    NLD_CUDA(cudaGetLastError());
-  }
-  if (ps.n_edges) {
-    dim3 grid(grid_blocks(ps.n_edges, 128), nrhs);
-    k_gather_edges<<<grid, 128, 0, st>>>(ps.edges, ps.n_edges, ps.wdev, ws.grid_out,
-                                         ps.grid_total, ws.wout, N, nrhs);
-    NLD_CUDA(cudaGetLastError());
-  }
+  launches += gather_stage(op, ps, nrhs, st);
   ev.mark();
   // 5. epilogue
   {
@@ -1018,17 +1050,9 @@ void apply_op(nld_operator* op, int which, int kind, const double* v, double* ou
                                                                  0, out, ld, eta, coef_dev);
     }
     NLD_CUDA(cudaGetLastError());
+    ++launches;
   }
   ev.mark();
-  {
-    int maxd = 0, generic = 0;
-    for (const auto& w : ps.wdev_h) {
-      maxd = std::max(maxd, w.d);
-      generic += w.fast ? 0 : 2;
-    }
-    launches += 1 /*assemble*/ + maxd /*conv*/ + 1 /*epilogue*/ + generic +
-                (ps.n_edges ? 2 : 0);
-  }
   op->stats.launches = launches;
 }
 

@@ -171,6 +171,12 @@ struct nld_operator {
   bool events = false;
   std::mutex build_mu;           // lazy plan build (per operator: shards may
                                  // build concurrently in one process)
+  // raw-torus plans (NFFT transform API): nodes used as given after the
+  // affine map (p - raw_center) * raw_scale, no bounding-box scaling
+  int raw = 0;
+  int raw_check = 0;             // ScalingOverflowError if |q| >= 1/2
+  double raw_center[3] = {0, 0, 0};
+  double raw_scale = 1.0;
 };
 
 namespace nld {
@@ -184,6 +190,11 @@ void free_workspace(Workspace& ws);
 void apply_op(nld_operator* op, int which, int kind, const double* v,
               double* out, int nrhs, int64_t ld, const double* coef_dev,
               const double* eta, cudaStream_t st);
+
+// the two halves of a product, reused by the NFFT transform API
+int spread_stage(nld_operator* op, const PlanSet& ps, const double* vt, int nrhs,
+                 cudaStream_t st);
+int gather_stage(nld_operator* op, const PlanSet& ps, int nrhs, cudaStream_t st);
 
 void dense_apply(nld_operator* op, int which, int kind, const double* v,
                  double* out, int nrhs, int64_t ld, const double* coef_dev,
@@ -206,6 +217,8 @@ void dev_basis(const double* v, const double* x, double* out, int64_t n,
                int adjoint, cudaStream_t st);
 
 int64_t expansion_degree(double sig_scaled, double eps);
+void point_geometry(const double* F, int64_t N, int d, double rmax, double* center,
+                    double* scale, cudaStream_t st);
 
 // collective helpers (no-ops without a comm hook)
 enum { RED_F64 = 0, RED_I32 = 1 };

@@ -117,6 +117,7 @@ struct TorusMap {
   int m;
   double b;        // KB shape
   double b_pi;     // b / pi
+  int check;       // raise ScalingOverflowError for |q| >= 1/2
 };
 
 __device__ __forceinline__ double torus_x(const TorusMap& t, double p, int s) {
@@ -145,7 +146,7 @@ __global__ void k_bases(const double* __restrict__ F, int64_t N, int D,
        j += (int64_t)gridDim.x * blockDim.x) {
     for (int s = 0; s < d; ++s) {
       double q = torus_x(tm, F[j * D + c[s]], s);
-      if (!(fabs(q) < 0.5)) atomicOr(flags, 1);   // ScalingOverflowError
+      if (tm.check && !(fabs(q) < 0.5)) atomicOr(flags, 1);   // ScalingOverflowError
       double xs = __dmul_rn(q, tm.nf);
       long long lo = (long long)floor(xs) - tm.m;
       base[j * 3 + s] = (int32_t)lo;
@@ -390,6 +391,38 @@ int64_t expansion_degree(double sig_scaled, double eps) {
   return std::min<int64_t>(n, 192);
 }
 
+// FastsumPlan.build geometry (transform.py:292-296): centre of the bounding
+// box and scale = rmax / max radius, for an (n, d) point set
+void point_geometry(const double* F, int64_t N, int d, double rmax, double* center,
+                    double* scale, cudaStream_t st) {
+  const int nb = kRedBlocks;
+  TmpBuf part(sizeof(double) * nb * 6, st);
+  std::vector<double> hpart(nb * 6);
+  int3 cols = make_int3(0, d > 1 ? 1 : 0, d > 2 ? 2 : 0);
+  k_minmax<<<nb, kRedThreads, 0, st>>>(F, N, d, cols, d, part.as<double>());
+  NLD_CUDA(cudaMemcpyAsync(hpart.data(), part.p, sizeof(double) * nb * 6,
+                           cudaMemcpyDeviceToHost, st));
+  NLD_CUDA(cudaStreamSynchronize(st));
+  for (int s = 0; s < d; ++s) {
+    double lo = INFINITY, hi = -INFINITY;
+    for (int k = 0; k < nb; ++k) {
+      lo = std::min(lo, hpart[k * 6 + s]);
+      hi = std::max(hi, hpart[k * 6 + 3 + s]);
+    }
+    center[s] = 0.5 * (lo + hi);
+  }
+  k_radius2<<<nb, kRedThreads, 0, st>>>(F, N, d, cols, d,
+                                        make_double3(center[0], d > 1 ? center[1] : 0.0,
+                                                     d > 2 ? center[2] : 0.0),
+                                        part.as<double>());
+  NLD_CUDA(cudaMemcpyAsync(hpart.data(), part.p, sizeof(double) * nb, cudaMemcpyDeviceToHost,
+                           st));
+  NLD_CUDA(cudaStreamSynchronize(st));
+  double r2 = 0.0;
+  for (int k = 0; k < nb; ++k) r2 = std::max(r2, hpart[k]);
+  *scale = rmax / std::max(std::sqrt(r2), 1e-30);
+}
+
 static bool window_fast(int d, int m) {
   return (m >= 3 && m <= 5) && d >= 1 && d <= 3;
 }
@@ -415,6 +448,11 @@ void build_planset(nld_operator* op, int which, cudaStream_t st) {
     wp.d = op->win_offset[w + 1] - op->win_offset[w];
     for (int s = 0; s < wp.d; ++s) wp.cols[s] = op->win_index[op->win_offset[w] + s];
     int3 cols = make_int3(wp.cols[0], wp.cols[1], wp.cols[2]);
+    if (op->raw) {
+      for (int s = 0; s < wp.d; ++s) wp.center[s] = op->raw_center[s];
+      wp.scale = op->raw_scale;
+      wp.sig_scaled = 0.0;
+    } else {
     k_minmax<<<nb, kRedThreads, 0, st>>>(op->feats, N, op->D, cols, wp.d,
                                          part.as<double>());
     NLD_CUDA(cudaMemcpyAsync(hpart.data(), part.p, sizeof(double) * nb * 6,
@@ -443,6 +481,7 @@ void build_planset(nld_operator* op, int which, cudaStream_t st) {
     double radius = std::sqrt(r2);
     wp.scale = P.rmax / std::max(radius, 1e-30);
     wp.sig_scaled = ps.sigbar / (wp.scale * wp.scale);
+    }
     int64_t M = P.n_expansion > 0 ? P.n_expansion
                                   : expansion_degree(wp.sig_scaled, P.truncation_eps);
     if (M % 2) throw Error(NLD_ERR_VALUE, "expansion degree must be even");
@@ -560,6 +599,7 @@ void build_planset(nld_operator* op, int which, cudaStream_t st) {
     tm.m = m;
     tm.b = wp.b;
     tm.b_pi = wp.b / 3.141592653589793;
+    tm.check = op->raw ? op->raw_check : 1;
     NLD_CUDA(cudaMemsetAsync(flags.p, 0, sizeof(int) * 8, st));
     int nbk = blocks_for(N);
     k_bases<<<nbk, 256, 0, st>>>(op->feats, N, op->D, cols, wp.d, tm,

@@ -86,3 +86,37 @@ def test_generator_is_deterministic():
 def test_alpha_sweep():
     al = synth.alpha_sweep(100.0, 16)
     assert al.size == 16 and np.isclose(al[0], 0.01) and np.isclose(al[-1], 1.0)
+
+
+class TestTransformValidation:
+    """transform.py validation (no GPU needed)."""
+
+    def test_plan_rules(self):
+        from paper_2407_06834_b200 import transform as T
+        with pytest.raises(ValueError):
+            T.NfftPlan((15,))
+        with pytest.raises(ValueError):
+            T.NfftPlan((16,), oversampling=1.0)
+        with pytest.raises(ValueError):
+            T.NfftPlan((16,), cutoff=0)
+        plan = T.NfftPlan((32, 32), oversampling=2.0, cutoff=4)
+        assert plan.nos == (64, 64) and plan.dim == 2
+        assert abs(plan._shape_b[0] - 1.5 * np.pi) < 1e-15
+
+    def test_nodes_rules(self):
+        from paper_2407_06834_b200 import transform as T
+        with pytest.raises(nld.DimensionMismatchError):
+            T.NodeSet(np.zeros((3, 4)))
+        with pytest.raises(ValueError):
+            T.NodeSet(np.array([0.5]))
+        ns = T.NodeSet(np.array([[0.0, 0.1], [-0.5, 0.49]]))
+        assert ns.dim == 2 and len(ns) == 2
+
+    def test_expansion_degree(self):
+        from oracle import nfft_oracle as O
+        from paper_2407_06834_b200 import transform as T
+        assert T.expansion_degree(1.0) == 16
+        assert T.expansion_degree(1000.0) > T.expansion_degree(100.0)
+        assert T.expansion_degree(1e9) == T.MAX_EXPANSION
+        for s in (0.5, 3.0, 250.77, 1e4):
+            assert T.expansion_degree(s) == O.expansion_degree(s)
