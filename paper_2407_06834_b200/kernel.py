@@ -151,6 +151,51 @@ class AnovaOperator:
                                self.n, cptr, dv.stream_of(self.device)))
         return out
 
+    def apply_pipelined(self, kind: int, inputs, outputs, nrhs: int = 1,
+                        coef=None):
+        """Host -> device -> host products for a sequence of batches.
+
+        ``inputs`` / ``outputs`` are equal-length sequences of pinned host
+        torch tensors of shape (nrhs, n).  Batch k's host->device copy, the
+        product of batch k-1 and the device->host copy of batch k-2 run
+        concurrently on three streams with double-buffered device buffers,
+        so PCIe traffic hides behind the kernels.  Returns after the last
+        result is on the host.
+        """
+        dev = self.device
+        cur = torch.cuda.current_stream(dev)
+        s_in, s_cmp, s_out = (torch.cuda.Stream(dev) for _ in range(3))
+        for s_ in (s_in, s_cmp, s_out):
+            s_.wait_stream(cur)
+        shape = (nrhs, self.n) if nrhs > 1 else (self.n,)
+        vd = [torch.empty(shape, dtype=torch.float64, device=dev) for _ in range(2)]
+        yd = [torch.empty(shape, dtype=torch.float64, device=dev) for _ in range(2)]
+        done_cmp = [None, None]      # compute finished with vd[b] / wrote yd[b]
+        done_out = [None, None]      # yd[b] copied out
+        for k, (xh, yh) in enumerate(zip(inputs, outputs)):
+            b = k & 1
+            with torch.cuda.stream(s_in):
+                if done_cmp[b] is not None:
+                    s_in.wait_event(done_cmp[b])
+                vd[b].copy_(xh, non_blocking=True)
+                ev_in = torch.cuda.Event()
+                ev_in.record(s_in)
+            with torch.cuda.stream(s_cmp):
+                s_cmp.wait_event(ev_in)
+                if done_out[b] is not None:
+                    s_cmp.wait_event(done_out[b])
+                self.apply_device(vd[b], kind, nrhs, coef, out=yd[b])
+                done_cmp[b] = torch.cuda.Event()
+                done_cmp[b].record(s_cmp)
+            with torch.cuda.stream(s_out):
+                s_out.wait_event(done_cmp[b])
+                yh.copy_(yd[b], non_blocking=True)
+                done_out[b] = torch.cuda.Event()
+                done_out[b].record(s_out)
+        for s_ in (s_in, s_cmp, s_out):
+            cur.wait_stream(s_)
+        torch.cuda.synchronize(dev)
+
     def _product(self, v, kind, coef=None):
         x, nrhs = self._vectors(v)
         out = self.apply_device(x, kind, nrhs, coef)
