@@ -138,6 +138,17 @@ int nld_op_create(const double* features_dev, int64_t n, int32_t n_features,
       throw Error(NLD_ERR_VALUE, "too many nodes for 32-bit node indices");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     select_device_of(features_dev, 0);
+    {
+      // keep stream-ordered temporaries cached instead of returning them to
+      // the OS at every synchronisation
+      int dev = 0;
+      cudaMemPool_t pool;
+      if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+      }
+      cudaGetLastError();
+    }
     auto* op = new nld_operator();
     try {
       NLD_CUDA(cudaGetDevice(&op->device));

@@ -880,7 +880,12 @@ void ensure_workspace(nld_operator* op, const PlanSet& ps, int nrhs) {
   if (ws.nrhs_cap >= nrhs && ws.grid_total >= ps.grid_total &&
       ws.blocks_total >= ps.blocks_total)
     return;
+  double* keep_cg = ws.cg;
+  int64_t keep_cap = ws.cg_cap;
+  ws.cg = nullptr;
   free_workspace(ws);
+  ws.cg = keep_cg;
+  ws.cg_cap = keep_cap;
   int cap = std::max(nrhs, 1);
   int64_t gt = std::max(ps.grid_total, std::max(op->sets[0].grid_total, op->sets[1].grid_total));
   int64_t bt = std::max(ps.blocks_total, std::max(op->sets[0].blocks_total, op->sets[1].blocks_total));
@@ -898,6 +903,7 @@ void ensure_workspace(nld_operator* op, const PlanSet& ps, int nrhs) {
 }
 
 void free_workspace(Workspace& ws) {
+  cudaFree(ws.cg);
   cudaFree(ws.blocks);
   cudaFree(ws.grid_in);
   cudaFree(ws.grid_out);

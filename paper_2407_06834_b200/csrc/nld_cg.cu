@@ -439,13 +439,21 @@ void cg_solve(nld_operator* op, const double* f, double* u, int nrhs, int64_t ld
   }
 
   const int64_t V = N * nrhs;
+  // persistent per-operator CG vectors (a solve per image/alpha batch reuses them)
+  if (op->ws.cg_cap < V) {
+    NLD_CUDA(cudaStreamSynchronize(st));
+    cudaFree(op->ws.cg);
+    op->ws.cg = nullptr;
+    NLD_CUDA(cudaMalloc(&op->ws.cg, sizeof(double) * 6 * V));
+    op->ws.cg_cap = V;
+  }
   CgPtr c{};
-  NLD_CUDA(cudaMallocAsync(&c.x, sizeof(double) * V, st));
-  NLD_CUDA(cudaMallocAsync(&c.r, sizeof(double) * V, st));
-  NLD_CUDA(cudaMallocAsync(&c.p, sizeof(double) * V, st));
-  NLD_CUDA(cudaMallocAsync(&c.q, sizeof(double) * V, st));
-  NLD_CUDA(cudaMallocAsync(&c.b, sizeof(double) * V, st));
-  NLD_CUDA(cudaMallocAsync(&c.t, sizeof(double) * V, st));
+  c.x = op->ws.cg;
+  c.r = c.x + op->ws.cg_cap;
+  c.p = c.r + op->ws.cg_cap;
+  c.q = c.p + op->ws.cg_cap;
+  c.b = c.q + op->ws.cg_cap;
+  c.t = c.b + op->ws.cg_cap;
   c.f = f;
   c.eta = eta;
   c.eta2 = eta2;
@@ -652,12 +660,6 @@ void cg_solve(nld_operator* op, const double* f, double* u, int nrhs, int64_t ld
             k < (int)H[r].size() ? H[r][k] : std::numeric_limits<double>::quiet_NaN();
     }
   }
-  cudaFreeAsync(c.x, st);
-  cudaFreeAsync(c.r, st);
-  cudaFreeAsync(c.p, st);
-  cudaFreeAsync(c.q, st);
-  cudaFreeAsync(c.b, st);
-  cudaFreeAsync(c.t, st);
   cudaFreeAsync(scd, st);
   cudaFreeAsync(coef, st);
   if (eta2) cudaFreeAsync(eta2, st);

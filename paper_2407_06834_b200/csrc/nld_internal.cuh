@@ -144,6 +144,9 @@ struct Workspace {
   double* vt = nullptr;          // [N][nrhs] pixel-major rhs
   double* coef = nullptr;        // [nrhs][2]
   int64_t grid_total = 0, blocks_total = 0;
+  // persistent CG vectors (x, r, p, q, b, t): [6][cg_cap]
+  double* cg = nullptr;
+  int64_t cg_cap = 0;
 };
 
 }  // namespace nld
