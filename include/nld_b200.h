@@ -219,6 +219,19 @@ NLD_API int nld_gauss_coeffs(int32_t bandwidth, int32_t d, double sig_scaled, do
 NLD_API int nld_window_factors(int32_t bandwidth, int32_t grid, int32_t cutoff,
                                double* out_host);
 
+/* ---- feature / window preparation (features.py:20-104) ------------------
+ * image: device, channel-planar [channels][h][w] fp64.  out: device
+ * (h*w, channels*patch^2), columns channel-major then raster patch order,
+ * value a * (v - b); mode 0 pads with zeros (the reference, a=1, b=0),
+ * mode 1 reflects (BASELINE's generator, a=0.4, b=0.5). */
+NLD_API int nld_extract_patches(const double* image, int64_t h, int64_t w, int32_t channels,
+                                int32_t patch, int32_t mode, double a, double b,
+                                double* out, void* stream);
+/* plug-in mutual information (nats) of every column with column `center`,
+ * 16 x 16 equal-width bins over each column's range; HOST output of d. */
+NLD_API int nld_mi_scores(const double* features, int64_t n, int32_t d, int32_t center,
+                          double* scores_host, void* stream);
+
 /* fp64 FMA throughput probe (the roofline denominator of the FMA-bound
  * spread/gather kernels): 8 independent DFMA chains per thread, `iters`
  * steps, `blocks` x 256 threads (<= 0: 8 per SM).  HOST outputs. */

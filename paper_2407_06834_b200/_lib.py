@@ -98,6 +98,8 @@ SIGNATURES = {
     "nld_fastsum_geometry": (ctypes.c_int, [_P, _I64, _I32, _D, _PD, _PD, _P]),
     "nld_gauss_coeffs": (ctypes.c_int, [_I32, _I32, _D, _P, _P]),
     "nld_window_factors": (ctypes.c_int, [_I32, _I32, _I32, _PD]),
+    "nld_extract_patches": (ctypes.c_int, [_P, _I64, _I64, _I32, _I32, _I32, _D, _D, _P, _P]),
+    "nld_mi_scores": (ctypes.c_int, [_P, _I64, _I32, _I32, _PD, _P]),
     "nld_probe_fp64": (ctypes.c_int, [_I64, _I32, _PD, _PD, _P]),
     "nld_probe_dmma": (ctypes.c_int, [_I64, _I32, _PD, _PD, _P]),
     "nld_probe_mixed": (ctypes.c_int, [_I64, _I64, _PD, _PD, _P]),
