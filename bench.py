@@ -203,12 +203,19 @@ def run_ours(args, world, rank, local):
     import paper_2407_06834_b200 as nld
     from paper_2407_06834_b200 import _lib, sharding, synth
 
+    # NLD_TEST_SHARED_GPU=1: every rank on cuda:0 over gloo -- a functional
+    # check of the sharded flow on a one-GPU box (numbers meaningless)
+    shared = os.environ.get("NLD_TEST_SHARED_GPU", "") not in ("", "0")
+    local = 0 if shared else local
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     pg = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
         pg = dist
     cfg = synth.CONFIGS[args.config]
     nrhs = args.nrhs or cfg.n_alpha

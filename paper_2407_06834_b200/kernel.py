@@ -167,7 +167,12 @@ class AnovaOperator:
         s_in, s_cmp, s_out = (torch.cuda.Stream(dev) for _ in range(3))
         for s_ in (s_in, s_cmp, s_out):
             s_.wait_stream(cur)
-        shape = (nrhs, self.n) if nrhs > 1 else (self.n,)
+        inputs, outputs = list(inputs), list(outputs)
+        if not inputs:
+            return
+        shape = tuple(inputs[0].shape)
+        if shape not in ((nrhs, self.n), (self.n,) if nrhs == 1 else (nrhs, self.n)):
+            raise DimensionMismatchError(f"batch shape {shape} != ({nrhs}, {self.n})")
         vd = [torch.empty(shape, dtype=torch.float64, device=dev) for _ in range(2)]
         yd = [torch.empty(shape, dtype=torch.float64, device=dev) for _ in range(2)]
         done_cmp = [None, None]      # compute finished with vd[b] / wrote yd[b]
