@@ -186,6 +186,15 @@ int nld_op_destroy(nld_operator* op) {
     cudaFree(op->feats);
     if (op->events)
       for (auto& e : op->ev) cudaEventDestroy(e);
+    if (op->aux) {
+      for (int w = 0; w < op->aux_windows; ++w) {
+        cudaEventDestroy(op->ev_spread[w]);
+        cudaEventDestroy(op->ev_conv[w]);
+      }
+      cudaEventDestroy(op->ev_fork);
+      cudaEventDestroy(op->ev_join);
+      cudaStreamDestroy(op->aux);
+    }
     delete op;
   });
 }

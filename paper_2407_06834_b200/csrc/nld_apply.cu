@@ -217,10 +217,10 @@ k_spread(const SubDev* __restrict__ subs, const WinDev* __restrict__ wins,
 // their partial sums are combined by a fixed xor tree (deterministic, no
 // atomics).  Lane layout: lane = 8 * item + slice.
 __global__ void __launch_bounds__(256, 4)
-k_assemble(const WinDev* __restrict__ wins, int L, const int2* __restrict__ cellinfo,
+k_assemble(const WinDev* __restrict__ wins, int w0, const int2* __restrict__ cellinfo,
            const double* __restrict__ blocks, int nrhs, double* __restrict__ grid,
            int64_t grid_ld) {
-  const int w = blockIdx.y;
+  const int w = w0 + blockIdx.y;
   const WinDev wd = wins[w];
   const int S = wd.S;
   const int d = wd.d;
@@ -293,6 +293,93 @@ k_assemble(const WinDev* __restrict__ wins, int L, const int2* __restrict__ cell
     sum += __shfl_xor_sync(0xffffffffu, sum, 2);
     sum += __shfl_xor_sync(0xffffffffu, sum, 4);
     if (live && slice == 0) grid[r * grid_ld + wd.grid_off + e] = sum;
+  }
+}
+
+// ---- separable assemble (d = 3, S = 8, no wrap) ----------------------------
+// G[p] = sum_{o in [0,8)^3} X[p - o][o], X[c][o] = sum of the cell's sub
+// blocks.  Three passes, one per offset axis, each summing 8 terms in a fixed
+// order (deterministic):
+//   Y1[c0][c1][p2][o0][o1] = sum_o2 X[c0][c1][p2-o2][o0][o1][o2]
+//   Y2[c0][p1][p2][o0]     = sum_o1 Y1[c0][p1-o1][p2][o0][o1]
+//   G[p0][p1][p2]          = sum_o0 Y2[p0-o0][p1][p2][o0]
+// (all with the rhs index innermost: [..][nrhs]).
+__global__ void __launch_bounds__(256)
+k_asm_p1(const WinDev* __restrict__ wins, int w, const int2* __restrict__ cellinfo,
+         const double* __restrict__ blocks, int nrhs, double* __restrict__ y1) {
+  const WinDev wd = wins[w];
+  const int B0 = wd.box_w[0], B1 = wd.box_w[1], B2 = wd.box_w[2];
+  const int2* __restrict__ ci = cellinfo + wd.cellmap_off;
+  const int64_t total = (int64_t)B0 * B1 * B2 * 64 * nrhs;
+  for (int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; id < total;
+       id += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(id % nrhs);
+    int64_t rest = id / nrhs;
+    const int o01 = (int)(rest & 63);
+    rest >>= 6;
+    const int p2 = (int)(rest % B2);
+    const int64_t row = rest / B2;            // c0 * B1 + c1
+    double sum = 0.0;
+#pragma unroll
+    for (int o2 = 0; o2 < 8; ++o2) {
+      const int c2 = p2 - o2;
+      if (c2 < 0) break;
+      const int2 c = ci[row * B2 + c2];
+      for (int q = 0; q < c.y; ++q)
+        sum += blocks[((int64_t)c.x + (int64_t)q * 512 + o01 * 8 + o2) * nrhs + r];
+    }
+    y1[id] = sum;
+  }
+}
+
+__global__ void __launch_bounds__(256)
+k_asm_p2(const WinDev* __restrict__ wins, int w, const double* __restrict__ y1, int nrhs,
+         double* __restrict__ y2) {
+  const WinDev wd = wins[w];
+  const int B0 = wd.box_w[0], B1 = wd.box_w[1], B2 = wd.box_w[2];
+  const int64_t total = (int64_t)B0 * B1 * B2 * 8 * nrhs;
+  for (int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; id < total;
+       id += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(id % nrhs);
+    int64_t rest = id / nrhs;
+    const int o0 = (int)(rest & 7);
+    rest >>= 3;
+    const int p2 = (int)(rest % B2);
+    rest /= B2;
+    const int p1 = (int)(rest % B1);
+    const int c0 = (int)(rest / B1);
+    double sum = 0.0;
+#pragma unroll
+    for (int o1 = 0; o1 < 8; ++o1) {
+      const int c1 = p1 - o1;
+      if (c1 < 0) break;
+      sum += y1[(((((int64_t)c0 * B1 + c1) * B2 + p2) * 64) + o0 * 8 + o1) * nrhs + r];
+    }
+    y2[id] = sum;
+  }
+}
+
+__global__ void __launch_bounds__(256)
+k_asm_p3(const WinDev* __restrict__ wins, int w, const double* __restrict__ y2, int nrhs,
+         double* __restrict__ grid, int64_t grid_ld) {
+  const WinDev wd = wins[w];
+  const int B1 = wd.box_w[1], B2 = wd.box_w[2];
+  const int64_t total = wd.box_size * nrhs;
+  for (int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; id < total;
+       id += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(id % nrhs);
+    const int64_t e = id / nrhs;
+    const int p2 = (int)(e % B2);
+    const int p1 = (int)((e / B2) % B1);
+    const int p0 = (int)(e / ((int64_t)B2 * B1));
+    double sum = 0.0;
+#pragma unroll
+    for (int o0 = 0; o0 < 8; ++o0) {
+      const int c0 = p0 - o0;
+      if (c0 < 0) break;
+      sum += y2[((((int64_t)c0 * B1 + p1) * B2 + p2) * 8 + o0) * nrhs + r];
+    }
+    grid[r * grid_ld + wd.grid_off + e] = sum;
   }
 }
 
@@ -449,12 +536,12 @@ __global__ void k_gather_generic(const WinDev* __restrict__ wins, int w, int nrh
 
 // ---- separable convolution pass --------------------------------------------
 
-__global__ void k_conv(const WinDev* __restrict__ wins, int pass,
+__global__ void k_conv(const WinDev* __restrict__ wins, int w0, int pass,
                        const double2* __restrict__ K,
                        const double* __restrict__ gin, const double2* __restrict__ cin,
                        double2* __restrict__ cout, double* __restrict__ gout,
                        int64_t grid_ld) {
-  const int w = blockIdx.y;
+  const int w = w0 + blockIdx.y;
   const int rhs = blockIdx.z;
   const WinDev wd = wins[w];
   if (pass >= wd.d) return;
@@ -758,11 +845,12 @@ bool use_mma() {
   return v == 1;
 }
 
+// ---- per-window launchers -----------------------------------------------
+
 template <int D, int MC>
-void launch_spread(const PlanSet& ps, const Workspace& ws, const double* vt, int nrhs,
-                   cudaStream_t st) {
+void launch_spread(const SubDev* subs, unsigned nsub, const PlanSet& ps, const Workspace& ws,
+                   const double* vt, int nrhs, cudaStream_t st) {
   using G = Geo<D, MC>;
-  if (ps.n_subs[D] == 0) return;
   size_t smem = sizeof(double) * G::SMEM;
   static bool attr = false;
   if (!attr) {
@@ -770,16 +858,15 @@ void launch_spread(const PlanSet& ps, const Workspace& ws, const double* vt, int
                                   (int)smem));
     attr = true;
   }
-  k_spread<D, MC><<<(unsigned)ps.n_subs[D], kSpreadThreads, smem, st>>>(
-      ps.subs[D], ps.wdev, ps.rows, ps.pix, vt, nrhs, ws.blocks);
+  k_spread<D, MC><<<nsub, kSpreadThreads, smem, st>>>(subs, ps.wdev, ps.rows, ps.pix, vt, nrhs,
+                                                      ws.blocks);
   NLD_CUDA(cudaGetLastError());
 }
 
 template <int D, int MC>
-void launch_gather(const PlanSet& ps, const Workspace& ws, int64_t N, int nrhs,
-                   cudaStream_t st) {
+void launch_gather(const SubDev* subs, unsigned nsub, const PlanSet& ps, const Workspace& ws,
+                   int64_t N, int nrhs, cudaStream_t st) {
   using G = Geo<D, MC>;
-  if (ps.n_subs[D] == 0) return;
   size_t smem = sizeof(double) * G::BLK * std::min(nrhs, G::GRB);
   static bool attr = false;
   if (!attr) {
@@ -787,15 +874,14 @@ void launch_gather(const PlanSet& ps, const Workspace& ws, int64_t N, int nrhs,
                                   (int)(sizeof(double) * G::BLK * G::GRB)));
     attr = true;
   }
-  k_gather<D, MC><<<(unsigned)ps.n_subs[D], kThreads, smem, st>>>(
-      ps.subs[D], ps.cells, ps.wdev, ps.rows, ps.pix, ws.grid_out, ps.grid_total, ws.wout, N,
-      nrhs);
+  k_gather<D, MC><<<nsub, kThreads, smem, st>>>(subs, ps.cells, ps.wdev, ps.rows, ps.pix,
+                                                ws.grid_out, ps.grid_total, ws.wout, N, nrhs);
   NLD_CUDA(cudaGetLastError());
 }
 
 template <int RPW>
-void launch_spread_mma(const PlanSet& ps, const Workspace& ws, const double* vt, int nrhs,
-                       cudaStream_t st) {
+void launch_spread_mma(const SubDev* subs, unsigned nsub, const PlanSet& ps,
+                       const Workspace& ws, const double* vt, int nrhs, cudaStream_t st) {
   const int rpp = std::min(nrhs, mma::kSpWarps * RPW);
   const size_t smem = sizeof(double) * mma::spread_smem(rpp);
   static bool attr = false;
@@ -805,36 +891,13 @@ void launch_spread_mma(const PlanSet& ps, const Workspace& ws, const double* vt,
                                   (int)(sizeof(double) * mma::spread_smem(mma::kSpWarps * RPW))));
     attr = true;
   }
-  mma::k_spread_mma<RPW><<<(unsigned)ps.n_subs[3], mma::kSpThreads, smem, st>>>(
-      ps.subs[3], ps.wdev, ps.rows, ps.pix, vt, nrhs, ws.blocks);
+  mma::k_spread_mma<RPW><<<nsub, mma::kSpThreads, smem, st>>>(subs, ps.wdev, ps.rows, ps.pix,
+                                                              vt, nrhs, ws.blocks);
   NLD_CUDA(cudaGetLastError());
 }
 
-template <int MC>
-void spread_all(const PlanSet& ps, const Workspace& ws, const double* vt, int nrhs,
-                cudaStream_t st) {
-  launch_spread<1, MC>(ps, ws, vt, nrhs, st);
-  launch_spread<2, MC>(ps, ws, vt, nrhs, st);
-  if (MC == 4 && use_mma() && ps.n_subs[3]) {
-    if (nrhs >= 16) {
-      launch_spread_mma<2>(ps, ws, vt, nrhs, st);
-    } else {
-      launch_spread_mma<1>(ps, ws, vt, nrhs, st);
-    }
-  } else {
-    launch_spread<3, MC>(ps, ws, vt, nrhs, st);
-  }
-}
-
-void launch_gather_mma(const PlanSet& ps, const Workspace& ws, int64_t N, int nrhs,
-                       cudaStream_t st) {
-  const size_t smem = sizeof(double) * mma::kBlk * std::min(nrhs, mma::kGaRhs);
-  static bool attr = false;
-  if (!attr) {
-    NLD_CUDA(cudaFuncSetAttribute(mma::k_gather_mma, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)(sizeof(double) * mma::kBlk * mma::kGaRhs)));
-    attr = true;
-  }
+void launch_gather_mma(const SubDev* subs, unsigned nsub, const PlanSet& ps,
+                       const Workspace& ws, int64_t N, int nrhs, cudaStream_t st) {
   if (nrhs >= 8) {
     const size_t smem16 = sizeof(double) * 16 * mma::kGRow;
     static bool attr16 = false;
@@ -843,24 +906,53 @@ void launch_gather_mma(const PlanSet& ps, const Workspace& ws, int64_t N, int nr
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem16));
       attr16 = true;
     }
-    mma::k_gather_mma16<<<(unsigned)ps.n_subs[3], mma::kGaThreads, smem16, st>>>(
-        ps.subs[3], ps.cells, ps.wdev, ps.rows, ps.pix, ws.grid_out, ps.grid_total, ws.wout, N,
-        nrhs);
+    mma::k_gather_mma16<<<nsub, mma::kGaThreads, smem16, st>>>(
+        subs, ps.cells, ps.wdev, ps.rows, ps.pix, ws.grid_out, ps.grid_total, ws.wout, N, nrhs);
   } else {
-    mma::k_gather_mma<<<(unsigned)ps.n_subs[3], mma::kGaThreads, smem, st>>>(
-        ps.subs[3], ps.cells, ps.wdev, ps.rows, ps.pix, ws.grid_out, ps.grid_total, ws.wout, N,
-        nrhs);
+    const size_t smem = sizeof(double) * mma::kBlk * std::min(nrhs, mma::kGaRhs);
+    static bool attr = false;
+    if (!attr) {
+      NLD_CUDA(cudaFuncSetAttribute(mma::k_gather_mma,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)(sizeof(double) * mma::kBlk * mma::kGaRhs)));
+      attr = true;
+    }
+    mma::k_gather_mma<<<nsub, mma::kGaThreads, smem, st>>>(
+        subs, ps.cells, ps.wdev, ps.rows, ps.pix, ws.grid_out, ps.grid_total, ws.wout, N, nrhs);
   }
   NLD_CUDA(cudaGetLastError());
 }
 
 template <int MC>
-void gather_all(const PlanSet& ps, const Workspace& ws, int64_t N, int nrhs,
-                cudaStream_t st) {
-  launch_gather<1, MC>(ps, ws, N, nrhs, st);
-  launch_gather<2, MC>(ps, ws, N, nrhs, st);
-  if (MC == 4 && use_mma() && ps.n_subs[3]) launch_gather_mma(ps, ws, N, nrhs, st);
-  else launch_gather<3, MC>(ps, ws, N, nrhs, st);
+void spread_window_fast(const PlanSet& ps, const Workspace& ws, int w, const double* vt,
+                        int nrhs, cudaStream_t st) {
+  const WinPlan& wp = ps.win[w];
+  if (!ps.wdev_h[w].fast || wp.n_subs == 0) return;
+  const SubDev* subs = ps.subs[wp.d] + wp.sub_off;
+  const unsigned nsub = (unsigned)wp.n_subs;
+  if (wp.d == 1) {
+    launch_spread<1, MC>(subs, nsub, ps, ws, vt, nrhs, st);
+  } else if (wp.d == 2) {
+    launch_spread<2, MC>(subs, nsub, ps, ws, vt, nrhs, st);
+  } else if (MC == 4 && use_mma()) {
+    if (nrhs >= 16) launch_spread_mma<2>(subs, nsub, ps, ws, vt, nrhs, st);
+    else launch_spread_mma<1>(subs, nsub, ps, ws, vt, nrhs, st);
+  } else {
+    launch_spread<3, MC>(subs, nsub, ps, ws, vt, nrhs, st);
+  }
+}
+
+template <int MC>
+void gather_window_fast(const PlanSet& ps, const Workspace& ws, int w, int64_t N, int nrhs,
+                        cudaStream_t st) {
+  const WinPlan& wp = ps.win[w];
+  if (!ps.wdev_h[w].fast || wp.n_subs == 0) return;
+  const SubDev* subs = ps.subs[wp.d] + wp.sub_off;
+  const unsigned nsub = (unsigned)wp.n_subs;
+  if (wp.d == 1) launch_gather<1, MC>(subs, nsub, ps, ws, N, nrhs, st);
+  else if (wp.d == 2) launch_gather<2, MC>(subs, nsub, ps, ws, N, nrhs, st);
+  else if (MC == 4 && use_mma()) launch_gather_mma(subs, nsub, ps, ws, N, nrhs, st);
+  else launch_gather<3, MC>(subs, nsub, ps, ws, N, nrhs, st);
 }
 
 struct EvScope {
@@ -897,12 +989,28 @@ void ensure_workspace(nld_operator* op, const PlanSet& ps, int nrhs) {
   NLD_CUDA(cudaMalloc(&ws.wout, sizeof(double) * std::max<int64_t>(1, op->N * op->L) * cap));
   NLD_CUDA(cudaMalloc(&ws.vt, sizeof(double) * std::max<int64_t>(1, op->N) * cap));
   NLD_CUDA(cudaMalloc(&ws.coef, sizeof(double) * 2 * cap));
+  {
+    // separable-assemble scratch: the largest 3-D box x 64 offsets x nrhs
+    int64_t mb = 0;
+    for (int k = 0; k < 2; ++k)
+      for (const auto& w : op->sets[k].wdev_h)
+        if (w.d == 3) mb = std::max(mb, w.box_size);
+    for (const auto& w : ps.wdev_h)
+      if (w.d == 3) mb = std::max(mb, w.box_size);
+    ws.asm_cap = mb * 64 * cap;
+    if (ws.asm_cap) {
+      NLD_CUDA(cudaMalloc(&ws.asm_y1, sizeof(double) * ws.asm_cap));
+      NLD_CUDA(cudaMalloc(&ws.asm_y2, sizeof(double) * (ws.asm_cap / 8 + 1)));
+    }
+  }
   ws.nrhs_cap = cap;
   ws.grid_total = gt;
   ws.blocks_total = bt;
 }
 
 void free_workspace(Workspace& ws) {
+  cudaFree(ws.asm_y1);
+  cudaFree(ws.asm_y2);
   cudaFree(ws.cg);
   cudaFree(ws.blocks);
   cudaFree(ws.grid_in);
@@ -915,86 +1023,123 @@ void free_workspace(Workspace& ws) {
   ws = Workspace();
 }
 
-// spread of all windows into the support boxes ws.grid_in [nrhs][grid_total]
-// (block path + assemble + generic/edge atomics + the shard allreduce).
-// vt: right-hand sides pixel-major [N][nrhs].
-static int spread_stage_impl(nld_operator* op, const PlanSet& ps, const double* vt, int nrhs,
-                             cudaStream_t st, EvScope* ev) {
-  Workspace& ws = op->ws;
-  const int64_t N = op->N;
-  const int L = (int)ps.wdev_h.size();
-  int launches = 0;
+// ---- per-window stages ------------------------------------------------------
+
+// spread of window w (block path) -- main stream
+static void spread_window(nld_operator* op, const PlanSet& ps, int w, const double* vt,
+                          int nrhs, cudaStream_t st) {
   switch (op->params.cutoff) {
-    case 3: spread_all<3>(ps, ws, vt, nrhs, st); break;
-    case 4: spread_all<4>(ps, ws, vt, nrhs, st); break;
-    case 5: spread_all<5>(ps, ws, vt, nrhs, st); break;
+    case 3: spread_window_fast<3>(ps, op->ws, w, vt, nrhs, st); break;
+    case 4: spread_window_fast<4>(ps, op->ws, w, vt, nrhs, st); break;
+    case 5: spread_window_fast<5>(ps, op->ws, w, vt, nrhs, st); break;
     default: break;
   }
-  for (int g = 1; g <= kMaxDim; ++g) launches += ps.n_subs[g] ? 1 : 0;
-  if (ev) ev->mark();
-  {
-    int64_t maxbox = 1;
-    for (const auto& w : ps.wdev_h) maxbox = std::max(maxbox, w.box_size);
-    dim3 grid(grid_blocks(maxbox * nrhs, 32, 148 * 16), L);
-    k_assemble<<<grid, 256, 0, st>>>(ps.wdev, L, ps.cellinfo, ws.blocks, nrhs, ws.grid_in,
+}
+
+// assemble of window w + its generic/edge atomics (writes ws.grid_in)
+static void assemble_window(nld_operator* op, const PlanSet& ps, int w, const double* vt,
+                            int nrhs, cudaStream_t st) {
+  Workspace& ws = op->ws;
+  const WinDev& wd = ps.wdev_h[w];
+  const WinPlan& wp = ps.win[w];
+  const int64_t y1n = wd.box_size * 64 * nrhs;
+  if (wd.fast && wd.d == 3 && wd.S == 8 && !wd.wrap && ws.asm_cap >= y1n) {
+    k_asm_p1<<<grid_blocks(y1n, 256, 148 * 32), 256, 0, st>>>(ps.wdev, w, ps.cellinfo,
+                                                              ws.blocks, nrhs, ws.asm_y1);
+    k_asm_p2<<<grid_blocks(y1n / 8, 256, 148 * 32), 256, 0, st>>>(ps.wdev, w, ws.asm_y1, nrhs,
+                                                                  ws.asm_y2);
+    k_asm_p3<<<grid_blocks(y1n / 64, 256, 148 * 32), 256, 0, st>>>(ps.wdev, w, ws.asm_y2, nrhs,
+                                                                   ws.grid_in, ps.grid_total);
+  } else {
+    dim3 grid(grid_blocks(wd.box_size * nrhs, 32, 148 * 16), 1);
+    k_assemble<<<grid, 256, 0, st>>>(ps.wdev, w, ps.cellinfo, ws.blocks, nrhs, ws.grid_in,
                                      ps.grid_total);
-    NLD_CUDA(cudaGetLastError());
-    ++launches;
   }
-  for (int w = 0; w < L; ++w) {
-    if (ps.wdev_h[w].fast) continue;
-    dim3 grid(grid_blocks(N, 256), nrhs);
-    k_spread_generic<<<grid, 256, 0, st>>>(ps.wdev, w, ps.rows, ps.pix, ps.key, vt, nrhs,
-                                           ws.grid_in, ps.grid_total, N);
+  NLD_CUDA(cudaGetLastError());
+  if (!wd.fast) {
+    dim3 g2(grid_blocks(op->N, 256), nrhs);
+    k_spread_generic<<<g2, 256, 0, st>>>(ps.wdev, w, ps.rows, ps.pix, ps.key, vt, nrhs,
+                                         ws.grid_in, ps.grid_total, op->N);
     NLD_CUDA(cudaGetLastError());
-    ++launches;
   }
-  if (ps.n_edges) {
-    dim3 grid(grid_blocks(ps.n_edges, 128), nrhs);
-    k_spread_edges<<<grid, 128, 0, st>>>(ps.edges, ps.n_edges, ps.wdev, vt, nrhs, ws.grid_in,
-                                         ps.grid_total);
+  if (wp.n_edge) {
+    dim3 g3(grid_blocks(wp.n_edge, 128), nrhs);
+    k_spread_edges<<<g3, 128, 0, st>>>(ps.edges + wp.edge_off, wp.n_edge, ps.wdev, vt, nrhs,
+                                       ws.grid_in, ps.grid_total);
     NLD_CUDA(cudaGetLastError());
-    ++launches;
   }
-  // pixel shards: sum the support-box grids of every rank
-  comm_device(op, ws.grid_in, ps.grid_total * nrhs, st);
-  return launches;
 }
 
-int spread_stage(nld_operator* op, const PlanSet& ps, const double* vt, int nrhs,
-                 cudaStream_t st) {
-  return spread_stage_impl(op, ps, vt, nrhs, st, nullptr);
+// separable convolution of window w: grid_in -> grid_out
+static void conv_window(nld_operator* op, const PlanSet& ps, int w, int nrhs, cudaStream_t st) {
+  Workspace& ws = op->ws;
+  const WinDev& wd = ps.wdev_h[w];
+  for (int pass = 0; pass < wd.d; ++pass) {
+    dim3 grid(grid_blocks(wd.box_size, 128, 1024), 1, nrhs);
+    const double2* cin = (pass % 2 == 1) ? ws.cbuf0 : ws.cbuf1;
+    double2* cout = (pass % 2 == 0) ? ws.cbuf0 : ws.cbuf1;
+    k_conv<<<grid, 128, 0, st>>>(ps.wdev, w, pass, ps.K, ws.grid_in, cin, cout, ws.grid_out,
+                                 ps.grid_total);
+    NLD_CUDA(cudaGetLastError());
+  }
 }
 
-// gather of all windows from ws.grid_out into ws.wout [L][N][nrhs]
-int gather_stage(nld_operator* op, const PlanSet& ps, int nrhs, cudaStream_t st) {
+// gather of window w from ws.grid_out into ws.wout (+ generic/edges)
+static void gather_window(nld_operator* op, const PlanSet& ps, int w, int nrhs,
+                          cudaStream_t st) {
   Workspace& ws = op->ws;
   const int64_t N = op->N;
-  const int L = (int)ps.wdev_h.size();
-  int launches = 0;
   switch (op->params.cutoff) {
-    case 3: gather_all<3>(ps, ws, N, nrhs, st); break;
-    case 4: gather_all<4>(ps, ws, N, nrhs, st); break;
-    case 5: gather_all<5>(ps, ws, N, nrhs, st); break;
+    case 3: gather_window_fast<3>(ps, ws, w, N, nrhs, st); break;
+    case 4: gather_window_fast<4>(ps, ws, w, N, nrhs, st); break;
+    case 5: gather_window_fast<5>(ps, ws, w, N, nrhs, st); break;
     default: break;
   }
-  for (int g = 1; g <= kMaxDim; ++g) launches += ps.n_subs[g] ? 1 : 0;
-  for (int w = 0; w < L; ++w) {
-    if (ps.wdev_h[w].fast) continue;
+  const WinDev& wd = ps.wdev_h[w];
+  const WinPlan& wp = ps.win[w];
+  if (!wd.fast) {
     dim3 grid(grid_blocks(N, 256), nrhs);
     k_gather_generic<<<grid, 256, 0, st>>>(ps.wdev, w, nrhs, ps.rows, ps.pix, ps.key,
                                            ws.grid_out, ps.grid_total, ws.wout, N);
     NLD_CUDA(cudaGetLastError());
-    ++launches;
   }
-  if (ps.n_edges) {
-    dim3 grid(grid_blocks(ps.n_edges, 128), nrhs);
-    k_gather_edges<<<grid, 128, 0, st>>>(ps.edges, ps.n_edges, ps.wdev, ws.grid_out,
-                                         ps.grid_total, ws.wout, N, nrhs);
+  if (wp.n_edge) {
+    dim3 grid(grid_blocks(wp.n_edge, 128), nrhs);
+    k_gather_edges<<<grid, 128, 0, st>>>(ps.edges + wp.edge_off, wp.n_edge, ps.wdev,
+                                         ws.grid_out, ps.grid_total, ws.wout, N, nrhs);
     NLD_CUDA(cudaGetLastError());
-    ++launches;
   }
-  return launches;
+}
+
+// spread of all windows into the support boxes ws.grid_in [nrhs][grid_total]
+// (+ the shard allreduce).  vt: right-hand sides pixel-major [N][nrhs].
+int spread_stage(nld_operator* op, const PlanSet& ps, const double* vt, int nrhs,
+                 cudaStream_t st) {
+  const int L = (int)ps.wdev_h.size();
+  for (int w = 0; w < L; ++w) spread_window(op, ps, w, vt, nrhs, st);
+  for (int w = 0; w < L; ++w) assemble_window(op, ps, w, vt, nrhs, st);
+  comm_device(op, op->ws.grid_in, ps.grid_total * nrhs, st);
+  return 2 * L;
+}
+
+int gather_stage(nld_operator* op, const PlanSet& ps, int nrhs, cudaStream_t st) {
+  const int L = (int)ps.wdev_h.size();
+  for (int w = 0; w < L; ++w) gather_window(op, ps, w, nrhs, st);
+  return L;
+}
+
+static void ensure_aux(nld_operator* op, int L) {
+  if (op->aux && op->aux_windows >= L) return;
+  if (!op->aux) {
+    NLD_CUDA(cudaStreamCreateWithFlags(&op->aux, cudaStreamNonBlocking));
+    NLD_CUDA(cudaEventCreateWithFlags(&op->ev_fork, cudaEventDisableTiming));
+    NLD_CUDA(cudaEventCreateWithFlags(&op->ev_join, cudaEventDisableTiming));
+  }
+  for (int w = op->aux_windows; w < L; ++w) {
+    NLD_CUDA(cudaEventCreateWithFlags(&op->ev_spread[w], cudaEventDisableTiming));
+    NLD_CUDA(cudaEventCreateWithFlags(&op->ev_conv[w], cudaEventDisableTiming));
+  }
+  op->aux_windows = L;
 }
 
 void apply_op(nld_operator* op, int which, int kind, const double* v, double* out,
@@ -1017,30 +1162,41 @@ void apply_op(nld_operator* op, int which, int kind, const double* v, double* ou
     vt = ws.vt;
     ++launches;
   }
-  // 1-2. spread + assemble (+ shard allreduce)
-  launches += spread_stage_impl(op, ps, vt, nrhs, st, &ev);
-  ev.mark();
-  // 3. separable convolution, one pass per axis
-  {
-    int maxd = 0;
-    int64_t maxbox = 1;
-    for (const auto& w : ps.wdev_h) {
-      maxd = std::max(maxd, w.d);
-      maxbox = std::max(maxbox, w.box_size);
+  const bool overlap = !op->comm && L <= 16;
+  if (overlap) {
+    // window w's assemble + convolution (latency / L2 bound) run on the aux
+    // stream while the main stream spreads window w+1 and, later, gathers
+    // the earlier windows (fp64 tensor bound)
+    ensure_aux(op, L);
+    for (int w = 0; w < L; ++w) {
+      spread_window(op, ps, w, vt, nrhs, st);
+      NLD_CUDA(cudaEventRecord(op->ev_spread[w], st));
+      NLD_CUDA(cudaStreamWaitEvent(op->aux, op->ev_spread[w], 0));
+      assemble_window(op, ps, w, vt, nrhs, op->aux);
+      conv_window(op, ps, w, nrhs, op->aux);
+      NLD_CUDA(cudaEventRecord(op->ev_conv[w], op->aux));
     }
-    for (int pass = 0; pass < maxd; ++pass) {
-      dim3 grid(grid_blocks(maxbox, 128, 1024), L, nrhs);
-      const double2* cin = (pass % 2 == 1) ? ws.cbuf0 : ws.cbuf1;
-      double2* cout = (pass % 2 == 0) ? ws.cbuf0 : ws.cbuf1;
-      k_conv<<<grid, 128, 0, st>>>(ps.wdev, pass, ps.K, ws.grid_in, cin, cout, ws.grid_out,
-                                   ps.grid_total);
-      NLD_CUDA(cudaGetLastError());
-      ++launches;
+    ev.mark();
+    NLD_CUDA(cudaStreamWaitEvent(st, op->ev_conv[0], 0));
+    ev.mark();
+    ev.mark();
+    for (int w = 0; w < L; ++w) {
+      if (w > 0) NLD_CUDA(cudaStreamWaitEvent(st, op->ev_conv[w], 0));
+      gather_window(op, ps, w, nrhs, st);
     }
+  } else {
+    spread_stage(op, ps, vt, nrhs, st);
+    ev.mark();
+    ev.mark();
+    for (int w = 0; w < L; ++w) conv_window(op, ps, w, nrhs, st);
+    ev.mark();
+    gather_stage(op, ps, nrhs, st);
   }
-  ev.mark();
-  // 4. gather
-  launches += gather_stage(op, ps, nrhs, st);
+  for (int w = 0; w < L; ++w) {
+    const WinDev& wd = ps.wdev_h[w];
+    launches += (wd.fast && ps.win[w].n_subs ? 2 : 0) + 1 + wd.d + (wd.fast ? 0 : 2) +
+                (ps.win[w].n_edge ? 2 : 0);
+  }
   ev.mark();
   // 5. epilogue
   {

@@ -106,6 +106,8 @@ struct WinPlan {
   int box_lo[3] = {0, 0, 0}, box_w[3] = {1, 1, 1};
   int wrap = 0;
   int64_t n_cells = 0, n_subs = 0, n_edge = 0;
+  int64_t sub_off = 0;           // first subproblem in its dimension group
+  int64_t edge_off = 0;          // first edge node in the edge list
 };
 
 // One Gaussian width (sigbar = 1/sigma^2 or 2/sigma^2) with its tables.
@@ -144,6 +146,10 @@ struct Workspace {
   double* vt = nullptr;          // [N][nrhs] pixel-major rhs
   double* coef = nullptr;        // [nrhs][2]
   int64_t grid_total = 0, blocks_total = 0;
+  // separable assemble scratch (3-D windows): Y1 [box][64][nrhs], Y2 /8
+  double* asm_y1 = nullptr;
+  double* asm_y2 = nullptr;
+  int64_t asm_cap = 0;
   // persistent CG vectors (x, r, p, q, b, t): [6][cg_cap]
   double* cg = nullptr;
   int64_t cg_cap = 0;
@@ -172,6 +178,9 @@ struct nld_operator {
   nld_stats stats{};
   cudaEvent_t ev[6] = {};
   bool events = false;
+  cudaStream_t aux = nullptr;    // assemble/convolution stream (overlap)
+  cudaEvent_t ev_spread[16] = {}, ev_conv[16] = {}, ev_fork = nullptr, ev_join = nullptr;
+  int aux_windows = 0;
   std::mutex build_mu;           // lazy plan build (per operator: shards may
                                  // build concurrently in one process)
   // raw-torus plans (NFFT transform API): nodes used as given after the

@@ -729,6 +729,7 @@ void build_planset(nld_operator* op, int which, cudaStream_t st) {
     if (fast) {
       block_total += nsub * blk;
       sub_group_off[w] = subs_in_group[wp.d];
+      wp.sub_off = subs_in_group[wp.d];
       subs_in_group[wp.d] += nsub;
     } else {
       ps.generic_nodes += N;
@@ -809,6 +810,7 @@ void build_planset(nld_operator* op, int which, cudaStream_t st) {
     NLD_CUDA(cudaMemcpyAsync(ps.cellmap + cellmap_off[w], cellmaps[w],
                              sizeof(int32_t) * ps.wdev_h[w].box_size,
                              cudaMemcpyDeviceToDevice, st));
+    ps.win[w].edge_off = eoff;
     if (wc[w].nedge) {
       NLD_CUDA(cudaMemcpyAsync(ps.edges + eoff, wc[w].edges, sizeof(EdgeDev) * wc[w].nedge,
                                cudaMemcpyDeviceToDevice, st));
