@@ -51,6 +51,9 @@ extern "C" {
 #define NLD_APPLY_SYSTEM 2         /* lam v + mu(eta v - Gamma v) linops.py:48-50 */
 #define NLD_APPLY_LAPLACIAN 3      /* eta v - Gamma v    linops.py:43-46     */
 #define NLD_APPLY_WINDOW_SUM 4     /* sum_l G_l v (unit diagonal kept)       */
+/* OR into `kind`: batched v / out are pixel-major [n][nrhs] (rhs fastest,
+ * ld ignored) -- the kernels' native layout, no transposes */
+#define NLD_LAYOUT_PIXEL_MAJOR 0x100
 
 /* preconditioners for nld_cg_solve (linops.py:447-454) */
 #define NLD_PREC_NONE 0

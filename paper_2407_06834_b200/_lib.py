@@ -22,6 +22,7 @@ ERR_BREAKDOWN, ERR_VALUE, ERR_CUDA = 5, 6, 7
 
 APPLY_GAMMA, APPLY_GAMMA_SQUARED, APPLY_SYSTEM, APPLY_LAPLACIAN = 0, 1, 2, 3
 APPLY_WINDOW_SUM = 4
+LAYOUT_PIXEL_MAJOR = 0x100     # OR into kind: batches are (n, nrhs)
 PREC = {"none": 0, "jacobi": 1, "l2": 2}
 
 _EXC = {

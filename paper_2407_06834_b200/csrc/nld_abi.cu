@@ -231,6 +231,9 @@ int nld_op_apply(nld_operator* op, int32_t kind, const double* v, double* out, i
     if (!op) throw Error(NLD_ERR_VALUE, "null operator");
     if (nrhs <= 0) throw Error(NLD_ERR_DIMENSION, "nrhs must be positive");
     if (ld < op->N) throw Error(NLD_ERR_DIMENSION, "leading dimension smaller than n");
+    const int pm = (kind & NLD_LAYOUT_PIXEL_MAJOR) ? 1 : 0;
+    kind &= ~NLD_LAYOUT_PIXEL_MAJOR;
+    if (pm && nrhs > 256) throw Error(NLD_ERR_VALUE, "pixel-major batches hold at most 256 rhs");
     if (kind < 0 || kind > NLD_APPLY_WINDOW_SUM) throw Error(NLD_ERR_VALUE, "unknown kind");
     NLD_CUDA(cudaSetDevice(op->device));
     cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -248,9 +251,9 @@ int nld_op_apply(nld_operator* op, int32_t kind, const double* v, double* out, i
     }
     if (op->params.mode == 1) {
       if (kind == NLD_APPLY_WINDOW_SUM) throw Error(NLD_ERR_VALUE, "window sums need fast mode");
-      nld::dense_apply(op, which, kind, v, out, nrhs, ld, coef, eta, st);
+      nld::dense_apply(op, which, kind, v, out, nrhs, ld, coef, eta, st, pm);
     } else {
-      nld::apply_op(op, which, kind, v, out, nrhs, ld, coef, eta, st);
+      nld::apply_op(op, which, kind, v, out, nrhs, ld, coef, eta, st, pm);
     }
     if (coef) cudaFreeAsync(coef, st);
     if (op->timing && op->events && op->params.mode == 0) {

@@ -758,6 +758,65 @@ __global__ void k_epilogue(int kind, int L, int64_t N, int nrhs, const double* _
   }
 }
 
+#ifndef NLD_EPI_PM_MINB
+#define NLD_EPI_PM_MINB 8
+#endif
+// pixel-major epilogue: v, out, wout all [.][N][nrhs] -- pure streaming.
+// A block is grp = 256 / nrhs pixel groups of nrhs threads (no divisions in
+// the element loop).
+__global__ void __launch_bounds__(256, NLD_EPI_PM_MINB)
+k_epilogue_pm(int kind, int L, int64_t N, int nrhs, const double* __restrict__ v,
+              const double* __restrict__ wsum, double* __restrict__ out,
+              const double* __restrict__ eta, const double* __restrict__ coef) {
+  const int grp = 256 / nrhs;
+  const int tid = threadIdx.x;
+  if (tid >= grp * nrhs) return;
+  const int r = tid % nrhs;
+  const int g = tid / nrhs;
+  const int64_t total = N * nrhs;
+  const double lam = coef ? coef[2 * r] : 0.0, mu = coef ? coef[2 * r + 1] : 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)grp + g; i < N; i += (int64_t)gridDim.x * grp) {
+    const int64_t e = i * nrhs + r;
+    double s = 0.0;
+#pragma unroll 4
+    for (int w = 0; w < L; ++w) s += wsum[(int64_t)w * total + e];
+    if (kind == NLD_APPLY_WINDOW_SUM) {
+      out[e] = s;
+      continue;
+    }
+    const double x = v[e];
+    const double gam = (s - (double)L * x) / (double)L;
+    double y;
+    if (kind == NLD_APPLY_SYSTEM) y = lam * x + mu * (eta[i] * x - gam);
+    else if (kind == NLD_APPLY_LAPLACIAN) y = eta[i] * x - gam;
+    else y = gam;
+    out[e] = y;
+  }
+}
+
+// vt [N][nrhs] -> out [nrhs][ldo]
+__global__ void __launch_bounds__(256)
+k_transpose_out(const double* __restrict__ vt, int64_t N, int nrhs, double* __restrict__ out,
+                int64_t ldo) {
+  extern __shared__ double tile[];   // [kTileP][nrhs + 1]
+  const int ld_t = nrhs + 1;
+  const int64_t ntiles = (N + kTileP - 1) / kTileP;
+  for (int64_t tl = blockIdx.x; tl < ntiles; tl += gridDim.x) {
+    const int64_t i0 = tl * kTileP;
+    const int np = (int)min((int64_t)kTileP, N - i0);
+    for (int e = threadIdx.x; e < np * nrhs; e += blockDim.x) {
+      const int p = e / nrhs, r = e - p * nrhs;
+      tile[p * ld_t + r] = vt[i0 * nrhs + e];
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < np * nrhs; e += blockDim.x) {
+      const int r = e / np, p = e - r * np;
+      out[r * ldo + i0 + p] = tile[p * ld_t + r];
+    }
+    __syncthreads();
+  }
+}
+
 // v [nrhs][ld] -> vt [N][nrhs] (pixel-major, for the spread's node gathers)
 __global__ void __launch_bounds__(256)
 k_transpose_in(const double* __restrict__ v, int64_t ldv, int64_t N, int nrhs,
@@ -879,20 +938,20 @@ void launch_gather(const SubDev* subs, unsigned nsub, const PlanSet& ps, const W
   NLD_CUDA(cudaGetLastError());
 }
 
-template <int RPW>
+template <int RPW, int NW = mma::kSpWarps>
 void launch_spread_mma(const SubDev* subs, unsigned nsub, const PlanSet& ps,
                        const Workspace& ws, const double* vt, int nrhs, cudaStream_t st) {
-  const int rpp = std::min(nrhs, mma::kSpWarps * RPW);
+  const int rpp = std::min(nrhs, NW * RPW);
   const size_t smem = sizeof(double) * mma::spread_smem(rpp);
   static bool attr = false;
   if (!attr) {
-    NLD_CUDA(cudaFuncSetAttribute(mma::k_spread_mma<RPW>,
+    NLD_CUDA(cudaFuncSetAttribute(mma::k_spread_mma<RPW, NW>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)(sizeof(double) * mma::spread_smem(mma::kSpWarps * RPW))));
+                                  (int)(sizeof(double) * mma::spread_smem(NW * RPW))));
     attr = true;
   }
-  mma::k_spread_mma<RPW><<<nsub, mma::kSpThreads, smem, st>>>(subs, ps.wdev, ps.rows, ps.pix,
-                                                              vt, nrhs, ws.blocks);
+  mma::k_spread_mma<RPW, NW><<<nsub, 32 * NW, smem, st>>>(subs, ps.wdev, ps.rows, ps.pix, vt,
+                                                          nrhs, ws.blocks);
   NLD_CUDA(cudaGetLastError());
 }
 
@@ -935,7 +994,13 @@ void spread_window_fast(const PlanSet& ps, const Workspace& ws, int w, const dou
   } else if (wp.d == 2) {
     launch_spread<2, MC>(subs, nsub, ps, ws, vt, nrhs, st);
   } else if (MC == 4 && use_mma()) {
-    if (nrhs >= 16) launch_spread_mma<2>(subs, nsub, ps, ws, vt, nrhs, st);
+    static int rpw4 = -1;
+    if (rpw4 < 0) {
+      const char* e = getenv("NLD_SPREAD_RPW4");
+      rpw4 = (e && e[0] && e[0] != '0') ? 1 : 0;
+    }
+    if (nrhs >= 16 && rpw4) launch_spread_mma<4, 4>(subs, nsub, ps, ws, vt, nrhs, st);
+    else if (nrhs >= 16) launch_spread_mma<2>(subs, nsub, ps, ws, vt, nrhs, st);
     else launch_spread_mma<1>(subs, nsub, ps, ws, vt, nrhs, st);
   } else {
     launch_spread<3, MC>(subs, nsub, ps, ws, vt, nrhs, st);
@@ -1142,9 +1207,23 @@ static void ensure_aux(nld_operator* op, int L) {
   op->aux_windows = L;
 }
 
+void to_pixel_major(const double* v, int64_t ldv, int64_t n, int nrhs, double* vt,
+                    cudaStream_t st) {
+  k_transpose_in<<<grid_blocks(n, kTileP, 148 * 16), 256,
+                   sizeof(double) * kTileP * (nrhs + 1), st>>>(v, ldv, n, nrhs, vt);
+  NLD_CUDA(cudaGetLastError());
+}
+
+void to_rhs_major(const double* vt, int64_t n, int nrhs, double* out, int64_t ldo,
+                  cudaStream_t st) {
+  k_transpose_out<<<grid_blocks(n, kTileP, 148 * 16), 256,
+                    sizeof(double) * kTileP * (nrhs + 1), st>>>(vt, n, nrhs, out, ldo);
+  NLD_CUDA(cudaGetLastError());
+}
+
 void apply_op(nld_operator* op, int which, int kind, const double* v, double* out,
               int nrhs, int64_t ld, const double* coef_dev, const double* eta,
-              cudaStream_t st) {
+              cudaStream_t st, int pixel_major) {
   const PlanSet& ps = op->sets[which];
   ensure_workspace(op, ps, nrhs);
   Workspace& ws = op->ws;
@@ -1155,14 +1234,17 @@ void apply_op(nld_operator* op, int which, int kind, const double* v, double* ou
   int launches = 0;
   // 0. pixel-major copy of the rhs for the node gathers
   const double* vt = v;
-  if (nrhs > 1 || ld != N) {
-    k_transpose_in<<<grid_blocks(N, kTileP, 148 * 16), 256,
-                     sizeof(double) * kTileP * (nrhs + 1), st>>>(v, ld, N, nrhs, ws.vt);
-    NLD_CUDA(cudaGetLastError());
+  if (!pixel_major && (nrhs > 1 || ld != N)) {
+    to_pixel_major(v, ld, N, nrhs, ws.vt, st);
     vt = ws.vt;
     ++launches;
   }
-  const bool overlap = !op->comm && L <= 16;
+  static int no_overlap = -1;
+  if (no_overlap < 0) {
+    const char* e = getenv("NLD_NO_OVERLAP");
+    no_overlap = (e && e[0] && e[0] != '0') ? 1 : 0;
+  }
+  const bool overlap = !op->comm && L <= 16 && !no_overlap;
   if (overlap) {
     // window w's assemble + convolution (latency / L2 bound) run on the aux
     // stream while the main stream spreads window w+1 and, later, gathers
@@ -1203,7 +1285,10 @@ void apply_op(nld_operator* op, int which, int kind, const double* v, double* ou
     int lg = -1;
     for (int k = 0; k <= 11; ++k)
       if ((1 << k) == nrhs) lg = k;
-    if (lg >= 0) {
+    if ((pixel_major || nrhs == 1) && nrhs <= 256) {
+      k_epilogue_pm<<<grid_blocks(N, 256 / nrhs, 148 * 16), 256, 0, st>>>(
+          kind, L, N, nrhs, v, ws.wout, out, eta, coef_dev);
+    } else if (lg >= 0) {
       const int tp = 2048 >> lg;
       k_epilogue_tiled<<<grid_blocks(N, tp, 148 * 8), kEpiThreads, 0, st>>>(
           kind, L, N, lg, v, ld, ws.wout, out, ld, eta, coef_dev);
@@ -1229,7 +1314,19 @@ static void dense_tables(nld_operator* op, int** widx, int** woff, cudaStream_t 
 
 void dense_apply(nld_operator* op, int which, int kind, const double* v, double* out,
                  int nrhs, int64_t ld, const double* coef_dev, const double* eta,
-                 cudaStream_t st) {
+                 cudaStream_t st, int pixel_major) {
+  if (pixel_major && nrhs > 1) {
+    // exact mode is desk-scale: go through an rhs-major copy
+    double *vr = nullptr, *orr = nullptr;
+    NLD_CUDA(cudaMallocAsync(&vr, sizeof(double) * op->N * nrhs, st));
+    NLD_CUDA(cudaMallocAsync(&orr, sizeof(double) * op->N * nrhs, st));
+    to_rhs_major(v, op->N, nrhs, vr, op->N, st);
+    dense_apply(op, which, kind, vr, orr, nrhs, op->N, coef_dev, eta, st, 0);
+    to_pixel_major(orr, op->N, op->N, nrhs, out, st);
+    cudaFreeAsync(vr, st);
+    cudaFreeAsync(orr, st);
+    return;
+  }
   if (op->N > op->params.dense_limit)
     throw Error(NLD_ERR_DENSE_LIMIT, "dense assembly of " + std::to_string(op->N) +
                                          " nodes exceeds the limit " +

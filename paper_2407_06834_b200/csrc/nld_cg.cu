@@ -54,6 +54,7 @@ struct CgPtr {
   const double* eta2;
   int64_t N;
   int64_t ldf;
+  int nrhs;
   int L;
   int prec;
   int deflate;
@@ -86,47 +87,65 @@ __device__ __forceinline__ void block_store(double (&v)[K], double* part) {
     for (int k = 0; k < K; ++k) part[k] = sh[k][0];
 }
 
-// vecA: generic input for RED_SUM / RED_NORM2 ([rhs][lda])
+// Vectors are pixel-major [N][nrhs] (element (i, r) at i * nrhs + r), the
+// kernels' native layout.  A reduction block holds kRT / nrhs pixel groups
+// of nrhs threads; thread r of every group accumulates rhs r, and the groups
+// are summed in a fixed order (deterministic).
 template <int MODE>
 __global__ void __launch_bounds__(kRT)
 k_cg_reduce(CgPtr c, const RhsScal* __restrict__ sc, const double* __restrict__ vecA,
-            int64_t lda, double* __restrict__ part) {
-  const int rhs = blockIdx.y;
-  const RhsScal s = sc[rhs];
-  const int64_t N = c.N;
-  const int64_t o = rhs * N;
+            double* __restrict__ part) {
+  const int nr = c.nrhs;
+  const int grp = kRT / nr;
+  const int tid = threadIdx.x;
+  const bool live = tid < grp * nr;
+  const int r = live ? tid % nr : 0;
+  const int g = tid / nr;
+  const RhsScal s = sc[r];
   double acc[kMaxK] = {0.0, 0.0, 0.0, 0.0};
-  for (int64_t i = blockIdx.x * (int64_t)kRT + threadIdx.x; i < N;
-       i += (int64_t)gridDim.x * kRT) {
-    if (MODE == RED_SUM) {
-      acc[0] += vecA[rhs * lda + i];
-    } else if (MODE == RED_NORM2) {
-      const double a = vecA[rhs * lda + i];
-      acc[0] += a * a;
-    } else if (MODE == RED_PQ) {
-      const double p = c.p[o + i], q = c.q[o + i];
-      acc[0] += q;
-      acc[1] += p * q;
-      acc[2] += p;
-    } else if (MODE == RED_UPDATE || MODE == RED_PREC) {
-      double r = c.r[o + i];
-      if (MODE == RED_UPDATE && s.active) {
-        c.x[o + i] += s.alpha * c.p[o + i];
-        r -= s.alpha * (c.q[o + i] - s.mq);
-        c.r[o + i] = r;
+  if (live) {
+    for (int64_t i = blockIdx.x * (int64_t)grp + g; i < c.N; i += (int64_t)gridDim.x * grp) {
+      const int64_t e = i * nr + r;
+      if (MODE == RED_SUM) {
+        acc[0] += vecA[e];
+      } else if (MODE == RED_NORM2) {
+        const double a = vecA[e];
+        acc[0] += a * a;
+      } else if (MODE == RED_PQ) {
+        const double p = c.p[e], q = c.q[e];
+        acc[0] += q;
+        acc[1] += p * q;
+        acc[2] += p;
+      } else if (MODE == RED_UPDATE || MODE == RED_PREC) {
+        double rr = c.r[e];
+        if (MODE == RED_UPDATE && s.active) {
+          c.x[e] += s.alpha * c.p[e];
+          rr -= s.alpha * (c.q[e] - s.mq);
+          c.r[e] = rr;
+        }
+        const double zt = dinv_at(c, s, i) * rr;
+        acc[0] += rr * rr;
+        acc[1] += zt;
+        acc[2] += rr * zt;
+        acc[3] += rr;
+      } else if (MODE == RED_RESID) {
+        const double d = c.b[e] - (c.t[e] - s.mq);
+        acc[0] += d * d;
       }
-      const double zt = dinv_at(c, s, i) * r;
-      acc[0] += r * r;
-      acc[1] += zt;
-      acc[2] += r * zt;
-      acc[3] += r;
-    } else if (MODE == RED_RESID) {
-      const double e = c.b[o + i] - (c.t[o + i] - s.mq);
-      acc[0] += e * e;
     }
   }
-  double* pp = part + ((int64_t)rhs * gridDim.x + blockIdx.x) * kMaxK;
-  block_store<kMaxK>(acc, pp);
+  __shared__ double sh[kMaxK][kRT];
+#pragma unroll
+  for (int k = 0; k < kMaxK; ++k) sh[k][tid] = acc[k];
+  __syncthreads();
+  if (tid < nr) {
+#pragma unroll
+    for (int k = 0; k < kMaxK; ++k) {
+      double t = 0.0;
+      for (int j = 0; j < grp; ++j) t += sh[k][j * nr + tid];
+      part[((int64_t)tid * gridDim.x + blockIdx.x) * kMaxK + k] = t;
+    }
+  }
 }
 
 __global__ void k_final(const double* __restrict__ part, int nblk, double* __restrict__ out) {
@@ -139,51 +158,47 @@ __global__ void k_final(const double* __restrict__ part, int nblk, double* __res
   out[rhs * kMaxK + k] = s;
 }
 
+// elementwise kernels over the N * nrhs pixel-major elements
 __global__ void k_cg_setup(CgPtr c, const RhsScal* __restrict__ sc, int warm) {
-  const int rhs = blockIdx.y;
-  const RhsScal s = sc[rhs];
-  const int64_t o = rhs * c.N;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < c.N;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const double f = c.f[rhs * c.ldf + i];
+  const int64_t total = c.N * c.nrhs;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const RhsScal s = sc[e % c.nrhs];
+    const double f = c.t[e];                 // f, pixel-major copy
     const double g = c.deflate ? f - s.mf : f;
-    c.b[o + i] = s.lam * g;
-    c.x[o + i] = warm ? g : 0.0;
+    c.b[e] = s.lam * g;
+    c.x[e] = warm ? g : 0.0;
   }
 }
 
 __global__ void k_cg_resid0(CgPtr c, const RhsScal* __restrict__ sc, int warm) {
   // r = b - Pi A x0 (warm) or r = b (x0 = 0; A 0 == 0 exactly)
-  const int rhs = blockIdx.y;
-  const RhsScal s = sc[rhs];
-  const int64_t o = rhs * c.N;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < c.N;
-       i += (int64_t)gridDim.x * blockDim.x)
-    c.r[o + i] = warm ? c.b[o + i] - (c.q[o + i] - s.mq) : c.b[o + i];
+  const int64_t total = c.N * c.nrhs;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x)
+    c.r[e] = warm ? c.b[e] - (c.q[e] - sc[e % c.nrhs].mq) : c.b[e];
 }
 
 __global__ void k_cg_direction(CgPtr c, const RhsScal* __restrict__ sc, int first) {
   // z = Pi(D^-1 r) (or r), p = z + beta p
-  const int rhs = blockIdx.y;
-  const RhsScal s = sc[rhs];
-  if (!s.active) return;
-  const int64_t o = rhs * c.N;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < c.N;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const double r = c.r[o + i];
+  const int64_t total = c.N * c.nrhs;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / c.nrhs;
+    const RhsScal s = sc[e - i * c.nrhs];
+    if (!s.active) continue;
+    const double r = c.r[e];
     const double z = (c.prec == NLD_PREC_NONE) ? r : dinv_at(c, s, i) * r - s.mz;
-    c.p[o + i] = first ? z : z + s.beta * c.p[o + i];
+    c.p[e] = first ? z : z + s.beta * c.p[e];
   }
 }
 
-__global__ void k_cg_finish(CgPtr c, const RhsScal* __restrict__ sc, double* __restrict__ u,
-                            int64_t ldu) {
-  const int rhs = blockIdx.y;
-  const RhsScal s = sc[rhs];
-  const int64_t o = rhs * c.N;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < c.N;
-       i += (int64_t)gridDim.x * blockDim.x)
-    u[rhs * ldu + i] = c.deflate ? s.mf + c.x[o + i] : c.x[o + i];
+__global__ void k_cg_finish(CgPtr c, const RhsScal* __restrict__ sc) {
+  // x += mean(f) (deflation), in place before the transpose out
+  const int64_t total = c.N * c.nrhs;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x)
+    if (c.deflate) c.x[e] += sc[e % c.nrhs].mf;
 }
 
 int eblocks(int64_t n) {
@@ -200,7 +215,8 @@ struct Reducer {
   int nblk;
   cudaStream_t st;
   Reducer(nld_operator* o, int nr, int64_t N, cudaStream_t s) : op(o), nrhs(nr), st(s) {
-    nblk = (int)std::max<int64_t>(1, std::min<int64_t>(kRB, (N + kRT - 1) / kRT));
+    const int64_t grp = std::max(1, kRT / nr);
+    nblk = (int)std::max<int64_t>(1, std::min<int64_t>(kRB, (N + grp - 1) / grp));
     NLD_CUDA(cudaMallocAsync(&part, sizeof(double) * nr * nblk * kMaxK, st));
     NLD_CUDA(cudaMallocAsync(&out, sizeof(double) * nr * kMaxK, st));
     host.resize((size_t)nr * kMaxK);
@@ -211,9 +227,8 @@ struct Reducer {
   }
   template <int MODE>
   const std::vector<double>& run(const CgPtr& c, const RhsScal* sc,
-                                 const double* vecA = nullptr, int64_t lda = 0) {
-    dim3 grid(nblk, nrhs);
-    k_cg_reduce<MODE><<<grid, kRT, 0, st>>>(c, sc, vecA, lda, part);
+                                 const double* vecA = nullptr) {
+    k_cg_reduce<MODE><<<nblk, kRT, 0, st>>>(c, sc, vecA, part);
     NLD_CUDA(cudaGetLastError());
     k_final<<<nrhs, 32, 0, st>>>(part, nblk, out);
     NLD_CUDA(cudaMemcpyAsync(host.data(), out, sizeof(double) * nrhs * kMaxK,
@@ -455,6 +470,7 @@ void cg_solve(nld_operator* op, const double* f, double* u, int nrhs, int64_t ld
   c.b = c.q + op->ws.cg_cap;
   c.t = c.b + op->ws.cg_cap;
   c.f = f;
+  c.nrhs = nrhs;
   c.eta = eta;
   c.eta2 = eta2;
   c.N = N;
@@ -479,13 +495,16 @@ void cg_solve(nld_operator* op, const double* f, double* u, int nrhs, int64_t ld
     NLD_CUDA(cudaMemcpyAsync(scd, sc.data(), sizeof(RhsScal) * nrhs, cudaMemcpyHostToDevice,
                              st));
   };
-  auto matvec = [&](const double* in, double* out) {
-    if (op->params.mode == 1) dense_apply(op, 0, NLD_APPLY_SYSTEM, in, out, nrhs, N, coef, eta, st);
-    else apply_op(op, 0, NLD_APPLY_SYSTEM, in, out, nrhs, N, coef, eta, st);
+  auto matvec = [&](const double* in, double* out) {   // pixel-major in/out
+    if (op->params.mode == 1)
+      dense_apply(op, 0, NLD_APPLY_SYSTEM, in, out, nrhs, N, coef, eta, st, 1);
+    else
+      apply_op(op, 0, NLD_APPLY_SYSTEM, in, out, nrhs, N, coef, eta, st, 1);
   };
   const double dN = (double)op->N_global;
+  if (nrhs > kRT) throw Error(NLD_ERR_VALUE, "at most 256 right-hand sides per solve");
   Reducer red(op, nrhs, N, st);
-  dim3 eg(eblocks(N), nrhs);
+  const int eg = eblocks(N * nrhs);
 
   std::vector<std::vector<double>> H(nrhs);
   std::vector<double> bnorm(nrhs, 0.0), rz(nrhs, 0.0);
@@ -497,9 +516,11 @@ void cg_solve(nld_operator* op, const double* f, double* u, int nrhs, int64_t ld
   }
 
   // mean of f (deflation: x_first = g0 carries the mean, linops.py:278-279)
+  // f -> pixel-major (in the t vector, free until the first true residual)
+  to_pixel_major(f, ld, N, nrhs, c.t, st);
   push();
   {
-    const auto& h = red.run<RED_SUM>(c, scd, f, ld);
+    const auto& h = red.run<RED_SUM>(c, scd, c.t);
     for (int r = 0; r < nrhs; ++r) sc[r].mf = deflate ? h[r * kMaxK] / dN : 0.0;
   }
   push();
@@ -507,7 +528,7 @@ void cg_solve(nld_operator* op, const double* f, double* u, int nrhs, int64_t ld
   if (warm) {
     matvec(c.x, c.q);
     if (deflate) {
-      const auto& h = red.run<RED_SUM>(c, scd, c.q, N);
+      const auto& h = red.run<RED_SUM>(c, scd, c.q);
       for (int r = 0; r < nrhs; ++r) sc[r].mq = h[r * kMaxK] / dN;
     }
     push();
@@ -516,7 +537,7 @@ void cg_solve(nld_operator* op, const double* f, double* u, int nrhs, int64_t ld
   NLD_CUDA(cudaGetLastError());
   std::vector<double> nb(nrhs), nr(nrhs);
   {
-    const auto& h = red.run<RED_NORM2>(c, scd, c.b, N);
+    const auto& h = red.run<RED_NORM2>(c, scd, c.b);
     for (int r = 0; r < nrhs; ++r) nb[r] = std::sqrt(h[r * kMaxK]);
   }
   {
@@ -563,7 +584,7 @@ void cg_solve(nld_operator* op, const double* f, double* u, int nrhs, int64_t ld
   auto true_residual = [&](std::vector<double>& out) {
     matvec(c.x, c.t);
     if (deflate) {
-      const auto& h = red.run<RED_SUM>(c, scd, c.t, N);
+      const auto& h = red.run<RED_SUM>(c, scd, c.t);
       for (int r = 0; r < nrhs; ++r) sc[r].mq = h[r * kMaxK] / dN;
     } else {
       for (int r = 0; r < nrhs; ++r) sc[r].mq = 0.0;
@@ -649,7 +670,8 @@ void cg_solve(nld_operator* op, const double* f, double* u, int nrhs, int64_t ld
       push();
     }
   }
-  k_cg_finish<<<eg, 256, 0, st>>>(c, scd, u, ld);
+  k_cg_finish<<<eg, 256, 0, st>>>(c, scd);
+  to_rhs_major(c.x, N, nrhs, u, ld, st);
   NLD_CUDA(cudaGetLastError());
   NLD_CUDA(cudaStreamSynchronize(st));
   for (int r = 0; r < nrhs; ++r) {

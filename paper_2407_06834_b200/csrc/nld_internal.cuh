@@ -201,7 +201,7 @@ void free_workspace(Workspace& ws);
 // one fused operator application (all windows, nrhs right-hand sides)
 void apply_op(nld_operator* op, int which, int kind, const double* v,
               double* out, int nrhs, int64_t ld, const double* coef_dev,
-              const double* eta, cudaStream_t st);
+              const double* eta, cudaStream_t st, int pixel_major = 0);
 
 // the two halves of a product, reused by the NFFT transform API
 int spread_stage(nld_operator* op, const PlanSet& ps, const double* vt, int nrhs,
@@ -210,7 +210,12 @@ int gather_stage(nld_operator* op, const PlanSet& ps, int nrhs, cudaStream_t st)
 
 void dense_apply(nld_operator* op, int which, int kind, const double* v,
                  double* out, int nrhs, int64_t ld, const double* coef_dev,
-                 const double* eta, cudaStream_t st);
+                 const double* eta, cudaStream_t st, int pixel_major = 0);
+// layout changes between rhs-major [nrhs][ld] and pixel-major [n][nrhs]
+void to_pixel_major(const double* v, int64_t ldv, int64_t n, int nrhs, double* vt,
+                    cudaStream_t st);
+void to_rhs_major(const double* vt, int64_t n, int nrhs, double* out, int64_t ldo,
+                  cudaStream_t st);
 void dense_assemble(nld_operator* op, int which, double* out, cudaStream_t st);
 
 void cg_solve(nld_operator* op, const double* f, double* u, int nrhs,

@@ -77,11 +77,13 @@ __host__ __device__ constexpr int spread_smem(int rpp) {
 // ---- spread ---------------------------------------------------------------
 // RPW rhs per warp; rpp = rhs per pass = 8 * RPW (or nrhs if smaller, then
 // several warps share an rhs and split the k-steps).
-template <int RPW>
-__global__ void __launch_bounds__(kSpThreads, NLD_SPREAD_MINB)
+template <int RPW, int NW = kSpWarps>
+__global__ void __launch_bounds__(32 * NW, (NW == kSpWarps ? NLD_SPREAD_MINB : 1))
 k_spread_mma(const SubDev* __restrict__ subs, const WinDev* __restrict__ wins,
              const double* __restrict__ rows, const int32_t* __restrict__ pix,
              const double* __restrict__ vt, int nrhs, double* __restrict__ blocks) {
+  constexpr int kSpWarps = NW;
+  constexpr int kSpThreads = 32 * NW;
   extern __shared__ __align__(16) double sm[];
   const int rpp_max = kSpWarps * RPW;
   const int rpp = nrhs < rpp_max ? nrhs : rpp_max;

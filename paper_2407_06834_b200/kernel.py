@@ -24,8 +24,8 @@ import torch
 
 from . import _device as dv
 from ._lib import (APPLY_GAMMA, APPLY_GAMMA_SQUARED, APPLY_LAPLACIAN,
-                   APPLY_SYSTEM, APPLY_WINDOW_SUM, Params, Stats, WindowInfo,
-                   check, lib)
+                   APPLY_SYSTEM, APPLY_WINDOW_SUM, LAYOUT_PIXEL_MAJOR, Params,
+                   Stats, WindowInfo, check, lib)
 from .errors import DimensionMismatchError, WindowSizeError
 
 DEFAULT_DENSE_LIMIT = 5000          # kernel.py:22
@@ -139,20 +139,25 @@ class AnovaOperator:
         return dv.to_device(v, self.device), nrhs
 
     def apply_device(self, x: torch.Tensor, kind: int, nrhs: int = 1,
-                     coef=None, out: torch.Tensor | None = None) -> torch.Tensor:
-        """Device product; x is a contiguous fp64 (nrhs, n) or (n,) tensor."""
+                     coef=None, out: torch.Tensor | None = None,
+                     pixel_major: bool = False) -> torch.Tensor:
+        """Device product; x is a contiguous fp64 (nrhs, n) or (n,) tensor,
+        or (n, nrhs) with ``pixel_major`` (the kernels' native layout: no
+        transposes)."""
         if out is None:
             out = torch.empty_like(x)
         cptr = None
         if coef is not None:
             carr = np.ascontiguousarray(coef, dtype=np.float64).ravel()
             cptr = carr.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+        if pixel_major:
+            kind |= LAYOUT_PIXEL_MAJOR
         check(lib.nld_op_apply(self._handle, kind, dv.ptr(x), dv.ptr(out), nrhs,
                                self.n, cptr, dv.stream_of(self.device)))
         return out
 
     def apply_pipelined(self, kind: int, inputs, outputs, nrhs: int = 1,
-                        coef=None):
+                        coef=None, pixel_major: bool = False):
         """Host -> device -> host products for a sequence of batches.
 
         ``inputs`` / ``outputs`` are equal-length sequences of pinned host
@@ -171,8 +176,9 @@ class AnovaOperator:
         if not inputs:
             return
         shape = tuple(inputs[0].shape)
-        if shape not in ((nrhs, self.n), (self.n,) if nrhs == 1 else (nrhs, self.n)):
-            raise DimensionMismatchError(f"batch shape {shape} != ({nrhs}, {self.n})")
+        want = (self.n, nrhs) if pixel_major else (nrhs, self.n)
+        if shape != want and not (nrhs == 1 and shape == (self.n,)):
+            raise DimensionMismatchError(f"batch shape {shape} != {want}")
         vd = [torch.empty(shape, dtype=torch.float64, device=dev) for _ in range(2)]
         yd = [torch.empty(shape, dtype=torch.float64, device=dev) for _ in range(2)]
         done_cmp = [None, None]      # compute finished with vd[b] / wrote yd[b]
@@ -189,7 +195,8 @@ class AnovaOperator:
                 s_cmp.wait_event(ev_in)
                 if done_out[b] is not None:
                     s_cmp.wait_event(done_out[b])
-                self.apply_device(vd[b], kind, nrhs, coef, out=yd[b])
+                self.apply_device(vd[b], kind, nrhs, coef, out=yd[b],
+                                  pixel_major=pixel_major)
                 done_cmp[b] = torch.cuda.Event()
                 done_cmp[b].record(s_cmp)
             with torch.cuda.stream(s_out):

@@ -370,3 +370,18 @@ def test_torchcomm_nccl_single_rank(golden):
             assert np.array_equal(a.x, b.x)
     finally:
         dist.destroy_process_group()
+
+
+def test_pixel_major_layout_matches_rhs_major():
+    """NLD_LAYOUT_PIXEL_MAJOR: (n, nrhs) batches give the same products."""
+    from paper_2407_06834_b200 import _lib
+    op, _, _, _ = operator("c1")
+    rng = np.random.default_rng(21)
+    V = torch.from_numpy(rng.standard_normal((5, op.n))).cuda()
+    coef = np.tile([1.0, 0.003], 5)
+    a = op.apply_device(V, _lib.APPLY_SYSTEM, 5, coef)
+    b = op.apply_device(V.T.contiguous(), _lib.APPLY_SYSTEM, 5, coef, pixel_major=True)
+    assert torch.allclose(a, b.T, rtol=1e-14, atol=0)
+    g = op.apply_device(V, _lib.APPLY_GAMMA, 5)
+    h = op.apply_device(V.T.contiguous(), _lib.APPLY_GAMMA, 5, pixel_major=True)
+    assert torch.allclose(g, h.T, rtol=1e-14, atol=0)
