@@ -192,7 +192,7 @@ def ncu_traffic(kernel_tag):
         with open(path) as fh:
             data = json.load(fh)
         ent = data.get("kernels", {}).get(kernel_tag)
-        return None if ent is None else ent.get("dram_bytes_per_launch")
+        return None if ent is None else ent.get("dram_bytes_per_product")
     except (OSError, ValueError):
         return None
 
@@ -354,12 +354,14 @@ def run_ours(args, world, rank, local):
         # figure, so the peak is measured here, in this run, on this GPU
         "bound": "tensor", "achieved": alg_tflops, "peak": fp64_peak,
         "unit": "TFLOP/s", "frac": alg_tflops / fp64_peak,
-        "traffic": ncu_traffic(tag), "traffic_unit": "bytes per launch (ncu)",
+        "traffic": ncu_traffic(tag),
+        "traffic_unit": "dram bytes per product (all window launches, ncu, committed profile)",
         "kernel": tag, "kernel_ms": dom_ms,
         "peak_source": (f"fp64 measured in this run: DMMA m8n8k4 probe {dmma_peak:.2f}, "
                         f"DFMA probe {dfma_peak:.2f} TFLOP/s (shared execution "
                         "resources; max taken)"),
-        "flops_model": "N*nrhs*sum_l 2*(2m)^d_l per launch (FMA = 2 flop)",
+        "flops_model": ("N*nrhs*sum_l 2*(2m)^d_l per product (all window launches of the "
+                        "kernel, FMA = 2 flop) / the kernel's event-timed stage"),
         "hbm": {"achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                 "frac": achieved / hbm_peak, "peak_source": f"{peak_src} hbm_gbs",
                 "bytes_model": ("minimal (SURVEY §8d): N*(8*sum_l d_l + 8*nrhs) "

@@ -13,14 +13,10 @@ for r in rows[1:]:
     name = name.replace("mma::", "").replace("void ", "")
     ns = float(r[iv]) * {"ns": 1, "us": 1e3, "usecond": 1e3, "ms": 1e6, "msecond": 1e6}.get(r[iu], 1)
     seq.append((name, ns / 1e6))
-# one steady-state matvec step: the last k_transpose_in .. k_epilogue_tiled run
+# one steady-state matvec step: everything after the second-to-last epilogue
+# up to the last one (the last product of the run)
 ends = [i for i, (n, _) in enumerate(seq) if n.startswith("k_epilogue")]
-starts = [i for i, (n, _) in enumerate(seq) if n.startswith("k_transpose_in")]
-step = []
-if ends and starts:
-    e = ends[-1]
-    s = max(i for i in starts if i < e)
-    step = seq[s:e + 1]
+step = seq[ends[-2] + 1:ends[-1] + 1] if len(ends) >= 2 else []
 agg = OrderedDict()
 for n, ms in step:
     agg[n] = agg.get(n, 0.0) + ms
