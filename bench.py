@@ -366,7 +366,7 @@ def run_ours(args, world, rank, local):
                 "frac": achieved / hbm_peak, "peak_source": f"{peak_src} hbm_gbs",
                 "bytes_model": ("minimal (SURVEY §8d): N*(8*sum_l d_l + 8*nrhs) "
                                 "per launch -- not the binding roofline")},
-        "stage_share": {k: v / max(elapsed_ms, 1e-9) for k, v in stage.items()},
+        "stage_share": {k[:-3]: v / max(elapsed_ms, 1e-9) for k, v in stage.items()},
     }
 
     # CG denoise solve (deflated Jacobi, tol 1e-6) over the alpha sweep
