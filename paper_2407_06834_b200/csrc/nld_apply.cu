@@ -429,7 +429,7 @@ __global__ void k_spread_edges(const EdgeDev* __restrict__ edges, int64_t ne,
 __global__ void k_gather_edges(const EdgeDev* __restrict__ edges, int64_t ne,
                                const WinDev* __restrict__ wins,
                                const double* __restrict__ grid, int64_t grid_ld,
-                               double* __restrict__ wout, int64_t N, int nrhs) {
+                               double* __restrict__ wout, int64_t win_stride, int nrhs) {
   const int rhs = blockIdx.y;
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < ne;
        k += (int64_t)gridDim.x * blockDim.x) {
@@ -449,7 +449,7 @@ __global__ void k_gather_edges(const EdgeDev* __restrict__ edges, int64_t ne,
       for (int s = 0; s < wd.d; ++s) f = f * wd.box_w[s] + p[s];
       y += grid[rhs * grid_ld + wd.grid_off + f] * wp;
     }
-    wout[((int64_t)ed.win * N + ed.pix) * nrhs + rhs] += y;
+    wout[((int64_t)ed.win * win_stride + ed.pix) * nrhs + rhs] += y;
   }
 }
 
@@ -955,8 +955,22 @@ void launch_spread_mma(const SubDev* subs, unsigned nsub, const PlanSet& ps,
   NLD_CUDA(cudaGetLastError());
 }
 
+static void launch_spread_bc(const SubDev* subs, unsigned nsub, const PlanSet& ps,
+                             const Workspace& ws, const double* vt, int nrhs, cudaStream_t st) {
+  const size_t smem = sizeof(double) * mma::spread_bc_smem();
+  static bool attr = false;
+  if (!attr) {
+    NLD_CUDA(cudaFuncSetAttribute(mma::k_spread_bc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem));
+    attr = true;
+  }
+  mma::k_spread_bc<<<nsub, 256, smem, st>>>(subs, ps.wdev, ps.rows, ps.pix, vt, nrhs, ws.blocks);
+  NLD_CUDA(cudaGetLastError());
+}
+
 void launch_gather_mma(const SubDev* subs, unsigned nsub, const PlanSet& ps,
-                       const Workspace& ws, int64_t N, int nrhs, cudaStream_t st) {
+                       const Workspace& ws, int64_t N, int nrhs, cudaStream_t st,
+                       const mma::GatherEpi& ep, double* out) {
   if (nrhs >= 8) {
     const size_t smem16 = sizeof(double) * 16 * mma::kGRow;
     static bool attr16 = false;
@@ -966,7 +980,8 @@ void launch_gather_mma(const SubDev* subs, unsigned nsub, const PlanSet& ps,
       attr16 = true;
     }
     mma::k_gather_mma16<<<nsub, mma::kGaThreads, smem16, st>>>(
-        subs, ps.cells, ps.wdev, ps.rows, ps.pix, ws.grid_out, ps.grid_total, ws.wout, N, nrhs);
+        subs, ps.cells, ps.wdev, ps.rows, ps.pix, ws.grid_out, ps.grid_total,
+        ep.mode == mma::kGatherStore ? ws.wout : out, N, nrhs, ep);
   } else {
     const size_t smem = sizeof(double) * mma::kBlk * std::min(nrhs, mma::kGaRhs);
     static bool attr = false;
@@ -999,7 +1014,14 @@ void spread_window_fast(const PlanSet& ps, const Workspace& ws, int w, const dou
       const char* e = getenv("NLD_SPREAD_RPW4");
       rpw4 = (e && e[0] && e[0] != '0') ? 1 : 0;
     }
-    if (nrhs >= 16 && rpw4) launch_spread_mma<4, 4>(subs, nsub, ps, ws, vt, nrhs, st);
+    static int bc = -1;   // shared (B (x) C) spread: default, NLD_SPREAD_BC=0 for A/B
+    if (bc < 0) {
+      const char* e = getenv("NLD_SPREAD_BC");
+      bc = (e && e[0] == '0') ? 0 : 1;
+    }
+    if (bc && nrhs % 16 == 0 && ((uintptr_t)vt & 15) == 0)
+      launch_spread_bc(subs, nsub, ps, ws, vt, nrhs, st);
+    else if (nrhs >= 16 && rpw4) launch_spread_mma<4, 4>(subs, nsub, ps, ws, vt, nrhs, st);
     else if (nrhs >= 16) launch_spread_mma<2>(subs, nsub, ps, ws, vt, nrhs, st);
     else launch_spread_mma<1>(subs, nsub, ps, ws, vt, nrhs, st);
   } else {
@@ -1009,14 +1031,14 @@ void spread_window_fast(const PlanSet& ps, const Workspace& ws, int w, const dou
 
 template <int MC>
 void gather_window_fast(const PlanSet& ps, const Workspace& ws, int w, int64_t N, int nrhs,
-                        cudaStream_t st) {
+                        cudaStream_t st, const mma::GatherEpi& ep, double* out) {
   const WinPlan& wp = ps.win[w];
   if (!ps.wdev_h[w].fast || wp.n_subs == 0) return;
   const SubDev* subs = ps.subs[wp.d] + wp.sub_off;
   const unsigned nsub = (unsigned)wp.n_subs;
   if (wp.d == 1) launch_gather<1, MC>(subs, nsub, ps, ws, N, nrhs, st);
   else if (wp.d == 2) launch_gather<2, MC>(subs, nsub, ps, ws, N, nrhs, st);
-  else if (MC == 4 && use_mma()) launch_gather_mma(subs, nsub, ps, ws, N, nrhs, st);
+  else if (MC == 4 && use_mma()) launch_gather_mma(subs, nsub, ps, ws, N, nrhs, st, ep, out);
   else launch_gather<3, MC>(subs, nsub, ps, ws, N, nrhs, st);
 }
 
@@ -1149,31 +1171,43 @@ static void conv_window(nld_operator* op, const PlanSet& ps, int w, int nrhs, cu
   }
 }
 
-// gather of window w from ws.grid_out into ws.wout (+ generic/edges)
+// gather of window w from ws.grid_out into ws.wout (+ generic/edges), or --
+// fused (ep->mode != kGatherStore, only fast d=3 m=4 windows, nrhs >= 8) --
+// accumulated into out with the epilogue applied by the last window.  The
+// edge corrections (+=) of the last window run before its fast gather so the
+// final formula sees the complete window sum.
 static void gather_window(nld_operator* op, const PlanSet& ps, int w, int nrhs,
-                          cudaStream_t st) {
+                          cudaStream_t st, const mma::GatherEpi* ep = nullptr,
+                          double* out = nullptr) {
   Workspace& ws = op->ws;
   const int64_t N = op->N;
-  switch (op->params.cutoff) {
-    case 3: gather_window_fast<3>(ps, ws, w, N, nrhs, st); break;
-    case 4: gather_window_fast<4>(ps, ws, w, N, nrhs, st); break;
-    case 5: gather_window_fast<5>(ps, ws, w, N, nrhs, st); break;
-    default: break;
-  }
   const WinDev& wd = ps.wdev_h[w];
   const WinPlan& wp = ps.win[w];
+  mma::GatherEpi store{mma::kGatherStore, 0, 0, nullptr, nullptr, nullptr};
+  const mma::GatherEpi& e = ep ? *ep : store;
+  double* edge_out = ep ? out : ws.wout;
+  const int64_t edge_stride = ep ? 0 : N;
+  auto edges = [&]() {
+    if (!wp.n_edge) return;
+    dim3 grid(grid_blocks(wp.n_edge, 128), nrhs);
+    k_gather_edges<<<grid, 128, 0, st>>>(ps.edges + wp.edge_off, wp.n_edge, ps.wdev,
+                                         ws.grid_out, ps.grid_total, edge_out, edge_stride, nrhs);
+    NLD_CUDA(cudaGetLastError());
+  };
+  if (e.mode == mma::kGatherFinal) edges();
+  switch (op->params.cutoff) {
+    case 3: gather_window_fast<3>(ps, ws, w, N, nrhs, st, e, out); break;
+    case 4: gather_window_fast<4>(ps, ws, w, N, nrhs, st, e, out); break;
+    case 5: gather_window_fast<5>(ps, ws, w, N, nrhs, st, e, out); break;
+    default: break;
+  }
   if (!wd.fast) {
     dim3 grid(grid_blocks(N, 256), nrhs);
     k_gather_generic<<<grid, 256, 0, st>>>(ps.wdev, w, nrhs, ps.rows, ps.pix, ps.key,
                                            ws.grid_out, ps.grid_total, ws.wout, N);
     NLD_CUDA(cudaGetLastError());
   }
-  if (wp.n_edge) {
-    dim3 grid(grid_blocks(wp.n_edge, 128), nrhs);
-    k_gather_edges<<<grid, 128, 0, st>>>(ps.edges + wp.edge_off, wp.n_edge, ps.wdev,
-                                         ws.grid_out, ps.grid_total, ws.wout, N, nrhs);
-    NLD_CUDA(cudaGetLastError());
-  }
+  if (e.mode != mma::kGatherFinal) edges();
 }
 
 // spread of all windows into the support boxes ws.grid_in [nrhs][grid_total]
@@ -1245,6 +1279,29 @@ void apply_op(nld_operator* op, int which, int kind, const double* v, double* ou
     no_overlap = (e && e[0] && e[0] != '0') ? 1 : 0;
   }
   const bool overlap = !op->comm && L <= 16 && !no_overlap;
+  // fused gather epilogue (see gather_window): every window on the DMMA
+  // gather, pixel-major in/out, out not aliasing v
+  static int no_fuse = -1;
+  if (no_fuse < 0) {
+    const char* e = getenv("NLD_NO_FUSED_EPILOGUE");
+    no_fuse = (e && e[0] && e[0] != '0') ? 1 : 0;
+  }
+  bool fused = !no_fuse && pixel_major && nrhs >= 8 && L >= 2 && out != v &&
+               op->params.cutoff == 4 && use_mma();
+  for (int w = 0; w < L && fused; ++w) {
+    const WinDev& wd = ps.wdev_h[w];
+    fused = wd.fast && wd.d == 3 && ps.win[w].n_subs > 0;
+  }
+  auto gather_w = [&](int w) {
+    if (!fused) {
+      gather_window(op, ps, w, nrhs, st);
+      return;
+    }
+    mma::GatherEpi ep{w == 0 ? mma::kGatherFirst
+                             : (w == L - 1 ? mma::kGatherFinal : mma::kGatherAccum),
+                      kind, L, v, eta, coef_dev};
+    gather_window(op, ps, w, nrhs, st, &ep, out);
+  };
   if (overlap) {
     // window w's assemble + convolution (latency / L2 bound) run on the aux
     // stream while the main stream spreads window w+1 and, later, gathers
@@ -1264,7 +1321,7 @@ void apply_op(nld_operator* op, int which, int kind, const double* v, double* ou
     ev.mark();
     for (int w = 0; w < L; ++w) {
       if (w > 0) NLD_CUDA(cudaStreamWaitEvent(st, op->ev_conv[w], 0));
-      gather_window(op, ps, w, nrhs, st);
+      gather_w(w);
     }
   } else {
     spread_stage(op, ps, vt, nrhs, st);
@@ -1272,7 +1329,7 @@ void apply_op(nld_operator* op, int which, int kind, const double* v, double* ou
     ev.mark();
     for (int w = 0; w < L; ++w) conv_window(op, ps, w, nrhs, st);
     ev.mark();
-    gather_stage(op, ps, nrhs, st);
+    for (int w = 0; w < L; ++w) gather_w(w);
   }
   for (int w = 0; w < L; ++w) {
     const WinDev& wd = ps.wdev_h[w];
@@ -1285,7 +1342,9 @@ void apply_op(nld_operator* op, int which, int kind, const double* v, double* ou
     int lg = -1;
     for (int k = 0; k <= 11; ++k)
       if ((1 << k) == nrhs) lg = k;
-    if ((pixel_major || nrhs == 1) && nrhs <= 256) {
+    if (fused) {
+      // done inside the last window's gather
+    } else if ((pixel_major || nrhs == 1) && nrhs <= 256) {
       k_epilogue_pm<<<grid_blocks(N, 256 / nrhs, 148 * 16), 256, 0, st>>>(
           kind, L, N, nrhs, v, ws.wout, out, eta, coef_dev);
     } else if (lg >= 0) {
@@ -1297,7 +1356,7 @@ void apply_op(nld_operator* op, int which, int kind, const double* v, double* ou
                                                                  0, out, ld, eta, coef_dev);
     }
     NLD_CUDA(cudaGetLastError());
-    ++launches;
+    if (!fused) ++launches;
   }
   ev.mark();
   op->stats.launches = launches;

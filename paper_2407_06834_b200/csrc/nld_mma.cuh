@@ -32,8 +32,13 @@
 namespace nld {
 namespace mma {
 
+#ifdef NLD_DMMA_NV
+#define NLD_DMMA_ASM asm
+#else
+#define NLD_DMMA_ASM asm volatile
+#endif
 __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+  NLD_DMMA_ASM("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(d[0]), "+d"(d[1])
                : "d"(a), "d"(b));
 }
@@ -70,8 +75,12 @@ constexpr int kGaThreads = 256;
 constexpr int kGaRhs = 16;        // rhs whose G blocks sit in smem at once
 
 // shared-memory doubles of the spread for a given rhs-per-pass count
+// v rows in shared memory are padded by 2 doubles (even rpp) so the 4 nodes of
+// a k-step read from distinct banks (16 rhs = 128 B would map them all to one)
+__host__ __device__ constexpr int spread_vst(int rpp) { return (rpp % 2 == 0) ? rpp + 2 : rpp; }
+
 __host__ __device__ constexpr int spread_smem(int rpp) {
-  return 2 * (kSpChunk * kSRow + kSpChunk * rpp);
+  return 2 * (kSpChunk * kSRow + kSpChunk * spread_vst(rpp));
 }
 
 // ---- spread ---------------------------------------------------------------
@@ -88,7 +97,8 @@ k_spread_mma(const SubDev* __restrict__ subs, const WinDev* __restrict__ wins,
   const int rpp_max = kSpWarps * RPW;
   const int rpp = nrhs < rpp_max ? nrhs : rpp_max;
   const int rowbuf = kSpChunk * kSRow;                // doubles per row buffer
-  const int vbuf = kSpChunk * rpp;                     // doubles per v buffer
+  const int vst = spread_vst(rpp);                     // v row stride
+  const int vbuf = kSpChunk * vst;                     // doubles per v buffer
   double* const sv0 = sm + 2 * rowbuf;
   const SubDev sd = subs[blockIdx.x];
   const WinDev wd = wins[sd.win];
@@ -123,23 +133,35 @@ k_spread_mma(const SubDev* __restrict__ subs, const WinDev* __restrict__ wins,
         cp_async16(sm + buf * rowbuf + pt * kSRow + (2 - dim) * kS + 2 * w4,
                    rw + (int64_t)(c0 + pt) * kRow + dim * kS + 2 * w4);
       }
-      for (int e = tid; e < cn * rn; e += kSpThreads) {
-        const int pt = e / rn, q = e - pt * rn;
-        cp_async8(sv0 + buf * vbuf + pt * rpp + q, vt + (int64_t)pw[c0 + pt] * nrhs + rg + q);
+      if (rn == 16 && rpp == 16 && nrhs % 2 == 0 && ((uintptr_t)vt & 15) == 0) {
+        // 16 rhs = one 128-B pixel-major line per node: 8 x 16-B copies
+        for (int e = tid; e < cn * 8; e += kSpThreads) {
+          const int pt = e >> 3, q = (e & 7) * 2;
+          cp_async16(sv0 + buf * vbuf + pt * vst + q, vt + (int64_t)pw[c0 + pt] * nrhs + rg + q);
+        }
+      } else {
+        for (int e = tid; e < cn * rn; e += kSpThreads) {
+          const int pt = e / rn, q = e - pt * rn;
+          cp_async8(sv0 + buf * vbuf + pt * vst + q, vt + (int64_t)pw[c0 + pt] * nrhs + rg + q);
+        }
       }
       // zero-pad to a multiple of 4 nodes so the k-step loop needs no bounds test
       const int cpad = (cn + 3) & ~3;
       for (int e = tid; e < (cpad - cn) * kSRow; e += kSpThreads)
         sm[buf * rowbuf + cn * kSRow + e] = 0.0;
-      for (int e = tid; e < (cpad - cn) * rpp; e += kSpThreads)
-        sv0[buf * vbuf + cn * rpp + e] = 0.0;
+      for (int e = tid; e < (cpad - cn) * vst; e += kSpThreads)
+        sv0[buf * vbuf + cn * vst + e] = 0.0;
       cp_commit();
     };
 
     stage(0, 0);
     for (int ck = 0; ck < nchunk; ++ck) {
       const int buf = ck & 1;
+#ifdef NLD_EXP_NOSTAGE
+      if (ck == 0 && nchunk > 1) {
+#else
       if (ck + 1 < nchunk) {
+#endif
         stage(ck + 1, buf ^ 1);
         cp_wait<1>();
       } else {
@@ -167,10 +189,18 @@ k_spread_mma(const SubDev* __restrict__ subs, const WinDev* __restrict__ wins,
           const double aw = row[2 * kS + g];
           double af[RPW];
 #pragma unroll
-          for (int q = 0; q < RPW; ++q) af[q] = V[j * rpp + q0 + q] * aw;
+#ifdef NLD_EXP_NODMUL
+          for (int q = 0; q < RPW; ++q) af[q] = q ? aw : V[j * vst + q0 + q];
+#else
+          for (int q = 0; q < RPW; ++q) af[q] = V[j * vst + q0 + q] * aw;
+#endif
 #pragma unroll
           for (int n = 0; n < 8; ++n) {
+#ifdef NLD_EXP_NODMUL
+            const double bf = n & 1 ? bw[n] : cw;
+#else
             const double bf = bw[n] * cw;
+#endif
 #pragma unroll
             for (int q = 0; q < RPW; ++q) dmma(acc[q][n], af[q], bf);
           }
@@ -211,6 +241,154 @@ k_spread_mma(const SubDev* __restrict__ subs, const WinDev* __restrict__ wins,
       }
       __syncthreads();
     }
+  }
+}
+
+// ---- spread with shared (B (x) C) operands (16 rhs per pass) --------------
+// Same product as k_spread_mma<2, 8>, but the B-fragments B_j[b] C_j[c] --
+// identical for all 8 warps (they differ only in their rhs) -- are formed
+// once per CTA into shared memory instead of once per warp, so the DMULs
+// that share the fp64 pipe with DMMA drop from 10 to 3 per 16 DMMA.
+// Software pipeline over chunks of 48 nodes, one barrier per chunk:
+//   iteration ck: cp.async raw rows of chunk ck+2 and v lines of chunk ck+1;
+//                 DMMA over chunk ck from BCA[ck&1] (B (x) C | A rows);
+//                 in the middle, each warp forms BCA of 6 nodes of chunk
+//                 ck+1 from the raw rows (no separate phase: the other warps
+//                 keep the tensor pipe busy meanwhile);
+//                 wait for the copies, barrier.
+// BCA rows are 76 doubles (24 banks apart: the 4 nodes of a k-step are
+// conflict-free for the B-fragment and A reads).
+constexpr int kBcChunk = 48;
+constexpr int kBcRow = 76;
+constexpr int kBcV = 18;          // v row stride: 16 rhs + 2 (bank spread)
+
+__host__ __device__ constexpr int spread_bc_smem() {
+  return 2 * kBcChunk * kRow + 2 * kBcChunk * kBcV + 2 * kBcChunk * kBcRow;
+}
+
+__global__ void __launch_bounds__(256, 2)
+k_spread_bc(const SubDev* __restrict__ subs, const WinDev* __restrict__ wins,
+            const double* __restrict__ rows, const int32_t* __restrict__ pix,
+            const double* __restrict__ vt, int nrhs, double* __restrict__ blocks) {
+  extern __shared__ __align__(16) double sm[];
+  double* const raw = sm;                                  // [2][48][24]
+  double* const sv = sm + 2 * kBcChunk * kRow;             // [2][48][18]
+  double* const bca = sv + 2 * kBcChunk * kBcV;            // [2][48][76]
+  const SubDev sd = subs[blockIdx.x];
+  const WinDev wd = wins[sd.win];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int64_t local = sd.start - wd.node_off;
+  const double* __restrict__ rw = rows + wd.row_off + local * kRow;
+  const int32_t* __restrict__ pw = pix + sd.start;
+  const int nchunk = (sd.count + kBcChunk - 1) / kBcChunk;
+  auto chunk_n = [&](int ck) { return min(kBcChunk, sd.count - ck * kBcChunk); };
+
+  for (int rg = 0; rg < nrhs; rg += 16) {
+    double acc[2][8][2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q)
+#pragma unroll
+      for (int n = 0; n < 8; ++n) acc[q][n][0] = acc[q][n][1] = 0.0;
+
+    auto stage_raw = [&](int ck) {
+      if (ck >= nchunk) return;
+      const double* src = rw + (int64_t)ck * kBcChunk * kRow;
+      double* dst = raw + (ck & 1) * kBcChunk * kRow;
+      for (int e = tid; e < chunk_n(ck) * (kRow / 2); e += 256) cp_async16(dst + 2 * e, src + 2 * e);
+    };
+    auto stage_v = [&](int ck) {
+      if (ck >= nchunk) return;
+      const int c0 = ck * kBcChunk, cn = chunk_n(ck);
+      double* dst = sv + (ck & 1) * kBcChunk * kBcV;
+      for (int e = tid; e < cn * 8; e += 256) {
+        const int pt = e >> 3, q = (e & 7) * 2;
+        cp_async16(dst + pt * kBcV + q, vt + (int64_t)pw[c0 + pt] * nrhs + rg + q);
+      }
+      // pad to a multiple of 4 nodes with v = 0 (uninitialised smem could be NaN)
+      for (int e = tid; e < (((cn + 3) & ~3) - cn) * kBcV; e += 256) dst[cn * kBcV + e] = 0.0;
+    };
+    // this warp's 6 nodes of chunk ck: BCA[p] = [B(x)C | A | pad]
+    auto form_bca = [&](int ck) {
+      if (ck >= nchunk) return;
+      const int cn = chunk_n(ck);
+      const double* R = raw + (ck & 1) * kBcChunk * kRow;
+      double* O = bca + (ck & 1) * kBcChunk * kBcRow;
+#pragma unroll
+      for (int i = 0; i < 6; ++i) {
+        const int e = lane + 32 * i;             // 192 pairs = 6 nodes x 32
+        const int p = warp * 6 + (e >> 5), pr = e & 31;
+        const int b = pr >> 2, c = (pr & 3) * 2;
+        double2 o;
+        if (p < cn) {
+          const double bw = R[p * kRow + kS + b];
+          const double2 cw = *reinterpret_cast<const double2*>(R + p * kRow + 2 * kS + c);
+          o.x = bw * cw.x;
+          o.y = bw * cw.y;
+        } else {
+          o.x = o.y = 0.0;
+        }
+        *reinterpret_cast<double2*>(O + p * kBcRow + b * 8 + c) = o;
+      }
+      if (lane < 24) {
+        const int p = warp * 6 + (lane >> 2), a = (lane & 3) * 2;
+        double2 o;
+        if (p < cn) o = *reinterpret_cast<const double2*>(R + p * kRow + a);
+        else o.x = o.y = 0.0;
+        *reinterpret_cast<double2*>(O + p * kBcRow + 64 + a) = o;
+      }
+    };
+
+    // prologue: BCA(0) formed, raw(1) and v(0) resident
+    stage_raw(0);
+    stage_v(0);
+    cp_commit();
+    stage_raw(1);
+    cp_commit();
+    cp_wait<1>();
+    __syncthreads();
+    form_bca(0);
+    cp_wait<0>();
+    __syncthreads();
+
+    for (int ck = 0; ck < nchunk; ++ck) {
+      stage_raw(ck + 2);     // raw buffer ck&1: chunk ck's rows were consumed by form_bca(ck)
+      stage_v(ck + 1);
+      cp_commit();
+      const int nks = (chunk_n(ck) + 3) >> 2;
+      const double* B = bca + (ck & 1) * kBcChunk * kBcRow;
+      const double* V = sv + (ck & 1) * kBcChunk * kBcV + 2 * warp;
+      auto kstep = [&](int ks) {
+        const int j = ks * 4 + t;
+        const double* row = B + j * kBcRow;
+        const double aw = row[64 + g];
+        const double2 vv = *reinterpret_cast<const double2*>(V + j * kBcV);
+        const double af0 = vv.x * aw, af1 = vv.y * aw;
+#pragma unroll
+        for (int n = 0; n < 8; ++n) {
+          const double bf = row[n * 8 + g];
+          dmma(acc[0][n], af0, bf);
+          dmma(acc[1][n], af1, bf);
+        }
+      };
+      const int half = nks >> 1;
+#pragma unroll 2
+      for (int ks = 0; ks < half; ++ks) kstep(ks);
+      form_bca(ck + 1);
+#pragma unroll 2
+      for (int ks = half; ks < nks; ++ks) kstep(ks);
+      cp_wait<0>();
+      __syncthreads();
+    }
+    // block element (a = g, b = n, c = 2t + i), rhs rg + 2 warp + q
+#pragma unroll
+    for (int q = 0; q < 2; ++q)
+#pragma unroll
+      for (int n = 0; n < 8; ++n)
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+          blocks[(sd.block + (g * 8 + n) * 8 + 2 * t + i) * nrhs + rg + 2 * warp + q] = acc[q][n][i];
+    __syncthreads();   // smem reuse by the next rhs group
   }
 }
 
@@ -335,6 +513,50 @@ k_gather_mma(const SubDev* __restrict__ subs, const CellDev* __restrict__ cells,
   }
 }
 
+// ---- fused gather epilogue ------------------------------------------------
+// The window sum and the degree / shift terms fused into the gather (the
+// separate epilogue pass re-read L window outputs + v from HBM).  The output
+// buffer itself accumulates the windows, pixel-major [N][nrhs]:
+//   kGatherStore    : wout[win] = G_w v          (unfused, per-window buffers)
+//   kGatherFirst    : out  = G_0 v
+//   kGatherAccum    : out += G_w v
+//   kGatherFinal    : out  = epi(out + G_{L-1} v)   (kind's formula)
+enum GatherMode { kGatherStore = 0, kGatherFirst = 1, kGatherAccum = 2, kGatherFinal = 3 };
+
+struct GatherEpi {
+  int mode;
+  int kind;
+  int L;
+  const double* v;      // pixel-major [N][nrhs]
+  const double* eta;    // [N] (SYSTEM / LAPLACIAN)
+  const double* coef;   // [nrhs][2] (lam, mu) for SYSTEM
+};
+
+// y from the window sum s (unit diagonals included) and x = v, kernel.py:118-127
+// (Gamma = (sum_l G_l - L I) / L) and linops.py:43-50
+__device__ __forceinline__ double epi_value(int kind, int L, double s, double x, double eta_i,
+                                            double lam, double mu) {
+  if (kind == NLD_APPLY_WINDOW_SUM) return s;
+  const double gam = (s - (double)L * x) / (double)L;
+  if (kind == NLD_APPLY_SYSTEM) return lam * x + mu * (eta_i * x - gam);
+  if (kind == NLD_APPLY_LAPLACIAN) return eta_i * x - gam;
+  return gam;
+}
+
+__device__ __forceinline__ void gather_put(const GatherEpi& ep, double* o, int64_t e, int64_t i,
+                                           int r, double val) {
+  if (ep.mode == kGatherStore || ep.mode == kGatherFirst) {
+    o[e] = val;
+  } else if (ep.mode == kGatherAccum) {
+    o[e] += val;
+  } else {
+    const double s = o[e] + val;
+    const double lam = ep.coef ? ep.coef[2 * r] : 0.0, mu = ep.coef ? ep.coef[2 * r + 1] : 0.0;
+    const double et = (ep.kind == NLD_APPLY_SYSTEM || ep.kind == NLD_APPLY_LAPLACIAN) ? ep.eta[i] : 0.0;
+    o[e] = epi_value(ep.kind, ep.L, s, ep.v[e], et, lam, mu);
+  }
+}
+
 // ---- gather, right-hand sides as the M dimension (nrhs >= 8) -------------
 // D[r][j] = sum_{k=(a,b,c)} G_r[k] W_j[k],  W_j = A_j (x) B_j (x) C_j.
 // M = 16 rhs (2 m-tiles), N = 8 nodes, K = 512 (128 k-steps).  The W
@@ -348,7 +570,8 @@ __global__ void __launch_bounds__(kGaThreads, 2)
 k_gather_mma16(const SubDev* __restrict__ subs, const CellDev* __restrict__ cells,
                const WinDev* __restrict__ wins, const double* __restrict__ rows,
                const int32_t* __restrict__ pix, const double* __restrict__ grid,
-               int64_t grid_ld, double* __restrict__ wout, int64_t N, int nrhs) {
+               int64_t grid_ld, double* __restrict__ wout, int64_t N, int nrhs,
+               GatherEpi ep) {
   extern __shared__ __align__(16) double gb[];   // [16][kGRow]
   const SubDev sd = subs[blockIdx.x];
   const CellDev cd = cells[sd.cell];
@@ -357,7 +580,7 @@ k_gather_mma16(const SubDev* __restrict__ subs, const CellDev* __restrict__ cell
   const int g = lane >> 2, t = lane & 3;
   const int64_t local = sd.start - wd.node_off;
   const double* __restrict__ rw = rows + wd.row_off + local * kRow;
-  double* __restrict__ out = wout + (int64_t)sd.win * N * nrhs;
+  double* __restrict__ out = wout + (ep.mode == kGatherStore ? (int64_t)sd.win * N * nrhs : 0);
   const int ntile = (sd.count + 7) >> 3;
   for (int rg = 0; rg < nrhs; rg += 16) {
     const int rn = min(16, nrhs - rg);
@@ -414,7 +637,11 @@ k_gather_mma16(const SubDev* __restrict__ subs, const CellDev* __restrict__ cell
         const double wa = aw[a];
 #pragma unroll
         for (int ks = 0; ks < 16; ++ks) {
+#ifdef NLD_EXP_GNODMUL
+          const double w = (a & 1) ? bc[ks] : wa;
+#else
           const double w = bc[ks] * wa;
+#endif
           const int k = a * 64 + 4 * ks;
           dmma(acc[0][ks & 3], G0[k], w);
           if (two) dmma(acc[1][ks & 3], G1[k], w);
@@ -424,12 +651,13 @@ k_gather_mma16(const SubDev* __restrict__ subs, const CellDev* __restrict__ cell
       for (int i = 0; i < 2; ++i) {
         const int j = j0 + 2 * t + i;
         if (j >= sd.count) continue;
-        double* o = out + (int64_t)pix[sd.start + j] * nrhs + rg;
+        const int64_t px = pix[sd.start + j];
 #pragma unroll
         for (int m = 0; m < 2; ++m) {
           const int r = m * 8 + g;
           if (r < rn)
-            o[r] = (acc[m][0][i] + acc[m][1][i]) + (acc[m][2][i] + acc[m][3][i]);
+            gather_put(ep, out, px * nrhs + rg + r, px, rg + r,
+                       (acc[m][0][i] + acc[m][1][i]) + (acc[m][2][i] + acc[m][3][i]));
         }
       }
     }

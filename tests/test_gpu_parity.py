@@ -385,3 +385,42 @@ def test_pixel_major_layout_matches_rhs_major():
     g = op.apply_device(V, _lib.APPLY_GAMMA, 5)
     h = op.apply_device(V.T.contiguous(), _lib.APPLY_GAMMA, 5, pixel_major=True)
     assert torch.allclose(g, h.T, rtol=1e-14, atol=0)
+
+
+def _edge_two_windows():
+    """Two 3-D windows whose nodes include exact grid-line (edge) nodes:
+    the golden edge set (make_golden.edge_case) and its half-scaled copy."""
+    rng = np.random.default_rng(7)
+    r = 0.21875
+    anchors = np.array([[r, 0, 0], [-r, 0, 0], [0, 0.1, 0], [0, -0.1, 0],
+                        [0, 0, 0.1], [0, 0, -0.1]])
+    body = rng.uniform(-0.1, 0.1, size=(400, 3))
+    on_grid = rng.integers(-6, 7, size=(60, 3)) / 64.0
+    pts = np.clip(np.concatenate([anchors, body, on_grid]), -r, r)
+    return np.concatenate([pts, pts * 0.5], axis=1), [np.arange(3), np.arange(3, 6)]
+
+
+@pytest.mark.parametrize("nrhs", [16, 24])
+@pytest.mark.parametrize("case", ["c1", "edges"])
+def test_fused_gather_epilogue(case, nrhs):
+    """Pixel-major batches of >= 8 rhs take the fused gather epilogue (window
+    sum + degree/shift inside the last window's gather); it must equal the
+    rhs-major path with its separate epilogue, for every product kind."""
+    from paper_2407_06834_b200 import _lib
+    if case == "c1":
+        op = operator("c1")[0]
+    else:
+        feats, wins = _edge_two_windows()
+        op = nld.AnovaOperator(feats, wins, 0.1, **PIN)
+    rng = np.random.default_rng(nrhs)
+    V = torch.from_numpy(rng.standard_normal((nrhs, op.n))).cuda()
+    coef = np.stack([rng.uniform(0.5, 2, nrhs), rng.uniform(0, 0.01, nrhs)], 1).ravel()
+    for kind in (_lib.APPLY_GAMMA, _lib.APPLY_GAMMA_SQUARED, _lib.APPLY_SYSTEM,
+                 _lib.APPLY_LAPLACIAN, _lib.APPLY_WINDOW_SUM):
+        c = coef if kind == _lib.APPLY_SYSTEM else None
+        a = op.apply_device(V, kind, nrhs, c)
+        b = op.apply_device(V.T.contiguous(), kind, nrhs, c, pixel_major=True)
+        err = float((a - b.T).norm() / a.norm())
+        assert err < 1e-14, (kind, err)
+    if case == "edges":
+        assert op.window_info(0)["n_edge"] > 0 and op.window_info(1)["n_edge"] > 0
