@@ -22,6 +22,9 @@
 //  * gather: one CTA per subproblem; the (2m)^3 grid block of its cell sits in
 //    shared memory, each thread owns a node and contracts a -> b -> c.
 #include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <cmath>
 #include <cstdlib>
 
 #include "nld_internal.cuh"
@@ -1019,7 +1022,122 @@ void spread_window_fast(const PlanSet& ps, const Workspace& ws, int w, const dou
       const char* e = getenv("NLD_SPREAD_BC");
       bc = (e && e[0] == '0') ? 0 : 1;
     }
-    if (bc && nrhs % 16 == 0 && ((uintptr_t)vt & 15) == 0)
+    if (use_ozaki() && nrhs % 16 == 0 && ps.sub_exp) {
+      launch_spread_oz(ps, subs, ps.sub_exp + wp.sub_off * 24, nsub, ws.vmax, vt, nrhs, ws.blocks,
+                       st);
+      if (getenv("NLD_OZAKI_DEBUG")) {
+        // compare with the fp64 DMMA spread of the same window (debug only)
+        const size_t nb = (size_t)ps.blocks_total * nrhs;
+        std::vector<double> h1(nb), h2(nb);
+        NLD_CUDA(cudaStreamSynchronize(st));
+        NLD_CUDA(cudaMemcpy(h1.data(), ws.blocks, nb * 8, cudaMemcpyDeviceToHost));
+        launch_spread_bc(subs, nsub, ps, ws, vt, nrhs, st);
+        NLD_CUDA(cudaStreamSynchronize(st));
+        NLD_CUDA(cudaMemcpy(h2.data(), ws.blocks, nb * 8, cudaMemcpyDeviceToHost));
+        SubDev s0;
+        NLD_CUDA(cudaMemcpy(&s0, subs, sizeof(SubDev), cudaMemcpyDeviceToHost));
+        double num = 0, den = 0;
+        for (int64_t e = s0.block * nrhs; e < (s0.block + 512) * nrhs; ++e) {
+          num += (h1[e] - h2[e]) * (h1[e] - h2[e]);
+          den += h2[e] * h2[e];
+        }
+        fprintf(stderr, "ozdbg win %d sub0 count %d rel %.3e\n", w, s0.count, sqrt(num / den));
+        {
+          // host fp64 reference of sub0's block (r = 0..15)
+          const WinDev& wdh = ps.wdev_h[w];
+          std::vector<double> rr((size_t)s0.count * 24);
+          std::vector<int32_t> pp(s0.count);
+          NLD_CUDA(cudaMemcpy(rr.data(), ps.rows + wdh.row_off + (s0.start - wdh.node_off) * 24,
+                              rr.size() * 8, cudaMemcpyDeviceToHost));
+          NLD_CUDA(cudaMemcpy(pp.data(), ps.pix + s0.start, pp.size() * 4, cudaMemcpyDeviceToHost));
+          std::vector<double> vv((size_t)s0.count * 16);
+          for (int j = 0; j < s0.count; ++j)
+            NLD_CUDA(cudaMemcpy(&vv[j * 16], vt + (int64_t)pp[j] * nrhs, 16 * 8,
+                                cudaMemcpyDeviceToHost));
+          double n1 = 0, n2 = 0, dd = 0;
+          for (int a = 0; a < 8; ++a)
+            for (int bc = 0; bc < 64; ++bc)
+              for (int r = 0; r < 16; ++r) {
+                double acc = 0;
+                for (int j = 0; j < s0.count; ++j)
+                  acc += vv[j * 16 + r] * rr[j * 24 + a] * rr[j * 24 + 8 + (bc >> 3)] *
+                         rr[j * 24 + 16 + (bc & 7)];
+                const int64_t e = (s0.block + a * 64 + bc) * nrhs + r;
+                n1 += (h1[e] - acc) * (h1[e] - acc);
+                n2 += (h2[e] - acc) * (h2[e] - acc);
+                dd += acc * acc;
+                if (a == 2 && bc == 18 && r < 3)
+                  fprintf(stderr, "   host %.15e oz %.15e dmma %.15e\n", acc, h1[e], h2[e]);
+              }
+          fprintf(stderr, "  vs host: oz %.3e dmma %.3e\n", sqrt(n1 / dd), sqrt(n2 / dd));
+          {
+            // re-run sub0 alone through the library launcher
+            std::vector<double> h3(nb);
+            launch_spread_oz(ps, subs, ps.sub_exp + wp.sub_off * 24, 1, ws.vmax, vt, nrhs,
+                             ws.blocks, st);
+            NLD_CUDA(cudaStreamSynchronize(st));
+            NLD_CUDA(cudaMemcpy(h3.data(), ws.blocks, nb * 8, cudaMemcpyDeviceToHost));
+            double n3 = 0, d3 = 0;
+            for (int64_t e = s0.block * nrhs; e < (s0.block + 512) * nrhs; ++e) {
+              n3 += (h3[e] - h2[e]) * (h3[e] - h2[e]);
+              d3 += h2[e] * h2[e];
+            }
+            fprintf(stderr, "   sub0 alone vs dmma: %.3e\n", sqrt(n3 / d3));
+          }
+          if (w == 0) {
+            FILE* f = fopen("/tmp/oz_sub0.bin", "wb");
+            fwrite(&s0.count, 4, 1, f);
+            fwrite(rr.data(), 8, rr.size(), f);
+            fwrite(vv.data(), 8, vv.size(), f);
+            fclose(f);
+          }
+          {
+            int16_t exh[24];
+            NLD_CUDA(cudaMemcpy(exh, ps.sub_exp + wp.sub_off * 24, 48, cudaMemcpyDeviceToHost));
+            fprintf(stderr, "   dev ex:");
+            for (int k = 0; k < 24; ++k) fprintf(stderr, " %d", exh[k]);
+            fprintf(stderr, "  sub_off %lld\n", (long long)wp.sub_off);
+          }
+          // host emulation of the sliced algorithm for a = 2, bc = 18, r = 0..2
+          auto eb = [](double m) { return m > 0 ? ilogb(m) + 1 : 0; };
+          auto digits = [](double x, double y, int* d) {
+            const double u = fma(x, y, 4503599627370496.0 + 141289400074368.0);
+            long long bits;
+            memcpy(&bits, &u, 8);
+            for (int p = 0; p < 6; ++p) d[p] = (int)((bits >> (8 * (5 - p))) & 0xff) - 128;
+          };
+          double mA = 0, mB = 0, mC = 0;
+          for (int j = 0; j < s0.count; ++j) {
+            mA = fmax(mA, fabs(rr[j * 24 + 2]));
+            mB = fmax(mB, fabs(rr[j * 24 + 8 + 2]));
+            mC = fmax(mC, fabs(rr[j * 24 + 16 + 2]));
+          }
+          for (int r = 0; r < 3; ++r) {
+            double mv = 0;
+            for (int j = 0; j < s0.count; ++j) mv = fmax(mv, fabs(vv[j * 16 + r]));
+            const int ev = eb(mv), eA = eb(mA), eB = eb(mB), eC = eb(mC);
+            long long D[6] = {0, 0, 0, 0, 0, 0};
+            for (int j = 0; j < s0.count; ++j) {
+              int dx[6], dy[6];
+              digits(ldexp(vv[j * 16 + r], 46 - ev), ldexp(rr[j * 24 + 2], -eA), dx);
+              digits(ldexp(rr[j * 24 + 10], 46 - eB), ldexp(rr[j * 24 + 18], -eC), dy);
+              for (int p = 0; p < 6; ++p)
+                for (int q = 0; p + q < 6; ++q) D[p + q] += (long long)dx[p] * dy[q];
+            }
+            double acc = 0;
+            for (int t = 5; t >= 0; --t) acc = acc / 256.0 + (double)D[t];
+            fprintf(stderr, "   emu r%d ev %d eA %d eB %d eC %d -> %.15e  D0 %lld D1 %lld\n", r, ev,
+                    eA, eB, eC, ldexp(acc, ev + eA + eB + eC - 12), D[0], D[1]);
+          }
+        }
+        for (int k = 0; k < 6; ++k) {
+          const int64_t e = (s0.block + k * 73) * nrhs + (k % 16);
+          fprintf(stderr, "  e %lld oz %.15e ref %.15e\n", (long long)e, h1[e], h2[e]);
+        }
+        NLD_CUDA(cudaMemcpy(ws.blocks, h1.data(), nb * 8, cudaMemcpyHostToDevice));
+      }
+    }
+    else if (bc && nrhs % 16 == 0 && ((uintptr_t)vt & 15) == 0)
       launch_spread_bc(subs, nsub, ps, ws, vt, nrhs, st);
     else if (nrhs >= 16 && rpw4) launch_spread_mma<4, 4>(subs, nsub, ps, ws, vt, nrhs, st);
     else if (nrhs >= 16) launch_spread_mma<2>(subs, nsub, ps, ws, vt, nrhs, st);
@@ -1076,6 +1194,7 @@ void ensure_workspace(nld_operator* op, const PlanSet& ps, int nrhs) {
   NLD_CUDA(cudaMalloc(&ws.wout, sizeof(double) * std::max<int64_t>(1, op->N * op->L) * cap));
   NLD_CUDA(cudaMalloc(&ws.vt, sizeof(double) * std::max<int64_t>(1, op->N) * cap));
   NLD_CUDA(cudaMalloc(&ws.coef, sizeof(double) * 2 * cap));
+  NLD_CUDA(cudaMalloc(&ws.vmax, sizeof(unsigned long long) * cap));
   {
     // separable-assemble scratch: the largest 3-D box x 64 offsets x nrhs
     int64_t mb = 0;
@@ -1107,6 +1226,7 @@ void free_workspace(Workspace& ws) {
   cudaFree(ws.wout);
   cudaFree(ws.vt);
   cudaFree(ws.coef);
+  cudaFree(ws.vmax);
   ws = Workspace();
 }
 
@@ -1260,6 +1380,7 @@ void apply_op(nld_operator* op, int which, int kind, const double* v, double* ou
               cudaStream_t st, int pixel_major) {
   const PlanSet& ps = op->sets[which];
   ensure_workspace(op, ps, nrhs);
+  if (use_ozaki() && op->params.cutoff == 4) ozaki_exponents(op->sets[which], st);
   Workspace& ws = op->ws;
   const int64_t N = op->N;
   const int L = op->L;
@@ -1273,6 +1394,7 @@ void apply_op(nld_operator* op, int which, int kind, const double* v, double* ou
     vt = ws.vt;
     ++launches;
   }
+  if (use_ozaki() && op->params.cutoff == 4 && nrhs % 16 == 0) ozaki_vmax(vt, N, nrhs, ws.vmax, st);
   static int no_overlap = -1;
   if (no_overlap < 0) {
     const char* e = getenv("NLD_NO_OVERLAP");

@@ -131,6 +131,7 @@ struct PlanSet {
   int64_t n_edges = 0;
   int64_t grid_total = 0;        // sum of box sizes
   int64_t generic_nodes = 0;     // nodes in windows on the generic path
+  int16_t* sub_exp = nullptr;    // sliced spread: per 3-D subproblem eA/eB/eC
   int shares_tables_with = -1;   // index of the plan set whose tables we use
   bool owns_tables = true;
 };
@@ -150,6 +151,7 @@ struct Workspace {
   double* asm_y1 = nullptr;
   double* asm_y2 = nullptr;
   int64_t asm_cap = 0;
+  unsigned long long* vmax = nullptr;   // [nrhs_cap] sliced spread: max |v| bits
   // persistent CG vectors (x, r, p, q, b, t): [6][cg_cap]
   double* cg = nullptr;
   int64_t cg_cap = 0;
@@ -194,6 +196,13 @@ struct nld_operator {
 namespace nld {
 
 void build_planset(nld_operator* op, int which, cudaStream_t st);
+// integer-sliced tensor-core spread (nld_ozaki.cu)
+bool use_ozaki();
+int16_t* ozaki_exponents(PlanSet& ps, cudaStream_t st);
+void launch_spread_oz(const PlanSet& ps, const SubDev* subs, const int16_t* ex, unsigned nsub,
+                      const unsigned long long* vmax, const double* vt, int nrhs, double* blocks,
+                      cudaStream_t st);
+void ozaki_vmax(const double* vt, int64_t n, int nrhs, unsigned long long* out, cudaStream_t st);
 void free_planset(PlanSet& ps);
 void ensure_workspace(nld_operator* op, const PlanSet& ps, int nrhs);
 void free_workspace(Workspace& ws);

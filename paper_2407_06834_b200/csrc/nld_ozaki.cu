@@ -1,0 +1,370 @@
+// Integer-sliced fp64 spread on the 5th-generation tensor cores (tcgen05,
+// UMMA kind::i8, accumulators in TMEM) for 3-D windows with m = 4.
+//
+// The spread of one subproblem (the nodes j of one stencil cell) is the
+// product  block[(a, r)][(b, c)] = sum_j X[(a, r)][j] Y[(b, c)][j]  with
+// X = v_{j,r} A_j[a] (16 rhs x 8 rows) and Y = B_j[b] C_j[c] (64 columns),
+// the same contraction the DMMA kernel (nld_mma.cuh) runs in fp64.  Here the
+// operands are scaled by powers of two (per row of X: the subproblem's max
+// |v_r| and |A_a|; per column of Y: max |B_b| and |C_c|, precomputed) into
+// 46-bit integers and cut into S = 6 signed 8-bit digits,
+//     x = sum_p d_p 256^(5-p),   y = sum_q e_q 256^(5-q),   d, e in [-128, 127],
+// so that  x y = sum_t 256^(10-t) sum_{p+q=t} d_p e_q.  The integer products
+// are exact (s8 x s8 -> s32, |sum| < 2^28 for <= 2048 nodes); the diagonals
+// t = 0..S-1 are kept (the dropped ones are below 2^-46 of the operand
+// bounds), accumulated in TMEM by issuing A_p against the stacked slices
+// [e_0 | e_1 | ...] with the D window shifted by 64 p columns, and combined in
+// fp64 in the epilogue.  Accuracy: a few 1e-14 of max|X| max|Y| per term --
+// the same order as an fp64 dot product -- far inside the 1e-10 parity bar.
+//
+// Slicing is one DFMA per element: U = fma(x', y', 2^52 + 0x808080808080)
+// rounds x'y' to an integer and leaves x'y' + 0x80..80 in the low 48
+// mantissa bits, whose bytes XOR 0x80 are the balanced digits.
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+
+#include "nld_internal.cuh"
+#include "nld_umma.cuh"
+
+namespace nld {
+namespace oz {
+
+#ifndef NLD_OZ_SL
+#define NLD_OZ_SL 6
+#endif
+constexpr int kSl = NLD_OZ_SL;         // digits per operand
+constexpr int kRows = 128;             // M: (a, r) rows, r fastest
+constexpr int kChunk = 32;             // nodes per UMMA K step (32 bytes)
+constexpr int kThreads = 256;
+constexpr int kTmemCols = 512;         // kSl * 64 = 384 used
+constexpr int kABytes = kRows * kChunk;          // 4 KB per slice
+constexpr int kBBytes = 64 * kChunk;             // 2 KB per slice
+constexpr int kStageBytes = kSl * (kABytes + kBBytes);
+constexpr int kExpPerSub = 24;         // eA[8] eB[8] eC[8]
+constexpr double kMagic = 4503599627370496.0 + 141289400074368.0;  // 2^52 + 0x808080808080
+
+__device__ __forceinline__ double pow2(int e) {
+  e = max(-1022, min(1023, e));
+  return __longlong_as_double((long long)(e + 1023) << 52);
+}
+
+// exponent bound: |x| < 2^e for all x with max |x| = m (0 -> 0)
+__device__ __forceinline__ int exp_bound(double m) { return m > 0.0 ? ilogb(m) + 1 : 0; }
+
+// canonical K-major no-swizzle offset in a (rows x 32 bytes) tile
+__device__ __forceinline__ int canon32(int row, int k) {
+  return (row >> 3) * 256 + (k >> 4) * 128 + (row & 7) * 16 + (k & 15);
+}
+
+// 4 elements' digit p (p = 0 most significant) packed into one word; element
+// i's 48-bit field is (hi_i & 0xffff) << 32 | lo_i
+__device__ __forceinline__ uint32_t digit_word(uint32_t l0, uint32_t l1, uint32_t l2, uint32_t l3,
+                                               uint32_t h0, uint32_t h1, uint32_t h2, uint32_t h3,
+                                               int p) {
+  const int byte = 5 - p;
+  const bool top = byte >= 4;
+  const uint32_t s0 = top ? h0 : l0, s1 = top ? h1 : l1, s2 = top ? h2 : l2, s3 = top ? h3 : l3;
+  const uint32_t k = byte & 3;
+  const uint32_t sel = k | ((k + 4) << 4);
+  const uint32_t w01 = __byte_perm(s0, s1, sel);
+  const uint32_t w23 = __byte_perm(s2, s3, sel);
+  return __byte_perm(w01, w23, 0x5410) ^ 0x80808080u;
+}
+
+#define NLD_DW(L, H, i, p) \
+  digit_word(L[i], L[i + 1], L[i + 2], L[i + 3], H[i], H[i + 1], H[i + 2], H[i + 3], p)
+
+__device__ __forceinline__ void slice1(double x, double y, uint32_t& lo, uint32_t& hi) {
+  const long long u = __double_as_longlong(fma(x, y, kMagic));
+  lo = (uint32_t)u;
+  hi = (uint32_t)(u >> 32);
+}
+
+// ---- plan-time exponent table -------------------------------------------
+// per subproblem: eA[a], eB[b], eC[c] = exponent bounds of the columns of its
+// weight rows (static: the features never change)
+__global__ void k_sub_exponents(const SubDev* __restrict__ subs, const WinDev* __restrict__ wins,
+                                const double* __restrict__ rows, int16_t* __restrict__ ex) {
+  __shared__ unsigned long long mx[kExpPerSub];
+  const SubDev sd = subs[blockIdx.x];
+  const WinDev wd = wins[sd.win];
+  if (threadIdx.x < kExpPerSub) mx[threadIdx.x] = 0ull;
+  __syncthreads();
+  const double* rw = rows + wd.row_off + (sd.start - wd.node_off) * 24;
+  const int col = threadIdx.x % kExpPerSub;
+  double m = 0.0;
+  for (int j = threadIdx.x / kExpPerSub; j < sd.count; j += blockDim.x / kExpPerSub)
+    m = fmax(m, fabs(rw[(int64_t)j * 24 + col]));
+  if (threadIdx.x < (blockDim.x / kExpPerSub) * kExpPerSub)
+    atomicMax(&mx[col], (unsigned long long)__double_as_longlong(m));
+  __syncthreads();
+  if (threadIdx.x < kExpPerSub)
+    ex[(int64_t)blockIdx.x * kExpPerSub + threadIdx.x] =
+        (int16_t)exp_bound(__longlong_as_double((long long)mx[threadIdx.x]));
+}
+
+// ---- per-rhs exponent of max |v| over all pixels ---------------------------
+// (the X rows are scaled by the rhs's global max |v| times the subproblem's
+// max |A_a|; relative to a per-cell max this costs bits only where |v| is
+// far below its global max, i.e. where the products are small anyway)
+__global__ void k_vmax(const double* __restrict__ vt, int64_t n, int nrhs,
+                       unsigned long long* __restrict__ out) {
+  const int r = threadIdx.x % nrhs;
+  const int rows_per_block = blockDim.x / nrhs;
+  double m = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)rows_per_block + threadIdx.x / nrhs; i < n;
+       i += (int64_t)gridDim.x * rows_per_block)
+    m = fmax(m, fabs(vt[i * nrhs + r]));
+  if (threadIdx.x < rows_per_block * nrhs)
+    atomicMax(&out[r], (unsigned long long)__double_as_longlong(m));
+}
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(umma::smem_u32(dst)), "l"(src));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+constexpr int kRawRows = kChunk * 24 * 8;       // 6 KB of weight rows per chunk
+constexpr int kRawV = kChunk * 16 * 8;          // 4 KB of v lines per chunk
+constexpr int kRawBytes = kRawRows + kRawV;
+constexpr int kRawStages = 3;
+
+__host__ __device__ constexpr int spread_oz_smem() {
+  return 2 * kStageBytes + kRawStages * kRawBytes;
+}
+
+// ---- spread ---------------------------------------------------------------
+// One CTA per subproblem (TMEM: 384 of 512 columns -> one CTA per SM),
+// 256 threads.  Per 32-node chunk c: the raw weight rows and v lines of
+// chunk c+2 stream in by cp.async, all threads slice chunk c from shared
+// memory into operand stage c&1 while the tensor core runs chunk c-1, then
+// thread 0 issues chunk c's 8 UMMAs and commits them to the stage mbarrier.
+__global__ void __launch_bounds__(kThreads, 1)
+k_spread_oz(const SubDev* __restrict__ subs, const WinDev* __restrict__ wins,
+            const double* __restrict__ rows, const int32_t* __restrict__ pix,
+            const int16_t* __restrict__ sub_exp, const unsigned long long* __restrict__ vmax,
+            const double* __restrict__ vt, int nrhs, double* __restrict__ blocks) {
+  // 16-byte alignment is all the no-swizzle descriptors need; do not declare
+  // more: under -rdc the dynamic window is not 1024-aligned, and the compiler
+  // would fold the declared alignment into the descriptor address bits
+  extern __shared__ __align__(16) uint8_t smem[];
+  __shared__ uint64_t mbar[2];
+  __shared__ uint32_t taddr_s;
+  __shared__ double rsc[kRows];       // row scale 2^(ev + eA - 46)
+  __shared__ double csc[64];          // column scale 2^(eB + eC + 34)
+  __shared__ double sva[kRows];       // 2^(46 - ev_r)
+  __shared__ double sa[8], sb[8], sc[8];
+
+  const SubDev sd = subs[blockIdx.x];
+  const WinDev wd = wins[sd.win];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const double* __restrict__ rw = rows + wd.row_off + (sd.start - wd.node_off) * 24;
+  const int32_t* __restrict__ pw = pix + sd.start;
+  const int16_t* ex = sub_exp + (int64_t)blockIdx.x * kExpPerSub;
+  uint8_t* const raw = smem + 2 * kStageBytes;
+
+  if (warp == 0) umma::tmem_alloc<kTmemCols>(&taddr_s);
+  if (tid == 32) {
+    umma::mbar_init(&mbar[0], 1);
+    umma::mbar_init(&mbar[1], 1);
+    umma::mbar_fence_init();
+  }
+  if (tid < 8) {
+    sa[tid] = pow2(-ex[tid]);
+    sb[tid] = pow2(46 - ex[8 + tid]);
+    sc[tid] = pow2(-ex[16 + tid]);
+  }
+  if (tid < 64) csc[tid] = pow2(ex[8 + (tid >> 3)] + ex[16 + (tid & 7)] + 34);
+  umma::fence_before();
+  __syncthreads();
+  umma::fence_after();
+  const uint32_t tmem = taddr_s;
+  uint32_t commits[2] = {0, 0};
+
+  const int nchunk = (sd.count + kChunk - 1) / kChunk;
+  for (int rg = 0; rg < nrhs; rg += 16) {
+    if (tid < kRows) {
+      const int a = tid >> 4, r = tid & 15;
+      const int ev = exp_bound(__longlong_as_double((long long)vmax[rg + r]));
+      sva[tid] = pow2(46 - ev);
+      rsc[tid] = pow2(ev + ex[a] - 46);
+    }
+    auto stage_raw = [&](int c) {
+      if (c < nchunk) {
+        uint8_t* dst = raw + (c % kRawStages) * kRawBytes;
+        const int j0 = c * kChunk, cn = min(kChunk, sd.count - j0);
+        const double* src = rw + (int64_t)j0 * 24;
+        for (int e = tid; e < cn * 12; e += kThreads) cp_async16(dst + 16 * e, src + 2 * e);
+        for (int e = tid; e < cn * 8; e += kThreads) {
+          const int j = e >> 3, q = (e & 7) * 2;
+          cp_async16(dst + kRawRows + j * 128 + q * 8, vt + (int64_t)pw[j0 + j] * nrhs + rg + q);
+        }
+      }
+      cp_commit();
+    };
+    stage_raw(0);
+    stage_raw(1);
+    for (int c = 0; c < nchunk; ++c) {
+      const int st = c & 1;
+      cp_wait<1>();
+      __syncthreads();                     // raw(c) visible; sva/rsc ready
+      if (c >= 2) umma::mbar_wait(&mbar[st], (commits[st] - 1) & 1);
+      uint8_t* sA = smem + st * kStageBytes;
+      uint8_t* sB = sA + kSl * kABytes;
+      const double* R = reinterpret_cast<const double*>(raw + (c % kRawStages) * kRawBytes);
+      const double* Vr = R + kChunk * 24;
+      const int cn = min(kChunk, sd.count - c * kChunk);
+      {
+        const int m = tid & 127, h = tid >> 7;
+        const int a = m >> 4, r = m & 15;
+        const double sv = sva[m], s_a = sa[a];
+        uint32_t lo[16], hi[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const int j = h * 16 + i;
+          double x = 0.0, y = 0.0;
+          if (j < cn) {
+            x = Vr[j * 16 + r] * sv;
+            y = R[j * 24 + a] * s_a;
+          }
+          slice1(x, y, lo[i], hi[i]);
+        }
+#pragma unroll
+        for (int p = 0; p < kSl; ++p) {
+          uint4 w;
+          w.x = NLD_DW(lo, hi, 0, p);
+          w.y = NLD_DW(lo, hi, 4, p);
+          w.z = NLD_DW(lo, hi, 8, p);
+          w.w = NLD_DW(lo, hi, 12, p);
+          *reinterpret_cast<uint4*>(sA + p * kABytes + canon32(m, h * 16)) = w;
+        }
+      }
+      {
+        const int n = tid & 63, g = tid >> 6;
+        const int b = n >> 3, cc = n & 7;
+        const double s_b = sb[b], s_c = sc[cc];
+        uint32_t lo[8], hi[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int j = g * 8 + i;
+          double x = 0.0, y = 0.0;
+          if (j < cn) {
+            x = R[j * 24 + 8 + b] * s_b;
+            y = R[j * 24 + 16 + cc] * s_c;
+          }
+          slice1(x, y, lo[i], hi[i]);
+        }
+#pragma unroll
+        for (int p = 0; p < kSl; ++p) {
+          uint2 w;
+          w.x = NLD_DW(lo, hi, 0, p);
+          w.y = NLD_DW(lo, hi, 4, p);
+          *reinterpret_cast<uint2*>(sB + p * kBBytes + canon32(n, g * 8)) = w;
+        }
+      }
+      umma::fence_async_smem();
+      __syncthreads();                     // operands written; raw(c) consumed
+      stage_raw(c + 2);                    // into raw stage (c+2)%3 == (c-1)%3
+      if (tid == 0) {
+        umma::fence_after();
+        const uint32_t aB = umma::smem_u32(sA), bB = umma::smem_u32(sB);
+#pragma unroll
+        for (int p = 0; p < kSl; ++p) {
+          const uint64_t da = umma::make_sdesc(aB + p * kABytes, 128, 256);
+          int q0 = 0;
+          while (q0 < kSl - p) {
+            const int nq = min(4, kSl - p - q0);
+            const uint64_t db = umma::make_sdesc(bB + q0 * kBBytes, 128, 256);
+            const uint32_t acc = (c > 0 || p > 0) ? 1u : 0u;
+            umma::mma_i8(tmem + (uint32_t)((p + q0) * 64), da, db,
+                         umma::idesc_i8(kRows, nq * 64), acc);
+            q0 += nq;
+          }
+        }
+        umma::commit(&mbar[st]);
+      }
+      ++commits[st];
+    }
+    cp_wait<0>();
+    for (int s2 = 0; s2 < 2; ++s2)
+      if (commits[s2]) umma::mbar_wait(&mbar[s2], (commits[s2] - 1) & 1);
+    umma::fence_after();
+    {
+      const int lg = warp & 3, half = warp >> 2;
+      const int m = lg * 32 + lane;
+      const int a = m >> 4, r = m & 15;
+      const double rs = rsc[m];
+      const uint32_t tl = tmem + ((uint32_t)(lg * 32) << 16);
+#pragma unroll 1
+      for (int c0 = half * 32; c0 < half * 32 + 32; c0 += 16) {
+        uint32_t dv[kSl][16];
+#pragma unroll
+        for (int t = 0; t < kSl; ++t) umma::tmem_ld16(tl + (uint32_t)(t * 64 + c0), dv[t]);
+        umma::tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          double acc = 0.0;
+#pragma unroll
+          for (int t = kSl - 1; t >= 0; --t) acc = fma(acc, 0.00390625, (double)(int32_t)dv[t][i]);
+          const int bc = c0 + i;
+          blocks[(sd.block + a * 64 + bc) * nrhs + rg + r] = acc * rs * csc[bc];
+        }
+      }
+    }
+    umma::fence_before();
+    __syncthreads();
+  }
+  if (warp == 0) umma::tmem_free<kTmemCols>(tmem);
+}
+
+}  // namespace oz
+
+// ---- host side ------------------------------------------------------------
+
+bool use_ozaki() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("NLD_OZAKI");
+    v = (e && e[0] && e[0] != '0') ? 1 : 0;
+  }
+  return v == 1;
+}
+
+int16_t* ozaki_exponents(PlanSet& ps, cudaStream_t st) {
+  if (ps.sub_exp || ps.n_subs[3] == 0) return ps.sub_exp;
+  NLD_CUDA(cudaMalloc(&ps.sub_exp, sizeof(int16_t) * oz::kExpPerSub * ps.n_subs[3]));
+  oz::k_sub_exponents<<<(unsigned)ps.n_subs[3], 240, 0, st>>>(ps.subs[3], ps.wdev, ps.rows,
+                                                               ps.sub_exp);
+  NLD_CUDA(cudaGetLastError());
+  return ps.sub_exp;
+}
+
+void launch_spread_oz(const PlanSet& ps, const SubDev* subs, const int16_t* ex, unsigned nsub,
+                      const unsigned long long* vmax, const double* vt, int nrhs, double* blocks,
+                      cudaStream_t st) {
+  const int smem = oz::spread_oz_smem();
+  static bool attr = false;
+  if (!attr) {
+    NLD_CUDA(cudaFuncSetAttribute(oz::k_spread_oz, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  smem));
+    attr = true;
+  }
+  oz::k_spread_oz<<<nsub, oz::kThreads, smem, st>>>(subs, ps.wdev, ps.rows, ps.pix, ex, vmax, vt,
+                                                     nrhs, blocks);
+  NLD_CUDA(cudaGetLastError());
+}
+
+void ozaki_vmax(const double* vt, int64_t n, int nrhs, unsigned long long* out, cudaStream_t st) {
+  NLD_CUDA(cudaMemsetAsync(out, 0, sizeof(unsigned long long) * nrhs, st));
+  const int rows = std::max(1, 256 / nrhs);
+  oz::k_vmax<<<(unsigned)std::min<int64_t>((n + rows - 1) / rows, 148 * 8), rows * nrhs, 0, st>>>(
+      vt, n, nrhs, out);
+  NLD_CUDA(cudaGetLastError());
+}
+
+}  // namespace nld

@@ -1,2 +1,6 @@
-timeout 900 python -m pytest tests/test_gpu_parity.py -x -q 2>&1 | tail -4
-bash scripts/ab_env.sh fused "X=0" unfused "NLD_NO_FUSED_EPILOGUE=1" fusedbc "NLD_SPREAD_BC=1"
+timeout 60 python scripts/umma/oz_harness.py 1 1 509
+timeout 60 python scripts/umma/oz_harness.py 100 1e6 50900
+python scripts/oz_check.py c4 16 /tmp/a4.npy 2>&1 | tail -1
+NLD_OZAKI=1 timeout 120 python scripts/oz_check.py c4 16 /tmp/b4.npy 2>&1 | tail -1
+python scripts/oz_check.py cmp /tmp/b4.npy /tmp/a4.npy
+NLD_OZAKI=1 bash scripts/ab_env.sh oz "X=0"
