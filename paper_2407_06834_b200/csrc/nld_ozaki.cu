@@ -132,7 +132,7 @@ __device__ __forceinline__ void cp_wait() {
 constexpr int kRawRows = kChunk * 24 * 8;       // 6 KB of weight rows per chunk
 constexpr int kRawV = kChunk * 16 * 8;          // 4 KB of v lines per chunk
 constexpr int kRawBytes = kRawRows + kRawV;
-constexpr int kRawStages = 3;
+constexpr int kRawStages = 5;         // raw chunks in flight: kRawStages - 1 ahead
 
 __host__ __device__ constexpr int spread_oz_smem() {
   return 2 * kStageBytes + kRawStages * kRawBytes;
@@ -140,11 +140,32 @@ __host__ __device__ constexpr int spread_oz_smem() {
 
 // ---- spread ---------------------------------------------------------------
 // One CTA per subproblem (TMEM: 384 of 512 columns -> one CTA per SM),
-// 256 threads.  Per 32-node chunk c: the raw weight rows and v lines of
-// chunk c+2 stream in by cp.async, all threads slice chunk c from shared
-// memory into operand stage c&1 while the tensor core runs chunk c-1, then
-// thread 0 issues chunk c's 8 UMMAs and commits them to the stage mbarrier.
-__global__ void __launch_bounds__(kThreads, 1)
+// warp-specialised, mbarrier-pipelined:
+//   warp 9  (loader): cp.async the weight rows and the 16-rhs v lines of
+//           32-node chunks into kRawStages raw stages; each lane's copies
+//           arrive on the stage's `full` barrier when they land
+//           (cp.async.mbarrier.arrive.noinc), so no thread ever waits on them;
+//   warps 0-7 (slicers): wait for a raw chunk, cut X = v A and Y = B C into
+//           digit slices in operand stage c&1, fence to the async proxy and
+//           arrive on the stage's `ready` barrier; after the last chunk they
+//           read TMEM and write the block (epilogue);
+//   warp 8  (issuer): per chunk, one lane issues the 8 UMMAs and commits them
+//           to the stage's `free` barrier (operand stage reusable) and, after
+//           the last chunk, to `acc`.
+constexpr int kSpreadThreads = 320;
+constexpr int kSlicers = 256;
+constexpr int kIssuerWarp = 8;
+constexpr int kLoaderWarp = 9;
+
+__device__ __forceinline__ void cp_async_mbar_arrive(uint64_t* mbar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(umma::smem_u32(mbar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* mbar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(umma::smem_u32(mbar)) : "memory");
+}
+
+__global__ void __launch_bounds__(kSpreadThreads, 1)
 k_spread_oz(const SubDev* __restrict__ subs, const WinDev* __restrict__ wins,
             const double* __restrict__ rows, const int32_t* __restrict__ pix,
             const int16_t* __restrict__ sub_exp, const unsigned long long* __restrict__ vmax,
@@ -153,7 +174,8 @@ k_spread_oz(const SubDev* __restrict__ subs, const WinDev* __restrict__ wins,
   // more: under -rdc the dynamic window is not 1024-aligned, and the compiler
   // would fold the declared alignment into the descriptor address bits
   extern __shared__ __align__(16) uint8_t smem[];
-  __shared__ uint64_t mbar[2];
+  __shared__ uint64_t raw_full[kRawStages], raw_empty[kRawStages];
+  __shared__ uint64_t op_ready[2], op_free[2], acc_full, acc_empty;
   __shared__ uint32_t taddr_s;
   __shared__ double rsc[kRows];       // row scale 2^(ev + eA - 46)
   __shared__ double csc[64];          // column scale 2^(eB + eC + 34)
@@ -167,11 +189,21 @@ k_spread_oz(const SubDev* __restrict__ subs, const WinDev* __restrict__ wins,
   const int32_t* __restrict__ pw = pix + sd.start;
   const int16_t* ex = sub_exp + (int64_t)blockIdx.x * kExpPerSub;
   uint8_t* const raw = smem + 2 * kStageBytes;
+  const int nchunk = (sd.count + kChunk - 1) / kChunk;
+  const int ngroups = nrhs / 16;
 
   if (warp == 0) umma::tmem_alloc<kTmemCols>(&taddr_s);
   if (tid == 32) {
-    umma::mbar_init(&mbar[0], 1);
-    umma::mbar_init(&mbar[1], 1);
+    for (int k = 0; k < kRawStages; ++k) {
+      umma::mbar_init(&raw_full[k], 32);      // one noinc arrive per loader lane
+      umma::mbar_init(&raw_empty[k], kSlicers / 32);
+    }
+    for (int k = 0; k < 2; ++k) {
+      umma::mbar_init(&op_ready[k], kSlicers / 32);
+      umma::mbar_init(&op_free[k], 1);
+    }
+    umma::mbar_init(&acc_full, 1);
+    umma::mbar_init(&acc_empty, kSlicers / 32);
     umma::mbar_fence_init();
   }
   if (tid < 8) {
@@ -184,141 +216,174 @@ k_spread_oz(const SubDev* __restrict__ subs, const WinDev* __restrict__ wins,
   __syncthreads();
   umma::fence_after();
   const uint32_t tmem = taddr_s;
-  uint32_t commits[2] = {0, 0};
 
-  const int nchunk = (sd.count + kChunk - 1) / kChunk;
-  for (int rg = 0; rg < nrhs; rg += 16) {
-    if (tid < kRows) {
-      const int a = tid >> 4, r = tid & 15;
-      const int ev = exp_bound(__longlong_as_double((long long)vmax[rg + r]));
-      sva[tid] = pow2(46 - ev);
-      rsc[tid] = pow2(ev + ex[a] - 46);
-    }
-    auto stage_raw = [&](int c) {
-      if (c < nchunk) {
-        uint8_t* dst = raw + (c % kRawStages) * kRawBytes;
+  if (warp == kLoaderWarp) {
+    // ---------------------------------------------------------------- loader
+    int g = 0;
+    auto pix_at = [&](int c) -> int32_t {
+      const int j = c * kChunk + lane;
+      return (c < nchunk && j < sd.count) ? __ldg(pw + j) : 0;
+    };
+    for (int grp = 0; grp < ngroups; ++grp) {
+      const int rg = grp * 16;
+      int32_t px = pix_at(0);
+      for (int c = 0; c < nchunk; ++c, ++g) {
+        const int32_t px_next = pix_at(c + 1);   // one chunk ahead
+        const int s = g % kRawStages;
+        if (g >= kRawStages) umma::mbar_wait(&raw_empty[s], ((g / kRawStages) - 1) & 1);
+        uint8_t* dst = raw + s * kRawBytes;
         const int j0 = c * kChunk, cn = min(kChunk, sd.count - j0);
         const double* src = rw + (int64_t)j0 * 24;
-        for (int e = tid; e < cn * 12; e += kThreads) cp_async16(dst + 16 * e, src + 2 * e);
-        for (int e = tid; e < cn * 8; e += kThreads) {
-          const int j = e >> 3, q = (e & 7) * 2;
-          cp_async16(dst + kRawRows + j * 128 + q * 8, vt + (int64_t)pw[j0 + j] * nrhs + rg + q);
+        for (int e = lane; e < cn * 12; e += 32) cp_async16(dst + 16 * e, src + 2 * e);
+        if (lane < cn) {
+          const double* vs = vt + (int64_t)(uint32_t)px * nrhs + rg;
+          uint8_t* vd = dst + kRawRows + lane * 128;
+#pragma unroll
+          for (int q = 0; q < 8; ++q) cp_async16(vd + 16 * q, vs + 2 * q);
         }
+        cp_async_mbar_arrive(&raw_full[s]);
+        px = px_next;
       }
-      cp_commit();
-    };
-    stage_raw(0);
-    stage_raw(1);
-    for (int c = 0; c < nchunk; ++c) {
-      const int st = c & 1;
-      cp_wait<1>();
-      __syncthreads();                     // raw(c) visible; sva/rsc ready
-      if (c >= 2) umma::mbar_wait(&mbar[st], (commits[st] - 1) & 1);
-      uint8_t* sA = smem + st * kStageBytes;
-      uint8_t* sB = sA + kSl * kABytes;
-      const double* R = reinterpret_cast<const double*>(raw + (c % kRawStages) * kRawBytes);
-      const double* Vr = R + kChunk * 24;
-      const int cn = min(kChunk, sd.count - c * kChunk);
-      {
-        const int m = tid & 127, h = tid >> 7;
-        const int a = m >> 4, r = m & 15;
-        const double sv = sva[m], s_a = sa[a];
-        uint32_t lo[16], hi[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const int j = h * 16 + i;
-          double x = 0.0, y = 0.0;
-          if (j < cn) {
-            x = Vr[j * 16 + r] * sv;
-            y = R[j * 24 + a] * s_a;
-          }
-          slice1(x, y, lo[i], hi[i]);
-        }
-#pragma unroll
-        for (int p = 0; p < kSl; ++p) {
-          uint4 w;
-          w.x = NLD_DW(lo, hi, 0, p);
-          w.y = NLD_DW(lo, hi, 4, p);
-          w.z = NLD_DW(lo, hi, 8, p);
-          w.w = NLD_DW(lo, hi, 12, p);
-          *reinterpret_cast<uint4*>(sA + p * kABytes + canon32(m, h * 16)) = w;
-        }
-      }
-      {
-        const int n = tid & 63, g = tid >> 6;
-        const int b = n >> 3, cc = n & 7;
-        const double s_b = sb[b], s_c = sc[cc];
-        uint32_t lo[8], hi[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int j = g * 8 + i;
-          double x = 0.0, y = 0.0;
-          if (j < cn) {
-            x = R[j * 24 + 8 + b] * s_b;
-            y = R[j * 24 + 16 + cc] * s_c;
-          }
-          slice1(x, y, lo[i], hi[i]);
-        }
-#pragma unroll
-        for (int p = 0; p < kSl; ++p) {
-          uint2 w;
-          w.x = NLD_DW(lo, hi, 0, p);
-          w.y = NLD_DW(lo, hi, 4, p);
-          *reinterpret_cast<uint2*>(sB + p * kBBytes + canon32(n, g * 8)) = w;
-        }
-      }
-      umma::fence_async_smem();
-      __syncthreads();                     // operands written; raw(c) consumed
-      stage_raw(c + 2);                    // into raw stage (c+2)%3 == (c-1)%3
-      if (tid == 0) {
+    }
+  } else if (warp == kIssuerWarp) {
+    // ---------------------------------------------------------------- issuer
+    int g = 0;
+    for (int grp = 0; grp < ngroups; ++grp) {
+      if (grp > 0) umma::mbar_wait(&acc_empty, (grp - 1) & 1);   // epilogue drained TMEM
+      for (int c = 0; c < nchunk; ++c, ++g) {
+        const int st = g & 1;
+        umma::mbar_wait(&op_ready[st], (g >> 1) & 1);
         umma::fence_after();
-        const uint32_t aB = umma::smem_u32(sA), bB = umma::smem_u32(sB);
+        if (lane == 0) {
+          const uint32_t aB = umma::smem_u32(smem + st * kStageBytes);
+          const uint32_t bB = aB + kSl * kABytes;
 #pragma unroll
-        for (int p = 0; p < kSl; ++p) {
-          const uint64_t da = umma::make_sdesc(aB + p * kABytes, 128, 256);
-          int q0 = 0;
-          while (q0 < kSl - p) {
-            const int nq = min(4, kSl - p - q0);
-            const uint64_t db = umma::make_sdesc(bB + q0 * kBBytes, 128, 256);
-            const uint32_t acc = (c > 0 || p > 0) ? 1u : 0u;
-            umma::mma_i8(tmem + (uint32_t)((p + q0) * 64), da, db,
-                         umma::idesc_i8(kRows, nq * 64), acc);
-            q0 += nq;
+          for (int p = 0; p < kSl; ++p) {
+            const uint64_t da = umma::make_sdesc(aB + p * kABytes, 128, 256);
+#pragma unroll
+            for (int q0 = 0; q0 < kSl - p; q0 += 4) {
+              const int nq = min(4, kSl - p - q0);
+              const uint64_t db = umma::make_sdesc(bB + q0 * kBBytes, 128, 256);
+              umma::mma_i8(tmem + (uint32_t)((p + q0) * 64), da, db,
+                           umma::idesc_i8(kRows, nq * 64), (c > 0 || p > 0) ? 1u : 0u);
+            }
+          }
+          umma::commit(&op_free[st]);
+          if (c == nchunk - 1) umma::commit(&acc_full);
+        }
+        __syncwarp();
+      }
+    }
+  } else {
+    // --------------------------------------------------------------- slicers
+    int g = 0;
+    for (int grp = 0; grp < ngroups; ++grp) {
+      const int rg = grp * 16;
+      if (tid < kRows) {
+        const int a = tid >> 4, r = tid & 15;
+        const int ev = exp_bound(__longlong_as_double((long long)vmax[rg + r]));
+        sva[tid] = pow2(46 - ev);
+        rsc[tid] = pow2(ev + ex[a] - 46);
+      }
+      asm volatile("bar.sync 1, %0;\n" ::"n"(kSlicers));      // slicers only
+      for (int c = 0; c < nchunk; ++c, ++g) {
+        const int st = g & 1, s = g % kRawStages;
+        umma::mbar_wait(&raw_full[s], (g / kRawStages) & 1);
+        if (g >= 2) umma::mbar_wait(&op_free[st], ((g >> 1) - 1) & 1);
+        uint8_t* sA = smem + st * kStageBytes;
+        uint8_t* sB = sA + kSl * kABytes;
+        const double* R = reinterpret_cast<const double*>(raw + s * kRawBytes);
+        const double* Vr = R + kChunk * 24;
+        const int cn = min(kChunk, sd.count - c * kChunk);
+        {
+          const int m = tid & 127, h = tid >> 7;
+          const int a = m >> 4, r = m & 15;
+          const double sv = sva[m], s_a = sa[a];
+          uint32_t lo[16], hi[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const int j = h * 16 + i;
+            double x = 0.0, y = 0.0;
+            if (j < cn) {
+              x = Vr[j * 16 + r] * sv;
+              y = R[j * 24 + a] * s_a;
+            }
+            slice1(x, y, lo[i], hi[i]);
+          }
+#pragma unroll
+          for (int p = 0; p < kSl; ++p) {
+            uint4 w;
+            w.x = NLD_DW(lo, hi, 0, p);
+            w.y = NLD_DW(lo, hi, 4, p);
+            w.z = NLD_DW(lo, hi, 8, p);
+            w.w = NLD_DW(lo, hi, 12, p);
+            *reinterpret_cast<uint4*>(sA + p * kABytes + canon32(m, h * 16)) = w;
           }
         }
-        umma::commit(&mbar[st]);
-      }
-      ++commits[st];
-    }
-    cp_wait<0>();
-    for (int s2 = 0; s2 < 2; ++s2)
-      if (commits[s2]) umma::mbar_wait(&mbar[s2], (commits[s2] - 1) & 1);
-    umma::fence_after();
-    {
-      const int lg = warp & 3, half = warp >> 2;
-      const int m = lg * 32 + lane;
-      const int a = m >> 4, r = m & 15;
-      const double rs = rsc[m];
-      const uint32_t tl = tmem + ((uint32_t)(lg * 32) << 16);
-#pragma unroll 1
-      for (int c0 = half * 32; c0 < half * 32 + 32; c0 += 16) {
-        uint32_t dv[kSl][16];
+        {
+          const int n = tid & 63, gq = tid >> 6;
+          const int b = n >> 3, cc = n & 7;
+          const double s_b = sb[b], s_c = sc[cc];
+          uint32_t lo[8], hi[8];
 #pragma unroll
-        for (int t = 0; t < kSl; ++t) umma::tmem_ld16(tl + (uint32_t)(t * 64 + c0), dv[t]);
-        umma::tmem_wait_ld();
+          for (int i = 0; i < 8; ++i) {
+            const int j = gq * 8 + i;
+            double x = 0.0, y = 0.0;
+            if (j < cn) {
+              x = R[j * 24 + 8 + b] * s_b;
+              y = R[j * 24 + 16 + cc] * s_c;
+            }
+            slice1(x, y, lo[i], hi[i]);
+          }
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          double acc = 0.0;
-#pragma unroll
-          for (int t = kSl - 1; t >= 0; --t) acc = fma(acc, 0.00390625, (double)(int32_t)dv[t][i]);
-          const int bc = c0 + i;
-          blocks[(sd.block + a * 64 + bc) * nrhs + rg + r] = acc * rs * csc[bc];
+          for (int p = 0; p < kSl; ++p) {
+            uint2 w;
+            w.x = NLD_DW(lo, hi, 0, p);
+            w.y = NLD_DW(lo, hi, 4, p);
+            *reinterpret_cast<uint2*>(sB + p * kBBytes + canon32(n, gq * 8)) = w;
+          }
+        }
+        umma::fence_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(&op_ready[st]);
+          mbar_arrive(&raw_empty[s]);
         }
       }
+      // epilogue: accumulators of this rhs group -> block
+      umma::mbar_wait(&acc_full, grp & 1);
+      umma::fence_after();
+      {
+        const int lg = warp & 3, half = warp >> 2;
+        const int m = lg * 32 + lane;
+        const int a = m >> 4, r = m & 15;
+        const double rs = rsc[m];
+        const uint32_t tl = tmem + ((uint32_t)(lg * 32) << 16);
+#pragma unroll 1
+        for (int c0 = half * 32; c0 < half * 32 + 32; c0 += 16) {
+          uint32_t dv[kSl][16];
+#pragma unroll
+          for (int t = 0; t < kSl; ++t) umma::tmem_ld16(tl + (uint32_t)(t * 64 + c0), dv[t]);
+          umma::tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            double acc = 0.0;
+#pragma unroll
+            for (int t = kSl - 1; t >= 0; --t)
+              acc = fma(acc, 0.00390625, (double)(int32_t)dv[t][i]);
+            const int bc = c0 + i;
+            blocks[(sd.block + a * 64 + bc) * nrhs + rg + r] = acc * rs * csc[bc];
+          }
+        }
+      }
+      umma::fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty);
+      asm volatile("bar.sync 1, %0;\n" ::"n"(kSlicers));      // rsc reuse by the next group
     }
-    umma::fence_before();
-    __syncthreads();
   }
+  umma::fence_before();
+  __syncthreads();
   if (warp == 0) umma::tmem_free<kTmemCols>(tmem);
 }
 
@@ -354,8 +419,8 @@ void launch_spread_oz(const PlanSet& ps, const SubDev* subs, const int16_t* ex, 
                                   smem));
     attr = true;
   }
-  oz::k_spread_oz<<<nsub, oz::kThreads, smem, st>>>(subs, ps.wdev, ps.rows, ps.pix, ex, vmax, vt,
-                                                     nrhs, blocks);
+  oz::k_spread_oz<<<nsub, oz::kSpreadThreads, smem, st>>>(subs, ps.wdev, ps.rows, ps.pix, ex, vmax,
+                                                           vt, nrhs, blocks);
   NLD_CUDA(cudaGetLastError());
 }
 
