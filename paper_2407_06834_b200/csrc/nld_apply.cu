@@ -1156,6 +1156,10 @@ void gather_window_fast(const PlanSet& ps, const Workspace& ws, int w, int64_t N
   const unsigned nsub = (unsigned)wp.n_subs;
   if (wp.d == 1) launch_gather<1, MC>(subs, nsub, ps, ws, N, nrhs, st);
   else if (wp.d == 2) launch_gather<2, MC>(subs, nsub, ps, ws, N, nrhs, st);
+  else if (MC == 4 && use_ozaki() && nrhs % 16 == 0 && ps.sub_exp)
+    launch_gather_oz(ps, subs, ps.sub_exp + wp.sub_off * 24, nsub, ws.grid_out, ps.grid_total,
+                     ep.mode == mma::kGatherStore ? ws.wout + (int64_t)w * N * nrhs : out, N, nrhs,
+                     ep, st);
   else if (MC == 4 && use_mma()) launch_gather_mma(subs, nsub, ps, ws, N, nrhs, st, ep, out);
   else launch_gather<3, MC>(subs, nsub, ps, ws, N, nrhs, st);
 }

@@ -25,6 +25,7 @@
 #include <cstdint>
 
 #include "nld_internal.cuh"
+#include "nld_epi.cuh"
 #include "nld_umma.cuh"
 
 namespace nld {
@@ -134,8 +135,10 @@ constexpr int kRawV = kChunk * 16 * 8;          // 4 KB of v lines per chunk
 constexpr int kRawBytes = kRawRows + kRawV;
 constexpr int kRawStages = 5;         // raw chunks in flight: kRawStages - 1 ahead
 
+constexpr int kOpStages = 3;           // operand stages (slicers <-> tensor core)
+
 __host__ __device__ constexpr int spread_oz_smem() {
-  return 2 * kStageBytes + kRawStages * kRawBytes;
+  return kOpStages * kStageBytes + kRawStages * kRawBytes;
 }
 
 // ---- spread ---------------------------------------------------------------
@@ -175,7 +178,7 @@ k_spread_oz(const SubDev* __restrict__ subs, const WinDev* __restrict__ wins,
   // would fold the declared alignment into the descriptor address bits
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ uint64_t raw_full[kRawStages], raw_empty[kRawStages];
-  __shared__ uint64_t op_ready[2], op_free[2], acc_full, acc_empty;
+  __shared__ uint64_t op_ready[kOpStages], op_free[kOpStages], acc_full, acc_empty;
   __shared__ uint32_t taddr_s;
   __shared__ double rsc[kRows];       // row scale 2^(ev + eA - 46)
   __shared__ double csc[64];          // column scale 2^(eB + eC + 34)
@@ -188,7 +191,7 @@ k_spread_oz(const SubDev* __restrict__ subs, const WinDev* __restrict__ wins,
   const double* __restrict__ rw = rows + wd.row_off + (sd.start - wd.node_off) * 24;
   const int32_t* __restrict__ pw = pix + sd.start;
   const int16_t* ex = sub_exp + (int64_t)blockIdx.x * kExpPerSub;
-  uint8_t* const raw = smem + 2 * kStageBytes;
+  uint8_t* const raw = smem + kOpStages * kStageBytes;
   const int nchunk = (sd.count + kChunk - 1) / kChunk;
   const int ngroups = nrhs / 16;
 
@@ -198,7 +201,7 @@ k_spread_oz(const SubDev* __restrict__ subs, const WinDev* __restrict__ wins,
       umma::mbar_init(&raw_full[k], 32);      // one noinc arrive per loader lane
       umma::mbar_init(&raw_empty[k], kSlicers / 32);
     }
-    for (int k = 0; k < 2; ++k) {
+    for (int k = 0; k < kOpStages; ++k) {
       umma::mbar_init(&op_ready[k], kSlicers / 32);
       umma::mbar_init(&op_free[k], 1);
     }
@@ -251,8 +254,8 @@ k_spread_oz(const SubDev* __restrict__ subs, const WinDev* __restrict__ wins,
     for (int grp = 0; grp < ngroups; ++grp) {
       if (grp > 0) umma::mbar_wait(&acc_empty, (grp - 1) & 1);   // epilogue drained TMEM
       for (int c = 0; c < nchunk; ++c, ++g) {
-        const int st = g & 1;
-        umma::mbar_wait(&op_ready[st], (g >> 1) & 1);
+        const int st = g % kOpStages;
+        umma::mbar_wait(&op_ready[st], (g / kOpStages) & 1);
         umma::fence_after();
         if (lane == 0) {
           const uint32_t aB = umma::smem_u32(smem + st * kStageBytes);
@@ -287,9 +290,9 @@ k_spread_oz(const SubDev* __restrict__ subs, const WinDev* __restrict__ wins,
       }
       asm volatile("bar.sync 1, %0;\n" ::"n"(kSlicers));      // slicers only
       for (int c = 0; c < nchunk; ++c, ++g) {
-        const int st = g & 1, s = g % kRawStages;
+        const int st = g % kOpStages, s = g % kRawStages;
         umma::mbar_wait(&raw_full[s], (g / kRawStages) & 1);
-        if (g >= 2) umma::mbar_wait(&op_free[st], ((g >> 1) - 1) & 1);
+        if (g >= kOpStages) umma::mbar_wait(&op_free[st], ((g / kOpStages) - 1) & 1);
         uint8_t* sA = smem + st * kStageBytes;
         uint8_t* sB = sA + kSl * kABytes;
         const double* R = reinterpret_cast<const double*>(raw + s * kRawBytes);
@@ -298,15 +301,15 @@ k_spread_oz(const SubDev* __restrict__ subs, const WinDev* __restrict__ wins,
         {
           const int m = tid & 127, h = tid >> 7;
           const int a = m >> 4, r = m & 15;
-          const double sv = sva[m], s_a = sa[a];
+          const double sx = sva[m] * sa[a];      // exact: a product of powers of two
           uint32_t lo[16], hi[16];
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
             const int j = h * 16 + i;
             double x = 0.0, y = 0.0;
             if (j < cn) {
-              x = Vr[j * 16 + r] * sv;
-              y = R[j * 24 + a] * s_a;
+              x = Vr[j * 16 + r];
+              y = R[j * 24 + a] * sx;
             }
             slice1(x, y, lo[i], hi[i]);
           }
@@ -323,15 +326,15 @@ k_spread_oz(const SubDev* __restrict__ subs, const WinDev* __restrict__ wins,
         {
           const int n = tid & 63, gq = tid >> 6;
           const int b = n >> 3, cc = n & 7;
-          const double s_b = sb[b], s_c = sc[cc];
+          const double sy = sb[b] * sc[cc];
           uint32_t lo[8], hi[8];
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             const int j = gq * 8 + i;
             double x = 0.0, y = 0.0;
             if (j < cn) {
-              x = R[j * 24 + 8 + b] * s_b;
-              y = R[j * 24 + 16 + cc] * s_c;
+              x = R[j * 24 + 8 + b] * sy;
+              y = R[j * 24 + 16 + cc];
             }
             slice1(x, y, lo[i], hi[i]);
           }
@@ -387,6 +390,283 @@ k_spread_oz(const SubDev* __restrict__ subs, const WinDev* __restrict__ wins,
   if (warp == 0) umma::tmem_free<kTmemCols>(tmem);
 }
 
+// ---- gather ---------------------------------------------------------------
+// T[(a, r)][j] = sum_{(b,c)} G_r[a][(b,c)] Y_j[(b,c)],  Y_j = B_j (x) C_j,
+// then y_r[j] = sum_a A_j[a] T[(a, r)][j]  (the DMMA gather's contraction,
+// nld_mma.cuh k_gather_mma16, with the a-sum moved to the epilogue).
+// UMMA M = 128 rows (a, r): the G digits of one subproblem (K = 64 = (b,c),
+// scaled per row), N = 32-node tiles with the Y digit slices stacked along N
+// ([e_0 | .. | e_{S-1-p}] against G digit p, D window shifted by 32 p), so a
+// tile's 6 diagonals take 192 TMEM columns and two tiles double-buffer.
+//   warp 9  (loader): cp.async each tile's weight rows -> raw stage;
+//   warps 4-7 (slicers): Y digits of a tile -> operand stage;
+//   warp 8  (issuer): 12 UMMAs per tile (2 K steps x 6 digit rows);
+//   warps 0-3 (epilogue): TMEM -> fp64 T -> x A_j[a] -> sum over a (shuffle +
+//           shared memory) -> fused window-sum / degree / shift epilogue.
+// The G digits are formed by all ten warps at the start of each rhs group.
+constexpr int kGTile = 32;                       // nodes per tile
+constexpr int kGA = kRows * 64;                  // 8 KB per G digit slice (K = 64)
+constexpr int kGB = kGTile * 64;                 // 2 KB per Y digit slice
+constexpr int kGBStage = kSl * kGB;              // 12 KB
+constexpr int kGOpStages = 3;
+constexpr int kGRaw = kGTile * 24 * 8;           // 6 KB rows per tile
+constexpr int kGRawStages = 4;
+constexpr int kGRed = 4 * kGTile * 16 * 8;       // 16 KB a-sum partials
+constexpr int kGatherThreads = 320;
+
+__host__ __device__ constexpr int gather_oz_smem() {
+  return kSl * kGA + kGOpStages * kGBStage + kGRawStages * kGRaw + kGRed;
+}
+
+// canonical K-major no-swizzle offset in a (rows x 64 bytes) tile
+__device__ __forceinline__ int canon64(int row, int k) {
+  return (row >> 3) * 512 + (k >> 4) * 128 + (row & 7) * 16 + (k & 15);
+}
+
+__global__ void __launch_bounds__(kGatherThreads, 1)
+k_gather_oz(const SubDev* __restrict__ subs, const CellDev* __restrict__ cells,
+            const WinDev* __restrict__ wins, const double* __restrict__ rows,
+            const int32_t* __restrict__ pix, const int16_t* __restrict__ sub_exp,
+            const double* __restrict__ grid, int64_t grid_ld, double* __restrict__ out,
+            int64_t N, int nrhs, mma::GatherEpi ep) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  __shared__ uint64_t raw_full[kGRawStages], raw_empty[kGRawStages];
+  __shared__ uint64_t op_ready[kGOpStages], op_free[kGOpStages];
+  __shared__ uint64_t acc_full[2], acc_empty[2];
+  __shared__ uint32_t taddr_s;
+  __shared__ double gmax[2][kRows];
+  __shared__ double tsc[kRows];           // T scale per row: 2^(eG + eY - 92 + 80)
+
+  const SubDev sd = subs[blockIdx.x];
+  const CellDev cd = cells[sd.cell];
+  const WinDev wd = wins[sd.win];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const double* __restrict__ rw = rows + wd.row_off + (sd.start - wd.node_off) * 24;
+  const int32_t* __restrict__ pw = pix + sd.start;
+  const int16_t* ex = sub_exp + (int64_t)blockIdx.x * kExpPerSub;
+  uint8_t* const sGA = smem;
+  uint8_t* const sGB = sGA + kSl * kGA;
+  uint8_t* const sRaw = sGB + kGOpStages * kGBStage;
+  double* const sRed = reinterpret_cast<double*>(sRaw + kGRawStages * kGRaw);
+  const int ntile = (sd.count + kGTile - 1) / kGTile;
+  const int ngroups = nrhs / 16;
+  // Y scale: one per subproblem, |B_j[b] C_j[c]| < 2^(eBm + eCm)
+  int eBm = -2000, eCm = -2000;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    eBm = max(eBm, (int)ex[8 + k]);
+    eCm = max(eCm, (int)ex[16 + k]);
+  }
+  const double syB = pow2(46 - eBm), syC = pow2(-eCm);
+
+  if (warp == 0) umma::tmem_alloc<kTmemCols>(&taddr_s);
+  if (tid == 32) {
+    for (int k = 0; k < kGRawStages; ++k) {
+      umma::mbar_init(&raw_full[k], 32);
+      umma::mbar_init(&raw_empty[k], 4);      // slicer warps
+    }
+    for (int k = 0; k < kGOpStages; ++k) {
+      umma::mbar_init(&op_ready[k], 4);
+      umma::mbar_init(&op_free[k], 1);
+    }
+    for (int k = 0; k < 2; ++k) {
+      umma::mbar_init(&acc_full[k], 1);
+      umma::mbar_init(&acc_empty[k], 4);      // epilogue warps
+    }
+    umma::mbar_fence_init();
+  }
+  umma::fence_before();
+  __syncthreads();
+  umma::fence_after();
+  const uint32_t tmem = taddr_s;
+
+  int gt = 0;   // tiles processed so far over all rhs groups (phase bookkeeping)
+  for (int grp = 0; grp < ngroups; ++grp) {
+    const int rg = grp * 16;
+    // ---- G digits of this rhs group (all warps) ---------------------------
+    // thread t < 256: row m = t & 127 = (a, r), bc half h = t >> 7
+    double gv[32];
+    const int m = tid & 127, h = (tid >> 7) & 1;
+    if (tid < 256) {
+      const int a = m >> 4, r = m & 15;
+      double mx = 0.0;
+      int p0 = cd.cc[0] + a;
+      if (p0 >= wd.box_w[0]) p0 -= wd.box_w[0];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const int bc = h * 32 + i;
+        int p1 = cd.cc[1] + (bc >> 3), p2 = cd.cc[2] + (bc & 7);
+        if (p1 >= wd.box_w[1]) p1 -= wd.box_w[1];
+        if (p2 >= wd.box_w[2]) p2 -= wd.box_w[2];
+        gv[i] = grid[(int64_t)(rg + r) * grid_ld + wd.grid_off +
+                     ((int64_t)p0 * wd.box_w[1] + p1) * wd.box_w[2] + p2];
+        mx = fmax(mx, fabs(gv[i]));
+      }
+      gmax[h][m] = mx;
+    }
+    __syncthreads();
+    if (tid < 256) {
+      const int eG = exp_bound(fmax(gmax[0][m], gmax[1][m]));
+      const double sg = pow2(46 - eG);
+      if (h == 0) tsc[m] = pow2(eG + eBm + eCm - 12);   // (eG-46)+(eBm+eCm-46)+80
+#pragma unroll
+      for (int kb = 0; kb < 2; ++kb) {
+        uint32_t lo[16], hi[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) slice1(gv[kb * 16 + i], sg, lo[i], hi[i]);
+#pragma unroll
+        for (int p = 0; p < kSl; ++p) {
+          uint4 w;
+          w.x = NLD_DW(lo, hi, 0, p);
+          w.y = NLD_DW(lo, hi, 4, p);
+          w.z = NLD_DW(lo, hi, 8, p);
+          w.w = NLD_DW(lo, hi, 12, p);
+          *reinterpret_cast<uint4*>(sGA + p * kGA + canon64(m, h * 32 + kb * 16)) = w;
+        }
+      }
+    }
+    umma::fence_async_smem();
+    umma::fence_before();
+    __syncthreads();
+    umma::fence_after();
+
+    if (warp == kLoaderWarp) {
+      // -------------------------------------------------------------- loader
+      for (int tl = 0; tl < ntile; ++tl) {
+        const int g = gt + tl, s = g % kGRawStages;
+        if (g >= kGRawStages) umma::mbar_wait(&raw_empty[s], ((g / kGRawStages) - 1) & 1);
+        const int j0 = tl * kGTile, cn = min(kGTile, sd.count - j0);
+        const double* src = rw + (int64_t)j0 * 24;
+        uint8_t* dst = sRaw + s * kGRaw;
+        for (int e = lane; e < cn * 12; e += 32) cp_async16(dst + 16 * e, src + 2 * e);
+        cp_async_mbar_arrive(&raw_full[s]);
+      }
+    } else if (warp == kIssuerWarp) {
+      // -------------------------------------------------------------- issuer
+      for (int tl = 0; tl < ntile; ++tl) {
+        const int g = gt + tl, st = g % kGOpStages, ab = g & 1;
+        if (g >= 2) umma::mbar_wait(&acc_empty[ab], ((g >> 1) - 1) & 1);
+        umma::mbar_wait(&op_ready[st], (g / kGOpStages) & 1);
+        umma::fence_after();
+        if (lane == 0) {
+          const uint32_t aB = umma::smem_u32(sGA);
+          const uint32_t bB = umma::smem_u32(sGB + st * kGBStage);
+          const uint32_t dcol = tmem + (uint32_t)(ab * kSl * kGTile);
+#pragma unroll
+          for (int ks = 0; ks < 2; ++ks)
+#pragma unroll
+            for (int p = 0; p < kSl; ++p) {
+              const uint64_t da = umma::make_sdesc(aB + p * kGA + ks * 256, 128, 512);
+              const uint64_t db = umma::make_sdesc(bB + ks * 256, 128, 512);
+              umma::mma_i8(dcol + (uint32_t)(p * kGTile), da, db,
+                           umma::idesc_i8(kRows, (kSl - p) * kGTile), (ks > 0 || p > 0) ? 1u : 0u);
+            }
+          umma::commit(&op_free[st]);
+          umma::commit(&acc_full[ab]);
+        }
+        __syncwarp();
+      }
+    } else if (warp >= 4) {
+      // ------------------------------------------------------------- slicers
+      const int t = tid - 128;                 // 0..127
+      const int n = t >> 2, kq = t & 3;        // node n, bc quarter kq (16 values)
+      for (int tl = 0; tl < ntile; ++tl) {
+        const int g = gt + tl, s = g % kGRawStages, st = g % kGOpStages;
+        umma::mbar_wait(&raw_full[s], (g / kGRawStages) & 1);
+        if (g >= kGOpStages) umma::mbar_wait(&op_free[st], ((g / kGOpStages) - 1) & 1);
+        const double* R = reinterpret_cast<const double*>(sRaw + s * kGRaw) + n * 24;
+        const bool ok = tl * kGTile + n < sd.count;
+        uint32_t lo[16], hi[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const int bc = kq * 16 + i;
+          double x = 0.0, y = 0.0;
+          if (ok) {
+            x = R[8 + (bc >> 3)] * syB;
+            y = R[16 + (bc & 7)] * syC;
+          }
+          slice1(x, y, lo[i], hi[i]);
+        }
+        uint8_t* sB = sGB + st * kGBStage;
+#pragma unroll
+        for (int p = 0; p < kSl; ++p) {
+          uint4 w;
+          w.x = NLD_DW(lo, hi, 0, p);
+          w.y = NLD_DW(lo, hi, 4, p);
+          w.z = NLD_DW(lo, hi, 8, p);
+          w.w = NLD_DW(lo, hi, 12, p);
+          *reinterpret_cast<uint4*>(sB + p * kGB + canon64(n, kq * 16)) = w;
+        }
+        umma::fence_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(&op_ready[st]);
+          mbar_arrive(&raw_empty[s]);   // A_j[a] is re-read below from the
+        }                               // row table by the epilogue (L1/L2)
+      }
+    } else {
+      // ------------------------------------------------------------ epilogue
+      const int a = 2 * warp + (lane >> 4), r = lane & 15;
+      const int mrow = warp * 32 + lane;
+      const double ts = tsc[mrow];
+      const uint32_t tl_lane = tmem + ((uint32_t)(warp * 32) << 16);
+      for (int tl = 0; tl < ntile; ++tl) {
+        const int g = gt + tl, ab = g & 1;
+        umma::mbar_wait(&acc_full[ab], (g >> 1) & 1);
+        umma::fence_after();
+        const int j0 = tl * kGTile;
+#pragma unroll 1
+        for (int hh = 0; hh < 2; ++hh) {
+          uint32_t dv[kSl][16];
+#pragma unroll
+          for (int tt = 0; tt < kSl; ++tt)
+            umma::tmem_ld16(tl_lane + (uint32_t)(ab * kSl * kGTile + tt * kGTile + hh * 16), dv[tt]);
+          umma::tmem_wait_ld();
+          if (hh == 1) {
+            umma::fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&acc_empty[ab]);
+          }
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const int nn = hh * 16 + i;
+            double acc = 0.0;
+#pragma unroll
+            for (int tt = kSl - 1; tt >= 0; --tt)
+              acc = fma(acc, 0.00390625, (double)(int32_t)dv[tt][i]);
+            const int j = j0 + nn;
+            const double aw = j < sd.count ? __ldg(rw + (int64_t)j * 24 + a) : 0.0;
+            double val = acc * ts * aw;
+            val += __shfl_xor_sync(0xffffffffu, val, 16);
+            if (lane < 16) sRed[(warp * kGTile + nn) * 16 + r] = val;
+          }
+        }
+        asm volatile("bar.sync 2, 128;\n" ::: "memory");
+        // 32 nodes x 16 rhs = 512 outputs, 4 per thread; r fastest (coalesced)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int o = tid + 128 * k;
+          const int nn = o >> 4, rr = o & 15;
+          const int j = j0 + nn;
+          if (j < sd.count) {
+            const double y = (sRed[(0 * kGTile + nn) * 16 + rr] + sRed[(1 * kGTile + nn) * 16 + rr]) +
+                             (sRed[(2 * kGTile + nn) * 16 + rr] + sRed[(3 * kGTile + nn) * 16 + rr]);
+            const int64_t px = pw[j];
+            const int64_t e = px * nrhs + rg + rr;
+            mma::gather_put(ep, out, e, px, rg + rr, y);
+          }
+        }
+        asm volatile("bar.sync 2, 128;\n" ::: "memory");
+      }
+    }
+    gt += ntile;
+    umma::fence_before();
+    __syncthreads();      // G digits / tsc reused by the next rhs group
+    umma::fence_after();
+  }
+  if (warp == 0) umma::tmem_free<kTmemCols>(tmem);
+}
+
 }  // namespace oz
 
 // ---- host side ------------------------------------------------------------
@@ -421,6 +701,21 @@ void launch_spread_oz(const PlanSet& ps, const SubDev* subs, const int16_t* ex, 
   }
   oz::k_spread_oz<<<nsub, oz::kSpreadThreads, smem, st>>>(subs, ps.wdev, ps.rows, ps.pix, ex, vmax,
                                                            vt, nrhs, blocks);
+  NLD_CUDA(cudaGetLastError());
+}
+
+void launch_gather_oz(const PlanSet& ps, const SubDev* subs, const int16_t* ex, unsigned nsub,
+                      const double* grid, int64_t grid_ld, double* out, int64_t N, int nrhs,
+                      const mma::GatherEpi& ep, cudaStream_t st) {
+  const int smem = oz::gather_oz_smem();
+  static bool attr = false;
+  if (!attr) {
+    NLD_CUDA(cudaFuncSetAttribute(oz::k_gather_oz, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  smem));
+    attr = true;
+  }
+  oz::k_gather_oz<<<nsub, oz::kGatherThreads, smem, st>>>(subs, ps.cells, ps.wdev, ps.rows, ps.pix,
+                                                          ex, grid, grid_ld, out, N, nrhs, ep);
   NLD_CUDA(cudaGetLastError());
 }
 
