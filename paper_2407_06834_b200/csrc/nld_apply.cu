@@ -1022,7 +1022,7 @@ void spread_window_fast(const PlanSet& ps, const Workspace& ws, int w, const dou
       const char* e = getenv("NLD_SPREAD_BC");
       bc = (e && e[0] == '0') ? 0 : 1;
     }
-    if (use_ozaki() && nrhs % 16 == 0 && ps.sub_exp) {
+    if (use_ozaki() && nrhs % 16 == 0 && ps.sub_exp && !getenv("NLD_OZAKI_NO_SPREAD")) {
       launch_spread_oz(ps, subs, ps.sub_exp + wp.sub_off * 24, nsub, ws.vmax, vt, nrhs, ws.blocks,
                        st);
       if (getenv("NLD_OZAKI_DEBUG")) {
@@ -1156,12 +1156,80 @@ void gather_window_fast(const PlanSet& ps, const Workspace& ws, int w, int64_t N
   const unsigned nsub = (unsigned)wp.n_subs;
   if (wp.d == 1) launch_gather<1, MC>(subs, nsub, ps, ws, N, nrhs, st);
   else if (wp.d == 2) launch_gather<2, MC>(subs, nsub, ps, ws, N, nrhs, st);
-  else if (MC == 4 && use_ozaki() && nrhs % 16 == 0 && ps.sub_exp)
+  else if (MC == 4 && use_ozaki() && nrhs % 16 == 0 && ps.sub_exp && !getenv("NLD_OZAKI_NO_GATHER"))
     launch_gather_oz(ps, subs, ps.sub_exp + wp.sub_off * 24, nsub, ws.grid_out, ps.grid_total,
                      ep.mode == mma::kGatherStore ? ws.wout + (int64_t)w * N * nrhs : out, N, nrhs,
                      ep, st);
   else if (MC == 4 && use_mma()) launch_gather_mma(subs, nsub, ps, ws, N, nrhs, st, ep, out);
   else launch_gather<3, MC>(subs, nsub, ps, ws, N, nrhs, st);
+  const bool oz_used = wp.d == 3 && MC == 4 && use_ozaki() && nrhs % 16 == 0 && ps.sub_exp &&
+                       !getenv("NLD_OZAKI_NO_GATHER");
+  if (!oz_used) return;
+  // ---- debug / profiling aids of the sliced gather (environment-gated) ----
+  if (MC == 4 && use_ozaki() && getenv("NLD_OZ_PROF_PRINT")) ozaki_prof_dump("gather", st);
+  if (MC == 4 && use_ozaki() && nrhs % 16 == 0 && ps.sub_exp && getenv("NLD_OZAKI_DEBUG2") &&
+      ep.mode != mma::kGatherStore) {
+    // debug: the fused mode of both gathers from the same starting `out`
+    const size_t nn = (size_t)N * nrhs;
+    double *ta = nullptr, *tb = nullptr;
+    NLD_CUDA(cudaMalloc(&ta, nn * 8));
+    NLD_CUDA(cudaMalloc(&tb, nn * 8));
+    NLD_CUDA(cudaStreamSynchronize(st));
+    NLD_CUDA(cudaMemcpy(ta, out, nn * 8, cudaMemcpyDeviceToDevice));
+    NLD_CUDA(cudaMemcpy(tb, out, nn * 8, cudaMemcpyDeviceToDevice));
+    launch_gather_oz(ps, subs, ps.sub_exp + wp.sub_off * 24, nsub, ws.grid_out, ps.grid_total, ta,
+                     N, nrhs, ep, st);
+    launch_gather_mma(subs, nsub, ps, ws, N, nrhs, st, ep, tb);
+    NLD_CUDA(cudaStreamSynchronize(st));
+    std::vector<double> h1(nn), h2(nn);
+    NLD_CUDA(cudaMemcpy(h1.data(), ta, nn * 8, cudaMemcpyDeviceToHost));
+    NLD_CUDA(cudaMemcpy(h2.data(), tb, nn * 8, cudaMemcpyDeviceToHost));
+    double num = 0, den = 0;
+    int shown = 0;
+    for (size_t e = 0; e < nn; ++e) {
+      num += (h1[e] - h2[e]) * (h1[e] - h2[e]);
+      den += h2[e] * h2[e];
+      if (fabs(h1[e] - h2[e]) > 1e-9 * fabs(h2[e]) + 1e-300 && shown < 6) {
+        fprintf(stderr, "   e %zu (px %zu r %zu) oz %.9e mma %.9e\n", e, e / nrhs, e % nrhs, h1[e],
+                h2[e]);
+        ++shown;
+      }
+    }
+    fprintf(stderr, "ozfdbg win %d mode %d rel %.3e\n", w, ep.mode, sqrt(num / den));
+    cudaFree(ta);
+    cudaFree(tb);
+  }
+  if (MC == 4 && use_ozaki() && nrhs % 16 == 0 && ps.sub_exp && getenv("NLD_OZAKI_DEBUG")) {
+    // debug: both gathers in store mode into wout[w], compare
+    const size_t nn = (size_t)N * nrhs;
+    std::vector<double> h1(nn), h2(nn);
+    mma::GatherEpi sto{mma::kGatherStore, 0, 0, nullptr, nullptr, nullptr};
+    double* wo = ws.wout + (int64_t)w * N * nrhs;
+    NLD_CUDA(cudaMemsetAsync(wo, 0, nn * 8, st));
+    launch_gather_oz(ps, subs, ps.sub_exp + wp.sub_off * 24, nsub, ws.grid_out, ps.grid_total, wo,
+                     N, nrhs, sto, st);
+    NLD_CUDA(cudaStreamSynchronize(st));
+    NLD_CUDA(cudaMemcpy(h1.data(), wo, nn * 8, cudaMemcpyDeviceToHost));
+    NLD_CUDA(cudaMemsetAsync(wo, 0, nn * 8, st));
+    launch_gather_mma(subs, nsub, ps, ws, N, nrhs, st, sto, nullptr);
+    NLD_CUDA(cudaStreamSynchronize(st));
+    NLD_CUDA(cudaMemcpy(h2.data(), wo, nn * 8, cudaMemcpyDeviceToHost));
+    SubDev s0;
+    NLD_CUDA(cudaMemcpy(&s0, subs, sizeof(SubDev), cudaMemcpyDeviceToHost));
+    std::vector<int32_t> pp(s0.count);
+    NLD_CUDA(cudaMemcpy(pp.data(), ps.pix + s0.start, pp.size() * 4, cudaMemcpyDeviceToHost));
+    double num = 0, den = 0;
+    for (size_t e = 0; e < nn; ++e) {
+      num += (h1[e] - h2[e]) * (h1[e] - h2[e]);
+      den += h2[e] * h2[e];
+    }
+    fprintf(stderr, "ozgdbg win %d rel %.3e  sub0 count %d\n", w, sqrt(num / den), s0.count);
+    for (int j = 0; j < std::min(40, s0.count); j += 1) {
+      const int64_t e = (int64_t)pp[j] * nrhs;
+      fprintf(stderr, "  node %d: r0 oz %.6e ref %.6e | r7 oz %.6e ref %.6e\n", j, h1[e], h2[e],
+              h1[e + 7], h2[e + 7]);
+    }
+  }
 }
 
 struct EvScope {

@@ -203,6 +203,7 @@ void launch_spread_oz(const PlanSet& ps, const SubDev* subs, const int16_t* ex, 
                       const unsigned long long* vmax, const double* vt, int nrhs, double* blocks,
                       cudaStream_t st);
 void ozaki_vmax(const double* vt, int64_t n, int nrhs, unsigned long long* out, cudaStream_t st);
+void ozaki_prof_dump(const char* what, cudaStream_t st);
 namespace mma { struct GatherEpi; }
 void launch_gather_oz(const PlanSet& ps, const SubDev* subs, const int16_t* ex, unsigned nsub,
                       const double* grid, int64_t grid_ld, double* out, int64_t N, int nrhs,

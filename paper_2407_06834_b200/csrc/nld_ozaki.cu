@@ -23,6 +23,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstdio>
 
 #include "nld_internal.cuh"
 #include "nld_epi.cuh"
@@ -35,6 +36,21 @@ namespace oz {
 #define NLD_OZ_SL 6
 #endif
 constexpr int kSl = NLD_OZ_SL;         // digits per operand
+
+// -DNLD_OZ_PROF: per-site clock64 totals of the pipeline waits (lane 0 of
+// each warp), printed after each launch -- a tuning aid, not built by default
+#ifdef NLD_OZ_PROF
+__device__ unsigned long long oz_prof[32];
+#define OZW(site, ...)                                                      \
+  do {                                                                      \
+    const long long _t0 = clock64();                                        \
+    __VA_ARGS__;                                                            \
+    if ((threadIdx.x & 31) == 0)                                            \
+      atomicAdd(&oz_prof[site], (unsigned long long)(clock64() - _t0));     \
+  } while (0)
+#else
+#define OZW(site, ...) __VA_ARGS__
+#endif
 constexpr int kRows = 128;             // M: (a, r) rows, r fastest
 constexpr int kChunk = 32;             // nodes per UMMA K step (32 bytes)
 constexpr int kThreads = 256;
@@ -123,6 +139,9 @@ __global__ void k_vmax(const double* __restrict__ vt, int64_t n, int nrhs,
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(umma::smem_u32(dst)), "l"(src));
+}
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(umma::smem_u32(dst)), "l"(src));
 }
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
@@ -409,10 +428,24 @@ constexpr int kGA = kRows * 64;                  // 8 KB per G digit slice (K = 
 constexpr int kGB = kGTile * 64;                 // 2 KB per Y digit slice
 constexpr int kGBStage = kSl * kGB;              // 12 KB
 constexpr int kGOpStages = 3;
-constexpr int kGRaw = kGTile * 24 * 8;           // 6 KB rows per tile
-constexpr int kGRawStages = 4;
+constexpr int kGRaw = kGTile * 24 * 8 + kGTile * 4;   // rows + pixel indices per tile
+constexpr int kGRawStages = 6;                   // slicers run <= 3 tiles ahead of MMA,
+                                                 // the epilogue trails it by <= 2
 constexpr int kGRed = 4 * kGTile * 16 * 8;       // 16 KB a-sum partials
-constexpr int kGatherThreads = 320;
+constexpr int kGatherThreads = 384;              // 8 epilogue, 2 slicer, issuer, loader
+constexpr int kGEpiWarps = 8;
+constexpr int kGSlicerWarp0 = 8;
+constexpr int kGIssuerWarp = 10;
+constexpr int kGLoaderWarp = 11;
+
+// exact int32 -> fp64 without I2F: 2^52 + 2^31 + x has x + 2^31 in its mantissa
+__device__ __forceinline__ double i2d(uint32_t x) {
+#ifdef NLD_OZ_I2F
+  return (double)(int32_t)x;
+#else
+  return __hiloint2double(0x43300000, (int)(x ^ 0x80000000u)) - 4503601774854144.0;
+#endif
+}
 
 __host__ __device__ constexpr int gather_oz_smem() {
   return kSl * kGA + kGOpStages * kGBStage + kGRawStages * kGRaw + kGRed;
@@ -463,15 +496,15 @@ k_gather_oz(const SubDev* __restrict__ subs, const CellDev* __restrict__ cells,
   if (tid == 32) {
     for (int k = 0; k < kGRawStages; ++k) {
       umma::mbar_init(&raw_full[k], 32);
-      umma::mbar_init(&raw_empty[k], 4);      // slicer warps
+      umma::mbar_init(&raw_empty[k], 2 + kGEpiWarps);   // slicer + epilogue warps
     }
     for (int k = 0; k < kGOpStages; ++k) {
-      umma::mbar_init(&op_ready[k], 4);
+      umma::mbar_init(&op_ready[k], 2);       // slicer warps
       umma::mbar_init(&op_free[k], 1);
     }
     for (int k = 0; k < 2; ++k) {
       umma::mbar_init(&acc_full[k], 1);
-      umma::mbar_init(&acc_empty[k], 4);      // epilogue warps
+      umma::mbar_init(&acc_empty[k], kGEpiWarps);
     }
     umma::mbar_fence_init();
   }
@@ -484,24 +517,22 @@ k_gather_oz(const SubDev* __restrict__ subs, const CellDev* __restrict__ cells,
   for (int grp = 0; grp < ngroups; ++grp) {
     const int rg = grp * 16;
     // ---- G digits of this rhs group (all warps) ---------------------------
-    // thread t < 256: row m = t & 127 = (a, r), bc half h = t >> 7
-    double gv[32];
+    // thread t < 256: row m = t & 127 = (a, r), bc half h = t >> 7; two passes
+    // over the (L2-resident) support box: the row max, then the digits
     const int m = tid & 127, h = (tid >> 7) & 1;
-    if (tid < 256) {
-      const int a = m >> 4, r = m & 15;
-      double mx = 0.0;
-      int p0 = cd.cc[0] + a;
+    const int ga = m >> 4, gr = m & 15;
+    auto gval = [&](int bc) -> double {
+      int p0 = cd.cc[0] + ga, p1 = cd.cc[1] + (bc >> 3), p2 = cd.cc[2] + (bc & 7);
       if (p0 >= wd.box_w[0]) p0 -= wd.box_w[0];
-#pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        const int bc = h * 32 + i;
-        int p1 = cd.cc[1] + (bc >> 3), p2 = cd.cc[2] + (bc & 7);
-        if (p1 >= wd.box_w[1]) p1 -= wd.box_w[1];
-        if (p2 >= wd.box_w[2]) p2 -= wd.box_w[2];
-        gv[i] = grid[(int64_t)(rg + r) * grid_ld + wd.grid_off +
-                     ((int64_t)p0 * wd.box_w[1] + p1) * wd.box_w[2] + p2];
-        mx = fmax(mx, fabs(gv[i]));
-      }
+      if (p1 >= wd.box_w[1]) p1 -= wd.box_w[1];
+      if (p2 >= wd.box_w[2]) p2 -= wd.box_w[2];
+      return grid[(int64_t)(rg + gr) * grid_ld + wd.grid_off +
+                  ((int64_t)p0 * wd.box_w[1] + p1) * wd.box_w[2] + p2];
+    };
+    if (tid < 256) {
+      double mx = 0.0;
+#pragma unroll 8
+      for (int i = 0; i < 32; ++i) mx = fmax(mx, fabs(gval(h * 32 + i)));
       gmax[h][m] = mx;
     }
     __syncthreads();
@@ -509,11 +540,11 @@ k_gather_oz(const SubDev* __restrict__ subs, const CellDev* __restrict__ cells,
       const int eG = exp_bound(fmax(gmax[0][m], gmax[1][m]));
       const double sg = pow2(46 - eG);
       if (h == 0) tsc[m] = pow2(eG + eBm + eCm - 12);   // (eG-46)+(eBm+eCm-46)+80
-#pragma unroll
+#pragma unroll 1
       for (int kb = 0; kb < 2; ++kb) {
         uint32_t lo[16], hi[16];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) slice1(gv[kb * 16 + i], sg, lo[i], hi[i]);
+        for (int i = 0; i < 16; ++i) slice1(gval(h * 32 + kb * 16 + i), sg, lo[i], hi[i]);
 #pragma unroll
         for (int p = 0; p < kSl; ++p) {
           uint4 w;
@@ -530,23 +561,27 @@ k_gather_oz(const SubDev* __restrict__ subs, const CellDev* __restrict__ cells,
     __syncthreads();
     umma::fence_after();
 
-    if (warp == kLoaderWarp) {
+#ifdef NLD_OZ_PROF
+    const long long t_role = clock64();
+#endif
+    if (warp == kGLoaderWarp) {
       // -------------------------------------------------------------- loader
       for (int tl = 0; tl < ntile; ++tl) {
         const int g = gt + tl, s = g % kGRawStages;
-        if (g >= kGRawStages) umma::mbar_wait(&raw_empty[s], ((g / kGRawStages) - 1) & 1);
+        if (g >= kGRawStages) OZW(0, umma::mbar_wait(&raw_empty[s], ((g / kGRawStages) - 1) & 1));
         const int j0 = tl * kGTile, cn = min(kGTile, sd.count - j0);
         const double* src = rw + (int64_t)j0 * 24;
         uint8_t* dst = sRaw + s * kGRaw;
         for (int e = lane; e < cn * 12; e += 32) cp_async16(dst + 16 * e, src + 2 * e);
+        if (lane < cn) cp_async4(dst + kGTile * 24 * 8 + 4 * lane, pw + j0 + lane);
         cp_async_mbar_arrive(&raw_full[s]);
       }
-    } else if (warp == kIssuerWarp) {
+    } else if (warp == kGIssuerWarp) {
       // -------------------------------------------------------------- issuer
       for (int tl = 0; tl < ntile; ++tl) {
         const int g = gt + tl, st = g % kGOpStages, ab = g & 1;
-        if (g >= 2) umma::mbar_wait(&acc_empty[ab], ((g >> 1) - 1) & 1);
-        umma::mbar_wait(&op_ready[st], (g / kGOpStages) & 1);
+        if (g >= 2) OZW(1, umma::mbar_wait(&acc_empty[ab], ((g >> 1) - 1) & 1));
+        OZW(2, umma::mbar_wait(&op_ready[st], (g / kGOpStages) & 1));
         umma::fence_after();
         if (lane == 0) {
           const uint32_t aB = umma::smem_u32(sGA);
@@ -566,61 +601,84 @@ k_gather_oz(const SubDev* __restrict__ subs, const CellDev* __restrict__ cells,
         }
         __syncwarp();
       }
-    } else if (warp >= 4) {
+    } else if (warp >= kGSlicerWarp0) {
       // ------------------------------------------------------------- slicers
-      const int t = tid - 128;                 // 0..127
-      const int n = t >> 2, kq = t & 3;        // node n, bc quarter kq (16 values)
+      const int t = tid - 32 * kGSlicerWarp0;  // 0..63
+      const int n = t >> 1, kh = t & 1;        // node n, bc half kh (32 values)
       for (int tl = 0; tl < ntile; ++tl) {
         const int g = gt + tl, s = g % kGRawStages, st = g % kGOpStages;
-        umma::mbar_wait(&raw_full[s], (g / kGRawStages) & 1);
-        if (g >= kGOpStages) umma::mbar_wait(&op_free[st], ((g / kGOpStages) - 1) & 1);
+        OZW(3, umma::mbar_wait(&raw_full[s], (g / kGRawStages) & 1));
+        if (g >= kGOpStages) OZW(4, umma::mbar_wait(&op_free[st], ((g / kGOpStages) - 1) & 1));
         const double* R = reinterpret_cast<const double*>(sRaw + s * kGRaw) + n * 24;
         const bool ok = tl * kGTile + n < sd.count;
-        uint32_t lo[16], hi[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const int bc = kq * 16 + i;
-          double x = 0.0, y = 0.0;
-          if (ok) {
-            x = R[8 + (bc >> 3)] * syB;
-            y = R[16 + (bc & 7)] * syC;
-          }
-          slice1(x, y, lo[i], hi[i]);
-        }
         uint8_t* sB = sGB + st * kGBStage;
 #pragma unroll
-        for (int p = 0; p < kSl; ++p) {
-          uint4 w;
-          w.x = NLD_DW(lo, hi, 0, p);
-          w.y = NLD_DW(lo, hi, 4, p);
-          w.z = NLD_DW(lo, hi, 8, p);
-          w.w = NLD_DW(lo, hi, 12, p);
-          *reinterpret_cast<uint4*>(sB + p * kGB + canon64(n, kq * 16)) = w;
+        for (int kq = 0; kq < 2; ++kq) {
+          uint32_t lo[16], hi[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const int bc = kh * 32 + kq * 16 + i;
+            double x = 0.0, y = 0.0;
+            if (ok) {
+              x = R[8 + (bc >> 3)] * syB;
+              y = R[16 + (bc & 7)] * syC;
+            }
+            slice1(x, y, lo[i], hi[i]);
+          }
+#pragma unroll
+          for (int p = 0; p < kSl; ++p) {
+            uint4 w;
+            w.x = NLD_DW(lo, hi, 0, p);
+            w.y = NLD_DW(lo, hi, 4, p);
+            w.z = NLD_DW(lo, hi, 8, p);
+            w.w = NLD_DW(lo, hi, 12, p);
+            *reinterpret_cast<uint4*>(sB + p * kGB + canon64(n, kh * 32 + kq * 16)) = w;
+          }
         }
         umma::fence_async_smem();
         __syncwarp();
         if (lane == 0) {
           mbar_arrive(&op_ready[st]);
-          mbar_arrive(&raw_empty[s]);   // A_j[a] is re-read below from the
-        }                               // row table by the epilogue (L1/L2)
+          mbar_arrive(&raw_empty[s]);
+        }
       }
     } else {
       // ------------------------------------------------------------ epilogue
-      const int a = 2 * warp + (lane >> 4), r = lane & 15;
-      const int mrow = warp * 32 + lane;
+      const int lg = warp & 3, nh = warp >> 2;          // TMEM lane group, node half
+      const int a = 2 * lg + (lane >> 4), r = lane & 15;
+      const int mrow = lg * 32 + lane;
       const double ts = tsc[mrow];
-      const uint32_t tl_lane = tmem + ((uint32_t)(warp * 32) << 16);
+      const uint32_t tl_lane = tmem + ((uint32_t)(lg * 32) << 16);
+      const bool need_eta = ep.kind == NLD_APPLY_SYSTEM || ep.kind == NLD_APPLY_LAPLACIAN;
+      const int et_id = tid;                            // 0..255
       for (int tl = 0; tl < ntile; ++tl) {
-        const int g = gt + tl, ab = g & 1;
-        umma::mbar_wait(&acc_full[ab], (g >> 1) & 1);
-        umma::fence_after();
+        const int g = gt + tl, ab = g & 1, s = g % kGRawStages;
         const int j0 = tl * kGTile;
+        OZW(5, umma::mbar_wait(&raw_full[s], (g / kGRawStages) & 1));
+        const double* R = reinterpret_cast<const double*>(sRaw + s * kGRaw);
+        const int32_t* sp = reinterpret_cast<const int32_t*>(sRaw + s * kGRaw + kGTile * 24 * 8);
+        // this tile's output-side reads, issued before waiting for the tensor core
+        int64_t oe[2];
+        double prev[2], vx[2], et[2];
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          const int o = et_id + 256 * k, nn = o >> 4, rr = o & 15;
+          const bool ok = j0 + nn < sd.count;
+          const int64_t px = ok ? (int64_t)sp[nn] : -1;
+          oe[k] = ok ? px * nrhs + rg + rr : -1;
+          prev[k] = (ok && ep.mode >= mma::kGatherAccum) ? out[oe[k]] : 0.0;
+          vx[k] = (ok && ep.mode == mma::kGatherFinal) ? ep.v[oe[k]] : 0.0;
+          et[k] = (ok && ep.mode == mma::kGatherFinal && need_eta) ? ep.eta[px] : 0.0;
+        }
+        OZW(6, umma::mbar_wait(&acc_full[ab], (g >> 1) & 1));
+        umma::fence_after();
 #pragma unroll 1
         for (int hh = 0; hh < 2; ++hh) {
-          uint32_t dv[kSl][16];
+          const int nb = nh * 16 + hh * 8;
+          uint32_t dv[kSl][8];
 #pragma unroll
           for (int tt = 0; tt < kSl; ++tt)
-            umma::tmem_ld16(tl_lane + (uint32_t)(ab * kSl * kGTile + tt * kGTile + hh * 16), dv[tt]);
+            umma::tmem_ld8(tl_lane + (uint32_t)(ab * kSl * kGTile + tt * kGTile + nb), dv[tt]);
           umma::tmem_wait_ld();
           if (hh == 1) {
             umma::fence_before();
@@ -628,37 +686,47 @@ k_gather_oz(const SubDev* __restrict__ subs, const CellDev* __restrict__ cells,
             if (lane == 0) mbar_arrive(&acc_empty[ab]);
           }
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const int nn = hh * 16 + i;
-            double acc = 0.0;
+          for (int i = 0; i < 8; ++i) {
+            const int nn = nb + i;
+            double acc = i2d(dv[kSl - 1][i]);
 #pragma unroll
-            for (int tt = kSl - 1; tt >= 0; --tt)
-              acc = fma(acc, 0.00390625, (double)(int32_t)dv[tt][i]);
-            const int j = j0 + nn;
-            const double aw = j < sd.count ? __ldg(rw + (int64_t)j * 24 + a) : 0.0;
-            double val = acc * ts * aw;
+            for (int tt = kSl - 2; tt >= 0; --tt) acc = fma(acc, 0.00390625, i2d(dv[tt][i]));
+            double val = acc * ts * R[nn * 24 + a];   // rows past the count are stale: not stored
             val += __shfl_xor_sync(0xffffffffu, val, 16);
-            if (lane < 16) sRed[(warp * kGTile + nn) * 16 + r] = val;
+            if (lane < 16) sRed[(lg * kGTile + nn) * 16 + r] = val;
           }
         }
-        asm volatile("bar.sync 2, 128;\n" ::: "memory");
-        // 32 nodes x 16 rhs = 512 outputs, 4 per thread; r fastest (coalesced)
+        asm volatile("bar.sync 2, 256;\n" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&raw_empty[s]);
+        // 32 nodes x 16 rhs = 512 outputs, 2 per thread; r fastest (coalesced)
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const int o = tid + 128 * k;
-          const int nn = o >> 4, rr = o & 15;
-          const int j = j0 + nn;
-          if (j < sd.count) {
-            const double y = (sRed[(0 * kGTile + nn) * 16 + rr] + sRed[(1 * kGTile + nn) * 16 + rr]) +
-                             (sRed[(2 * kGTile + nn) * 16 + rr] + sRed[(3 * kGTile + nn) * 16 + rr]);
-            const int64_t px = pw[j];
-            const int64_t e = px * nrhs + rg + rr;
-            mma::gather_put(ep, out, e, px, rg + rr, y);
+        for (int k = 0; k < 2; ++k) {
+          if (oe[k] < 0) continue;
+          const int o = et_id + 256 * k, nn = o >> 4, rr = o & 15;
+          const double y = (sRed[(0 * kGTile + nn) * 16 + rr] + sRed[(1 * kGTile + nn) * 16 + rr]) +
+                           (sRed[(2 * kGTile + nn) * 16 + rr] + sRed[(3 * kGTile + nn) * 16 + rr]);
+          double res;
+          if (ep.mode == mma::kGatherStore || ep.mode == mma::kGatherFirst) {
+            res = y;
+          } else if (ep.mode == mma::kGatherAccum) {
+            res = prev[k] + y;
+          } else {
+            const int rc = rg + rr;
+            const double lam = ep.coef ? ep.coef[2 * rc] : 0.0;
+            const double mu = ep.coef ? ep.coef[2 * rc + 1] : 0.0;
+            res = mma::epi_value(ep.kind, ep.L, prev[k] + y, vx[k], et[k], lam, mu);
           }
+          out[oe[k]] = res;
         }
-        asm volatile("bar.sync 2, 128;\n" ::: "memory");
+        asm volatile("bar.sync 2, 256;\n" ::: "memory");
       }
     }
+#ifdef NLD_OZ_PROF
+    if (lane == 0)
+      atomicAdd(&oz_prof[8 + (warp == kGLoaderWarp ? 0 : warp == kGIssuerWarp ? 1 : warp >= kGSlicerWarp0 ? 2 : 3)],
+                (unsigned long long)(clock64() - t_role));
+#endif
     gt += ntile;
     umma::fence_before();
     __syncthreads();      // G digits / tsc reused by the next rhs group
@@ -718,6 +786,21 @@ void launch_gather_oz(const PlanSet& ps, const SubDev* subs, const int16_t* ex, 
                                                           ex, grid, grid_ld, out, N, nrhs, ep);
   NLD_CUDA(cudaGetLastError());
 }
+
+#ifdef NLD_OZ_PROF
+void ozaki_prof_dump(const char* what, cudaStream_t st) {
+  unsigned long long h[32];
+  cudaStreamSynchronize(st);
+  cudaMemcpyFromSymbol(h, oz::oz_prof, sizeof(h));
+  fprintf(stderr, "ozprof %s:", what);
+  for (int k = 0; k < 16; ++k) fprintf(stderr, " [%d]%.3g", k, (double)h[k]);
+  fprintf(stderr, "\n");
+  unsigned long long z[32] = {0};
+  cudaMemcpyToSymbol(oz::oz_prof, z, sizeof(z));
+}
+#else
+void ozaki_prof_dump(const char*, cudaStream_t) {}
+#endif
 
 void ozaki_vmax(const double* vt, int64_t n, int nrhs, unsigned long long* out, cudaStream_t st) {
   NLD_CUDA(cudaMemsetAsync(out, 0, sizeof(unsigned long long) * nrhs, st));
