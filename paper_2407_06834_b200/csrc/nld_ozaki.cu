@@ -428,15 +428,33 @@ constexpr int kGA = kRows * 64;                  // 8 KB per G digit slice (K = 
 constexpr int kGB = kGTile * 64;                 // 2 KB per Y digit slice
 constexpr int kGBStage = kSl * kGB;              // 12 KB
 constexpr int kGOpStages = 3;
-constexpr int kGRaw = kGTile * 24 * 8 + kGTile * 4;   // rows + pixel indices per tile
+constexpr int kGRowS = 26;                       // smem row stride (doubles): conflict-free
+constexpr int kGRaw = kGTile * kGRowS * 8 + kGTile * 4;   // rows + pixel indices per tile
 constexpr int kGRawStages = 6;                   // slicers run <= 3 tiles ahead of MMA,
                                                  // the epilogue trails it by <= 2
-constexpr int kGRed = 4 * kGTile * 16 * 8;       // 16 KB a-sum partials
+constexpr int kGRed = 8 * kGTile * 16 * 8;       // 32 KB: T A_j[a] per (a, node, r)
 constexpr int kGatherThreads = 384;              // 8 epilogue, 2 slicer, issuer, loader
 constexpr int kGEpiWarps = 8;
 constexpr int kGSlicerWarp0 = 8;
 constexpr int kGIssuerWarp = 10;
 constexpr int kGLoaderWarp = 11;
+
+// sum_t D_t 2^(16 - 8t), t = 0..5, from the six int32 diagonals: two exact
+// 45-bit integers H = (D0 2^8 + D1) 2^8 + D2, L = (D3 2^8 + D4) 2^8 + D5 on the
+// integer pipe, then H + 2^-24 L with one rounding (2 DADD + 1 DFMA instead of
+// 6 conversions + 5 DFMA per value)
+static_assert(kSl == 6, "combine6 assumes six digits");
+template <int NCOL>
+__device__ __forceinline__ double combine6(const uint32_t (&dv)[6][NCOL], int i) {
+  const long long H = ((long long)(int32_t)dv[0][i] << 16) + ((long long)(int32_t)dv[1][i] << 8) +
+                      (long long)(int32_t)dv[2][i];
+  const long long L = ((long long)(int32_t)dv[3][i] << 16) + ((long long)(int32_t)dv[4][i] << 8) +
+                      (long long)(int32_t)dv[5][i];
+  // |H|, |L| < 2^51: 2^52 + 2^51 + x is exact and has x in its low mantissa bits
+  const double hd = __longlong_as_double(H + 0x4338000000000000LL) - 6755399441055744.0;
+  const double ld = __longlong_as_double(L + 0x4338000000000000LL) - 6755399441055744.0;
+  return fma(ld, 5.9604644775390625e-08, hd);   // 2^-24
+}
 
 // exact int32 -> fp64 without I2F: 2^52 + 2^31 + x has x + 2^31 in its mantissa
 __device__ __forceinline__ double i2d(uint32_t x) {
@@ -539,7 +557,7 @@ k_gather_oz(const SubDev* __restrict__ subs, const CellDev* __restrict__ cells,
     if (tid < 256) {
       const int eG = exp_bound(fmax(gmax[0][m], gmax[1][m]));
       const double sg = pow2(46 - eG);
-      if (h == 0) tsc[m] = pow2(eG + eBm + eCm - 12);   // (eG-46)+(eBm+eCm-46)+80
+      if (h == 0) tsc[m] = pow2(eG + eBm + eCm - 28);   // (eG-46)+(eBm+eCm-46)+80-16
 #pragma unroll 1
       for (int kb = 0; kb < 2; ++kb) {
         uint32_t lo[16], hi[16];
@@ -572,8 +590,11 @@ k_gather_oz(const SubDev* __restrict__ subs, const CellDev* __restrict__ cells,
         const int j0 = tl * kGTile, cn = min(kGTile, sd.count - j0);
         const double* src = rw + (int64_t)j0 * 24;
         uint8_t* dst = sRaw + s * kGRaw;
-        for (int e = lane; e < cn * 12; e += 32) cp_async16(dst + 16 * e, src + 2 * e);
-        if (lane < cn) cp_async4(dst + kGTile * 24 * 8 + 4 * lane, pw + j0 + lane);
+        for (int e = lane; e < cn * 12; e += 32) {
+          const int node = e / 12, gi = e - node * 12;
+          cp_async16(dst + node * kGRowS * 8 + 16 * gi, src + 2 * e);
+        }
+        if (lane < cn) cp_async4(dst + kGTile * kGRowS * 8 + 4 * lane, pw + j0 + lane);
         cp_async_mbar_arrive(&raw_full[s]);
       }
     } else if (warp == kGIssuerWarp) {
@@ -603,21 +624,23 @@ k_gather_oz(const SubDev* __restrict__ subs, const CellDev* __restrict__ cells,
       }
     } else if (warp >= kGSlicerWarp0) {
       // ------------------------------------------------------------- slicers
-      const int t = tid - 32 * kGSlicerWarp0;  // 0..63
-      const int n = t >> 1, kh = t & 1;        // node n, bc half kh (32 values)
+      const int sw = warp - kGSlicerWarp0;     // 0..1
+      const int kq = lane >> 3;                // bc quarter (16 values)
       for (int tl = 0; tl < ntile; ++tl) {
         const int g = gt + tl, s = g % kGRawStages, st = g % kGOpStages;
         OZW(3, umma::mbar_wait(&raw_full[s], (g / kGRawStages) & 1));
         if (g >= kGOpStages) OZW(4, umma::mbar_wait(&op_free[st], ((g / kGOpStages) - 1) & 1));
-        const double* R = reinterpret_cast<const double*>(sRaw + s * kGRaw) + n * 24;
-        const bool ok = tl * kGTile + n < sd.count;
         uint8_t* sB = sGB + st * kGBStage;
-#pragma unroll
-        for (int kq = 0; kq < 2; ++kq) {
+#pragma unroll 1
+        for (int pass = 0; pass < 2; ++pass) {
+          // 8 nodes per warp and pass; rows 26 doubles apart: conflict-free
+          const int n = pass * 16 + sw * 8 + (lane & 7);
+          const double* R = reinterpret_cast<const double*>(sRaw + s * kGRaw) + n * kGRowS;
+          const bool ok = tl * kGTile + n < sd.count;
           uint32_t lo[16], hi[16];
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
-            const int bc = kh * 32 + kq * 16 + i;
+            const int bc = kq * 16 + i;
             double x = 0.0, y = 0.0;
             if (ok) {
               x = R[8 + (bc >> 3)] * syB;
@@ -632,7 +655,7 @@ k_gather_oz(const SubDev* __restrict__ subs, const CellDev* __restrict__ cells,
             w.y = NLD_DW(lo, hi, 4, p);
             w.z = NLD_DW(lo, hi, 8, p);
             w.w = NLD_DW(lo, hi, 12, p);
-            *reinterpret_cast<uint4*>(sB + p * kGB + canon64(n, kh * 32 + kq * 16)) = w;
+            *reinterpret_cast<uint4*>(sB + p * kGB + canon64(n, kq * 16)) = w;
           }
         }
         umma::fence_async_smem();
@@ -651,25 +674,40 @@ k_gather_oz(const SubDev* __restrict__ subs, const CellDev* __restrict__ cells,
       const uint32_t tl_lane = tmem + ((uint32_t)(lg * 32) << 16);
       const bool need_eta = ep.kind == NLD_APPLY_SYSTEM || ep.kind == NLD_APPLY_LAPLACIAN;
       const int et_id = tid;                            // 0..255
-      for (int tl = 0; tl < ntile; ++tl) {
-        const int g = gt + tl, ab = g & 1, s = g % kGRawStages;
-        const int j0 = tl * kGTile;
-        OZW(5, umma::mbar_wait(&raw_full[s], (g / kGRawStages) & 1));
-        const double* R = reinterpret_cast<const double*>(sRaw + s * kGRaw);
-        const int32_t* sp = reinterpret_cast<const int32_t*>(sRaw + s * kGRaw + kGTile * 24 * 8);
-        // this tile's output-side reads, issued before waiting for the tensor core
+      // output-side reads (running sum, v, eta) of tile tl, issued one tile
+      // ahead so their latency hides behind the previous tile's epilogue
+      struct Pre {
         int64_t oe[2];
         double prev[2], vx[2], et[2];
+      };
+      auto prefetch = [&](int tl, Pre& P) {
+        if (tl >= ntile) return;
+        const int g = gt + tl, s = g % kGRawStages, j0 = tl * kGTile;
+        OZW(5, umma::mbar_wait(&raw_full[s], (g / kGRawStages) & 1));
+        const int32_t* sp = reinterpret_cast<const int32_t*>(sRaw + s * kGRaw + kGTile * kGRowS * 8);
 #pragma unroll
         for (int k = 0; k < 2; ++k) {
           const int o = et_id + 256 * k, nn = o >> 4, rr = o & 15;
           const bool ok = j0 + nn < sd.count;
           const int64_t px = ok ? (int64_t)sp[nn] : -1;
-          oe[k] = ok ? px * nrhs + rg + rr : -1;
-          prev[k] = (ok && ep.mode >= mma::kGatherAccum) ? out[oe[k]] : 0.0;
-          vx[k] = (ok && ep.mode == mma::kGatherFinal) ? ep.v[oe[k]] : 0.0;
-          et[k] = (ok && ep.mode == mma::kGatherFinal && need_eta) ? ep.eta[px] : 0.0;
+          P.oe[k] = ok ? px * nrhs + rg + rr : -1;
+          P.prev[k] = (ok && ep.mode >= mma::kGatherAccum) ? out[P.oe[k]] : 0.0;
+          P.vx[k] = (ok && ep.mode == mma::kGatherFinal) ? ep.v[P.oe[k]] : 0.0;
+          P.et[k] = (ok && ep.mode == mma::kGatherFinal && need_eta) ? ep.eta[px] : 0.0;
         }
+      };
+      Pre nxt;
+      prefetch(0, nxt);
+      for (int tl = 0; tl < ntile; ++tl) {
+        const int g = gt + tl, ab = g & 1, s = g % kGRawStages;
+        const int j0 = tl * kGTile;
+        const double* R = reinterpret_cast<const double*>(sRaw + s * kGRaw);
+        const Pre cur = nxt;
+        prefetch(tl + 1, nxt);
+        const int64_t* oe = cur.oe;
+        const double* prev = cur.prev;
+        const double* vx = cur.vx;
+        const double* et = cur.et;
         OZW(6, umma::mbar_wait(&acc_full[ab], (g >> 1) & 1));
         umma::fence_after();
 #pragma unroll 1
@@ -679,24 +717,20 @@ k_gather_oz(const SubDev* __restrict__ subs, const CellDev* __restrict__ cells,
 #pragma unroll
           for (int tt = 0; tt < kSl; ++tt)
             umma::tmem_ld8(tl_lane + (uint32_t)(ab * kSl * kGTile + tt * kGTile + nb), dv[tt]);
-          umma::tmem_wait_ld();
+          OZW(7, umma::tmem_wait_ld());
           if (hh == 1) {
             umma::fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&acc_empty[ab]);
           }
+          double vals[8];
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const int nn = nb + i;
-            double acc = i2d(dv[kSl - 1][i]);
+          for (int i = 0; i < 8; ++i)   // rows past the count are stale: never stored
+            vals[i] = combine6(dv, i) * ts * R[(nb + i) * kGRowS + a];
 #pragma unroll
-            for (int tt = kSl - 2; tt >= 0; --tt) acc = fma(acc, 0.00390625, i2d(dv[tt][i]));
-            double val = acc * ts * R[nn * 24 + a];   // rows past the count are stale: not stored
-            val += __shfl_xor_sync(0xffffffffu, val, 16);
-            if (lane < 16) sRed[(lg * kGTile + nn) * 16 + r] = val;
-          }
+          for (int i = 0; i < 8; ++i) sRed[(a * kGTile + nb + i) * 16 + r] = vals[i];
         }
-        asm volatile("bar.sync 2, 256;\n" ::: "memory");
+        OZW(12, asm volatile("bar.sync 2, 256;\n" ::: "memory"));
         __syncwarp();
         if (lane == 0) mbar_arrive(&raw_empty[s]);
         // 32 nodes x 16 rhs = 512 outputs, 2 per thread; r fastest (coalesced)
@@ -704,8 +738,9 @@ k_gather_oz(const SubDev* __restrict__ subs, const CellDev* __restrict__ cells,
         for (int k = 0; k < 2; ++k) {
           if (oe[k] < 0) continue;
           const int o = et_id + 256 * k, nn = o >> 4, rr = o & 15;
-          const double y = (sRed[(0 * kGTile + nn) * 16 + rr] + sRed[(1 * kGTile + nn) * 16 + rr]) +
-                           (sRed[(2 * kGTile + nn) * 16 + rr] + sRed[(3 * kGTile + nn) * 16 + rr]);
+          const double* q = sRed + nn * 16 + rr;
+          const double y = ((q[0] + q[512]) + (q[1024] + q[1536])) +
+                           ((q[2048] + q[2560]) + (q[3072] + q[3584]));   // sum over a
           double res;
           if (ep.mode == mma::kGatherStore || ep.mode == mma::kGatherFirst) {
             res = y;
@@ -719,7 +754,7 @@ k_gather_oz(const SubDev* __restrict__ subs, const CellDev* __restrict__ cells,
           }
           out[oe[k]] = res;
         }
-        asm volatile("bar.sync 2, 256;\n" ::: "memory");
+        OZW(13, asm volatile("bar.sync 2, 256;\n" ::: "memory"));
       }
     }
 #ifdef NLD_OZ_PROF
