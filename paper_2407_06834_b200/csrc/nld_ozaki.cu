@@ -66,7 +66,9 @@ __device__ __forceinline__ double pow2(int e) {
   return __longlong_as_double((long long)(e + 1023) << 52);
 }
 
-// exponent bound: |x| < 2^e for all x with max |x| = m (0 -> 0)
+// exponent bound: |x| < 2^e for all x with max |x| = m (0 -> 0).  Callers
+// clamp it below at -900 so every 2^(46 - e) scale stays finite; a clamped
+// (tiny) operand then keeps fewer significant digits, never a wrong scale.
 __device__ __forceinline__ int exp_bound(double m) { return m > 0.0 ? ilogb(m) + 1 : 0; }
 
 // canonical K-major no-swizzle offset in a (rows x 32 bytes) tile
@@ -118,7 +120,7 @@ __global__ void k_sub_exponents(const SubDev* __restrict__ subs, const WinDev* _
   __syncthreads();
   if (threadIdx.x < kExpPerSub)
     ex[(int64_t)blockIdx.x * kExpPerSub + threadIdx.x] =
-        (int16_t)exp_bound(__longlong_as_double((long long)mx[threadIdx.x]));
+        (int16_t)max(-900, exp_bound(__longlong_as_double((long long)mx[threadIdx.x])));
 }
 
 // ---- per-rhs exponent of max |v| over all pixels ---------------------------
@@ -233,7 +235,7 @@ k_spread_oz(const SubDev* __restrict__ subs, const WinDev* __restrict__ wins,
     sb[tid] = pow2(46 - ex[8 + tid]);
     sc[tid] = pow2(-ex[16 + tid]);
   }
-  if (tid < 64) csc[tid] = pow2(ex[8 + (tid >> 3)] + ex[16 + (tid & 7)] + 34);
+  if (tid < 64) csc[tid] = ldexp(1.0, ex[8 + (tid >> 3)] + ex[16 + (tid & 7)] + 34);
   umma::fence_before();
   __syncthreads();
   umma::fence_after();
@@ -303,9 +305,11 @@ k_spread_oz(const SubDev* __restrict__ subs, const WinDev* __restrict__ wins,
       const int rg = grp * 16;
       if (tid < kRows) {
         const int a = tid >> 4, r = tid & 15;
-        const int ev = exp_bound(__longlong_as_double((long long)vmax[rg + r]));
+        // |v| below 2^-900 would push 2^(46 - ev) out of range; clamping ev
+        // keeps it finite (tiny v just keeps fewer digits)
+        const int ev = max(-900, exp_bound(__longlong_as_double((long long)vmax[rg + r])));
         sva[tid] = pow2(46 - ev);
-        rsc[tid] = pow2(ev + ex[a] - 46);
+        rsc[tid] = ldexp(1.0, ev + ex[a] - 46);
       }
       asm volatile("bar.sync 1, %0;\n" ::"n"(kSlicers));      // slicers only
       for (int c = 0; c < nchunk; ++c, ++g) {
@@ -555,9 +559,10 @@ k_gather_oz(const SubDev* __restrict__ subs, const CellDev* __restrict__ cells,
     }
     __syncthreads();
     if (tid < 256) {
-      const int eG = exp_bound(fmax(gmax[0][m], gmax[1][m]));
+      // clamped like ev: the digit scale and tsc must use the same exponent
+      const int eG = max(-900, exp_bound(fmax(gmax[0][m], gmax[1][m])));
       const double sg = pow2(46 - eG);
-      if (h == 0) tsc[m] = pow2(eG + eBm + eCm - 28);   // (eG-46)+(eBm+eCm-46)+80-16
+      if (h == 0) tsc[m] = ldexp(1.0, eG + eBm + eCm - 28);   // (eG-46)+(eBm+eCm-46)+80-16
 #pragma unroll 1
       for (int kb = 0; kb < 2; ++kb) {
         uint32_t lo[16], hi[16];
@@ -774,11 +779,13 @@ k_gather_oz(const SubDev* __restrict__ subs, const CellDev* __restrict__ cells,
 
 // ---- host side ------------------------------------------------------------
 
+// integer-sliced tensor-core path: on by default for its shapes (3-D windows,
+// m = 4, rhs batches of 16k); NLD_OZAKI=0 selects the fp64 DMMA kernels
 bool use_ozaki() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("NLD_OZAKI");
-    v = (e && e[0] && e[0] != '0') ? 1 : 0;
+    v = (e && e[0] == '0') ? 0 : 1;
   }
   return v == 1;
 }

@@ -424,3 +424,66 @@ def test_fused_gather_epilogue(case, nrhs):
         assert err < 1e-14, (kind, err)
     if case == "edges":
         assert op.window_info(0)["n_edge"] > 0 and op.window_info(1)["n_edge"] > 0
+
+
+# ------------------------------ integer-sliced tensor-core path (16k rhs)
+
+def test_sliced_products_match_reference(golden):
+    """Batches of 16 rhs take the tcgen05 integer-sliced spread/gather
+    (nld_ozaki.cu); the golden vector rides in column 0 and must match the
+    reference's own outputs at the fp64 parity bar."""
+    from paper_2407_06834_b200 import _lib
+    g = golden("c1")
+    op = operator("c1")[0]
+    v = synth.random_vector(op.n)
+    rng = np.random.default_rng(16)
+    V = rng.standard_normal((op.n, 16))
+    V[:, 0] = v
+    Vd = torch.from_numpy(V).cuda()
+    gam = op.apply_device(Vd, _lib.APPLY_GAMMA, 16, pixel_major=True).cpu().numpy()
+    assert rel(gam[:, 0], g["gv"]) < MATVEC_TOL
+    mu = float(g["mu"])
+    coef = np.tile([1.0, mu], 16)
+    av = op.apply_device(Vd, _lib.APPLY_SYSTEM, 16, coef, pixel_major=True).cpu().numpy()
+    want = v + mu * (g["eta"] * v - g["gv"])
+    assert rel(av[:, 0], want) < MATVEC_TOL
+    # every column equals its own single-rhs (fp64 DMMA) product
+    for k in (1, 7, 15):
+        one = op.apply_device(torch.from_numpy(V[:, k].copy()).cuda(), _lib.APPLY_GAMMA, 1)
+        assert rel(gam[:, k], one.cpu().numpy()) < 1e-12
+
+
+def test_sliced_scale_extremes():
+    """Per-rhs scaling of the digit slices: columns of very different
+    magnitude (and an all-zero column) in one batch keep their accuracy."""
+    from paper_2407_06834_b200 import _lib
+    op = operator("c0")[0]
+    rng = np.random.default_rng(3)
+    V = rng.standard_normal((op.n, 16))
+    scales = np.array([1e-200, 1e200, 0.0, 1.0, 1e-30, 1e30, 2.0 ** -600, 3.0] * 2)
+    V *= scales
+    gam = op.apply_device(torch.from_numpy(V).cuda(), _lib.APPLY_GAMMA, 16,
+                          pixel_major=True).cpu().numpy()
+    for k in range(8):
+        one = op.apply_device(torch.from_numpy(V[:, k].copy()).cuda(), _lib.APPLY_GAMMA, 1)
+        one = one.cpu().numpy()
+        if scales[k] == 0.0:
+            assert np.all(gam[:, k] == 0.0)
+        else:
+            # compare at unit scale (norms of 1e-200 vectors underflow)
+            assert rel(gam[:, k] / scales[k], one / scales[k]) < 1e-12, (k, scales[k])
+
+
+def test_sliced_alpha_sweep_matches_single_solves(golden):
+    """16 alphas share every product on the sliced path; each solve matches
+    the single-rhs fp64 solve (same iterations within one, 1e-9)."""
+    op, _, _, f = operator("c1")
+    eta = op.degree()
+    alphas = synth.alpha_sweep(float(eta.mean()), 16)
+    batch = nld.deflated_solve_batched(op, f[:, 0], 1.0, alphas,
+                                       tol=synth.CG_TOL, maxit=200)
+    for a, res in list(zip(alphas, batch))[::5]:
+        single = nld.deflated_solve(nld.ShiftedSystem(op, 1.0, a), f[:, 0],
+                                    tol=synth.CG_TOL, maxit=200)
+        assert abs(res.iterations - single.iterations) <= 1
+        assert rel(res.x, single.x) < 1e-9
