@@ -262,6 +262,13 @@ def run_ours(args, world, rank, local):
                                        ctypes.c_void_p(stream.cuda_stream)))
     dmma_peak = tf.value
     fp64_peak = max(dfma_peak, dmma_peak)
+    _lib.check(_lib.lib.nld_probe_imma(1 << 14, 0, ctypes.byref(tf), ctypes.byref(pms),
+                                       ctypes.c_void_p(stream.cuda_stream)))
+    imma_peak = tf.value
+    # the library runs 16k-rhs batches of 3-D, m = 4 windows on the
+    # integer-sliced tcgen05 kernels (nld_ozaki.cu) unless NLD_OZAKI=0
+    sliced = (nrhs % 16 == 0 and synth.CUTOFF == 4
+              and os.environ.get("NLD_OZAKI", "1") != "0")
 
     for _ in range(max(args.warmup, 0)):
         step()
@@ -346,28 +353,54 @@ def run_ours(args, world, rank, local):
     except (OSError, ValueError, KeyError):
         peak_src = "fallback"
     achieved = alg_bytes / (dom_ms * 1e-3) / 1e9
-    tag = "k_gather_mma" if dominant == "gather" else "k_spread_mma"
     alg_tflops = alg_flops / (dom_ms * 1e-3) / 1e12
-    roofline = {
-        # the binding roofline: the spread/gather run on the fp64 tensor path
-        # (DMMA), bound by fp64 throughput; MEASURED_PEAKS.json has no fp64
-        # figure, so the peak is measured here, in this run, on this GPU
-        "bound": "tensor", "achieved": alg_tflops, "peak": fp64_peak,
-        "unit": "TFLOP/s", "frac": alg_tflops / fp64_peak,
-        "traffic": ncu_traffic(tag),
-        "traffic_unit": "dram bytes per product (all window launches, ncu, committed profile)",
-        "kernel": tag, "kernel_ms": dom_ms,
-        "peak_source": (f"fp64 measured in this run: DMMA m8n8k4 probe {dmma_peak:.2f}, "
-                        f"DFMA probe {dfma_peak:.2f} TFLOP/s (shared execution "
-                        "resources; max taken)"),
-        "flops_model": ("N*nrhs*sum_l 2*(2m)^d_l per product (all window launches of the "
-                        "kernel, FMA = 2 flop) / the kernel's event-timed stage"),
-        "hbm": {"achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                "frac": achieved / hbm_peak, "peak_source": f"{peak_src} hbm_gbs",
-                "bytes_model": ("minimal (SURVEY §8d): N*(8*sum_l d_l + 8*nrhs) "
-                                "per launch -- not the binding roofline")},
-        "stage_share": {k[:-3]: v / max(elapsed_ms, 1e-9) for k, v in stage.items()},
-    }
+    hbm = {"achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+           "frac": achieved / hbm_peak, "peak_source": f"{peak_src} hbm_gbs",
+           "bytes_model": ("minimal (SURVEY §8d): N*(8*sum_l d_l + 8*nrhs) "
+                           "per launch -- not the binding roofline")}
+    share = {k[:-3]: v / max(elapsed_ms, 1e-9) for k, v in stage.items()}
+    if sliced:
+        # int8 UMMA work actually issued: per 32 nodes and 16 rhs, 6 digit
+        # rows p against (6 - p) stacked 64-wide digit slices, K = 32 (spread)
+        # and the same volume for the gather (2 K steps x (6 - p) 32-node
+        # slices) -> 1344 * 128 * 32 * 2 ops per 32 nodes
+        n3 = sum(1 for i in info if i["dim"] == 3)
+        ops = n * (nrhs // 16) * (1344 * 128 * 32 * 2 // 32) * n3
+        tag = "k_gather_oz" if dominant == "gather" else "k_spread_oz"
+        tops = ops / (dom_ms * 1e-3) / 1e12
+        roofline = {
+            "bound": "tensor", "achieved": tops, "peak": imma_peak, "unit": "TOPS (int8)",
+            "frac": tops / imma_peak,
+            "traffic": ncu_traffic(tag),
+            "traffic_unit": "dram bytes per product (all window launches, ncu, committed profile)",
+            "kernel": tag, "kernel_ms": dom_ms,
+            "peak_source": (f"int8 tcgen05 UMMA probe measured in this run (M=128 N=256 K=32, "
+                            f"one CTA per SM): {imma_peak:.0f} TOPS"),
+            "ops_model": ("int8 MMA ops issued per product: N*(nrhs/16)*344064 per 3-D window "
+                          "(6x6 digit slices, diagonals t<=5) / the kernel's event-timed stage"),
+            "fp64_equivalent": {
+                "achieved": alg_tflops, "unit": "TFLOP/s",
+                "dmma_peak": fp64_peak, "frac_of_dmma_peak": alg_tflops / fp64_peak,
+                "flops_model": "N*nrhs*sum_l 2*(2m)^d_l (the fp64 algorithm's flops)"},
+            "hbm": hbm, "stage_share": share,
+        }
+    else:
+        tag = "k_gather_mma" if dominant == "gather" else "k_spread_mma"
+        roofline = {
+            # fp64 tensor path (DMMA): bound by fp64 throughput; MEASURED_PEAKS.json has
+            # no fp64 figure, so the peak is measured here, in this run, on this GPU
+            "bound": "tensor", "achieved": alg_tflops, "peak": fp64_peak,
+            "unit": "TFLOP/s", "frac": alg_tflops / fp64_peak,
+            "traffic": ncu_traffic(tag),
+            "traffic_unit": "dram bytes per product (all window launches, ncu, committed profile)",
+            "kernel": tag, "kernel_ms": dom_ms,
+            "peak_source": (f"fp64 measured in this run: DMMA m8n8k4 probe {dmma_peak:.2f}, "
+                            f"DFMA probe {dfma_peak:.2f} TFLOP/s (shared execution "
+                            "resources; max taken)"),
+            "flops_model": ("N*nrhs*sum_l 2*(2m)^d_l per product (all window launches of the "
+                            "kernel, FMA = 2 flop) / the kernel's event-timed stage"),
+            "hbm": hbm, "stage_share": share,
+        }
 
     # CG denoise solve (deflated Jacobi, tol 1e-6) over the alpha sweep
     cg = None
@@ -418,6 +451,9 @@ def run_ours(args, world, rank, local):
                        "parallelism": (f"pixel-sharded x{world} (grid allreduce over NCCL)"
                                        if world > 1 else "single"),
                        "l2": "inputs larger than L2 (no flush)",
+                       "kernels": ("integer-sliced tcgen05 spread/gather (exact s8 x s8 -> s32 "
+                                   "digit products, fp64 combine)" if sliced
+                                   else "fp64 DMMA spread/gather"),
                        "setup_s": t_setup},
             "roofline": roofline, "cpu_baseline": cpu,
             "e2e": {"value": e2e_val, "unit": UNIT,

@@ -244,6 +244,10 @@ NLD_API int nld_probe_fp64(int64_t iters, int32_t blocks, double* tflops,
 NLD_API int nld_probe_dmma(int64_t iters, int32_t blocks, double* tflops,
                            double* ms, void* stream);
 /* half the warps DMMA, half DFMA: do the two fp64 paths share resources? */
+/* int8 tensor-core (tcgen05 kind::i8, M=128 N=256 K=32) throughput probe: the
+ * roofline denominator of the integer-sliced spread / gather (TOPS). */
+NLD_API int nld_probe_imma(int64_t iters, int32_t blocks, double* tops, double* ms,
+                           void* stream);
 NLD_API int nld_probe_mixed(int64_t iters_mma, int64_t iters_fma, double* tflops,
                             double* ms, void* stream);
 

@@ -104,6 +104,7 @@ SIGNATURES = {
     "nld_probe_fp64": (ctypes.c_int, [_I64, _I32, _PD, _PD, _P]),
     "nld_probe_dmma": (ctypes.c_int, [_I64, _I32, _PD, _PD, _P]),
     "nld_probe_mixed": (ctypes.c_int, [_I64, _I64, _PD, _PD, _P]),
+    "nld_probe_imma": (ctypes.c_int, [_I64, _I32, _PD, _PD, _P]),
 }
 
 

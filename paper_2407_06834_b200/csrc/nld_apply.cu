@@ -1025,6 +1025,7 @@ void spread_window_fast(const PlanSet& ps, const Workspace& ws, int w, const dou
     if (use_ozaki() && nrhs % 16 == 0 && ps.sub_exp && !getenv("NLD_OZAKI_NO_SPREAD")) {
       launch_spread_oz(ps, subs, ps.sub_exp + wp.sub_off * 24, nsub, ws.vmax, vt, nrhs, ws.blocks,
                        st);
+      if (getenv("NLD_OZ_PROF_PRINT")) ozaki_prof_dump("spread", st);
       if (getenv("NLD_OZAKI_DEBUG")) {
         // compare with the fp64 DMMA spread of the same window (debug only)
         const size_t nb = (size_t)ps.blocks_total * nrhs;

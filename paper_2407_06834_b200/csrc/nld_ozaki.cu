@@ -154,7 +154,7 @@ __device__ __forceinline__ void cp_wait() {
 constexpr int kRawRows = kChunk * 24 * 8;       // 6 KB of weight rows per chunk
 constexpr int kRawV = kChunk * 16 * 8;          // 4 KB of v lines per chunk
 constexpr int kRawBytes = kRawRows + kRawV;
-constexpr int kRawStages = 5;         // raw chunks in flight: kRawStages - 1 ahead
+constexpr int kRawStages = 8;         // raw chunks in flight
 
 constexpr int kOpStages = 3;           // operand stages (slicers <-> tensor core)
 
@@ -219,7 +219,7 @@ k_spread_oz(const SubDev* __restrict__ subs, const WinDev* __restrict__ wins,
   if (warp == 0) umma::tmem_alloc<kTmemCols>(&taddr_s);
   if (tid == 32) {
     for (int k = 0; k < kRawStages; ++k) {
-      umma::mbar_init(&raw_full[k], 32);      // one noinc arrive per loader lane
+      umma::mbar_init(&raw_full[k], 33);      // 32 noinc cp.async arrivals + the bulk copy's
       umma::mbar_init(&raw_empty[k], kSlicers / 32);
     }
     for (int k = 0; k < kOpStages; ++k) {
@@ -240,6 +240,9 @@ k_spread_oz(const SubDev* __restrict__ subs, const WinDev* __restrict__ wins,
   __syncthreads();
   umma::fence_after();
   const uint32_t tmem = taddr_s;
+#ifdef NLD_OZ_PROF
+  const long long t_role = clock64();
+#endif
 
   if (warp == kLoaderWarp) {
     // ---------------------------------------------------------------- loader
@@ -250,33 +253,60 @@ k_spread_oz(const SubDev* __restrict__ subs, const WinDev* __restrict__ wins,
     };
     for (int grp = 0; grp < ngroups; ++grp) {
       const int rg = grp * 16;
-      int32_t px = pix_at(0);
-      for (int c = 0; c < nchunk; ++c, ++g) {
-        const int32_t px_next = pix_at(c + 1);   // one chunk ahead
+      // pixel indices: four registers, each refilled with the index of the
+      // chunk four ahead right after its copies are issued (no register moves
+      // of in-flight loads, so the load latency hides behind four chunks)
+      auto body = [&](int c, int32_t px) {
+        if (c >= nchunk) return;
         const int s = g % kRawStages;
-        if (g >= kRawStages) umma::mbar_wait(&raw_empty[s], ((g / kRawStages) - 1) & 1);
+        if (g >= kRawStages) OZW(16, umma::mbar_wait(&raw_empty[s], ((g / kRawStages) - 1) & 1));
         uint8_t* dst = raw + s * kRawBytes;
         const int j0 = c * kChunk, cn = min(kChunk, sd.count - j0);
-        const double* src = rw + (int64_t)j0 * 24;
-        for (int e = lane; e < cn * 12; e += 32) cp_async16(dst + 16 * e, src + 2 * e);
+        if (lane == 0) {
+          // the chunk's weight rows are contiguous: one TMA bulk copy
+          const uint32_t bytes = (uint32_t)cn * 24 * 8;
+          umma::mbar_arrive_expect_tx(&raw_full[s], bytes);
+          umma::bulk_g2s(dst, rw + (int64_t)j0 * 24, bytes, &raw_full[s]);
+        }
         if (lane < cn) {
+#ifdef NLD_EXP_CONTIG_V
+          const double* vs = vt + (int64_t)(j0 + lane) * nrhs + rg;   // timing experiment only
+#else
           const double* vs = vt + (int64_t)(uint32_t)px * nrhs + rg;
+#endif
           uint8_t* vd = dst + kRawRows + lane * 128;
 #pragma unroll
           for (int q = 0; q < 8; ++q) cp_async16(vd + 16 * q, vs + 2 * q);
         }
+#ifdef NLD_EXP_WAITGROUP
+        cp_commit();
+        cp_wait<0>();
+        mbar_arrive(&raw_full[s]);
+#else
         cp_async_mbar_arrive(&raw_full[s]);
-        px = px_next;
+#endif
+        ++g;
+      };
+      int32_t p0 = pix_at(0), p1 = pix_at(1), p2 = pix_at(2), p3 = pix_at(3);
+      for (int c = 0; c < nchunk; c += 4) {
+        body(c, p0);
+        p0 = pix_at(c + 4);
+        body(c + 1, p1);
+        p1 = pix_at(c + 5);
+        body(c + 2, p2);
+        p2 = pix_at(c + 6);
+        body(c + 3, p3);
+        p3 = pix_at(c + 7);
       }
     }
   } else if (warp == kIssuerWarp) {
     // ---------------------------------------------------------------- issuer
     int g = 0;
     for (int grp = 0; grp < ngroups; ++grp) {
-      if (grp > 0) umma::mbar_wait(&acc_empty, (grp - 1) & 1);   // epilogue drained TMEM
+      if (grp > 0) OZW(18, umma::mbar_wait(&acc_empty, (grp - 1) & 1));   // epilogue drained TMEM
       for (int c = 0; c < nchunk; ++c, ++g) {
         const int st = g % kOpStages;
-        umma::mbar_wait(&op_ready[st], (g / kOpStages) & 1);
+        OZW(17, umma::mbar_wait(&op_ready[st], (g / kOpStages) & 1));
         umma::fence_after();
         if (lane == 0) {
           const uint32_t aB = umma::smem_u32(smem + st * kStageBytes);
@@ -314,8 +344,10 @@ k_spread_oz(const SubDev* __restrict__ subs, const WinDev* __restrict__ wins,
       asm volatile("bar.sync 1, %0;\n" ::"n"(kSlicers));      // slicers only
       for (int c = 0; c < nchunk; ++c, ++g) {
         const int st = g % kOpStages, s = g % kRawStages;
-        umma::mbar_wait(&raw_full[s], (g / kRawStages) & 1);
-        if (g >= kOpStages) umma::mbar_wait(&op_free[st], ((g / kOpStages) - 1) & 1);
+#ifndef NLD_EXP_NORAWWAIT
+        OZW(19, umma::mbar_wait(&raw_full[s], (g / kRawStages) & 1));
+#endif
+        if (g >= kOpStages) OZW(20, umma::mbar_wait(&op_free[st], ((g / kOpStages) - 1) & 1));
         uint8_t* sA = smem + st * kStageBytes;
         uint8_t* sB = sA + kSl * kABytes;
         const double* R = reinterpret_cast<const double*>(raw + s * kRawBytes);
@@ -377,7 +409,7 @@ k_spread_oz(const SubDev* __restrict__ subs, const WinDev* __restrict__ wins,
         }
       }
       // epilogue: accumulators of this rhs group -> block
-      umma::mbar_wait(&acc_full, grp & 1);
+      OZW(21, umma::mbar_wait(&acc_full, grp & 1));
       umma::fence_after();
       {
         const int lg = warp & 3, half = warp >> 2;
@@ -408,6 +440,11 @@ k_spread_oz(const SubDev* __restrict__ subs, const WinDev* __restrict__ wins,
       asm volatile("bar.sync 1, %0;\n" ::"n"(kSlicers));      // rsc reuse by the next group
     }
   }
+#ifdef NLD_OZ_PROF
+  if (lane == 0)
+    atomicAdd(&oz_prof[24 + (warp == kLoaderWarp ? 0 : warp == kIssuerWarp ? 1 : 2)],
+              (unsigned long long)(clock64() - t_role));
+#endif
   umma::fence_before();
   __syncthreads();
   if (warp == 0) umma::tmem_free<kTmemCols>(tmem);
@@ -835,7 +872,8 @@ void ozaki_prof_dump(const char* what, cudaStream_t st) {
   cudaStreamSynchronize(st);
   cudaMemcpyFromSymbol(h, oz::oz_prof, sizeof(h));
   fprintf(stderr, "ozprof %s:", what);
-  for (int k = 0; k < 16; ++k) fprintf(stderr, " [%d]%.3g", k, (double)h[k]);
+  for (int k = 0; k < 32; ++k)
+    if (h[k]) fprintf(stderr, " [%d]%.3g", k, (double)h[k]);
   fprintf(stderr, "\n");
   unsigned long long z[32] = {0};
   cudaMemcpyToSymbol(oz::oz_prof, z, sizeof(z));

@@ -3,6 +3,7 @@
 // MEASURED_PEAKS.json carries HBM and bf16 only, so bench.py measures the
 // sustained DFMA rate on the same box, in the same run.
 #include "nld_internal.cuh"
+#include "nld_umma.cuh"
 
 namespace {
 
@@ -172,6 +173,76 @@ extern "C" NLD_API int nld_probe_fp64(int64_t iters, int32_t blocks, double* tfl
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     cudaFreeAsync(out, st);
+    return NLD_OK;
+  } catch (const nld::Error& e) {
+    return nld::fail(e.code, e.msg);
+  }
+}
+
+// int8 tensor-core (tcgen05 UMMA kind::i8) peak: one CTA per SM issues
+// M = 128, N = 256, K = 32 MMAs back to back from shared memory into TMEM --
+// the roofline denominator of the integer-sliced spread / gather
+__global__ void __launch_bounds__(128, 1) k_imma(int iters, int32_t* sink) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  __shared__ uint64_t mbar;
+  __shared__ uint32_t taddr;
+  for (int e = threadIdx.x; e < (128 + 256) * 32; e += blockDim.x) sm[e] = (uint8_t)(e * 7 + 3);
+  nld::umma::fence_async_smem();
+  if (threadIdx.x < 32) nld::umma::tmem_alloc<512>(&taddr);
+  if (threadIdx.x == 32) {
+    nld::umma::mbar_init(&mbar, 1);
+    nld::umma::mbar_fence_init();
+  }
+  nld::umma::fence_before();
+  __syncthreads();
+  nld::umma::fence_after();
+  const uint32_t t = taddr;
+  if (threadIdx.x == 0) {
+    const uint32_t base = nld::umma::smem_u32(sm);
+    const uint64_t da = nld::umma::make_sdesc(base, 128, 256);
+    const uint64_t db = nld::umma::make_sdesc(base + 128 * 32, 128, 256);
+    const uint32_t idesc = nld::umma::idesc_i8(128, 256);
+    for (int it = 0; it < iters; ++it) nld::umma::mma_i8(t + (it & 1) * 256, da, db, idesc, 1);
+    nld::umma::commit(&mbar);
+  }
+  nld::umma::mbar_wait(&mbar, 0);
+  nld::umma::fence_after();
+  uint32_t r[16];
+  nld::umma::tmem_ld16(t + ((uint32_t)((threadIdx.x >> 5) * 32) << 16), r);
+  nld::umma::tmem_wait_ld();
+  if (r[0] == 0x12345678u) sink[0] = (int32_t)r[1];
+  nld::umma::fence_before();
+  __syncthreads();
+  if (threadIdx.x < 32) nld::umma::tmem_free<512>(t);
+}
+
+extern "C" NLD_API int nld_probe_imma(int64_t iters, int32_t blocks, double* tops, double* ms,
+                                      void* stream) {
+  try {
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    int dev = 0;
+    NLD_CUDA(cudaGetDevice(&dev));
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (blocks <= 0) blocks = sms;
+    int32_t* sink = nullptr;
+    NLD_CUDA(cudaMallocAsync(&sink, sizeof(int32_t), st));
+    const int smem = (128 + 256) * 32;
+    cudaEvent_t e0, e1;
+    NLD_CUDA(cudaEventCreate(&e0));
+    NLD_CUDA(cudaEventCreate(&e1));
+    k_imma<<<blocks, 128, smem, st>>>((int)(iters / 8), sink);
+    NLD_CUDA(cudaEventRecord(e0, st));
+    k_imma<<<blocks, 128, smem, st>>>((int)iters, sink);
+    NLD_CUDA(cudaEventRecord(e1, st));
+    NLD_CUDA(cudaEventSynchronize(e1));
+    float t = 0.f;
+    cudaEventElapsedTime(&t, e0, e1);
+    *ms = t;
+    *tops = 2.0 * 128 * 256 * 32 * (double)iters * blocks / (t * 1e-3) / 1e12;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFreeAsync(sink, st);
     return NLD_OK;
   } catch (const nld::Error& e) {
     return nld::fail(e.code, e.msg);

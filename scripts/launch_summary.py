@@ -10,13 +10,21 @@ ik, iv, iu = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Met
 seq = []
 for r in rows[1:]:
     name = r[ik].split("(")[0].replace("nld::", "").replace("<unnamed>::", "")
-    name = name.replace("mma::", "").replace("void ", "")
+    name = name.replace("mma::", "").replace("oz::", "").replace("void ", "")
     ns = float(r[iv]) * {"ns": 1, "us": 1e3, "usecond": 1e3, "ms": 1e6, "msecond": 1e6}.get(r[iu], 1)
     seq.append((name, ns / 1e6))
-# one steady-state matvec step: everything after the second-to-last epilogue
-# up to the last one (the last product of the run)
+# one steady-state matvec step.  Sliced path: every product starts with the
+# per-rhs max kernel (k_vmax) -> the launches from the second-to-last k_vmax
+# up to the last one.  fp64 DMMA path: after the second-to-last epilogue up
+# to the last one.
+starts = [i for i, (n, _) in enumerate(seq) if "k_vmax" in n]
 ends = [i for i, (n, _) in enumerate(seq) if n.startswith("k_epilogue")]
-step = seq[ends[-2] + 1:ends[-1] + 1] if len(ends) >= 2 else []
+if len(starts) >= 2:
+    step = seq[starts[-2]:starts[-1]]
+elif len(ends) >= 2:
+    step = seq[ends[-2] + 1:ends[-1] + 1]
+else:
+    step = []
 agg = OrderedDict()
 for n, ms in step:
     agg[n] = agg.get(n, 0.0) + ms
