@@ -94,6 +94,42 @@ __device__ __forceinline__ uint32_t digit_word(uint32_t l0, uint32_t l1, uint32_
 #define NLD_DW(L, H, i, p) \
   digit_word(L[i], L[i + 1], L[i + 2], L[i + 3], H[i], H[i + 1], H[i + 2], H[i + 3], p)
 
+// all six digit words of 4 elements (w[p] byte i = digit p of element i):
+// a 4x4 byte transpose of the low words and a 4x2 one of the high words,
+// 12 PRMT + 6 LOP instead of 6 x (3 PRMT + 1 LOP)
+__device__ __forceinline__ void pack4(const uint32_t* l, const uint32_t* h, uint32_t* w) {
+  const uint32_t a01 = __byte_perm(l[0], l[1], 0x5140), b01 = __byte_perm(l[0], l[1], 0x7362);
+  const uint32_t a23 = __byte_perm(l[2], l[3], 0x5140), b23 = __byte_perm(l[2], l[3], 0x7362);
+  const uint32_t h01 = __byte_perm(h[0], h[1], 0x5140), h23 = __byte_perm(h[2], h[3], 0x5140);
+  w[5] = __byte_perm(a01, a23, 0x5410) ^ 0x80808080u;
+  w[4] = __byte_perm(a01, a23, 0x7632) ^ 0x80808080u;
+  w[3] = __byte_perm(b01, b23, 0x5410) ^ 0x80808080u;
+  w[2] = __byte_perm(b01, b23, 0x7632) ^ 0x80808080u;
+  w[1] = __byte_perm(h01, h23, 0x5410) ^ 0x80808080u;
+  w[0] = __byte_perm(h01, h23, 0x7632) ^ 0x80808080u;
+}
+
+// store the 6 digit slices of 16 elements (lo/hi[16]) as one 16-byte word per
+// slice: dst + p * stride
+__device__ __forceinline__ void store16(const uint32_t (&lo)[16], const uint32_t (&hi)[16],
+                                        uint8_t* dst, int stride) {
+  uint32_t w[4][6];
+#pragma unroll
+  for (int g = 0; g < 4; ++g) pack4(lo + 4 * g, hi + 4 * g, w[g]);
+#pragma unroll
+  for (int p = 0; p < 6; ++p)
+    *reinterpret_cast<uint4*>(dst + p * stride) = make_uint4(w[0][p], w[1][p], w[2][p], w[3][p]);
+}
+__device__ __forceinline__ void store8(const uint32_t (&lo)[8], const uint32_t (&hi)[8],
+                                       uint8_t* dst, int stride) {
+  uint32_t w[2][6];
+#pragma unroll
+  for (int g = 0; g < 2; ++g) pack4(lo + 4 * g, hi + 4 * g, w[g]);
+#pragma unroll
+  for (int p = 0; p < 6; ++p)
+    *reinterpret_cast<uint2*>(dst + p * stride) = make_uint2(w[0][p], w[1][p]);
+}
+
 __device__ __forceinline__ void slice1(double x, double y, uint32_t& lo, uint32_t& hi) {
   const long long u = __double_as_longlong(fma(x, y, kMagic));
   lo = (uint32_t)u;
@@ -368,15 +404,7 @@ k_spread_oz(const SubDev* __restrict__ subs, const WinDev* __restrict__ wins,
             }
             slice1(x, y, lo[i], hi[i]);
           }
-#pragma unroll
-          for (int p = 0; p < kSl; ++p) {
-            uint4 w;
-            w.x = NLD_DW(lo, hi, 0, p);
-            w.y = NLD_DW(lo, hi, 4, p);
-            w.z = NLD_DW(lo, hi, 8, p);
-            w.w = NLD_DW(lo, hi, 12, p);
-            *reinterpret_cast<uint4*>(sA + p * kABytes + canon32(m, h * 16)) = w;
-          }
+        store16(lo, hi, sA + canon32(m, h * 16), kABytes);
         }
         {
           const int n = tid & 63, gq = tid >> 6;
@@ -393,13 +421,7 @@ k_spread_oz(const SubDev* __restrict__ subs, const WinDev* __restrict__ wins,
             }
             slice1(x, y, lo[i], hi[i]);
           }
-#pragma unroll
-          for (int p = 0; p < kSl; ++p) {
-            uint2 w;
-            w.x = NLD_DW(lo, hi, 0, p);
-            w.y = NLD_DW(lo, hi, 4, p);
-            *reinterpret_cast<uint2*>(sB + p * kBBytes + canon32(n, gq * 8)) = w;
-          }
+        store8(lo, hi, sB + canon32(n, gq * 8), kBBytes);
         }
         umma::fence_async_smem();
         __syncwarp();
@@ -605,15 +627,7 @@ k_gather_oz(const SubDev* __restrict__ subs, const CellDev* __restrict__ cells,
         uint32_t lo[16], hi[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) slice1(gval(h * 32 + kb * 16 + i), sg, lo[i], hi[i]);
-#pragma unroll
-        for (int p = 0; p < kSl; ++p) {
-          uint4 w;
-          w.x = NLD_DW(lo, hi, 0, p);
-          w.y = NLD_DW(lo, hi, 4, p);
-          w.z = NLD_DW(lo, hi, 8, p);
-          w.w = NLD_DW(lo, hi, 12, p);
-          *reinterpret_cast<uint4*>(sGA + p * kGA + canon64(m, h * 32 + kb * 16)) = w;
-        }
+      store16(lo, hi, sGA + canon64(m, h * 32 + kb * 16), kGA);
       }
     }
     umma::fence_async_smem();
@@ -690,15 +704,7 @@ k_gather_oz(const SubDev* __restrict__ subs, const CellDev* __restrict__ cells,
             }
             slice1(x, y, lo[i], hi[i]);
           }
-#pragma unroll
-          for (int p = 0; p < kSl; ++p) {
-            uint4 w;
-            w.x = NLD_DW(lo, hi, 0, p);
-            w.y = NLD_DW(lo, hi, 4, p);
-            w.z = NLD_DW(lo, hi, 8, p);
-            w.w = NLD_DW(lo, hi, 12, p);
-            *reinterpret_cast<uint4*>(sB + p * kGB + canon64(n, kq * 16)) = w;
-          }
+        store16(lo, hi, sB + canon64(n, kq * 16), kGB);
         }
         umma::fence_async_smem();
         __syncwarp();
