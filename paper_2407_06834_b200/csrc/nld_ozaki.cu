@@ -21,6 +21,7 @@
 // rounds x'y' to an integer and leaves x'y' + 0x80..80 in the low 48
 // mantissa bits, whose bytes XOR 0x80 are the balanced digits.
 #include <algorithm>
+#include <type_traits>
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
@@ -389,40 +390,45 @@ k_spread_oz(const SubDev* __restrict__ subs, const WinDev* __restrict__ wins,
         const double* R = reinterpret_cast<const double*>(raw + s * kRawBytes);
         const double* Vr = R + kChunk * 24;
         const int cn = min(kChunk, sd.count - c * kChunk);
-        {
-          const int m = tid & 127, h = tid >> 7;
-          const int a = m >> 4, r = m & 15;
-          const double sx = sva[m] * sa[a];      // exact: a product of powers of two
-          uint32_t lo[16], hi[16];
+        // full chunks (all but a subproblem's last) skip the per-node guards
+        auto slice_chunk = [&](auto full) {
+          {
+            const int m = tid & 127, h = tid >> 7;
+            const int a = m >> 4, r = m & 15;
+            const double sx = sva[m] * sa[a];      // exact: a product of powers of two
+            uint32_t lo[16], hi[16];
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const int j = h * 16 + i;
-            double x = 0.0, y = 0.0;
-            if (j < cn) {
-              x = Vr[j * 16 + r];
-              y = R[j * 24 + a] * sx;
+            for (int i = 0; i < 16; ++i) {
+              const int j = h * 16 + i;
+              double x = 0.0, y = 0.0;
+              if (full || j < cn) {
+                x = Vr[j * 16 + r];
+                y = R[j * 24 + a] * sx;
+              }
+              slice1(x, y, lo[i], hi[i]);
             }
-            slice1(x, y, lo[i], hi[i]);
+            store16(lo, hi, sA + canon32(m, h * 16), kABytes);
           }
-        store16(lo, hi, sA + canon32(m, h * 16), kABytes);
-        }
-        {
-          const int n = tid & 63, gq = tid >> 6;
-          const int b = n >> 3, cc = n & 7;
-          const double sy = sb[b] * sc[cc];
-          uint32_t lo[8], hi[8];
+          {
+            const int n = tid & 63, gq = tid >> 6;
+            const int b = n >> 3, cc = n & 7;
+            const double sy = sb[b] * sc[cc];
+            uint32_t lo[8], hi[8];
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const int j = gq * 8 + i;
-            double x = 0.0, y = 0.0;
-            if (j < cn) {
-              x = R[j * 24 + 8 + b] * sy;
-              y = R[j * 24 + 16 + cc];
+            for (int i = 0; i < 8; ++i) {
+              const int j = gq * 8 + i;
+              double x = 0.0, y = 0.0;
+              if (full || j < cn) {
+                x = R[j * 24 + 8 + b] * sy;
+                y = R[j * 24 + 16 + cc];
+              }
+              slice1(x, y, lo[i], hi[i]);
             }
-            slice1(x, y, lo[i], hi[i]);
+            store8(lo, hi, sB + canon32(n, gq * 8), kBBytes);
           }
-        store8(lo, hi, sB + canon32(n, gq * 8), kBBytes);
-        }
+        };
+        if (cn == kChunk) slice_chunk(std::true_type{});
+        else slice_chunk(std::false_type{});
         umma::fence_async_smem();
         __syncwarp();
         if (lane == 0) {
