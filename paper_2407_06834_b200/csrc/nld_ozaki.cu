@@ -607,7 +607,7 @@ k_gather_oz(const SubDev* __restrict__ subs, const CellDev* __restrict__ cells,
     // thread t < 256: row m = t & 127 = (a, r), bc half h = t >> 7; two passes
     // over the (L2-resident) support box: the row max, then the digits
     const int m = tid & 127, h = (tid >> 7) & 1;
-    const int ga = m >> 4, gr = m & 15;
+    const int ga = m & 7, gr = m >> 3;        // rows ordered (r, a): a fastest
     auto gval = [&](int bc) -> double {
       int p0 = cd.cc[0] + ga, p1 = cd.cc[1] + (bc >> 3), p2 = cd.cc[2] + (bc & 7);
       if (p0 >= wd.box_w[0]) p0 -= wd.box_w[0];
@@ -721,101 +721,97 @@ k_gather_oz(const SubDev* __restrict__ subs, const CellDev* __restrict__ cells,
       }
     } else {
       // ------------------------------------------------------------ epilogue
+      // TMEM lane = row (r, a) with a fastest: the 8 a-rows of one rhs sit in
+      // 8 adjacent lanes, so the sum over a is an in-warp butterfly that also
+      // scatters the 8 nodes of a group over those lanes (lane a ends with
+      // node a's sum) -- no shared-memory round trip, no named barriers
       const int lg = warp & 3, nh = warp >> 2;          // TMEM lane group, node half
-      const int a = 2 * lg + (lane >> 4), r = lane & 15;
+      const int a = lane & 7, r = 4 * lg + (lane >> 3);
       const int mrow = lg * 32 + lane;
       const double ts = tsc[mrow];
       const uint32_t tl_lane = tmem + ((uint32_t)(lg * 32) << 16);
       const bool need_eta = ep.kind == NLD_APPLY_SYSTEM || ep.kind == NLD_APPLY_LAPLACIAN;
-      const int et_id = tid;                            // 0..255
-      // output-side reads (running sum, v, eta) of tile tl, issued one tile
-      // ahead so their latency hides behind the previous tile's epilogue
-      struct Pre {
-        int64_t oe[2];
-        double prev[2], vx[2], et[2];
-      };
-      auto prefetch = [&](int tl, Pre& P) {
-        if (tl >= ntile) return;
-        const int g = gt + tl, s = g % kGRawStages, j0 = tl * kGTile;
-        OZW(5, umma::mbar_wait(&raw_full[s], (g / kGRawStages) & 1));
-        const int32_t* sp = reinterpret_cast<const int32_t*>(sRaw + s * kGRaw + kGTile * kGRowS * 8);
-#pragma unroll
-        for (int k = 0; k < 2; ++k) {
-          const int o = et_id + 256 * k, nn = o >> 4, rr = o & 15;
-          const bool ok = j0 + nn < sd.count;
-          const int64_t px = ok ? (int64_t)sp[nn] : -1;
-          P.oe[k] = ok ? px * nrhs + rg + rr : -1;
-          P.prev[k] = (ok && ep.mode >= mma::kGatherAccum) ? out[P.oe[k]] : 0.0;
-          P.vx[k] = (ok && ep.mode == mma::kGatherFinal) ? ep.v[P.oe[k]] : 0.0;
-          P.et[k] = (ok && ep.mode == mma::kGatherFinal && need_eta) ? ep.eta[px] : 0.0;
-        }
-      };
-      Pre nxt;
-      prefetch(0, nxt);
       for (int tl = 0; tl < ntile; ++tl) {
         const int g = gt + tl, ab = g & 1, s = g % kGRawStages;
         const int j0 = tl * kGTile;
+        umma::mbar_wait(&raw_full[s], (g / kGRawStages) & 1);
         const double* R = reinterpret_cast<const double*>(sRaw + s * kGRaw);
-        const Pre cur = nxt;
-        prefetch(tl + 1, nxt);
-        const int64_t* oe = cur.oe;
-        const double* prev = cur.prev;
-        const double* vx = cur.vx;
-        const double* et = cur.et;
-        OZW(6, umma::mbar_wait(&acc_full[ab], (g >> 1) & 1));
+        const int32_t* sp = reinterpret_cast<const int32_t*>(sRaw + s * kGRaw + kGTile * kGRowS * 8);
+        // this lane's two outputs: node nb + a of each 8-node group, rhs r
+        int64_t oe[2];
+        double prev[2], vx[2], et[2];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int nn = nh * 16 + q * 8 + a;
+          const bool ok = j0 + nn < sd.count;
+          const int64_t px = ok ? (int64_t)sp[nn] : -1;
+          oe[q] = ok ? px * nrhs + rg + r : -1;
+          prev[q] = (ok && ep.mode >= mma::kGatherAccum) ? out[oe[q]] : 0.0;
+          vx[q] = (ok && ep.mode == mma::kGatherFinal) ? ep.v[oe[q]] : 0.0;
+          et[q] = (ok && ep.mode == mma::kGatherFinal && need_eta) ? ep.eta[px] : 0.0;
+        }
+        umma::mbar_wait(&acc_full[ab], (g >> 1) & 1);
         umma::fence_after();
-#pragma unroll 1
-        for (int hh = 0; hh < 2; ++hh) {
-          const int nb = nh * 16 + hh * 8;
+        double ysum[2];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int nb = nh * 16 + q * 8;
           uint32_t dv[kSl][8];
 #pragma unroll
           for (int tt = 0; tt < kSl; ++tt)
             umma::tmem_ld8(tl_lane + (uint32_t)(ab * kSl * kGTile + tt * kGTile + nb), dv[tt]);
-          OZW(7, umma::tmem_wait_ld());
-          if (hh == 1) {
+          umma::tmem_wait_ld();
+          if (q == 1) {
             umma::fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&acc_empty[ab]);
           }
-          double vals[8];
+          double v8[8];
 #pragma unroll
           for (int i = 0; i < 8; ++i)   // rows past the count are stale: never stored
-            vals[i] = combine6(dv, i) * ts * R[(nb + i) * kGRowS + a];
+            v8[i] = combine6(dv, i) * ts * R[(nb + i) * kGRowS + a];
+          // butterfly reduce-scatter over the 8 a-lanes (lane bits 0..2)
 #pragma unroll
-          for (int i = 0; i < 8; ++i) sRed[(a * kGTile + nb + i) * 16 + r] = vals[i];
+          for (int i = 0; i < 4; ++i) {
+            const bool up = lane & 4;
+            const double send = up ? v8[i] : v8[i + 4];
+            const double keep = up ? v8[i + 4] : v8[i];
+            v8[i] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+          }
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            const bool up = lane & 2;
+            const double send = up ? v8[i] : v8[i + 2];
+            const double keep = up ? v8[i + 2] : v8[i];
+            v8[i] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+          }
+          {
+            const bool up = lane & 1;
+            const double send = up ? v8[0] : v8[1];
+            const double keep = up ? v8[1] : v8[0];
+            ysum[q] = keep + __shfl_xor_sync(0xffffffffu, send, 1);
+          }
         }
-        OZW(12, asm volatile("bar.sync 2, 256;\n" ::: "memory"));
         __syncwarp();
         if (lane == 0) mbar_arrive(&raw_empty[s]);
-        // 32 nodes x 16 rhs = 512 outputs, 2 per thread; r fastest (coalesced)
 #pragma unroll
-        for (int k = 0; k < 2; ++k) {
-          if (oe[k] < 0) continue;
-          const int o = et_id + 256 * k, nn = o >> 4, rr = o & 15;
-          const double* q = sRed + nn * 16 + rr;
-          const double y = ((q[0] + q[512]) + (q[1024] + q[1536])) +
-                           ((q[2048] + q[2560]) + (q[3072] + q[3584]));   // sum over a
+        for (int q = 0; q < 2; ++q) {
+          if (oe[q] < 0) continue;
+          const double y = ysum[q];
           double res;
           if (ep.mode == mma::kGatherStore || ep.mode == mma::kGatherFirst) {
             res = y;
           } else if (ep.mode == mma::kGatherAccum) {
-            res = prev[k] + y;
+            res = prev[q] + y;
           } else {
-            const int rc = rg + rr;
-            const double lam = ep.coef ? ep.coef[2 * rc] : 0.0;
-            const double mu = ep.coef ? ep.coef[2 * rc + 1] : 0.0;
-            res = mma::epi_value(ep.kind, ep.L, prev[k] + y, vx[k], et[k], lam, mu);
+            const double lam = ep.coef ? ep.coef[2 * (rg + r)] : 0.0;
+            const double mu = ep.coef ? ep.coef[2 * (rg + r) + 1] : 0.0;
+            res = mma::epi_value(ep.kind, ep.L, prev[q] + y, vx[q], et[q], lam, mu);
           }
-          out[oe[k]] = res;
+          out[oe[q]] = res;
         }
-        OZW(13, asm volatile("bar.sync 2, 256;\n" ::: "memory"));
       }
     }
-#ifdef NLD_OZ_PROF
-    if (lane == 0)
-      atomicAdd(&oz_prof[8 + (warp == kGLoaderWarp ? 0 : warp == kGIssuerWarp ? 1 : warp >= kGSlicerWarp0 ? 2 : 3)],
-                (unsigned long long)(clock64() - t_role));
-#endif
     gt += ntile;
     umma::fence_before();
     __syncthreads();      // G digits / tsc reused by the next rhs group
