@@ -496,17 +496,27 @@ constexpr int kGTile = 32;                       // nodes per tile
 constexpr int kGA = kRows * 64;                  // 8 KB per G digit slice (K = 64)
 constexpr int kGB = kGTile * 64;                 // 2 KB per Y digit slice
 constexpr int kGBStage = kSl * kGB;              // 12 KB
-constexpr int kGOpStages = 3;
+// Two CTAs per SM (default; NLD_GATHER_CTAS=1 builds the one-CTA variant with a
+// double-buffered TMEM accumulator and 8 epilogue warps): each CTA has a single
+// 192-column accumulator, 4 epilogue warps and shallower stages, so one CTA's
+// per-subproblem G setup and drain overlap the other's tiles
+#ifndef NLD_GATHER_CTAS
+#define NLD_GATHER_CTAS 2
+#endif
+constexpr int kGCtas = NLD_GATHER_CTAS;
+constexpr int kGAccBufs = kGCtas == 2 ? 1 : 2;
+constexpr int kGTmemCols = kGCtas == 2 ? 256 : 512;
+constexpr int kGOpStages = kGCtas == 2 ? 2 : 3;
 constexpr int kGRowS = 26;                       // smem row stride (doubles): conflict-free
 constexpr int kGRaw = kGTile * kGRowS * 8 + kGTile * 4;   // rows + pixel indices per tile
-constexpr int kGRawStages = 6;                   // slicers run <= 3 tiles ahead of MMA,
-                                                 // the epilogue trails it by <= 2
-constexpr int kGRed = 8 * kGTile * 16 * 8;       // 32 KB: T A_j[a] per (a, node, r)
-constexpr int kGatherThreads = 384;              // 8 epilogue, 2 slicer, issuer, loader
-constexpr int kGEpiWarps = 8;
-constexpr int kGSlicerWarp0 = 8;
-constexpr int kGIssuerWarp = 10;
-constexpr int kGLoaderWarp = 11;
+constexpr int kGRawStages = kGCtas == 2 ? 4 : 6; // slicers run ahead of the MMA, the
+                                                 // epilogue trails it
+constexpr int kGEpiWarps = kGCtas == 2 ? 4 : 8;
+constexpr int kGatherThreads = 32 * (kGEpiWarps + 4);   // epilogue, 2 slicer, issuer, loader
+constexpr int kGSlicerWarp0 = kGEpiWarps;
+constexpr int kGIssuerWarp = kGEpiWarps + 2;
+constexpr int kGLoaderWarp = kGEpiWarps + 3;
+constexpr int kGNodeGroups = kGTile / 8 / (kGEpiWarps / 4);   // 8-node groups per epilogue warp
 
 // sum_t D_t 2^(16 - 8t), t = 0..5, from the six int32 diagonals: two exact
 // 45-bit integers H = (D0 2^8 + D1) 2^8 + D2, L = (D3 2^8 + D4) 2^8 + D5 on the
@@ -535,7 +545,7 @@ __device__ __forceinline__ double i2d(uint32_t x) {
 }
 
 __host__ __device__ constexpr int gather_oz_smem() {
-  return kSl * kGA + kGOpStages * kGBStage + kGRawStages * kGRaw + kGRed;
+  return kSl * kGA + kGOpStages * kGBStage + kGRawStages * kGRaw;
 }
 
 // canonical K-major no-swizzle offset in a (rows x 64 bytes) tile
@@ -543,7 +553,7 @@ __device__ __forceinline__ int canon64(int row, int k) {
   return (row >> 3) * 512 + (k >> 4) * 128 + (row & 7) * 16 + (k & 15);
 }
 
-__global__ void __launch_bounds__(kGatherThreads, 1)
+__global__ void __launch_bounds__(kGatherThreads, kGCtas)
 k_gather_oz(const SubDev* __restrict__ subs, const CellDev* __restrict__ cells,
             const WinDev* __restrict__ wins, const double* __restrict__ rows,
             const int32_t* __restrict__ pix, const int16_t* __restrict__ sub_exp,
@@ -552,7 +562,7 @@ k_gather_oz(const SubDev* __restrict__ subs, const CellDev* __restrict__ cells,
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ uint64_t raw_full[kGRawStages], raw_empty[kGRawStages];
   __shared__ uint64_t op_ready[kGOpStages], op_free[kGOpStages];
-  __shared__ uint64_t acc_full[2], acc_empty[2];
+  __shared__ uint64_t acc_full[kGAccBufs], acc_empty[kGAccBufs];
   __shared__ uint32_t taddr_s;
   __shared__ double gmax[2][kRows];
   __shared__ double tsc[kRows];           // T scale per row: 2^(eG + eY - 92 + 80)
@@ -567,7 +577,6 @@ k_gather_oz(const SubDev* __restrict__ subs, const CellDev* __restrict__ cells,
   uint8_t* const sGA = smem;
   uint8_t* const sGB = sGA + kSl * kGA;
   uint8_t* const sRaw = sGB + kGOpStages * kGBStage;
-  double* const sRed = reinterpret_cast<double*>(sRaw + kGRawStages * kGRaw);
   const int ntile = (sd.count + kGTile - 1) / kGTile;
   const int ngroups = nrhs / 16;
   // Y scale: one per subproblem, |B_j[b] C_j[c]| < 2^(eBm + eCm)
@@ -579,7 +588,7 @@ k_gather_oz(const SubDev* __restrict__ subs, const CellDev* __restrict__ cells,
   }
   const double syB = pow2(46 - eBm), syC = pow2(-eCm);
 
-  if (warp == 0) umma::tmem_alloc<kTmemCols>(&taddr_s);
+  if (warp == 0) umma::tmem_alloc<kGTmemCols>(&taddr_s);
   if (tid == 32) {
     for (int k = 0; k < kGRawStages; ++k) {
       umma::mbar_init(&raw_full[k], 32);
@@ -589,7 +598,7 @@ k_gather_oz(const SubDev* __restrict__ subs, const CellDev* __restrict__ cells,
       umma::mbar_init(&op_ready[k], 2);       // slicer warps
       umma::mbar_init(&op_free[k], 1);
     }
-    for (int k = 0; k < 2; ++k) {
+    for (int k = 0; k < kGAccBufs; ++k) {
       umma::mbar_init(&acc_full[k], 1);
       umma::mbar_init(&acc_empty[k], kGEpiWarps);
     }
@@ -662,14 +671,15 @@ k_gather_oz(const SubDev* __restrict__ subs, const CellDev* __restrict__ cells,
     } else if (warp == kGIssuerWarp) {
       // -------------------------------------------------------------- issuer
       for (int tl = 0; tl < ntile; ++tl) {
-        const int g = gt + tl, st = g % kGOpStages, ab = g & 1;
-        if (g >= 2) OZW(1, umma::mbar_wait(&acc_empty[ab], ((g >> 1) - 1) & 1));
+        const int g = gt + tl, st = g % kGOpStages, ab = g % kGAccBufs;
+        if (g >= kGAccBufs) OZW(1, umma::mbar_wait(&acc_empty[ab], ((g / kGAccBufs) - 1) & 1));
         OZW(2, umma::mbar_wait(&op_ready[st], (g / kGOpStages) & 1));
         umma::fence_after();
         if (lane == 0) {
           const uint32_t aB = umma::smem_u32(sGA);
           const uint32_t bB = umma::smem_u32(sGB + st * kGBStage);
           const uint32_t dcol = tmem + (uint32_t)(ab * kSl * kGTile);
+#ifndef NLD_EXP_GNOMMA
 #pragma unroll
           for (int ks = 0; ks < 2; ++ks)
 #pragma unroll
@@ -679,6 +689,7 @@ k_gather_oz(const SubDev* __restrict__ subs, const CellDev* __restrict__ cells,
               umma::mma_i8(dcol + (uint32_t)(p * kGTile), da, db,
                            umma::idesc_i8(kRows, (kSl - p) * kGTile), (ks > 0 || p > 0) ? 1u : 0u);
             }
+#endif
           umma::commit(&op_free[st]);
           umma::commit(&acc_full[ab]);
         }
@@ -693,6 +704,7 @@ k_gather_oz(const SubDev* __restrict__ subs, const CellDev* __restrict__ cells,
         OZW(3, umma::mbar_wait(&raw_full[s], (g / kGRawStages) & 1));
         if (g >= kGOpStages) OZW(4, umma::mbar_wait(&op_free[st], ((g / kGOpStages) - 1) & 1));
         uint8_t* sB = sGB + st * kGBStage;
+#ifndef NLD_EXP_GNOSLICE
 #pragma unroll 1
         for (int pass = 0; pass < 2; ++pass) {
           // 8 nodes per warp and pass; rows 26 doubles apart: conflict-free
@@ -712,6 +724,7 @@ k_gather_oz(const SubDev* __restrict__ subs, const CellDev* __restrict__ cells,
           }
         store16(lo, hi, sB + canon64(n, kq * 16), kGB);
         }
+#endif
         umma::fence_async_smem();
         __syncwarp();
         if (lane == 0) {
@@ -732,17 +745,17 @@ k_gather_oz(const SubDev* __restrict__ subs, const CellDev* __restrict__ cells,
       const uint32_t tl_lane = tmem + ((uint32_t)(lg * 32) << 16);
       const bool need_eta = ep.kind == NLD_APPLY_SYSTEM || ep.kind == NLD_APPLY_LAPLACIAN;
       for (int tl = 0; tl < ntile; ++tl) {
-        const int g = gt + tl, ab = g & 1, s = g % kGRawStages;
+        const int g = gt + tl, ab = g % kGAccBufs, s = g % kGRawStages;
         const int j0 = tl * kGTile;
         umma::mbar_wait(&raw_full[s], (g / kGRawStages) & 1);
         const double* R = reinterpret_cast<const double*>(sRaw + s * kGRaw);
         const int32_t* sp = reinterpret_cast<const int32_t*>(sRaw + s * kGRaw + kGTile * kGRowS * 8);
         // this lane's two outputs: node nb + a of each 8-node group, rhs r
-        int64_t oe[2];
-        double prev[2], vx[2], et[2];
+        int64_t oe[kGNodeGroups];
+        double prev[kGNodeGroups], vx[kGNodeGroups], et[kGNodeGroups];
 #pragma unroll
-        for (int q = 0; q < 2; ++q) {
-          const int nn = nh * 16 + q * 8 + a;
+        for (int q = 0; q < kGNodeGroups; ++q) {
+          const int nn = (nh * kGNodeGroups + q) * 8 + a;
           const bool ok = j0 + nn < sd.count;
           const int64_t px = ok ? (int64_t)sp[nn] : -1;
           oe[q] = ok ? px * nrhs + rg + r : -1;
@@ -750,18 +763,18 @@ k_gather_oz(const SubDev* __restrict__ subs, const CellDev* __restrict__ cells,
           vx[q] = (ok && ep.mode == mma::kGatherFinal) ? ep.v[oe[q]] : 0.0;
           et[q] = (ok && ep.mode == mma::kGatherFinal && need_eta) ? ep.eta[px] : 0.0;
         }
-        umma::mbar_wait(&acc_full[ab], (g >> 1) & 1);
+        umma::mbar_wait(&acc_full[ab], (g / kGAccBufs) & 1);
         umma::fence_after();
-        double ysum[2];
+        double ysum[kGNodeGroups];
 #pragma unroll
-        for (int q = 0; q < 2; ++q) {
-          const int nb = nh * 16 + q * 8;
+        for (int q = 0; q < kGNodeGroups; ++q) {
+          const int nb = (nh * kGNodeGroups + q) * 8;
           uint32_t dv[kSl][8];
 #pragma unroll
           for (int tt = 0; tt < kSl; ++tt)
             umma::tmem_ld8(tl_lane + (uint32_t)(ab * kSl * kGTile + tt * kGTile + nb), dv[tt]);
           umma::tmem_wait_ld();
-          if (q == 1) {
+          if (q == kGNodeGroups - 1) {
             umma::fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&acc_empty[ab]);
@@ -795,7 +808,7 @@ k_gather_oz(const SubDev* __restrict__ subs, const CellDev* __restrict__ cells,
         __syncwarp();
         if (lane == 0) mbar_arrive(&raw_empty[s]);
 #pragma unroll
-        for (int q = 0; q < 2; ++q) {
+        for (int q = 0; q < kGNodeGroups; ++q) {
           if (oe[q] < 0) continue;
           const double y = ysum[q];
           double res;
@@ -817,7 +830,7 @@ k_gather_oz(const SubDev* __restrict__ subs, const CellDev* __restrict__ cells,
     __syncthreads();      // G digits / tsc reused by the next rhs group
     umma::fence_after();
   }
-  if (warp == 0) umma::tmem_free<kTmemCols>(tmem);
+  if (warp == 0) umma::tmem_free<kGTmemCols>(tmem);
 }
 
 }  // namespace oz

@@ -487,3 +487,47 @@ def test_sliced_alpha_sweep_matches_single_solves(golden):
                                     tol=synth.CG_TOL, maxit=200)
         assert abs(res.iterations - single.iterations) <= 1
         assert rel(res.x, single.x) < 1e-9
+
+
+def test_sharded_sliced_path_matches_single_gpu():
+    """2 ranks (ThreadComm on one GPU) with 16-rhs batches: the sliced
+    tcgen05 spread/gather + grid allreduce equal the unsharded products; the
+    ranks' digit scales differ (local max |v|) but the fp64 results agree."""
+    import threading
+
+    from paper_2407_06834_b200 import _lib
+    from paper_2407_06834_b200 import sharding as S
+    full, feats, wins, f = operator("c1")
+    n = feats.shape[0]
+    rng = np.random.default_rng(17)
+    V = rng.standard_normal((n, 16))
+    V[: n // 2] *= 1e3                     # rank 0 and rank 1 see different scales
+    coef = np.stack([np.ones(16), rng.uniform(0, 0.01, 16)], 1).ravel()
+    want = full.apply_device(torch.from_numpy(V).cuda(), _lib.APPLY_SYSTEM, 16, coef,
+                             pixel_major=True).cpu().numpy()
+    world = 2
+    comm = S.ThreadComm(world, device=torch.device("cuda", 0))
+    out, errs = {}, []
+
+    def rank_main(rank):
+        try:
+            lo, hi = S.shard_range(n, rank, world)
+            op = nld.AnovaOperator(torch.from_numpy(feats[lo:hi]).cuda(), wins,
+                                   synth.SIGMA, **PIN)
+            S.attach(op, comm, rank, n)
+            op.degree()
+            y = op.apply_device(torch.from_numpy(V[lo:hi].copy()).cuda(), _lib.APPLY_SYSTEM,
+                                16, coef, pixel_major=True)
+            out[rank] = y.cpu().numpy()
+        except Exception as exc:  # pragma: no cover - reported below
+            errs.append(exc)
+            comm.barrier.abort()
+
+    threads = [threading.Thread(target=rank_main, args=(r,)) for r in range(world)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join(timeout=600)
+    assert not errs, errs
+    got = np.concatenate([out[0], out[1]])
+    assert rel(got, want) < 1e-12
