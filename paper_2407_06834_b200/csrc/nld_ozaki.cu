@@ -58,7 +58,11 @@ constexpr int kThreads = 256;
 constexpr int kTmemCols = 512;         // kSl * 64 = 384 used
 constexpr int kABytes = kRows * kChunk;          // 4 KB per slice
 constexpr int kBBytes = 64 * kChunk;             // 2 KB per slice
-constexpr int kStageBytes = kSl * (kABytes + kBBytes);
+// X digits (the M = 128 operand) live in TMEM: per operand stage 6 slices x 8
+// columns after the 384 accumulator columns; shared memory holds only the Y
+// digits (and raw rows), halving the operand traffic through shared memory
+constexpr int kStageBytes = kSl * kBBytes;
+constexpr int kXTmem0 = kSl * 64;                // first X column (after the accumulator)
 constexpr int kExpPerSub = 24;         // eA[8] eB[8] eC[8]
 constexpr double kMagic = 4503599627370496.0 + 141289400074368.0;  // 2^52 + 0x808080808080
 
@@ -191,9 +195,15 @@ __device__ __forceinline__ void cp_wait() {
 constexpr int kRawRows = kChunk * 24 * 8;       // 6 KB of weight rows per chunk
 constexpr int kRawV = kChunk * 16 * 8;          // 4 KB of v lines per chunk
 constexpr int kRawBytes = kRawRows + kRawV;
-constexpr int kRawStages = 8;         // raw chunks in flight
+#ifndef NLD_SP_RAWSTAGES
+#define NLD_SP_RAWSTAGES 8
+#endif
+constexpr int kRawStages = NLD_SP_RAWSTAGES;   // raw chunks in flight
 
-constexpr int kOpStages = 3;           // operand stages (slicers <-> tensor core)
+#ifndef NLD_SP_OPSTAGES
+#define NLD_SP_OPSTAGES 2                    // 384 + 2 x 48 TMEM columns <= 512
+#endif
+constexpr int kOpStages = NLD_SP_OPSTAGES;   // operand stages (slicers <-> tensor core)
 
 __host__ __device__ constexpr int spread_oz_smem() {
   return kOpStages * kStageBytes + kRawStages * kRawBytes;
@@ -346,19 +356,20 @@ k_spread_oz(const SubDev* __restrict__ subs, const WinDev* __restrict__ wins,
         OZW(17, umma::mbar_wait(&op_ready[st], (g / kOpStages) & 1));
         umma::fence_after();
         if (lane == 0) {
-          const uint32_t aB = umma::smem_u32(smem + st * kStageBytes);
-          const uint32_t bB = aB + kSl * kABytes;
+          const uint32_t bB = umma::smem_u32(smem + st * kStageBytes);
+          const uint32_t xa = tmem + (uint32_t)(kXTmem0 + st * kSl * 8);
+#ifndef NLD_EXP_SNOMMA
 #pragma unroll
           for (int p = 0; p < kSl; ++p) {
-            const uint64_t da = umma::make_sdesc(aB + p * kABytes, 128, 256);
 #pragma unroll
             for (int q0 = 0; q0 < kSl - p; q0 += 4) {
               const int nq = min(4, kSl - p - q0);
               const uint64_t db = umma::make_sdesc(bB + q0 * kBBytes, 128, 256);
-              umma::mma_i8(tmem + (uint32_t)((p + q0) * 64), da, db,
-                           umma::idesc_i8(kRows, nq * 64), (c > 0 || p > 0) ? 1u : 0u);
+              umma::mma_i8_ta(tmem + (uint32_t)((p + q0) * 64), xa + (uint32_t)(p * 8), db,
+                              umma::idesc_i8(kRows, nq * 64), (c > 0 || p > 0) ? 1u : 0u);
             }
           }
+#endif
           umma::commit(&op_free[st]);
           if (c == nchunk - 1) umma::commit(&acc_full);
         }
@@ -385,8 +396,7 @@ k_spread_oz(const SubDev* __restrict__ subs, const WinDev* __restrict__ wins,
         OZW(19, umma::mbar_wait(&raw_full[s], (g / kRawStages) & 1));
 #endif
         if (g >= kOpStages) OZW(20, umma::mbar_wait(&op_free[st], ((g / kOpStages) - 1) & 1));
-        uint8_t* sA = smem + st * kStageBytes;
-        uint8_t* sB = sA + kSl * kABytes;
+        uint8_t* sB = smem + st * kStageBytes;
         const double* R = reinterpret_cast<const double*>(raw + s * kRawBytes);
         const double* Vr = R + kChunk * 24;
         const int cn = min(kChunk, sd.count - c * kChunk);
@@ -407,7 +417,16 @@ k_spread_oz(const SubDev* __restrict__ subs, const WinDev* __restrict__ wins,
               }
               slice1(x, y, lo[i], hi[i]);
             }
-            store16(lo, hi, sA + canon32(m, h * 16), kABytes);
+            // row m = TMEM lane m (warp w holds lanes 32 (w % 4)..): 16 nodes =
+            // 4 columns per digit slice
+            uint32_t w4[4][6];
+#pragma unroll
+            for (int g4 = 0; g4 < 4; ++g4) pack4(lo + 4 * g4, hi + 4 * g4, w4[g4]);
+            const uint32_t xt = tmem + ((uint32_t)((m >> 5) * 32) << 16) +
+                                (uint32_t)(kXTmem0 + st * kSl * 8 + h * 4);
+#pragma unroll
+            for (int p = 0; p < kSl; ++p)
+              umma::tmem_st4(xt + (uint32_t)(p * 8), w4[0][p], w4[1][p], w4[2][p], w4[3][p]);
           }
           {
             const int n = tid & 63, gq = tid >> 6;
@@ -429,6 +448,8 @@ k_spread_oz(const SubDev* __restrict__ subs, const WinDev* __restrict__ wins,
         };
         if (cn == kChunk) slice_chunk(std::true_type{});
         else slice_chunk(std::false_type{});
+        umma::tmem_wait_st();
+        umma::fence_before();
         umma::fence_async_smem();
         __syncwarp();
         if (lane == 0) {
@@ -439,6 +460,7 @@ k_spread_oz(const SubDev* __restrict__ subs, const WinDev* __restrict__ wins,
       // epilogue: accumulators of this rhs group -> block
       OZW(21, umma::mbar_wait(&acc_full, grp & 1));
       umma::fence_after();
+#ifndef NLD_EXP_SNOEPI
       {
         const int lg = warp & 3, half = warp >> 2;
         const int m = lg * 32 + lane;
@@ -462,6 +484,7 @@ k_spread_oz(const SubDev* __restrict__ subs, const WinDev* __restrict__ wins,
           }
         }
       }
+#endif
       umma::fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&acc_empty);

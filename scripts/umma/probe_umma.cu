@@ -181,3 +181,75 @@ extern "C" int slice_check(const double* x, const double* y, int n, uint32_t* ou
   cudaFree(dx); cudaFree(dy); cudaFree(dout);
   return e != cudaSuccess;
 }
+
+// ---- A operand from TMEM (written with tcgen05.st) ----
+__global__ void k_check_tmemA(const int8_t* A, const int8_t* B, int N, int32_t* D) {
+  // M = 128, K = 32: A row m in TMEM lane m, 8 columns of 4 int8 (k = 4 c + byte)
+  extern __shared__ __align__(16) uint8_t sm[];
+  __shared__ uint64_t mbar;
+  __shared__ uint32_t taddr;
+  const int K = 32;
+  for (int e = threadIdx.x; e < N * K; e += blockDim.x)
+    sm[((e / K) >> 3) * 256 + ((e % K) >> 4) * 128 + ((e / K) & 7) * 16 + ((e % K) & 15)] =
+        (uint8_t)B[e];
+  fence_async_smem();
+  if (threadIdx.x < 32) tmem_alloc<512>(&taddr);
+  if (threadIdx.x == 32) { mbar_init(&mbar, 1); mbar_fence_init(); }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t t = taddr;
+  // D at columns [0, N), A at columns [256, 264)
+  {
+    const int row = threadIdx.x;   // 128 threads = 4 warps = 128 lanes
+    uint32_t w[8];
+    for (int c = 0; c < 8; ++c) {
+      uint32_t v = 0;
+      for (int b = 0; b < 4; ++b) v |= (uint32_t)(uint8_t)A[row * K + 4 * c + b] << (8 * b);
+      w[c] = v;
+    }
+    const uint32_t ta = t + ((uint32_t)((threadIdx.x >> 5) * 32) << 16) + 256;
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};\n" ::"r"(ta),
+                 "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]),
+                 "r"(w[7]));
+    asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  if (threadIdx.x == 0) {
+    const uint32_t idesc = idesc_i8(128, N);
+    const uint64_t db = make_sdesc(smem_u32(sm), 128, 256);
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(t),
+        "r"(t + 256), "l"(db), "r"(idesc), "r"(0));
+    commit(&mbar);
+  }
+  mbar_wait(&mbar, 0);
+  fence_after();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int c0 = 0; c0 < N; c0 += 16) {
+    uint32_t r[16];
+    tmem_ld16(t + ((uint32_t)(warp * 32) << 16) + c0, r);
+    tmem_wait_ld();
+    for (int j = 0; j < 16; ++j) D[(warp * 32 + lane) * N + c0 + j] = (int32_t)r[j];
+  }
+  fence_before();
+  __syncthreads();
+  if (threadIdx.x < 32) tmem_free<512>(t);
+}
+
+extern "C" int umma_check_tmemA(const int8_t* A, const int8_t* B, int N, int32_t* D) {
+  int8_t *dA, *dB;
+  int32_t* dD;
+  cudaMalloc(&dA, 128 * 32); cudaMalloc(&dB, N * 32); cudaMalloc(&dD, 128 * N * 4);
+  cudaMemcpy(dA, A, 128 * 32, cudaMemcpyHostToDevice);
+  cudaMemcpy(dB, B, N * 32, cudaMemcpyHostToDevice);
+  k_check_tmemA<<<1, 128, N * 32>>>(dA, dB, N, dD);
+  cudaError_t e = cudaDeviceSynchronize();
+  cudaMemcpy(D, dD, 128 * N * 4, cudaMemcpyDeviceToHost);
+  cudaFree(dA); cudaFree(dB); cudaFree(dD);
+  if (e != cudaSuccess) { printf("err %s\n", cudaGetErrorString(e)); return 1; }
+  return 0;
+}

@@ -48,3 +48,13 @@ if mode == "slice":
                 if bad < 5:
                     print("bad", g, e, val, ref, d[g, :, e].tolist())
     print("slice rc", rc, "bad", bad, "of", n)
+
+if mode == "tmemA":
+    for N in (64, 256):
+        A = rng.integers(-128, 128, size=(128, 32), dtype=np.int8)
+        B = rng.integers(-128, 128, size=(N, 32), dtype=np.int8)
+        ref = A.astype(np.int64) @ B.astype(np.int64).T
+        D = np.zeros((128, N), dtype=np.int32)
+        rc = lib.umma_check_tmemA(A.ctypes.data_as(P), B.ctypes.data_as(P), N, D.ctypes.data_as(P))
+        print("tmemA N", N, "rc", rc, "ok", np.array_equal(D.astype(np.int64), ref),
+              "maxdiff", np.abs(D - ref).max())
