@@ -519,15 +519,20 @@ constexpr int kGTile = 32;                       // nodes per tile
 constexpr int kGA = kRows * 64;                  // 8 KB per G digit slice (K = 64)
 constexpr int kGB = kGTile * 64;                 // 2 KB per Y digit slice
 constexpr int kGBStage = kSl * kGB;              // 12 KB
-// Two CTAs per SM (default; NLD_GATHER_CTAS=1 builds the one-CTA variant with a
-// double-buffered TMEM accumulator and 8 epilogue warps): each CTA has a single
-// 192-column accumulator, 4 epilogue warps and shallower stages, so one CTA's
-// per-subproblem G setup and drain overlap the other's tiles
+// One CTA per SM (default): double-buffered 192-column TMEM accumulator, the G
+// digits in TMEM as the A operand, 8 epilogue warps.  NLD_GATHER_CTAS=2 builds
+// the two-CTA variant (single accumulator and G digits in shared memory per CTA,
+// 4 epilogue warps) whose G setup / drain overlap the other CTA's tiles -- within
+// 1% of the default on B200.
 #ifndef NLD_GATHER_CTAS
-#define NLD_GATHER_CTAS 2
+#define NLD_GATHER_CTAS 1
 #endif
 constexpr int kGCtas = NLD_GATHER_CTAS;
 constexpr int kGAccBufs = kGCtas == 2 ? 1 : 2;
+// one CTA per SM: the subproblem's G digits live in TMEM (96 columns after the
+// two 192-column accumulators) and feed the UMMAs as the TMEM A operand
+constexpr bool kGTmemA = kGCtas == 1;
+constexpr int kGTmemA0 = 2 * kSl * kGTile;      // 384
 constexpr int kGTmemCols = kGCtas == 2 ? 256 : 512;
 constexpr int kGOpStages = kGCtas == 2 ? 2 : 3;
 constexpr int kGRowS = 26;                       // smem row stride (doubles): conflict-free
@@ -568,7 +573,7 @@ __device__ __forceinline__ double i2d(uint32_t x) {
 }
 
 __host__ __device__ constexpr int gather_oz_smem() {
-  return kSl * kGA + kGOpStages * kGBStage + kGRawStages * kGRaw;
+  return (kGTmemA ? 0 : kSl * kGA) + kGOpStages * kGBStage + kGRawStages * kGRaw;
 }
 
 // canonical K-major no-swizzle offset in a (rows x 64 bytes) tile
@@ -598,7 +603,7 @@ k_gather_oz(const SubDev* __restrict__ subs, const CellDev* __restrict__ cells,
   const int32_t* __restrict__ pw = pix + sd.start;
   const int16_t* ex = sub_exp + (int64_t)blockIdx.x * kExpPerSub;
   uint8_t* const sGA = smem;
-  uint8_t* const sGB = sGA + kSl * kGA;
+  uint8_t* const sGB = sGA + (kGTmemA ? 0 : kSl * kGA);
   uint8_t* const sRaw = sGB + kGOpStages * kGBStage;
   const int ntile = (sd.count + kGTile - 1) / kGTile;
   const int ngroups = nrhs / 16;
@@ -665,9 +670,23 @@ k_gather_oz(const SubDev* __restrict__ subs, const CellDev* __restrict__ cells,
         uint32_t lo[16], hi[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) slice1(gval(h * 32 + kb * 16 + i), sg, lo[i], hi[i]);
-      store16(lo, hi, sGA + canon64(m, h * 32 + kb * 16), kGA);
+        if constexpr (kGTmemA) {
+          uint32_t w4[4][6];
+#pragma unroll
+          for (int g4 = 0; g4 < 4; ++g4) pack4(lo + 4 * g4, hi + 4 * g4, w4[g4]);
+          // lane m, 16 columns per digit slice (K = 64 bytes); this thread's
+          // 16 values are columns h * 8 + kb * 4 .. + 3
+          const uint32_t gt_addr = tmem + ((uint32_t)((m >> 5) * 32) << 16) +
+                                   (uint32_t)(kGTmemA0 + h * 8 + kb * 4);
+#pragma unroll
+          for (int p = 0; p < kSl; ++p)
+            umma::tmem_st4(gt_addr + (uint32_t)(p * 16), w4[0][p], w4[1][p], w4[2][p], w4[3][p]);
+        } else {
+          store16(lo, hi, sGA + canon64(m, h * 32 + kb * 16), kGA);
+        }
       }
     }
+    if constexpr (kGTmemA) umma::tmem_wait_st();
     umma::fence_async_smem();
     umma::fence_before();
     __syncthreads();
@@ -707,10 +726,18 @@ k_gather_oz(const SubDev* __restrict__ subs, const CellDev* __restrict__ cells,
           for (int ks = 0; ks < 2; ++ks)
 #pragma unroll
             for (int p = 0; p < kSl; ++p) {
-              const uint64_t da = umma::make_sdesc(aB + p * kGA + ks * 256, 128, 512);
               const uint64_t db = umma::make_sdesc(bB + ks * 256, 128, 512);
-              umma::mma_i8(dcol + (uint32_t)(p * kGTile), da, db,
-                           umma::idesc_i8(kRows, (kSl - p) * kGTile), (ks > 0 || p > 0) ? 1u : 0u);
+              if constexpr (kGTmemA) {
+                umma::mma_i8_ta(dcol + (uint32_t)(p * kGTile),
+                                tmem + (uint32_t)(kGTmemA0 + p * 16 + ks * 8), db,
+                                umma::idesc_i8(kRows, (kSl - p) * kGTile),
+                                (ks > 0 || p > 0) ? 1u : 0u);
+              } else {
+                const uint64_t da = umma::make_sdesc(aB + p * kGA + ks * 256, 128, 512);
+                umma::mma_i8(dcol + (uint32_t)(p * kGTile), da, db,
+                             umma::idesc_i8(kRows, (kSl - p) * kGTile),
+                             (ks > 0 || p > 0) ? 1u : 0u);
+              }
             }
 #endif
           umma::commit(&op_free[st]);

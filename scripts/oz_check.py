@@ -8,8 +8,8 @@ import numpy as np
 
 if sys.argv[1] == "cmp":
     a, b = np.load(sys.argv[2]), np.load(sys.argv[3])
-    for k in range(a.shape[0]):
-        print("kind", k, "rel L2", float(np.linalg.norm(a[k] - b[k]) / np.linalg.norm(b[k])))
+    print("rel L2 per kind:", [float(np.linalg.norm(a[k] - b[k]) / np.linalg.norm(b[k]))
+                               for k in range(a.shape[0])])
     sys.exit(0)
 import torch  # noqa: E402
 sys.path.insert(0, ".")
