@@ -65,7 +65,7 @@ __global__ void k_check(const int8_t* A, const int8_t* B, int M, int N, int K, i
 }
 
 template <int NCOLS>
-__global__ void k_rate(int M, int N, int K, int iters, int32_t* sink) {
+__global__ void k_rate(int M, int N, int K, int iters, int32_t* sink, int nacc) {
   extern __shared__ __align__(1024) uint8_t sm[];
   __shared__ uint64_t mbar;
   __shared__ uint32_t taddr;
@@ -84,7 +84,7 @@ __global__ void k_rate(int M, int N, int K, int iters, int32_t* sink) {
       for (int kc = 0; kc < K / 32; ++kc) {
         const uint64_t da = make_sdesc(smem_u32(sm) + kc * 256, 128, sboA);
         const uint64_t db = make_sdesc(smem_u32(sm + M * K) + kc * 256, 128, sboA);
-        mma_i8(t + (it & 1) * N, da, db, idesc, 1);
+        mma_i8(t + (it % nacc) * N, da, db, idesc, 1);
       }
     commit(&mbar);
   }
@@ -120,17 +120,17 @@ extern "C" int umma_check(const int8_t* A, const int8_t* B, int M, int N, int K,
   return 0;
 }
 
-extern "C" int umma_rate(int M, int N, int K, int iters, int blocks, double* tops) {
+extern "C" int umma_rate(int M, int N, int K, int iters, int blocks, double* tops, int nacc) {
   int32_t* sink;
   cudaMalloc(&sink, 4);
   const int smem = (M + N) * K;
   cudaFuncSetAttribute(k_rate<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  k_rate<512><<<blocks, 128, smem>>>(M, N, K, 2, sink);
+  k_rate<512><<<blocks, 128, smem>>>(M, N, K, 2, sink, nacc);
   cudaDeviceSynchronize();
   cudaEvent_t a, b;
   cudaEventCreate(&a); cudaEventCreate(&b);
   cudaEventRecord(a);
-  k_rate<512><<<blocks, 128, smem>>>(M, N, K, iters, sink);
+  k_rate<512><<<blocks, 128, smem>>>(M, N, K, iters, sink, nacc);
   cudaEventRecord(b);
   cudaError_t e = cudaEventSynchronize(b);
   float ms; cudaEventElapsedTime(&ms, a, b);

@@ -26,10 +26,12 @@ if mode == "check":
         print("D[:4,:8]", D[:4, :8].tolist())
         print("ref[:4,:8]", ref[:4, :8].tolist())
 elif mode == "rate":
-    M, N, K, blocks = map(int, sys.argv[2:6])
+    M, N, K, blocks, nacc = map(int, sys.argv[2:7])
     t = ctypes.c_double()
-    rc = lib.umma_rate(M, N, K, 4000, blocks, ctypes.byref(t))
-    print(f"rate M={M} N={N} K={K} blocks={blocks} rc={rc} {t.value:.1f} TOPS", flush=True)
+    rc = lib.umma_rate(M, N, K, 4000, blocks, ctypes.byref(t), nacc)
+    per = 2 * M * N * K / (t.value * 1e12 / blocks / 1.965e9) if t.value else 0
+    print(f"rate M={M} N={N} K={K} blocks={blocks} nacc={nacc} rc={rc} {t.value:.1f} TOPS "
+          f"~{per:.0f} clk per instr", flush=True)
 
 if mode == "slice":
     n = 4096

@@ -531,3 +531,23 @@ def test_sharded_sliced_path_matches_single_gpu():
     assert not errs, errs
     got = np.concatenate([out[0], out[1]])
     assert rel(got, want) < 1e-12
+
+
+@pytest.mark.parametrize("nrhs", [32, 48])
+def test_sliced_multiple_rhs_groups(nrhs):
+    """nrhs = 16k runs k rhs groups through the same sliced kernels (G digits,
+    row scales and accumulators per group): every column equals its own
+    single-rhs fp64 product, for each product kind."""
+    from paper_2407_06834_b200 import _lib
+    op = operator("c1")[0]
+    rng = np.random.default_rng(nrhs)
+    V = rng.standard_normal((op.n, nrhs)) * rng.uniform(0.1, 10.0, nrhs)
+    coef = np.stack([rng.uniform(0.5, 2, nrhs), rng.uniform(0, 0.01, nrhs)], 1).ravel()
+    Vd = torch.from_numpy(V).cuda()
+    for kind in (_lib.APPLY_GAMMA, _lib.APPLY_SYSTEM):
+        c = coef if kind == _lib.APPLY_SYSTEM else None
+        got = op.apply_device(Vd, kind, nrhs, c, pixel_major=True).cpu().numpy()
+        for k in (0, 17, nrhs - 1):
+            ck = None if c is None else c[2 * k:2 * k + 2]
+            one = op.apply_device(torch.from_numpy(V[:, k].copy()).cuda(), kind, 1, ck)
+            assert rel(got[:, k], one.cpu().numpy()) < 1e-12, (kind, k)
