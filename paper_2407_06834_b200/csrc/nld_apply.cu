@@ -1158,7 +1158,7 @@ void gather_window_fast(const PlanSet& ps, const Workspace& ws, int w, int64_t N
   if (wp.d == 1) launch_gather<1, MC>(subs, nsub, ps, ws, N, nrhs, st);
   else if (wp.d == 2) launch_gather<2, MC>(subs, nsub, ps, ws, N, nrhs, st);
   else if (MC == 4 && use_ozaki() && nrhs % 16 == 0 && ps.sub_exp && !getenv("NLD_OZAKI_NO_GATHER"))
-    launch_gather_oz(ps, subs, ps.sub_exp + wp.sub_off * 24, nsub, ws.grid_out, ps.grid_total,
+    launch_gather_oz(ps, subs, ps.sub_exp + wp.sub_off * 24, ps.sub_order + wp.sub_off, nsub, ws.grid_out, ps.grid_total,
                      ep.mode == mma::kGatherStore ? ws.wout + (int64_t)w * N * nrhs : out, N, nrhs,
                      ep, st);
   else if (MC == 4 && use_mma()) launch_gather_mma(subs, nsub, ps, ws, N, nrhs, st, ep, out);
@@ -1178,7 +1178,7 @@ void gather_window_fast(const PlanSet& ps, const Workspace& ws, int w, int64_t N
     NLD_CUDA(cudaStreamSynchronize(st));
     NLD_CUDA(cudaMemcpy(ta, out, nn * 8, cudaMemcpyDeviceToDevice));
     NLD_CUDA(cudaMemcpy(tb, out, nn * 8, cudaMemcpyDeviceToDevice));
-    launch_gather_oz(ps, subs, ps.sub_exp + wp.sub_off * 24, nsub, ws.grid_out, ps.grid_total, ta,
+    launch_gather_oz(ps, subs, ps.sub_exp + wp.sub_off * 24, ps.sub_order + wp.sub_off, nsub, ws.grid_out, ps.grid_total, ta,
                      N, nrhs, ep, st);
     launch_gather_mma(subs, nsub, ps, ws, N, nrhs, st, ep, tb);
     NLD_CUDA(cudaStreamSynchronize(st));
@@ -1207,7 +1207,7 @@ void gather_window_fast(const PlanSet& ps, const Workspace& ws, int w, int64_t N
     mma::GatherEpi sto{mma::kGatherStore, 0, 0, nullptr, nullptr, nullptr};
     double* wo = ws.wout + (int64_t)w * N * nrhs;
     NLD_CUDA(cudaMemsetAsync(wo, 0, nn * 8, st));
-    launch_gather_oz(ps, subs, ps.sub_exp + wp.sub_off * 24, nsub, ws.grid_out, ps.grid_total, wo,
+    launch_gather_oz(ps, subs, ps.sub_exp + wp.sub_off * 24, ps.sub_order + wp.sub_off, nsub, ws.grid_out, ps.grid_total, wo,
                      N, nrhs, sto, st);
     NLD_CUDA(cudaStreamSynchronize(st));
     NLD_CUDA(cudaMemcpy(h1.data(), wo, nn * 8, cudaMemcpyDeviceToHost));

@@ -132,6 +132,7 @@ struct PlanSet {
   int64_t grid_total = 0;        // sum of box sizes
   int64_t generic_nodes = 0;     // nodes in windows on the generic path
   int16_t* sub_exp = nullptr;    // sliced spread: per 3-D subproblem eA/eB/eC
+  int32_t* sub_order = nullptr;  // per window: its 3-D subproblems by descending size
   int shares_tables_with = -1;   // index of the plan set whose tables we use
   bool owns_tables = true;
 };
@@ -205,9 +206,10 @@ void launch_spread_oz(const PlanSet& ps, const SubDev* subs, const int16_t* ex, 
 void ozaki_vmax(const double* vt, int64_t n, int nrhs, unsigned long long* out, cudaStream_t st);
 void ozaki_prof_dump(const char* what, cudaStream_t st);
 namespace mma { struct GatherEpi; }
-void launch_gather_oz(const PlanSet& ps, const SubDev* subs, const int16_t* ex, unsigned nsub,
-                      const double* grid, int64_t grid_ld, double* out, int64_t N, int nrhs,
-                      const mma::GatherEpi& ep, cudaStream_t st);
+void launch_gather_oz(const PlanSet& ps, const SubDev* subs, const int16_t* ex,
+                      const int32_t* order, unsigned nsub, const double* grid, int64_t grid_ld,
+                      double* out, int64_t N, int nrhs, const mma::GatherEpi& ep,
+                      cudaStream_t st);
 void free_planset(PlanSet& ps);
 void ensure_workspace(nld_operator* op, const PlanSet& ps, int nrhs);
 void free_workspace(Workspace& ws);

@@ -21,6 +21,7 @@
 // rounds x'y' to an integer and leaves x'y' + 0x80..80 in the low 48
 // mantissa bits, whose bytes XOR 0x80 are the balanced digits.
 #include <algorithm>
+#include <vector>
 #include <type_traits>
 #include <cmath>
 #include <cstdint>
@@ -883,6 +884,312 @@ k_gather_oz(const SubDev* __restrict__ subs, const CellDev* __restrict__ cells,
   if (warp == 0) umma::tmem_free<kGTmemCols>(tmem);
 }
 
+// ---- persistent gather -----------------------------------------------------
+// One CTA per SM walks a list of work items (subproblem, rhs group): the
+// subproblems in descending node count, dealt to the CTAs in snake order so
+// every CTA gets a near-equal share.  All warp roles stream across item
+// boundaries; the G digits are double-buffered in shared memory, so the
+// slicer warps cut item k+1's G while the issuer and the epilogue finish item
+// k -- no per-subproblem launch, TMEM allocation, pipeline fill or drain (the
+// fixed cost that grows when pixel sharding makes subproblems small).
+//   warps 0-7  epilogue       warps 8-11 slicers (G digits + Y digits)
+//   warp 12    UMMA issuer    warp 13    loader
+constexpr int kPEpi = 8;
+constexpr int kPSl0 = 8;
+constexpr int kPSlicers = 4;
+constexpr int kPIssuer = 12;
+constexpr int kPLoader = 13;
+constexpr int kPThreads = 32 * 14;
+
+__host__ __device__ constexpr int gather_ozp_smem() {
+  return 2 * kSl * kGA + 3 * kGBStage + 6 * kGRaw;
+}
+
+__global__ void __launch_bounds__(kPThreads, 1)
+k_gather_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order, int nsub,
+             const CellDev* __restrict__ cells, const WinDev* __restrict__ wins,
+             const double* __restrict__ rows, const int32_t* __restrict__ pix,
+             const int16_t* __restrict__ sub_exp, const double* __restrict__ grid,
+             int64_t grid_ld, double* __restrict__ out, int64_t N, int nrhs, mma::GatherEpi ep) {
+  constexpr int RS = 6, OS = 3;                    // raw / operand stages
+  extern __shared__ __align__(16) uint8_t smem[];
+  __shared__ uint64_t raw_full[RS], raw_empty[RS], op_ready[OS], op_free[OS];
+  __shared__ uint64_t acc_full[2], acc_empty[2], g_full[2], g_empty[2];
+  __shared__ uint32_t taddr_s;
+  __shared__ double tsc[2][kRows];
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  uint8_t* const sGA = smem;                                    // [2][6][128 x 64]
+  uint8_t* const sGB = sGA + 2 * kSl * kGA;                     // [3][6][32 x 64]
+  uint8_t* const sRaw = sGB + OS * kGBStage;                    // [6][rows | pix]
+  const int ngroups = nrhs / 16;
+  const int G = (int)gridDim.x, b = (int)blockIdx.x;
+  const int rounds = nsub / G, rem = nsub % G;
+  const int my_rounds = rounds + ((rem > 0 && ((rounds & 1) ? (G - 1 - b) : b) < rem) ? 1 : 0);
+  const int nitems = my_rounds * ngroups;
+  auto item_sub = [&](int k) {
+    const int i = k / ngroups;
+    return order[i * G + ((i & 1) ? (G - 1 - b) : b)];
+  };
+
+  if (warp == 0) umma::tmem_alloc<512>(&taddr_s);
+  if (tid == 32) {
+    for (int k = 0; k < RS; ++k) {
+      umma::mbar_init(&raw_full[k], 32);
+      umma::mbar_init(&raw_empty[k], kPSlicers + kPEpi);
+    }
+    for (int k = 0; k < OS; ++k) {
+      umma::mbar_init(&op_ready[k], kPSlicers);
+      umma::mbar_init(&op_free[k], 1);
+    }
+    for (int k = 0; k < 2; ++k) {
+      umma::mbar_init(&acc_full[k], 1);
+      umma::mbar_init(&acc_empty[k], kPEpi);
+      umma::mbar_init(&g_full[k], kPSlicers);
+      umma::mbar_init(&g_empty[k], 1 + kPEpi);     // last MMA commit + epilogue warps
+    }
+    umma::mbar_fence_init();
+  }
+  umma::fence_before();
+  __syncthreads();
+  umma::fence_after();
+  const uint32_t tmem = taddr_s;
+
+  if (warp == kPLoader) {
+    // ---------------------------------------------------------------- loader
+    int gt = 0;
+    for (int k = 0; k < nitems; ++k) {
+      const SubDev sd = subs[item_sub(k)];
+      const WinDev wd = wins[sd.win];
+      const double* rw = rows + wd.row_off + (sd.start - wd.node_off) * 24;
+      const int32_t* pw = pix + sd.start;
+      const int ntile = (sd.count + kGTile - 1) / kGTile;
+      for (int tl = 0; tl < ntile; ++tl, ++gt) {
+        const int s = gt % RS;
+        if (gt >= RS) umma::mbar_wait(&raw_empty[s], ((gt / RS) - 1) & 1);
+        const int j0 = tl * kGTile, cn = min(kGTile, sd.count - j0);
+        const double* src = rw + (int64_t)j0 * 24;
+        uint8_t* dst = sRaw + s * kGRaw;
+        for (int e = lane; e < cn * 12; e += 32) {
+          const int node = e / 12, gi = e - node * 12;
+          cp_async16(dst + node * kGRowS * 8 + 16 * gi, src + 2 * e);
+        }
+        if (lane < cn) cp_async4(dst + kGTile * kGRowS * 8 + 4 * lane, pw + j0 + lane);
+        cp_async_mbar_arrive(&raw_full[s]);
+      }
+    }
+  } else if (warp == kPIssuer) {
+    // ---------------------------------------------------------------- issuer
+    int gt = 0;
+    for (int k = 0; k < nitems; ++k) {
+      const int gs = k & 1;
+      const SubDev sd = subs[item_sub(k)];
+      const int ntile = (sd.count + kGTile - 1) / kGTile;
+      umma::mbar_wait(&g_full[gs], (k >> 1) & 1);
+      for (int tl = 0; tl < ntile; ++tl, ++gt) {
+        const int st = gt % OS, ab = gt & 1;
+        if (gt >= 2) umma::mbar_wait(&acc_empty[ab], ((gt >> 1) - 1) & 1);
+        umma::mbar_wait(&op_ready[st], (gt / OS) & 1);
+        umma::fence_after();
+        if (lane == 0) {
+          const uint32_t aB = umma::smem_u32(sGA + gs * kSl * kGA);
+          const uint32_t bB = umma::smem_u32(sGB + st * kGBStage);
+          const uint32_t dcol = tmem + (uint32_t)(ab * kSl * kGTile);
+#pragma unroll
+          for (int ks = 0; ks < 2; ++ks)
+#pragma unroll
+            for (int p = 0; p < kSl; ++p) {
+              const uint64_t da = umma::make_sdesc(aB + p * kGA + ks * 256, 128, 512);
+              const uint64_t db = umma::make_sdesc(bB + ks * 256, 128, 512);
+              umma::mma_i8(dcol + (uint32_t)(p * kGTile), da, db,
+                           umma::idesc_i8(kRows, (kSl - p) * kGTile), (ks > 0 || p > 0) ? 1u : 0u);
+            }
+          umma::commit(&op_free[st]);
+          umma::commit(&acc_full[ab]);
+          if (tl == ntile - 1) umma::commit(&g_empty[gs]);   // item k's G digits released
+        }
+        __syncwarp();
+      }
+    }
+  } else if (warp >= kPSl0) {
+    // ------------------------------------------- slicers: G digits, Y digits
+    const int t = tid - 32 * kPSl0;            // 0..127
+    int gt = 0;
+    for (int k = 0; k < nitems; ++k) {
+      const int gs = k & 1;
+      const int si = item_sub(k);
+      const SubDev sd = subs[si];
+      const CellDev cd = cells[sd.cell];
+      const WinDev wd = wins[sd.win];
+      const int16_t* ex = sub_exp + (int64_t)si * kExpPerSub;
+      const int rg = (k % ngroups) * 16;
+      const int ntile = (sd.count + kGTile - 1) / kGTile;
+      int eBm = -2000, eCm = -2000;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        eBm = max(eBm, (int)ex[8 + q]);
+        eCm = max(eCm, (int)ex[16 + q]);
+      }
+      const double syB = pow2(46 - eBm), syC = pow2(-eCm);
+      if (k >= 2) umma::mbar_wait(&g_empty[gs], ((k >> 1) - 1) & 1);
+      {
+        // G digits: row m = (r, a) = t, its 64 (b, c) from the support box
+        const int m = t, ga = m & 7, gr = m >> 3;
+        auto gval = [&](int bc) -> double {
+          int p0 = cd.cc[0] + ga, p1 = cd.cc[1] + (bc >> 3), p2 = cd.cc[2] + (bc & 7);
+          if (p0 >= wd.box_w[0]) p0 -= wd.box_w[0];
+          if (p1 >= wd.box_w[1]) p1 -= wd.box_w[1];
+          if (p2 >= wd.box_w[2]) p2 -= wd.box_w[2];
+          return grid[(int64_t)(rg + gr) * grid_ld + wd.grid_off +
+                      ((int64_t)p0 * wd.box_w[1] + p1) * wd.box_w[2] + p2];
+        };
+        double mx = 0.0;
+#pragma unroll 16
+        for (int i = 0; i < 64; ++i) mx = fmax(mx, fabs(gval(i)));
+        const int eG = max(-900, exp_bound(mx));
+        const double sg = pow2(46 - eG);
+        tsc[gs][m] = ldexp(1.0, eG + eBm + eCm - 28);
+        uint8_t* dA = sGA + gs * kSl * kGA;
+#pragma unroll 1
+        for (int kb = 0; kb < 4; ++kb) {
+          uint32_t lo[16], hi[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) slice1(gval(kb * 16 + i), sg, lo[i], hi[i]);
+          store16(lo, hi, dA + canon64(m, kb * 16), kGA);
+        }
+        umma::fence_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&g_full[gs]);
+      }
+      // Y digits of each tile: node n = t >> 2 (8 per warp), bc quarter kq
+      const int n = t >> 2, kq = t & 3;
+      for (int tl = 0; tl < ntile; ++tl, ++gt) {
+        const int s = gt % RS, st = gt % OS;
+        umma::mbar_wait(&raw_full[s], (gt / RS) & 1);
+        if (gt >= OS) umma::mbar_wait(&op_free[st], ((gt / OS) - 1) & 1);
+        const double* R = reinterpret_cast<const double*>(sRaw + s * kGRaw) + n * kGRowS;
+        const bool ok = tl * kGTile + n < sd.count;
+        uint32_t lo[16], hi[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const int bc = kq * 16 + i;
+          double x = 0.0, y = 0.0;
+          if (ok) {
+            x = R[8 + (bc >> 3)] * syB;
+            y = R[16 + (bc & 7)] * syC;
+          }
+          slice1(x, y, lo[i], hi[i]);
+        }
+        store16(lo, hi, sGB + st * kGBStage + canon64(n, kq * 16), kGB);
+        umma::fence_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(&op_ready[st]);
+          mbar_arrive(&raw_empty[s]);
+        }
+      }
+    }
+  } else {
+    // -------------------------------------------------------------- epilogue
+    const int lg = warp & 3, nh = warp >> 2;
+    const int a = lane & 7, r = 4 * lg + (lane >> 3);
+    const int mrow = lg * 32 + lane;
+    const uint32_t tl_lane = tmem + ((uint32_t)(lg * 32) << 16);
+    const bool need_eta = ep.kind == NLD_APPLY_SYSTEM || ep.kind == NLD_APPLY_LAPLACIAN;
+    int gt = 0;
+    for (int k = 0; k < nitems; ++k) {
+      const int gs = k & 1;
+      const SubDev sd = subs[item_sub(k)];
+      const int rg = (k % ngroups) * 16;
+      const int ntile = (sd.count + kGTile - 1) / kGTile;
+      umma::mbar_wait(&g_full[gs], (k >> 1) & 1);
+      const double ts = tsc[gs][mrow];
+      for (int tl = 0; tl < ntile; ++tl, ++gt) {
+        const int ab = gt & 1, s = gt % RS, j0 = tl * kGTile;
+        umma::mbar_wait(&raw_full[s], (gt / RS) & 1);
+        const double* R = reinterpret_cast<const double*>(sRaw + s * kGRaw);
+        const int32_t* sp = reinterpret_cast<const int32_t*>(sRaw + s * kGRaw + kGTile * kGRowS * 8);
+        int64_t oe[2];
+        double prev[2], vx[2], et[2];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int nn = nh * 16 + q * 8 + a;
+          const bool ok = j0 + nn < sd.count;
+          const int64_t px = ok ? (int64_t)sp[nn] : -1;
+          oe[q] = ok ? px * nrhs + rg + r : -1;
+          prev[q] = (ok && ep.mode >= mma::kGatherAccum) ? out[oe[q]] : 0.0;
+          vx[q] = (ok && ep.mode == mma::kGatherFinal) ? ep.v[oe[q]] : 0.0;
+          et[q] = (ok && ep.mode == mma::kGatherFinal && need_eta) ? ep.eta[px] : 0.0;
+        }
+        umma::mbar_wait(&acc_full[ab], (gt >> 1) & 1);
+        umma::fence_after();
+        double ysum[2];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int nb = nh * 16 + q * 8;
+          uint32_t dv[kSl][8];
+#pragma unroll
+          for (int tt = 0; tt < kSl; ++tt)
+            umma::tmem_ld8(tl_lane + (uint32_t)(ab * kSl * kGTile + tt * kGTile + nb), dv[tt]);
+          umma::tmem_wait_ld();
+          if (q == 1) {
+            umma::fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&acc_empty[ab]);
+          }
+          double v8[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            v8[i] = combine6(dv, i) * ts * R[(nb + i) * kGRowS + a];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const bool up = lane & 4;
+            const double send = up ? v8[i] : v8[i + 4];
+            const double keep = up ? v8[i + 4] : v8[i];
+            v8[i] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+          }
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            const bool up = lane & 2;
+            const double send = up ? v8[i] : v8[i + 2];
+            const double keep = up ? v8[i + 2] : v8[i];
+            v8[i] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+          }
+          {
+            const bool up = lane & 1;
+            const double send = up ? v8[0] : v8[1];
+            const double keep = up ? v8[1] : v8[0];
+            ysum[q] = keep + __shfl_xor_sync(0xffffffffu, send, 1);
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&raw_empty[s]);
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          if (oe[q] < 0) continue;
+          const double y = ysum[q];
+          double res;
+          if (ep.mode == mma::kGatherStore || ep.mode == mma::kGatherFirst) {
+            res = y;
+          } else if (ep.mode == mma::kGatherAccum) {
+            res = prev[q] + y;
+          } else {
+            const double lam = ep.coef ? ep.coef[2 * (rg + r)] : 0.0;
+            const double mu = ep.coef ? ep.coef[2 * (rg + r) + 1] : 0.0;
+            res = mma::epi_value(ep.kind, ep.L, prev[q] + y, vx[q], et[q], lam, mu);
+          }
+          out[oe[q]] = res;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&g_empty[gs]);   // tsc[gs] no longer read
+    }
+  }
+  umma::fence_before();
+  __syncthreads();
+  if (warp == 0) umma::tmem_free<512>(tmem);
+}
+
 }  // namespace oz
 
 // ---- host side ------------------------------------------------------------
@@ -904,6 +1211,25 @@ int16_t* ozaki_exponents(PlanSet& ps, cudaStream_t st) {
   oz::k_sub_exponents<<<(unsigned)ps.n_subs[3], 240, 0, st>>>(ps.subs[3], ps.wdev, ps.rows,
                                                                ps.sub_exp);
   NLD_CUDA(cudaGetLastError());
+  // per window, its 3-D subproblems in descending node count (window-local
+  // indices): the persistent gather deals them out in snake order
+  std::vector<SubDev> h(ps.n_subs[3]);
+  NLD_CUDA(cudaMemcpyAsync(h.data(), ps.subs[3], sizeof(SubDev) * h.size(), cudaMemcpyDeviceToHost,
+                           st));
+  NLD_CUDA(cudaStreamSynchronize(st));
+  std::vector<int32_t> ord(h.size());
+  for (const WinPlan& wp : ps.win) {
+    if (wp.d != 3 || wp.n_subs == 0) continue;
+    int32_t* o = ord.data() + wp.sub_off;
+    for (int64_t i = 0; i < wp.n_subs; ++i) o[i] = (int32_t)i;
+    const SubDev* hs = h.data() + wp.sub_off;
+    std::stable_sort(o, o + wp.n_subs,
+                     [&](int32_t x, int32_t y) { return hs[x].count > hs[y].count; });
+  }
+  NLD_CUDA(cudaMalloc(&ps.sub_order, sizeof(int32_t) * ord.size()));
+  NLD_CUDA(cudaMemcpyAsync(ps.sub_order, ord.data(), sizeof(int32_t) * ord.size(),
+                           cudaMemcpyHostToDevice, st));
+  NLD_CUDA(cudaStreamSynchronize(st));
   return ps.sub_exp;
 }
 
@@ -922,9 +1248,34 @@ void launch_spread_oz(const PlanSet& ps, const SubDev* subs, const int16_t* ex, 
   NLD_CUDA(cudaGetLastError());
 }
 
-void launch_gather_oz(const PlanSet& ps, const SubDev* subs, const int16_t* ex, unsigned nsub,
-                      const double* grid, int64_t grid_ld, double* out, int64_t N, int nrhs,
-                      const mma::GatherEpi& ep, cudaStream_t st) {
+void launch_gather_oz(const PlanSet& ps, const SubDev* subs, const int16_t* ex,
+                      const int32_t* order, unsigned nsub, const double* grid, int64_t grid_ld,
+                      double* out, int64_t N, int nrhs, const mma::GatherEpi& ep,
+                      cudaStream_t st) {
+  static int persist = -1;
+  if (persist < 0) {
+    const char* e = getenv("NLD_GATHER_PERSIST");
+    persist = (e && e[0] == '0') ? 0 : 1;
+  }
+  if (persist && order) {
+    const int smem_p = oz::gather_ozp_smem();
+    static bool attr_p = false;
+    static int sms = 148;
+    if (!attr_p) {
+      NLD_CUDA(cudaFuncSetAttribute(oz::k_gather_ozp, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    smem_p));
+      int dev = 0;
+      NLD_CUDA(cudaGetDevice(&dev));
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      attr_p = true;
+    }
+    const unsigned grid_n = std::min<unsigned>(nsub, (unsigned)sms);
+    oz::k_gather_ozp<<<grid_n, oz::kPThreads, smem_p, st>>>(subs, order, (int)nsub, ps.cells,
+                                                            ps.wdev, ps.rows, ps.pix, ex, grid,
+                                                            grid_ld, out, N, nrhs, ep);
+    NLD_CUDA(cudaGetLastError());
+    return;
+  }
   const int smem = oz::gather_oz_smem();
   static bool attr = false;
   if (!attr) {

@@ -847,6 +847,7 @@ void build_planset(nld_operator* op, int which, cudaStream_t st) {
 void free_planset(PlanSet& ps) {
   cudaFree(ps.wdev);
   cudaFree(ps.sub_exp);
+  cudaFree(ps.sub_order);
   cudaFree(ps.K);
   if (ps.owns_tables) {
     cudaFree(ps.rows);
