@@ -1023,8 +1023,9 @@ void spread_window_fast(const PlanSet& ps, const Workspace& ws, int w, const dou
       bc = (e && e[0] == '0') ? 0 : 1;
     }
     if (use_ozaki() && nrhs % 16 == 0 && ps.sub_exp && !getenv("NLD_OZAKI_NO_SPREAD")) {
-      launch_spread_oz(ps, subs, ps.sub_exp + wp.sub_off * 24, nsub, ws.vmax, vt, nrhs, ws.blocks,
-                       st);
+      launch_spread_oz(ps, subs, ps.sub_exp + wp.sub_off * 24,
+                       ps.ychunk ? ps.ychunk + wp.sub_off : nullptr, nsub, ws.vmax, vt, nrhs,
+                       ws.blocks, st);
       if (getenv("NLD_OZ_PROF_PRINT")) ozaki_prof_dump("spread", st);
       if (getenv("NLD_OZAKI_DEBUG")) {
         // compare with the fp64 DMMA spread of the same window (debug only)
@@ -1074,7 +1075,8 @@ void spread_window_fast(const PlanSet& ps, const Workspace& ws, int w, const dou
           {
             // re-run sub0 alone through the library launcher
             std::vector<double> h3(nb);
-            launch_spread_oz(ps, subs, ps.sub_exp + wp.sub_off * 24, 1, ws.vmax, vt, nrhs,
+            launch_spread_oz(ps, subs, ps.sub_exp + wp.sub_off * 24,
+                             ps.ychunk ? ps.ychunk + wp.sub_off : nullptr, 1, ws.vmax, vt, nrhs,
                              ws.blocks, st);
             NLD_CUDA(cudaStreamSynchronize(st));
             NLD_CUDA(cudaMemcpy(h3.data(), ws.blocks, nb * 8, cudaMemcpyDeviceToHost));

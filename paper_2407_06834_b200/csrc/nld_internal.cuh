@@ -133,6 +133,9 @@ struct PlanSet {
   int64_t generic_nodes = 0;     // nodes in windows on the generic path
   int16_t* sub_exp = nullptr;    // sliced spread: per 3-D subproblem eA/eB/eC
   int32_t* sub_order = nullptr;  // per window: its 3-D subproblems by descending size
+  uint8_t* ydig = nullptr;       // sliced spread: Y = B (x) C digit slices per 32-node
+                                 // chunk, UMMA B-operand layout (12 KB per chunk)
+  int64_t* ychunk = nullptr;     // per 3-D subproblem: its first chunk in ydig
   int shares_tables_with = -1;   // index of the plan set whose tables we use
   bool owns_tables = true;
 };
@@ -200,9 +203,9 @@ void build_planset(nld_operator* op, int which, cudaStream_t st);
 // integer-sliced tensor-core spread (nld_ozaki.cu)
 bool use_ozaki();
 int16_t* ozaki_exponents(PlanSet& ps, cudaStream_t st);
-void launch_spread_oz(const PlanSet& ps, const SubDev* subs, const int16_t* ex, unsigned nsub,
-                      const unsigned long long* vmax, const double* vt, int nrhs, double* blocks,
-                      cudaStream_t st);
+void launch_spread_oz(const PlanSet& ps, const SubDev* subs, const int16_t* ex,
+                      const int64_t* ychunk, unsigned nsub, const unsigned long long* vmax,
+                      const double* vt, int nrhs, double* blocks, cudaStream_t st);
 void ozaki_vmax(const double* vt, int64_t n, int nrhs, unsigned long long* out, cudaStream_t st);
 void ozaki_prof_dump(const char* what, cudaStream_t st);
 namespace mma { struct GatherEpi; }

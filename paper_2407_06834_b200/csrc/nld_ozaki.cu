@@ -181,6 +181,13 @@ __global__ void k_vmax(const double* __restrict__ vt, int64_t n, int nrhs,
     atomicMax(&out[r], (unsigned long long)__double_as_longlong(m));
 }
 
+// ---- plan-time Y digits for the sliced spread (PY) ------------------------
+// Exactly the slicers' Y = B_b C_c (scaled by 2^(46 - eB_b - eC_c)) of every
+// 32-node chunk, as six 64 x 32 K-major digit slices (zero past the count).
+__global__ void k_spread_ydig(const SubDev* __restrict__ subs, const WinDev* __restrict__ wins,
+                              const double* __restrict__ rows, const int16_t* __restrict__ sub_exp,
+                              const int64_t* __restrict__ ychunk, uint8_t* __restrict__ ydig);
+
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(umma::smem_u32(dst)), "l"(src));
 }
@@ -193,6 +200,9 @@ __device__ __forceinline__ void cp_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
+#ifndef NLD_SP_COALESCE
+#define NLD_SP_COALESCE 1                        // spread loader: line-coalesced cp.async
+#endif
 constexpr int kRawRows = kChunk * 24 * 8;       // 6 KB of weight rows per chunk
 constexpr int kRawV = kChunk * 16 * 8;          // 4 KB of v lines per chunk
 constexpr int kRawBytes = kRawRows + kRawV;
@@ -209,6 +219,26 @@ constexpr int kOpStages = NLD_SP_OPSTAGES;   // operand stages (slicers <-> tens
 __host__ __device__ constexpr int spread_oz_smem() {
   return kOpStages * kStageBytes + kRawStages * kRawBytes;
 }
+
+// Precomputed-Y variant (PY): Y = B (x) C depends only on the (static) node
+// tables, so its digit slices are cut once at plan time (k_spread_ydig) in
+// the UMMA B-operand layout and streamed per chunk by one TMA bulk copy into
+// the raw stage, which the UMMAs then read directly.  The slicers cut only X,
+// shared memory carries no operand stage, and a raw stage is released by the
+// slicers and by the chunk's UMMA commit.  Raw stage: [A rows 32 x 8 doubles |
+// v lines 32 x 16 doubles | Y digits 6 x 2 KB].
+constexpr int kPyA = kChunk * 8 * 8;             // 2 KB
+constexpr int kPyY = kPyA + kRawV;               // Y digits offset
+constexpr int kPyRawBytes = kPyY + kSl * kBBytes;   // 18 KB
+#ifndef NLD_PY_STAGES
+#define NLD_PY_STAGES 8
+#endif
+#ifndef NLD_PY_YBULK
+#define NLD_PY_YBULK 1                           // Y digits by one TMA bulk copy (else cp.async)
+#endif
+constexpr int kPyRawStages = NLD_PY_STAGES;
+constexpr int kYChunkBytes = kSl * kBBytes;      // 12 KB per chunk in HBM
+__host__ __device__ constexpr int spread_oz_py_smem() { return kPyRawStages * kPyRawBytes; }
 
 // ---- spread ---------------------------------------------------------------
 // One CTA per subproblem (TMEM: 384 of 512 columns -> one CTA per SM),
@@ -237,16 +267,22 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* mbar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(umma::smem_u32(mbar)) : "memory");
 }
 
+template <bool PY>
 __global__ void __launch_bounds__(kSpreadThreads, 1)
 k_spread_oz(const SubDev* __restrict__ subs, const WinDev* __restrict__ wins,
             const double* __restrict__ rows, const int32_t* __restrict__ pix,
-            const int16_t* __restrict__ sub_exp, const unsigned long long* __restrict__ vmax,
+            const int16_t* __restrict__ sub_exp, const uint8_t* __restrict__ ydig,
+            const int64_t* __restrict__ ychunk, const unsigned long long* __restrict__ vmax,
             const double* __restrict__ vt, int nrhs, double* __restrict__ blocks) {
+  constexpr int RS = PY ? kPyRawStages : kRawStages;
+  constexpr int RB = PY ? kPyRawBytes : kRawBytes;
+  constexpr int RowS = PY ? 8 : 24;                 // doubles per node row in the raw stage
+  constexpr int VOff = PY ? kPyA : kRawRows;        // v lines in the raw stage
   // 16-byte alignment is all the no-swizzle descriptors need; do not declare
   // more: under -rdc the dynamic window is not 1024-aligned, and the compiler
   // would fold the declared alignment into the descriptor address bits
   extern __shared__ __align__(16) uint8_t smem[];
-  __shared__ uint64_t raw_full[kRawStages], raw_empty[kRawStages];
+  __shared__ uint64_t raw_full[RS], raw_empty[RS];
   __shared__ uint64_t op_ready[kOpStages], op_free[kOpStages], acc_full, acc_empty;
   __shared__ uint32_t taddr_s;
   __shared__ double rsc[kRows];       // row scale 2^(ev + eA - 46)
@@ -260,15 +296,17 @@ k_spread_oz(const SubDev* __restrict__ subs, const WinDev* __restrict__ wins,
   const double* __restrict__ rw = rows + wd.row_off + (sd.start - wd.node_off) * 24;
   const int32_t* __restrict__ pw = pix + sd.start;
   const int16_t* ex = sub_exp + (int64_t)blockIdx.x * kExpPerSub;
-  uint8_t* const raw = smem + kOpStages * kStageBytes;
+  uint8_t* const raw = smem + (PY ? 0 : kOpStages * kStageBytes);
   const int nchunk = (sd.count + kChunk - 1) / kChunk;
   const int ngroups = nrhs / 16;
+  const uint8_t* yd = PY ? ydig + ychunk[blockIdx.x] * (int64_t)kYChunkBytes : nullptr;
 
   if (warp == 0) umma::tmem_alloc<kTmemCols>(&taddr_s);
   if (tid == 32) {
-    for (int k = 0; k < kRawStages; ++k) {
-      umma::mbar_init(&raw_full[k], 33);      // 32 noinc cp.async arrivals + the bulk copy's
-      umma::mbar_init(&raw_empty[k], kSlicers / 32);
+    for (int k = 0; k < RS; ++k) {
+      // 32 noinc cp.async arrivals + the bulk copy's
+      umma::mbar_init(&raw_full[k], (PY && !NLD_PY_YBULK) ? 32 : 33);
+      umma::mbar_init(&raw_empty[k], kSlicers / 32 + (PY ? 1 : 0));   // (+ the UMMA commit)
     }
     for (int k = 0; k < kOpStages; ++k) {
       umma::mbar_init(&op_ready[k], kSlicers / 32);
@@ -306,26 +344,69 @@ k_spread_oz(const SubDev* __restrict__ subs, const WinDev* __restrict__ wins,
       // of in-flight loads, so the load latency hides behind four chunks)
       auto body = [&](int c, int32_t px) {
         if (c >= nchunk) return;
-        const int s = g % kRawStages;
-        if (g >= kRawStages) OZW(16, umma::mbar_wait(&raw_empty[s], ((g / kRawStages) - 1) & 1));
-        uint8_t* dst = raw + s * kRawBytes;
+        const int s = g % RS;
+        if (g >= RS) OZW(16, umma::mbar_wait(&raw_empty[s], ((g / RS) - 1) & 1));
+        uint8_t* dst = raw + s * RB;
         const int j0 = c * kChunk, cn = min(kChunk, sd.count - j0);
         if (lane == 0) {
-          // the chunk's weight rows are contiguous: one TMA bulk copy
-          const uint32_t bytes = (uint32_t)cn * 24 * 8;
-          umma::mbar_arrive_expect_tx(&raw_full[s], bytes);
-          umma::bulk_g2s(dst, rw + (int64_t)j0 * 24, bytes, &raw_full[s]);
+          if constexpr (PY) {
+#if NLD_PY_YBULK
+            // the chunk's precomputed Y digits: one TMA bulk copy
+            umma::mbar_arrive_expect_tx(&raw_full[s], kYChunkBytes);
+            umma::bulk_g2s(dst + kPyY, yd + (int64_t)c * kYChunkBytes, kYChunkBytes, &raw_full[s]);
+#endif
+          } else {
+            // the chunk's weight rows are contiguous: one TMA bulk copy
+            const uint32_t bytes = (uint32_t)cn * 24 * 8;
+            umma::mbar_arrive_expect_tx(&raw_full[s], bytes);
+            umma::bulk_g2s(dst, rw + (int64_t)j0 * 24, bytes, &raw_full[s]);
+          }
         }
+#if NLD_SP_COALESCE
+        // coalesced: each instruction copies whole lines -- 8 lanes per 128-byte
+        // v line (4 nodes per instruction), 4 lanes per 64-byte A part (8 nodes);
+        // the node's pixel comes from its lane by shuffle
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int nd = q * 4 + (lane >> 3), pc = lane & 7;
+          const int32_t pxn = __shfl_sync(0xffffffffu, px, nd);
+          if (nd < cn)
+            cp_async16(dst + VOff + nd * 128 + pc * 16,
+                       vt + (int64_t)(uint32_t)pxn * nrhs + rg + 2 * pc);
+        }
+#if !NLD_PY_YBULK
+        if constexpr (PY) {
+#pragma unroll
+          for (int q = 0; q < kYChunkBytes / 512; ++q)
+            cp_async16(dst + kPyY + (q * 32 + lane) * 16,
+                       yd + (int64_t)c * kYChunkBytes + (q * 32 + lane) * 16);
+        }
+#endif
+        if constexpr (PY) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int nd = q * 8 + (lane >> 2), pc = lane & 3;
+            if (nd < cn) cp_async16(dst + nd * 64 + pc * 16, rw + (int64_t)(j0 + nd) * 24 + 2 * pc);
+          }
+        }
+#else
         if (lane < cn) {
+          if constexpr (PY) {
+            // A part (8 doubles) of the node's weight row
+            const double* as = rw + (int64_t)(j0 + lane) * 24;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) cp_async16(dst + lane * 64 + 16 * q, as + 2 * q);
+          }
 #ifdef NLD_EXP_CONTIG_V
           const double* vs = vt + (int64_t)(j0 + lane) * nrhs + rg;   // timing experiment only
 #else
           const double* vs = vt + (int64_t)(uint32_t)px * nrhs + rg;
 #endif
-          uint8_t* vd = dst + kRawRows + lane * 128;
+          uint8_t* vd = dst + VOff + lane * 128;
 #pragma unroll
           for (int q = 0; q < 8; ++q) cp_async16(vd + 16 * q, vs + 2 * q);
         }
+#endif
 #ifdef NLD_EXP_WAITGROUP
         cp_commit();
         cp_wait<0>();
@@ -353,11 +434,13 @@ k_spread_oz(const SubDev* __restrict__ subs, const WinDev* __restrict__ wins,
     for (int grp = 0; grp < ngroups; ++grp) {
       if (grp > 0) OZW(18, umma::mbar_wait(&acc_empty, (grp - 1) & 1));   // epilogue drained TMEM
       for (int c = 0; c < nchunk; ++c, ++g) {
-        const int st = g % kOpStages;
+        const int st = g % kOpStages, s = g % RS;
         OZW(17, umma::mbar_wait(&op_ready[st], (g / kOpStages) & 1));
+        if constexpr (PY) umma::mbar_wait(&raw_full[s], (g / RS) & 1);   // Y digits landed
         umma::fence_after();
         if (lane == 0) {
-          const uint32_t bB = umma::smem_u32(smem + st * kStageBytes);
+          const uint32_t bB = PY ? umma::smem_u32(raw + s * RB + kPyY)
+                                 : umma::smem_u32(smem + st * kStageBytes);
           const uint32_t xa = tmem + (uint32_t)(kXTmem0 + st * kSl * 8);
 #ifndef NLD_EXP_SNOMMA
 #pragma unroll
@@ -372,6 +455,7 @@ k_spread_oz(const SubDev* __restrict__ subs, const WinDev* __restrict__ wins,
           }
 #endif
           umma::commit(&op_free[st]);
+          if constexpr (PY) umma::commit(&raw_empty[s]);   // Y digits consumed
           if (c == nchunk - 1) umma::commit(&acc_full);
         }
         __syncwarp();
@@ -392,14 +476,14 @@ k_spread_oz(const SubDev* __restrict__ subs, const WinDev* __restrict__ wins,
       }
       asm volatile("bar.sync 1, %0;\n" ::"n"(kSlicers));      // slicers only
       for (int c = 0; c < nchunk; ++c, ++g) {
-        const int st = g % kOpStages, s = g % kRawStages;
+        const int st = g % kOpStages, s = g % RS;
 #ifndef NLD_EXP_NORAWWAIT
-        OZW(19, umma::mbar_wait(&raw_full[s], (g / kRawStages) & 1));
+        OZW(19, umma::mbar_wait(&raw_full[s], (g / RS) & 1));
 #endif
         if (g >= kOpStages) OZW(20, umma::mbar_wait(&op_free[st], ((g / kOpStages) - 1) & 1));
         uint8_t* sB = smem + st * kStageBytes;
-        const double* R = reinterpret_cast<const double*>(raw + s * kRawBytes);
-        const double* Vr = R + kChunk * 24;
+        const double* R = reinterpret_cast<const double*>(raw + s * RB);
+        const double* Vr = reinterpret_cast<const double*>(raw + s * RB + VOff);
         const int cn = min(kChunk, sd.count - c * kChunk);
         // full chunks (all but a subproblem's last) skip the per-node guards
         auto slice_chunk = [&](auto full) {
@@ -414,7 +498,7 @@ k_spread_oz(const SubDev* __restrict__ subs, const WinDev* __restrict__ wins,
               double x = 0.0, y = 0.0;
               if (full || j < cn) {
                 x = Vr[j * 16 + r];
-                y = R[j * 24 + a] * sx;
+                y = R[j * RowS + a] * sx;
               }
               slice1(x, y, lo[i], hi[i]);
             }
@@ -429,7 +513,7 @@ k_spread_oz(const SubDev* __restrict__ subs, const WinDev* __restrict__ wins,
             for (int p = 0; p < kSl; ++p)
               umma::tmem_st4(xt + (uint32_t)(p * 8), w4[0][p], w4[1][p], w4[2][p], w4[3][p]);
           }
-          {
+          if constexpr (!PY) {
             const int n = tid & 63, gq = tid >> 6;
             const int b = n >> 3, cc = n & 7;
             const double sy = sb[b] * sc[cc];
@@ -447,11 +531,11 @@ k_spread_oz(const SubDev* __restrict__ subs, const WinDev* __restrict__ wins,
             store8(lo, hi, sB + canon32(n, gq * 8), kBBytes);
           }
         };
-        if (cn == kChunk) slice_chunk(std::true_type{});
-        else slice_chunk(std::false_type{});
-        umma::tmem_wait_st();
+        if (cn == kChunk) OZW(23, slice_chunk(std::true_type{}));
+        else OZW(23, slice_chunk(std::false_type{}));
+        OZW(22, umma::tmem_wait_st());
         umma::fence_before();
-        umma::fence_async_smem();
+        if constexpr (!PY) umma::fence_async_smem();
         __syncwarp();
         if (lane == 0) {
           mbar_arrive(&op_ready[st]);
@@ -502,6 +586,35 @@ k_spread_oz(const SubDev* __restrict__ subs, const WinDev* __restrict__ wins,
   if (warp == 0) umma::tmem_free<kTmemCols>(tmem);
 }
 
+__global__ void __launch_bounds__(256)
+k_spread_ydig(const SubDev* __restrict__ subs, const WinDev* __restrict__ wins,
+              const double* __restrict__ rows, const int16_t* __restrict__ sub_exp,
+              const int64_t* __restrict__ ychunk, uint8_t* __restrict__ ydig) {
+  const SubDev sd = subs[blockIdx.x];
+  const WinDev wd = wins[sd.win];
+  const double* __restrict__ rw = rows + wd.row_off + (sd.start - wd.node_off) * 24;
+  const int16_t* ex = sub_exp + (int64_t)blockIdx.x * kExpPerSub;
+  const int n = threadIdx.x & 63, gq = threadIdx.x >> 6;
+  const int b = n >> 3, cc = n & 7;
+  const double sy = pow2(46 - ex[8 + b]) * pow2(-ex[16 + cc]);
+  const int nchunk = (sd.count + kChunk - 1) / kChunk;
+  uint8_t* base = ydig + ychunk[blockIdx.x] * (int64_t)kYChunkBytes;
+  for (int c = 0; c < nchunk; ++c) {
+    uint32_t lo[8], hi[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int j = c * kChunk + gq * 8 + i;
+      double x = 0.0, y = 0.0;
+      if (j < sd.count) {
+        x = rw[(int64_t)j * 24 + 8 + b] * sy;
+        y = rw[(int64_t)j * 24 + 16 + cc];
+      }
+      slice1(x, y, lo[i], hi[i]);
+    }
+    store8(lo, hi, base + (int64_t)c * kYChunkBytes + canon32(n, gq * 8), kBBytes);
+  }
+}
+
 // ---- gather ---------------------------------------------------------------
 // T[(a, r)][j] = sum_{(b,c)} G_r[a][(b,c)] Y_j[(b,c)],  Y_j = B_j (x) C_j,
 // then y_r[j] = sum_a A_j[a] T[(a, r)][j]  (the DMMA gather's contraction,
@@ -547,21 +660,33 @@ constexpr int kGIssuerWarp = kGEpiWarps + 2;
 constexpr int kGLoaderWarp = kGEpiWarps + 3;
 constexpr int kGNodeGroups = kGTile / 8 / (kGEpiWarps / 4);   // 8-node groups per epilogue warp
 
-// sum_t D_t 2^(16 - 8t), t = 0..5, from the six int32 diagonals: two exact
-// 45-bit integers H = (D0 2^8 + D1) 2^8 + D2, L = (D3 2^8 + D4) 2^8 + D5 on the
-// integer pipe, then H + 2^-24 L with one rounding (2 DADD + 1 DFMA instead of
-// 6 conversions + 5 DFMA per value)
+// sum_t D_t 2^(40 - 8t), t = 0..5, from the six int32 diagonals of a K = 64
+// product (|D_t| <= (t + 1) 2^20): the pairs D_2k 2^8 + D_2k+1 are exact in
+// int32 (|.| < 1.35e9), so three IMADs, three exact int32 -> fp64 conversions
+// and (X01 2^16 + X23) 2^16 + X45 with one rounding (the first FMA is exact).
+// The caller's scale carries the 2^-24 (vs sum_t D_t 2^(16 - 8t)).
+#ifndef NLD_OZ_COMBINE64
+#define NLD_OZ_COMBINE64 0
+#endif
 static_assert(kSl == 6, "combine6 assumes six digits");
+__device__ __forceinline__ double i2d(uint32_t x);
 template <int NCOL>
 __device__ __forceinline__ double combine6(const uint32_t (&dv)[6][NCOL], int i) {
+#if NLD_OZ_COMBINE64
+  // reference form: two exact 45-bit integers on the 64-bit integer path
   const long long H = ((long long)(int32_t)dv[0][i] << 16) + ((long long)(int32_t)dv[1][i] << 8) +
                       (long long)(int32_t)dv[2][i];
   const long long L = ((long long)(int32_t)dv[3][i] << 16) + ((long long)(int32_t)dv[4][i] << 8) +
                       (long long)(int32_t)dv[5][i];
-  // |H|, |L| < 2^51: 2^52 + 2^51 + x is exact and has x in its low mantissa bits
   const double hd = __longlong_as_double(H + 0x4338000000000000LL) - 6755399441055744.0;
   const double ld = __longlong_as_double(L + 0x4338000000000000LL) - 6755399441055744.0;
-  return fma(ld, 5.9604644775390625e-08, hd);   // 2^-24
+  return fma(ld, 5.9604644775390625e-08, hd) * 16777216.0;   // x 2^24 (exact)
+#else
+  const uint32_t x01 = dv[0][i] * 256u + dv[1][i];
+  const uint32_t x23 = dv[2][i] * 256u + dv[3][i];
+  const uint32_t x45 = dv[4][i] * 256u + dv[5][i];
+  return fma(fma(i2d(x01), 65536.0, i2d(x23)), 65536.0, i2d(x45));
+#endif
 }
 
 // exact int32 -> fp64 without I2F: 2^52 + 2^31 + x has x + 2^31 in its mantissa
@@ -665,7 +790,7 @@ k_gather_oz(const SubDev* __restrict__ subs, const CellDev* __restrict__ cells,
       // clamped like ev: the digit scale and tsc must use the same exponent
       const int eG = max(-900, exp_bound(fmax(gmax[0][m], gmax[1][m])));
       const double sg = pow2(46 - eG);
-      if (h == 0) tsc[m] = ldexp(1.0, eG + eBm + eCm - 28);   // (eG-46)+(eBm+eCm-46)+80-16
+      if (h == 0) tsc[m] = ldexp(1.0, eG + eBm + eCm - 52);   // (eG-46)+(eBm+eCm-46)+80-16-24
 #pragma unroll 1
       for (int kb = 0; kb < 2; ++kb) {
         uint32_t lo[16], hi[16];
@@ -723,10 +848,13 @@ k_gather_oz(const SubDev* __restrict__ subs, const CellDev* __restrict__ cells,
           const uint32_t bB = umma::smem_u32(sGB + st * kGBStage);
           const uint32_t dcol = tmem + (uint32_t)(ab * kSl * kGTile);
 #ifndef NLD_EXP_GNOMMA
+          // p outer, ks inner: the two K steps of one digit row hit the same D
+          // window back to back and chain in the tensor pipe (a D window / N
+          // change between every UMMA costs ~60% more: scripts/umma/probe_pattern.cu)
 #pragma unroll
-          for (int ks = 0; ks < 2; ++ks)
+          for (int p = 0; p < kSl; ++p)
 #pragma unroll
-            for (int p = 0; p < kSl; ++p) {
+            for (int ks = 0; ks < 2; ++ks) {
               const uint64_t db = umma::make_sdesc(bB + ks * 256, 128, 512);
               if constexpr (kGTmemA) {
                 umma::mma_i8_ta(dcol + (uint32_t)(p * kGTile),
@@ -995,10 +1123,13 @@ k_gather_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
           const uint32_t aB = umma::smem_u32(sGA + gs * kSl * kGA);
           const uint32_t bB = umma::smem_u32(sGB + st * kGBStage);
           const uint32_t dcol = tmem + (uint32_t)(ab * kSl * kGTile);
+          // p outer, ks inner: the two K steps of one digit row hit the same D
+          // window back to back and chain in the tensor pipe (a D window / N
+          // change between every UMMA costs ~60% more: scripts/umma/probe_pattern.cu)
 #pragma unroll
-          for (int ks = 0; ks < 2; ++ks)
+          for (int p = 0; p < kSl; ++p)
 #pragma unroll
-            for (int p = 0; p < kSl; ++p) {
+            for (int ks = 0; ks < 2; ++ks) {
               const uint64_t da = umma::make_sdesc(aB + p * kGA + ks * 256, 128, 512);
               const uint64_t db = umma::make_sdesc(bB + ks * 256, 128, 512);
               umma::mma_i8(dcol + (uint32_t)(p * kGTile), da, db,
@@ -1048,7 +1179,7 @@ k_gather_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
         for (int i = 0; i < 64; ++i) mx = fmax(mx, fabs(gval(i)));
         const int eG = max(-900, exp_bound(mx));
         const double sg = pow2(46 - eG);
-        tsc[gs][m] = ldexp(1.0, eG + eBm + eCm - 28);
+        tsc[gs][m] = ldexp(1.0, eG + eBm + eCm - 52);   // combine6 carries 2^24
         uint8_t* dA = sGA + gs * kSl * kGA;
 #pragma unroll 1
         for (int kb = 0; kb < 4; ++kb) {
@@ -1061,8 +1192,10 @@ k_gather_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
         __syncwarp();
         if (lane == 0) mbar_arrive(&g_full[gs]);
       }
-      // Y digits of each tile: node n = t >> 2 (8 per warp), bc quarter kq
-      const int n = t >> 2, kq = t & 3;
+      // Y digits of each tile: 8 nodes per warp, node = lane & 7, bc quarter
+      // kq = lane >> 3, so each quarter-warp's 16-byte stores cover one
+      // contiguous 128-byte line (conflict-free)
+      const int n = (t >> 5) * 8 + (lane & 7), kq = lane >> 3;
       for (int tl = 0; tl < ntile; ++tl, ++gt) {
         const int s = gt % RS, st = gt % OS;
         umma::mbar_wait(&raw_full[s], (gt / RS) & 1);
@@ -1096,6 +1229,34 @@ k_gather_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
     const int mrow = lg * 32 + lane;
     const uint32_t tl_lane = tmem + ((uint32_t)(lg * 32) << 16);
     const bool need_eta = ep.kind == NLD_APPLY_SYSTEM || ep.kind == NLD_APPLY_LAPLACIAN;
+    // The running window sum, v and eta of a tile's pixels are scattered
+    // global loads: they are issued one tile ahead (software pipeline over
+    // the flat tile sequence, across item boundaries), so their latency
+    // hides behind the current tile's TMEM drain instead of stalling it.
+    struct EpiIn {
+      int64_t oe[2];
+      double prev[2], vx[2], et[2];
+    };
+    auto epi_load = [&](int kk, int tt, int gg) {
+      EpiIn e;
+      const SubDev sdn = subs[item_sub(kk)];
+      const int rgn = (kk % ngroups) * 16, sn = gg % RS;
+      umma::mbar_wait(&raw_full[sn], (gg / RS) & 1);
+      const int32_t* spn = reinterpret_cast<const int32_t*>(sRaw + sn * kGRaw + kGTile * kGRowS * 8);
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int nn = nh * 16 + q * 8 + a;
+        const bool ok = tt * kGTile + nn < sdn.count;
+        const int64_t px = ok ? (int64_t)spn[nn] : -1;
+        e.oe[q] = ok ? px * nrhs + rgn + r : -1;
+        e.prev[q] = (ok && ep.mode >= mma::kGatherAccum) ? out[e.oe[q]] : 0.0;
+        e.vx[q] = (ok && ep.mode == mma::kGatherFinal) ? ep.v[e.oe[q]] : 0.0;
+        e.et[q] = (ok && ep.mode == mma::kGatherFinal && need_eta) ? ep.eta[px] : 0.0;
+      }
+      return e;
+    };
+    EpiIn nxt;
+    if (nitems > 0) nxt = epi_load(0, 0, 0);
     int gt = 0;
     for (int k = 0; k < nitems; ++k) {
       const int gs = k & 1;
@@ -1105,22 +1266,13 @@ k_gather_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
       umma::mbar_wait(&g_full[gs], (k >> 1) & 1);
       const double ts = tsc[gs][mrow];
       for (int tl = 0; tl < ntile; ++tl, ++gt) {
-        const int ab = gt & 1, s = gt % RS, j0 = tl * kGTile;
-        umma::mbar_wait(&raw_full[s], (gt / RS) & 1);
+        const int ab = gt & 1, s = gt % RS;
         const double* R = reinterpret_cast<const double*>(sRaw + s * kGRaw);
-        const int32_t* sp = reinterpret_cast<const int32_t*>(sRaw + s * kGRaw + kGTile * kGRowS * 8);
-        int64_t oe[2];
-        double prev[2], vx[2], et[2];
-#pragma unroll
-        for (int q = 0; q < 2; ++q) {
-          const int nn = nh * 16 + q * 8 + a;
-          const bool ok = j0 + nn < sd.count;
-          const int64_t px = ok ? (int64_t)sp[nn] : -1;
-          oe[q] = ok ? px * nrhs + rg + r : -1;
-          prev[q] = (ok && ep.mode >= mma::kGatherAccum) ? out[oe[q]] : 0.0;
-          vx[q] = (ok && ep.mode == mma::kGatherFinal) ? ep.v[oe[q]] : 0.0;
-          et[q] = (ok && ep.mode == mma::kGatherFinal && need_eta) ? ep.eta[px] : 0.0;
-        }
+        const EpiIn cur = nxt;
+        if (tl + 1 < ntile) nxt = epi_load(k, tl + 1, gt + 1);
+        else if (k + 1 < nitems) nxt = epi_load(k + 1, 0, gt + 1);
+        const int64_t* oe = cur.oe;
+        const double *prev = cur.prev, *vx = cur.vx, *et = cur.et;
         umma::mbar_wait(&acc_full[ab], (gt >> 1) & 1);
         umma::fence_after();
         double ysum[2];
@@ -1229,22 +1381,52 @@ int16_t* ozaki_exponents(PlanSet& ps, cudaStream_t st) {
   NLD_CUDA(cudaMalloc(&ps.sub_order, sizeof(int32_t) * ord.size()));
   NLD_CUDA(cudaMemcpyAsync(ps.sub_order, ord.data(), sizeof(int32_t) * ord.size(),
                            cudaMemcpyHostToDevice, st));
+  // precomputed Y digits for the spread (12 KB per 32-node chunk) when they
+  // fit comfortably: at most half of the free memory (NLD_SPREAD_PREY=0: off)
+  const char* py = getenv("NLD_SPREAD_PREY");
+  if (!(py && py[0] == '0')) {
+    std::vector<int64_t> off(h.size());
+    int64_t chunks = 0;
+    for (size_t i = 0; i < h.size(); ++i) {
+      off[i] = chunks;
+      chunks += (h[i].count + oz::kChunk - 1) / oz::kChunk;
+    }
+    const size_t need = (size_t)chunks * oz::kYChunkBytes;
+    size_t free_b = 0, total_b = 0;
+    NLD_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    if (need > 0 && need <= free_b / 2) {
+      NLD_CUDA(cudaMalloc(&ps.ychunk, sizeof(int64_t) * off.size()));
+      NLD_CUDA(cudaMalloc(&ps.ydig, need));
+      NLD_CUDA(cudaMemcpyAsync(ps.ychunk, off.data(), sizeof(int64_t) * off.size(),
+                               cudaMemcpyHostToDevice, st));
+      oz::k_spread_ydig<<<(unsigned)h.size(), 256, 0, st>>>(ps.subs[3], ps.wdev, ps.rows,
+                                                            ps.sub_exp, ps.ychunk, ps.ydig);
+      NLD_CUDA(cudaGetLastError());
+    }
+  }
   NLD_CUDA(cudaStreamSynchronize(st));
   return ps.sub_exp;
 }
 
-void launch_spread_oz(const PlanSet& ps, const SubDev* subs, const int16_t* ex, unsigned nsub,
-                      const unsigned long long* vmax, const double* vt, int nrhs, double* blocks,
-                      cudaStream_t st) {
-  const int smem = oz::spread_oz_smem();
+void launch_spread_oz(const PlanSet& ps, const SubDev* subs, const int16_t* ex,
+                      const int64_t* ychunk, unsigned nsub, const unsigned long long* vmax,
+                      const double* vt, int nrhs, double* blocks, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    NLD_CUDA(cudaFuncSetAttribute(oz::k_spread_oz, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  smem));
+    NLD_CUDA(cudaFuncSetAttribute(oz::k_spread_oz<false>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  oz::spread_oz_smem()));
+    NLD_CUDA(cudaFuncSetAttribute(oz::k_spread_oz<true>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  oz::spread_oz_py_smem()));
     attr = true;
   }
-  oz::k_spread_oz<<<nsub, oz::kSpreadThreads, smem, st>>>(subs, ps.wdev, ps.rows, ps.pix, ex, vmax,
-                                                           vt, nrhs, blocks);
+  if (ps.ydig && ychunk)
+    oz::k_spread_oz<true><<<nsub, oz::kSpreadThreads, oz::spread_oz_py_smem(), st>>>(
+        subs, ps.wdev, ps.rows, ps.pix, ex, ps.ydig, ychunk, vmax, vt, nrhs, blocks);
+  else
+    oz::k_spread_oz<false><<<nsub, oz::kSpreadThreads, oz::spread_oz_smem(), st>>>(
+        subs, ps.wdev, ps.rows, ps.pix, ex, nullptr, nullptr, vmax, vt, nrhs, blocks);
   NLD_CUDA(cudaGetLastError());
 }
 
