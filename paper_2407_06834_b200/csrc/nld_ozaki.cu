@@ -1022,12 +1022,16 @@ k_gather_oz(const SubDev* __restrict__ subs, const CellDev* __restrict__ cells,
 // fixed cost that grows when pixel sharding makes subproblems small).
 //   warps 0-7  epilogue       warps 8-11 slicers (G digits + Y digits)
 //   warp 12    UMMA issuer    warp 13    loader
-constexpr int kPEpi = 8;
-constexpr int kPSl0 = 8;
+#ifndef NLD_GP_EPI
+#define NLD_GP_EPI 8
+#endif
+constexpr int kPEpi = NLD_GP_EPI;                // 8 or 16 epilogue warps
+constexpr int kPG = 16 / kPEpi;                  // 8-node groups per epilogue warp and tile
+constexpr int kPSl0 = kPEpi;
 constexpr int kPSlicers = 4;
-constexpr int kPIssuer = 12;
-constexpr int kPLoader = 13;
-constexpr int kPThreads = 32 * 14;
+constexpr int kPIssuer = kPEpi + 4;
+constexpr int kPLoader = kPEpi + 5;
+constexpr int kPThreads = 32 * (kPEpi + 6);
 
 __host__ __device__ constexpr int gather_ozp_smem() {
   return 2 * kSl * kGA + 3 * kGBStage + 6 * kGRaw;
@@ -1098,10 +1102,12 @@ k_gather_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
         const int j0 = tl * kGTile, cn = min(kGTile, sd.count - j0);
         const double* src = rw + (int64_t)j0 * 24;
         uint8_t* dst = sRaw + s * kGRaw;
+#ifndef NLD_EXP_PNOLOAD
         for (int e = lane; e < cn * 12; e += 32) {
           const int node = e / 12, gi = e - node * 12;
           cp_async16(dst + node * kGRowS * 8 + 16 * gi, src + 2 * e);
         }
+#endif
         if (lane < cn) cp_async4(dst + kGTile * kGRowS * 8 + 4 * lane, pw + j0 + lane);
         cp_async_mbar_arrive(&raw_full[s]);
       }
@@ -1126,6 +1132,7 @@ k_gather_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
           // p outer, ks inner: the two K steps of one digit row hit the same D
           // window back to back and chain in the tensor pipe (a D window / N
           // change between every UMMA costs ~60% more: scripts/umma/probe_pattern.cu)
+#ifndef NLD_EXP_PNOMMA
 #pragma unroll
           for (int p = 0; p < kSl; ++p)
 #pragma unroll
@@ -1135,6 +1142,7 @@ k_gather_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
               umma::mma_i8(dcol + (uint32_t)(p * kGTile), da, db,
                            umma::idesc_i8(kRows, (kSl - p) * kGTile), (ks > 0 || p > 0) ? 1u : 0u);
             }
+#endif
           umma::commit(&op_free[st]);
           umma::commit(&acc_full[ab]);
           if (tl == ntile - 1) umma::commit(&g_empty[gs]);   // item k's G digits released
@@ -1176,7 +1184,9 @@ k_gather_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
         };
         double mx = 0.0;
 #pragma unroll 16
+#ifndef NLD_EXP_PNOG
         for (int i = 0; i < 64; ++i) mx = fmax(mx, fabs(gval(i)));
+#endif
         const int eG = max(-900, exp_bound(mx));
         const double sg = pow2(46 - eG);
         tsc[gs][m] = ldexp(1.0, eG + eBm + eCm - 52);   // combine6 carries 2^24
@@ -1200,6 +1210,7 @@ k_gather_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
         const int s = gt % RS, st = gt % OS;
         umma::mbar_wait(&raw_full[s], (gt / RS) & 1);
         if (gt >= OS) umma::mbar_wait(&op_free[st], ((gt / OS) - 1) & 1);
+#ifndef NLD_EXP_PNOSLICE
         const double* R = reinterpret_cast<const double*>(sRaw + s * kGRaw) + n * kGRowS;
         const bool ok = tl * kGTile + n < sd.count;
         uint32_t lo[16], hi[16];
@@ -1214,6 +1225,7 @@ k_gather_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
           slice1(x, y, lo[i], hi[i]);
         }
         store16(lo, hi, sGB + st * kGBStage + canon64(n, kq * 16), kGB);
+#endif
         umma::fence_async_smem();
         __syncwarp();
         if (lane == 0) {
@@ -1234,65 +1246,88 @@ k_gather_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
     // the flat tile sequence, across item boundaries), so their latency
     // hides behind the current tile's TMEM drain instead of stalling it.
     struct EpiIn {
-      int64_t oe[2];
-      double prev[2], vx[2], et[2];
+      int64_t oe[kPG];
+      double prev[kPG], vx[kPG], et[kPG];
     };
-    auto epi_load = [&](int kk, int tt, int gg) {
+    // (count, rhs group) of the tile's item are passed in: the item's SubDev
+    // is read once per item, one item ahead, not per tile
+    auto epi_load = [&](int cnt, int rgn, int tt, int gg) {
       EpiIn e;
-      const SubDev sdn = subs[item_sub(kk)];
-      const int rgn = (kk % ngroups) * 16, sn = gg % RS;
+      const int sn = gg % RS;
       umma::mbar_wait(&raw_full[sn], (gg / RS) & 1);
       const int32_t* spn = reinterpret_cast<const int32_t*>(sRaw + sn * kGRaw + kGTile * kGRowS * 8);
 #pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        const int nn = nh * 16 + q * 8 + a;
-        const bool ok = tt * kGTile + nn < sdn.count;
+      for (int q = 0; q < kPG; ++q) {
+        const int nn = (nh * kPG + q) * 8 + a;
+        const bool ok = tt * kGTile + nn < cnt;
+#ifdef NLD_EXP_CONTIG_G
+        const int64_t px = ok ? (int64_t)(tt * kGTile + nn) : -1;   // timing experiment only
+#else
         const int64_t px = ok ? (int64_t)spn[nn] : -1;
+#endif
         e.oe[q] = ok ? px * nrhs + rgn + r : -1;
+#ifdef NLD_EXP_PNOGLD
+        e.prev[q] = e.vx[q] = e.et[q] = 0.0;   // timing experiment only
+#else
         e.prev[q] = (ok && ep.mode >= mma::kGatherAccum) ? out[e.oe[q]] : 0.0;
         e.vx[q] = (ok && ep.mode == mma::kGatherFinal) ? ep.v[e.oe[q]] : 0.0;
         e.et[q] = (ok && ep.mode == mma::kGatherFinal && need_eta) ? ep.eta[px] : 0.0;
+#endif
       }
       return e;
     };
     EpiIn nxt;
-    if (nitems > 0) nxt = epi_load(0, 0, 0);
+    int cnt_next = 0;
+    if (nitems > 0) {
+      cnt_next = subs[item_sub(0)].count;
+      nxt = epi_load(cnt_next, 0, 0, 0);
+    }
     int gt = 0;
     for (int k = 0; k < nitems; ++k) {
       const int gs = k & 1;
-      const SubDev sd = subs[item_sub(k)];
+      const int cnt = cnt_next;
+      if (k + 1 < nitems) cnt_next = subs[item_sub(k + 1)].count;
       const int rg = (k % ngroups) * 16;
-      const int ntile = (sd.count + kGTile - 1) / kGTile;
+      const int ntile = (cnt + kGTile - 1) / kGTile;
       umma::mbar_wait(&g_full[gs], (k >> 1) & 1);
       const double ts = tsc[gs][mrow];
       for (int tl = 0; tl < ntile; ++tl, ++gt) {
         const int ab = gt & 1, s = gt % RS;
         const double* R = reinterpret_cast<const double*>(sRaw + s * kGRaw);
         const EpiIn cur = nxt;
-        if (tl + 1 < ntile) nxt = epi_load(k, tl + 1, gt + 1);
-        else if (k + 1 < nitems) nxt = epi_load(k + 1, 0, gt + 1);
+        if (tl + 1 < ntile) nxt = epi_load(cnt, rg, tl + 1, gt + 1);
+        else if (k + 1 < nitems) nxt = epi_load(cnt_next, ((k + 1) % ngroups) * 16, 0, gt + 1);
         const int64_t* oe = cur.oe;
         const double *prev = cur.prev, *vx = cur.vx, *et = cur.et;
         umma::mbar_wait(&acc_full[ab], (gt >> 1) & 1);
         umma::fence_after();
-        double ysum[2];
+        double ysum[kPG];
 #pragma unroll
-        for (int q = 0; q < 2; ++q) {
-          const int nb = nh * 16 + q * 8;
+        for (int q = 0; q < kPG; ++q) {
+          const int nb = (nh * kPG + q) * 8;
           uint32_t dv[kSl][8];
 #pragma unroll
           for (int tt = 0; tt < kSl; ++tt)
+#ifndef NLD_EXP_PNOTLD
             umma::tmem_ld8(tl_lane + (uint32_t)(ab * kSl * kGTile + tt * kGTile + nb), dv[tt]);
+#else
+            dv[tt][0] = tt;
+#endif
           umma::tmem_wait_ld();
-          if (q == 1) {
+          if (q == kPG - 1) {
             umma::fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&acc_empty[ab]);
           }
           double v8[8];
+#ifdef NLD_EXP_PNOEPI
+#pragma unroll
+          for (int i = 0; i < 8; ++i) v8[i] = (double)(int)dv[i % 6][i];
+#else
 #pragma unroll
           for (int i = 0; i < 8; ++i)
             v8[i] = combine6(dv, i) * ts * R[(nb + i) * kGRowS + a];
+#endif
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
             const bool up = lane & 4;
@@ -1317,7 +1352,7 @@ k_gather_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
         __syncwarp();
         if (lane == 0) mbar_arrive(&raw_empty[s]);
 #pragma unroll
-        for (int q = 0; q < 2; ++q) {
+        for (int q = 0; q < kPG; ++q) {
           if (oe[q] < 0) continue;
           const double y = ysum[q];
           double res;
@@ -1330,7 +1365,11 @@ k_gather_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
             const double mu = ep.coef ? ep.coef[2 * (rg + r) + 1] : 0.0;
             res = mma::epi_value(ep.kind, ep.L, prev[q] + y, vx[q], et[q], lam, mu);
           }
+#ifndef NLD_EXP_PNOGST
           out[oe[q]] = res;
+#else
+          if (res == 1.2345e-300) out[oe[q]] = res;   // timing experiment only
+#endif
         }
       }
       __syncwarp();

@@ -201,3 +201,62 @@ extern "C" int tld_rate(int warps, int iters, int blocks, double* bytes_per_cyc)
   cudaFree(sink);
   return e != cudaSuccess;
 }
+
+// commit round trip: lane 0 of warp 0 issues (optionally one UMMA and) a
+// tcgen05.commit to bar_a; warp 1 waits on bar_a and arrives on bar_b;
+// warp 0 waits on bar_b -- cycles per iteration
+__global__ void __launch_bounds__(64, 1) k_commit_rt(int iters, int with_mma, long long* out) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  __shared__ uint64_t bar_a, bar_b;
+  __shared__ uint32_t taddr;
+  for (int e = threadIdx.x; e < 128 * 32 + 32 * 32; e += blockDim.x) sm[e] = (uint8_t)e;
+  fence_async_smem();
+  if (threadIdx.x < 32) tmem_alloc<512>(&taddr);
+  if (threadIdx.x == 32) {
+    mbar_init(&bar_a, 1);
+    mbar_init(&bar_b, 1);
+    mbar_fence_init();
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t t = taddr;
+  const long long t0 = clock64();
+  if (threadIdx.x < 32) {
+    for (int it = 0; it < iters; ++it) {
+      if (threadIdx.x == 0) {
+        if (with_mma) {
+          const uint64_t da = make_sdesc(smem_u32(sm), 128, 256);
+          const uint64_t db = make_sdesc(smem_u32(sm + 4096), 128, 256);
+          mma_i8(t, da, db, idesc_i8(128, 32), 1u);
+        }
+        commit(&bar_a);
+      }
+      __syncwarp();
+      mbar_wait(&bar_b, it & 1);
+    }
+  } else {
+    for (int it = 0; it < iters; ++it) {
+      mbar_wait(&bar_a, it & 1);
+      if (threadIdx.x == 32) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(&bar_b)) : "memory");
+      __syncwarp();
+    }
+  }
+  const long long t1 = clock64();
+  if (threadIdx.x == 0) out[blockIdx.x] = t1 - t0;
+  fence_before();
+  __syncthreads();
+  if (threadIdx.x < 32) tmem_free<512>(t);
+}
+
+extern "C" int commit_rt(int iters, int with_mma, int blocks, double* cyc) {
+  long long* d;
+  cudaMalloc(&d, sizeof(long long) * blocks);
+  k_commit_rt<<<blocks, 64, 8192>>>(iters, with_mma, d);
+  cudaError_t e = cudaDeviceSynchronize();
+  long long h[256];
+  cudaMemcpy(h, d, sizeof(long long) * (blocks < 256 ? blocks : 256), cudaMemcpyDeviceToHost);
+  *cyc = (double)h[0] / iters;
+  cudaFree(d);
+  return e != cudaSuccess;
+}
