@@ -26,10 +26,14 @@ elif len(ends) >= 2:
 else:
     step = []
 agg = OrderedDict()
+cnt = OrderedDict()
 for n, ms in step:
+    n = n.split("<")[0]
     agg[n] = agg.get(n, 0.0) + ms
+    cnt[n] = cnt.get(n, 0) + 1
 tot = sum(agg.values())
 out = {"launches_total": len(seq), "step_launches": len(step),
        "step_ms_serialized": tot,
-       "step_share": {k: {"ms": v, "share": v / tot} for k, v in agg.items()}}
+       "step_share": {k: {"ms": v, "share": v / tot} for k, v in agg.items()},
+       "step_launch_counts": cnt}
 print(json.dumps(out, indent=1))
