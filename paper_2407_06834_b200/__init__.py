@@ -6,6 +6,7 @@ hand-written sm_100a CUDA kernels behind the C-ABI in include/nld_b200.h;
 importing this package fails if libnld_b200.so is missing (no CPU fallback).
 """
 
+from . import bilevel
 from ._lib import LIB_PATH
 from .errors import (ConfigError, DenseLimitError, DimensionMismatchError,
                      NldenoiseError, ScalingOverflowError, SolverBreakdownError,
@@ -28,5 +29,5 @@ __all__ = [
     "deflated_solve_batched", "pcg", "plain_solve", "scs_down", "scs_up",
     "FastsumPlan", "NfftPlan", "NodeSet", "expansion_degree",
     "gauss_transform_direct", "gauss_transform_fast", "ndft", "ndft_adjoint",
-    "nfft", "nfft_adjoint",
+    "nfft", "nfft_adjoint", "bilevel",
 ]
