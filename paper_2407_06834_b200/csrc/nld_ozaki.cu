@@ -1241,6 +1241,7 @@ k_gather_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
     const int mrow = lg * 32 + lane;
     const uint32_t tl_lane = tmem + ((uint32_t)(lg * 32) << 16);
     const bool need_eta = ep.kind == NLD_APPLY_SYSTEM || ep.kind == NLD_APPLY_LAPLACIAN;
+    const double inv_L = 1.0 / (double)ep.L;
     // The running window sum, v and eta of a tile's pixels are scattered
     // global loads: they are issued one tile ahead (software pipeline over
     // the flat tile sequence, across item boundaries), so their latency
@@ -1289,6 +1290,9 @@ k_gather_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
       if (k + 1 < nitems) cnt_next = subs[item_sub(k + 1)].count;
       const int rg = (k % ngroups) * 16;
       const int ntile = (cnt + kGTile - 1) / kGTile;
+      // this lane's rhs coefficients, once per item
+      const double lam_r = (ep.mode == mma::kGatherFinal && ep.coef) ? ep.coef[2 * (rg + r)] : 0.0;
+      const double mu_r = (ep.mode == mma::kGatherFinal && ep.coef) ? ep.coef[2 * (rg + r) + 1] : 0.0;
       umma::mbar_wait(&g_full[gs], (k >> 1) & 1);
       const double ts = tsc[gs][mrow];
       for (int tl = 0; tl < ntile; ++tl, ++gt) {
@@ -1361,9 +1365,8 @@ k_gather_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
           } else if (ep.mode == mma::kGatherAccum) {
             res = prev[q] + y;
           } else {
-            const double lam = ep.coef ? ep.coef[2 * (rg + r)] : 0.0;
-            const double mu = ep.coef ? ep.coef[2 * (rg + r) + 1] : 0.0;
-            res = mma::epi_value(ep.kind, ep.L, prev[q] + y, vx[q], et[q], lam, mu);
+            res = mma::epi_value_r(ep.kind, (double)ep.L, inv_L, prev[q] + y, vx[q], et[q], lam_r,
+                                   mu_r);
           }
 #ifndef NLD_EXP_PNOGST
           out[oe[q]] = res;
