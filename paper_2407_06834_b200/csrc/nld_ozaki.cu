@@ -362,7 +362,9 @@ k_spread_oz(const SubDev* __restrict__ subs, const WinDev* __restrict__ wins,
             umma::bulk_g2s(dst, rw + (int64_t)j0 * 24, bytes, &raw_full[s]);
           }
         }
-#if NLD_SP_COALESCE
+#if defined(NLD_EXP_SNOLOAD)
+        if (lane < cn) cp_async16(dst + VOff + lane * 16, vt + (int64_t)(uint32_t)px * nrhs + rg);
+#elif NLD_SP_COALESCE
         // coalesced: each instruction copies whole lines -- 8 lanes per 128-byte
         // v line (4 nodes per instruction), 4 lanes per 64-byte A part (8 nodes);
         // the node's pixel comes from its lane by shuffle
@@ -531,8 +533,10 @@ k_spread_oz(const SubDev* __restrict__ subs, const WinDev* __restrict__ wins,
             store8(lo, hi, sB + canon32(n, gq * 8), kBBytes);
           }
         };
+#ifndef NLD_EXP_SNOSLICE
         if (cn == kChunk) OZW(23, slice_chunk(std::true_type{}));
         else OZW(23, slice_chunk(std::false_type{}));
+#endif
         OZW(22, umma::tmem_wait_st());
         umma::fence_before();
         if constexpr (!PY) umma::fence_async_smem();
@@ -1032,9 +1036,16 @@ constexpr int kPSlicers = 4;
 constexpr int kPIssuer = kPEpi + 4;
 constexpr int kPLoader = kPEpi + 5;
 constexpr int kPThreads = 32 * (kPEpi + 6);
+#ifndef NLD_GP_RS
+#define NLD_GP_RS 6
+#endif
+#ifndef NLD_GP_OS
+#define NLD_GP_OS 3
+#endif
+constexpr int kPRS = NLD_GP_RS, kPOS = NLD_GP_OS;   // raw / operand stages
 
 __host__ __device__ constexpr int gather_ozp_smem() {
-  return 2 * kSl * kGA + 3 * kGBStage + 6 * kGRaw;
+  return 2 * kSl * kGA + kPOS * kGBStage + kPRS * kGRaw;
 }
 
 __global__ void __launch_bounds__(kPThreads, 1)
@@ -1043,7 +1054,7 @@ k_gather_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
              const double* __restrict__ rows, const int32_t* __restrict__ pix,
              const int16_t* __restrict__ sub_exp, const double* __restrict__ grid,
              int64_t grid_ld, double* __restrict__ out, int64_t N, int nrhs, mma::GatherEpi ep) {
-  constexpr int RS = 6, OS = 3;                    // raw / operand stages
+  constexpr int RS = kPRS, OS = kPOS;              // raw / operand stages
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ uint64_t raw_full[RS], raw_empty[RS], op_ready[OS], op_free[OS];
   __shared__ uint64_t acc_full[2], acc_empty[2], g_full[2], g_empty[2];
