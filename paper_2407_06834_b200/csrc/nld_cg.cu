@@ -29,7 +29,7 @@ namespace nld {
 
 namespace {
 
-constexpr int kRB = 296;   // reduction blocks (2 per SM)
+constexpr int kRB = 148 * 8;   // reduction blocks (8 per SM: enough loads in flight)
 constexpr int kRT = 256;
 constexpr int kMaxK = 4;
 
@@ -61,7 +61,8 @@ struct CgPtr {
 };
 
 __device__ __forceinline__ double dinv_at(const CgPtr& c, const RhsScal& s, int64_t i) {
-  if (c.prec == NLD_PREC_JACOBI) return 1.0 / (s.lam + s.mu * c.eta[i]);
+  // correctly rounded reciprocal without the division's slow path
+  if (c.prec == NLD_PREC_JACOBI) return __drcp_rn(s.lam + s.mu * c.eta[i]);
   if (c.prec == NLD_PREC_L2) {
     const double pa = s.lam + s.mu * c.eta[i];
     const double row_sq = c.eta2[i] / (double)(c.L * c.L);
@@ -103,35 +104,58 @@ k_cg_reduce(CgPtr c, const RhsScal* __restrict__ sc, const double* __restrict__ 
   const int g = tid / nr;
   const RhsScal s = sc[r];
   double acc[kMaxK] = {0.0, 0.0, 0.0, 0.0};
-  if (live) {
-    for (int64_t i = blockIdx.x * (int64_t)grp + g; i < c.N; i += (int64_t)gridDim.x * grp) {
-      const int64_t e = i * nr + r;
-      if (MODE == RED_SUM) {
-        acc[0] += vecA[e];
-      } else if (MODE == RED_NORM2) {
-        const double a = vecA[e];
-        acc[0] += a * a;
-      } else if (MODE == RED_PQ) {
-        const double p = c.p[e], q = c.q[e];
-        acc[0] += q;
-        acc[1] += p * q;
-        acc[2] += p;
-      } else if (MODE == RED_UPDATE || MODE == RED_PREC) {
-        double rr = c.r[e];
-        if (MODE == RED_UPDATE && s.active) {
-          c.x[e] += s.alpha * c.p[e];
-          rr -= s.alpha * (c.q[e] - s.mq);
-          c.r[e] = rr;
-        }
-        const double zt = dinv_at(c, s, i) * rr;
-        acc[0] += rr * rr;
-        acc[1] += zt;
-        acc[2] += rr * zt;
-        acc[3] += rr;
-      } else if (MODE == RED_RESID) {
-        const double d = c.b[e] - (c.t[e] - s.mq);
-        acc[0] += d * d;
+  // one element (pixel i, rhs r) per step, four steps' loads issued together
+  // (memory-level parallelism); the accumulation order is the plain
+  // sequential one, so the result does not depend on the unrolling
+  auto body = [&](int64_t i, double va, double vr, double vp, double vq, double vb, double vt) {
+    const int64_t e = i * nr + r;
+    if (MODE == RED_SUM) {
+      acc[0] += va;
+    } else if (MODE == RED_NORM2) {
+      acc[0] += va * va;
+    } else if (MODE == RED_PQ) {
+      acc[0] += vq;
+      acc[1] += vp * vq;
+      acc[2] += vp;
+    } else if (MODE == RED_UPDATE || MODE == RED_PREC) {
+      double rr = vr;
+      if (MODE == RED_UPDATE && s.active) {
+        c.x[e] += s.alpha * vp;
+        rr -= s.alpha * (vq - s.mq);
+        c.r[e] = rr;
       }
+      const double zt = dinv_at(c, s, i) * rr;
+      acc[0] += rr * rr;
+      acc[1] += zt;
+      acc[2] += rr * zt;
+      acc[3] += rr;
+    } else if (MODE == RED_RESID) {
+      const double d = vb - (vt - s.mq);
+      acc[0] += d * d;
+    }
+  };
+  auto load = [&](int64_t i, double& va, double& vr, double& vp, double& vq, double& vb,
+                  double& vt) {
+    const int64_t e = i * nr + r;
+    if (MODE == RED_SUM || MODE == RED_NORM2) va = vecA[e];
+    if (MODE == RED_PQ || MODE == RED_UPDATE) { vp = c.p[e]; vq = c.q[e]; }
+    if (MODE == RED_UPDATE || MODE == RED_PREC) vr = c.r[e];
+    if (MODE == RED_RESID) { vb = c.b[e]; vt = c.t[e]; }
+  };
+  if (live) {
+    const int64_t stride = (int64_t)gridDim.x * grp;
+    int64_t i = blockIdx.x * (int64_t)grp + g;
+    for (; i + 3 * stride < c.N; i += 4 * stride) {
+      double va[4] = {}, vr[4] = {}, vp[4] = {}, vq[4] = {}, vb[4] = {}, vt[4] = {};
+#pragma unroll
+      for (int u = 0; u < 4; ++u) load(i + u * stride, va[u], vr[u], vp[u], vq[u], vb[u], vt[u]);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) body(i + u * stride, va[u], vr[u], vp[u], vq[u], vb[u], vt[u]);
+    }
+    for (; i < c.N; i += stride) {
+      double va = 0, vr = 0, vp = 0, vq = 0, vb = 0, vt = 0;
+      load(i, va, vr, vp, vq, vb, vt);
+      body(i, va, vr, vp, vq, vb, vt);
     }
   }
   __shared__ double sh[kMaxK][kRT];
@@ -180,16 +204,35 @@ __global__ void k_cg_resid0(CgPtr c, const RhsScal* __restrict__ sc, int warm) {
 }
 
 __global__ void k_cg_direction(CgPtr c, const RhsScal* __restrict__ sc, int first) {
-  // z = Pi(D^-1 r) (or r), p = z + beta p
-  const int64_t total = c.N * c.nrhs;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = e / c.nrhs;
-    const RhsScal s = sc[e - i * c.nrhs];
-    if (!s.active) continue;
-    const double r = c.r[e];
-    const double z = (c.prec == NLD_PREC_NONE) ? r : dinv_at(c, s, i) * r - s.mz;
-    c.p[e] = first ? z : z + s.beta * c.p[e];
+  // z = Pi(D^-1 r) (or r), p = z + beta p.  Thread layout as in k_cg_reduce:
+  // a fixed rhs per thread (its scalars in registers), pixels strided, four
+  // pixels' loads in flight per step
+  const int nr = c.nrhs;
+  const int grp = blockDim.x / nr;
+  if ((int)threadIdx.x >= grp * nr) return;
+  const int r = threadIdx.x % nr, g = threadIdx.x / nr;
+  const RhsScal s = sc[r];
+  if (!s.active) return;
+  const int64_t stride = (int64_t)gridDim.x * grp;
+  auto one = [&](int64_t i, double rv, double pv) {
+    const double z = (c.prec == NLD_PREC_NONE) ? rv : dinv_at(c, s, i) * rv - s.mz;
+    c.p[i * nr + r] = first ? z : z + s.beta * pv;
+  };
+  int64_t i = blockIdx.x * (int64_t)grp + g;
+  for (; i + 3 * stride < c.N; i += 4 * stride) {
+    double rv[4], pv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t e = (i + u * stride) * nr + r;
+      rv[u] = c.r[e];
+      pv[u] = first ? 0.0 : c.p[e];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) one(i + u * stride, rv[u], pv[u]);
+  }
+  for (; i < c.N; i += stride) {
+    const int64_t e = i * nr + r;
+    one(i, c.r[e], first ? 0.0 : c.p[e]);
   }
 }
 
