@@ -1043,6 +1043,9 @@ constexpr int kPThreads = 32 * (kPEpi + 6);
 #define NLD_GP_OS 3
 #endif
 constexpr int kPRS = NLD_GP_RS, kPOS = NLD_GP_OS;   // raw / operand stages
+#ifndef NLD_GP_GTMEM
+#define NLD_GP_GTMEM 1      // G digits copied to TMEM per item (UMMA A from TMEM)
+#endif
 
 __host__ __device__ constexpr int gather_ozp_smem() {
   return 2 * kSl * kGA + kPOS * kGBStage + kPRS * kGRaw;
@@ -1097,6 +1100,9 @@ k_gather_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
   __syncthreads();
   umma::fence_after();
   const uint32_t tmem = taddr_s;
+#ifdef NLD_OZ_PROF
+  const long long t_role = clock64();
+#endif
 
   if (warp == kPLoader) {
     // ---------------------------------------------------------------- loader
@@ -1109,7 +1115,7 @@ k_gather_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
       const int ntile = (sd.count + kGTile - 1) / kGTile;
       for (int tl = 0; tl < ntile; ++tl, ++gt) {
         const int s = gt % RS;
-        if (gt >= RS) umma::mbar_wait(&raw_empty[s], ((gt / RS) - 1) & 1);
+        if (gt >= RS) OZW(0, umma::mbar_wait(&raw_empty[s], ((gt / RS) - 1) & 1));
         const int j0 = tl * kGTile, cn = min(kGTile, sd.count - j0);
         const double* src = rw + (int64_t)j0 * 24;
         uint8_t* dst = sRaw + s * kGRaw;
@@ -1130,11 +1136,29 @@ k_gather_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
       const int gs = k & 1;
       const SubDev sd = subs[item_sub(k)];
       const int ntile = (sd.count + kGTile - 1) / kGTile;
-      umma::mbar_wait(&g_full[gs], (k >> 1) & 1);
+      OZW(9, umma::mbar_wait(&g_full[gs], (k >> 1) & 1));
+#if NLD_GP_GTMEM
+      // item k's G digits: shared-memory staging -> TMEM (the UMMA A operand,
+      // read from TMEM instead of shared memory by every tile's 12 UMMAs).
+      // tcgen05.cp runs in issue order behind item k-1's UMMAs, so the copy
+      // never overwrites digits still being read; its commit frees the staging
+      umma::fence_after();
+      if (lane == 0) {
+        const uint32_t aB = umma::smem_u32(sGA + gs * kSl * kGA);
+#pragma unroll
+        for (int p = 0; p < kSl; ++p)
+#pragma unroll
+          for (int ks = 0; ks < 2; ++ks)
+            umma::tmem_cp_128x256b(tmem + (uint32_t)(kGTmemA0 + p * 16 + ks * 8),
+                                   umma::make_sdesc(aB + p * kGA + ks * 256, 128, 512));
+        umma::commit(&g_empty[gs]);
+      }
+      __syncwarp();
+#endif
       for (int tl = 0; tl < ntile; ++tl, ++gt) {
         const int st = gt % OS, ab = gt & 1;
-        if (gt >= 2) umma::mbar_wait(&acc_empty[ab], ((gt >> 1) - 1) & 1);
-        umma::mbar_wait(&op_ready[st], (gt / OS) & 1);
+        if (gt >= 2) OZW(1, umma::mbar_wait(&acc_empty[ab], ((gt >> 1) - 1) & 1));
+        OZW(2, umma::mbar_wait(&op_ready[st], (gt / OS) & 1));
         umma::fence_after();
         if (lane == 0) {
           const uint32_t aB = umma::smem_u32(sGA + gs * kSl * kGA);
@@ -1148,15 +1172,24 @@ k_gather_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
           for (int p = 0; p < kSl; ++p)
 #pragma unroll
             for (int ks = 0; ks < 2; ++ks) {
-              const uint64_t da = umma::make_sdesc(aB + p * kGA + ks * 256, 128, 512);
               const uint64_t db = umma::make_sdesc(bB + ks * 256, 128, 512);
+#if NLD_GP_GTMEM
+              umma::mma_i8_ta(dcol + (uint32_t)(p * kGTile),
+                              tmem + (uint32_t)(kGTmemA0 + p * 16 + ks * 8), db,
+                              umma::idesc_i8(kRows, (kSl - p) * kGTile),
+                              (ks > 0 || p > 0) ? 1u : 0u);
+#else
+              const uint64_t da = umma::make_sdesc(aB + p * kGA + ks * 256, 128, 512);
               umma::mma_i8(dcol + (uint32_t)(p * kGTile), da, db,
                            umma::idesc_i8(kRows, (kSl - p) * kGTile), (ks > 0 || p > 0) ? 1u : 0u);
+#endif
             }
 #endif
           umma::commit(&op_free[st]);
           umma::commit(&acc_full[ab]);
+#if !NLD_GP_GTMEM
           if (tl == ntile - 1) umma::commit(&g_empty[gs]);   // item k's G digits released
+#endif
         }
         __syncwarp();
       }
@@ -1181,7 +1214,7 @@ k_gather_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
         eCm = max(eCm, (int)ex[16 + q]);
       }
       const double syB = pow2(46 - eBm), syC = pow2(-eCm);
-      if (k >= 2) umma::mbar_wait(&g_empty[gs], ((k >> 1) - 1) & 1);
+      if (k >= 2) OZW(5, umma::mbar_wait(&g_empty[gs], ((k >> 1) - 1) & 1));
       {
         // G digits: row m = (r, a) = t, its 64 (b, c) from the support box
         const int m = t, ga = m & 7, gr = m >> 3;
@@ -1194,10 +1227,15 @@ k_gather_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
                       ((int64_t)p0 * wd.box_w[1] + p1) * wd.box_w[2] + p2];
         };
         double mx = 0.0;
-#pragma unroll 16
 #ifndef NLD_EXP_PNOG
+#pragma unroll 16
         for (int i = 0; i < 64; ++i) mx = fmax(mx, fabs(gval(i)));
 #endif
+        // one scale per rhs (max over its 8 a-rows, adjacent lanes): the
+        // epilogue scales once per output, after the sum over a
+        mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+        mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+        mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 4));
         const int eG = max(-900, exp_bound(mx));
         const double sg = pow2(46 - eG);
         tsc[gs][m] = ldexp(1.0, eG + eBm + eCm - 52);   // combine6 carries 2^24
@@ -1219,8 +1257,8 @@ k_gather_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
       const int n = (t >> 5) * 8 + (lane & 7), kq = lane >> 3;
       for (int tl = 0; tl < ntile; ++tl, ++gt) {
         const int s = gt % RS, st = gt % OS;
-        umma::mbar_wait(&raw_full[s], (gt / RS) & 1);
-        if (gt >= OS) umma::mbar_wait(&op_free[st], ((gt / OS) - 1) & 1);
+        OZW(3, umma::mbar_wait(&raw_full[s], (gt / RS) & 1));
+        if (gt >= OS) OZW(4, umma::mbar_wait(&op_free[st], ((gt / OS) - 1) & 1));
 #ifndef NLD_EXP_PNOSLICE
         const double* R = reinterpret_cast<const double*>(sRaw + s * kGRaw) + n * kGRowS;
         const bool ok = tl * kGTile + n < sd.count;
@@ -1266,7 +1304,7 @@ k_gather_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
     auto epi_load = [&](int cnt, int rgn, int tt, int gg) {
       EpiIn e;
       const int sn = gg % RS;
-      umma::mbar_wait(&raw_full[sn], (gg / RS) & 1);
+      OZW(7, umma::mbar_wait(&raw_full[sn], (gg / RS) & 1));
       const int32_t* spn = reinterpret_cast<const int32_t*>(sRaw + sn * kGRaw + kGTile * kGRowS * 8);
 #pragma unroll
       for (int q = 0; q < kPG; ++q) {
@@ -1304,7 +1342,7 @@ k_gather_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
       // this lane's rhs coefficients, once per item
       const double lam_r = (ep.mode == mma::kGatherFinal && ep.coef) ? ep.coef[2 * (rg + r)] : 0.0;
       const double mu_r = (ep.mode == mma::kGatherFinal && ep.coef) ? ep.coef[2 * (rg + r) + 1] : 0.0;
-      umma::mbar_wait(&g_full[gs], (k >> 1) & 1);
+      OZW(6, umma::mbar_wait(&g_full[gs], (k >> 1) & 1));
       const double ts = tsc[gs][mrow];
       for (int tl = 0; tl < ntile; ++tl, ++gt) {
         const int ab = gt & 1, s = gt % RS;
@@ -1314,7 +1352,7 @@ k_gather_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
         else if (k + 1 < nitems) nxt = epi_load(cnt_next, ((k + 1) % ngroups) * 16, 0, gt + 1);
         const int64_t* oe = cur.oe;
         const double *prev = cur.prev, *vx = cur.vx, *et = cur.et;
-        umma::mbar_wait(&acc_full[ab], (gt >> 1) & 1);
+        OZW(8, umma::mbar_wait(&acc_full[ab], (gt >> 1) & 1));
         umma::fence_after();
         double ysum[kPG];
 #pragma unroll
@@ -1341,7 +1379,7 @@ k_gather_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
 #else
 #pragma unroll
           for (int i = 0; i < 8; ++i)
-            v8[i] = combine6(dv, i) * ts * R[(nb + i) * kGRowS + a];
+            v8[i] = combine6(dv, i) * R[(nb + i) * kGRowS + a];
 #endif
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
@@ -1361,7 +1399,7 @@ k_gather_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
             const bool up = lane & 1;
             const double send = up ? v8[0] : v8[1];
             const double keep = up ? v8[1] : v8[0];
-            ysum[q] = keep + __shfl_xor_sync(0xffffffffu, send, 1);
+            ysum[q] = (keep + __shfl_xor_sync(0xffffffffu, send, 1)) * ts;
           }
         }
         __syncwarp();
@@ -1390,6 +1428,11 @@ k_gather_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
       if (lane == 0) mbar_arrive(&g_empty[gs]);   // tsc[gs] no longer read
     }
   }
+#ifdef NLD_OZ_PROF
+  if (lane == 0)
+    atomicAdd(&oz_prof[24 + (warp == kPLoader ? 0 : warp == kPIssuer ? 1 : warp >= kPSl0 ? 2 : 3)],
+              (unsigned long long)(clock64() - t_role));
+#endif
   umma::fence_before();
   __syncthreads();
   if (warp == 0) umma::tmem_free<512>(tmem);

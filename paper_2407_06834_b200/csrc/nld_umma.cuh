@@ -56,6 +56,13 @@ __device__ __forceinline__ void mma_i8_ta(uint32_t tmem_d, uint32_t tmem_a, uint
       "r"(tmem_a), "l"(db), "r"(idesc), "r"(accumulate));
 }
 
+// shared memory (matrix descriptor, canonical K-major layout) -> TMEM, 128
+// rows x 256 bits: row i to lane i, 8 columns; issued by one thread and
+// ordered with this thread's tcgen05.mma (completion tracked by commit)
+__device__ __forceinline__ void tmem_cp_128x256b(uint32_t taddr, uint64_t sdesc) {
+  asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;\n" ::"r"(taddr), "l"(sdesc));
+}
+
 // 32 lanes x 32 bits, 4 consecutive columns per thread (register -> TMEM)
 __device__ __forceinline__ void tmem_st4(uint32_t taddr, uint32_t a, uint32_t b, uint32_t c,
                                          uint32_t d) {
