@@ -1162,7 +1162,8 @@ void gather_window_fast(const PlanSet& ps, const Workspace& ws, int w, int64_t N
   else if (MC == 4 && use_ozaki() && nrhs % 16 == 0 && ps.sub_exp && !getenv("NLD_OZAKI_NO_GATHER"))
     launch_gather_oz(ps, subs, ps.sub_exp + wp.sub_off * 24, ps.sub_order + wp.sub_off, nsub, ws.grid_out, ps.grid_total,
                      ep.mode == mma::kGatherStore ? ws.wout + (int64_t)w * N * nrhs : out, N, nrhs,
-                     ep, st);
+                     ep, st, ws.gdig, w < (int)ps.gcell_lo.size() ? ps.gcell_lo[w] : 0,
+                     w < (int)ps.gcell_n.size() ? ps.gcell_n[w] : 0);
   else if (MC == 4 && use_mma()) launch_gather_mma(subs, nsub, ps, ws, N, nrhs, st, ep, out);
   else launch_gather<3, MC>(subs, nsub, ps, ws, N, nrhs, st);
   const bool oz_used = wp.d == 3 && MC == 4 && use_ozaki() && nrhs % 16 == 0 && ps.sub_exp &&
@@ -1250,7 +1251,7 @@ struct EvScope {
 void ensure_workspace(nld_operator* op, const PlanSet& ps, int nrhs) {
   Workspace& ws = op->ws;
   if (ws.nrhs_cap >= nrhs && ws.grid_total >= ps.grid_total &&
-      ws.blocks_total >= ps.blocks_total)
+      ws.blocks_total >= ps.blocks_total && ws.gdig_cells >= ps.n_cells)
     return;
   double* keep_cg = ws.cg;
   int64_t keep_cap = ws.cg_cap;
@@ -1284,6 +1285,14 @@ void ensure_workspace(nld_operator* op, const PlanSet& ps, int nrhs) {
       NLD_CUDA(cudaMalloc(&ws.asm_y2, sizeof(double) * (ws.asm_cap / 8 + 1)));
     }
   }
+  {
+    // sliced gather: G digits of every cell and 16-rhs group, rebuilt per product
+    const int64_t nc = std::max(ps.n_cells, std::max(op->sets[0].n_cells, op->sets[1].n_cells));
+    if (use_ozaki() && nc > 0) {
+      NLD_CUDA(cudaMalloc(&ws.gdig, (size_t)gather_gdig_bytes() * nc * std::max(1, cap / 16)));
+      ws.gdig_cells = nc;
+    }
+  }
   ws.nrhs_cap = cap;
   ws.grid_total = gt;
   ws.blocks_total = bt;
@@ -1302,6 +1311,7 @@ void free_workspace(Workspace& ws) {
   cudaFree(ws.vt);
   cudaFree(ws.coef);
   cudaFree(ws.vmax);
+  cudaFree(ws.gdig);
   ws = Workspace();
 }
 

@@ -136,6 +136,7 @@ struct PlanSet {
   uint8_t* ydig = nullptr;       // sliced spread: Y = B (x) C digit slices per 32-node
                                  // chunk, UMMA B-operand layout (12 KB per chunk)
   int64_t* ychunk = nullptr;     // per 3-D subproblem: its first chunk in ydig
+  std::vector<int64_t> gcell_lo, gcell_n;   // per window: its cells' global range
   int shares_tables_with = -1;   // index of the plan set whose tables we use
   bool owns_tables = true;
 };
@@ -156,6 +157,8 @@ struct Workspace {
   double* asm_y2 = nullptr;
   int64_t asm_cap = 0;
   unsigned long long* vmax = nullptr;   // [nrhs_cap] sliced spread: max |v| bits
+  uint8_t* gdig = nullptr;       // sliced gather: per (cell, 16-rhs group) G digits + exponents
+  int64_t gdig_cells = 0;
   // persistent CG vectors (x, r, p, q, b, t): [6][cg_cap]
   double* cg = nullptr;
   int64_t cg_cap = 0;
@@ -212,7 +215,10 @@ namespace mma { struct GatherEpi; }
 void launch_gather_oz(const PlanSet& ps, const SubDev* subs, const int16_t* ex,
                       const int32_t* order, unsigned nsub, const double* grid, int64_t grid_ld,
                       double* out, int64_t N, int nrhs, const mma::GatherEpi& ep,
-                      cudaStream_t st);
+                      cudaStream_t st, uint8_t* gdig = nullptr, int64_t cell_lo = 0,
+                      int64_t ncell = 0);
+// bytes per (cell, 16-rhs group) of precomputed gather G digits
+int64_t gather_gdig_bytes();
 void free_planset(PlanSet& ps);
 void ensure_workspace(nld_operator* op, const PlanSet& ps, int nrhs);
 void free_workspace(Workspace& ws);

@@ -1016,6 +1016,55 @@ k_gather_oz(const SubDev* __restrict__ subs, const CellDev* __restrict__ cells,
   if (warp == 0) umma::tmem_free<kGTmemCols>(tmem);
 }
 
+// ---- G digits of every cell, once per product (persistent gather) ----------
+// Per (cell, 16-rhs group): the 128 rows (r, a) x 64 (b, c) of the support-box
+// grid at the cell, scaled per rhs (max over its 8 a-rows and 64 values) and
+// cut into six digit slices in the UMMA A-operand layout (canonical K-major,
+// 6 x 8 KB), followed by the 128 row exponents (int32).  Massively parallel
+// (every cell at once), so the gather's per-subproblem G setup becomes one
+// 48 KB TMA load that the pipeline prefetches a subproblem ahead.
+constexpr int kGdigBytes = kSl * kGA + kRows * 4;
+
+__global__ void __launch_bounds__(kRows)
+k_gdig(const CellDev* __restrict__ cells, const WinDev* __restrict__ wins,
+       const double* __restrict__ grid, int64_t grid_ld, int64_t cell_lo, int ngroups,
+       uint8_t* __restrict__ gdig) {
+  const int64_t cell = cell_lo + blockIdx.x;
+  const int grp = blockIdx.y, rg = grp * 16;
+  const CellDev cd = cells[cell];
+  const WinDev wd = wins[cd.win];
+  const int m = threadIdx.x, ga = m & 7, gr = m >> 3;
+  auto gval = [&](int bc) -> double {
+    int p0 = cd.cc[0] + ga, p1 = cd.cc[1] + (bc >> 3), p2 = cd.cc[2] + (bc & 7);
+    if (p0 >= wd.box_w[0]) p0 -= wd.box_w[0];
+    if (p1 >= wd.box_w[1]) p1 -= wd.box_w[1];
+    if (p2 >= wd.box_w[2]) p2 -= wd.box_w[2];
+    return grid[(int64_t)(rg + gr) * grid_ld + wd.grid_off +
+                ((int64_t)p0 * wd.box_w[1] + p1) * wd.box_w[2] + p2];
+  };
+  double g[64];
+  double mx = 0.0;
+#pragma unroll
+  for (int i = 0; i < 64; ++i) {
+    g[i] = gval(i);
+    mx = fmax(mx, fabs(g[i]));
+  }
+  mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+  mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+  mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 4));
+  const int eG = max(-900, exp_bound(mx));
+  const double sg = pow2(46 - eG);
+  uint8_t* base = gdig + (cell * ngroups + grp) * (int64_t)kGdigBytes;
+#pragma unroll
+  for (int kb = 0; kb < 4; ++kb) {
+    uint32_t lo[16], hi[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) slice1(g[kb * 16 + i], sg, lo[i], hi[i]);
+    store16(lo, hi, base + canon64(m, kb * 16), kGA);
+  }
+  reinterpret_cast<int32_t*>(base + kSl * kGA)[m] = eG;
+}
+
 // ---- persistent gather -----------------------------------------------------
 // One CTA per SM walks a list of work items (subproblem, rhs group): the
 // subproblems in descending node count, dealt to the CTAs in snake order so
@@ -1056,13 +1105,15 @@ k_gather_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
              const CellDev* __restrict__ cells, const WinDev* __restrict__ wins,
              const double* __restrict__ rows, const int32_t* __restrict__ pix,
              const int16_t* __restrict__ sub_exp, const double* __restrict__ grid,
-             int64_t grid_ld, double* __restrict__ out, int64_t N, int nrhs, mma::GatherEpi ep) {
+             int64_t grid_ld, double* __restrict__ out, int64_t N, int nrhs, mma::GatherEpi ep,
+             const uint8_t* __restrict__ gdig) {
   constexpr int RS = kPRS, OS = kPOS;              // raw / operand stages
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ uint64_t raw_full[RS], raw_empty[RS], op_ready[OS], op_free[OS];
   __shared__ uint64_t acc_full[2], acc_empty[2], g_full[2], g_empty[2];
   __shared__ uint32_t taddr_s;
   __shared__ double tsc[2][kRows];
+  __shared__ __align__(16) int32_t gexs[2][kRows];   // precomputed-G row exponents
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   uint8_t* const sGA = smem;                                    // [2][6][128 x 64]
@@ -1091,7 +1142,7 @@ k_gather_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
     for (int k = 0; k < 2; ++k) {
       umma::mbar_init(&acc_full[k], 1);
       umma::mbar_init(&acc_empty[k], kPEpi);
-      umma::mbar_init(&g_full[k], kPSlicers);
+      umma::mbar_init(&g_full[k], gdig ? 1 : kPSlicers);   // TMA arrival / slicer warps
       umma::mbar_init(&g_empty[k], 1 + kPEpi);     // last MMA commit + epilogue warps
     }
     umma::mbar_fence_init();
@@ -1214,6 +1265,19 @@ k_gather_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
         eCm = max(eCm, (int)ex[16 + q]);
       }
       const double syB = pow2(46 - eBm), syC = pow2(-eCm);
+      if (gdig) {
+        // precomputed G digits (k_gdig): one thread loads them with TMA into
+        // the staging buffer, a subproblem ahead of the MMAs
+        if (t == 0) {
+          if (k >= 2) OZW(5, umma::mbar_wait(&g_empty[gs], ((k >> 1) - 1) & 1));
+          const uint8_t* src = gdig + ((int64_t)sd.cell * ngroups + (k % ngroups)) * kGdigBytes;
+          umma::mbar_arrive_expect_tx(&g_full[gs], (uint32_t)(kSl * kGA + kRows * 4));
+#pragma unroll
+          for (int p = 0; p < kSl; ++p)
+            umma::bulk_g2s(sGA + gs * kSl * kGA + p * kGA, src + p * kGA, kGA, &g_full[gs]);
+          umma::bulk_g2s(&gexs[gs][0], src + kSl * kGA, kRows * 4, &g_full[gs]);
+        }
+      } else {
       if (k >= 2) OZW(5, umma::mbar_wait(&g_empty[gs], ((k >> 1) - 1) & 1));
       {
         // G digits: row m = (r, a) = t, its 64 (b, c) from the support box
@@ -1250,6 +1314,7 @@ k_gather_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
         umma::fence_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive(&g_full[gs]);
+      }
       }
       // Y digits of each tile: 8 nodes per warp, node = lane & 7, bc quarter
       // kq = lane >> 3, so each quarter-warp's 16-byte stores cover one
@@ -1343,7 +1408,20 @@ k_gather_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
       const double lam_r = (ep.mode == mma::kGatherFinal && ep.coef) ? ep.coef[2 * (rg + r)] : 0.0;
       const double mu_r = (ep.mode == mma::kGatherFinal && ep.coef) ? ep.coef[2 * (rg + r) + 1] : 0.0;
       OZW(6, umma::mbar_wait(&g_full[gs], (k >> 1) & 1));
-      const double ts = tsc[gs][mrow];
+      double ts;
+      if (gdig) {
+        // T scale of the row: G exponent (per rhs) + the subproblem's Y exponents
+        const int16_t* exk = sub_exp + (int64_t)item_sub(k) * kExpPerSub;
+        int eBm = -2000, eCm = -2000;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          eBm = max(eBm, (int)exk[8 + q]);
+          eCm = max(eCm, (int)exk[16 + q]);
+        }
+        ts = ldexp(1.0, gexs[gs][mrow] + eBm + eCm - 52);
+      } else {
+        ts = tsc[gs][mrow];
+      }
       for (int tl = 0; tl < ntile; ++tl, ++gt) {
         const int ab = gt & 1, s = gt % RS;
         const double* R = reinterpret_cast<const double*>(sRaw + s * kGRaw);
@@ -1477,6 +1555,20 @@ int16_t* ozaki_exponents(PlanSet& ps, cudaStream_t st) {
   NLD_CUDA(cudaMalloc(&ps.sub_order, sizeof(int32_t) * ord.size()));
   NLD_CUDA(cudaMemcpyAsync(ps.sub_order, ord.data(), sizeof(int32_t) * ord.size(),
                            cudaMemcpyHostToDevice, st));
+  // per window: the global index range of its cells (contiguous per window)
+  ps.gcell_lo.assign(ps.win.size(), 0);
+  ps.gcell_n.assign(ps.win.size(), 0);
+  for (size_t w = 0; w < ps.win.size(); ++w) {
+    const WinPlan& wp = ps.win[w];
+    if (wp.d != 3 || wp.n_subs == 0) continue;
+    int64_t lo = INT64_MAX, hi = -1;
+    for (int64_t i = 0; i < wp.n_subs; ++i) {
+      lo = std::min<int64_t>(lo, h[wp.sub_off + i].cell);
+      hi = std::max<int64_t>(hi, h[wp.sub_off + i].cell);
+    }
+    ps.gcell_lo[w] = lo;
+    ps.gcell_n[w] = hi - lo + 1;
+  }
   // precomputed Y digits for the spread (12 KB per 32-node chunk) when they
   // fit comfortably: at most half of the free memory (NLD_SPREAD_PREY=0: off)
   const char* py = getenv("NLD_SPREAD_PREY");
@@ -1526,10 +1618,12 @@ void launch_spread_oz(const PlanSet& ps, const SubDev* subs, const int16_t* ex,
   NLD_CUDA(cudaGetLastError());
 }
 
+int64_t gather_gdig_bytes() { return oz::kGdigBytes; }
+
 void launch_gather_oz(const PlanSet& ps, const SubDev* subs, const int16_t* ex,
                       const int32_t* order, unsigned nsub, const double* grid, int64_t grid_ld,
                       double* out, int64_t N, int nrhs, const mma::GatherEpi& ep,
-                      cudaStream_t st) {
+                      cudaStream_t st, uint8_t* gdig, int64_t cell_lo, int64_t ncell) {
   static int persist = -1;
   if (persist < 0) {
     const char* e = getenv("NLD_GATHER_PERSIST");
@@ -1548,9 +1642,21 @@ void launch_gather_oz(const PlanSet& ps, const SubDev* subs, const int16_t* ex,
       attr_p = true;
     }
     const unsigned grid_n = std::min<unsigned>(nsub, (unsigned)sms);
+    static int pre = -1;
+    if (pre < 0) {
+      const char* e = getenv("NLD_GATHER_PREG");
+      pre = (e && e[0] == '0') ? 0 : 1;
+    }
+    const bool use_g = pre && gdig && ncell > 0;
+    if (use_g) {
+      oz::k_gdig<<<dim3((unsigned)ncell, (unsigned)(nrhs / 16)), oz::kRows, 0, st>>>(
+          ps.cells, ps.wdev, grid, grid_ld, cell_lo, nrhs / 16, gdig);
+      NLD_CUDA(cudaGetLastError());
+    }
     oz::k_gather_ozp<<<grid_n, oz::kPThreads, smem_p, st>>>(subs, order, (int)nsub, ps.cells,
                                                             ps.wdev, ps.rows, ps.pix, ex, grid,
-                                                            grid_ld, out, N, nrhs, ep);
+                                                            grid_ld, out, N, nrhs, ep,
+                                                            use_g ? gdig : nullptr);
     NLD_CUDA(cudaGetLastError());
     return;
   }
