@@ -1025,7 +1025,7 @@ void spread_window_fast(const PlanSet& ps, const Workspace& ws, int w, const dou
     if (use_ozaki() && nrhs % 16 == 0 && ps.sub_exp && !getenv("NLD_OZAKI_NO_SPREAD")) {
       launch_spread_oz(ps, subs, ps.sub_exp + wp.sub_off * 24,
                        ps.ychunk ? ps.ychunk + wp.sub_off : nullptr, nsub, ws.vmax, vt, nrhs,
-                       ws.blocks, st);
+                       ws.blocks, st, ps.sub_order ? ps.sub_order + wp.sub_off : nullptr);
       if (getenv("NLD_OZ_PROF_PRINT")) ozaki_prof_dump("spread", st);
       if (getenv("NLD_OZAKI_DEBUG")) {
         // compare with the fp64 DMMA spread of the same window (debug only)

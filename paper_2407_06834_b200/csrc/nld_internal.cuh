@@ -208,7 +208,8 @@ bool use_ozaki();
 int16_t* ozaki_exponents(PlanSet& ps, cudaStream_t st);
 void launch_spread_oz(const PlanSet& ps, const SubDev* subs, const int16_t* ex,
                       const int64_t* ychunk, unsigned nsub, const unsigned long long* vmax,
-                      const double* vt, int nrhs, double* blocks, cudaStream_t st);
+                      const double* vt, int nrhs, double* blocks, cudaStream_t st,
+                      const int32_t* order = nullptr);
 void ozaki_vmax(const double* vt, int64_t n, int nrhs, unsigned long long* out, cudaStream_t st);
 void ozaki_prof_dump(const char* what, cudaStream_t st);
 namespace mma { struct GatherEpi; }

@@ -619,6 +619,237 @@ k_spread_ydig(const SubDev* __restrict__ subs, const WinDev* __restrict__ wins,
   }
 }
 
+// ---- persistent spread (plan-time Y digits) ---------------------------------
+// One CTA per SM walks (subproblem, rhs group) items -- the window's
+// subproblems in descending size, dealt in snake order as in the persistent
+// gather -- so the per-subproblem fixed costs of k_spread_oz (TMEM
+// allocation, barrier set-up, pipeline fill behind the first v gathers,
+// drain, epilogue) overlap the neighbouring items: the loader and the slicers
+// stream across item boundaries, and 4 dedicated epilogue warps drain an
+// item's accumulator (releasing TMEM as soon as it is read) while the slicers
+// already cut the next item's first chunks.  The only serialisation left per
+// item is the TMEM drain (the accumulator is single-buffered: 384 of 512
+// columns).  Scales are per-thread registers (no per-item shared state).
+//   warps 0-7 slicers (X digits -> TMEM)   warp 8 UMMA issuer
+//   warp 9    loader                       warps 10-13 epilogue
+constexpr int kSPEpi0 = 10;
+constexpr int kSPThreads = 32 * 14;
+
+__global__ void __launch_bounds__(kSPThreads, 1)
+k_spread_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order, int nsub,
+             const WinDev* __restrict__ wins, const double* __restrict__ rows,
+             const int32_t* __restrict__ pix, const int16_t* __restrict__ sub_exp,
+             const uint8_t* __restrict__ ydig, const int64_t* __restrict__ ychunk,
+             const unsigned long long* __restrict__ vmax, const double* __restrict__ vt,
+             int nrhs, double* __restrict__ blocks) {
+  constexpr int RS = kPyRawStages, RB = kPyRawBytes;
+  extern __shared__ __align__(16) uint8_t smem[];
+  __shared__ uint64_t raw_full[RS], raw_empty[RS];
+  __shared__ uint64_t op_ready[kOpStages], op_free[kOpStages], acc_full, acc_empty;
+  __shared__ uint32_t taddr_s;
+  uint8_t* const raw = smem;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int ngroups = nrhs / 16;
+  const int G = (int)gridDim.x, b = (int)blockIdx.x;
+  const int rounds = nsub / G, rem = nsub % G;
+  const int my_rounds = rounds + ((rem > 0 && ((rounds & 1) ? (G - 1 - b) : b) < rem) ? 1 : 0);
+  const int nitems = my_rounds * ngroups;
+  auto item_sub = [&](int k) {
+    const int i = k / ngroups;
+    return order[i * G + ((i & 1) ? (G - 1 - b) : b)];
+  };
+
+  if (warp == 0) umma::tmem_alloc<kTmemCols>(&taddr_s);
+  if (tid == 32) {
+    for (int k = 0; k < RS; ++k) {
+      umma::mbar_init(&raw_full[k], 33);                  // 32 noinc cp.async + the bulk copy
+      umma::mbar_init(&raw_empty[k], kSlicers / 32 + 1);  // slicers + the UMMA commit
+    }
+    for (int k = 0; k < kOpStages; ++k) {
+      umma::mbar_init(&op_ready[k], kSlicers / 32);
+      umma::mbar_init(&op_free[k], 1);
+    }
+    umma::mbar_init(&acc_full, 1);
+    umma::mbar_init(&acc_empty, 4);                       // epilogue warps
+    umma::mbar_fence_init();
+  }
+  umma::fence_before();
+  __syncthreads();
+  umma::fence_after();
+  const uint32_t tmem = taddr_s;
+
+  if (warp == kLoaderWarp) {
+    // ---------------------------------------------------------------- loader
+    int g = 0;
+    for (int k = 0; k < nitems; ++k) {
+      const int si = item_sub(k);
+      const SubDev sd = subs[si];
+      const WinDev wd = wins[sd.win];
+      const double* __restrict__ rw = rows + wd.row_off + (sd.start - wd.node_off) * 24;
+      const int32_t* __restrict__ pw = pix + sd.start;
+      const uint8_t* yd = ydig + ychunk[si] * (int64_t)kYChunkBytes;
+      const int rg = (k % ngroups) * 16;
+      const int nchunk = (sd.count + kChunk - 1) / kChunk;
+      int32_t px = (lane < sd.count) ? __ldg(pw + lane) : 0;
+      for (int c = 0; c < nchunk; ++c, ++g) {
+        const int s = g % RS;
+        // next chunk's pixel index, loaded before this chunk's copies
+        const int jn = (c + 1) * kChunk + lane;
+        const int32_t px_next = (c + 1 < nchunk && jn < sd.count) ? __ldg(pw + jn) : 0;
+        if (g >= RS) umma::mbar_wait(&raw_empty[s], ((g / RS) - 1) & 1);
+        uint8_t* dst = raw + s * RB;
+        const int j0 = c * kChunk, cn = min(kChunk, sd.count - j0);
+        if (lane == 0) {
+          umma::mbar_arrive_expect_tx(&raw_full[s], kYChunkBytes);
+          umma::bulk_g2s(dst + kPyY, yd + (int64_t)c * kYChunkBytes, kYChunkBytes, &raw_full[s]);
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int nd = q * 4 + (lane >> 3), pc = lane & 7;
+          const int32_t pxn = __shfl_sync(0xffffffffu, px, nd);
+          if (nd < cn)
+            cp_async16(dst + kPyA + nd * 128 + pc * 16,
+                       vt + (int64_t)(uint32_t)pxn * nrhs + rg + 2 * pc);
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int nd = q * 8 + (lane >> 2), pc = lane & 3;
+          if (nd < cn) cp_async16(dst + nd * 64 + pc * 16, rw + (int64_t)(j0 + nd) * 24 + 2 * pc);
+        }
+        cp_async_mbar_arrive(&raw_full[s]);
+        px = px_next;
+      }
+    }
+  } else if (warp == kIssuerWarp) {
+    // ---------------------------------------------------------------- issuer
+    int g = 0;
+    for (int k = 0; k < nitems; ++k) {
+      const SubDev sd = subs[item_sub(k)];
+      const int nchunk = (sd.count + kChunk - 1) / kChunk;
+      if (k > 0) umma::mbar_wait(&acc_empty, (k - 1) & 1);   // previous item drained
+      for (int c = 0; c < nchunk; ++c, ++g) {
+        const int st = g % kOpStages, s = g % RS;
+        umma::mbar_wait(&op_ready[st], (g / kOpStages) & 1);
+        umma::mbar_wait(&raw_full[s], (g / RS) & 1);
+        umma::fence_after();
+        if (lane == 0) {
+          const uint32_t bB = umma::smem_u32(raw + s * RB + kPyY);
+          const uint32_t xa = tmem + (uint32_t)(kXTmem0 + st * kSl * 8);
+#pragma unroll
+          for (int p = 0; p < kSl; ++p) {
+#pragma unroll
+            for (int q0 = 0; q0 < kSl - p; q0 += 4) {
+              const int nq = min(4, kSl - p - q0);
+              const uint64_t db = umma::make_sdesc(bB + q0 * kBBytes, 128, 256);
+              umma::mma_i8_ta(tmem + (uint32_t)((p + q0) * 64), xa + (uint32_t)(p * 8), db,
+                              umma::idesc_i8(kRows, nq * 64), (c > 0 || p > 0) ? 1u : 0u);
+            }
+          }
+          umma::commit(&op_free[st]);
+          umma::commit(&raw_empty[s]);
+          if (c == nchunk - 1) umma::commit(&acc_full);
+        }
+        __syncwarp();
+      }
+    }
+  } else if (warp < kIssuerWarp) {
+    // --------------------------------------------------------------- slicers
+    const int m = tid & 127, h = tid >> 7;
+    const int a = m >> 4, r = m & 15;
+    int g = 0;
+    for (int k = 0; k < nitems; ++k) {
+      const int si = item_sub(k);
+      const SubDev sd = subs[si];
+      const int rg = (k % ngroups) * 16;
+      const int nchunk = (sd.count + kChunk - 1) / kChunk;
+      // X row scale: the rhs's max |v| times the subproblem's max |A_a|
+      const int ev = max(-900, exp_bound(__longlong_as_double((long long)vmax[rg + r])));
+      const double sx = pow2(46 - ev) * pow2(-(int)sub_exp[(int64_t)si * kExpPerSub + a]);
+      for (int c = 0; c < nchunk; ++c, ++g) {
+        const int st = g % kOpStages, s = g % RS;
+        umma::mbar_wait(&raw_full[s], (g / RS) & 1);
+        if (g >= kOpStages) umma::mbar_wait(&op_free[st], ((g / kOpStages) - 1) & 1);
+        const double* R = reinterpret_cast<const double*>(raw + s * RB);
+        const double* Vr = reinterpret_cast<const double*>(raw + s * RB + kPyA);
+        const int cn = min(kChunk, sd.count - c * kChunk);
+        uint32_t lo[16], hi[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const int j = h * 16 + i;
+          double x = 0.0, y = 0.0;
+          if (j < cn) {
+            x = Vr[j * 16 + r];
+            y = R[j * 8 + a] * sx;
+          }
+          slice1(x, y, lo[i], hi[i]);
+        }
+        uint32_t w4[4][6];
+#pragma unroll
+        for (int g4 = 0; g4 < 4; ++g4) pack4(lo + 4 * g4, hi + 4 * g4, w4[g4]);
+        const uint32_t xt = tmem + ((uint32_t)((m >> 5) * 32) << 16) +
+                            (uint32_t)(kXTmem0 + st * kSl * 8 + h * 4);
+#pragma unroll
+        for (int p = 0; p < kSl; ++p)
+          umma::tmem_st4(xt + (uint32_t)(p * 8), w4[0][p], w4[1][p], w4[2][p], w4[3][p]);
+        umma::tmem_wait_st();
+        umma::fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(&op_ready[st]);
+          mbar_arrive(&raw_empty[s]);
+        }
+      }
+    }
+  } else {
+    // -------------------------------------------------------------- epilogue
+    const int lg = warp & 3;
+    const int m = lg * 32 + lane;
+    const int a = m >> 4, r = m & 15;
+    const uint32_t tl = tmem + ((uint32_t)(lg * 32) << 16);
+    for (int k = 0; k < nitems; ++k) {
+      const int si = item_sub(k);
+      const SubDev sd = subs[si];
+      const int rg = (k % ngroups) * 16;
+      const int16_t* ex = sub_exp + (int64_t)si * kExpPerSub;
+      const int ev = max(-900, exp_bound(__longlong_as_double((long long)vmax[rg + r])));
+      const double rs = ldexp(1.0, ev + ex[a] - 46);
+      int eb[8], ec[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        eb[q] = ex[8 + q];
+        ec[q] = ex[16 + q];
+      }
+      umma::mbar_wait(&acc_full, k & 1);
+      umma::fence_after();
+      double* bo = blocks + (sd.block + a * 64) * nrhs + rg + r;
+#pragma unroll 1
+      for (int c0 = 0; c0 < 64; c0 += 16) {
+        uint32_t dv[kSl][16];
+#pragma unroll
+        for (int t = 0; t < kSl; ++t) umma::tmem_ld16(tl + (uint32_t)(t * 64 + c0), dv[t]);
+        umma::tmem_wait_ld();
+        if (c0 == 48) {
+          // every column read: the next item's UMMAs may overwrite the accumulator
+          umma::fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&acc_empty);
+        }
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          double acc = 0.0;
+#pragma unroll
+          for (int t = kSl - 1; t >= 0; --t) acc = fma(acc, 0.00390625, (double)(int32_t)dv[t][i]);
+          const int bc = c0 + i;
+          bo[(int64_t)bc * nrhs] = acc * rs * pow2(eb[bc >> 3] + ec[bc & 7] + 34);
+        }
+      }
+    }
+  }
+  umma::fence_before();
+  __syncthreads();
+  if (warp == 0) umma::tmem_free<kTmemCols>(tmem);
+}
+
 // ---- gather ---------------------------------------------------------------
 // T[(a, r)][j] = sum_{(b,c)} G_r[a][(b,c)] Y_j[(b,c)],  Y_j = B_j (x) C_j,
 // then y_r[j] = sum_a A_j[a] T[(a, r)][j]  (the DMMA gather's contraction,
@@ -1598,7 +1829,8 @@ int16_t* ozaki_exponents(PlanSet& ps, cudaStream_t st) {
 
 void launch_spread_oz(const PlanSet& ps, const SubDev* subs, const int16_t* ex,
                       const int64_t* ychunk, unsigned nsub, const unsigned long long* vmax,
-                      const double* vt, int nrhs, double* blocks, cudaStream_t st) {
+                      const double* vt, int nrhs, double* blocks, cudaStream_t st,
+                      const int32_t* order) {
   static bool attr = false;
   if (!attr) {
     NLD_CUDA(cudaFuncSetAttribute(oz::k_spread_oz<false>,
@@ -1609,7 +1841,23 @@ void launch_spread_oz(const PlanSet& ps, const SubDev* subs, const int16_t* ex,
                                   oz::spread_oz_py_smem()));
     attr = true;
   }
-  if (ps.ydig && ychunk)
+  static int persist = -1;
+  static int sms = 148;
+  if (persist < 0) {
+    const char* e = getenv("NLD_SPREAD_PERSIST");
+    persist = (e && e[0] == '0') ? 0 : 1;
+    int dev = 0;
+    NLD_CUDA(cudaGetDevice(&dev));
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    NLD_CUDA(cudaFuncSetAttribute(oz::k_spread_ozp, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  oz::spread_oz_py_smem()));
+  }
+  if (ps.ydig && ychunk && order && persist) {
+    const unsigned grid_n = std::min<unsigned>(nsub, (unsigned)sms);
+    oz::k_spread_ozp<<<grid_n, oz::kSPThreads, oz::spread_oz_py_smem(), st>>>(
+        subs, order, (int)nsub, ps.wdev, ps.rows, ps.pix, ex, ps.ydig, ychunk, vmax, vt, nrhs,
+        blocks);
+  } else if (ps.ydig && ychunk)
     oz::k_spread_oz<true><<<nsub, oz::kSpreadThreads, oz::spread_oz_py_smem(), st>>>(
         subs, ps.wdev, ps.rows, ps.pix, ex, ps.ydig, ychunk, vmax, vt, nrhs, blocks);
   else
