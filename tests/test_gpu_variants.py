@@ -45,6 +45,7 @@ print(json.dumps({"gamma": rel(gam[:, 0], g["gv"]), "system": rel(av[:, 0], want
 VARIANTS = {
     "default": {},
     "spread_on_the_fly_y": {"NLD_SPREAD_PREY": "0"},
+    "spread_per_subproblem": {"NLD_SPREAD_PERSIST": "0"},
     "gather_in_kernel_g": {"NLD_GATHER_PREG": "0"},
     "gather_per_subproblem": {"NLD_GATHER_PERSIST": "0"},
     "fp64_dmma": {"NLD_OZAKI": "0"},
