@@ -1479,7 +1479,11 @@ void apply_op(nld_operator* op, int which, int kind, const double* v, double* ou
     vt = ws.vt;
     ++launches;
   }
-  if (use_ozaki() && op->params.cutoff == 4 && nrhs % 16 == 0) ozaki_vmax(vt, N, nrhs, ws.vmax, st);
+  const bool sliced = use_ozaki() && op->params.cutoff == 4 && nrhs % 16 == 0;
+  if (sliced) {
+    ozaki_vmax(vt, N, nrhs, ws.vmax, st);
+    launches += 1;   // k_vmax (its reset is a memset, not a kernel)
+  }
   static int no_overlap = -1;
   if (no_overlap < 0) {
     const char* e = getenv("NLD_NO_OVERLAP");
@@ -1539,9 +1543,14 @@ void apply_op(nld_operator* op, int which, int kind, const double* v, double* ou
     for (int w = 0; w < L; ++w) gather_w(w);
   }
   for (int w = 0; w < L; ++w) {
+    // spread + gather (+ the sliced gather's per-cell G digits), assemble
+    // (three separable passes for 3-D m = 4 boxes), d convolution passes,
+    // generic-path and edge-node kernels
     const WinDev& wd = ps.wdev_h[w];
-    launches += (wd.fast && ps.win[w].n_subs ? 2 : 0) + 1 + wd.d + (wd.fast ? 0 : 2) +
-                (ps.win[w].n_edge ? 2 : 0);
+    const bool fastw = wd.fast && ps.win[w].n_subs;
+    const bool asm3 = wd.fast && wd.d == 3 && wd.S == 8 && !wd.wrap;
+    launches += (fastw ? 2 : 0) + (fastw && sliced && wd.d == 3 && ws.gdig ? 1 : 0) +
+                (asm3 ? 3 : 1) + wd.d + (wd.fast ? 0 : 2) + (ps.win[w].n_edge ? 2 : 0);
   }
   ev.mark();
   // 5. epilogue
