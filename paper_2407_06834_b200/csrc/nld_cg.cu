@@ -36,7 +36,7 @@ constexpr int kMaxK = 4;
 struct RhsScal {
   double alpha, mq, mz, beta, lam, mu, mf;
   int active;
-  int pad;
+  int sel;     // column selection: 1 = x into the mixed product input, 2 = copy t -> q
 };
 
 enum RedMode { RED_SUM = 0, RED_PQ = 1, RED_UPDATE = 2, RED_PREC = 3, RED_RESID = 4,
@@ -233,6 +233,23 @@ __global__ void k_cg_direction(CgPtr c, const RhsScal* __restrict__ sc, int firs
   for (; i < c.N; i += stride) {
     const int64_t e = i * nr + r;
     one(i, c.r[e], first ? 0.0 : c.p[e]);
+  }
+}
+
+// column selection between the CG vectors (pixel-major): mode 0 builds the
+// product input t = x for rhs awaiting their true-residual check (sel == 1)
+// and p otherwise; mode 1 copies t -> q for the rhs flagged sel == 2
+__global__ void k_cg_colsel(CgPtr c, const RhsScal* __restrict__ sc, int mode) {
+  const int nr = c.nrhs;
+  const int grp = blockDim.x / nr;
+  if ((int)threadIdx.x >= grp * nr) return;
+  const int r = threadIdx.x % nr, g = threadIdx.x / nr;
+  const int sel = sc[r].sel;
+  if (mode == 1 && sel != 2) return;
+  for (int64_t i = blockIdx.x * (int64_t)grp + g; i < c.N; i += (int64_t)gridDim.x * grp) {
+    const int64_t e = i * nr + r;
+    if (mode == 0) c.t[e] = sel == 1 ? c.x[e] : c.p[e];
+    else c.q[e] = c.t[e];
   }
 }
 
@@ -639,9 +656,88 @@ void cg_solve(nld_operator* op, const double* f, double* u, int nrhs, int64_t ld
   };
 
   std::vector<double> truer;
-  while (any_active()) {
-    matvec(c.p, c.q);
-    const auto& hpq = red.run<RED_PQ>(c, scd);
+  // The reference confirms a converged-looking iterate with an explicit
+  // residual b - A x (one extra product, linops.py:218-231).  Here that
+  // product rides in the NEXT iteration's batch: the columns of rhs awaiting
+  // the check carry x instead of p (columns are independent products), so the
+  // check costs no product of its own.  Only when the check fails (the rhs
+  // must continue) is its deferred direction formed and an extra product run.
+  // Iterates, stopping decisions and histories are the reference's.
+  std::vector<int> pending(nrhs, 0);
+  std::vector<double> save_rzn(nrhs, 0.0), save_mz(nrhs, 0.0);
+  auto any_pending = [&]() {
+    for (int r = 0; r < nrhs; ++r)
+      if (pending[r]) return true;
+    return false;
+  };
+  while (any_active() ) {
+    const bool pend = any_pending();
+    if (pend) {
+      for (int r = 0; r < nrhs; ++r) sc[r].sel = pending[r] ? 1 : 0;
+      push();
+      k_cg_colsel<<<kRB, kRT, 0, st>>>(c, scd, 0);
+      NLD_CUDA(cudaGetLastError());
+      matvec(c.t, c.q);
+    } else {
+      matvec(c.p, c.q);
+    }
+    auto hpq = red.run<RED_PQ>(c, scd);
+    if (pend) {
+      // true residuals of the pending rhs: q holds A x in their columns
+      for (int r = 0; r < nrhs; ++r)
+        if (pending[r]) sc[r].mq = deflate ? hpq[r * kMaxK] / dN : 0.0;
+      push();
+      CgPtr c2 = c;
+      c2.t = c.q;
+      const auto& hres = red.run<RED_RESID>(c2, scd);
+      std::vector<int> failed;
+      for (int r = 0; r < nrhs; ++r) {
+        if (!pending[r]) continue;
+        const double tr = std::sqrt(hres[r * kMaxK]) / (bnorm[r] > 0 ? bnorm[r] : 1.0);
+        H[r].back() = tr;
+        pending[r] = 0;
+        if (tr <= tol) {
+          done[r] = 1;
+          conv[r] = 1;
+          relres[r] = tr;
+          sc[r].active = 0;
+        } else if (it[r] >= maxit) {
+          done[r] = 1;
+          conv[r] = 0;
+          relres[r] = tr;
+          sc[r].active = 0;
+        } else {
+          failed.push_back(r);
+        }
+      }
+      if (!failed.empty()) {
+        // deferred direction of the rhs that must continue, then their A p
+        std::vector<int> keep(nrhs);
+        for (int r = 0; r < nrhs; ++r) {
+          keep[r] = sc[r].active;
+          sc[r].active = 0;
+          sc[r].sel = 0;
+        }
+        for (int r : failed) {
+          sc[r].mz = save_mz[r];
+          sc[r].beta = save_rzn[r] / rz[r];
+          rz[r] = save_rzn[r];
+          sc[r].active = 1;
+          sc[r].sel = 2;
+        }
+        push();
+        k_cg_direction<<<eg, 256, 0, st>>>(c, scd, 0);
+        NLD_CUDA(cudaGetLastError());
+        matvec(c.p, c.t);
+        k_cg_colsel<<<kRB, kRT, 0, st>>>(c, scd, 1);
+        NLD_CUDA(cudaGetLastError());
+        for (int r = 0; r < nrhs; ++r) sc[r].active = keep[r];
+        for (int r : failed) sc[r].active = 1;
+        push();
+        hpq = red.run<RED_PQ>(c, scd);
+      }
+      if (!any_active()) break;
+    }
     for (int r = 0; r < nrhs; ++r) {
       if (done[r]) continue;
       const double mq = deflate ? hpq[r * kMaxK] / dN : 0.0;
@@ -651,43 +747,30 @@ void cg_solve(nld_operator* op, const double* f, double* u, int nrhs, int64_t ld
                                            std::to_string(it[r]));
       sc[r].mq = mq;
       sc[r].alpha = rz[r] / pap;
+      sc[r].active = 1;
     }
     push();
     const auto& hu = red.run<RED_UPDATE>(c, scd);
-    std::vector<int> check(nrhs, 0);
-    bool need_true = false;
     std::vector<double> hsave(hu.begin(), hu.end());
-    for (int r = 0; r < nrhs; ++r) {
-      if (done[r]) continue;
-      it[r] += 1;
-      const double rel = std::sqrt(hsave[r * kMaxK]) / bnorm[r];
-      H[r].push_back(rel);
-      if (rel <= tol) {
-        check[r] = 1;
-        need_true = true;
-      }
-    }
-    if (need_true) {
-      true_residual(truer);
-      for (int r = 0; r < nrhs; ++r) {
-        if (!check[r]) continue;
-        H[r].back() = truer[r];
-        if (truer[r] <= tol) {
-          done[r] = 1;
-          conv[r] = 1;
-          relres[r] = truer[r];
-        }
-      }
-    }
-    // next direction for the still-active rhs
     std::vector<int> hit_max(nrhs, 0);
     for (int r = 0; r < nrhs; ++r) {
       if (done[r]) {
         sc[r].active = 0;
         continue;
       }
+      it[r] += 1;
+      const double rel = std::sqrt(hsave[r * kMaxK]) / bnorm[r];
+      H[r].push_back(rel);
       const double mz = (deflate && prec != NLD_PREC_NONE) ? hsave[r * kMaxK + 1] / dN : 0.0;
       const double rzn = hsave[r * kMaxK + 2] - mz * hsave[r * kMaxK + 3];
+      if (rel <= tol) {
+        // check in the next product; the direction waits for its outcome
+        pending[r] = 1;
+        save_rzn[r] = rzn;
+        save_mz[r] = mz;
+        sc[r].active = 0;
+        continue;
+      }
       if (!std::isfinite(rzn))
         throw Error(NLD_ERR_BREAKDOWN, "non-finite residual inner product");
       sc[r].mz = mz;
@@ -702,16 +785,56 @@ void cg_solve(nld_operator* op, const double* f, double* u, int nrhs, int64_t ld
     bool any_max = false;
     for (int r = 0; r < nrhs; ++r) any_max |= hit_max[r] != 0;
     if (any_max) {
+      // (pending rhs are resolved by the next loop's product; resolve them
+      // here too so this explicit residual serves both)
       true_residual(truer);
       for (int r = 0; r < nrhs; ++r) {
+        if (pending[r]) {
+          H[r].back() = truer[r];
+          pending[r] = 0;
+          if (truer[r] <= tol || it[r] >= maxit) {
+            done[r] = 1;
+            conv[r] = truer[r] <= tol;
+            relres[r] = truer[r];
+            sc[r].active = 0;
+          } else {
+            // must continue: its deferred direction
+            sc[r].mz = save_mz[r];
+            sc[r].beta = save_rzn[r] / rz[r];
+            rz[r] = save_rzn[r];
+            sc[r].active = 1;
+            sc[r].sel = 3;   // marker only
+          }
+        }
         if (!hit_max[r]) continue;
         done[r] = 1;
         relres[r] = truer[r];
         conv[r] = truer[r] <= tol;
         sc[r].active = 0;
       }
+      // directions of rhs released from pending above
+      bool rel_dir = false;
+      std::vector<int> keep(nrhs);
+      for (int r = 0; r < nrhs; ++r) {
+        keep[r] = sc[r].active;
+        if (sc[r].sel == 3) rel_dir = true;
+      }
+      if (rel_dir) {
+        for (int r = 0; r < nrhs; ++r) sc[r].active = (sc[r].sel == 3) ? 1 : 0;
+        push();
+        k_cg_direction<<<eg, 256, 0, st>>>(c, scd, 0);
+        NLD_CUDA(cudaGetLastError());
+        for (int r = 0; r < nrhs; ++r) {
+          sc[r].active = keep[r];
+          sc[r].sel = 0;
+        }
+      }
       push();
     }
+    // rhs waiting for their check stay "active" for the loop condition
+    bool waiting = false;
+    for (int r = 0; r < nrhs; ++r) waiting |= pending[r] != 0;
+    if (!any_active() && !waiting) break;
   }
   k_cg_finish<<<eg, 256, 0, st>>>(c, scd);
   to_rhs_major(c.x, N, nrhs, u, ld, st);

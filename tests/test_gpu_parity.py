@@ -551,3 +551,29 @@ def test_sliced_multiple_rhs_groups(nrhs):
             ck = None if c is None else c[2 * k:2 * k + 2]
             one = op.apply_device(torch.from_numpy(V[:, k].copy()).cuda(), kind, 1, ck)
             assert rel(got[:, k], one.cpu().numpy()) < 1e-12, (kind, k)
+
+
+@pytest.mark.parametrize("tol", [1e-12, 1e-13, 3e-14, 1e-14])
+def test_true_residual_confirmation_near_roundoff(tol):
+    """The explicit-residual confirmation (linops.py:218-231) rides in the
+    next product's batch; near round-off the recursive residual can pass
+    while the explicit one fails, and the solve must then continue exactly
+    as the reference does (checked against the oracle's restatement, batched
+    and single)."""
+    op, _, _, f = operator("c0")
+    eta = op.degree()
+    mu = synth.ALPHA_SCALE / float(np.mean(eta))
+    system = nld.ShiftedSystem(op, 1.0, mu)
+    ref = O.AnovaOracle(*operator("c0")[1:3], synth.SIGMA, **PIN)
+    u, it, conv, relres, hist = O.deflated_solve(O.SystemOracle(ref, 1.0, mu), f[:, 0],
+                                                 "jacobi", tol, 80)
+    res = nld.deflated_solve(system, f[:, 0], prec="jacobi", tol=tol, maxit=80)
+    assert res.converged == conv
+    assert abs(res.iterations - it) <= 1
+    assert rel(res.x, u) < 1e-8
+    batch = nld.deflated_solve_batched(op, f[:, 0], 1.0, [mu, 2 * mu, mu], prec="jacobi",
+                                       tol=tol, maxit=80)
+    for r in (0, 2):
+        assert batch[r].iterations == res.iterations
+        assert batch[r].converged == res.converged
+        assert rel(batch[r].x, res.x) < 1e-12
