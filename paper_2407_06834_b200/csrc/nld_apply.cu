@@ -1027,118 +1027,6 @@ void spread_window_fast(const PlanSet& ps, const Workspace& ws, int w, const dou
                        ps.ychunk ? ps.ychunk + wp.sub_off : nullptr, nsub, ws.vmax, vt, nrhs,
                        ws.blocks, st, ps.sub_order ? ps.sub_order + wp.sub_off : nullptr);
       if (getenv("NLD_OZ_PROF_PRINT")) ozaki_prof_dump("spread", st);
-      if (getenv("NLD_OZAKI_DEBUG")) {
-        // compare with the fp64 DMMA spread of the same window (debug only)
-        const size_t nb = (size_t)ps.blocks_total * nrhs;
-        std::vector<double> h1(nb), h2(nb);
-        NLD_CUDA(cudaStreamSynchronize(st));
-        NLD_CUDA(cudaMemcpy(h1.data(), ws.blocks, nb * 8, cudaMemcpyDeviceToHost));
-        launch_spread_bc(subs, nsub, ps, ws, vt, nrhs, st);
-        NLD_CUDA(cudaStreamSynchronize(st));
-        NLD_CUDA(cudaMemcpy(h2.data(), ws.blocks, nb * 8, cudaMemcpyDeviceToHost));
-        SubDev s0;
-        NLD_CUDA(cudaMemcpy(&s0, subs, sizeof(SubDev), cudaMemcpyDeviceToHost));
-        double num = 0, den = 0;
-        for (int64_t e = s0.block * nrhs; e < (s0.block + 512) * nrhs; ++e) {
-          num += (h1[e] - h2[e]) * (h1[e] - h2[e]);
-          den += h2[e] * h2[e];
-        }
-        fprintf(stderr, "ozdbg win %d sub0 count %d rel %.3e\n", w, s0.count, sqrt(num / den));
-        {
-          // host fp64 reference of sub0's block (r = 0..15)
-          const WinDev& wdh = ps.wdev_h[w];
-          std::vector<double> rr((size_t)s0.count * 24);
-          std::vector<int32_t> pp(s0.count);
-          NLD_CUDA(cudaMemcpy(rr.data(), ps.rows + wdh.row_off + (s0.start - wdh.node_off) * 24,
-                              rr.size() * 8, cudaMemcpyDeviceToHost));
-          NLD_CUDA(cudaMemcpy(pp.data(), ps.pix + s0.start, pp.size() * 4, cudaMemcpyDeviceToHost));
-          std::vector<double> vv((size_t)s0.count * 16);
-          for (int j = 0; j < s0.count; ++j)
-            NLD_CUDA(cudaMemcpy(&vv[j * 16], vt + (int64_t)pp[j] * nrhs, 16 * 8,
-                                cudaMemcpyDeviceToHost));
-          double n1 = 0, n2 = 0, dd = 0;
-          for (int a = 0; a < 8; ++a)
-            for (int bc = 0; bc < 64; ++bc)
-              for (int r = 0; r < 16; ++r) {
-                double acc = 0;
-                for (int j = 0; j < s0.count; ++j)
-                  acc += vv[j * 16 + r] * rr[j * 24 + a] * rr[j * 24 + 8 + (bc >> 3)] *
-                         rr[j * 24 + 16 + (bc & 7)];
-                const int64_t e = (s0.block + a * 64 + bc) * nrhs + r;
-                n1 += (h1[e] - acc) * (h1[e] - acc);
-                n2 += (h2[e] - acc) * (h2[e] - acc);
-                dd += acc * acc;
-                if (a == 2 && bc == 18 && r < 3)
-                  fprintf(stderr, "   host %.15e oz %.15e dmma %.15e\n", acc, h1[e], h2[e]);
-              }
-          fprintf(stderr, "  vs host: oz %.3e dmma %.3e\n", sqrt(n1 / dd), sqrt(n2 / dd));
-          {
-            // re-run sub0 alone through the library launcher
-            std::vector<double> h3(nb);
-            launch_spread_oz(ps, subs, ps.sub_exp + wp.sub_off * 24,
-                             ps.ychunk ? ps.ychunk + wp.sub_off : nullptr, 1, ws.vmax, vt, nrhs,
-                             ws.blocks, st);
-            NLD_CUDA(cudaStreamSynchronize(st));
-            NLD_CUDA(cudaMemcpy(h3.data(), ws.blocks, nb * 8, cudaMemcpyDeviceToHost));
-            double n3 = 0, d3 = 0;
-            for (int64_t e = s0.block * nrhs; e < (s0.block + 512) * nrhs; ++e) {
-              n3 += (h3[e] - h2[e]) * (h3[e] - h2[e]);
-              d3 += h2[e] * h2[e];
-            }
-            fprintf(stderr, "   sub0 alone vs dmma: %.3e\n", sqrt(n3 / d3));
-          }
-          if (w == 0) {
-            FILE* f = fopen("/tmp/oz_sub0.bin", "wb");
-            fwrite(&s0.count, 4, 1, f);
-            fwrite(rr.data(), 8, rr.size(), f);
-            fwrite(vv.data(), 8, vv.size(), f);
-            fclose(f);
-          }
-          {
-            int16_t exh[24];
-            NLD_CUDA(cudaMemcpy(exh, ps.sub_exp + wp.sub_off * 24, 48, cudaMemcpyDeviceToHost));
-            fprintf(stderr, "   dev ex:");
-            for (int k = 0; k < 24; ++k) fprintf(stderr, " %d", exh[k]);
-            fprintf(stderr, "  sub_off %lld\n", (long long)wp.sub_off);
-          }
-          // host emulation of the sliced algorithm for a = 2, bc = 18, r = 0..2
-          auto eb = [](double m) { return m > 0 ? ilogb(m) + 1 : 0; };
-          auto digits = [](double x, double y, int* d) {
-            const double u = fma(x, y, 4503599627370496.0 + 141289400074368.0);
-            long long bits;
-            memcpy(&bits, &u, 8);
-            for (int p = 0; p < 6; ++p) d[p] = (int)((bits >> (8 * (5 - p))) & 0xff) - 128;
-          };
-          double mA = 0, mB = 0, mC = 0;
-          for (int j = 0; j < s0.count; ++j) {
-            mA = fmax(mA, fabs(rr[j * 24 + 2]));
-            mB = fmax(mB, fabs(rr[j * 24 + 8 + 2]));
-            mC = fmax(mC, fabs(rr[j * 24 + 16 + 2]));
-          }
-          for (int r = 0; r < 3; ++r) {
-            double mv = 0;
-            for (int j = 0; j < s0.count; ++j) mv = fmax(mv, fabs(vv[j * 16 + r]));
-            const int ev = eb(mv), eA = eb(mA), eB = eb(mB), eC = eb(mC);
-            long long D[6] = {0, 0, 0, 0, 0, 0};
-            for (int j = 0; j < s0.count; ++j) {
-              int dx[6], dy[6];
-              digits(ldexp(vv[j * 16 + r], 46 - ev), ldexp(rr[j * 24 + 2], -eA), dx);
-              digits(ldexp(rr[j * 24 + 10], 46 - eB), ldexp(rr[j * 24 + 18], -eC), dy);
-              for (int p = 0; p < 6; ++p)
-                for (int q = 0; p + q < 6; ++q) D[p + q] += (long long)dx[p] * dy[q];
-            }
-            double acc = 0;
-            for (int t = 5; t >= 0; --t) acc = acc / 256.0 + (double)D[t];
-            fprintf(stderr, "   emu r%d ev %d eA %d eB %d eC %d -> %.15e  D0 %lld D1 %lld\n", r, ev,
-                    eA, eB, eC, ldexp(acc, ev + eA + eB + eC - 12), D[0], D[1]);
-          }
-        }
-        for (int k = 0; k < 6; ++k) {
-          const int64_t e = (s0.block + k * 73) * nrhs + (k % 16);
-          fprintf(stderr, "  e %lld oz %.15e ref %.15e\n", (long long)e, h1[e], h2[e]);
-        }
-        NLD_CUDA(cudaMemcpy(ws.blocks, h1.data(), nb * 8, cudaMemcpyHostToDevice));
-      }
     }
     else if (bc && nrhs % 16 == 0 && ((uintptr_t)vt & 15) == 0)
       launch_spread_bc(subs, nsub, ps, ws, vt, nrhs, st);
@@ -1171,69 +1059,6 @@ void gather_window_fast(const PlanSet& ps, const Workspace& ws, int w, int64_t N
   if (!oz_used) return;
   // ---- debug / profiling aids of the sliced gather (environment-gated) ----
   if (MC == 4 && use_ozaki() && getenv("NLD_OZ_PROF_PRINT")) ozaki_prof_dump("gather", st);
-  if (MC == 4 && use_ozaki() && nrhs % 16 == 0 && ps.sub_exp && getenv("NLD_OZAKI_DEBUG2") &&
-      ep.mode != mma::kGatherStore) {
-    // debug: the fused mode of both gathers from the same starting `out`
-    const size_t nn = (size_t)N * nrhs;
-    double *ta = nullptr, *tb = nullptr;
-    NLD_CUDA(cudaMalloc(&ta, nn * 8));
-    NLD_CUDA(cudaMalloc(&tb, nn * 8));
-    NLD_CUDA(cudaStreamSynchronize(st));
-    NLD_CUDA(cudaMemcpy(ta, out, nn * 8, cudaMemcpyDeviceToDevice));
-    NLD_CUDA(cudaMemcpy(tb, out, nn * 8, cudaMemcpyDeviceToDevice));
-    launch_gather_oz(ps, subs, ps.sub_exp + wp.sub_off * 24, ps.sub_order + wp.sub_off, nsub, ws.grid_out, ps.grid_total, ta,
-                     N, nrhs, ep, st);
-    launch_gather_mma(subs, nsub, ps, ws, N, nrhs, st, ep, tb);
-    NLD_CUDA(cudaStreamSynchronize(st));
-    std::vector<double> h1(nn), h2(nn);
-    NLD_CUDA(cudaMemcpy(h1.data(), ta, nn * 8, cudaMemcpyDeviceToHost));
-    NLD_CUDA(cudaMemcpy(h2.data(), tb, nn * 8, cudaMemcpyDeviceToHost));
-    double num = 0, den = 0;
-    int shown = 0;
-    for (size_t e = 0; e < nn; ++e) {
-      num += (h1[e] - h2[e]) * (h1[e] - h2[e]);
-      den += h2[e] * h2[e];
-      if (fabs(h1[e] - h2[e]) > 1e-9 * fabs(h2[e]) + 1e-300 && shown < 6) {
-        fprintf(stderr, "   e %zu (px %zu r %zu) oz %.9e mma %.9e\n", e, e / nrhs, e % nrhs, h1[e],
-                h2[e]);
-        ++shown;
-      }
-    }
-    fprintf(stderr, "ozfdbg win %d mode %d rel %.3e\n", w, ep.mode, sqrt(num / den));
-    cudaFree(ta);
-    cudaFree(tb);
-  }
-  if (MC == 4 && use_ozaki() && nrhs % 16 == 0 && ps.sub_exp && getenv("NLD_OZAKI_DEBUG")) {
-    // debug: both gathers in store mode into wout[w], compare
-    const size_t nn = (size_t)N * nrhs;
-    std::vector<double> h1(nn), h2(nn);
-    mma::GatherEpi sto{mma::kGatherStore, 0, 0, nullptr, nullptr, nullptr};
-    double* wo = ws.wout + (int64_t)w * N * nrhs;
-    NLD_CUDA(cudaMemsetAsync(wo, 0, nn * 8, st));
-    launch_gather_oz(ps, subs, ps.sub_exp + wp.sub_off * 24, ps.sub_order + wp.sub_off, nsub, ws.grid_out, ps.grid_total, wo,
-                     N, nrhs, sto, st);
-    NLD_CUDA(cudaStreamSynchronize(st));
-    NLD_CUDA(cudaMemcpy(h1.data(), wo, nn * 8, cudaMemcpyDeviceToHost));
-    NLD_CUDA(cudaMemsetAsync(wo, 0, nn * 8, st));
-    launch_gather_mma(subs, nsub, ps, ws, N, nrhs, st, sto, nullptr);
-    NLD_CUDA(cudaStreamSynchronize(st));
-    NLD_CUDA(cudaMemcpy(h2.data(), wo, nn * 8, cudaMemcpyDeviceToHost));
-    SubDev s0;
-    NLD_CUDA(cudaMemcpy(&s0, subs, sizeof(SubDev), cudaMemcpyDeviceToHost));
-    std::vector<int32_t> pp(s0.count);
-    NLD_CUDA(cudaMemcpy(pp.data(), ps.pix + s0.start, pp.size() * 4, cudaMemcpyDeviceToHost));
-    double num = 0, den = 0;
-    for (size_t e = 0; e < nn; ++e) {
-      num += (h1[e] - h2[e]) * (h1[e] - h2[e]);
-      den += h2[e] * h2[e];
-    }
-    fprintf(stderr, "ozgdbg win %d rel %.3e  sub0 count %d\n", w, sqrt(num / den), s0.count);
-    for (int j = 0; j < std::min(40, s0.count); j += 1) {
-      const int64_t e = (int64_t)pp[j] * nrhs;
-      fprintf(stderr, "  node %d: r0 oz %.6e ref %.6e | r7 oz %.6e ref %.6e\n", j, h1[e], h2[e],
-              h1[e + 7], h2[e + 7]);
-    }
-  }
 }
 
 struct EvScope {
