@@ -118,13 +118,16 @@ k_cg_reduce(CgPtr c, const RhsScal* __restrict__ sc, const double* __restrict__ 
       acc[1] += vp * vq;
       acc[2] += vp;
     } else if (MODE == RED_UPDATE || MODE == RED_PREC) {
+      // (vb, vt) carry x and eta here: every load of the step is issued up front
       double rr = vr;
       if (MODE == RED_UPDATE && s.active) {
-        c.x[e] += s.alpha * vp;
+        c.x[e] = vb + s.alpha * vp;
         rr -= s.alpha * (vq - s.mq);
         c.r[e] = rr;
       }
-      const double zt = dinv_at(c, s, i) * rr;
+      const double di = c.prec == NLD_PREC_JACOBI ? __drcp_rn(s.lam + s.mu * vt)
+                                                  : dinv_at(c, s, i);
+      const double zt = di * rr;
       acc[0] += rr * rr;
       acc[1] += zt;
       acc[2] += rr * zt;
@@ -139,7 +142,11 @@ k_cg_reduce(CgPtr c, const RhsScal* __restrict__ sc, const double* __restrict__ 
     const int64_t e = i * nr + r;
     if (MODE == RED_SUM || MODE == RED_NORM2) va = vecA[e];
     if (MODE == RED_PQ || MODE == RED_UPDATE) { vp = c.p[e]; vq = c.q[e]; }
-    if (MODE == RED_UPDATE || MODE == RED_PREC) vr = c.r[e];
+    if (MODE == RED_UPDATE || MODE == RED_PREC) {
+      vr = c.r[e];
+      if (MODE == RED_UPDATE && s.active) vb = c.x[e];
+      if (c.prec == NLD_PREC_JACOBI) vt = c.eta[i];
+    }
     if (MODE == RED_RESID) { vb = c.b[e]; vt = c.t[e]; }
   };
   if (live) {
@@ -214,25 +221,28 @@ __global__ void k_cg_direction(CgPtr c, const RhsScal* __restrict__ sc, int firs
   const RhsScal s = sc[r];
   if (!s.active) return;
   const int64_t stride = (int64_t)gridDim.x * grp;
-  auto one = [&](int64_t i, double rv, double pv) {
-    const double z = (c.prec == NLD_PREC_NONE) ? rv : dinv_at(c, s, i) * rv - s.mz;
+  const bool jac = c.prec == NLD_PREC_JACOBI;
+  auto one = [&](int64_t i, double rv, double pv, double ev) {
+    const double di = jac ? __drcp_rn(s.lam + s.mu * ev) : dinv_at(c, s, i);
+    const double z = (c.prec == NLD_PREC_NONE) ? rv : di * rv - s.mz;
     c.p[i * nr + r] = first ? z : z + s.beta * pv;
   };
   int64_t i = blockIdx.x * (int64_t)grp + g;
   for (; i + 3 * stride < c.N; i += 4 * stride) {
-    double rv[4], pv[4];
+    double rv[4], pv[4], ev[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int64_t e = (i + u * stride) * nr + r;
       rv[u] = c.r[e];
       pv[u] = first ? 0.0 : c.p[e];
+      ev[u] = jac ? c.eta[i + u * stride] : 0.0;
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) one(i + u * stride, rv[u], pv[u]);
+    for (int u = 0; u < 4; ++u) one(i + u * stride, rv[u], pv[u], ev[u]);
   }
   for (; i < c.N; i += stride) {
     const int64_t e = i * nr + r;
-    one(i, c.r[e], first ? 0.0 : c.p[e]);
+    one(i, c.r[e], first ? 0.0 : c.p[e], jac ? c.eta[i] : 0.0);
   }
 }
 
