@@ -1051,7 +1051,8 @@ void gather_window_fast(const PlanSet& ps, const Workspace& ws, int w, int64_t N
     launch_gather_oz(ps, subs, ps.sub_exp + wp.sub_off * 24, ps.sub_order + wp.sub_off, nsub, ws.grid_out, ps.grid_total,
                      ep.mode == mma::kGatherStore ? ws.wout + (int64_t)w * N * nrhs : out, N, nrhs,
                      ep, st, ws.gdig, w < (int)ps.gcell_lo.size() ? ps.gcell_lo[w] : 0,
-                     w < (int)ps.gcell_n.size() ? ps.gcell_n[w] : 0);
+                     w < (int)ps.gcell_n.size() ? ps.gcell_n[w] : 0,
+                     ps.ychunk ? ps.ychunk + wp.sub_off : nullptr);
   else if (MC == 4 && use_mma()) launch_gather_mma(subs, nsub, ps, ws, N, nrhs, st, ep, out);
   else launch_gather<3, MC>(subs, nsub, ps, ws, N, nrhs, st);
   const bool oz_used = wp.d == 3 && MC == 4 && use_ozaki() && nrhs % 16 == 0 && ps.sub_exp &&

@@ -136,6 +136,7 @@ struct PlanSet {
   uint8_t* ydig = nullptr;       // sliced spread: Y = B (x) C digit slices per 32-node
                                  // chunk, UMMA B-operand layout (12 KB per chunk)
   int64_t* ychunk = nullptr;     // per 3-D subproblem: its first chunk in ydig
+  uint8_t* gydig = nullptr;      // sliced gather: Y digits per 32-node tile (12 KB, K-major)
   std::vector<int64_t> gcell_lo, gcell_n;   // per window: its cells' global range
   int shares_tables_with = -1;   // index of the plan set whose tables we use
   bool owns_tables = true;
@@ -217,7 +218,7 @@ void launch_gather_oz(const PlanSet& ps, const SubDev* subs, const int16_t* ex,
                       const int32_t* order, unsigned nsub, const double* grid, int64_t grid_ld,
                       double* out, int64_t N, int nrhs, const mma::GatherEpi& ep,
                       cudaStream_t st, uint8_t* gdig = nullptr, int64_t cell_lo = 0,
-                      int64_t ncell = 0);
+                      int64_t ncell = 0, const int64_t* ychunk = nullptr);
 // bytes per (cell, 16-rhs group) of precomputed gather G digits
 int64_t gather_gdig_bytes();
 void free_planset(PlanSet& ps);

@@ -1247,6 +1247,45 @@ k_gather_oz(const SubDev* __restrict__ subs, const CellDev* __restrict__ cells,
   if (warp == 0) umma::tmem_free<kGTmemCols>(tmem);
 }
 
+// ---- plan-time Y digits for the sliced gather (GY) -------------------------
+// Y_j[(b, c)] = B_j[b] C_j[c] scaled per subproblem (2^(46 - max eB - max eC),
+// exactly the slicers' scaling), six K-major slices of each 32-node tile
+// (32 nodes x 64 bytes, canonical layout), zero past the count.
+__global__ void __launch_bounds__(128)
+k_gather_ydig(const SubDev* __restrict__ subs, const WinDev* __restrict__ wins,
+              const double* __restrict__ rows, const int16_t* __restrict__ sub_exp,
+              const int64_t* __restrict__ ychunk, uint8_t* __restrict__ gydig) {
+  const SubDev sd = subs[blockIdx.x];
+  const WinDev wd = wins[sd.win];
+  const double* __restrict__ rw = rows + wd.row_off + (sd.start - wd.node_off) * 24;
+  const int16_t* ex = sub_exp + (int64_t)blockIdx.x * kExpPerSub;
+  int eBm = -2000, eCm = -2000;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    eBm = max(eBm, (int)ex[8 + q]);
+    eCm = max(eCm, (int)ex[16 + q]);
+  }
+  const double syB = pow2(46 - eBm), syC = pow2(-eCm);
+  const int t = threadIdx.x, n = t >> 2, kq = t & 3;     // node, bc quarter
+  const int ntile = (sd.count + kGTile - 1) / kGTile;
+  uint8_t* base = gydig + ychunk[blockIdx.x] * (int64_t)(kSl * kGB);
+  for (int tl = 0; tl < ntile; ++tl) {
+    const int j = tl * kGTile + n;
+    uint32_t lo[16], hi[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int bc = kq * 16 + i;
+      double x = 0.0, y = 0.0;
+      if (j < sd.count) {
+        x = rw[(int64_t)j * 24 + 8 + (bc >> 3)] * syB;
+        y = rw[(int64_t)j * 24 + 16 + (bc & 7)] * syC;
+      }
+      slice1(x, y, lo[i], hi[i]);
+    }
+    store16(lo, hi, base + (int64_t)tl * (kSl * kGB) + canon64(n, kq * 16), kGB);
+  }
+}
+
 // ---- G digits of every cell, once per product (persistent gather) ----------
 // Per (cell, 16-rhs group): the 128 rows (r, a) x 64 (b, c) of the support-box
 // grid at the cell, scaled per rhs (max over its 8 a-rows and 64 values) and
@@ -1330,15 +1369,23 @@ constexpr int kPRS = NLD_GP_RS, kPOS = NLD_GP_OS;   // raw / operand stages
 __host__ __device__ constexpr int gather_ozp_smem() {
   return 2 * kSl * kGA + kPOS * kGBStage + kPRS * kGRaw;
 }
+// plan-time Y digits (GY): no operand stages; each raw stage carries the
+// tile's 12 KB of Y digits after its rows and pixel indices
+constexpr int kGYOff = (kGRaw + 15) / 16 * 16;
+constexpr int kGRawGY = kGYOff + kSl * kGB;
+__host__ __device__ constexpr int gather_ozp_gy_smem() { return 2 * kSl * kGA + kPRS * kGRawGY; }
 
+template <bool GY>
 __global__ void __launch_bounds__(kPThreads, 1)
 k_gather_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order, int nsub,
              const CellDev* __restrict__ cells, const WinDev* __restrict__ wins,
              const double* __restrict__ rows, const int32_t* __restrict__ pix,
              const int16_t* __restrict__ sub_exp, const double* __restrict__ grid,
              int64_t grid_ld, double* __restrict__ out, int64_t N, int nrhs, mma::GatherEpi ep,
-             const uint8_t* __restrict__ gdig) {
+             const uint8_t* __restrict__ gdig, const uint8_t* __restrict__ gydig,
+             const int64_t* __restrict__ ychunk) {
   constexpr int RS = kPRS, OS = kPOS;              // raw / operand stages
+  constexpr int kRawB = GY ? kGRawGY : kGRaw;      // raw stage bytes
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ uint64_t raw_full[RS], raw_empty[RS], op_ready[OS], op_free[OS];
   __shared__ uint64_t acc_full[2], acc_empty[2], g_full[2], g_empty[2];
@@ -1349,7 +1396,7 @@ k_gather_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   uint8_t* const sGA = smem;                                    // [2][6][128 x 64]
   uint8_t* const sGB = sGA + 2 * kSl * kGA;                     // [3][6][32 x 64]
-  uint8_t* const sRaw = sGB + OS * kGBStage;                    // [6][rows | pix]
+  uint8_t* const sRaw = sGB + (GY ? 0 : OS * kGBStage);         // [6][rows | pix (| Y)]
   const int ngroups = nrhs / 16;
   const int G = (int)gridDim.x, b = (int)blockIdx.x;
   const int rounds = nsub / G, rem = nsub % G;
@@ -1363,8 +1410,10 @@ k_gather_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
   if (warp == 0) umma::tmem_alloc<512>(&taddr_s);
   if (tid == 32) {
     for (int k = 0; k < RS; ++k) {
-      umma::mbar_init(&raw_full[k], 32);
-      umma::mbar_init(&raw_empty[k], kPSlicers + kPEpi);
+      // GY: 32 noinc cp.async arrivals + the Y bulk copy's; released by the
+      // epilogue warps and the tile's UMMA commit (no slicer pass over Y)
+      umma::mbar_init(&raw_full[k], GY ? 33 : 32);
+      umma::mbar_init(&raw_empty[k], GY ? kPEpi + 1 : kPSlicers + kPEpi);
     }
     for (int k = 0; k < OS; ++k) {
       umma::mbar_init(&op_ready[k], kPSlicers);
@@ -1395,12 +1444,19 @@ k_gather_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
       const double* rw = rows + wd.row_off + (sd.start - wd.node_off) * 24;
       const int32_t* pw = pix + sd.start;
       const int ntile = (sd.count + kGTile - 1) / kGTile;
+      const uint8_t* gyd = GY ? gydig + ychunk[item_sub(k)] * (int64_t)(kSl * kGB) : nullptr;
       for (int tl = 0; tl < ntile; ++tl, ++gt) {
         const int s = gt % RS;
         if (gt >= RS) OZW(0, umma::mbar_wait(&raw_empty[s], ((gt / RS) - 1) & 1));
         const int j0 = tl * kGTile, cn = min(kGTile, sd.count - j0);
         const double* src = rw + (int64_t)j0 * 24;
-        uint8_t* dst = sRaw + s * kGRaw;
+        uint8_t* dst = sRaw + s * kRawB;
+        if constexpr (GY) {
+          if (lane == 0) {
+            umma::mbar_arrive_expect_tx(&raw_full[s], kSl * kGB);
+            umma::bulk_g2s(dst + kGYOff, gyd + (int64_t)tl * (kSl * kGB), kSl * kGB, &raw_full[s]);
+          }
+        }
 #ifndef NLD_EXP_PNOLOAD
         for (int e = lane; e < cn * 12; e += 32) {
           const int node = e / 12, gi = e - node * 12;
@@ -1440,11 +1496,14 @@ k_gather_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
       for (int tl = 0; tl < ntile; ++tl, ++gt) {
         const int st = gt % OS, ab = gt & 1;
         if (gt >= 2) OZW(1, umma::mbar_wait(&acc_empty[ab], ((gt >> 1) - 1) & 1));
-        OZW(2, umma::mbar_wait(&op_ready[st], (gt / OS) & 1));
+        const int s = gt % RS;
+        if constexpr (GY) OZW(2, umma::mbar_wait(&raw_full[s], (gt / RS) & 1));   // Y landed
+        else OZW(2, umma::mbar_wait(&op_ready[st], (gt / OS) & 1));
         umma::fence_after();
         if (lane == 0) {
           const uint32_t aB = umma::smem_u32(sGA + gs * kSl * kGA);
-          const uint32_t bB = umma::smem_u32(sGB + st * kGBStage);
+          const uint32_t bB = GY ? umma::smem_u32(sRaw + s * kRawB + kGYOff)
+                                 : umma::smem_u32(sGB + st * kGBStage);
           const uint32_t dcol = tmem + (uint32_t)(ab * kSl * kGTile);
           // p outer, ks inner: the two K steps of one digit row hit the same D
           // window back to back and chain in the tensor pipe (a D window / N
@@ -1467,7 +1526,8 @@ k_gather_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
 #endif
             }
 #endif
-          umma::commit(&op_free[st]);
+          if constexpr (GY) umma::commit(&raw_empty[s]);   // Y digits consumed
+          else umma::commit(&op_free[st]);
           umma::commit(&acc_full[ab]);
 #if !NLD_GP_GTMEM
           if (tl == ntile - 1) umma::commit(&g_empty[gs]);   // item k's G digits released
@@ -1547,6 +1607,7 @@ k_gather_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
         if (lane == 0) mbar_arrive(&g_full[gs]);
       }
       }
+      if constexpr (GY) continue;   // Y digits come precomputed with the raw stage
       // Y digits of each tile: 8 nodes per warp, node = lane & 7, bc quarter
       // kq = lane >> 3, so each quarter-warp's 16-byte stores cover one
       // contiguous 128-byte line (conflict-free)
@@ -1556,7 +1617,7 @@ k_gather_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
         OZW(3, umma::mbar_wait(&raw_full[s], (gt / RS) & 1));
         if (gt >= OS) OZW(4, umma::mbar_wait(&op_free[st], ((gt / OS) - 1) & 1));
 #ifndef NLD_EXP_PNOSLICE
-        const double* R = reinterpret_cast<const double*>(sRaw + s * kGRaw) + n * kGRowS;
+        const double* R = reinterpret_cast<const double*>(sRaw + s * kRawB) + n * kGRowS;
         const bool ok = tl * kGTile + n < sd.count;
         uint32_t lo[16], hi[16];
 #pragma unroll
@@ -1601,7 +1662,7 @@ k_gather_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
       EpiIn e;
       const int sn = gg % RS;
       OZW(7, umma::mbar_wait(&raw_full[sn], (gg / RS) & 1));
-      const int32_t* spn = reinterpret_cast<const int32_t*>(sRaw + sn * kGRaw + kGTile * kGRowS * 8);
+      const int32_t* spn = reinterpret_cast<const int32_t*>(sRaw + sn * kRawB + kGTile * kGRowS * 8);
 #pragma unroll
       for (int q = 0; q < kPG; ++q) {
         const int nn = (nh * kPG + q) * 8 + a;
@@ -1655,7 +1716,7 @@ k_gather_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
       }
       for (int tl = 0; tl < ntile; ++tl, ++gt) {
         const int ab = gt & 1, s = gt % RS;
-        const double* R = reinterpret_cast<const double*>(sRaw + s * kGRaw);
+        const double* R = reinterpret_cast<const double*>(sRaw + s * kRawB);
         const EpiIn cur = nxt;
         if (tl + 1 < ntile) nxt = epi_load(cnt, rg, tl + 1, gt + 1);
         else if (k + 1 < nitems) nxt = epi_load(cnt_next, ((k + 1) % ngroups) * 16, 0, gt + 1);
@@ -1821,6 +1882,17 @@ int16_t* ozaki_exponents(PlanSet& ps, cudaStream_t st) {
       oz::k_spread_ydig<<<(unsigned)h.size(), 256, 0, st>>>(ps.subs[3], ps.wdev, ps.rows,
                                                             ps.sub_exp, ps.ychunk, ps.ydig);
       NLD_CUDA(cudaGetLastError());
+      // the gather's Y digits (same chunking, K-major per node): when a second
+      // table of the same size still fits in half of the free memory
+      const char* gy = getenv("NLD_GATHER_PREY");
+      size_t free2 = 0;
+      NLD_CUDA(cudaMemGetInfo(&free2, &total_b));
+      if (!(gy && gy[0] == '0') && need <= free2 / 2) {
+        NLD_CUDA(cudaMalloc(&ps.gydig, need));
+        oz::k_gather_ydig<<<(unsigned)h.size(), 128, 0, st>>>(ps.subs[3], ps.wdev, ps.rows,
+                                                              ps.sub_exp, ps.ychunk, ps.gydig);
+        NLD_CUDA(cudaGetLastError());
+      }
     }
   }
   NLD_CUDA(cudaStreamSynchronize(st));
@@ -1871,7 +1943,8 @@ int64_t gather_gdig_bytes() { return oz::kGdigBytes; }
 void launch_gather_oz(const PlanSet& ps, const SubDev* subs, const int16_t* ex,
                       const int32_t* order, unsigned nsub, const double* grid, int64_t grid_ld,
                       double* out, int64_t N, int nrhs, const mma::GatherEpi& ep,
-                      cudaStream_t st, uint8_t* gdig, int64_t cell_lo, int64_t ncell) {
+                      cudaStream_t st, uint8_t* gdig, int64_t cell_lo, int64_t ncell,
+                      const int64_t* ychunk) {
   static int persist = -1;
   if (persist < 0) {
     const char* e = getenv("NLD_GATHER_PERSIST");
@@ -1882,8 +1955,11 @@ void launch_gather_oz(const PlanSet& ps, const SubDev* subs, const int16_t* ex,
     static bool attr_p = false;
     static int sms = 148;
     if (!attr_p) {
-      NLD_CUDA(cudaFuncSetAttribute(oz::k_gather_ozp, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    smem_p));
+      NLD_CUDA(cudaFuncSetAttribute(oz::k_gather_ozp<false>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem_p));
+      NLD_CUDA(cudaFuncSetAttribute(oz::k_gather_ozp<true>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    oz::gather_ozp_gy_smem()));
       int dev = 0;
       NLD_CUDA(cudaGetDevice(&dev));
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -1901,10 +1977,14 @@ void launch_gather_oz(const PlanSet& ps, const SubDev* subs, const int16_t* ex,
           ps.cells, ps.wdev, grid, grid_ld, cell_lo, nrhs / 16, gdig);
       NLD_CUDA(cudaGetLastError());
     }
-    oz::k_gather_ozp<<<grid_n, oz::kPThreads, smem_p, st>>>(subs, order, (int)nsub, ps.cells,
-                                                            ps.wdev, ps.rows, ps.pix, ex, grid,
-                                                            grid_ld, out, N, nrhs, ep,
-                                                            use_g ? gdig : nullptr);
+    if (ps.gydig && ychunk)
+      oz::k_gather_ozp<true><<<grid_n, oz::kPThreads, oz::gather_ozp_gy_smem(), st>>>(
+          subs, order, (int)nsub, ps.cells, ps.wdev, ps.rows, ps.pix, ex, grid, grid_ld, out, N,
+          nrhs, ep, use_g ? gdig : nullptr, ps.gydig, ychunk);
+    else
+      oz::k_gather_ozp<false><<<grid_n, oz::kPThreads, smem_p, st>>>(
+          subs, order, (int)nsub, ps.cells, ps.wdev, ps.rows, ps.pix, ex, grid, grid_ld, out, N,
+          nrhs, ep, use_g ? gdig : nullptr, nullptr, nullptr);
     NLD_CUDA(cudaGetLastError());
     return;
   }

@@ -849,6 +849,7 @@ void free_planset(PlanSet& ps) {
   cudaFree(ps.sub_exp);
   cudaFree(ps.sub_order);
   cudaFree(ps.ydig);
+  cudaFree(ps.gydig);
   cudaFree(ps.ychunk);
   cudaFree(ps.K);
   if (ps.owns_tables) {

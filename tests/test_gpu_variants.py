@@ -48,6 +48,7 @@ VARIANTS = {
     "spread_per_subproblem": {"NLD_SPREAD_PERSIST": "0"},
     "gather_in_kernel_g": {"NLD_GATHER_PREG": "0"},
     "gather_per_subproblem": {"NLD_GATHER_PERSIST": "0"},
+    "gather_on_the_fly_y": {"NLD_GATHER_PREY": "0"},
     "fp64_dmma": {"NLD_OZAKI": "0"},
 }
 
