@@ -1371,7 +1371,10 @@ __host__ __device__ constexpr int gather_ozp_smem() {
 }
 // plan-time Y digits (GY): no operand stages; each raw stage carries the
 // tile's 12 KB of Y digits after its rows and pixel indices
-constexpr int kGYOff = (kGRaw + 15) / 16 * 16;
+// (GY: only the A parts of the weight rows are staged -- 8 doubles per node --
+// then the pixel indices, then the Y digits)
+constexpr int kGYRowS = 8;
+constexpr int kGYOff = kGTile * kGYRowS * 8 + kGTile * 4;       // 2 KB + 128 B
 constexpr int kGRawGY = kGYOff + kSl * kGB;
 __host__ __device__ constexpr int gather_ozp_gy_smem() { return 2 * kSl * kGA + kPRS * kGRawGY; }
 
@@ -1386,6 +1389,7 @@ k_gather_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
              const int64_t* __restrict__ ychunk) {
   constexpr int RS = kPRS, OS = kPOS;              // raw / operand stages
   constexpr int kRawB = GY ? kGRawGY : kGRaw;      // raw stage bytes
+  constexpr int kRowS = GY ? kGYRowS : kGRowS;     // doubles per staged node row
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ uint64_t raw_full[RS], raw_empty[RS], op_ready[OS], op_free[OS];
   __shared__ uint64_t acc_full[2], acc_empty[2], g_full[2], g_empty[2];
@@ -1458,12 +1462,21 @@ k_gather_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
           }
         }
 #ifndef NLD_EXP_PNOLOAD
-        for (int e = lane; e < cn * 12; e += 32) {
-          const int node = e / 12, gi = e - node * 12;
-          cp_async16(dst + node * kGRowS * 8 + 16 * gi, src + 2 * e);
+        if constexpr (GY) {
+          // A parts only: 4 lanes per node's 64 bytes, 8 nodes per instruction
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int nd = q * 8 + (lane >> 2), pc = lane & 3;
+            if (nd < cn) cp_async16(dst + nd * 64 + pc * 16, src + (int64_t)nd * 24 + 2 * pc);
+          }
+        } else {
+          for (int e = lane; e < cn * 12; e += 32) {
+            const int node = e / 12, gi = e - node * 12;
+            cp_async16(dst + node * kGRowS * 8 + 16 * gi, src + 2 * e);
+          }
         }
 #endif
-        if (lane < cn) cp_async4(dst + kGTile * kGRowS * 8 + 4 * lane, pw + j0 + lane);
+        if (lane < cn) cp_async4(dst + kGTile * kRowS * 8 + 4 * lane, pw + j0 + lane);
         cp_async_mbar_arrive(&raw_full[s]);
       }
     }
@@ -1662,7 +1675,7 @@ k_gather_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
       EpiIn e;
       const int sn = gg % RS;
       OZW(7, umma::mbar_wait(&raw_full[sn], (gg / RS) & 1));
-      const int32_t* spn = reinterpret_cast<const int32_t*>(sRaw + sn * kRawB + kGTile * kGRowS * 8);
+      const int32_t* spn = reinterpret_cast<const int32_t*>(sRaw + sn * kRawB + kGTile * kRowS * 8);
 #pragma unroll
       for (int q = 0; q < kPG; ++q) {
         const int nn = (nh * kPG + q) * 8 + a;
@@ -1749,7 +1762,7 @@ k_gather_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
 #else
 #pragma unroll
           for (int i = 0; i < 8; ++i)
-            v8[i] = combine6(dv, i) * R[(nb + i) * kGRowS + a];
+            v8[i] = combine6(dv, i) * R[(nb + i) * kRowS + a];
 #endif
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
