@@ -1346,7 +1346,7 @@ k_gdig(const CellDev* __restrict__ cells, const WinDev* __restrict__ wins,
 //   warps 0-7  epilogue       warps 8-11 slicers (G digits + Y digits)
 //   warp 12    UMMA issuer    warp 13    loader
 #ifndef NLD_GP_EPI
-#define NLD_GP_EPI 8
+#define NLD_GP_EPI 16
 #endif
 constexpr int kPEpi = NLD_GP_EPI;                // 8 or 16 epilogue warps
 constexpr int kPG = 16 / kPEpi;                  // 8-node groups per epilogue warp and tile
