@@ -66,7 +66,7 @@ def dist_env():
 
 def cpu_sample(cfg_name, steps=2, warmup=1):
     from oracle.cpu_port import CpuPort
-    from paper_2407_06834_b200 import synth
+    import synth
 
     feats, wins, _ = synth.make_problem(cfg_name)
     n_full = feats.shape[0]
@@ -102,10 +102,68 @@ def cpu_sample(cfg_name, steps=2, warmup=1):
     }
 
 
+REF_SAMPLE_NODES = 1 << 17   # the real reference (numba, one thread): pixels [0, 2^17)
+
+
+def reference_numba_sample(cfg_name, nodes=REF_SAMPLE_NODES):
+    """The UNMODIFIED reference package (baseline/_ref, installed offline from
+    /root/reference/pkg) timed through its own public API: one
+    ShiftedSystem.apply (linops.py:48-50 -> kernel.py:79-93) per step, after a
+    warm-up that JIT-compiles its numba loops, on the first `nodes` pixels
+    of the config, scaled by nodes/N.  Its loops are serial
+    (_kernels.py:48,91), so this is one host thread.  As in the golden
+    generator only `_build_plans` is overridden, to pass the
+    BASELINE NFFT parameters that kernel.py:74 otherwise hard-codes."""
+    ref_dir = os.path.join(REPO, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref_dir, "nldenoise")):
+        return {"value": None, "sample": "unavailable: baseline/_ref not installed"}
+    if ref_dir not in sys.path:
+        sys.path.insert(0, ref_dir)
+    try:
+        from nldenoise import kernel as rk
+        from nldenoise import linops as rl
+        from nldenoise import transform as rt
+    except Exception as exc:  # numba / scipy missing on this host
+        return {"value": None, "sample": f"unavailable: {exc}"}
+    import synth
+
+    class Pinned(rk.AnovaOperator):
+        def _build_plans(self, sigbar):
+            plans = []
+            for w in self.windows:
+                pts = np.ascontiguousarray(self.features[:, w])
+                plan = rt.FastsumPlan.build(pts, sigbar, n_expansion=synth.N_EXPANSION,
+                                            cutoff=synth.CUTOFF,
+                                            oversampling=synth.OVERSAMPLING)
+                plans.append((pts, plan, plan.tables_for(pts)))
+            return plans
+
+    feats, wins, _ = synth.make_problem(cfg_name)
+    n_full = feats.shape[0]
+    ns = min(nodes, n_full)
+    op = Pinned(np.ascontiguousarray(feats[:ns]), wins, synth.SIGMA)
+    eta = op.degree()                      # builds the plans + JIT warm-up
+    system = rl.ShiftedSystem(op, 1.0, synth.ALPHA_SCALE / float(eta.mean()))
+    v = synth.random_vector(ns)
+    t0 = time.perf_counter()
+    system.apply(v)
+    best = time.perf_counter() - t0
+    return {"value": (ns / n_full) / best, "unit": UNIT, "cores": 1, "kind": "reference",
+            "sample_seconds": best,
+            "sample": (f"UNMODIFIED reference nldenoise (baseline/_ref, numba, one thread): "
+                       f"ShiftedSystem.apply on pixels [0,{ns}) of {n_full} of {cfg_name} "
+                       f"(M=32, m=4 via the _build_plans override), one timed call after "
+                       f"a JIT warm-up, scaled by {ns}/{n_full}")}
+
+
 def run_reference(args, world, rank):
     if rank != 0:
         return
     res = cpu_sample(args.config, steps=max(1, args.steps), warmup=max(0, args.warmup))
+    try:
+        numba_ref = reference_numba_sample(args.config)
+    except Exception as exc:  # the extra sample must not sink the line
+        numba_ref = {"value": None, "sample": f"failed: {exc}"}
     line = {
         "metric": METRIC, "value": res["value"], "unit": UNIT,
         "impl": "reference", "n_gpus": args.gpus, "steps": args.steps,
@@ -116,6 +174,8 @@ def run_reference(args, world, rank):
                    "n_nodes": int(4096 * 4096 if args.config == "c4" else 0)},
         "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind",
                                              "sample")},
+        "host_cpus": os.cpu_count(),
+        "reference_numba": numba_ref,
         "e2e": {"value": res["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -203,7 +263,8 @@ def run_ours(args, world, rank, local):
     import torch
 
     import paper_2407_06834_b200 as nld
-    from paper_2407_06834_b200 import _lib, sharding, synth
+    from paper_2407_06834_b200 import _lib, sharding
+    import synth
 
     # NLD_TEST_SHARED_GPU=1: every rank on cuda:0 over gloo -- a functional
     # check of the sharded flow on a one-GPU box (numbers meaningless)
@@ -459,7 +520,7 @@ def run_ours(args, world, rank, local):
                                    "digit products, fp64 combine)" if sliced
                                    else "fp64 DMMA spread/gather"),
                        "setup_s": t_setup},
-            "roofline": roofline, "cpu_baseline": cpu,
+            "roofline": roofline, "cpu_baseline": cpu, "host_cpus": os.cpu_count(),
             "e2e": {"value": e2e_val, "unit": UNIT,
                     "h2d_bytes_per_step": int(nrhs * n_global * 8),
                     "d2h_bytes_per_step": int(nrhs * n_global * 8),

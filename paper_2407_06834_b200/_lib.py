@@ -13,8 +13,9 @@ import os
 from . import errors
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-# NLD_LIB selects an alternative build of the same library (A/B experiments)
-LIB_PATH = os.environ.get("NLD_LIB") or os.path.join(_HERE, "libnld_b200.so")
+# always the in-tree product build (no environment override: a mis-set
+# variable can never swap in an experiment build)
+LIB_PATH = os.path.join(_HERE, "libnld_b200.so")
 
 NLD_OK = 0
 ERR_DIMENSION, ERR_SCALING, ERR_WINDOW, ERR_DENSE_LIMIT = 1, 2, 3, 4

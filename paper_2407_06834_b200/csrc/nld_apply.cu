@@ -1076,8 +1076,13 @@ struct EvScope {
 
 void ensure_workspace(nld_operator* op, const PlanSet& ps, int nrhs) {
   Workspace& ws = op->ws;
+  // the sliced gather's per-cell G digits exist only where that path runs
+  // (m = 4; 16k-rhs batches): other cutoffs neither allocate nor re-check them
+  const int64_t nc_need = std::max(ps.n_cells, std::max(op->sets[0].n_cells, op->sets[1].n_cells));
+  const bool oz_shape = use_ozaki() && op->params.cutoff == 4 && nc_need > 0;
+  const bool need_gdig = oz_shape && nrhs % 16 == 0;
   if (ws.nrhs_cap >= nrhs && ws.grid_total >= ps.grid_total &&
-      ws.blocks_total >= ps.blocks_total && ws.gdig_cells >= ps.n_cells)
+      ws.blocks_total >= ps.blocks_total && (!need_gdig || ws.gdig_cells >= ps.n_cells))
     return;
   double* keep_cg = ws.cg;
   int64_t keep_cap = ws.cg_cap;
@@ -1089,7 +1094,9 @@ void ensure_workspace(nld_operator* op, const PlanSet& ps, int nrhs) {
   int64_t gt = std::max(ps.grid_total, std::max(op->sets[0].grid_total, op->sets[1].grid_total));
   int64_t bt = std::max(ps.blocks_total, std::max(op->sets[0].blocks_total, op->sets[1].blocks_total));
   NLD_CUDA(cudaMalloc(&ws.blocks, sizeof(double) * std::max<int64_t>(1, bt) * cap));
-  NLD_CUDA(cudaMalloc(&ws.grid_in, sizeof(double) * std::max<int64_t>(1, gt) * cap));
+  // + one flag per rhs after the grids (non-finite rhs, summed with the grids
+  // by the shard allreduce; see k_vmax / k_poison)
+  NLD_CUDA(cudaMalloc(&ws.grid_in, sizeof(double) * (std::max<int64_t>(1, gt) * cap + cap)));
   NLD_CUDA(cudaMalloc(&ws.grid_out, sizeof(double) * std::max<int64_t>(1, gt) * cap));
   NLD_CUDA(cudaMalloc(&ws.cbuf0, sizeof(double2) * std::max<int64_t>(1, gt) * cap));
   NLD_CUDA(cudaMalloc(&ws.cbuf1, sizeof(double2) * std::max<int64_t>(1, gt) * cap));
@@ -1113,10 +1120,9 @@ void ensure_workspace(nld_operator* op, const PlanSet& ps, int nrhs) {
   }
   {
     // sliced gather: G digits of every cell and 16-rhs group, rebuilt per product
-    const int64_t nc = std::max(ps.n_cells, std::max(op->sets[0].n_cells, op->sets[1].n_cells));
-    if (use_ozaki() && nc > 0) {
-      NLD_CUDA(cudaMalloc(&ws.gdig, (size_t)gather_gdig_bytes() * nc * std::max(1, cap / 16)));
-      ws.gdig_cells = nc;
+    if (oz_shape && cap >= 16) {
+      NLD_CUDA(cudaMalloc(&ws.gdig, (size_t)gather_gdig_bytes() * nc_need * (cap / 16)));
+      ws.gdig_cells = nc_need;
     }
   }
   ws.nrhs_cap = cap;
@@ -1244,11 +1250,12 @@ static void gather_window(nld_operator* op, const PlanSet& ps, int w, int nrhs,
 // spread of all windows into the support boxes ws.grid_in [nrhs][grid_total]
 // (+ the shard allreduce).  vt: right-hand sides pixel-major [N][nrhs].
 int spread_stage(nld_operator* op, const PlanSet& ps, const double* vt, int nrhs,
-                 cudaStream_t st) {
+                 cudaStream_t st, bool flags) {
   const int L = (int)ps.wdev_h.size();
   for (int w = 0; w < L; ++w) spread_window(op, ps, w, vt, nrhs, st);
   for (int w = 0; w < L; ++w) assemble_window(op, ps, w, vt, nrhs, st);
-  comm_device(op, op->ws.grid_in, ps.grid_total * nrhs, st);
+  // the non-finite flags ride behind the grids in the same allreduce
+  comm_device(op, op->ws.grid_in, ps.grid_total * nrhs + (flags ? nrhs : 0), st);
   return 2 * L;
 }
 
@@ -1306,9 +1313,10 @@ void apply_op(nld_operator* op, int which, int kind, const double* v, double* ou
     ++launches;
   }
   const bool sliced = use_ozaki() && op->params.cutoff == 4 && nrhs % 16 == 0;
+  double* const flags = ws.grid_in + ps.grid_total * nrhs;
   if (sliced) {
-    ozaki_vmax(vt, N, nrhs, ws.vmax, st);
-    launches += 1;   // k_vmax (its reset is a memset, not a kernel)
+    ozaki_vmax(vt, N, nrhs, ws.vmax, flags, st);
+    launches += 1;   // k_vmax (its resets are memsets, not kernels)
   }
   static int no_overlap = -1;
   if (no_overlap < 0) {
@@ -1361,7 +1369,7 @@ void apply_op(nld_operator* op, int which, int kind, const double* v, double* ou
       gather_w(w);
     }
   } else {
-    spread_stage(op, ps, vt, nrhs, st);
+    spread_stage(op, ps, vt, nrhs, st, sliced);
     ev.mark();
     ev.mark();
     for (int w = 0; w < L; ++w) conv_window(op, ps, w, nrhs, st);
@@ -1399,6 +1407,11 @@ void apply_op(nld_operator* op, int which, int kind, const double* v, double* ou
     }
     NLD_CUDA(cudaGetLastError());
     if (!fused) ++launches;
+  }
+  if (sliced) {
+    // NaN into the columns of non-finite right-hand sides (a no-op otherwise)
+    ozaki_poison(flags, nrhs, out, N, ld, pixel_major || nrhs == 1, st);
+    ++launches;
   }
   ev.mark();
   op->stats.launches = launches;

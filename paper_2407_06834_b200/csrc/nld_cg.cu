@@ -481,11 +481,27 @@ void dev_basis(const double* v, const double* x, double* out, int64_t n, int adj
   cudaFreeAsync(s, st);
 }
 
+struct Scratch {
+  cudaStream_t st;
+  std::vector<void*> p;
+  ~Scratch() {
+    for (void* q : p) cudaFreeAsync(q, st);
+  }
+  template <class T>
+  T* alloc(size_t count) {
+    void* q = nullptr;
+    NLD_CUDA(cudaMallocAsync(&q, sizeof(T) * std::max<size_t>(count, 1), st));
+    p.push_back(q);
+    return static_cast<T*>(q);
+  }
+};
+
 void cg_solve(nld_operator* op, const double* f, double* u, int nrhs, int64_t ld,
               const double* lam, const double* mu, int prec, int deflate, double tol,
               int maxit, int warm, int* iters, double* relres, int* conv, double* hist,
               int hist_cap, cudaStream_t st) {
   const int64_t N = op->N;
+  if (nrhs > kRT) throw Error(NLD_ERR_VALUE, "at most 256 right-hand sides per solve");
   if (deflate && op->N_global < 2)
     throw Error(NLD_ERR_DIMENSION, "basis needs at least two entries");
   for (int r = 0; r < nrhs; ++r)
@@ -511,6 +527,9 @@ void cg_solve(nld_operator* op, const double* f, double* u, int nrhs, int64_t ld
     op->built[0] = true;
   }
   const double* eta = degree(0);
+  // stream-ordered scratch, released on every exit (including the throws
+  // below: breakdown, communicator failure)
+  Scratch scratch{st, {}};
   double* eta2 = nullptr;
   if (prec == NLD_PREC_L2) {
     if (op->params.mode != 1 && !op->built[1]) {
@@ -519,7 +538,7 @@ void cg_solve(nld_operator* op, const double* f, double* u, int nrhs, int64_t ld
     }
     degree(1);
     // degree_squared = apply_squared(1) * L (kernel.py:148-154)
-    NLD_CUDA(cudaMallocAsync(&eta2, sizeof(double) * N, st));
+    eta2 = scratch.alloc<double>(N);
     dev_axpby((double)op->L, op->eta[1], 0.0, op->eta[1], eta2, N, st);
   }
 
@@ -548,10 +567,8 @@ void cg_solve(nld_operator* op, const double* f, double* u, int nrhs, int64_t ld
   c.L = op->L;
   c.prec = prec;
   c.deflate = deflate;
-  RhsScal* scd = nullptr;
-  double* coef = nullptr;
-  NLD_CUDA(cudaMallocAsync(&scd, sizeof(RhsScal) * nrhs, st));
-  NLD_CUDA(cudaMallocAsync(&coef, sizeof(double) * 2 * nrhs, st));
+  RhsScal* scd = scratch.alloc<RhsScal>(nrhs);
+  double* coef = scratch.alloc<double>(2 * nrhs);
   std::vector<RhsScal> sc(nrhs);
   std::vector<double> hcoef(2 * nrhs);
   for (int r = 0; r < nrhs; ++r) {
@@ -572,7 +589,6 @@ void cg_solve(nld_operator* op, const double* f, double* u, int nrhs, int64_t ld
       apply_op(op, 0, NLD_APPLY_SYSTEM, in, out, nrhs, N, coef, eta, st, 1);
   };
   const double dN = (double)op->N_global;
-  if (nrhs > kRT) throw Error(NLD_ERR_VALUE, "at most 256 right-hand sides per solve");
   Reducer red(op, nrhs, N, st);
   const int eg = eblocks(N * nrhs);
 
@@ -858,10 +874,6 @@ void cg_solve(nld_operator* op, const double* f, double* u, int nrhs, int64_t ld
             k < (int)H[r].size() ? H[r][k] : std::numeric_limits<double>::quiet_NaN();
     }
   }
-  cudaFreeAsync(scd, st);
-  cudaFreeAsync(coef, st);
-  if (eta2) cudaFreeAsync(eta2, st);
-  NLD_CUDA(cudaStreamSynchronize(st));
 }
 
 }  // namespace nld

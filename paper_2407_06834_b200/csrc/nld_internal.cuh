@@ -211,7 +211,10 @@ void launch_spread_oz(const PlanSet& ps, const SubDev* subs, const int16_t* ex,
                       const int64_t* ychunk, unsigned nsub, const unsigned long long* vmax,
                       const double* vt, int nrhs, double* blocks, cudaStream_t st,
                       const int32_t* order = nullptr);
-void ozaki_vmax(const double* vt, int64_t n, int nrhs, unsigned long long* out, cudaStream_t st);
+void ozaki_vmax(const double* vt, int64_t n, int nrhs, unsigned long long* out, double* flag,
+                cudaStream_t st);
+void ozaki_poison(const double* flag, int nrhs, double* out, int64_t n, int64_t ld,
+                  int pixel_major, cudaStream_t st);
 void ozaki_prof_dump(const char* what, cudaStream_t st);
 namespace mma { struct GatherEpi; }
 void launch_gather_oz(const PlanSet& ps, const SubDev* subs, const int16_t* ex,
@@ -232,7 +235,7 @@ void apply_op(nld_operator* op, int which, int kind, const double* v,
 
 // the two halves of a product, reused by the NFFT transform API
 int spread_stage(nld_operator* op, const PlanSet& ps, const double* vt, int nrhs,
-                 cudaStream_t st);
+                 cudaStream_t st, bool flags = false);
 int gather_stage(nld_operator* op, const PlanSet& ps, int nrhs, cudaStream_t st);
 
 void dense_apply(nld_operator* op, int which, int kind, const double* v,

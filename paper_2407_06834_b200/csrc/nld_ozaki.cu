@@ -75,7 +75,11 @@ __device__ __forceinline__ double pow2(int e) {
 // exponent bound: |x| < 2^e for all x with max |x| = m (0 -> 0).  Callers
 // clamp it below at -900 so every 2^(46 - e) scale stays finite; a clamped
 // (tiny) operand then keeps fewer significant digits, never a wrong scale.
-__device__ __forceinline__ int exp_bound(double m) { return m > 0.0 ? ilogb(m) + 1 : 0; }
+// Non-finite m (a NaN/Inf right-hand side, flagged by k_vmax and poisoned
+// after the product) gets 0, so no scale ever overflows.
+__device__ __forceinline__ int exp_bound(double m) {
+  return (m > 0.0 && m <= 1.7976931348623157e308) ? ilogb(m) + 1 : 0;
+}
 
 // canonical K-major no-swizzle offset in a (rows x 32 bytes) tile
 __device__ __forceinline__ int canon32(int row, int k) {
@@ -168,17 +172,49 @@ __global__ void k_sub_exponents(const SubDev* __restrict__ subs, const WinDev* _
 // ---- per-rhs exponent of max |v| over all pixels ---------------------------
 // (the X rows are scaled by the rhs's global max |v| times the subproblem's
 // max |A_a|; relative to a per-cell max this costs bits only where |v| is
-// far below its global max, i.e. where the products are small anyway)
-__global__ void k_vmax(const double* __restrict__ vt, int64_t n, int nrhs,
-                       unsigned long long* __restrict__ out) {
-  const int r = threadIdx.x % nrhs;
-  const int rows_per_block = blockDim.x / nrhs;
-  double m = 0.0;
-  for (int64_t i = blockIdx.x * (int64_t)rows_per_block + threadIdx.x / nrhs; i < n;
-       i += (int64_t)gridDim.x * rows_per_block)
-    m = fmax(m, fabs(vt[i * nrhs + r]));
-  if (threadIdx.x < rows_per_block * nrhs)
-    atomicMax(&out[r], (unsigned long long)__double_as_longlong(m));
+// far below its global max, i.e. where the products are small anyway).
+// The max is taken over the bit patterns of |v| (sign cleared): NaN > Inf >
+// every finite value, so a non-finite entry is never dropped (fmax would drop
+// NaN).  Such a rhs also sets flag[r] = 1: the digit slices of NaN/Inf are
+// meaningless, so the product poisons that column afterwards (k_poison), as
+// the reference's numpy arithmetic would propagate it (transform.py:323-333).
+__global__ void __launch_bounds__(256)
+k_vmax(const double* __restrict__ vt, int64_t n, int nrhs, unsigned long long* __restrict__ out,
+       double* __restrict__ flag) {
+  const int rows = nrhs <= 256 ? 256 / nrhs : 1;
+  const int r0 = nrhs <= 256 ? threadIdx.x % nrhs : threadIdx.x;
+  const int rstep = nrhs <= 256 ? nrhs : 256;
+  const int64_t row0 = (int64_t)blockIdx.x * rows + (nrhs <= 256 ? threadIdx.x / nrhs : 0);
+  if (nrhs <= 256 && threadIdx.x >= rows * nrhs) return;
+  for (int r = r0; r < nrhs; r += rstep) {
+    unsigned long long m = 0ull;
+    for (int64_t i = row0; i < n; i += (int64_t)gridDim.x * rows)
+      m = max(m, (unsigned long long)__double_as_longlong(vt[i * nrhs + r]) & 0x7fffffffffffffffull);
+    if (m) atomicMax(&out[r], m);
+    if (m >= 0x7ff0000000000000ull) flag[r] = 1.0;
+  }
+}
+
+// NaN into every column r of a product whose flag[r] is set (rhs-major
+// [nrhs][ld] or pixel-major [N][nrhs]); a no-op unless some flag is set
+__global__ void __launch_bounds__(256)
+k_poison(const double* __restrict__ flag, int nrhs, double* __restrict__ out, int64_t n,
+         int64_t ld, int pixel_major) {
+  __shared__ int any;
+  if (threadIdx.x == 0) {
+    int a = 0;
+    for (int r = 0; r < nrhs; ++r) a |= flag[r] != 0.0;
+    any = a;
+  }
+  __syncthreads();
+  if (!any) return;
+  const int64_t total = n * nrhs;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = pixel_major ? e / nrhs : e % n;
+    const int r = (int)(pixel_major ? e % nrhs : e / n);
+    if (flag[r] != 0.0) out[pixel_major ? e : (int64_t)r * ld + i] = __longlong_as_double(0x7ff8000000000000ll);
+  }
 }
 
 // ---- plan-time Y digits for the sliced spread (PY) ------------------------
@@ -2029,11 +2065,19 @@ void ozaki_prof_dump(const char* what, cudaStream_t st) {
 void ozaki_prof_dump(const char*, cudaStream_t) {}
 #endif
 
-void ozaki_vmax(const double* vt, int64_t n, int nrhs, unsigned long long* out, cudaStream_t st) {
+void ozaki_vmax(const double* vt, int64_t n, int nrhs, unsigned long long* out, double* flag,
+                cudaStream_t st) {
   NLD_CUDA(cudaMemsetAsync(out, 0, sizeof(unsigned long long) * nrhs, st));
-  const int rows = std::max(1, 256 / nrhs);
-  oz::k_vmax<<<(unsigned)std::min<int64_t>((n + rows - 1) / rows, 148 * 8), rows * nrhs, 0, st>>>(
-      vt, n, nrhs, out);
+  NLD_CUDA(cudaMemsetAsync(flag, 0, sizeof(double) * nrhs, st));
+  const int rows = nrhs <= 256 ? 256 / nrhs : 1;
+  oz::k_vmax<<<(unsigned)std::min<int64_t>((n + rows - 1) / rows, 148 * 8), 256, 0, st>>>(
+      vt, n, nrhs, out, flag);
+  NLD_CUDA(cudaGetLastError());
+}
+
+void ozaki_poison(const double* flag, int nrhs, double* out, int64_t n, int64_t ld,
+                  int pixel_major, cudaStream_t st) {
+  oz::k_poison<<<148 * 4, 256, 0, st>>>(flag, nrhs, out, n, ld, pixel_major);
   NLD_CUDA(cudaGetLastError());
 }
 

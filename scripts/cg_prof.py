@@ -9,7 +9,7 @@ import torch
 
 sys.path.insert(0, ".")
 import paper_2407_06834_b200 as nld  # noqa: E402
-from paper_2407_06834_b200 import synth  # noqa: E402
+import synth  # noqa: E402
 
 feats, wins, f_img = synth.make_problem("c4")
 op = nld.AnovaOperator(torch.from_numpy(feats).cuda(), wins, synth.SIGMA,

@@ -8,7 +8,7 @@ import torch
 sys.path.insert(0, ".")
 import paper_2407_06834_b200 as nld  # noqa: E402
 from oracle import nfft_oracle as O  # noqa: E402
-from paper_2407_06834_b200 import synth  # noqa: E402
+import synth  # noqa: E402
 
 PIN = dict(n_expansion=32, cutoff=4, oversampling=2.0)
 

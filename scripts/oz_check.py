@@ -14,7 +14,8 @@ if sys.argv[1] == "cmp":
 import torch  # noqa: E402
 sys.path.insert(0, ".")
 import paper_2407_06834_b200 as nld  # noqa: E402
-from paper_2407_06834_b200 import _lib, synth  # noqa: E402
+from paper_2407_06834_b200 import _lib  # noqa: E402
+import synth  # noqa: E402
 
 cfg, nrhs, out = sys.argv[1], int(sys.argv[2]), sys.argv[3]
 feats, wins, _ = synth.make_problem(cfg)

@@ -6,7 +6,8 @@ import torch
 
 sys.path.insert(0, ".")
 import paper_2407_06834_b200 as nld  # noqa: E402
-from paper_2407_06834_b200 import _lib, synth  # noqa: E402
+from paper_2407_06834_b200 import _lib  # noqa: E402
+import synth  # noqa: E402
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "c4"
 nrhs = int(sys.argv[2]) if len(sys.argv) > 2 else 16

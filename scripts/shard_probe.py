@@ -8,7 +8,8 @@ import torch
 
 sys.path.insert(0, ".")
 import paper_2407_06834_b200 as nld  # noqa: E402
-from paper_2407_06834_b200 import _lib, synth  # noqa: E402
+from paper_2407_06834_b200 import _lib  # noqa: E402
+import synth  # noqa: E402
 
 feats, wins, _ = synth.make_problem("c4")
 n = feats.shape[0]

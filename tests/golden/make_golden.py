@@ -31,7 +31,7 @@ from nldenoise import kernel as ref_kernel  # noqa: E402
 from nldenoise import linops as ref_linops  # noqa: E402
 from nldenoise import transform as ref_transform  # noqa: E402
 
-from paper_2407_06834_b200 import synth  # noqa: E402
+import synth  # noqa: E402
 
 PLAN_KW = dict(n_expansion=synth.N_EXPANSION, cutoff=synth.CUTOFF,
                oversampling=synth.OVERSAMPLING)

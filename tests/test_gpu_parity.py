@@ -20,7 +20,7 @@ from conftest import GOLDEN  # noqa: E402
 
 import paper_2407_06834_b200 as nld  # noqa: E402
 from oracle import nfft_oracle as O  # noqa: E402
-from paper_2407_06834_b200 import synth  # noqa: E402
+import synth  # noqa: E402
 
 PIN = dict(n_expansion=synth.N_EXPANSION, cutoff=synth.CUTOFF,
            oversampling=synth.OVERSAMPLING)

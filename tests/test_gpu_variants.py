@@ -23,7 +23,8 @@ import json, sys
 import numpy as np, torch
 sys.path.insert(0, %r)
 import paper_2407_06834_b200 as nld
-from paper_2407_06834_b200 import _lib, synth
+from paper_2407_06834_b200 import _lib
+import synth
 g = dict(np.load(%r))
 feats, wins, _ = synth.make_problem("c1")
 op = nld.AnovaOperator(torch.from_numpy(feats).cuda(), wins, synth.SIGMA,

@@ -4,7 +4,8 @@ import numpy as np
 import pytest
 
 import paper_2407_06834_b200 as nld
-from paper_2407_06834_b200 import _lib, synth
+from paper_2407_06834_b200 import _lib
+import synth
 
 
 class TestValidation:

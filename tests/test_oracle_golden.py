@@ -10,7 +10,7 @@ import numpy as np
 import pytest
 
 from oracle import nfft_oracle as O
-from paper_2407_06834_b200 import synth
+import synth
 
 PIN = dict(n_expansion=32, cutoff=4, oversampling=2.0)
 

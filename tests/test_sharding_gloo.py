@@ -43,7 +43,7 @@ def _worker(rank, world, port, q):
     try:
         from oracle import nfft_oracle as O
         from paper_2407_06834_b200 import sharding as S
-        from paper_2407_06834_b200 import synth
+        import synth
         comm_rank[0] = rank
         comm = S.TorchComm()
         res = {}
