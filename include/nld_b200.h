@@ -55,7 +55,7 @@ extern "C" {
  * ld ignored) -- the kernels' native layout, no transposes */
 #define NLD_LAYOUT_PIXEL_MAJOR 0x100
 
-/* preconditioners for nld_cg_solve (linops.py:447-454) */
+/* preconditioners for nld_cg_solve (deflated_solve's prec, linops.py:286-293) */
 #define NLD_PREC_NONE 0
 #define NLD_PREC_JACOBI 1
 #define NLD_PREC_L2 2
@@ -72,7 +72,11 @@ typedef int (*nld_allreduce_fn)(void* ctx, void* buf, int64_t count, int32_t dty
 
 /* NFFT / fast-summation parameters, FastsumPlan.build (transform.py:273-283).
  * n_expansion <= 0 selects the reference's adaptive expansion_degree
- * (transform.py:254-258); mode 0 = "fast", 1 = "exact" (kernel.py:28-29). */
+ * (transform.py:254-258); mode 0 = "fast", 1 = "exact" (kernel.py:28-29).
+ * digit_tables (memory budget of the 16k-rhs tensor-core path, no effect on
+ * results beyond rounding): 0 = build the plan-time digit tables of 3-D m = 4
+ * windows when each fits in half of the free device memory (default), 1 = never
+ * (those products then run on the fp64 DMMA kernels). */
 typedef struct {
   int32_t n_expansion;
   int32_t cutoff;
@@ -80,7 +84,7 @@ typedef struct {
   double rmax;
   double truncation_eps;
   int32_t mode;
-  int32_t reserved;
+  int32_t digit_tables;
   int64_t dense_limit;
 } nld_params;
 

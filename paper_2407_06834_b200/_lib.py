@@ -41,7 +41,7 @@ class Params(ctypes.Structure):
     _fields_ = [("n_expansion", ctypes.c_int32), ("cutoff", ctypes.c_int32),
                 ("oversampling", ctypes.c_double), ("rmax", ctypes.c_double),
                 ("truncation_eps", ctypes.c_double), ("mode", ctypes.c_int32),
-                ("reserved", ctypes.c_int32), ("dense_limit", ctypes.c_int64)]
+                ("digit_tables", ctypes.c_int32), ("dense_limit", ctypes.c_int64)]
 
 
 class WindowInfo(ctypes.Structure):

@@ -101,7 +101,11 @@ extern "C" {
 
 const char* nld_last_error(void) { return nld::g_last_error.c_str(); }
 
+#ifdef NLD_AB_BUILD
+int nld_abi_version(void) { return 1000 + NLD_ABI_VERSION; }   // test build: never the product
+#else
 int nld_abi_version(void) { return NLD_ABI_VERSION; }
+#endif
 
 int nld_op_create(const double* features_dev, int64_t n, int32_t n_features,
                   const int32_t* window_index, const int32_t* window_offset,

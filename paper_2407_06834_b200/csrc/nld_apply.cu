@@ -28,6 +28,7 @@
 #include <cstdlib>
 
 #include "nld_internal.cuh"
+#include "nld_switch.cuh"
 #include "nld_mma.cuh"
 
 namespace nld {
@@ -681,7 +682,9 @@ __global__ void __launch_bounds__(kEpiThreads, NLD_EPI_MINB)
 k_epilogue_tiled(int kind, int L, int64_t N, int lg_nrhs, const double* __restrict__ v,
                  int64_t ldv, const double* __restrict__ wsum, double* __restrict__ out,
                  int64_t ldo, const double* __restrict__ eta, const double* __restrict__ coef) {
-  __shared__ double tile[kEpiElems + kEpiElems / 16];
+  // rows of TP + 1 (odd stride: conflict-free for the 8-byte accesses); the
+  // host routes nrhs <= 256 here, so at most 2048 + 256 doubles
+  __shared__ double tile[kEpiElems + 256];
   const int nrhs = 1 << lg_nrhs;
   const int lg_tp = 11 - lg_nrhs;           // TP = 2048 / nrhs
   const int TP = 1 << lg_tp;
@@ -705,7 +708,7 @@ k_epilogue_tiled(int kind, int L, int64_t N, int lg_nrhs, const double* __restri
     for (int k = 0; k < kEpiPer; ++k) {
       const int e = tid + k * kEpiThreads;     // e = p * nrhs + r
       const int p = e >> lg_nrhs, r = e & (nrhs - 1);
-      tile[r * (TP + 8) + p] = s[k];           // rhs-major, padded rows
+      tile[r * (TP + 1) + p] = s[k];           // rhs-major, padded rows
     }
     __syncthreads();
 #pragma unroll
@@ -715,7 +718,7 @@ k_epilogue_tiled(int kind, int L, int64_t N, int lg_nrhs, const double* __restri
       const int64_t i = i0 + p;
       if (i >= N) continue;
       const double x = v[r * ldv + i];
-      const double sum = tile[r * (TP + 8) + p];
+      const double sum = tile[r * (TP + 1) + p];
       double y;
       if (kind == NLD_APPLY_WINDOW_SUM) {
         y = sum;
@@ -898,14 +901,7 @@ int grid_blocks(int64_t n, int threads, int cap = 148 * 8) {
 
 // NLD_NO_MMA=1 selects the CUDA-core (DFMA) kernels for the 3-D m=4 shape
 // (kept for A/B measurements; both paths are hand-written sm_100a CUDA).
-bool use_mma() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("NLD_NO_MMA");
-    v = (e && e[0] && e[0] != '0') ? 0 : 1;
-  }
-  return v == 1;
-}
+bool use_mma() { return !ab_switch("NLD_NO_MMA", 0); }
 
 // ---- per-window launchers -----------------------------------------------
 
@@ -1012,21 +1008,12 @@ void spread_window_fast(const PlanSet& ps, const Workspace& ws, int w, const dou
   } else if (wp.d == 2) {
     launch_spread<2, MC>(subs, nsub, ps, ws, vt, nrhs, st);
   } else if (MC == 4 && use_mma()) {
-    static int rpw4 = -1;
-    if (rpw4 < 0) {
-      const char* e = getenv("NLD_SPREAD_RPW4");
-      rpw4 = (e && e[0] && e[0] != '0') ? 1 : 0;
-    }
-    static int bc = -1;   // shared (B (x) C) spread: default, NLD_SPREAD_BC=0 for A/B
-    if (bc < 0) {
-      const char* e = getenv("NLD_SPREAD_BC");
-      bc = (e && e[0] == '0') ? 0 : 1;
-    }
-    if (use_ozaki() && nrhs % 16 == 0 && ps.sub_exp && !getenv("NLD_OZAKI_NO_SPREAD")) {
-      launch_spread_oz(ps, subs, ps.sub_exp + wp.sub_off * 24,
-                       ps.ychunk ? ps.ychunk + wp.sub_off : nullptr, nsub, ws.vmax, vt, nrhs,
-                       ws.blocks, st, ps.sub_order ? ps.sub_order + wp.sub_off : nullptr);
-      if (getenv("NLD_OZ_PROF_PRINT")) ozaki_prof_dump("spread", st);
+    const int rpw4 = ab_switch("NLD_SPREAD_RPW4", 0);
+    const int bc = ab_switch("NLD_SPREAD_BC", 1);   // shared (B (x) C) DMMA spread
+    if (use_ozaki() && nrhs % 16 == 0 && ps.sub_exp && ps.ydig && ps.ychunk && ps.sub_order &&
+        !ab_switch("NLD_OZAKI_NO_SPREAD", 0)) {
+      launch_spread_oz(ps, subs, ps.sub_exp + wp.sub_off * 24, ps.ychunk + wp.sub_off, nsub,
+                       ws.vmax, vt, nrhs, ws.blocks, st, ps.sub_order + wp.sub_off);
     }
     else if (bc && nrhs % 16 == 0 && ((uintptr_t)vt & 15) == 0)
       launch_spread_bc(subs, nsub, ps, ws, vt, nrhs, st);
@@ -1047,19 +1034,14 @@ void gather_window_fast(const PlanSet& ps, const Workspace& ws, int w, int64_t N
   const unsigned nsub = (unsigned)wp.n_subs;
   if (wp.d == 1) launch_gather<1, MC>(subs, nsub, ps, ws, N, nrhs, st);
   else if (wp.d == 2) launch_gather<2, MC>(subs, nsub, ps, ws, N, nrhs, st);
-  else if (MC == 4 && use_ozaki() && nrhs % 16 == 0 && ps.sub_exp && !getenv("NLD_OZAKI_NO_GATHER"))
-    launch_gather_oz(ps, subs, ps.sub_exp + wp.sub_off * 24, ps.sub_order + wp.sub_off, nsub, ws.grid_out, ps.grid_total,
-                     ep.mode == mma::kGatherStore ? ws.wout + (int64_t)w * N * nrhs : out, N, nrhs,
-                     ep, st, ws.gdig, w < (int)ps.gcell_lo.size() ? ps.gcell_lo[w] : 0,
-                     w < (int)ps.gcell_n.size() ? ps.gcell_n[w] : 0,
-                     ps.ychunk ? ps.ychunk + wp.sub_off : nullptr);
+  else if (MC == 4 && use_ozaki() && nrhs % 16 == 0 && ps.gtile && ws.gdig &&
+           w < (int)ps.gcell_n.size() && ps.gcell_n[w] > 0)
+    launch_gather_nm(ps, subs, ps.sub_exp + wp.sub_off * 24, ps.sub_order + wp.sub_off,
+                     ps.gtile_off + wp.sub_off, nsub, ws.grid_out, ps.grid_total,
+                     ep.mode == mma::kGatherStore ? ws.wout + (int64_t)w * N * nrhs : out, nrhs,
+                     ep, st, ws.gdig, ps.gcell_lo[w], ps.gcell_n[w]);
   else if (MC == 4 && use_mma()) launch_gather_mma(subs, nsub, ps, ws, N, nrhs, st, ep, out);
   else launch_gather<3, MC>(subs, nsub, ps, ws, N, nrhs, st);
-  const bool oz_used = wp.d == 3 && MC == 4 && use_ozaki() && nrhs % 16 == 0 && ps.sub_exp &&
-                       !getenv("NLD_OZAKI_NO_GATHER");
-  if (!oz_used) return;
-  // ---- debug / profiling aids of the sliced gather (environment-gated) ----
-  if (MC == 4 && use_ozaki() && getenv("NLD_OZ_PROF_PRINT")) ozaki_prof_dump("gather", st);
 }
 
 struct EvScope {
@@ -1298,7 +1280,8 @@ void apply_op(nld_operator* op, int which, int kind, const double* v, double* ou
               cudaStream_t st, int pixel_major) {
   const PlanSet& ps = op->sets[which];
   ensure_workspace(op, ps, nrhs);
-  if (use_ozaki() && op->params.cutoff == 4) ozaki_exponents(op->sets[which], st);
+  if (use_ozaki() && op->params.cutoff == 4)
+    ozaki_exponents(op->sets[which], op->params.digit_tables == 0, st);
   Workspace& ws = op->ws;
   const int64_t N = op->N;
   const int L = op->L;
@@ -1318,19 +1301,11 @@ void apply_op(nld_operator* op, int which, int kind, const double* v, double* ou
     ozaki_vmax(vt, N, nrhs, ws.vmax, flags, st);
     launches += 1;   // k_vmax (its resets are memsets, not kernels)
   }
-  static int no_overlap = -1;
-  if (no_overlap < 0) {
-    const char* e = getenv("NLD_NO_OVERLAP");
-    no_overlap = (e && e[0] && e[0] != '0') ? 1 : 0;
-  }
+  const int no_overlap = ab_switch("NLD_NO_OVERLAP", 0);
   const bool overlap = !op->comm && L <= 16 && !no_overlap;
   // fused gather epilogue (see gather_window): every window on the DMMA
   // gather, pixel-major in/out, out not aliasing v
-  static int no_fuse = -1;
-  if (no_fuse < 0) {
-    const char* e = getenv("NLD_NO_FUSED_EPILOGUE");
-    no_fuse = (e && e[0] && e[0] != '0') ? 1 : 0;
-  }
+  const int no_fuse = ab_switch("NLD_NO_FUSED_EPILOGUE", 0);
   bool fused = !no_fuse && pixel_major && nrhs >= 8 && L >= 2 && out != v &&
                op->params.cutoff == 4 && use_mma();
   for (int w = 0; w < L && fused; ++w) {
@@ -1390,7 +1365,7 @@ void apply_op(nld_operator* op, int which, int kind, const double* v, double* ou
   // 5. epilogue
   {
     int lg = -1;
-    for (int k = 0; k <= 11; ++k)
+    for (int k = 0; k <= 8; ++k)
       if ((1 << k) == nrhs) lg = k;
     if (fused) {
       // done inside the last window's gather

@@ -158,11 +158,7 @@ k_spread_mma(const SubDev* __restrict__ subs, const WinDev* __restrict__ wins,
     stage(0, 0);
     for (int ck = 0; ck < nchunk; ++ck) {
       const int buf = ck & 1;
-#ifdef NLD_EXP_NOSTAGE
-      if (ck == 0 && nchunk > 1) {
-#else
       if (ck + 1 < nchunk) {
-#endif
         stage(ck + 1, buf ^ 1);
         cp_wait<1>();
       } else {
@@ -190,18 +186,10 @@ k_spread_mma(const SubDev* __restrict__ subs, const WinDev* __restrict__ wins,
           const double aw = row[2 * kS + g];
           double af[RPW];
 #pragma unroll
-#ifdef NLD_EXP_NODMUL
-          for (int q = 0; q < RPW; ++q) af[q] = q ? aw : V[j * vst + q0 + q];
-#else
           for (int q = 0; q < RPW; ++q) af[q] = V[j * vst + q0 + q] * aw;
-#endif
 #pragma unroll
           for (int n = 0; n < 8; ++n) {
-#ifdef NLD_EXP_NODMUL
-            const double bf = n & 1 ? bw[n] : cw;
-#else
             const double bf = bw[n] * cw;
-#endif
 #pragma unroll
             for (int q = 0; q < RPW; ++q) dmma(acc[q][n], af[q], bf);
           }
@@ -594,11 +582,7 @@ k_gather_mma16(const SubDev* __restrict__ subs, const CellDev* __restrict__ cell
         const double wa = aw[a];
 #pragma unroll
         for (int ks = 0; ks < 16; ++ks) {
-#ifdef NLD_EXP_GNODMUL
-          const double w = (a & 1) ? bc[ks] : wa;
-#else
           const double w = bc[ks] * wa;
-#endif
           const int k = a * 64 + 4 * ks;
           dmma(acc[0][ks & 3], G0[k], w);
           if (two) dmma(acc[1][ks & 3], G1[k], w);

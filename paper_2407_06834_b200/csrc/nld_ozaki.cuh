@@ -1,0 +1,212 @@
+// Shared device helpers of the integer-sliced (Ozaki) tensor-core kernels:
+// digit slicing, byte packing into the UMMA canonical layouts, the exact
+// int32 -> fp64 diagonal combine, cp.async / mbarrier plumbing.
+#pragma once
+
+#include <cstdint>
+
+#include "nld_umma.cuh"
+
+namespace nld {
+namespace oz {
+
+#ifndef NLD_OZ_SL
+#define NLD_OZ_SL 6
+#endif
+constexpr int kSl = NLD_OZ_SL;         // digits per operand
+
+// -DNLD_OZ_PROF: per-site clock64 totals of the pipeline waits (lane 0 of
+// each warp), printed after each launch -- a tuning aid, not built by default
+#ifdef NLD_OZ_PROF
+__device__ unsigned long long oz_prof[32];
+#define OZW(site, ...)                                                      \
+  do {                                                                      \
+    const long long _t0 = clock64();                                        \
+    __VA_ARGS__;                                                            \
+    if ((threadIdx.x & 31) == 0)                                            \
+      atomicAdd(&oz_prof[site], (unsigned long long)(clock64() - _t0));     \
+  } while (0)
+#else
+#define OZW(site, ...) __VA_ARGS__
+#endif
+constexpr int kRows = 128;             // M: (a, r) rows, r fastest
+constexpr int kChunk = 32;             // nodes per UMMA K step (32 bytes)
+constexpr int kThreads = 256;
+constexpr int kTmemCols = 512;         // kSl * 64 = 384 used
+constexpr int kABytes = kRows * kChunk;          // 4 KB per slice
+constexpr int kBBytes = 64 * kChunk;             // 2 KB per slice
+// X digits (the M = 128 operand) live in TMEM: per operand stage 6 slices x 8
+// columns after the 384 accumulator columns; shared memory holds only the Y
+// digits (and raw rows), halving the operand traffic through shared memory
+constexpr int kStageBytes = kSl * kBBytes;
+constexpr int kXTmem0 = kSl * 64;                // first X column (after the accumulator)
+constexpr int kExpPerSub = 24;         // eA[8] eB[8] eC[8]
+constexpr double kMagic = 4503599627370496.0 + 141289400074368.0;  // 2^52 + 0x808080808080
+
+__device__ __forceinline__ double pow2(int e) {
+  e = max(-1022, min(1023, e));
+  return __longlong_as_double((long long)(e + 1023) << 52);
+}
+
+// exponent bound: |x| < 2^e for all x with max |x| = m (0 -> 0).  Callers
+// clamp it below at -900 so every 2^(46 - e) scale stays finite; a clamped
+// (tiny) operand then keeps fewer significant digits, never a wrong scale.
+// Non-finite m (a NaN/Inf right-hand side, flagged by k_vmax and poisoned
+// after the product) gets 0, so no scale ever overflows.
+__device__ __forceinline__ int exp_bound(double m) {
+  return (m > 0.0 && m <= 1.7976931348623157e308) ? ilogb(m) + 1 : 0;
+}
+
+// canonical K-major no-swizzle offset in a (rows x 32 bytes) tile
+__device__ __forceinline__ int canon32(int row, int k) {
+  return (row >> 3) * 256 + (k >> 4) * 128 + (row & 7) * 16 + (k & 15);
+}
+
+// 4 elements' digit p (p = 0 most significant) packed into one word; element
+// i's 48-bit field is (hi_i & 0xffff) << 32 | lo_i
+__device__ __forceinline__ uint32_t digit_word(uint32_t l0, uint32_t l1, uint32_t l2, uint32_t l3,
+                                               uint32_t h0, uint32_t h1, uint32_t h2, uint32_t h3,
+                                               int p) {
+  const int byte = 5 - p;
+  const bool top = byte >= 4;
+  const uint32_t s0 = top ? h0 : l0, s1 = top ? h1 : l1, s2 = top ? h2 : l2, s3 = top ? h3 : l3;
+  const uint32_t k = byte & 3;
+  const uint32_t sel = k | ((k + 4) << 4);
+  const uint32_t w01 = __byte_perm(s0, s1, sel);
+  const uint32_t w23 = __byte_perm(s2, s3, sel);
+  return __byte_perm(w01, w23, 0x5410) ^ 0x80808080u;
+}
+
+#define NLD_DW(L, H, i, p) \
+  digit_word(L[i], L[i + 1], L[i + 2], L[i + 3], H[i], H[i + 1], H[i + 2], H[i + 3], p)
+
+// all six digit words of 4 elements (w[p] byte i = digit p of element i):
+// a 4x4 byte transpose of the low words and a 4x2 one of the high words,
+// 12 PRMT + 6 LOP instead of 6 x (3 PRMT + 1 LOP)
+__device__ __forceinline__ void pack4(const uint32_t* l, const uint32_t* h, uint32_t* w) {
+  const uint32_t a01 = __byte_perm(l[0], l[1], 0x5140), b01 = __byte_perm(l[0], l[1], 0x7362);
+  const uint32_t a23 = __byte_perm(l[2], l[3], 0x5140), b23 = __byte_perm(l[2], l[3], 0x7362);
+  const uint32_t h01 = __byte_perm(h[0], h[1], 0x5140), h23 = __byte_perm(h[2], h[3], 0x5140);
+  w[5] = __byte_perm(a01, a23, 0x5410) ^ 0x80808080u;
+  w[4] = __byte_perm(a01, a23, 0x7632) ^ 0x80808080u;
+  w[3] = __byte_perm(b01, b23, 0x5410) ^ 0x80808080u;
+  w[2] = __byte_perm(b01, b23, 0x7632) ^ 0x80808080u;
+  w[1] = __byte_perm(h01, h23, 0x5410) ^ 0x80808080u;
+  w[0] = __byte_perm(h01, h23, 0x7632) ^ 0x80808080u;
+}
+
+// store the 6 digit slices of 16 elements (lo/hi[16]) as one 16-byte word per
+// slice: dst + p * stride
+__device__ __forceinline__ void store16(const uint32_t (&lo)[16], const uint32_t (&hi)[16],
+                                        uint8_t* dst, int stride) {
+  uint32_t w[4][6];
+#pragma unroll
+  for (int g = 0; g < 4; ++g) pack4(lo + 4 * g, hi + 4 * g, w[g]);
+#pragma unroll
+  for (int p = 0; p < 6; ++p)
+    *reinterpret_cast<uint4*>(dst + p * stride) = make_uint4(w[0][p], w[1][p], w[2][p], w[3][p]);
+}
+__device__ __forceinline__ void store8(const uint32_t (&lo)[8], const uint32_t (&hi)[8],
+                                       uint8_t* dst, int stride) {
+  uint32_t w[2][6];
+#pragma unroll
+  for (int g = 0; g < 2; ++g) pack4(lo + 4 * g, hi + 4 * g, w[g]);
+#pragma unroll
+  for (int p = 0; p < 6; ++p)
+    *reinterpret_cast<uint2*>(dst + p * stride) = make_uint2(w[0][p], w[1][p]);
+}
+
+__device__ __forceinline__ void slice1(double x, double y, uint32_t& lo, uint32_t& hi) {
+  const long long u = __double_as_longlong(fma(x, y, kMagic));
+  lo = (uint32_t)u;
+  hi = (uint32_t)(u >> 32);
+}
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(umma::smem_u32(dst)), "l"(src));
+}
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(umma::smem_u32(dst)), "l"(src));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+__device__ __forceinline__ void cp_async_mbar_arrive(uint64_t* mbar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(umma::smem_u32(mbar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* mbar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(umma::smem_u32(mbar)) : "memory");
+}
+
+// sum_t D_t 2^(40 - 8t), t = 0..5, from the six int32 diagonals of a K = 64
+// product (|D_t| <= (t + 1) 2^20): the pairs D_2k 2^8 + D_2k+1 are exact in
+// int32 (|.| < 1.35e9), so three IMADs, three exact int32 -> fp64 conversions
+// and (X01 2^16 + X23) 2^16 + X45 with one rounding (the first FMA is exact).
+// The caller's scale carries the 2^-24 (vs sum_t D_t 2^(16 - 8t)).
+#ifndef NLD_OZ_COMBINE64
+#define NLD_OZ_COMBINE64 0
+#endif
+static_assert(kSl == 6, "combine6 assumes six digits");
+__device__ __forceinline__ double i2d(uint32_t x);
+template <int NCOL>
+__device__ __forceinline__ double combine6(const uint32_t (&dv)[6][NCOL], int i) {
+#if NLD_OZ_COMBINE64
+  // reference form: two exact 45-bit integers on the 64-bit integer path
+  const long long H = ((long long)(int32_t)dv[0][i] << 16) + ((long long)(int32_t)dv[1][i] << 8) +
+                      (long long)(int32_t)dv[2][i];
+  const long long L = ((long long)(int32_t)dv[3][i] << 16) + ((long long)(int32_t)dv[4][i] << 8) +
+                      (long long)(int32_t)dv[5][i];
+  const double hd = __longlong_as_double(H + 0x4338000000000000LL) - 6755399441055744.0;
+  const double ld = __longlong_as_double(L + 0x4338000000000000LL) - 6755399441055744.0;
+  return fma(ld, 5.9604644775390625e-08, hd) * 16777216.0;   // x 2^24 (exact)
+#else
+  const uint32_t x01 = dv[0][i] * 256u + dv[1][i];
+  const uint32_t x23 = dv[2][i] * 256u + dv[3][i];
+  const uint32_t x45 = dv[4][i] * 256u + dv[5][i];
+  return fma(fma(i2d(x01), 65536.0, i2d(x23)), 65536.0, i2d(x45));
+#endif
+}
+
+// The six diagonals as two exact fp64 parts, value = hi 2^32 + lo, with two
+// fp64 operations (the rest on the integer pipe): hi = x01 = D0 2^8 + D1 by
+// the int32 magic below; lo = x23 2^16 + x45 (|.| < 2^47) formed by one
+// IMAD.WIDE onto the bit pattern of 2^52 + 2^51 (+ 2^31, the bias that makes
+// x45 unsigned), whose mantissa then holds it exactly.  Callers accumulate
+// the hi and lo parts of their weighted sums separately.
+template <int NCOL>
+__device__ __forceinline__ void combine6_parts(const uint32_t (&dv)[6][NCOL], int i, double& hi,
+                                               double& lo);
+
+// exact int32 -> fp64 without I2F: 2^52 + 2^31 + x has x + 2^31 in its mantissa
+__device__ __forceinline__ double i2d(uint32_t x) {
+#ifdef NLD_OZ_I2F
+  return (double)(int32_t)x;
+#else
+  return __hiloint2double(0x43300000, (int)(x ^ 0x80000000u)) - 4503601774854144.0;
+#endif
+}
+
+// canonical K-major no-swizzle offset in a (rows x 64 bytes) tile
+__device__ __forceinline__ int canon64(int row, int k) {
+  return (row >> 3) * 512 + (k >> 4) * 128 + (row & 7) * 16 + (k & 15);
+}
+
+template <int NCOL>
+__device__ __forceinline__ void combine6_parts(const uint32_t (&dv)[6][NCOL], int i, double& hi,
+                                               double& lo) {
+  const uint32_t x01 = dv[0][i] * 256u + dv[1][i];
+  const int32_t x23 = (int32_t)(dv[2][i] * 256u + dv[3][i]);
+  const uint32_t x45b = dv[4][i] * 256u + (dv[5][i] ^ 0x80000000u);
+  double r;
+  asm("{\n\t.reg .b64 c;\n\tmov.b64 c, {%1, %2};\n\tmad.wide.s32 c, %3, 65536, c;\n\t"
+      "mov.b64 %0, c;\n\t}" : "=d"(r) : "r"(x45b), "r"(0x43380000u), "r"(x23));
+  lo = r - 6755401921888256.0;   // 2^52 + 2^51 + 2^31
+  hi = i2d(x01);
+}
+
+}  // namespace oz
+}  // namespace nld

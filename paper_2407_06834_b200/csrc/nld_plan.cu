@@ -849,7 +849,8 @@ void free_planset(PlanSet& ps) {
   cudaFree(ps.sub_exp);
   cudaFree(ps.sub_order);
   cudaFree(ps.ydig);
-  cudaFree(ps.gydig);
+  cudaFree(ps.gtile);
+  cudaFree(ps.gtile_off);
   cudaFree(ps.ychunk);
   cudaFree(ps.K);
   if (ps.owns_tables) {

@@ -113,6 +113,11 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
         "=r"(r[14]), "=r"(r[15])
       : "r"(taddr));
 }
+__device__ __forceinline__ void tmem_ld4(uint32_t taddr, uint32_t (&r)[4]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];\n"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(taddr));
+}
 __device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&r)[8]) {
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
@@ -129,7 +134,22 @@ __device__ __forceinline__ void mbar_init(uint64_t* mbar, uint32_t count) {
 __device__ __forceinline__ void mbar_fence_init() {
   asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
 }
+// try_wait with a suspend-time hint: a waiting warp is suspended until the
+// phase completes (or the hint elapses) instead of spinning, so waiting roles
+// do not steal issue slots from the working ones
+#ifndef NLD_MBAR_HINT
+#define NLD_MBAR_HINT 1
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* mbar, uint32_t parity) {
+#if NLD_MBAR_HINT
+  asm volatile(
+      "{\n\t.reg .pred done;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1, %2;\n\t"
+      "@!done bra WAIT_%=;\n\t}\n" ::"r"(smem_u32(mbar)),
+      "r"(parity), "r"(0x989680)
+      : "memory");
+#else
   asm volatile(
       "{\n\t.reg .pred done;\n\t"
       "WAIT_%=:\n\t"
@@ -137,6 +157,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* mbar, uint32_t parity) {
       "@!done bra WAIT_%=;\n\t}\n" ::"r"(smem_u32(mbar)),
       "r"(parity)
       : "memory");
+#endif
 }
 
 // TMA bulk copy global -> shared, completion counted on an mbarrier (bytes)
