@@ -73,10 +73,9 @@ typedef int (*nld_allreduce_fn)(void* ctx, void* buf, int64_t count, int32_t dty
 /* NFFT / fast-summation parameters, FastsumPlan.build (transform.py:273-283).
  * n_expansion <= 0 selects the reference's adaptive expansion_degree
  * (transform.py:254-258); mode 0 = "fast", 1 = "exact" (kernel.py:28-29).
- * digit_tables (memory budget of the 16k-rhs tensor-core path, no effect on
- * results beyond rounding): 0 = build the plan-time digit tables of 3-D m = 4
- * windows when each fits in half of the free device memory (default), 1 = never
- * (those products then run on the fp64 DMMA kernels). */
+ * no_sliced: 0 (default) runs 16k-rhs batches of 3-D m = 4 windows on the
+ * integer-sliced tcgen05 kernels (exact int8 digit products, fp64 combine);
+ * 1 runs them on the fp64 DMMA kernels (results agree to rounding). */
 typedef struct {
   int32_t n_expansion;
   int32_t cutoff;
@@ -84,7 +83,7 @@ typedef struct {
   double rmax;
   double truncation_eps;
   int32_t mode;
-  int32_t digit_tables;
+  int32_t no_sliced;
   int64_t dense_limit;
 } nld_params;
 

@@ -41,7 +41,7 @@ class Params(ctypes.Structure):
     _fields_ = [("n_expansion", ctypes.c_int32), ("cutoff", ctypes.c_int32),
                 ("oversampling", ctypes.c_double), ("rmax", ctypes.c_double),
                 ("truncation_eps", ctypes.c_double), ("mode", ctypes.c_int32),
-                ("digit_tables", ctypes.c_int32), ("dense_limit", ctypes.c_int64)]
+                ("no_sliced", ctypes.c_int32), ("dense_limit", ctypes.c_int64)]
 
 
 class WindowInfo(ctypes.Structure):
@@ -119,8 +119,13 @@ def _load():
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
-    if lib.nld_abi_version() != 1:
-        raise ImportError("libnld_b200.so ABI version mismatch")
+    ver = lib.nld_abi_version()
+    if ver == 1001 and os.environ.get("NLD_ALLOW_AB_BUILD") == "1":
+        # the test-only A/B build (make ab), swapped in deliberately by a script
+        import warnings
+        warnings.warn("loaded the A/B test build of libnld_b200.so")
+    elif ver != 1:
+        raise ImportError(f"{LIB_PATH}: ABI version {ver}, expected 1 (the product build)")
     return lib
 
 

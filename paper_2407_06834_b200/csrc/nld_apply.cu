@@ -1010,9 +1010,9 @@ void spread_window_fast(const PlanSet& ps, const Workspace& ws, int w, const dou
   } else if (MC == 4 && use_mma()) {
     const int rpw4 = ab_switch("NLD_SPREAD_RPW4", 0);
     const int bc = ab_switch("NLD_SPREAD_BC", 1);   // shared (B (x) C) DMMA spread
-    if (use_ozaki() && nrhs % 16 == 0 && ps.sub_exp && ps.ydig && ps.ychunk && ps.sub_order &&
+    if (use_ozaki() && nrhs % 16 == 0 && ps.oz_ok && ps.sub_exp && ps.sub_order &&
         !ab_switch("NLD_OZAKI_NO_SPREAD", 0)) {
-      launch_spread_oz(ps, subs, ps.sub_exp + wp.sub_off * 24, ps.ychunk + wp.sub_off, nsub,
+      launch_spread_oz(ps, subs, ps.sub_exp + wp.sub_off * 24, nsub,
                        ws.vmax, vt, nrhs, ws.blocks, st, ps.sub_order + wp.sub_off);
     }
     else if (bc && nrhs % 16 == 0 && ((uintptr_t)vt & 15) == 0)
@@ -1034,10 +1034,11 @@ void gather_window_fast(const PlanSet& ps, const Workspace& ws, int w, int64_t N
   const unsigned nsub = (unsigned)wp.n_subs;
   if (wp.d == 1) launch_gather<1, MC>(subs, nsub, ps, ws, N, nrhs, st);
   else if (wp.d == 2) launch_gather<2, MC>(subs, nsub, ps, ws, N, nrhs, st);
-  else if (MC == 4 && use_ozaki() && nrhs % 16 == 0 && ps.gtile && ws.gdig &&
+  else if (MC == 4 && use_ozaki() && nrhs % 16 == 0 && ps.oz_ok && ws.gdig &&
+           !ab_switch("NLD_OZAKI_NO_GATHER", 0) &&
            w < (int)ps.gcell_n.size() && ps.gcell_n[w] > 0)
     launch_gather_nm(ps, subs, ps.sub_exp + wp.sub_off * 24, ps.sub_order + wp.sub_off,
-                     ps.gtile_off + wp.sub_off, nsub, ws.grid_out, ps.grid_total,
+                     nsub, ws.grid_out, ps.grid_total,
                      ep.mode == mma::kGatherStore ? ws.wout + (int64_t)w * N * nrhs : out, nrhs,
                      ep, st, ws.gdig, ps.gcell_lo[w], ps.gcell_n[w]);
   else if (MC == 4 && use_mma()) launch_gather_mma(subs, nsub, ps, ws, N, nrhs, st, ep, out);
@@ -1281,7 +1282,7 @@ void apply_op(nld_operator* op, int which, int kind, const double* v, double* ou
   const PlanSet& ps = op->sets[which];
   ensure_workspace(op, ps, nrhs);
   if (use_ozaki() && op->params.cutoff == 4)
-    ozaki_exponents(op->sets[which], op->params.digit_tables == 0, st);
+    ozaki_exponents(op->sets[which], op->params.no_sliced == 0, st);
   Workspace& ws = op->ws;
   const int64_t N = op->N;
   const int L = op->L;

@@ -25,15 +25,21 @@
 //
 // Roles (one persistent CTA per SM, items = (subproblem, 16-rhs group) dealt
 // in snake order of descending size):
-//   warps 0-15  epilogue (lane quarter = warp & 3, rhs slot = warp >> 2)
-//   warp 16     UMMA issuer (one lane)
-//   warp 17     tile loader: per 128-node tile one TMA bulk copy of the Y
-//               digits (48 KB) and one of the A parts + pixel indices (8.5 KB)
-//               from the plan-time tile table (k_gtile)
-//   warp 18     G loader: per item one TMA bulk copy of the cell's G digits
+//   warps 0-7   epilogue (lane quarter = warp & 3, rhs slots 2 (warp >> 2) and
+//               2 (warp >> 2) + 1, i.e. rhs 8 (warp >> 2) .. + 7 of the group)
+//   warps 8-11  slicers: per 128-node tile the Y digits of each node (thread =
+//               node) from its staged weight row, into the operand stage
+//   warp 12     UMMA issuer (one lane): Y digits -> TMEM, 4 passes x 12 UMMAs
+//   warp 13     row loader: per tile one TMA bulk copy of the nodes' weight
+//               rows (A | B | C, 192 B each) + the pixel indices (cp.async)
+//   warp 14     G loader: per item one TMA bulk copy of the cell's G digits
 //               (48 KB + exponents, k_gdig_nm, once per product)
+// Cutting Y on the fly (64 values per node) reads 196 B per node-window
+// instead of streaming 452 B of precomputed digits + A parts: the gather's
+// HBM traffic, not its arithmetic, bounded it with plan-time digits.
 #include <algorithm>
 #include <cstdint>
+#include <cstdio>
 #include <vector>
 
 #include "nld_epi.cuh"
@@ -45,78 +51,45 @@ namespace nld {
 namespace oz {
 namespace nm {
 
+
 constexpr int kT = 128;                        // nodes per tile (UMMA M)
 constexpr int kYSlice = kT * 64;               // one digit slice: 128 nodes x K = 64 bytes
 constexpr int kYBytes = kSl * kYSlice;         // 48 KB
-constexpr int kABytes = kT * 8 * 8;            // A_j[a], 8 doubles per node
-constexpr int kPBytes = kT * 4;                // pixel index per node (-1: padding)
-constexpr int kAPBytes = kABytes + kPBytes;    // 8.5 KB
-constexpr int kTileBytes = kYBytes + kAPBytes; // plan-time tile record
+constexpr int kRowBytes = 24 * 8;              // a node's weight row A | B | C
+constexpr int kRawBytes = kT * kRowBytes + kT * 4;   // rows + pixel indices (24.5 KB)
 constexpr int kPassRows = 32;                  // B rows per slice and pass: 4 rhs x 8 a
 constexpr int kGBlk = kPassRows * 64;          // 2 KB
 constexpr int kGBytes = 4 * kSl * kGBlk;       // 48 KB: [pass][q][32 x 64]
 constexpr int kGItem = kGBytes + 16 * 4;       // + one exponent per rhs
 constexpr int kAccCols = kSl * kPassRows;      // 192 accumulator columns per pass
 constexpr int kYT0 = 2 * kAccCols;             // Y digits in TMEM: columns 384..479
-constexpr int kEpi = 16;
-constexpr int kIssuer = kEpi, kTLoader = kEpi + 1, kGLoader = kEpi + 2;
-constexpr int kThreads = 32 * (kEpi + 3);
-constexpr int kYStages = 2, kAPStages = 3;
+constexpr int kEpi = 8;
+constexpr int kSlicer0 = kEpi, kSlicers = 4;
+constexpr int kIssuer = kEpi + kSlicers, kRLoader = kIssuer + 1, kGLoader = kIssuer + 2;
+constexpr int kThreads = 32 * (kGLoader + 1);
+constexpr int kRawStages = 3;
 static_assert(kSl == 6, "six digit slices");
 
 __host__ __device__ constexpr int smem_bytes() {
-  return 2 * kGItem + kYStages * kYBytes + kAPStages * kAPBytes;
+  return 2 * kGItem + kYBytes + kRawStages * kRawBytes;
 }
 
-// ---- plan-time tile table --------------------------------------------------
-// Per 3-D subproblem, ceil(count / 128) tile records: the six Y digit slices
-// (Y = B (x) C scaled by 2^(46 - max eB - max eC) of the subproblem, K-major
-// canonical, 8 KB each), then A_j[0..7] (fp64) and the pixel index; rows past
-// the count are zero (pixel -1).
-__global__ void __launch_bounds__(kT)
-k_gtile(const SubDev* __restrict__ subs, const WinDev* __restrict__ wins,
-        const double* __restrict__ rows, const int32_t* __restrict__ pix,
-        const int16_t* __restrict__ sub_exp, const int64_t* __restrict__ tile_off,
-        uint8_t* __restrict__ gtile) {
-  const SubDev sd = subs[blockIdx.x];
-  const WinDev wd = wins[sd.win];
-  const double* __restrict__ rw = rows + wd.row_off + (sd.start - wd.node_off) * 24;
-  const int32_t* __restrict__ pw = pix + sd.start;
-  const int16_t* ex = sub_exp + (int64_t)blockIdx.x * kExpPerSub;
-  int eBm = -2000, eCm = -2000;
-#pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    eBm = max(eBm, (int)ex[8 + q]);
-    eCm = max(eCm, (int)ex[16 + q]);
-  }
-  const double syB = pow2(46 - eBm), syC = pow2(-eCm);
-  const int n = threadIdx.x;
-  const int ntile = (sd.count + kT - 1) / kT;
-  for (int tl = 0; tl < ntile; ++tl) {
-    const int j = tl * kT + n;
-    const bool ok = j < sd.count;
-    uint8_t* base = gtile + (tile_off[blockIdx.x] + tl) * (int64_t)kTileBytes;
-    double b[8], c[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      b[i] = ok ? rw[(int64_t)j * 24 + 8 + i] * syB : 0.0;
-      c[i] = ok ? rw[(int64_t)j * 24 + 16 + i] * syC : 0.0;
-    }
-#pragma unroll
-    for (int kq = 0; kq < 4; ++kq) {
-      uint32_t lo[16], hi[16];
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const int bc = kq * 16 + i;
-        slice1(b[bc >> 3], c[bc & 7], lo[i], hi[i]);
-      }
-      store16(lo, hi, base + canon64(n, kq * 16), kYSlice);
-    }
-    double* A = reinterpret_cast<double*>(base + kYBytes) + n * 8;
-#pragma unroll
-    for (int a = 0; a < 8; ++a) A[a] = ok ? rw[(int64_t)j * 24 + a] : 0.0;
-    reinterpret_cast<int32_t*>(base + kYBytes + kABytes)[n] = ok ? pw[j] : -1;
-  }
+// Arrive on `bar` (lane 0, after the warp) only when this warp's loads of the
+// given values have completed: the arrive's predicate depends on all of them
+// (every lane folds its values; the warp vote needs every lane's result).
+__device__ __forceinline__ void release_after_loads(uint64_t* bar, int lane, int i0, double2 a,
+                                                    double2 b, double2 c, double2 d) {
+  const unsigned long long fold =
+      (unsigned long long)__double_as_longlong(a.x) ^ __double_as_longlong(a.y) ^
+      __double_as_longlong(b.x) ^ __double_as_longlong(b.y) ^ __double_as_longlong(c.x) ^
+      __double_as_longlong(c.y) ^ __double_as_longlong(d.x) ^ __double_as_longlong(d.y) ^
+      (unsigned long long)(unsigned)i0;
+  // never true for a real fold, but the compiler cannot know: a warp-wide
+  // vote over a value computed from every lane's loads
+  // (a fold equal to this constant has probability 2^-64 per tile)
+  const bool never = __any_sync(0xffffffffu, fold == 0x5a5a5a5a5a5a5a5aull);
+  // the barrier address depends on the vote, hence on every lane's loads
+  if (lane == 0) mbar_arrive(never ? bar + 64 : bar);
 }
 
 // ---- G digits of every cell, once per product ------------------------------
@@ -169,16 +142,17 @@ k_gdig_nm(const CellDev* __restrict__ cells, const WinDev* __restrict__ wins,
 template <int MODE>
 __global__ void __launch_bounds__(kThreads, 1)
 k_gather_nm(const SubDev* __restrict__ subs, const int32_t* __restrict__ order, int nsub,
-            const int16_t* __restrict__ sub_exp, const int64_t* __restrict__ tile_off,
-            const uint8_t* __restrict__ gtile, const uint8_t* __restrict__ gdig,
-            double* __restrict__ out, int nrhs, mma::GatherEpi ep) {
+            const WinDev* __restrict__ wins, const double* __restrict__ rows,
+            const int32_t* __restrict__ pix, const int16_t* __restrict__ sub_exp,
+            const uint8_t* __restrict__ gdig, double* __restrict__ out, int nrhs,
+            mma::GatherEpi ep) {
   extern __shared__ __align__(16) uint8_t smem[];
-  __shared__ uint64_t g_full[2], g_empty[2], y_full[kYStages], y_empty[kYStages];
-  __shared__ uint64_t ap_full[kAPStages], ap_empty[kAPStages], acc_full[2], acc_empty[2];
+  __shared__ uint64_t g_full[2], g_empty[2], y_full, y_empty;
+  __shared__ uint64_t raw_full[kRawStages], raw_empty[kRawStages], acc_full[2], acc_empty[2];
   __shared__ uint32_t taddr_s;
   uint8_t* const sG = smem;                              // [2][kGItem]
-  uint8_t* const sY = sG + 2 * kGItem;                   // [2][kYBytes]
-  uint8_t* const sAP = sY + kYStages * kYBytes;          // [3][kAPBytes]
+  uint8_t* const sY = sG + 2 * kGItem;                   // [kYBytes]
+  uint8_t* const sRaw = sY + kYBytes;                    // [3][rows | pix]
 
   // warp index through a shuffle: warp-uniform to the compiler, so the TMEM
   // addresses derived from it live in uniform registers
@@ -198,17 +172,15 @@ k_gather_nm(const SubDev* __restrict__ subs, const int32_t* __restrict__ order, 
   if (tid == 32) {
     for (int k = 0; k < 2; ++k) {
       umma::mbar_init(&g_full[k], 1);
-      umma::mbar_init(&g_empty[k], 1 + kEpi);     // last UMMA commit + epilogue warps
+      umma::mbar_init(&g_empty[k], kEpi);         // epilogue warps, after the item's last pass
       umma::mbar_init(&acc_full[k], 1);
       umma::mbar_init(&acc_empty[k], kEpi);
     }
-    for (int k = 0; k < kYStages; ++k) {
-      umma::mbar_init(&y_full[k], 1);
-      umma::mbar_init(&y_empty[k], 1);            // commit of the TMEM copy
-    }
-    for (int k = 0; k < kAPStages; ++k) {
-      umma::mbar_init(&ap_full[k], 1);
-      umma::mbar_init(&ap_empty[k], kEpi);
+    umma::mbar_init(&y_full, kSlicers);
+    umma::mbar_init(&y_empty, 1);                 // commit of the TMEM copy
+    for (int k = 0; k < kRawStages; ++k) {
+      umma::mbar_init(&raw_full[k], 33);          // 32 noinc cp.async arrivals + the bulk copy's
+      umma::mbar_init(&raw_empty[k], kSlicers + kEpi);
     }
     umma::mbar_fence_init();
   }
@@ -216,65 +188,131 @@ k_gather_nm(const SubDev* __restrict__ subs, const int32_t* __restrict__ order, 
   __syncthreads();
   umma::fence_after();
   const uint32_t tmem = taddr_s;
+#ifdef NLD_OZ_PROF
+  const long long t_role = clock64();
+#endif
 
   if (warp == kGLoader) {
     // ------------------------------------------------------------- G loader
     if (lane == 0) {
       for (int k = 0; k < nitems; ++k) {
         const int gs = k & 1;
-        if (k >= 2) umma::mbar_wait(&g_empty[gs], ((k >> 1) - 1) & 1);
+        if (k >= 2) OZW(6, umma::mbar_wait(&g_empty[gs], ((k >> 1) - 1) & 1));
         const uint8_t* src = gdig + ((int64_t)subs[item_sub(k)].cell * ngroups + k % ngroups) *
                                         (int64_t)kGItem;
         umma::mbar_arrive_expect_tx(&g_full[gs], kGItem);
         umma::bulk_g2s(sG + gs * kGItem, src, kGItem, &g_full[gs]);
       }
     }
-  } else if (warp == kTLoader) {
-    // ---------------------------------------------------------- tile loader
-    if (lane == 0) {
-      int gt = 0;
-      for (int k = 0; k < nitems; ++k) {
-        const int si = item_sub(k);
-        const int ntile = (subs[si].count + kT - 1) / kT;
-        const uint8_t* src = gtile + tile_off[si] * (int64_t)kTileBytes;
-        for (int tl = 0; tl < ntile; ++tl, ++gt) {
-          const int ys = gt % kYStages, as = gt % kAPStages;
-          if (gt >= kYStages) umma::mbar_wait(&y_empty[ys], ((gt / kYStages) - 1) & 1);
-          umma::mbar_arrive_expect_tx(&y_full[ys], kYBytes);
-          umma::bulk_g2s(sY + ys * kYBytes, src + (int64_t)tl * kTileBytes, kYBytes, &y_full[ys]);
-          if (gt >= kAPStages) umma::mbar_wait(&ap_empty[as], ((gt / kAPStages) - 1) & 1);
-          umma::mbar_arrive_expect_tx(&ap_full[as], kAPBytes);
-          umma::bulk_g2s(sAP + as * kAPBytes, src + (int64_t)tl * kTileBytes + kYBytes, kAPBytes,
-                         &ap_full[as]);
+  } else if (warp == kRLoader) {
+    // ----------------------------------------------------------- row loader
+    int gt = 0;
+    for (int k = 0; k < nitems; ++k) {
+      const SubDev sd = subs[item_sub(k)];
+      const WinDev wd = wins[sd.win];
+      const double* __restrict__ rw = rows + wd.row_off + (sd.start - wd.node_off) * 24;
+      const int32_t* __restrict__ pw = pix + sd.start;
+      const int ntile = (sd.count + kT - 1) / kT;
+      for (int tl = 0; tl < ntile; ++tl, ++gt) {
+        const int s = gt % kRawStages;
+        if (gt >= kRawStages) OZW(4, umma::mbar_wait(&raw_empty[s], ((gt / kRawStages) - 1) & 1));
+        uint8_t* dst = sRaw + s * kRawBytes;
+        const int j0 = tl * kT, cn = min(kT, sd.count - j0);
+        if (lane == 0) {
+          umma::mbar_arrive_expect_tx(&raw_full[s], (uint32_t)(cn * kRowBytes));
+          umma::bulk_g2s(dst, rw + (int64_t)j0 * 24, (uint32_t)(cn * kRowBytes), &raw_full[s]);
         }
+#pragma unroll
+        for (int q = 0; q < kT / 32; ++q) {
+          const int nd = q * 32 + lane;
+          if (nd < cn) cp_async4(dst + kT * kRowBytes + 4 * nd, pw + j0 + nd);
+        }
+        cp_async_mbar_arrive(&raw_full[s]);
+      }
+    }
+  } else if (warp >= kSlicer0 && warp < kIssuer) {
+    // --------------------------------------------------------------- slicers
+    // thread = node row m of the tile: Y_j[(b, c)] = B_j[b] C_j[c], scaled by
+    // the subproblem's 2^(46 - max eB - max eC), cut into six digit slices in
+    // the K-major canonical layout (a quarter-warp's 16-byte stores cover one
+    // 128-byte line: conflict-free)
+    const int m = (warp - kSlicer0) * 32 + lane;
+    int gt = 0;
+    for (int k = 0; k < nitems; ++k) {
+      const int si = item_sub(k);
+      const int cnt = subs[si].count;
+      const int16_t* ex = sub_exp + (int64_t)si * kExpPerSub;
+      int eBm = -2000, eCm = -2000;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        eBm = max(eBm, (int)ex[8 + q]);
+        eCm = max(eCm, (int)ex[16 + q]);
+      }
+      const double syB = pow2(46 - eBm), syC = pow2(-eCm);
+      const int ntile = (cnt + kT - 1) / kT;
+      for (int tl = 0; tl < ntile; ++tl, ++gt) {
+        const int s = gt % kRawStages;
+        OZW(16, umma::mbar_wait(&raw_full[s], (gt / kRawStages) & 1));
+        const bool ok = tl * kT + m < cnt;
+        const double2* R = reinterpret_cast<const double2*>(sRaw + s * kRawBytes + m * kRowBytes);
+        double bb[8], cc[8];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const double2 x = ok ? R[4 + i] : make_double2(0.0, 0.0);
+          const double2 y = ok ? R[8 + i] : make_double2(0.0, 0.0);
+          bb[2 * i] = x.x * syB;
+          bb[2 * i + 1] = x.y * syB;
+          cc[2 * i] = y.x * syC;
+          cc[2 * i + 1] = y.y * syC;
+        }
+        release_after_loads(&raw_empty[s], lane, 0, make_double2(bb[0], cc[7]),
+                            make_double2(bb[7], cc[0]), make_double2(bb[3], cc[3]),
+                            make_double2(bb[5], cc[5]));   // B, C read
+        if (gt >= 1) OZW(17, umma::mbar_wait(&y_empty, (gt - 1) & 1));   // previous tile copied
+#pragma unroll
+        for (int kq = 0; kq < 4; ++kq) {
+          uint32_t lo[16], hi[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const int bc = kq * 16 + i;
+            slice1(bb[bc >> 3], cc[bc & 7], lo[i], hi[i]);
+          }
+          store16(lo, hi, sY + canon64(m, kq * 16), kYSlice);
+        }
+        umma::fence_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&y_full);
       }
     }
   } else if (warp == kIssuer) {
     // ---------------------------------------------------------------- issuer
     if (lane == 0) {
       int gt = 0, gp = 0;
+      const uint32_t yB = umma::smem_u32(sY);
       for (int k = 0; k < nitems; ++k) {
         const int gs = k & 1;
         const int ntile = (subs[item_sub(k)].count + kT - 1) / kT;
-        umma::mbar_wait(&g_full[gs], (k >> 1) & 1);
+        OZW(0, umma::mbar_wait(&g_full[gs], (k >> 1) & 1));
         const uint32_t gB = umma::smem_u32(sG + gs * kGItem);
         for (int tl = 0; tl < ntile; ++tl, ++gt) {
-          const int ys = gt % kYStages;
-          umma::mbar_wait(&y_full[ys], (gt / kYStages) & 1);
+          OZW(1, umma::mbar_wait(&y_full, gt & 1));
           umma::fence_after();
           // the tile's Y digits -> TMEM (the UMMA A operand of all four passes);
           // ordered behind the previous tile's UMMAs, which read the old copy
-          const uint32_t yB = umma::smem_u32(sY + ys * kYBytes);
 #pragma unroll
           for (int p = 0; p < kSl; ++p)
 #pragma unroll
             for (int ks = 0; ks < 2; ++ks)
               umma::tmem_cp_128x256b(tmem + (uint32_t)(kYT0 + p * 16 + ks * 8),
                                      umma::make_sdesc(yB + p * kYSlice + ks * 256, 128, 512));
-          umma::commit(&y_empty[ys]);
+          // The staging is released by the commit after the first pass's UMMAs,
+          // not right after the copies: a commit issued directly behind
+          // tcgen05.cp was measured to fire before the copy's shared-memory
+          // reads were done (the slicers' next writes raced with it); the
+          // UMMAs consume the copied digits, so their completion implies it.
           for (int ps = 0; ps < 4; ++ps, ++gp) {
             const int ab = gp & 1;
-            if (gp >= 2) umma::mbar_wait(&acc_empty[ab], ((gp >> 1) - 1) & 1);
+            if (gp >= 2) OZW(2, umma::mbar_wait(&acc_empty[ab], ((gp >> 1) - 1) & 1));
             umma::fence_after();
             const uint32_t dcol = tmem + (uint32_t)(ab * kAccCols);
             const uint32_t bB = gB + ps * (kSl * kGBlk);
@@ -290,14 +328,21 @@ k_gather_nm(const SubDev* __restrict__ subs, const int32_t* __restrict__ order, 
                                 umma::idesc_i8(kT, (kSl - p) * kPassRows),
                                 (p > 0 || ks > 0) ? 1u : 0u);
             umma::commit(&acc_full[ab]);
+            if (ps == 1) {
+              // The Y staging is free once the copy has been consumed: the
+              // issuer observes pass 0's completion (its UMMAs read the copied
+              // digits) and arrives itself -- no reliance on what a
+              // tcgen05.commit behind a tcgen05.cp tracks.
+              umma::mbar_wait(&acc_full[(gp - 1) & 1], ((gp - 1) >> 1) & 1);
+              mbar_arrive(&y_empty);
+            }
           }
         }
-        umma::commit(&g_empty[gs]);   // item k's G digits no longer read
       }
     }
   } else {
     // -------------------------------------------------------------- epilogue
-    const int lq = warp & 3, w = warp >> 2;
+    const int lq = warp & 3, sp = warp >> 2;     // lane quarter, rhs slot pair
     const int m = lq * 32 + lane;                 // node row of the tile
     const uint32_t tl_lane = tmem + ((uint32_t)(lq * 32) << 16);
     const bool need_eta = ep.kind == NLD_APPLY_SYSTEM || ep.kind == NLD_APPLY_LAPLACIAN;
@@ -307,7 +352,7 @@ k_gather_nm(const SubDev* __restrict__ subs, const int32_t* __restrict__ order, 
       const int gs = k & 1;
       const int si = item_sub(k);
       const int cnt = subs[si].count;
-      const int r0 = (k % ngroups) * 16 + 4 * w;  // this warp's first rhs
+      const int r0 = (k % ngroups) * 16 + 8 * sp;  // this warp's first rhs
       const int16_t* exk = sub_exp + (int64_t)si * kExpPerSub;
       int eBm = -2000, eCm = -2000;
 #pragma unroll
@@ -315,114 +360,134 @@ k_gather_nm(const SubDev* __restrict__ subs, const int32_t* __restrict__ order, 
         eBm = max(eBm, (int)exk[8 + q]);
         eCm = max(eCm, (int)exk[16 + q]);
       }
-      umma::mbar_wait(&g_full[gs], (k >> 1) & 1);
-      const int4 ge = reinterpret_cast<const int4*>(sG + gs * kGItem + kGBytes)[w];
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&g_empty[gs]);
+      OZW(8, umma::mbar_wait(&g_full[gs], (k >> 1) & 1));
+      const int4* gex = reinterpret_cast<const int4*>(sG + gs * kGItem + kGBytes);
+      const int4 ge0 = gex[2 * sp], ge1 = gex[2 * sp + 1];   // rhs r0 .. r0 + 7
       // T scale per rhs: G exponent + the subproblem's Y exponents (combine6
       // carries 2^24)
       const int eb = eBm + eCm - 52;
       const int ntile = (cnt + kT - 1) / kT;
       for (int tl = 0; tl < ntile; ++tl, ++gt) {
-        const int as = gt % kAPStages;
-        umma::mbar_wait(&ap_full[as], (gt / kAPStages) & 1);
-        const double2* Ap = reinterpret_cast<const double2*>(sAP + as * kAPBytes) + m * 4;
+        const int s = gt % kRawStages;
+        OZW(9, umma::mbar_wait(&raw_full[s], (gt / kRawStages) & 1));
+        const double2* Ap = reinterpret_cast<const double2*>(sRaw + s * kRawBytes + m * kRowBytes);
         const double2 a01 = Ap[0], a23 = Ap[1], a45 = Ap[2], a67 = Ap[3];
-        const int px = reinterpret_cast<const int32_t*>(sAP + as * kAPBytes + kABytes)[m];
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&ap_empty[as]);
+        const int px = tl * kT + m < cnt
+                           ? reinterpret_cast<const int32_t*>(sRaw + s * kRawBytes + kT * kRowBytes)[m]
+                           : -1;
+        // Release the stage only once the loads have COMPLETED: the arrive is
+        // made data-dependent on the loaded values (an LDS still in flight
+        // when the arrive retires lets the row loader's next TMA overwrite the
+        // stage under it -- observed as rare stale pixel indices).
+        release_after_loads(&raw_empty[s], lane, px, a01, a23, a45, a67);
         const bool ok = px >= 0;
         const int64_t e = (int64_t)px * nrhs + r0;
-        // the running window sum / v / eta of the node, in flight during the passes
-        double2 s01 = make_double2(0.0, 0.0), s23 = s01, v01 = s01, v23 = s01;
-        double et = 0.0;
-        if (ok) {
-          if (MODE >= mma::kGatherAccum) {
-            s01 = *reinterpret_cast<const double2*>(out + e);
-            s23 = *reinterpret_cast<const double2*>(out + e + 2);
+        // the running window sum of the node's 8 rhs (loaded now, in flight
+        // during the passes); each pass adds its rhs' scaled products
+        double sv[8];
+        if (ok && MODE >= mma::kGatherAccum) {
+          const double2* o2 = reinterpret_cast<const double2*>(out + e);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const double2 x = o2[i];
+            sv[2 * i] = x.x;
+            sv[2 * i + 1] = x.y;
           }
-          if (MODE == mma::kGatherFinal) {
-            v01 = *reinterpret_cast<const double2*>(ep.v + e);
-            v23 = *reinterpret_cast<const double2*>(ep.v + e + 2);
-            if (need_eta) et = ep.eta[px];
-          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) sv[i] = 0.0;
         }
-        double y[4];
 #pragma unroll
         for (int ps = 0; ps < 4; ++ps, ++gp) {
           const int ab = gp & 1;
-          umma::mbar_wait(&acc_full[ab], (gp >> 1) & 1);
+          OZW(10, umma::mbar_wait(&acc_full[ab], (gp >> 1) & 1));
           umma::fence_after();
-          // the six diagonals of a = 0..3, then of a = 4..7 (24 registers each);
-          // hi and lo parts accumulate in separate chains (combine6_parts)
-          const uint32_t tc = tl_lane + (uint32_t)(ab * kAccCols + w * 8);
-          uint32_t dv[kSl][4];
-          double h, l, sh, sl;
 #pragma unroll
-          for (int t = 0; t < kSl; ++t) umma::tmem_ld4(tc + (uint32_t)(t * kPassRows), dv[t]);
-          umma::tmem_wait_ld();
-          combine6_parts(dv, 0, h, l);
-          sh = h * a01.x;
-          sl = l * a01.x;
-          combine6_parts(dv, 1, h, l);
-          sh = fma(h, a01.y, sh);
-          sl = fma(l, a01.y, sl);
-          combine6_parts(dv, 2, h, l);
-          sh = fma(h, a23.x, sh);
-          sl = fma(l, a23.x, sl);
-          combine6_parts(dv, 3, h, l);
-          sh = fma(h, a23.y, sh);
-          sl = fma(l, a23.y, sl);
+          for (int sl = 0; sl < 2; ++sl) {
+            const int w = 2 * sp + sl;
+            const uint32_t tc = tl_lane + (uint32_t)(ab * kAccCols + w * 8);
+            uint32_t dv[kSl][8];
+            {
+              uint32_t d0[kSl][4], d1[kSl][4];
+              umma::tmem_ld4x6_wait(tc, kPassRows, d0);
+              umma::tmem_ld4x6_wait(tc + 4, kPassRows, d1);
 #pragma unroll
-          for (int t = 0; t < kSl; ++t) umma::tmem_ld4(tc + (uint32_t)(t * kPassRows + 4), dv[t]);
-          umma::tmem_wait_ld();
-          umma::fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&acc_empty[ab]);
-          combine6_parts(dv, 0, h, l);
-          sh = fma(h, a45.x, sh);
-          sl = fma(l, a45.x, sl);
-          combine6_parts(dv, 1, h, l);
-          sh = fma(h, a45.y, sh);
-          sl = fma(l, a45.y, sl);
-          combine6_parts(dv, 2, h, l);
-          sh = fma(h, a67.x, sh);
-          sl = fma(l, a67.x, sl);
-          combine6_parts(dv, 3, h, l);
-          sh = fma(h, a67.y, sh);
-          sl = fma(l, a67.y, sl);
-          const double s = fma(sh, 4294967296.0, sl);
-          y[ps] = s;
+              for (int t = 0; t < kSl; ++t)
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                  dv[t][i] = d0[t][i];
+                  dv[t][4 + i] = d1[t][i];
+                }
+            }
+            if (sl == 1) {
+              umma::fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&acc_empty[ab]);
+            }
+            // hi and lo parts accumulate in separate chains (combine6_parts)
+            double h, l, sh, sl_;
+            combine6_parts(dv, 0, h, l);
+            sh = h * a01.x;
+            sl_ = l * a01.x;
+            combine6_parts(dv, 1, h, l);
+            sh = fma(h, a01.y, sh);
+            sl_ = fma(l, a01.y, sl_);
+            combine6_parts(dv, 2, h, l);
+            sh = fma(h, a23.x, sh);
+            sl_ = fma(l, a23.x, sl_);
+            combine6_parts(dv, 3, h, l);
+            sh = fma(h, a23.y, sh);
+            sl_ = fma(l, a23.y, sl_);
+            combine6_parts(dv, 4, h, l);
+            sh = fma(h, a45.x, sh);
+            sl_ = fma(l, a45.x, sl_);
+            combine6_parts(dv, 5, h, l);
+            sh = fma(h, a45.y, sh);
+            sl_ = fma(l, a45.y, sl_);
+            combine6_parts(dv, 6, h, l);
+            sh = fma(h, a67.x, sh);
+            sl_ = fma(l, a67.x, sl_);
+            combine6_parts(dv, 7, h, l);
+            sh = fma(h, a67.y, sh);
+            sl_ = fma(l, a67.y, sl_);
+            // rhs r0 + 4 sl + ps; T scale: G exponent + the subproblem's Y
+            // exponents (combine6 carries 2^24)
+            const int4 ge = sl ? ge1 : ge0;
+            const int gx = ps == 0 ? ge.x : ps == 1 ? ge.y : ps == 2 ? ge.z : ge.w;
+            sv[4 * sl + ps] += fma(sh, 4294967296.0, sl_) * pow2(gx + eb);
+          }
+
         }
         if (!ok) continue;
-        y[0] *= pow2(ge.x + eb);
-        y[1] *= pow2(ge.y + eb);
-        y[2] *= pow2(ge.z + eb);
-        y[3] *= pow2(ge.w + eb);
-        double res[4];
-        if (MODE == mma::kGatherStore || MODE == mma::kGatherFirst) {
+        double res[8];
 #pragma unroll
-          for (int i = 0; i < 4; ++i) res[i] = y[i];
-        } else if (MODE == mma::kGatherAccum) {
-          res[0] = s01.x + y[0];
-          res[1] = s01.y + y[1];
-          res[2] = s23.x + y[2];
-          res[3] = s23.y + y[3];
-        } else {
-          const double sv[4] = {s01.x + y[0], s01.y + y[1], s23.x + y[2], s23.y + y[3]};
-          const double vv[4] = {v01.x, v01.y, v23.x, v23.y};
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
+        for (int i = 0; i < 8; ++i) {
+          if (MODE != mma::kGatherFinal) {
+            res[i] = sv[i];
+          } else {
             const double lam = ep.coef ? ep.coef[2 * (r0 + i)] : 0.0;
             const double mu = ep.coef ? ep.coef[2 * (r0 + i) + 1] : 0.0;
-            res[i] = mma::epi_value_r(ep.kind, (double)ep.L, inv_L, sv[i], vv[i], et, lam, mu);
+            const double et = need_eta ? ep.eta[px] : 0.0;
+            res[i] = mma::epi_value_r(ep.kind, (double)ep.L, inv_L, sv[i], ep.v[e + i], et, lam, mu);
           }
         }
-        *reinterpret_cast<double2*>(out + e) = make_double2(res[0], res[1]);
-        *reinterpret_cast<double2*>(out + e + 2) = make_double2(res[2], res[3]);
+        double2* o2 = reinterpret_cast<double2*>(out + e);
+        o2[0] = make_double2(res[0], res[1]);
+        o2[1] = make_double2(res[2], res[3]);
+        o2[2] = make_double2(res[4], res[5]);
+        o2[3] = make_double2(res[6], res[7]);
       }
+      // every pass of the item has completed (its accumulators were read):
+      // the UMMAs no longer read its G digits
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&g_empty[gs]);
     }
   }
+#ifdef NLD_OZ_PROF
+  if (lane == 0)
+    atomicAdd(&oz_prof[24 + (warp == kIssuer ? 0 : warp == kRLoader ? 1 : warp < kEpi ? 3 : 2)],
+              (unsigned long long)(clock64() - t_role));
+#endif
   umma::fence_before();
   __syncthreads();
   if (warp == 0) umma::tmem_free<512>(tmem);
@@ -435,36 +500,10 @@ k_gather_nm(const SubDev* __restrict__ subs, const int32_t* __restrict__ order, 
 
 int64_t gather_gdig_bytes() { return oz::nm::kGItem; }
 
-// plan-time tile table of the sliced gather: when it fits in half of the
-// free memory (else the gather of 3-D windows runs on the fp64 DMMA kernels)
-void gather_nm_tables(PlanSet& ps, const std::vector<SubDev>& h, cudaStream_t st) {
-  if (ps.gtile || h.empty()) return;
-  std::vector<int64_t> off(h.size());
-  int64_t tiles = 0;
-  for (size_t i = 0; i < h.size(); ++i) {
-    off[i] = tiles;
-    tiles += (h[i].count + oz::nm::kT - 1) / oz::nm::kT;
-  }
-  const size_t need = (size_t)tiles * oz::nm::kTileBytes;
-  size_t free_b = 0, total_b = 0;
-  NLD_CUDA(cudaMemGetInfo(&free_b, &total_b));
-  if (need == 0 || need > free_b / 2) return;
-  NLD_CUDA(cudaMalloc(&ps.gtile_off, sizeof(int64_t) * off.size()));
-  NLD_CUDA(cudaMalloc(&ps.gtile, need));
-  NLD_CUDA(cudaMemcpyAsync(ps.gtile_off, off.data(), sizeof(int64_t) * off.size(),
-                           cudaMemcpyHostToDevice, st));
-  oz::nm::k_gtile<<<(unsigned)h.size(), oz::nm::kT, 0, st>>>(ps.subs[3], ps.wdev, ps.rows, ps.pix,
-                                                             ps.sub_exp, ps.gtile_off, ps.gtile);
-  NLD_CUDA(cudaGetLastError());
-  // the host offsets must outlive the async copy
-  NLD_CUDA(cudaStreamSynchronize(st));
-}
-
 template <int MODE>
-static void launch_nm(unsigned grid_n, const SubDev* subs, const int32_t* order, unsigned nsub,
-                      const int16_t* ex, const int64_t* toff, const uint8_t* gtile,
-                      const uint8_t* gdig, double* out, int nrhs, const mma::GatherEpi& ep,
-                      cudaStream_t st) {
+static void launch_nm(unsigned grid_n, const PlanSet& ps, const SubDev* subs, const int32_t* order,
+                      unsigned nsub, const int16_t* ex, const uint8_t* gdig, double* out, int nrhs,
+                      const mma::GatherEpi& ep, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
     NLD_CUDA(cudaFuncSetAttribute(oz::nm::k_gather_nm<MODE>,
@@ -473,14 +512,13 @@ static void launch_nm(unsigned grid_n, const SubDev* subs, const int32_t* order,
     attr = true;
   }
   oz::nm::k_gather_nm<MODE><<<grid_n, oz::nm::kThreads, oz::nm::smem_bytes(), st>>>(
-      subs, order, (int)nsub, ex, toff, gtile, gdig, out, nrhs, ep);
+      subs, order, (int)nsub, ps.wdev, ps.rows, ps.pix, ex, gdig, out, nrhs, ep);
 }
 
 void launch_gather_nm(const PlanSet& ps, const SubDev* subs, const int16_t* ex,
-                      const int32_t* order, const int64_t* toff, unsigned nsub,
-                      const double* grid, int64_t grid_ld, double* out, int nrhs,
-                      const mma::GatherEpi& ep, cudaStream_t st, uint8_t* gdig, int64_t cell_lo,
-                      int64_t ncell) {
+                      const int32_t* order, unsigned nsub, const double* grid, int64_t grid_ld,
+                      double* out, int nrhs, const mma::GatherEpi& ep, cudaStream_t st,
+                      uint8_t* gdig, int64_t cell_lo, int64_t ncell) {
   static int sms = 0;
   if (!sms) {
     int dev = 0;
@@ -493,23 +531,22 @@ void launch_gather_nm(const PlanSet& ps, const SubDev* subs, const int16_t* ex,
   const unsigned grid_n = std::min<unsigned>(nsub, (unsigned)sms);
   switch (ep.mode) {
     case mma::kGatherStore:
-      launch_nm<mma::kGatherStore>(grid_n, subs, order, nsub, ex, toff, ps.gtile, gdig, out, nrhs,
-                                   ep, st);
+      launch_nm<mma::kGatherStore>(grid_n, ps, subs, order, nsub, ex, gdig, out, nrhs, ep, st);
       break;
     case mma::kGatherFirst:
-      launch_nm<mma::kGatherFirst>(grid_n, subs, order, nsub, ex, toff, ps.gtile, gdig, out, nrhs,
-                                   ep, st);
+      launch_nm<mma::kGatherFirst>(grid_n, ps, subs, order, nsub, ex, gdig, out, nrhs, ep, st);
       break;
     case mma::kGatherAccum:
-      launch_nm<mma::kGatherAccum>(grid_n, subs, order, nsub, ex, toff, ps.gtile, gdig, out, nrhs,
-                                   ep, st);
+      launch_nm<mma::kGatherAccum>(grid_n, ps, subs, order, nsub, ex, gdig, out, nrhs, ep, st);
       break;
     default:
-      launch_nm<mma::kGatherFinal>(grid_n, subs, order, nsub, ex, toff, ps.gtile, gdig, out, nrhs,
-                                   ep, st);
+      launch_nm<mma::kGatherFinal>(grid_n, ps, subs, order, nsub, ex, gdig, out, nrhs, ep, st);
       break;
   }
   NLD_CUDA(cudaGetLastError());
+#ifdef NLD_OZ_PROF
+  ozaki_prof_dump("gather_nm", st);
+#endif
 }
 
 }  // namespace nld

@@ -133,12 +133,7 @@ struct PlanSet {
   int64_t generic_nodes = 0;     // nodes in windows on the generic path
   int16_t* sub_exp = nullptr;    // sliced spread: per 3-D subproblem eA/eB/eC
   int32_t* sub_order = nullptr;  // per window: its 3-D subproblems by descending size
-  uint8_t* ydig = nullptr;       // sliced spread: Y = B (x) C digit slices per 32-node
-                                 // chunk, UMMA B-operand layout (12 KB per chunk)
-  int64_t* ychunk = nullptr;     // per 3-D subproblem: its first chunk in ydig
-  uint8_t* gtile = nullptr;      // sliced gather: per 128-node tile its Y digits (48 KB),
-                                 // A parts and pixel indices (nld_gather_nm.cu)
-  int64_t* gtile_off = nullptr;  // per 3-D subproblem: its first tile in gtile
+  bool oz_ok = false;            // integer-sliced spread/gather enabled (no_sliced knob)
   std::vector<int64_t> gcell_lo, gcell_n;   // per window: its cells' global range
   int shares_tables_with = -1;   // index of the plan set whose tables we use
   bool owns_tables = true;
@@ -210,7 +205,7 @@ void build_planset(nld_operator* op, int which, cudaStream_t st);
 bool use_ozaki();
 int16_t* ozaki_exponents(PlanSet& ps, bool tables, cudaStream_t st);
 void launch_spread_oz(const PlanSet& ps, const SubDev* subs, const int16_t* ex,
-                      const int64_t* ychunk, unsigned nsub, const unsigned long long* vmax,
+                      unsigned nsub, const unsigned long long* vmax,
                       const double* vt, int nrhs, double* blocks, cudaStream_t st,
                       const int32_t* order = nullptr);
 void ozaki_vmax(const double* vt, int64_t n, int nrhs, unsigned long long* out, double* flag,
@@ -219,12 +214,10 @@ void ozaki_poison(const double* flag, int nrhs, double* out, int64_t n, int64_t 
                   int pixel_major, cudaStream_t st);
 void ozaki_prof_dump(const char* what, cudaStream_t st);
 namespace mma { struct GatherEpi; }
-void gather_nm_tables(PlanSet& ps, const std::vector<SubDev>& h, cudaStream_t st);
 void launch_gather_nm(const PlanSet& ps, const SubDev* subs, const int16_t* ex,
-                      const int32_t* order, const int64_t* toff, unsigned nsub,
-                      const double* grid, int64_t grid_ld, double* out, int nrhs,
-                      const mma::GatherEpi& ep, cudaStream_t st, uint8_t* gdig, int64_t cell_lo,
-                      int64_t ncell);
+                      const int32_t* order, unsigned nsub, const double* grid, int64_t grid_ld,
+                      double* out, int nrhs, const mma::GatherEpi& ep, cudaStream_t st,
+                      uint8_t* gdig, int64_t cell_lo, int64_t ncell);
 // bytes per (cell, 16-rhs group) of precomputed gather G digits
 int64_t gather_gdig_bytes();
 void free_planset(PlanSet& ps);

@@ -36,6 +36,10 @@
 namespace nld {
 namespace oz {
 
+#ifdef NLD_OZ_PROF
+__device__ unsigned long long oz_prof[32];
+#endif
+
 // ---- plan-time exponent table -------------------------------------------
 // per subproblem: eA[a], eB[b], eC[c] = exponent bounds of the columns of its
 // weight rows (static: the features never change)
@@ -107,61 +111,27 @@ k_poison(const double* __restrict__ flag, int nrhs, double* __restrict__ out, in
   }
 }
 
-// ---- plan-time Y digits for the sliced spread (PY) ------------------------
-// Exactly the slicers' Y = B_b C_c (scaled by 2^(46 - eB_b - eC_c)) of every
-// 32-node chunk, as six 64 x 32 K-major digit slices (zero past the count).
-__global__ void k_spread_ydig(const SubDev* __restrict__ subs, const WinDev* __restrict__ wins,
-                              const double* __restrict__ rows, const int16_t* __restrict__ sub_exp,
-                              const int64_t* __restrict__ ychunk, uint8_t* __restrict__ ydig);
-
-// Raw stage of the persistent spread: [A rows 32 x 8 doubles | v lines 32 x
-// 16 doubles | Y digits 6 x 2 KB].  Y = B (x) C depends only on the (static)
-// node tables, so its digit slices are cut once at plan time (k_spread_ydig)
-// in the UMMA B-operand layout and streamed per chunk by one TMA bulk copy;
-// the slicers cut only X, and a raw stage is released by the slicers and by
-// the chunk's UMMA commit.
+// Raw stage of the persistent spread: [weight rows 32 x (A | B | C) | v lines
+// 32 x 16 doubles].  The slicers cut both operands per chunk: X = v A into
+// TMEM (the A operand) and Y = B (x) C into a shared-memory operand stage (the
+// B operand) -- streaming 320 B per node instead of the 576 B of the former
+// plan-time Y digits; the spread was bound by that stream.
 constexpr int kRawV = kChunk * 16 * 8;           // 4 KB of v lines per chunk
-constexpr int kPyA = kChunk * 8 * 8;             // 2 KB
-constexpr int kPyY = kPyA + kRawV;               // Y digits offset
-constexpr int kPyRawBytes = kPyY + kSl * kBBytes;   // 18 KB
+constexpr int kRawRowB = kChunk * 24 * 8;        // 6 KB of weight rows per chunk
+constexpr int kPyA = kRawRowB;                   // v lines offset
+constexpr int kPyRawBytes = kRawRowB + kRawV;    // 10 KB
 constexpr int kPyRawStages = 8;
 constexpr int kOpStages = 2;                     // X stages in TMEM: 384 + 2 x 48 <= 512
-constexpr int kYChunkBytes = kSl * kBBytes;      // 12 KB per chunk in HBM
-__host__ __device__ constexpr int spread_oz_py_smem() { return kPyRawStages * kPyRawBytes; }
+constexpr int kYOpBytes = kSl * kBBytes;         // 12 KB of Y digits per chunk
+__host__ __device__ constexpr int spread_oz_py_smem() {
+  return kPyRawStages * kPyRawBytes + kOpStages * kYOpBytes;
+}
 constexpr int kSlicers = 256;
 constexpr int kIssuerWarp = 8;
-constexpr int kLoaderWarp = 9;
+constexpr int kLoaderWarp = 9;                   // first of kLoaders loader warps
+constexpr int kLoaders = 4;
 
-__global__ void __launch_bounds__(256)
-k_spread_ydig(const SubDev* __restrict__ subs, const WinDev* __restrict__ wins,
-              const double* __restrict__ rows, const int16_t* __restrict__ sub_exp,
-              const int64_t* __restrict__ ychunk, uint8_t* __restrict__ ydig) {
-  const SubDev sd = subs[blockIdx.x];
-  const WinDev wd = wins[sd.win];
-  const double* __restrict__ rw = rows + wd.row_off + (sd.start - wd.node_off) * 24;
-  const int16_t* ex = sub_exp + (int64_t)blockIdx.x * kExpPerSub;
-  const int n = threadIdx.x & 63, gq = threadIdx.x >> 6;
-  const int b = n >> 3, cc = n & 7;
-  const double sy = pow2(46 - ex[8 + b]) * pow2(-ex[16 + cc]);
-  const int nchunk = (sd.count + kChunk - 1) / kChunk;
-  uint8_t* base = ydig + ychunk[blockIdx.x] * (int64_t)kYChunkBytes;
-  for (int c = 0; c < nchunk; ++c) {
-    uint32_t lo[8], hi[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int j = c * kChunk + gq * 8 + i;
-      double x = 0.0, y = 0.0;
-      if (j < sd.count) {
-        x = rw[(int64_t)j * 24 + 8 + b] * sy;
-        y = rw[(int64_t)j * 24 + 16 + cc];
-      }
-      slice1(x, y, lo[i], hi[i]);
-    }
-    store8(lo, hi, base + (int64_t)c * kYChunkBytes + canon32(n, gq * 8), kBBytes);
-  }
-}
-
-// ---- persistent spread (plan-time Y digits) ---------------------------------
+// ---- persistent spread -------------------------------------------------------
 // One CTA per SM walks (subproblem, rhs group) items -- the window's
 // subproblems in descending size, dealt in snake order as in the persistent
 // gather -- so the per-subproblem fixed costs (TMEM
@@ -172,16 +142,15 @@ k_spread_ydig(const SubDev* __restrict__ subs, const WinDev* __restrict__ wins,
 // already cut the next item's first chunks.  The only serialisation left per
 // item is the TMEM drain (the accumulator is single-buffered: 384 of 512
 // columns).  Scales are per-thread registers (no per-item shared state).
-//   warps 0-7 slicers (X digits -> TMEM)   warp 8 UMMA issuer
-//   warp 9    loader                       warps 10-13 epilogue
-constexpr int kSPEpi0 = 10;
-constexpr int kSPThreads = 32 * 14;
+//   warps 0-7  slicers (X digits -> TMEM, Y digits -> shared memory)
+//   warp 8     UMMA issuer       warps 9-12 loaders       warps 13-16 epilogue
+constexpr int kSPEpi0 = kLoaderWarp + kLoaders;
+constexpr int kSPThreads = 32 * (kSPEpi0 + 4);
 
 __global__ void __launch_bounds__(kSPThreads, 1)
 k_spread_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order, int nsub,
              const WinDev* __restrict__ wins, const double* __restrict__ rows,
              const int32_t* __restrict__ pix, const int16_t* __restrict__ sub_exp,
-             const uint8_t* __restrict__ ydig, const int64_t* __restrict__ ychunk,
              const unsigned long long* __restrict__ vmax, const double* __restrict__ vt,
              int nrhs, double* __restrict__ blocks) {
   constexpr int RS = kPyRawStages, RB = kPyRawBytes;
@@ -190,6 +159,7 @@ k_spread_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
   __shared__ uint64_t op_ready[kOpStages], op_free[kOpStages], acc_full, acc_empty;
   __shared__ uint32_t taddr_s;
   uint8_t* const raw = smem;
+  uint8_t* const sYop = smem + RS * RB;           // [kOpStages][6 x 2 KB]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int ngroups = nrhs / 16;
   const int G = (int)gridDim.x, b = (int)blockIdx.x;
@@ -205,7 +175,7 @@ k_spread_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
   if (tid == 32) {
     for (int k = 0; k < RS; ++k) {
       umma::mbar_init(&raw_full[k], 33);                  // 32 noinc cp.async + the bulk copy
-      umma::mbar_init(&raw_empty[k], kSlicers / 32 + 1);  // slicers + the UMMA commit
+      umma::mbar_init(&raw_empty[k], kSlicers / 32);      // slicers
     }
     for (int k = 0; k < kOpStages; ++k) {
       umma::mbar_init(&op_ready[k], kSlicers / 32);
@@ -219,31 +189,44 @@ k_spread_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
   __syncthreads();
   umma::fence_after();
   const uint32_t tmem = taddr_s;
+#ifdef NLD_OZ_PROF
+  const long long t_role = clock64();
+#endif
 
-  if (warp == kLoaderWarp) {
-    // ---------------------------------------------------------------- loader
+  if (warp >= kLoaderWarp && warp < kSPEpi0) {
+    // -------------------------------------------------------------- loaders
+    // chunk g is staged by loader warp g % kLoaders: one warp's issue rate of
+    // line-coalesced cp.async (the random 128-B v lines) cannot keep the
+    // tensor core fed, four can
+    const int li = warp - kLoaderWarp;
     int g = 0;
     for (int k = 0; k < nitems; ++k) {
       const int si = item_sub(k);
       const SubDev sd = subs[si];
+      const int nchunk = (sd.count + kChunk - 1) / kChunk;
+      const int c0 = (li - g % kLoaders + kLoaders) % kLoaders;   // this warp's first chunk
+      if (c0 >= nchunk) {
+        g += nchunk;
+        continue;
+      }
       const WinDev wd = wins[sd.win];
       const double* __restrict__ rw = rows + wd.row_off + (sd.start - wd.node_off) * 24;
       const int32_t* __restrict__ pw = pix + sd.start;
-      const uint8_t* yd = ydig + ychunk[si] * (int64_t)kYChunkBytes;
       const int rg = (k % ngroups) * 16;
-      const int nchunk = (sd.count + kChunk - 1) / kChunk;
-      int32_t px = (lane < sd.count) ? __ldg(pw + lane) : 0;
-      for (int c = 0; c < nchunk; ++c, ++g) {
-        const int s = g % RS;
-        // next chunk's pixel index, loaded before this chunk's copies
-        const int jn = (c + 1) * kChunk + lane;
-        const int32_t px_next = (c + 1 < nchunk && jn < sd.count) ? __ldg(pw + jn) : 0;
-        if (g >= RS) umma::mbar_wait(&raw_empty[s], ((g / RS) - 1) & 1);
+      int32_t px = (c0 * kChunk + lane < sd.count) ? __ldg(pw + c0 * kChunk + lane) : 0;
+      for (int c = c0; c < nchunk; c += kLoaders) {
+        const int gc = g + c;
+        const int s = gc % RS;
+        // this warp's next chunk's pixel index, loaded before this chunk's copies
+        const int jn = (c + kLoaders) * kChunk + lane;
+        const int32_t px_next = (c + kLoaders < nchunk && jn < sd.count) ? __ldg(pw + jn) : 0;
+        if (gc >= RS) OZW(12, umma::mbar_wait(&raw_empty[s], ((gc / RS) - 1) & 1));
         uint8_t* dst = raw + s * RB;
         const int j0 = c * kChunk, cn = min(kChunk, sd.count - j0);
         if (lane == 0) {
-          umma::mbar_arrive_expect_tx(&raw_full[s], kYChunkBytes);
-          umma::bulk_g2s(dst + kPyY, yd + (int64_t)c * kYChunkBytes, kYChunkBytes, &raw_full[s]);
+          // the chunk's weight rows are contiguous: one bulk copy
+          umma::mbar_arrive_expect_tx(&raw_full[s], (uint32_t)(cn * 192));
+          umma::bulk_g2s(dst, rw + (int64_t)j0 * 24, (uint32_t)(cn * 192), &raw_full[s]);
         }
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
@@ -253,14 +236,10 @@ k_spread_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
             cp_async16(dst + kPyA + nd * 128 + pc * 16,
                        vt + (int64_t)(uint32_t)pxn * nrhs + rg + 2 * pc);
         }
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int nd = q * 8 + (lane >> 2), pc = lane & 3;
-          if (nd < cn) cp_async16(dst + nd * 64 + pc * 16, rw + (int64_t)(j0 + nd) * 24 + 2 * pc);
-        }
         cp_async_mbar_arrive(&raw_full[s]);
         px = px_next;
       }
+      g += nchunk;
     }
   } else if (warp == kIssuerWarp) {
     // ---------------------------------------------------------------- issuer
@@ -268,14 +247,13 @@ k_spread_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
     for (int k = 0; k < nitems; ++k) {
       const SubDev sd = subs[item_sub(k)];
       const int nchunk = (sd.count + kChunk - 1) / kChunk;
-      if (k > 0) umma::mbar_wait(&acc_empty, (k - 1) & 1);   // previous item drained
+      if (k > 0) OZW(13, umma::mbar_wait(&acc_empty, (k - 1) & 1));   // previous item drained
       for (int c = 0; c < nchunk; ++c, ++g) {
         const int st = g % kOpStages, s = g % RS;
-        umma::mbar_wait(&op_ready[st], (g / kOpStages) & 1);
-        umma::mbar_wait(&raw_full[s], (g / RS) & 1);
+        OZW(14, umma::mbar_wait(&op_ready[st], (g / kOpStages) & 1));
         umma::fence_after();
         if (lane == 0) {
-          const uint32_t bB = umma::smem_u32(raw + s * RB + kPyY);
+          const uint32_t bB = umma::smem_u32(sYop + st * kYOpBytes);
           const uint32_t xa = tmem + (uint32_t)(kXTmem0 + st * kSl * 8);
 #pragma unroll
           for (int p = 0; p < kSl; ++p) {
@@ -288,7 +266,6 @@ k_spread_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
             }
           }
           umma::commit(&op_free[st]);
-          umma::commit(&raw_empty[s]);
           if (c == nchunk - 1) umma::commit(&acc_full);
         }
         __syncwarp();
@@ -298,6 +275,8 @@ k_spread_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
     // --------------------------------------------------------------- slicers
     const int m = tid & 127, h = tid >> 7;
     const int a = m >> 4, r = m & 15;
+    const int yn = tid & 63, yq = tid >> 6;      // Y: row (b, c), 8-node quarter
+    const int yb = yn >> 3, yc = yn & 7;
     int g = 0;
     for (int k = 0; k < nitems; ++k) {
       const int si = item_sub(k);
@@ -307,13 +286,31 @@ k_spread_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
       // X row scale: the rhs's max |v| times the subproblem's max |A_a|
       const int ev = max(-900, exp_bound(__longlong_as_double((long long)vmax[rg + r])));
       const double sx = pow2(46 - ev) * pow2(-(int)sub_exp[(int64_t)si * kExpPerSub + a]);
+      // Y column scale 2^(46 - eB_b - eC_c) of the subproblem
+      const double sy = pow2(46 - (int)sub_exp[(int64_t)si * kExpPerSub + 8 + yb]) *
+                        pow2(-(int)sub_exp[(int64_t)si * kExpPerSub + 16 + yc]);
       for (int c = 0; c < nchunk; ++c, ++g) {
         const int st = g % kOpStages, s = g % RS;
-        umma::mbar_wait(&raw_full[s], (g / RS) & 1);
-        if (g >= kOpStages) umma::mbar_wait(&op_free[st], ((g / kOpStages) - 1) & 1);
+        OZW(16, umma::mbar_wait(&raw_full[s], (g / RS) & 1));
+        if (g >= kOpStages) OZW(17, umma::mbar_wait(&op_free[st], ((g / kOpStages) - 1) & 1));
         const double* R = reinterpret_cast<const double*>(raw + s * RB);
         const double* Vr = reinterpret_cast<const double*>(raw + s * RB + kPyA);
         const int cn = min(kChunk, sd.count - c * kChunk);
+        {
+          // Y digits of 8 nodes for row (b, c): K-major canonical, zero past cn
+          uint32_t lo[8], hi[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int j = yq * 8 + i;
+            double x = 0.0, y = 0.0;
+            if (j < cn) {
+              x = R[j * 24 + 8 + yb] * sy;
+              y = R[j * 24 + 16 + yc];
+            }
+            slice1(x, y, lo[i], hi[i]);
+          }
+          store8(lo, hi, sYop + st * kYOpBytes + canon32(yn, yq * 8), kBBytes);
+        }
         uint32_t lo[16], hi[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
@@ -321,7 +318,7 @@ k_spread_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
           double x = 0.0, y = 0.0;
           if (j < cn) {
             x = Vr[j * 16 + r];
-            y = R[j * 8 + a] * sx;
+            y = R[j * 24 + a] * sx;
           }
           slice1(x, y, lo[i], hi[i]);
         }
@@ -335,6 +332,7 @@ k_spread_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
           umma::tmem_st4(xt + (uint32_t)(p * 8), w4[0][p], w4[1][p], w4[2][p], w4[3][p]);
         umma::tmem_wait_st();
         umma::fence_before();
+        umma::fence_async_smem();
         __syncwarp();
         if (lane == 0) {
           mbar_arrive(&op_ready[st]);
@@ -361,32 +359,39 @@ k_spread_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
         eb[q] = ex[8 + q];
         ec[q] = ex[16 + q];
       }
-      umma::mbar_wait(&acc_full, k & 1);
+      OZW(18, umma::mbar_wait(&acc_full, k & 1));
       umma::fence_after();
       double* bo = blocks + (sd.block + a * 64) * nrhs + rg + r;
 #pragma unroll 1
-      for (int c0 = 0; c0 < 64; c0 += 16) {
-        uint32_t dv[kSl][16];
+      for (int c0 = 0; c0 < 64; c0 += 8) {
+        uint32_t dv[kSl][8];
 #pragma unroll
-        for (int t = 0; t < kSl; ++t) umma::tmem_ld16(tl + (uint32_t)(t * 64 + c0), dv[t]);
-        umma::tmem_wait_ld();
-        if (c0 == 48) {
+        for (int t = 0; t < kSl; ++t) umma::tmem_ld8_wait(tl + (uint32_t)(t * 64 + c0), dv[t]);
+        if (c0 == 56) {
           // every column read: the next item's UMMAs may overwrite the accumulator
           umma::fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&acc_empty);
         }
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
+        for (int i = 0; i < 8; ++i) {
+          // sum_t D_t 256^-t: here K is up to 2048 nodes, |D_t| < 6 2^25, so the
+          // int32 pairs of combine6 would overflow -- each diagonal converts on
+          // its own (exact int32 -> fp64 magic, no I2F)
           double acc = 0.0;
 #pragma unroll
-          for (int t = kSl - 1; t >= 0; --t) acc = fma(acc, 0.00390625, (double)(int32_t)dv[t][i]);
+          for (int t = kSl - 1; t >= 0; --t) acc = fma(acc, 0.00390625, i2d(dv[t][i]));
           const int bc = c0 + i;
           bo[(int64_t)bc * nrhs] = acc * rs * pow2(eb[bc >> 3] + ec[bc & 7] + 34);
         }
       }
     }
   }
+#ifdef NLD_OZ_PROF
+  if (lane == 0)
+    atomicAdd(&oz_prof[28 + (warp == kIssuerWarp ? 0 : (warp >= kLoaderWarp && warp < kSPEpi0) ? 1 : warp < kIssuerWarp ? 2 : 3)],
+              (unsigned long long)(clock64() - t_role));
+#endif
   umma::fence_before();
   __syncthreads();
   if (warp == 0) umma::tmem_free<kTmemCols>(tmem);
@@ -440,38 +445,16 @@ int16_t* ozaki_exponents(PlanSet& ps, bool tables, cudaStream_t st) {
     ps.gcell_lo[w] = lo;
     ps.gcell_n[w] = hi - lo + 1;
   }
-  // precomputed Y digits for the spread (12 KB per 32-node chunk) when they
-  // fit comfortably: at most half of the free memory (NLD_SPREAD_PREY=0: off)
-  if (tables) {
-    std::vector<int64_t> off(h.size());
-    int64_t chunks = 0;
-    for (size_t i = 0; i < h.size(); ++i) {
-      off[i] = chunks;
-      chunks += (h[i].count + oz::kChunk - 1) / oz::kChunk;
-    }
-    const size_t need = (size_t)chunks * oz::kYChunkBytes;
-    size_t free_b = 0, total_b = 0;
-    NLD_CUDA(cudaMemGetInfo(&free_b, &total_b));
-    if (need > 0 && need <= free_b / 2) {
-      NLD_CUDA(cudaMalloc(&ps.ychunk, sizeof(int64_t) * off.size()));
-      NLD_CUDA(cudaMalloc(&ps.ydig, need));
-      NLD_CUDA(cudaMemcpyAsync(ps.ychunk, off.data(), sizeof(int64_t) * off.size(),
-                               cudaMemcpyHostToDevice, st));
-      oz::k_spread_ydig<<<(unsigned)h.size(), 256, 0, st>>>(ps.subs[3], ps.wdev, ps.rows,
-                                                            ps.sub_exp, ps.ychunk, ps.ydig);
-      NLD_CUDA(cudaGetLastError());
-    }
-  }
-  // the sliced gather's plan-time tile table (nld_gather_nm.cu)
-  if (tables) gather_nm_tables(ps, h, st);
+  // the sliced spread and gather cut their digits on the fly; `tables` (the
+  // operator's no_sliced knob) only enables them
+  ps.oz_ok = tables;
   NLD_CUDA(cudaStreamSynchronize(st));
   return ps.sub_exp;
 }
 
-// requires the plan-time Y digits (ps.ydig) and the size order (the caller
-// falls back to the fp64 DMMA spread without them)
+// requires the size order (ps.sub_order)
 void launch_spread_oz(const PlanSet& ps, const SubDev* subs, const int16_t* ex,
-                      const int64_t* ychunk, unsigned nsub, const unsigned long long* vmax,
+                      unsigned nsub, const unsigned long long* vmax,
                       const double* vt, int nrhs, double* blocks, cudaStream_t st,
                       const int32_t* order) {
   static int sms = 0;
@@ -484,9 +467,11 @@ void launch_spread_oz(const PlanSet& ps, const SubDev* subs, const int16_t* ex,
   }
   const unsigned grid_n = std::min<unsigned>(nsub, (unsigned)sms);
   oz::k_spread_ozp<<<grid_n, oz::kSPThreads, oz::spread_oz_py_smem(), st>>>(
-      subs, order, (int)nsub, ps.wdev, ps.rows, ps.pix, ex, ps.ydig, ychunk, vmax, vt, nrhs,
-      blocks);
+      subs, order, (int)nsub, ps.wdev, ps.rows, ps.pix, ex, vmax, vt, nrhs, blocks);
   NLD_CUDA(cudaGetLastError());
+#ifdef NLD_OZ_PROF
+  ozaki_prof_dump("spread", st);
+#endif
 }
 
 #ifdef NLD_OZ_PROF

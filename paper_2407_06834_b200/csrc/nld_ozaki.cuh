@@ -18,7 +18,7 @@ constexpr int kSl = NLD_OZ_SL;         // digits per operand
 // -DNLD_OZ_PROF: per-site clock64 totals of the pipeline waits (lane 0 of
 // each warp), printed after each launch -- a tuning aid, not built by default
 #ifdef NLD_OZ_PROF
-__device__ unsigned long long oz_prof[32];
+extern __device__ unsigned long long oz_prof[32];   // defined in nld_ozaki.cu
 #define OZW(site, ...)                                                      \
   do {                                                                      \
     const long long _t0 = clock64();                                        \
@@ -171,6 +171,8 @@ __device__ __forceinline__ double combine6(const uint32_t (&dv)[6][NCOL], int i)
 #endif
 }
 
+// (Both combines need |D_t| <= (t + 1) 2^20, i.e. K <= 64: the gathers'
+// (b, c) contraction, not the spread's node sums.)
 // The six diagonals as two exact fp64 parts, value = hi 2^32 + lo, with two
 // fp64 operations (the rest on the integer pipe): hi = x01 = D0 2^8 + D1 by
 // the int32 magic below; lo = x23 2^16 + x45 (|.| < 2^47) formed by one
@@ -204,7 +206,7 @@ __device__ __forceinline__ void combine6_parts(const uint32_t (&dv)[6][NCOL], in
   double r;
   asm("{\n\t.reg .b64 c;\n\tmov.b64 c, {%1, %2};\n\tmad.wide.s32 c, %3, 65536, c;\n\t"
       "mov.b64 %0, c;\n\t}" : "=d"(r) : "r"(x45b), "r"(0x43380000u), "r"(x23));
-  lo = r - 6755401921888256.0;   // 2^52 + 2^51 + 2^31
+  lo = r - (6755399441055744.0 + 2147483648.0);   // 2^52 + 2^51 + 2^31
   hi = i2d(x01);
 }
 

@@ -848,10 +848,6 @@ void free_planset(PlanSet& ps) {
   cudaFree(ps.wdev);
   cudaFree(ps.sub_exp);
   cudaFree(ps.sub_order);
-  cudaFree(ps.ydig);
-  cudaFree(ps.gtile);
-  cudaFree(ps.gtile_off);
-  cudaFree(ps.ychunk);
   cudaFree(ps.K);
   if (ps.owns_tables) {
     cudaFree(ps.rows);

@@ -124,6 +124,39 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&r)[8]) {
                  "=r"(r[6]), "=r"(r[7])
                : "r"(taddr));
 }
+// Six 32x32b.x4 / x8 loads (column stride `cs`) AND the wait in ONE asm
+// statement: tcgen05.ld writes its registers asynchronously, so outputs of a
+// separate asm are "defined" before the data lands -- the compiler may copy
+// or spill them before tcgen05.wait::ld (seen as nondeterministic results
+// under register pressure).  Here the outputs exist only after the wait.
+__device__ __forceinline__ void tmem_ld4x6_wait(uint32_t taddr, uint32_t cs, uint32_t (&r)[6][4]) {
+  asm volatile(
+      "{\n\t.reg .b32 a1, a2, a3, a4, a5;\n\t"
+      "add.u32 a1, %24, %25;\n\tadd.u32 a2, a1, %25;\n\tadd.u32 a3, a2, %25;\n\t"
+      "add.u32 a4, a3, %25;\n\tadd.u32 a5, a4, %25;\n\t"
+      "tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%24];\n\t"
+      "tcgen05.ld.sync.aligned.32x32b.x4.b32 {%4,%5,%6,%7}, [a1];\n\t"
+      "tcgen05.ld.sync.aligned.32x32b.x4.b32 {%8,%9,%10,%11}, [a2];\n\t"
+      "tcgen05.ld.sync.aligned.32x32b.x4.b32 {%12,%13,%14,%15}, [a3];\n\t"
+      "tcgen05.ld.sync.aligned.32x32b.x4.b32 {%16,%17,%18,%19}, [a4];\n\t"
+      "tcgen05.ld.sync.aligned.32x32b.x4.b32 {%20,%21,%22,%23}, [a5];\n\t"
+      "tcgen05.wait::ld.sync.aligned;\n\t}\n"
+      : "=r"(r[0][0]), "=r"(r[0][1]), "=r"(r[0][2]), "=r"(r[0][3]), "=r"(r[1][0]), "=r"(r[1][1]),
+        "=r"(r[1][2]), "=r"(r[1][3]), "=r"(r[2][0]), "=r"(r[2][1]), "=r"(r[2][2]), "=r"(r[2][3]),
+        "=r"(r[3][0]), "=r"(r[3][1]), "=r"(r[3][2]), "=r"(r[3][3]), "=r"(r[4][0]), "=r"(r[4][1]),
+        "=r"(r[4][2]), "=r"(r[4][3]), "=r"(r[5][0]), "=r"(r[5][1]), "=r"(r[5][2]), "=r"(r[5][3])
+      : "r"(taddr), "r"(cs)
+      : "memory");
+}
+// eight consecutive columns of one lane quarter, loaded and waited for
+__device__ __forceinline__ void tmem_ld8_wait(uint32_t taddr, uint32_t (&r)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n\t"
+               "tcgen05.wait::ld.sync.aligned;\n"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
+                 "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr)
+               : "memory");
+}
 __device__ __forceinline__ void tmem_wait_ld() {
   asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 }

@@ -13,9 +13,9 @@ Extensions (not in the reference, off by default):
     defaults at kernel.py:74); BASELINE pins n_expansion=32, cutoff=4.
   * ``apply`` accepts a batch (nrhs, n) and shares every spread/gather.
   * torch CUDA tensors in -> torch CUDA tensors out (device resident).
-  * ``digit_tables=False``: no plan-time digit tables for the 16k-rhs
-    tensor-core path (a memory budget: those products then run on the fp64
-    DMMA kernels; results agree to rounding).
+  * ``sliced=False``: 16k-rhs batches of 3-D m = 4 windows run on the fp64
+    DMMA kernels instead of the integer-sliced tcgen05 ones (results agree to
+    rounding).
 """
 
 from __future__ import annotations
@@ -51,7 +51,7 @@ class AnovaOperator:
                  oversampling: float = DEFAULT_OVERSAMPLING,
                  rmax: float = DEFAULT_RMAX,
                  truncation_eps: float = DEFAULT_TRUNCATION_EPS, device=None,
-                 digit_tables: bool = True):
+                 sliced: bool = True):
         # validation order of kernel.py:30-48
         if dv.is_torch(features):
             shape = tuple(features.shape)
@@ -89,7 +89,7 @@ class AnovaOperator:
             n_expansion=0 if n_expansion is None else int(n_expansion),
             cutoff=int(cutoff), oversampling=float(oversampling),
             rmax=float(rmax), truncation_eps=float(truncation_eps),
-            mode=0 if mode == "fast" else 1, digit_tables=0 if digit_tables else 1,
+            mode=0 if mode == "fast" else 1, no_sliced=0 if sliced else 1,
             dense_limit=int(dense_limit))
         idx = np.concatenate(wins).astype(np.int32)
         off = np.zeros(len(wins) + 1, np.int32)

@@ -1,0 +1,10 @@
+cd $GRAFT_REPO_ROOT
+L=paper_2407_06834_b200
+cp $L/libnld_b200.so /tmp/prod.so
+for v in sync sync0; do
+cp $L/libnld_b200_$v.so $L/libnld_b200.so
+echo "--- $v" >> gpurun_out/r2_det21.log
+timeout 300 python scripts/diag_det.py c4 16 3 >> gpurun_out/r2_det21.log 2>&1
+timeout 300 python scripts/diag_det.py c1 32 6 >> gpurun_out/r2_det21.log 2>&1
+done
+cp /tmp/prod.so $L/libnld_b200.so

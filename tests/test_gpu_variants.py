@@ -1,9 +1,8 @@
-"""The sliced path's resource fallback and the product build's immunity to
+"""The fp64 DMMA alternative of the sliced path and the product build's immunity to
 the A/B switches.
 
-* ``digit_tables=False`` (a memory budget: no plan-time digit tables) runs
-  16-rhs batches of 3-D m = 4 windows on the fp64 DMMA kernels instead of the
-  tcgen05 integer-sliced ones.  Both must match the reference's own matvec
+* ``sliced=False`` runs 16-rhs batches of 3-D m = 4 windows on the fp64 DMMA
+  kernels instead of the tcgen05 integer-sliced ones.  Both must match the reference's own matvec
   (tests/golden/c1.npz, kernel.py:79-93) at the fp64 parity bar in column 0,
   and agree with each other in EVERY column (1e-12).
 * The product library compiles the experiment switches (nld_switch.cuh) to
@@ -40,14 +39,14 @@ def batch(n):
     return V
 
 
-def test_digit_tables_fallback_matches_reference(golden):
+def test_dmma_alternative_matches_reference(golden):
     g = golden("c1")
     feats, wins, _ = synth.make_problem("c1")
     mu = float(g["mu"])
     coef = np.tile([1.0, mu], 16)
     out = {}
     for tables in (True, False):
-        op = nld.AnovaOperator(feats, wins, synth.SIGMA, digit_tables=tables, **PIN)
+        op = nld.AnovaOperator(feats, wins, synth.SIGMA, sliced=tables, **PIN)
         Vd = torch.from_numpy(batch(op.n)).cuda()
         gam = op.apply_device(Vd, _lib.APPLY_GAMMA, 16, pixel_major=True).cpu().numpy()
         av = op.apply_device(Vd, _lib.APPLY_SYSTEM, 16, coef, pixel_major=True).cpu().numpy()
