@@ -1034,7 +1034,7 @@ void gather_window_fast(const PlanSet& ps, const Workspace& ws, int w, int64_t N
   const unsigned nsub = (unsigned)wp.n_subs;
   if (wp.d == 1) launch_gather<1, MC>(subs, nsub, ps, ws, N, nrhs, st);
   else if (wp.d == 2) launch_gather<2, MC>(subs, nsub, ps, ws, N, nrhs, st);
-  else if (MC == 4 && use_ozaki() && nrhs % 16 == 0 && ps.oz_ok && ws.gdig &&
+  else if (MC == 4 && use_ozaki() && nrhs % 16 == 0 && nrhs <= 256 && ps.oz_ok && ws.gdig &&
            !ab_switch("NLD_OZAKI_NO_GATHER", 0) &&
            w < (int)ps.gcell_n.size() && ps.gcell_n[w] > 0)
     launch_gather_nm(ps, subs, ps.sub_exp + wp.sub_off * 24, ps.sub_order + wp.sub_off,

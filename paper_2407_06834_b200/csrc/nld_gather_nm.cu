@@ -68,6 +68,7 @@ constexpr int kSlicer0 = kEpi, kSlicers = 4;
 constexpr int kIssuer = kEpi + kSlicers, kRLoader = kIssuer + 1, kGLoader = kIssuer + 2;
 constexpr int kThreads = 32 * (kGLoader + 1);
 constexpr int kRawStages = 3;
+constexpr int kMaxCoef = 256;                  // rhs per call (nrhs <= 256 on this path)
 static_assert(kSl == 6, "six digit slices");
 
 __host__ __device__ constexpr int smem_bytes() {
@@ -150,6 +151,7 @@ k_gather_nm(const SubDev* __restrict__ subs, const int32_t* __restrict__ order, 
   __shared__ uint64_t g_full[2], g_empty[2], y_full, y_empty;
   __shared__ uint64_t raw_full[kRawStages], raw_empty[kRawStages], acc_full[2], acc_empty[2];
   __shared__ uint32_t taddr_s;
+  __shared__ double2 s_coef[kMaxCoef];                   // (lam, mu) per rhs (Final mode)
   uint8_t* const sG = smem;                              // [2][kGItem]
   uint8_t* const sY = sG + 2 * kGItem;                   // [kYBytes]
   uint8_t* const sRaw = sY + kYBytes;                    // [3][rows | pix]
@@ -168,6 +170,9 @@ k_gather_nm(const SubDev* __restrict__ subs, const int32_t* __restrict__ order, 
     return order[i * G + ((i & 1) ? (G - 1 - b) : b)];
   };
 
+  if (MODE == mma::kGatherFinal)
+    for (int r = tid; r < nrhs && r < kMaxCoef; r += kThreads)
+      s_coef[r] = ep.coef ? make_double2(ep.coef[2 * r], ep.coef[2 * r + 1]) : make_double2(0.0, 0.0);
   if (warp == 0) umma::tmem_alloc<512>(&taddr_s);
   if (tid == 32) {
     for (int k = 0; k < 2; ++k) {
@@ -397,8 +402,21 @@ k_gather_nm(const SubDev* __restrict__ subs, const int32_t* __restrict__ order, 
 #pragma unroll
           for (int i = 0; i < 8; ++i) sv[i] = 0.0;
         }
+        // Final window: v and eta of the node, issued after pass 1 so their
+        // latency hides behind passes 2-3 (loads at the tile's end stalled
+        // the epilogue -- this window ran at twice the others' time)
+        double2 v01 = make_double2(0.0, 0.0), v23 = v01, v45 = v01, v67 = v01;
+        double et = 0.0;
 #pragma unroll
         for (int ps = 0; ps < 4; ++ps, ++gp) {
+          if (MODE == mma::kGatherFinal && ps == 2 && ok) {
+            const double2* vv = reinterpret_cast<const double2*>(ep.v + e);
+            v01 = vv[0];
+            v23 = vv[1];
+            v45 = vv[2];
+            v67 = vv[3];
+            if (need_eta) et = ep.eta[px];
+          }
           const int ab = gp & 1;
           OZW(10, umma::mbar_wait(&acc_full[ab], (gp >> 1) & 1));
           umma::fence_after();
@@ -460,15 +478,14 @@ k_gather_nm(const SubDev* __restrict__ subs, const int32_t* __restrict__ order, 
         }
         if (!ok) continue;
         double res[8];
+        const double vx[8] = {v01.x, v01.y, v23.x, v23.y, v45.x, v45.y, v67.x, v67.y};
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
           if (MODE != mma::kGatherFinal) {
             res[i] = sv[i];
           } else {
-            const double lam = ep.coef ? ep.coef[2 * (r0 + i)] : 0.0;
-            const double mu = ep.coef ? ep.coef[2 * (r0 + i) + 1] : 0.0;
-            const double et = need_eta ? ep.eta[px] : 0.0;
-            res[i] = mma::epi_value_r(ep.kind, (double)ep.L, inv_L, sv[i], ep.v[e + i], et, lam, mu);
+            const double2 lm = s_coef[r0 + i];
+            res[i] = mma::epi_value_r(ep.kind, (double)ep.L, inv_L, sv[i], vx[i], et, lm.x, lm.y);
           }
         }
         double2* o2 = reinterpret_cast<double2*>(out + e);

@@ -120,7 +120,7 @@ constexpr int kRawV = kChunk * 16 * 8;           // 4 KB of v lines per chunk
 constexpr int kRawRowB = kChunk * 24 * 8;        // 6 KB of weight rows per chunk
 constexpr int kPyA = kRawRowB;                   // v lines offset
 constexpr int kPyRawBytes = kRawRowB + kRawV;    // 10 KB
-constexpr int kPyRawStages = 8;
+constexpr int kPyRawStages = 16;                // deep: the random v-line gathers are latency bound
 constexpr int kOpStages = 2;                     // X stages in TMEM: 384 + 2 x 48 <= 512
 constexpr int kYOpBytes = kSl * kBBytes;         // 12 KB of Y digits per chunk
 __host__ __device__ constexpr int spread_oz_py_smem() {
