@@ -365,8 +365,7 @@ k_spread_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
 #pragma unroll 1
       for (int c0 = 0; c0 < 64; c0 += 8) {
         uint32_t dv[kSl][8];
-#pragma unroll
-        for (int t = 0; t < kSl; ++t) umma::tmem_ld8_wait(tl + (uint32_t)(t * 64 + c0), dv[t]);
+        umma::tmem_ld8x6_wait(tl + (uint32_t)c0, 64, dv);
         if (c0 == 56) {
           // every column read: the next item's UMMAs may overwrite the accumulator
           umma::fence_before();
