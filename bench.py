@@ -429,9 +429,7 @@ def run_ours(args, world, rank, local):
         # slices) -> 1344 * 128 * 32 * 2 ops per 32 nodes
         n3 = sum(1 for i in info if i["dim"] == 3)
         ops = n * (nrhs // 16) * (1344 * 128 * 32 * 2 // 32) * n3
-        persist = os.environ.get("NLD_GATHER_PERSIST", "1") != "0"
-        gtag = "k_gather_ozp" if persist else "k_gather_oz"
-        tag = gtag if dominant == "gather" else "k_spread_oz"
+        tag = "k_gather_nm" if dominant == "gather" else "k_spread_ozp"
         tops = ops / (dom_ms * 1e-3) / 1e12
         roofline = {
             "bound": "tensor", "achieved": tops, "peak": imma_peak, "unit": "TOPS (int8)",
