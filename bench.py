@@ -281,7 +281,10 @@ def run_ours(args, world, rank, local):
             dist.init_process_group("nccl", device_id=dev)
         pg = dist
     cfg = synth.CONFIGS[args.config]
-    nrhs = args.nrhs or cfg.n_alpha
+    # the throughput line is the 16-rhs batch at every config (c4: its alpha
+    # sweep; c2/c3: 16 right-hand sides sharing each product); the config's
+    # own solve (c2: one image, c3: three channels) is timed in `cg`
+    nrhs = args.nrhs or 16
     feats, wins, f_img = synth.make_problem(args.config)
     n_global = feats.shape[0]
     # pixel sharding (strong scaling): this rank's contiguous slice
@@ -303,7 +306,8 @@ def run_ours(args, world, rank, local):
     if pg:
         pg.all_reduce(eta_sum)
     mean_eta = float(eta_sum) / n_global
-    alphas = synth.alpha_sweep(mean_eta, nrhs)
+    alphas = (synth.alpha_sweep(mean_eta, nrhs) if cfg.n_alpha > 1
+              else np.full(nrhs, synth.ALPHA_SCALE / mean_eta))
     coef = np.stack([np.ones(nrhs), alphas], axis=1).ravel()
     gen = torch.Generator(device=dev)
     gen.manual_seed(1234 + rank)
@@ -465,20 +469,59 @@ def run_ours(args, world, rank, local):
             "hbm": hbm, "stage_share": share,
         }
 
-    # CG denoise solve (deflated Jacobi, tol 1e-6) over the alpha sweep
+    # single-rhs product throughput (the reference's own bench-op times one
+    # ShiftedSystem.apply(v), cli.py:347-357): fp64 DMMA kernels at nrhs = 1
+    single = None
+    if cfg.n_alpha == 1 and not args.no_cg:
+        v1 = torch.randn(n, dtype=torch.float64, device=dev, generator=gen)
+        y1 = torch.empty_like(v1)
+        c1v = coef[:2].copy()
+        for _ in range(2):
+            op.apply_device(v1, _lib.APPLY_SYSTEM, 1, c1v, out=y1, pixel_major=True)
+        if pg:
+            pg.barrier()
+        torch.cuda.synchronize()
+        s0 = torch.cuda.Event(enable_timing=True)
+        s1 = torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        for _ in range(args.steps):
+            op.apply_device(v1, _lib.APPLY_SYSTEM, 1, c1v, out=y1, pixel_major=True)
+        s1.record(stream)
+        torch.cuda.synchronize()
+        sms = s0.elapsed_time(s1) / max(args.steps, 1)
+        if pg:
+            t = torch.tensor([sms], device=dev)
+            pg.all_reduce(t, op=pg.ReduceOp.MAX)
+            sms = float(t.item())
+        single = {"value": 1e3 / sms, "unit": UNIT, "ms_per_matvec": sms,
+                  "kernels": "fp64 DMMA spread/gather (nrhs = 1)"}
+        del v1, y1
+
+    # CG denoise solve (deflated Jacobi, tol 1e-6): c4 the 16-alpha sweep,
+    # c2 the image, c3 its three channels as right-hand sides (alpha =
+    # 10 / mean eta)
     cg = None
     if not args.no_cg:
-        f = torch.from_numpy(np.ascontiguousarray(f_img[:, 0])).to(dev)
+        if cfg.n_alpha > 1:
+            f = torch.from_numpy(np.ascontiguousarray(f_img[:, 0])).to(dev)
+            cg_alpha = alphas
+        else:
+            f = torch.from_numpy(np.ascontiguousarray(f_img.T)).to(dev)
+            if f.shape[0] == 1:
+                f = f[0]
+            cg_alpha = synth.ALPHA_SCALE / mean_eta
         torch.cuda.synchronize()
         c0 = torch.cuda.Event(enable_timing=True)
         c1 = torch.cuda.Event(enable_timing=True)
         c0.record(stream)
-        res = nld.deflated_solve_batched(op, f, 1.0, alphas, prec="jacobi",
+        res = nld.deflated_solve_batched(op, f, 1.0, cg_alpha, prec="jacobi",
                                          tol=synth.CG_TOL, maxit=200)
         c1.record(stream)
         torch.cuda.synchronize()
         its = [r.iterations for r in res]
-        cg = {"solve_ms": c0.elapsed_time(c1), "nrhs": nrhs,
+        cg = {"solve_ms": c0.elapsed_time(c1), "nrhs": len(res),
+              "rhs": ("16 alphas log-spaced over [1,100]/mean eta" if cfg.n_alpha > 1
+                      else f"{cfg.channels} channel(s), alpha = 10/mean eta"),
               "iterations": its, "converged": all(r.converged for r in res),
               "relres_max": max(r.relative_residual for r in res),
               "tol": synth.CG_TOL, "prec": "jacobi (deflated)"}
@@ -492,7 +535,7 @@ def run_ours(args, world, rank, local):
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "port",
                    "sample": f"unavailable: {exc}"}
     if cg is not None and cpu is not None and cpu.get("value"):
-        nmv = sum(cg["iterations"]) + 2 * nrhs
+        nmv = sum(cg["iterations"]) + 2 * cg["nrhs"]
         cg["cpu_extrapolated_s"] = nmv / cpu["value"]
         cg["cpu_extrapolation"] = ("reference matvecs (iterations + 2 per alpha) "
                                    "x sampled CPU matvec time")
@@ -525,6 +568,7 @@ def run_ours(args, world, rank, local):
                     "steps": e2e_steps,
                     "api": "AnovaOperator.apply_pipelined (pinned host batches; H2D of batch "
                            "k+1, product of k, D2H of k-1 overlapped on three streams)"},
+            "single_rhs": single,
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
             "cg": cg,

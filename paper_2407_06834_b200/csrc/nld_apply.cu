@@ -323,15 +323,21 @@ k_asm_p1(const WinDev* __restrict__ wins, int w, const int2* __restrict__ cellin
     rest >>= 6;
     const int p2 = (int)(rest % B2);
     const int64_t row = rest / B2;            // c0 * B1 + c1
+    // the eight cells' (first block, count) first, all loads independent --
+    // most cells of the box are empty, so a chain of dependent index -> block
+    // loads per o2 left this pass latency bound
+    int2 cs[8];
+#pragma unroll
+    for (int o2 = 0; o2 < 8; ++o2)
+      cs[o2] = p2 - o2 >= 0 ? __ldg(ci + row * B2 + p2 - o2) : make_int2(0, 0);
     double sum = 0.0;
 #pragma unroll
-    for (int o2 = 0; o2 < 8; ++o2) {
-      const int c2 = p2 - o2;
-      if (c2 < 0) break;
-      const int2 c = ci[row * B2 + c2];
-      for (int q = 0; q < c.y; ++q)
-        sum += blocks[((int64_t)c.x + (int64_t)q * 512 + o01 * 8 + o2) * nrhs + r];
-    }
+    for (int o2 = 0; o2 < 8; ++o2)
+      if (cs[o2].y > 0) sum += __ldg(blocks + ((int64_t)cs[o2].x + o01 * 8 + o2) * nrhs + r);
+#pragma unroll
+    for (int o2 = 0; o2 < 8; ++o2)   // cells split into several subproblems
+      for (int q = 1; q < cs[o2].y; ++q)
+        sum += __ldg(blocks + ((int64_t)cs[o2].x + (int64_t)q * 512 + o01 * 8 + o2) * nrhs + r);
     y1[id] = sum;
   }
 }
@@ -596,7 +602,7 @@ __global__ void __launch_bounds__(kThreads)
 k_gather(const SubDev* __restrict__ subs, const CellDev* __restrict__ cells,
          const WinDev* __restrict__ wins, const double* __restrict__ rows,
          const int32_t* __restrict__ pix, const double* __restrict__ grid,
-         int64_t grid_ld, double* __restrict__ wout, int64_t N, int nrhs) {
+         int64_t grid_ld, double* __restrict__ wout, int64_t N, int nrhs, int accum) {
   using G = Geo<D, MC>;
   extern __shared__ double gb[];   // [GRB][BLK]
   const SubDev sd = subs[blockIdx.x];
@@ -604,7 +610,10 @@ k_gather(const SubDev* __restrict__ subs, const CellDev* __restrict__ cells,
   const WinDev wd = wins[sd.win];
   const int64_t local = sd.start - wd.node_off;
   const double* __restrict__ rw = rows + wd.row_off + local * G::ROW;
-  double* __restrict__ out = wout + (int64_t)sd.win * N * nrhs;
+  // accum < 0: this window's slot of wout [L][N][nrhs]; otherwise wout is the
+  // fused product's running window sum [N][nrhs] (store if accum == 0, add if
+  // 1 -- each node is in exactly one subproblem of the window: no races)
+  double* __restrict__ out = accum < 0 ? wout + (int64_t)sd.win * N * nrhs : wout;
   for (int rg = 0; rg < nrhs; rg += G::GRB) {
     const int rn = min(G::GRB, nrhs - rg);
     __syncthreads();
@@ -659,7 +668,7 @@ k_gather(const SubDev* __restrict__ subs, const CellDev* __restrict__ cells,
           if (D == 3) y = fma(ua, wrow[a], y);
           else y = ua;
         }
-        o[q] = y;
+        o[q] = accum > 0 ? o[q] + y : y;
       }
     }
   }
@@ -923,7 +932,7 @@ void launch_spread(const SubDev* subs, unsigned nsub, const PlanSet& ps, const W
 
 template <int D, int MC>
 void launch_gather(const SubDev* subs, unsigned nsub, const PlanSet& ps, const Workspace& ws,
-                   int64_t N, int nrhs, cudaStream_t st) {
+                   int64_t N, int nrhs, cudaStream_t st, double* fout = nullptr, int accum = -1) {
   using G = Geo<D, MC>;
   size_t smem = sizeof(double) * G::BLK * std::min(nrhs, G::GRB);
   static bool attr = false;
@@ -933,7 +942,9 @@ void launch_gather(const SubDev* subs, unsigned nsub, const PlanSet& ps, const W
     attr = true;
   }
   k_gather<D, MC><<<nsub, kThreads, smem, st>>>(subs, ps.cells, ps.wdev, ps.rows, ps.pix,
-                                                ws.grid_out, ps.grid_total, ws.wout, N, nrhs);
+                                                ws.grid_out, ps.grid_total,
+                                                fout ? fout : ws.wout, N, nrhs,
+                                                fout ? accum : -1);
   NLD_CUDA(cudaGetLastError());
 }
 
@@ -1032,8 +1043,12 @@ void gather_window_fast(const PlanSet& ps, const Workspace& ws, int w, int64_t N
   if (!ps.wdev_h[w].fast || wp.n_subs == 0) return;
   const SubDev* subs = ps.subs[wp.d] + wp.sub_off;
   const unsigned nsub = (unsigned)wp.n_subs;
-  if (wp.d == 1) launch_gather<1, MC>(subs, nsub, ps, ws, N, nrhs, st);
-  else if (wp.d == 2) launch_gather<2, MC>(subs, nsub, ps, ws, N, nrhs, st);
+  // fused product (ep.mode != kGatherStore): 1-/2-D windows run before the
+  // 3-D ones and store (first) or add into the running window sum `out`
+  double* fout = ep.mode == mma::kGatherStore ? nullptr : out;
+  const int acc = ep.mode == mma::kGatherFirst ? 0 : 1;
+  if (wp.d == 1) launch_gather<1, MC>(subs, nsub, ps, ws, N, nrhs, st, fout, acc);
+  else if (wp.d == 2) launch_gather<2, MC>(subs, nsub, ps, ws, N, nrhs, st, fout, acc);
   else if (MC == 4 && use_ozaki() && nrhs % 16 == 0 && nrhs <= 256 && ps.oz_ok && ws.gdig &&
            !ab_switch("NLD_OZAKI_NO_GATHER", 0) &&
            w < (int)ps.gcell_n.size() && ps.gcell_n[w] > 0)
@@ -1230,6 +1245,61 @@ static void gather_window(nld_operator* op, const PlanSet& ps, int w, int nrhs,
   if (e.mode != mma::kGatherFinal) edges();
 }
 
+// window w's slice of the support-box grids [nrhs][grid_ld] <-> a contiguous
+// [nrhs][box] buffer (+ `extra` trailing values), for a per-window allreduce
+__global__ void k_pack_win(const double* __restrict__ grid, int64_t grid_ld, int64_t off,
+                           int64_t box, int nrhs, const double* __restrict__ extra, int n_extra,
+                           double* __restrict__ buf) {
+  const int64_t total = box * nrhs;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total + n_extra;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    if (e < total) {
+      const int64_t r = e / box, f = e - r * box;
+      buf[e] = grid[r * grid_ld + off + f];
+    } else {
+      buf[e] = extra[e - total];
+    }
+  }
+}
+__global__ void k_unpack_win(const double* __restrict__ buf, int64_t grid_ld, int64_t off,
+                             int64_t box, int nrhs, double* __restrict__ extra, int n_extra,
+                             double* __restrict__ grid) {
+  const int64_t total = box * nrhs;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total + n_extra;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    if (e < total) {
+      const int64_t r = e / box, f = e - r * box;
+      grid[r * grid_ld + off + f] = buf[e];
+    } else {
+      extra[e - total] = buf[e];
+    }
+  }
+}
+
+// the shard allreduce of window w's grids alone (so it can run on the aux
+// stream behind that window's assemble while the main stream spreads the
+// next window): packed into the convolution scratch, summed, unpacked; the
+// last window also carries the per-rhs non-finite flags
+static void comm_window(nld_operator* op, const PlanSet& ps, int w, int nrhs, bool flags,
+                        cudaStream_t st) {
+  if (!op->comm) return;
+  Workspace& ws = op->ws;
+  const WinDev& wd = ps.wdev_h[w];
+  double* extra = ws.grid_in + ps.grid_total * nrhs;
+  const int ne = flags ? nrhs : 0;
+  double* buf = reinterpret_cast<double*>(ws.cbuf0);
+  const int64_t cnt = wd.box_size * nrhs + ne;
+  k_pack_win<<<grid_blocks(cnt, 256, 148 * 8), 256, 0, st>>>(ws.grid_in, ps.grid_total,
+                                                             wd.grid_off, wd.box_size, nrhs,
+                                                             extra, ne, buf);
+  NLD_CUDA(cudaGetLastError());
+  comm_device(op, buf, cnt, st);
+  k_unpack_win<<<grid_blocks(cnt, 256, 148 * 8), 256, 0, st>>>(buf, ps.grid_total, wd.grid_off,
+                                                               wd.box_size, nrhs, extra, ne,
+                                                               ws.grid_in);
+  NLD_CUDA(cudaGetLastError());
+}
+
 // spread of all windows into the support boxes ws.grid_in [nrhs][grid_total]
 // (+ the shard allreduce).  vt: right-hand sides pixel-major [N][nrhs].
 int spread_stage(nld_operator* op, const PlanSet& ps, const double* vt, int nrhs,
@@ -1303,23 +1373,37 @@ void apply_op(nld_operator* op, int which, int kind, const double* v, double* ou
     launches += 1;   // k_vmax (its resets are memsets, not kernels)
   }
   const int no_overlap = ab_switch("NLD_NO_OVERLAP", 0);
-  const bool overlap = !op->comm && L <= 16 && !no_overlap;
+  const bool overlap = L <= 16 && !no_overlap;
   // fused gather epilogue (see gather_window): every window on the DMMA
   // gather, pixel-major in/out, out not aliasing v
   const int no_fuse = ab_switch("NLD_NO_FUSED_EPILOGUE", 0);
   bool fused = !no_fuse && pixel_major && nrhs >= 8 && L >= 2 && out != v &&
                op->params.cutoff == 4 && use_mma();
+  // gather order: 1-/2-D windows first, then the 3-D ones (the last of which
+  // applies the epilogue); every window on a fast path with subproblems
+  std::vector<int> gorder;
+  int n3 = 0;
   for (int w = 0; w < L && fused; ++w) {
     const WinDev& wd = ps.wdev_h[w];
-    fused = wd.fast && wd.d == 3 && ps.win[w].n_subs > 0;
+    fused = wd.fast && ps.win[w].n_subs > 0;
+    if (wd.d != 3) gorder.push_back(w);
+    else ++n3;
   }
-  auto gather_w = [&](int w) {
+  fused = fused && n3 > 0;
+  for (int w = 0; w < L; ++w)
+    if (ps.wdev_h[w].d == 3) gorder.push_back(w);
+  if (!fused) {
+    gorder.resize(L);
+    for (int w = 0; w < L; ++w) gorder[w] = w;
+  }
+  auto gather_k = [&](int k) {   // the k-th window in gather order
+    const int w = gorder[k];
     if (!fused) {
       gather_window(op, ps, w, nrhs, st);
       return;
     }
-    mma::GatherEpi ep{w == 0 ? mma::kGatherFirst
-                             : (w == L - 1 ? mma::kGatherFinal : mma::kGatherAccum),
+    mma::GatherEpi ep{k == 0 ? mma::kGatherFirst
+                             : (k == L - 1 ? mma::kGatherFinal : mma::kGatherAccum),
                       kind, L, v, eta, coef_dev};
     gather_window(op, ps, w, nrhs, st, &ep, out);
   };
@@ -1333,16 +1417,17 @@ void apply_op(nld_operator* op, int which, int kind, const double* v, double* ou
       NLD_CUDA(cudaEventRecord(op->ev_spread[w], st));
       NLD_CUDA(cudaStreamWaitEvent(op->aux, op->ev_spread[w], 0));
       assemble_window(op, ps, w, vt, nrhs, op->aux);
+      comm_window(op, ps, w, nrhs, sliced && w == L - 1, op->aux);
       conv_window(op, ps, w, nrhs, op->aux);
       NLD_CUDA(cudaEventRecord(op->ev_conv[w], op->aux));
     }
     ev.mark();
-    NLD_CUDA(cudaStreamWaitEvent(st, op->ev_conv[0], 0));
+    NLD_CUDA(cudaStreamWaitEvent(st, op->ev_conv[gorder[0]], 0));
     ev.mark();
     ev.mark();
-    for (int w = 0; w < L; ++w) {
-      if (w > 0) NLD_CUDA(cudaStreamWaitEvent(st, op->ev_conv[w], 0));
-      gather_w(w);
+    for (int k = 0; k < L; ++k) {
+      if (k > 0) NLD_CUDA(cudaStreamWaitEvent(st, op->ev_conv[gorder[k]], 0));
+      gather_k(k);
     }
   } else {
     spread_stage(op, ps, vt, nrhs, st, sliced);
@@ -1350,7 +1435,7 @@ void apply_op(nld_operator* op, int which, int kind, const double* v, double* ou
     ev.mark();
     for (int w = 0; w < L; ++w) conv_window(op, ps, w, nrhs, st);
     ev.mark();
-    for (int w = 0; w < L; ++w) gather_w(w);
+    for (int k = 0; k < L; ++k) gather_k(k);
   }
   for (int w = 0; w < L; ++w) {
     // spread + gather (+ the sliced gather's per-cell G digits), assemble

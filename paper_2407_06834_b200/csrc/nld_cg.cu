@@ -301,10 +301,12 @@ struct Reducer {
     k_cg_reduce<MODE><<<nblk, kRT, 0, st>>>(c, sc, vecA, part);
     NLD_CUDA(cudaGetLastError());
     k_final<<<nrhs, 32, 0, st>>>(part, nblk, out);
+    // sharded: the per-rank partial scalars are summed on the device, on the
+    // stream (NCCL), before the one host read the solver's decisions need
+    comm_device(op, out, (int64_t)nrhs * kMaxK, st);
     NLD_CUDA(cudaMemcpyAsync(host.data(), out, sizeof(double) * nrhs * kMaxK,
                              cudaMemcpyDeviceToHost, st));
     NLD_CUDA(cudaStreamSynchronize(st));
-    comm_host(op, host.data(), (int64_t)nrhs * kMaxK, RED_F64, RED_OP_SUM);
     return host;
   }
 };

@@ -24,16 +24,20 @@
 // as M and nodes as N, needed a 3-stage shuffle butterfly over a per output.)
 //
 // Roles (one persistent CTA per SM, items = (subproblem, 16-rhs group) dealt
-// in snake order of descending size):
-//   warps 0-7   epilogue (lane quarter = warp & 3, rhs slots 2 (warp >> 2) and
-//               2 (warp >> 2) + 1, i.e. rhs 8 (warp >> 2) .. + 7 of the group)
-//   warps 8-11  slicers: per 128-node tile the Y digits of each node (thread =
+// in snake order of descending size), one warpgroup each except the epilogue:
+//   warps 0-15  epilogue (lane quarter = warp & 3, rhs slot w = warp >> 2: rhs
+//               4w .. 4w + 3 of the group, one per pass); 4 warpgroups, whose
+//               latency-bound combine chains need the warps more than the
+//               registers (setmaxnreg moves the producers' spare registers here)
+//   warps 16-19 slicers: per 128-node tile the Y digits of each node (thread =
 //               node) from its staged weight row, into the operand stage
-//   warp 12     UMMA issuer (one lane): Y digits -> TMEM, 4 passes x 12 UMMAs
-//   warp 13     row loader: per tile one TMA bulk copy of the nodes' weight
-//               rows (A | B | C, 192 B each) + the pixel indices (cp.async)
-//   warp 14     G loader: per item one TMA bulk copy of the cell's G digits
+//   warp 20     UMMA issuer (one lane): Y digits -> TMEM, 4 passes x 12 UMMAs
+//   warp 21     row loader: per tile one TMA bulk copy of the nodes' weight
+//               rows (A | B | C, 192 B each) + the pixel indices (cp.async),
+//               and an L2 prefetch of the tile's random per-pixel lines
+//   warp 22     G loader: per item one TMA bulk copy of the cell's G digits
 //               (48 KB + exponents, k_gdig_nm, once per product)
+//   warp 23     idle (completes the producer warpgroup)
 // Cutting Y on the fly (64 values per node) reads 196 B per node-window
 // instead of streaming 452 B of precomputed digits + A parts: the gather's
 // HBM traffic, not its arithmetic, bounded it with plan-time digits.
@@ -46,6 +50,7 @@
 #include "nld_internal.cuh"
 #include "nld_ozaki.cuh"
 #include "nld_umma.cuh"
+#include "nld_switch.cuh"
 
 namespace nld {
 namespace oz {
@@ -63,10 +68,38 @@ constexpr int kGBytes = 4 * kSl * kGBlk;       // 48 KB: [pass][q][32 x 64]
 constexpr int kGItem = kGBytes + 16 * 4;       // + one exponent per rhs
 constexpr int kAccCols = kSl * kPassRows;      // 192 accumulator columns per pass
 constexpr int kYT0 = 2 * kAccCols;             // Y digits in TMEM: columns 384..479
-constexpr int kEpi = 8;
-constexpr int kSlicer0 = kEpi, kSlicers = 4;
+#ifndef NLD_GNM_EPI
+#define NLD_GNM_EPI 8
+#endif
+constexpr int kEpi = NLD_GNM_EPI;                  // 8 or 16 epilogue warps
+constexpr int kSPW = 16 / kEpi;                    // rhs slots (4 rhs each) per epilogue warp
+#ifndef NLD_GNM_SLC
+#define NLD_GNM_SLC 4
+#endif
+// slicer warps: 4 (one node per thread, all 64 (b, c)) or 8 (two warps per
+// node quarter, 32 (b, c) each) -- cutting a tile's digits is a latency-bound
+// chain (DFMA, byte transposes, stores) on the issuer's critical path
+constexpr int kSlicer0 = kEpi, kSlicers = NLD_GNM_SLC;
+constexpr int kKqPer = 16 / kSlicers;              // 16-element (b, c) groups per slicer thread
 constexpr int kIssuer = kEpi + kSlicers, kRLoader = kIssuer + 1, kGLoader = kIssuer + 2;
-constexpr int kThreads = 32 * (kGLoader + 1);
+constexpr int kThreads = 32 * (kIssuer + 4);          // whole warpgroups
+static_assert(kEpi == 8 || kEpi == 16, "epilogue warps");
+static_assert(kSlicers == 4 || kSlicers == 8, "slicer warps");
+// register budgets per warpgroup when the launch budget (65536 / kThreads,
+// multiple of 8) is below what the epilogue and slicers need: the producer
+// warpgroup (issuer, loaders) gives registers back, the epilogue takes them
+constexpr int kRegsLaunch = ((65536 / kThreads) & ~7) > 255 ? 255 : ((65536 / kThreads) & ~7);
+constexpr bool kSetRegs = kRegsLaunch < 128;
+#ifndef NLD_GNM_RP
+#define NLD_GNM_RP 64
+#endif
+constexpr int kRegsProducer = NLD_GNM_RP;
+constexpr int kRegsSlicer = kRegsLaunch;
+constexpr int kRegsEpi =
+    ((kRegsLaunch * 32 * kEpi + (kRegsLaunch - kRegsProducer) * 128) / (32 * kEpi)) & ~7;
+static_assert(!kSetRegs || kRegsEpi * 32 * kEpi + kRegsSlicer * 32 * kSlicers + kRegsProducer * 128 <=
+                               kRegsLaunch * kThreads,
+              "register budget");
 constexpr int kRawStages = 3;
 constexpr int kMaxCoef = 256;                  // rhs per call (nrhs <= 256 on this path)
 static_assert(kSl == 6, "six digit slices");
@@ -91,6 +124,13 @@ __device__ __forceinline__ void release_after_loads(uint64_t* bar, int lane, int
   const bool never = __any_sync(0xffffffffu, fold == 0x5a5a5a5a5a5a5a5aull);
   // the barrier address depends on the vote, hence on every lane's loads
   if (lane == 0) mbar_arrive(never ? bar + 64 : bar);
+}
+
+// timing experiments: spin for n cycles (causal profiling of a role)
+__device__ __forceinline__ void spin_cycles(long long n) {
+  const long long t0 = clock64();
+  while (clock64() - t0 < n) {
+  }
 }
 
 // ---- G digits of every cell, once per product ------------------------------
@@ -146,7 +186,10 @@ k_gather_nm(const SubDev* __restrict__ subs, const int32_t* __restrict__ order, 
             const WinDev* __restrict__ wins, const double* __restrict__ rows,
             const int32_t* __restrict__ pix, const int16_t* __restrict__ sub_exp,
             const uint8_t* __restrict__ gdig, double* __restrict__ out, int nrhs,
-            mma::GatherEpi ep) {
+            mma::GatherEpi ep, int xf) {
+#ifndef NLD_AB_BUILD
+  xf = 0;   // timing experiments (bit mask) exist only in the A/B build
+#endif
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ uint64_t g_full[2], g_empty[2], y_full, y_empty;
   __shared__ uint64_t raw_full[kRawStages], raw_empty[kRawStages], acc_full[2], acc_empty[2];
@@ -158,6 +201,7 @@ k_gather_nm(const SubDev* __restrict__ subs, const int32_t* __restrict__ order, 
 
   // warp index through a shuffle: warp-uniform to the compiler, so the TMEM
   // addresses derived from it live in uniform registers
+  OZ_TRACE_DECL
   const int tid = threadIdx.x, lane = tid & 31;
   const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
   const int ngroups = nrhs / 16;
@@ -197,51 +241,136 @@ k_gather_nm(const SubDev* __restrict__ subs, const int32_t* __restrict__ order, 
   const long long t_role = clock64();
 #endif
 
-  if (warp == kGLoader) {
-    // ------------------------------------------------------------- G loader
-    if (lane == 0) {
+  if (warp >= kIssuer) {
+    // producer warpgroup: issuer, row loader, G loader (+ one idle warp)
+    if (kSetRegs) umma::regs_dec<kRegsProducer>();
+    if (warp == kGLoader) {
+      // ------------------------------------------------------------- G loader
+      if (lane == 0) {
+        for (int k = 0; k < nitems; ++k) {
+          const int gs = k & 1;
+          if (k >= 2) OZW(6, umma::mbar_wait(&g_empty[gs], ((k >> 1) - 1) & 1));
+          const uint8_t* src = gdig + ((int64_t)subs[item_sub(k)].cell * ngroups + k % ngroups) *
+                                          (int64_t)kGItem;
+          umma::mbar_arrive_expect_tx(&g_full[gs], (xf & 512) ? 0 : kGItem);
+          if (!(xf & 512)) umma::bulk_g2s(sG + gs * kGItem, src, kGItem, &g_full[gs]);
+        }
+      }
+    } else if (warp == kRLoader) {
+      // ----------------------------------------------------------- row loader
+      int gt = 0;
       for (int k = 0; k < nitems; ++k) {
-        const int gs = k & 1;
-        if (k >= 2) OZW(6, umma::mbar_wait(&g_empty[gs], ((k >> 1) - 1) & 1));
-        const uint8_t* src = gdig + ((int64_t)subs[item_sub(k)].cell * ngroups + k % ngroups) *
-                                        (int64_t)kGItem;
-        umma::mbar_arrive_expect_tx(&g_full[gs], kGItem);
-        umma::bulk_g2s(sG + gs * kGItem, src, kGItem, &g_full[gs]);
+        const SubDev sd = subs[item_sub(k)];
+        const WinDev wd = wins[sd.win];
+        const double* __restrict__ rw = rows + wd.row_off + (sd.start - wd.node_off) * 24;
+        const int32_t* __restrict__ pw = pix + sd.start;
+        const int ntile = (sd.count + kT - 1) / kT;
+        for (int tl = 0; tl < ntile; ++tl, ++gt) {
+          const int s = gt % kRawStages;
+          if (gt >= kRawStages) OZW(4, umma::mbar_wait(&raw_empty[s], ((gt / kRawStages) - 1) & 1));
+          if (xf & 32768) spin_cycles(1000);
+          uint8_t* dst = sRaw + s * kRawBytes;
+          const int j0 = tl * kT, cn = min(kT, sd.count - j0);
+          if (lane == 0) {
+            umma::mbar_arrive_expect_tx(&raw_full[s], (xf & 1024) ? 0u : (uint32_t)(cn * kRowBytes));
+            if (!(xf & 1024))
+              umma::bulk_g2s(dst, rw + (int64_t)j0 * 24, (uint32_t)(cn * kRowBytes), &raw_full[s]);
+          }
+  #pragma unroll
+          for (int q = 0; q < kT / 32; ++q) {
+            const int nd = q * 32 + lane;
+            if (nd < cn && !(xf & 1024)) cp_async4(dst + kT * kRowBytes + 4 * nd, pw + j0 + nd);
+          }
+          cp_async_mbar_arrive(&raw_full[s]);
+          // The epilogue's per-node accesses (running window sum; v and eta in
+          // the final window) are random 128-B lines: pull them into L2 now, a
+          // few tiles before the epilogue reads them, so its loads wait for L2,
+          // not HBM (one tile of lines in flight per SM cannot cover HBM latency)
+          if (MODE >= mma::kGatherAccum && !(xf & 64)) {
+            const int rq = k % ngroups;
+  #pragma unroll
+            for (int q = 0; q < kT / 32; ++q) {
+              const int nd = q * 32 + lane;
+              if (nd < cn) {
+                const int64_t px = __ldg(pw + j0 + nd);
+                prefetch_l2(out + px * nrhs + rq * 16);
+                if (MODE == mma::kGatherFinal) {
+                  prefetch_l2(ep.v + px * nrhs + rq * 16);
+                  if (ep.eta) prefetch_l2(ep.eta + px);
+                }
+              }
+            }
+          }
+        }
+      }
+    } else if (warp == kIssuer) {
+      // ---------------------------------------------------------------- issuer
+      if (lane == 0) {
+        int gt = 0, gp = 0;
+        const uint32_t yB = umma::smem_u32(sY);
+        for (int k = 0; k < nitems; ++k) {
+          const int gs = k & 1;
+          const int ntile = (subs[item_sub(k)].count + kT - 1) / kT;
+          OZW(0, umma::mbar_wait(&g_full[gs], (k >> 1) & 1));
+          const uint32_t gB = umma::smem_u32(sG + gs * kGItem);
+          for (int tl = 0; tl < ntile; ++tl, ++gt) {
+            OZW(1, umma::mbar_wait(&y_full, gt & 1));
+            if (xf & 4096) spin_cycles(1000);
+            umma::fence_after();
+            // the tile's Y digits -> TMEM (the UMMA A operand of all four passes);
+            // ordered behind the previous tile's UMMAs, which read the old copy
+  #pragma unroll
+            for (int p = 0; p < kSl; ++p)
+  #pragma unroll
+              for (int ks = 0; ks < 2; ++ks)
+                if (!(xf & 16)) umma::tmem_cp_128x256b(tmem + (uint32_t)(kYT0 + p * 16 + ks * 8),
+                                       umma::make_sdesc(yB + p * kYSlice + ks * 256, 128, 512));
+            // The staging is released by the commit after the first pass's UMMAs,
+            // not right after the copies: a commit issued directly behind
+            // tcgen05.cp was measured to fire before the copy's shared-memory
+            // reads were done (the slicers' next writes raced with it); the
+            // UMMAs consume the copied digits, so their completion implies it.
+            for (int ps = 0; ps < 4; ++ps, ++gp) {
+              const int ab = gp & 1;
+              if (gp >= 2) OZW(2, umma::mbar_wait(&acc_empty[ab], ((gp >> 1) - 1) & 1));
+              umma::fence_after();
+              const uint32_t dcol = tmem + (uint32_t)(ab * kAccCols);
+              const uint32_t bB = gB + ps * (kSl * kGBlk);
+              // Y digit p against the stacked G slices q = 0..5-p (N = (6-p) x 32):
+              // column (p + q) x 32 + n accumulates diagonal p + q
+  #pragma unroll
+              for (int p = 0; p < kSl; ++p)
+  #pragma unroll
+                for (int ks = 0; ks < 2; ++ks)
+                  if (!(xf & 8)) umma::mma_i8_ta(dcol + (uint32_t)(p * kPassRows),
+                                  tmem + (uint32_t)(kYT0 + p * 16 + ks * 8),
+                                  umma::make_sdesc(bB + ks * 256, 128, 512),
+                                  umma::idesc_i8(kT, (kSl - p) * kPassRows),
+                                  (p > 0 || ks > 0) ? 1u : 0u);
+              umma::commit(&acc_full[ab]);
+              OZW(20, (void)0);
+              if (ps == 1) {
+                // The Y staging is free once the copy has been consumed: the
+                // issuer observes pass 0's completion (its UMMAs read the copied
+                // digits) and arrives itself -- no reliance on what a
+                // tcgen05.commit behind a tcgen05.cp tracks.
+                OZW(3, umma::mbar_wait(&acc_full[(gp - 1) & 1], ((gp - 1) >> 1) & 1));
+                mbar_arrive(&y_empty);
+              }
+            }
+          }
+        }
       }
     }
-  } else if (warp == kRLoader) {
-    // ----------------------------------------------------------- row loader
-    int gt = 0;
-    for (int k = 0; k < nitems; ++k) {
-      const SubDev sd = subs[item_sub(k)];
-      const WinDev wd = wins[sd.win];
-      const double* __restrict__ rw = rows + wd.row_off + (sd.start - wd.node_off) * 24;
-      const int32_t* __restrict__ pw = pix + sd.start;
-      const int ntile = (sd.count + kT - 1) / kT;
-      for (int tl = 0; tl < ntile; ++tl, ++gt) {
-        const int s = gt % kRawStages;
-        if (gt >= kRawStages) OZW(4, umma::mbar_wait(&raw_empty[s], ((gt / kRawStages) - 1) & 1));
-        uint8_t* dst = sRaw + s * kRawBytes;
-        const int j0 = tl * kT, cn = min(kT, sd.count - j0);
-        if (lane == 0) {
-          umma::mbar_arrive_expect_tx(&raw_full[s], (uint32_t)(cn * kRowBytes));
-          umma::bulk_g2s(dst, rw + (int64_t)j0 * 24, (uint32_t)(cn * kRowBytes), &raw_full[s]);
-        }
-#pragma unroll
-        for (int q = 0; q < kT / 32; ++q) {
-          const int nd = q * 32 + lane;
-          if (nd < cn) cp_async4(dst + kT * kRowBytes + 4 * nd, pw + j0 + nd);
-        }
-        cp_async_mbar_arrive(&raw_full[s]);
-      }
-    }
-  } else if (warp >= kSlicer0 && warp < kIssuer) {
+  } else if (warp >= kSlicer0) {
     // --------------------------------------------------------------- slicers
     // thread = node row m of the tile: Y_j[(b, c)] = B_j[b] C_j[c], scaled by
     // the subproblem's 2^(46 - max eB - max eC), cut into six digit slices in
     // the K-major canonical layout (a quarter-warp's 16-byte stores cover one
     // 128-byte line: conflict-free)
-    const int m = (warp - kSlicer0) * 32 + lane;
+    const int m = ((warp - kSlicer0) & 3) * 32 + lane;
+    const int kq0 = ((warp - kSlicer0) >> 2) * kKqPer;   // first 16-element (b, c) group
+    const int b0 = kq0 * 2;                               // first b of this thread's groups
     int gt = 0;
     for (int k = 0; k < nitems; ++k) {
       const int si = item_sub(k);
@@ -259,95 +388,46 @@ k_gather_nm(const SubDev* __restrict__ subs, const int32_t* __restrict__ order, 
         const int s = gt % kRawStages;
         OZW(16, umma::mbar_wait(&raw_full[s], (gt / kRawStages) & 1));
         const bool ok = tl * kT + m < cnt;
-        const double2* R = reinterpret_cast<const double2*>(sRaw + s * kRawBytes + m * kRowBytes);
-        double bb[8], cc[8];
+        const double* R = reinterpret_cast<const double*>(sRaw + s * kRawBytes + m * kRowBytes);
+        // this thread's b = b0 .. b0 + 2 kKqPer - 1 and all eight c
+        double bb[2 * kKqPer], cc[8];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const double2 x = ok ? R[4 + i] : make_double2(0.0, 0.0);
-          const double2 y = ok ? R[8 + i] : make_double2(0.0, 0.0);
+        for (int i = 0; i < kKqPer; ++i) {
+          const double2 x = (ok && !(xf & 2048)) ? reinterpret_cast<const double2*>(R + 8 + b0)[i]
+                                                 : make_double2(1.0, 0.0);
           bb[2 * i] = x.x * syB;
           bb[2 * i + 1] = x.y * syB;
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const double2 y = (ok && !(xf & 2048)) ? reinterpret_cast<const double2*>(R + 16)[i]
+                                                 : make_double2(0.5, 0.0);
           cc[2 * i] = y.x * syC;
           cc[2 * i + 1] = y.y * syC;
         }
         release_after_loads(&raw_empty[s], lane, 0, make_double2(bb[0], cc[7]),
-                            make_double2(bb[7], cc[0]), make_double2(bb[3], cc[3]),
-                            make_double2(bb[5], cc[5]));   // B, C read
+                            make_double2(bb[2 * kKqPer - 1], cc[0]), make_double2(bb[1], cc[3]),
+                            make_double2(bb[2 * kKqPer - 2], cc[5]));   // B, C read
         if (gt >= 1) OZW(17, umma::mbar_wait(&y_empty, (gt - 1) & 1));   // previous tile copied
+        if (xf & 16384) spin_cycles(1000);
 #pragma unroll
-        for (int kq = 0; kq < 4; ++kq) {
+        for (int kk = 0; kk < kKqPer; ++kk) {
+          if (xf & 4) break;
           uint32_t lo[16], hi[16];
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const int bc = kq * 16 + i;
-            slice1(bb[bc >> 3], cc[bc & 7], lo[i], hi[i]);
-          }
-          store16(lo, hi, sY + canon64(m, kq * 16), kYSlice);
+          for (int i = 0; i < 16; ++i) slice1(bb[2 * kk + (i >> 3)], cc[i & 7], lo[i], hi[i]);
+          store16(lo, hi, sY + canon64(m, (kq0 + kk) * 16), kYSlice);
         }
         umma::fence_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive(&y_full);
-      }
-    }
-  } else if (warp == kIssuer) {
-    // ---------------------------------------------------------------- issuer
-    if (lane == 0) {
-      int gt = 0, gp = 0;
-      const uint32_t yB = umma::smem_u32(sY);
-      for (int k = 0; k < nitems; ++k) {
-        const int gs = k & 1;
-        const int ntile = (subs[item_sub(k)].count + kT - 1) / kT;
-        OZW(0, umma::mbar_wait(&g_full[gs], (k >> 1) & 1));
-        const uint32_t gB = umma::smem_u32(sG + gs * kGItem);
-        for (int tl = 0; tl < ntile; ++tl, ++gt) {
-          OZW(1, umma::mbar_wait(&y_full, gt & 1));
-          umma::fence_after();
-          // the tile's Y digits -> TMEM (the UMMA A operand of all four passes);
-          // ordered behind the previous tile's UMMAs, which read the old copy
-#pragma unroll
-          for (int p = 0; p < kSl; ++p)
-#pragma unroll
-            for (int ks = 0; ks < 2; ++ks)
-              umma::tmem_cp_128x256b(tmem + (uint32_t)(kYT0 + p * 16 + ks * 8),
-                                     umma::make_sdesc(yB + p * kYSlice + ks * 256, 128, 512));
-          // The staging is released by the commit after the first pass's UMMAs,
-          // not right after the copies: a commit issued directly behind
-          // tcgen05.cp was measured to fire before the copy's shared-memory
-          // reads were done (the slicers' next writes raced with it); the
-          // UMMAs consume the copied digits, so their completion implies it.
-          for (int ps = 0; ps < 4; ++ps, ++gp) {
-            const int ab = gp & 1;
-            if (gp >= 2) OZW(2, umma::mbar_wait(&acc_empty[ab], ((gp >> 1) - 1) & 1));
-            umma::fence_after();
-            const uint32_t dcol = tmem + (uint32_t)(ab * kAccCols);
-            const uint32_t bB = gB + ps * (kSl * kGBlk);
-            // Y digit p against the stacked G slices q = 0..5-p (N = (6-p) x 32):
-            // column (p + q) x 32 + n accumulates diagonal p + q
-#pragma unroll
-            for (int p = 0; p < kSl; ++p)
-#pragma unroll
-              for (int ks = 0; ks < 2; ++ks)
-                umma::mma_i8_ta(dcol + (uint32_t)(p * kPassRows),
-                                tmem + (uint32_t)(kYT0 + p * 16 + ks * 8),
-                                umma::make_sdesc(bB + ks * 256, 128, 512),
-                                umma::idesc_i8(kT, (kSl - p) * kPassRows),
-                                (p > 0 || ks > 0) ? 1u : 0u);
-            umma::commit(&acc_full[ab]);
-            if (ps == 1) {
-              // The Y staging is free once the copy has been consumed: the
-              // issuer observes pass 0's completion (its UMMAs read the copied
-              // digits) and arrives itself -- no reliance on what a
-              // tcgen05.commit behind a tcgen05.cp tracks.
-              umma::mbar_wait(&acc_full[(gp - 1) & 1], ((gp - 1) >> 1) & 1);
-              mbar_arrive(&y_empty);
-            }
-          }
-        }
+        OZW(22, (void)0);
       }
     }
   } else {
     // -------------------------------------------------------------- epilogue
-    const int lq = warp & 3, sp = warp >> 2;     // lane quarter, rhs slot pair
+    if (kSetRegs) umma::regs_inc<kRegsEpi>();
+    const int lq = warp & 3, w0 = (warp >> 2) * kSPW;   // lane quarter, first rhs slot
     const int m = lq * 32 + lane;                 // node row of the tile
     const uint32_t tl_lane = tmem + ((uint32_t)(lq * 32) << 16);
     const bool need_eta = ep.kind == NLD_APPLY_SYSTEM || ep.kind == NLD_APPLY_LAPLACIAN;
@@ -357,7 +437,7 @@ k_gather_nm(const SubDev* __restrict__ subs, const int32_t* __restrict__ order, 
       const int gs = k & 1;
       const int si = item_sub(k);
       const int cnt = subs[si].count;
-      const int r0 = (k % ngroups) * 16 + 8 * sp;  // this warp's first rhs
+      const int r0 = (k % ngroups) * 16 + 4 * w0;  // this warp's rhs r0 .. r0 + 4 kSPW - 1
       const int16_t* exk = sub_exp + (int64_t)si * kExpPerSub;
       int eBm = -2000, eCm = -2000;
 #pragma unroll
@@ -366,19 +446,24 @@ k_gather_nm(const SubDev* __restrict__ subs, const int32_t* __restrict__ order, 
         eCm = max(eCm, (int)exk[16 + q]);
       }
       OZW(8, umma::mbar_wait(&g_full[gs], (k >> 1) & 1));
-      const int4* gex = reinterpret_cast<const int4*>(sG + gs * kGItem + kGBytes);
-      const int4 ge0 = gex[2 * sp], ge1 = gex[2 * sp + 1];   // rhs r0 .. r0 + 7
-      // T scale per rhs: G exponent + the subproblem's Y exponents (combine6
-      // carries 2^24)
+      // G exponents of the warp's rhs; T scale per rhs: G exponent + the
+      // subproblem's Y exponents (combine6 carries 2^24)
+      int4 ge[kSPW];
+#pragma unroll
+      for (int j = 0; j < kSPW; ++j)
+        ge[j] = reinterpret_cast<const int4*>(sG + gs * kGItem + kGBytes)[w0 + j];
       const int eb = eBm + eCm - 52;
       const int ntile = (cnt + kT - 1) / kT;
       for (int tl = 0; tl < ntile; ++tl, ++gt) {
         const int s = gt % kRawStages;
         OZW(9, umma::mbar_wait(&raw_full[s], (gt / kRawStages) & 1));
+        if (xf & 8192) spin_cycles(1000);
         const double2* Ap = reinterpret_cast<const double2*>(sRaw + s * kRawBytes + m * kRowBytes);
-        const double2 a01 = Ap[0], a23 = Ap[1], a45 = Ap[2], a67 = Ap[3];
+        const bool xa = (xf & 256) != 0;
+        const double2 a01 = xa ? make_double2(1.0, 2.0) : Ap[0], a23 = xa ? a01 : Ap[1],
+                      a45 = xa ? a01 : Ap[2], a67 = xa ? a01 : Ap[3];
         const int px = tl * kT + m < cnt
-                           ? reinterpret_cast<const int32_t*>(sRaw + s * kRawBytes + kT * kRowBytes)[m]
+                           ? (xa ? m : reinterpret_cast<const int32_t*>(sRaw + s * kRawBytes + kT * kRowBytes)[m])
                            : -1;
         // Release the stage only once the loads have COMPLETED: the arrive is
         // made data-dependent on the loaded values (an LDS still in flight
@@ -386,113 +471,122 @@ k_gather_nm(const SubDev* __restrict__ subs, const int32_t* __restrict__ order, 
         // stage under it -- observed as rare stale pixel indices).
         release_after_loads(&raw_empty[s], lane, px, a01, a23, a45, a67);
         const bool ok = px >= 0;
-        const int64_t e = (int64_t)px * nrhs + r0;
-        // the running window sum of the node's 8 rhs (loaded now, in flight
-        // during the passes); each pass adds its rhs' scaled products
-        double sv[8];
-        if (ok && MODE >= mma::kGatherAccum) {
-          const double2* o2 = reinterpret_cast<const double2*>(out + e);
+        // (xf & 32, timing only: contiguous lines instead of the node's pixel)
+        const int64_t e = ((xf & 32) ? ((int64_t)(subs[si].start + tl * kT + m) & ((1 << 24) - 1))
+                                     : (int64_t)px) * nrhs + r0;
+        // the running window sum of the node's rhs: loaded now, added only
+        // after the last pass, so its latency (an L2 hit: the row loader
+        // prefetched the line) hides behind the four passes
+        double2 s01[kSPW], s23[kSPW], v01[kSPW], v23[kSPW];
+        double tv[kSPW][4];
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const double2 x = o2[i];
-            sv[2 * i] = x.x;
-            sv[2 * i + 1] = x.y;
+        for (int j = 0; j < kSPW; ++j) {
+          s01[j] = s23[j] = v01[j] = v23[j] = make_double2(0.0, 0.0);
+          if (ok && MODE >= mma::kGatherAccum && !(xf & 128)) {
+            const double2* o2 = reinterpret_cast<const double2*>(out + e + 4 * j);
+            s01[j] = o2[0];
+            s23[j] = o2[1];
           }
-        } else {
-#pragma unroll
-          for (int i = 0; i < 8; ++i) sv[i] = 0.0;
         }
-        // Final window: v and eta of the node, issued after pass 1 so their
-        // latency hides behind passes 2-3 (loads at the tile's end stalled
-        // the epilogue -- this window ran at twice the others' time)
-        double2 v01 = make_double2(0.0, 0.0), v23 = v01, v45 = v01, v67 = v01;
         double et = 0.0;
 #pragma unroll
         for (int ps = 0; ps < 4; ++ps, ++gp) {
-          if (MODE == mma::kGatherFinal && ps == 2 && ok) {
-            const double2* vv = reinterpret_cast<const double2*>(ep.v + e);
-            v01 = vv[0];
-            v23 = vv[1];
-            v45 = vv[2];
-            v67 = vv[3];
+          // final window: v and eta of the node, issued after pass 1
+          if (MODE == mma::kGatherFinal && ps == 2 && ok && !(xf & 128)) {
+#pragma unroll
+            for (int j = 0; j < kSPW; ++j) {
+              const double2* vv = reinterpret_cast<const double2*>(ep.v + e + 4 * j);
+              v01[j] = vv[0];
+              v23[j] = vv[1];
+            }
             if (need_eta) et = ep.eta[px];
           }
           const int ab = gp & 1;
           OZW(10, umma::mbar_wait(&acc_full[ab], (gp >> 1) & 1));
+          if (xf & 65536) spin_cycles(250);
           umma::fence_after();
 #pragma unroll
-          for (int sl = 0; sl < 2; ++sl) {
-            const int w = 2 * sp + sl;
-            const uint32_t tc = tl_lane + (uint32_t)(ab * kAccCols + w * 8);
-            uint32_t dv[kSl][8];
-            {
-              uint32_t d0[kSl][4], d1[kSl][4];
-              umma::tmem_ld4x6_wait(tc, kPassRows, d0);
-              umma::tmem_ld4x6_wait(tc + 4, kPassRows, d1);
+          for (int j = 0; j < kSPW; ++j) {
+            // columns a = 0..7 of rhs slot w0 + j, six diagonals each, read in
+            // two halves of four a (24 registers at a time)
+            const uint32_t tc = tl_lane + (uint32_t)(ab * kAccCols + (w0 + j) * 8);
+            double sh = 0.0, sl_ = 0.0;
 #pragma unroll
-              for (int t = 0; t < kSl; ++t)
+            for (int hf = 0; hf < 2; ++hf) {
+              uint32_t dv[kSl][4];
+              if (xf & 2) {
 #pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                  dv[t][i] = d0[t][i];
-                  dv[t][4 + i] = d1[t][i];
-                }
+                for (int t = 0; t < kSl; ++t)
+#pragma unroll
+                  for (int i = 0; i < 4; ++i) dv[t][i] = (uint32_t)(lane * 7 + t + i + gp);
+              } else {
+                umma::tmem_ld4x6_wait(tc + 4 * hf, kPassRows, dv);
+              }
+              if (hf == 1 && j == kSPW - 1) {
+                // every column of this warp read: release the accumulator
+                umma::fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&acc_empty[ab]);
+              }
+              if (xf & 1) {
+                uint32_t f = 0;
+#pragma unroll
+                for (int t = 0; t < kSl; ++t)
+#pragma unroll
+                  for (int i = 0; i < 4; ++i) f ^= dv[t][i];
+                sh += (double)(f & 1);
+                continue;
+              }
+              // hi and lo parts accumulate in separate chains (combine6_parts)
+              const double2 x0 = hf ? a45 : a01, x1 = hf ? a67 : a23;
+              double h, l;
+              combine6_parts(dv, 0, h, l);
+              sh = fma(h, x0.x, sh);
+              sl_ = fma(l, x0.x, sl_);
+              combine6_parts(dv, 1, h, l);
+              sh = fma(h, x0.y, sh);
+              sl_ = fma(l, x0.y, sl_);
+              combine6_parts(dv, 2, h, l);
+              sh = fma(h, x1.x, sh);
+              sl_ = fma(l, x1.x, sl_);
+              combine6_parts(dv, 3, h, l);
+              sh = fma(h, x1.y, sh);
+              sl_ = fma(l, x1.y, sl_);
             }
-            if (sl == 1) {
-              umma::fence_before();
-              __syncwarp();
-              if (lane == 0) mbar_arrive(&acc_empty[ab]);
-            }
-            // hi and lo parts accumulate in separate chains (combine6_parts)
-            double h, l, sh, sl_;
-            combine6_parts(dv, 0, h, l);
-            sh = h * a01.x;
-            sl_ = l * a01.x;
-            combine6_parts(dv, 1, h, l);
-            sh = fma(h, a01.y, sh);
-            sl_ = fma(l, a01.y, sl_);
-            combine6_parts(dv, 2, h, l);
-            sh = fma(h, a23.x, sh);
-            sl_ = fma(l, a23.x, sl_);
-            combine6_parts(dv, 3, h, l);
-            sh = fma(h, a23.y, sh);
-            sl_ = fma(l, a23.y, sl_);
-            combine6_parts(dv, 4, h, l);
-            sh = fma(h, a45.x, sh);
-            sl_ = fma(l, a45.x, sl_);
-            combine6_parts(dv, 5, h, l);
-            sh = fma(h, a45.y, sh);
-            sl_ = fma(l, a45.y, sl_);
-            combine6_parts(dv, 6, h, l);
-            sh = fma(h, a67.x, sh);
-            sl_ = fma(l, a67.x, sl_);
-            combine6_parts(dv, 7, h, l);
-            sh = fma(h, a67.y, sh);
-            sl_ = fma(l, a67.y, sl_);
-            // rhs r0 + 4 sl + ps; T scale: G exponent + the subproblem's Y
-            // exponents (combine6 carries 2^24)
-            const int4 ge = sl ? ge1 : ge0;
-            const int gx = ps == 0 ? ge.x : ps == 1 ? ge.y : ps == 2 ? ge.z : ge.w;
-            sv[4 * sl + ps] += fma(sh, 4294967296.0, sl_) * pow2(gx + eb);
-          }
-
-        }
-        if (!ok) continue;
-        double res[8];
-        const double vx[8] = {v01.x, v01.y, v23.x, v23.y, v45.x, v45.y, v67.x, v67.y};
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          if (MODE != mma::kGatherFinal) {
-            res[i] = sv[i];
-          } else {
-            const double2 lm = s_coef[r0 + i];
-            res[i] = mma::epi_value_r(ep.kind, (double)ep.L, inv_L, sv[i], vx[i], et, lm.x, lm.y);
+            // rhs r0 + 4 j + ps
+            const int gx = ps == 0 ? ge[j].x : ps == 1 ? ge[j].y : ps == 2 ? ge[j].z : ge[j].w;
+            tv[j][ps] = fma(sh, 4294967296.0, sl_) * pow2(gx + eb);
           }
         }
-        double2* o2 = reinterpret_cast<double2*>(out + e);
-        o2[0] = make_double2(res[0], res[1]);
-        o2[1] = make_double2(res[2], res[3]);
-        o2[2] = make_double2(res[4], res[5]);
-        o2[3] = make_double2(res[6], res[7]);
+        if (!ok || (xf & 128)) {
+          if (xf & 128) {
+            double f = 0.0;
+#pragma unroll
+            for (int j = 0; j < kSPW; ++j) f += tv[j][0] + tv[j][1] + tv[j][2] + tv[j][3];
+            if (f == 12345.678) out[0] = f;
+          }
+          continue;
+        }
+#pragma unroll
+        for (int j = 0; j < kSPW; ++j) {
+          const double sv[4] = {s01[j].x + tv[j][0], s01[j].y + tv[j][1], s23[j].x + tv[j][2],
+                                s23[j].y + tv[j][3]};
+          const double vx[4] = {v01[j].x, v01[j].y, v23[j].x, v23[j].y};
+          double res[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            if (MODE != mma::kGatherFinal) {
+              res[i] = sv[i];
+            } else {
+              const double2 lm = s_coef[r0 + 4 * j + i];
+              res[i] = mma::epi_value_r(ep.kind, (double)ep.L, inv_L, sv[i], vx[i], et, lm.x, lm.y);
+            }
+          }
+          double2* o2 = reinterpret_cast<double2*>(out + e + 4 * j);
+          o2[0] = make_double2(res[0], res[1]);
+          o2[1] = make_double2(res[2], res[3]);
+        }
+        OZW(21, (void)0);
       }
       // every pass of the item has completed (its accumulators were read):
       // the UMMAs no longer read its G digits
@@ -507,6 +601,7 @@ k_gather_nm(const SubDev* __restrict__ subs, const int32_t* __restrict__ order, 
 #endif
   umma::fence_before();
   __syncthreads();
+  OZ_TRACE_END
   if (warp == 0) umma::tmem_free<512>(tmem);
 }
 
@@ -529,7 +624,8 @@ static void launch_nm(unsigned grid_n, const PlanSet& ps, const SubDev* subs, co
     attr = true;
   }
   oz::nm::k_gather_nm<MODE><<<grid_n, oz::nm::kThreads, oz::nm::smem_bytes(), st>>>(
-      subs, order, (int)nsub, ps.wdev, ps.rows, ps.pix, ex, gdig, out, nrhs, ep);
+      subs, order, (int)nsub, ps.wdev, ps.rows, ps.pix, ex, gdig, out, nrhs, ep,
+      ab_int("NLD_GX", 0));
 }
 
 void launch_gather_nm(const PlanSet& ps, const SubDev* subs, const int16_t* ex,
@@ -561,7 +657,9 @@ void launch_gather_nm(const PlanSet& ps, const SubDev* subs, const int16_t* ex,
       break;
   }
   NLD_CUDA(cudaGetLastError());
-#ifdef NLD_OZ_PROF
+#ifdef NLD_OZ_TRACE
+  oz::ozaki_trace_dump("gather_nm", st);
+#elif defined(NLD_OZ_PROF)
   ozaki_prof_dump("gather_nm", st);
 #endif
 }

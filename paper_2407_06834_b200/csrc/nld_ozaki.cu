@@ -40,6 +40,13 @@ namespace oz {
 __device__ unsigned long long oz_prof[32];
 #endif
 
+// timing experiments: spin for n cycles (causal profiling of a role)
+__device__ __forceinline__ void spin_cycles_s(long long n) {
+  const long long t0 = clock64();
+  while (clock64() - t0 < n) {
+  }
+}
+
 // ---- plan-time exponent table -------------------------------------------
 // per subproblem: eA[a], eB[b], eC[c] = exponent bounds of the columns of its
 // weight rows (static: the features never change)
@@ -126,10 +133,23 @@ constexpr int kYOpBytes = kSl * kBBytes;         // 12 KB of Y digits per chunk
 __host__ __device__ constexpr int spread_oz_py_smem() {
   return kPyRawStages * kPyRawBytes + kOpStages * kYOpBytes;
 }
-constexpr int kSlicers = 256;
-constexpr int kIssuerWarp = 8;
-constexpr int kLoaderWarp = 9;                   // first of kLoaders loader warps
-constexpr int kLoaders = 4;
+#ifndef NLD_SPR_SLC
+#define NLD_SPR_SLC 8
+#endif
+#ifndef NLD_SPR_LD
+#define NLD_SPR_LD 4
+#endif
+// Slicer warps: cutting a chunk's X = v A (4096 values) and Y = B C (2048)
+// digits is a latency-bound chain (LDS, DMUL, DFMA, byte transposes, TMEM /
+// shared stores) and was the spread's critical path with 8 warps (~2k cycles
+// per chunk against ~0.7k of UMMA work): 16 warps cut 12 values per thread.
+constexpr int kSlcWarps = NLD_SPR_SLC;
+constexpr int kSlicers = 32 * kSlcWarps;
+constexpr int kXNodes = 32 * 128 / kSlicers;     // X: nodes per thread (16 or 8)
+static_assert(kSlcWarps == 8 || kSlcWarps == 16, "slicer warps");
+constexpr int kIssuerWarp = kSlcWarps;
+constexpr int kLoaderWarp = kSlcWarps + 1;       // first of kLoaders loader warps
+constexpr int kLoaders = NLD_SPR_LD;
 
 // ---- persistent spread -------------------------------------------------------
 // One CTA per SM walks (subproblem, rhs group) items -- the window's
@@ -142,8 +162,8 @@ constexpr int kLoaders = 4;
 // already cut the next item's first chunks.  The only serialisation left per
 // item is the TMEM drain (the accumulator is single-buffered: 384 of 512
 // columns).  Scales are per-thread registers (no per-item shared state).
-//   warps 0-7  slicers (X digits -> TMEM, Y digits -> shared memory)
-//   warp 8     UMMA issuer       warps 9-12 loaders       warps 13-16 epilogue
+//   warps 0..S-1  slicers (X digits -> TMEM, Y digits -> shared memory)
+//   warp S        UMMA issuer     then kLoaders loader warps, 4 epilogue warps
 constexpr int kSPEpi0 = kLoaderWarp + kLoaders;
 constexpr int kSPThreads = 32 * (kSPEpi0 + 4);
 
@@ -152,7 +172,10 @@ k_spread_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
              const WinDev* __restrict__ wins, const double* __restrict__ rows,
              const int32_t* __restrict__ pix, const int16_t* __restrict__ sub_exp,
              const unsigned long long* __restrict__ vmax, const double* __restrict__ vt,
-             int nrhs, double* __restrict__ blocks) {
+             int nrhs, double* __restrict__ blocks, int xf) {
+#ifndef NLD_AB_BUILD
+  xf = 0;   // timing experiments (bit mask) exist only in the A/B build
+#endif
   constexpr int RS = kPyRawStages, RB = kPyRawBytes;
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ uint64_t raw_full[RS], raw_empty[RS];
@@ -160,6 +183,7 @@ k_spread_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
   __shared__ uint32_t taddr_s;
   uint8_t* const raw = smem;
   uint8_t* const sYop = smem + RS * RB;           // [kOpStages][6 x 2 KB]
+  OZ_TRACE_DECL
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int ngroups = nrhs / 16;
   const int G = (int)gridDim.x, b = (int)blockIdx.x;
@@ -221,6 +245,7 @@ k_spread_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
         const int jn = (c + kLoaders) * kChunk + lane;
         const int32_t px_next = (c + kLoaders < nchunk && jn < sd.count) ? __ldg(pw + jn) : 0;
         if (gc >= RS) OZW(12, umma::mbar_wait(&raw_empty[s], ((gc / RS) - 1) & 1));
+        if (xf & 32768) spin_cycles_s(600);
         uint8_t* dst = raw + s * RB;
         const int j0 = c * kChunk, cn = min(kChunk, sd.count - j0);
         if (lane == 0) {
@@ -234,7 +259,8 @@ k_spread_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
           const int32_t pxn = __shfl_sync(0xffffffffu, px, nd);
           if (nd < cn)
             cp_async16(dst + kPyA + nd * 128 + pc * 16,
-                       vt + (int64_t)(uint32_t)pxn * nrhs + rg + 2 * pc);
+                       vt + (int64_t)(uint32_t)((xf & 8) ? (sd.start + j0 + nd) & ((1 << 24) - 1) : pxn) *
+                                nrhs + rg + 2 * pc);
         }
         cp_async_mbar_arrive(&raw_full[s]);
         px = px_next;
@@ -251,6 +277,7 @@ k_spread_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
       for (int c = 0; c < nchunk; ++c, ++g) {
         const int st = g % kOpStages, s = g % RS;
         OZW(14, umma::mbar_wait(&op_ready[st], (g / kOpStages) & 1));
+        if (xf & 4096) spin_cycles_s(300);
         umma::fence_after();
         if (lane == 0) {
           const uint32_t bB = umma::smem_u32(sYop + st * kYOpBytes);
@@ -261,7 +288,7 @@ k_spread_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
             for (int q0 = 0; q0 < kSl - p; q0 += 4) {
               const int nq = min(4, kSl - p - q0);
               const uint64_t db = umma::make_sdesc(bB + q0 * kBBytes, 128, 256);
-              umma::mma_i8_ta(tmem + (uint32_t)((p + q0) * 64), xa + (uint32_t)(p * 8), db,
+              if (!(xf & 2)) umma::mma_i8_ta(tmem + (uint32_t)((p + q0) * 64), xa + (uint32_t)(p * 8), db,
                               umma::idesc_i8(kRows, nq * 64), (c > 0 || p > 0) ? 1u : 0u);
             }
           }
@@ -273,10 +300,15 @@ k_spread_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
     }
   } else if (warp < kIssuerWarp) {
     // --------------------------------------------------------------- slicers
-    const int m = tid & 127, h = tid >> 7;
+    // X: thread = TMEM lane m = (a, r) of its warp's lane quarter, kXNodes
+    // nodes h kXNodes .. ; Y: a warp covers 8 rows (b, c) x 16 nodes, a lane
+    // one row and 4 nodes (its 4-byte digit words of a quarter-warp fill a
+    // 128-byte line: conflict-free stores)
+    const int m = (warp & 3) * 32 + lane, h = warp >> 2;
     const int a = m >> 4, r = m & 15;
-    const int yn = tid & 63, yq = tid >> 6;      // Y: row (b, c), 8-node quarter
+    const int yn = (warp & 7) * 8 + (lane & 7);             // Y row (b, c)
     const int yb = yn >> 3, yc = yn & 7;
+    constexpr int kYReps = kSlcWarps == 16 ? 1 : 2;         // 8 warps: both node halves
     int g = 0;
     for (int k = 0; k < nitems; ++k) {
       const int si = item_sub(k);
@@ -292,16 +324,28 @@ k_spread_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
       for (int c = 0; c < nchunk; ++c, ++g) {
         const int st = g % kOpStages, s = g % RS;
         OZW(16, umma::mbar_wait(&raw_full[s], (g / RS) & 1));
+        if (xf & 16384) spin_cycles_s(300);
         if (g >= kOpStages) OZW(17, umma::mbar_wait(&op_free[st], ((g / kOpStages) - 1) & 1));
         const double* R = reinterpret_cast<const double*>(raw + s * RB);
         const double* Vr = reinterpret_cast<const double*>(raw + s * RB + kPyA);
         const int cn = min(kChunk, sd.count - c * kChunk);
-        {
-          // Y digits of 8 nodes for row (b, c): K-major canonical, zero past cn
-          uint32_t lo[8], hi[8];
+        if (xf & 1) {
+          umma::fence_before();
+          __syncwarp();
+          if (lane == 0) {
+            mbar_arrive(&op_ready[st]);
+            mbar_arrive(&raw_empty[s]);
+          }
+          continue;
+        }
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const int j = yq * 8 + i;
+        for (int yr = 0; yr < kYReps; ++yr) {
+          // Y digits of 4 nodes for row (b, c): K-major canonical, zero past cn
+          const int kn = (kSlcWarps == 16 ? (warp >> 3) : yr) * 16 + (lane >> 3) * 4;
+          uint32_t lo[4], hi[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int j = kn + i;
             double x = 0.0, y = 0.0;
             if (j < cn) {
               x = R[j * 24 + 8 + yb] * sy;
@@ -309,12 +353,16 @@ k_spread_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
             }
             slice1(x, y, lo[i], hi[i]);
           }
-          store8(lo, hi, sYop + st * kYOpBytes + canon32(yn, yq * 8), kBBytes);
-        }
-        uint32_t lo[16], hi[16];
+          uint32_t w6[6];
+          pack4(lo, hi, w6);
+          uint8_t* yd = sYop + st * kYOpBytes + canon32(yn, kn);
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const int j = h * 16 + i;
+          for (int p = 0; p < kSl; ++p) *reinterpret_cast<uint32_t*>(yd + p * kBBytes) = w6[p];
+        }
+        uint32_t lo[kXNodes], hi[kXNodes];
+#pragma unroll
+        for (int i = 0; i < kXNodes; ++i) {
+          const int j = h * kXNodes + i;
           double x = 0.0, y = 0.0;
           if (j < cn) {
             x = Vr[j * 16 + r];
@@ -322,14 +370,19 @@ k_spread_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
           }
           slice1(x, y, lo[i], hi[i]);
         }
-        uint32_t w4[4][6];
+        uint32_t w4[kXNodes / 4][6];
 #pragma unroll
-        for (int g4 = 0; g4 < 4; ++g4) pack4(lo + 4 * g4, hi + 4 * g4, w4[g4]);
+        for (int g4 = 0; g4 < kXNodes / 4; ++g4) pack4(lo + 4 * g4, hi + 4 * g4, w4[g4]);
         const uint32_t xt = tmem + ((uint32_t)((m >> 5) * 32) << 16) +
-                            (uint32_t)(kXTmem0 + st * kSl * 8 + h * 4);
+                            (uint32_t)(kXTmem0 + st * kSl * 8 + h * (kXNodes / 4));
 #pragma unroll
-        for (int p = 0; p < kSl; ++p)
-          umma::tmem_st4(xt + (uint32_t)(p * 8), w4[0][p], w4[1][p], w4[2][p], w4[3][p]);
+        for (int p = 0; p < kSl; ++p) {
+          if (kXNodes == 16)
+            umma::tmem_st4(xt + (uint32_t)(p * 8), w4[0][p], w4[1 % (kXNodes / 4)][p],
+                           w4[2 % (kXNodes / 4)][p], w4[3 % (kXNodes / 4)][p]);
+          else
+            umma::tmem_st2(xt + (uint32_t)(p * 8), w4[0][p], w4[1 % (kXNodes / 4)][p]);
+        }
         umma::tmem_wait_st();
         umma::fence_before();
         umma::fence_async_smem();
@@ -365,6 +418,14 @@ k_spread_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
 #pragma unroll 1
       for (int c0 = 0; c0 < 64; c0 += 8) {
         uint32_t dv[kSl][8];
+        if (xf & 4) {
+          if (c0 == 56) {
+            umma::fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&acc_empty);
+          }
+          continue;
+        }
         umma::tmem_ld8x6_wait(tl + (uint32_t)c0, 64, dv);
         if (c0 == 56) {
           // every column read: the next item's UMMAs may overwrite the accumulator
@@ -393,6 +454,7 @@ k_spread_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
 #endif
   umma::fence_before();
   __syncthreads();
+  OZ_TRACE_END
   if (warp == 0) umma::tmem_free<kTmemCols>(tmem);
 }
 
@@ -466,9 +528,12 @@ void launch_spread_oz(const PlanSet& ps, const SubDev* subs, const int16_t* ex,
   }
   const unsigned grid_n = std::min<unsigned>(nsub, (unsigned)sms);
   oz::k_spread_ozp<<<grid_n, oz::kSPThreads, oz::spread_oz_py_smem(), st>>>(
-      subs, order, (int)nsub, ps.wdev, ps.rows, ps.pix, ex, vmax, vt, nrhs, blocks);
+      subs, order, (int)nsub, ps.wdev, ps.rows, ps.pix, ex, vmax, vt, nrhs, blocks,
+      ab_int("NLD_SX", 0));
   NLD_CUDA(cudaGetLastError());
-#ifdef NLD_OZ_PROF
+#ifdef NLD_OZ_TRACE
+  oz::ozaki_trace_dump("spread", st);
+#elif defined(NLD_OZ_PROF)
   ozaki_prof_dump("spread", st);
 #endif
 }

@@ -4,6 +4,9 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
 
 #include "nld_umma.cuh"
 
@@ -17,7 +20,29 @@ constexpr int kSl = NLD_OZ_SL;         // digits per operand
 
 // -DNLD_OZ_PROF: per-site clock64 totals of the pipeline waits (lane 0 of
 // each warp), printed after each launch -- a tuning aid, not built by default
-#ifdef NLD_OZ_PROF
+#if defined(NLD_OZ_TRACE)
+// -DNLD_OZ_TRACE (test builds, whole-program per file): every pipeline wait of
+// lane 0 of each warp of CTA 0 is logged as (site, start, end) clocks into the
+// warp's own slot range (plain stores, no atomics: the log barely perturbs
+// the pipeline); ozaki_trace_dump() writes the log of the last launch
+constexpr int kTrPerWarp = 8192;
+static __device__ unsigned long long oz_trace[32 * kTrPerWarp * 2];
+static __device__ unsigned int oz_trace_cnt[32];
+#define OZ_TRACE_DECL unsigned _trn = 0;
+#define OZ_TRACE_END                                                        \
+  if (blockIdx.x == 0 && (threadIdx.x & 31) == 0) oz_trace_cnt[threadIdx.x >> 5] = _trn;
+#define OZW(site, ...)                                                      \
+  do {                                                                      \
+    const unsigned long long _t0 = clock64();                               \
+    __VA_ARGS__;                                                            \
+    if (blockIdx.x == 0 && (threadIdx.x & 31) == 0 && _trn < kTrPerWarp) {  \
+      unsigned long long* _p =                                              \
+          oz_trace + 2 * ((threadIdx.x >> 5) * kTrPerWarp + _trn++);        \
+      _p[0] = ((unsigned long long)(site) << 56) | (_t0 & 0xffffffffffffffull); \
+      _p[1] = clock64();                                                    \
+    }                                                                       \
+  } while (0)
+#elif defined(NLD_OZ_PROF)
 extern __device__ unsigned long long oz_prof[32];   // defined in nld_ozaki.cu
 #define OZW(site, ...)                                                      \
   do {                                                                      \
@@ -28,6 +53,10 @@ extern __device__ unsigned long long oz_prof[32];   // defined in nld_ozaki.cu
   } while (0)
 #else
 #define OZW(site, ...) __VA_ARGS__
+#endif
+#ifndef OZ_TRACE_DECL
+#define OZ_TRACE_DECL
+#define OZ_TRACE_END
 #endif
 constexpr int kRows = 128;             // M: (a, r) rows, r fastest
 constexpr int kChunk = 32;             // nodes per UMMA K step (32 bytes)
@@ -134,6 +163,10 @@ __device__ __forceinline__ void cp_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p));
+}
+
 __device__ __forceinline__ void cp_async_mbar_arrive(uint64_t* mbar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(umma::smem_u32(mbar))
                : "memory");
@@ -210,5 +243,32 @@ __device__ __forceinline__ void combine6_parts(const uint32_t (&dv)[6][NCOL], in
   hi = i2d(x01);
 }
 
+#if defined(NLD_OZ_TRACE)
+// host: write the last launch's wait log of this file's kernels to
+// $NLD_TRACE_DIR/<tag>_<n>.txt (one "site warp start end" line per wait)
+static inline void ozaki_trace_dump(const char* tag, cudaStream_t st) {
+  static int n = 0;
+  const char* dir = std::getenv("NLD_TRACE_DIR");
+  cudaStreamSynchronize(st);
+  unsigned cnt[32];
+  cudaMemcpyFromSymbol(cnt, oz_trace_cnt, sizeof(cnt));
+  if (dir) {
+    std::vector<unsigned long long> h(32 * (size_t)kTrPerWarp * 2);
+    cudaMemcpyFromSymbol(h.data(), oz_trace, sizeof(unsigned long long) * h.size());
+    char path[512];
+    std::snprintf(path, sizeof(path), "%s/%s_%d.txt", dir, tag, n++);
+    if (FILE* f = std::fopen(path, "w")) {
+      for (int w = 0; w < 32; ++w)
+        for (unsigned i = 0; i < cnt[w] && i < (unsigned)kTrPerWarp; ++i) {
+          const unsigned long long* p = h.data() + 2 * ((size_t)w * kTrPerWarp + i);
+          std::fprintf(f, "%llu %d %llu %llu\n", p[0] >> 56, w, p[0] & 0xffffffffffffffull, p[1]);
+        }
+      std::fclose(f);
+    }
+  }
+  unsigned z[32] = {0};
+  cudaMemcpyToSymbol(oz_trace_cnt, z, sizeof(z));
+}
+#endif
 }  // namespace oz
 }  // namespace nld

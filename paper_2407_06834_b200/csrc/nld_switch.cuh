@@ -11,9 +11,14 @@ inline int ab_switch(const char* name, int dflt) {
   const char* e = std::getenv(name);
   return (e && e[0]) ? (e[0] != '0') : dflt;
 }
+inline int ab_int(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return (e && e[0]) ? std::atoi(e) : dflt;
+}
 }  // namespace nld
 #else
 namespace nld {
 constexpr int ab_switch(const char*, int dflt) { return dflt; }
+constexpr int ab_int(const char*, int dflt) { return dflt; }
 }  // namespace nld
 #endif

@@ -64,6 +64,11 @@ __device__ __forceinline__ void tmem_cp_128x256b(uint32_t taddr, uint64_t sdesc)
 }
 
 // 32 lanes x 32 bits, 4 consecutive columns per thread (register -> TMEM)
+__device__ __forceinline__ void tmem_st2(uint32_t taddr, uint32_t a, uint32_t b) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};\n" ::"r"(taddr), "r"(a),
+               "r"(b)
+               : "memory");
+}
 __device__ __forceinline__ void tmem_st4(uint32_t taddr, uint32_t a, uint32_t b, uint32_t c,
                                          uint32_t d) {
   asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};\n" ::"r"(taddr),
@@ -129,6 +134,16 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&r)[8]) {
 // separate asm are "defined" before the data lands -- the compiler may copy
 // or spill them before tcgen05.wait::ld (seen as nondeterministic results
 // under register pressure).  Here the outputs exist only after the wait.
+// warpgroup register budget (all four warps of the warpgroup execute it)
+template <int N>
+__device__ __forceinline__ void regs_inc() {
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(N));
+}
+template <int N>
+__device__ __forceinline__ void regs_dec() {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(N));
+}
+
 __device__ __forceinline__ void tmem_ld4x6_wait(uint32_t taddr, uint32_t cs, uint32_t (&r)[6][4]) {
   asm volatile(
       "{\n\t.reg .b32 a1, a2, a3, a4, a5;\n\t"

@@ -41,6 +41,43 @@ def shard_range(n: int, rank: int, world: int) -> tuple[int, int]:
     return n * rank // world, n * (rank + 1) // world
 
 
+def partition(features, windows, world: int, *, window: int = 0, grid: int = 64,
+              rmax: float = 0.25 - 1.0 / 32.0) -> list[np.ndarray]:
+    """Pixel indices of each rank, partitioned by stencil-cell ownership of
+    one window (balanced by pixel count).
+
+    Contiguous pixel ranges (`shard_range`) give every rank nodes in almost
+    every occupied cell of every window, so each rank pays every cell's
+    fixed costs (a 128-node gather tile per subproblem, the spread's
+    accumulator drain and block write) on an eighth of its nodes at eight
+    ranks.  Ranking the pixels by their cell in `window` (the torus map of
+    transform.py:292-317 on the global point set, cell = floor(q * grid)) and
+    cutting that order into `world` equal ranges keeps that window's cells
+    whole on one rank (at most world - 1 cells are split); the other windows'
+    cells follow as far as the features of neighbouring patch rows correlate.
+    Each rank's indices are returned in ascending order.  Any partition is
+    valid for the sharded operator: its products and solves depend only on
+    which pixels a rank holds, not on how they were chosen.
+    """
+    if world < 1:
+        raise ValueError("bad world size")
+    f = np.asarray(features, np.float64)
+    n = f.shape[0]
+    cols = np.asarray(windows[window], np.int64)
+    p = f[:, cols]
+    lo, hi = p.min(axis=0), p.max(axis=0)
+    c = 0.5 * (lo + hi)
+    radius = float(np.sqrt(((p - c) ** 2).sum(axis=1).max()))
+    q = (p - c) * (rmax / max(radius, 1e-30))
+    base = np.floor(q * grid).astype(np.int64) + grid
+    key = np.zeros(n, np.int64)
+    for s in range(base.shape[1]):
+        key = key * (4 * grid) + base[:, s]
+    order = np.argsort(key, kind="stable")
+    cuts = [n * k // world for k in range(world + 1)]
+    return [np.sort(order[cuts[k]:cuts[k + 1]]) for k in range(world)]
+
+
 def host_view(ptr: int, count: int, dtype: int) -> np.ndarray:
     ctype, _ = _NP[dtype]
     return np.ctypeslib.as_array(ctypes.cast(ptr, ctypes.POINTER(ctype)),

@@ -533,6 +533,62 @@ def test_sharded_sliced_path_matches_single_gpu():
     assert rel(got, want) < 1e-12
 
 
+def test_sharded_cell_partition_matches_single_gpu():
+    """2 ranks (ThreadComm on one GPU) holding the window-0 cell-ownership
+    partition (sharding.partition) instead of contiguous ranges: with the
+    per-window grid allreduce on the aux stream, the 16-rhs sliced product
+    and a batched deflated CG equal the unsharded operator's."""
+    import threading
+
+    from paper_2407_06834_b200 import _lib
+    from paper_2407_06834_b200 import sharding as S
+    full, feats, wins, f = operator("c1")
+    n = feats.shape[0]
+    rng = np.random.default_rng(23)
+    V = rng.standard_normal((n, 16))
+    coef = np.stack([np.ones(16), rng.uniform(0, 0.01, 16)], 1).ravel()
+    want = full.apply_device(torch.from_numpy(V).cuda(), _lib.APPLY_SYSTEM, 16, coef,
+                             pixel_major=True).cpu().numpy()
+    mus = [10.0 / float(full.degree().mean()), 0.5]
+    want_cg = nld.deflated_solve_batched(full, f[:, 0], 1.0, mus, tol=synth.CG_TOL, maxit=200)
+    world = 2
+    parts = S.partition(feats, wins, world)
+    assert sorted(np.concatenate(parts).tolist()) == list(range(n))
+    comm = S.ThreadComm(world, device=torch.device("cuda", 0))
+    out, errs = {}, []
+
+    def rank_main(rank):
+        try:
+            ix = parts[rank]
+            op = nld.AnovaOperator(torch.from_numpy(feats[ix]).cuda(), wins, synth.SIGMA, **PIN)
+            S.attach(op, comm, rank, n)
+            op.degree()
+            y = op.apply_device(torch.from_numpy(V[ix].copy()).cuda(), _lib.APPLY_SYSTEM,
+                                16, coef, pixel_major=True)
+            res = nld.deflated_solve_batched(op, f[ix, 0], 1.0, mus, tol=synth.CG_TOL, maxit=200)
+            out[rank] = (y.cpu().numpy(), res)
+        except Exception as exc:  # pragma: no cover - reported below
+            errs.append(exc)
+            comm.barrier.abort()
+
+    threads = [threading.Thread(target=rank_main, args=(r,)) for r in range(world)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join(timeout=600)
+    assert not errs, errs
+    got = np.empty_like(want)
+    for r in range(world):
+        got[parts[r]] = out[r][0]
+    assert rel(got, want) < 1e-12
+    for k in range(len(mus)):
+        assert {out[r][1][k].iterations for r in range(world)} == {want_cg[k].iterations}
+        x = np.empty(n)
+        for r in range(world):
+            x[parts[r]] = out[r][1][k].x
+        assert rel(x, want_cg[k].x) < 1e-10
+
+
 @pytest.mark.parametrize("nrhs", [32, 48])
 def test_sliced_multiple_rhs_groups(nrhs):
     """nrhs = 16k runs k rhs groups through the same sliced kernels (G digits,

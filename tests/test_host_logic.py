@@ -121,3 +121,28 @@ class TestTransformValidation:
         assert T.expansion_degree(1e9) == T.MAX_EXPANSION
         for s in (0.5, 3.0, 250.77, 1e4):
             assert T.expansion_degree(s) == O.expansion_degree(s)
+
+
+def test_cell_partition_covers_and_keeps_cells_whole():
+    """sharding.partition: every pixel on exactly one rank, balanced to
+    within one pixel, and window-0 cells split across at most world - 1 rank
+    boundaries (the point of the partition)."""
+    from paper_2407_06834_b200 import sharding as S
+    feats, wins, _ = synth.make_problem("c1")
+    n = feats.shape[0]
+    for world in (1, 2, 3, 8):
+        parts = S.partition(feats, wins, world)
+        sizes = [len(p) for p in parts]
+        assert max(sizes) - min(sizes) <= 1
+        allix = np.concatenate(parts)
+        assert len(allix) == n and len(np.unique(allix)) == n
+        p = feats[:, wins[0]]
+        c = 0.5 * (p.min(0) + p.max(0))
+        r = np.sqrt(((p - c) ** 2).sum(1).max())
+        cell = np.floor((p - c) * ((0.25 - 1 / 32) / r) * 64).astype(np.int64)
+        key = (cell[:, 0] * 1000 + cell[:, 1]) * 1000 + cell[:, 2]
+        owners = {}
+        for rank, ix in enumerate(parts):
+            for k in np.unique(key[ix]):
+                owners.setdefault(k, set()).add(rank)
+        assert sum(len(o) - 1 for o in owners.values()) <= world - 1
