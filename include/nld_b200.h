@@ -158,6 +158,12 @@ NLD_API int nld_op_window_info(const nld_operator* op, int32_t window,
                        nld_window_info* out);
 NLD_API int nld_op_stats(const nld_operator* op, nld_stats* out);
 NLD_API int nld_op_set_timing(nld_operator* op, int32_t enabled);
+/* Test hook (no reference counterpart): fill every allocated workspace
+ * buffer of the operator (blocks, grids, convolution scratch, per-window
+ * gathers, G digits, assemble scratch, CG vectors) with 0xFF bytes -- NaN as
+ * doubles -- so a later product that read workspace it did not write first
+ * would return NaN or garbage (an initcheck that needs no sanitizer). */
+NLD_API int nld_op_debug_poison(nld_operator* op);
 
 /* deflated_solve / plain_solve (linops.py:263-319) on nrhs systems
  * A_r = lam_r I + mu_r (diag eta - Gamma) sharing every Gamma application.

@@ -84,6 +84,7 @@ SIGNATURES = {
     "nld_op_window_info": (ctypes.c_int, [_P, _I32, ctypes.POINTER(WindowInfo)]),
     "nld_op_stats": (ctypes.c_int, [_P, ctypes.POINTER(Stats)]),
     "nld_op_set_timing": (ctypes.c_int, [_P, _I32]),
+    "nld_op_debug_poison": (ctypes.c_int, [_P]),
     "nld_cg_solve": (ctypes.c_int, [_P, _P, _P, _I32, _I64, _PD, _PD, _I32, _I32,
                                     _D, _I32, _I32, _PI32, _PD, _PI32, _PD, _I32,
                                     _P]),

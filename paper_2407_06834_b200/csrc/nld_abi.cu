@@ -229,6 +229,32 @@ int nld_op_set_timing(nld_operator* op, int32_t enabled) {
   });
 }
 
+int nld_op_debug_poison(nld_operator* op) {
+  return guarded([&] {
+    if (!op) throw Error(NLD_ERR_VALUE, "null operator");
+    NLD_CUDA(cudaSetDevice(op->device));
+    NLD_CUDA(cudaDeviceSynchronize());
+    nld::Workspace& ws = op->ws;
+    const int64_t cap = std::max(ws.nrhs_cap, 1);
+    const int64_t gt = std::max<int64_t>(1, ws.grid_total) * cap;
+    auto fill = [](void* p, size_t bytes) {
+      if (p && bytes) NLD_CUDA(cudaMemset(p, 0xFF, bytes));
+    };
+    fill(ws.blocks, sizeof(double) * std::max<int64_t>(1, ws.blocks_total) * cap);
+    fill(ws.grid_in, sizeof(double) * (gt + cap));
+    fill(ws.grid_out, sizeof(double) * gt);
+    fill(ws.cbuf0, sizeof(double2) * gt);
+    fill(ws.cbuf1, sizeof(double2) * gt);
+    fill(ws.wout, sizeof(double) * std::max<int64_t>(1, op->N * op->L) * cap);
+    fill(ws.vt, sizeof(double) * std::max<int64_t>(1, op->N) * cap);
+    fill(ws.asm_y1, sizeof(double) * ws.asm_cap);
+    fill(ws.asm_y2, sizeof(double) * (ws.asm_cap / 8 + 1));
+    if (ws.gdig) fill(ws.gdig, (size_t)nld::gather_gdig_bytes() * ws.gdig_cells * (cap / 16));
+    fill(ws.cg, sizeof(double) * 6 * ws.cg_cap);
+    NLD_CUDA(cudaDeviceSynchronize());
+  });
+}
+
 int nld_op_apply(nld_operator* op, int32_t kind, const double* v, double* out, int32_t nrhs,
                  int64_t ld, const double* coef_host, void* stream) {
   return guarded([&] {

@@ -278,6 +278,11 @@ class AnovaOperator:
     def set_timing(self, enabled: bool = True):
         check(lib.nld_op_set_timing(self._handle, 1 if enabled else 0))
 
+    def debug_poison_workspace(self):
+        """Test hook: fill the operator's device workspace with NaN bytes
+        (nld_op_debug_poison); products must not depend on its contents."""
+        check(lib.nld_op_debug_poison(self._handle))
+
     def stats(self) -> dict:
         s = Stats()
         check(lib.nld_op_stats(self._handle, ctypes.byref(s)))

@@ -1,16 +1,20 @@
 """Pixel sharding across GPUs: one process per GPU.
 
-Each rank holds a contiguous slice of the pixels (features, vectors, node
-tables, sort permutations).  The library calls one collective hook:
+Each rank holds a set of the pixels (features, vectors, node tables, sort
+permutations): a contiguous slice (`shard_range`) or the window-0 stencil-cell
+ownership partition (`partition`, what bench.py uses).  The library calls one
+collective hook:
 
 * at plan build: MIN/MAX of every window's bounding box, MAX of the torus
   radius and MIN/MAX of the stencil bases, so all ranks share the same torus
   map, kernel coefficients and support box (transform.py:292-296);
 * once per product: SUM of the per-window support-box grids (all windows and
-  right-hand sides in one call, ~2.5 MB per rhs at config 4), after which
-  every rank runs the small separable convolution redundantly and gathers its
-  own pixels;
-* in CG: SUM of the per-iteration scalars (dots, norms, means).
+  right-hand sides, ~0.47 MB per rhs at config 4: 3 support boxes of 27^3;
+  one call per window on the aux stream, overlapped with the next window's
+  spread), after which every rank runs the small separable convolution
+  redundantly and gathers its own pixels;
+* in CG: SUM of the per-iteration scalars (dots, norms, means), as a device
+  buffer on the solver's stream (one host read per reduction follows).
 
 `TorchComm` implements the hook with torch.distributed (NCCL over NVLink for
 device buffers; host buffers go through the same process group).
