@@ -73,6 +73,9 @@ constexpr int kYT0 = 2 * kAccCols;             // Y digits in TMEM: columns 384.
 #endif
 constexpr int kEpi = NLD_GNM_EPI;                  // 8 or 16 epilogue warps
 constexpr int kSPW = 16 / kEpi;                    // rhs slots (4 rhs each) per epilogue warp
+#ifndef NLD_GNM_PAIR
+#define NLD_GNM_PAIR 1
+#endif
 #ifndef NLD_GNM_SLC
 #define NLD_GNM_SLC 4
 #endif
@@ -505,59 +508,96 @@ k_gather_nm(const SubDev* __restrict__ subs, const int32_t* __restrict__ order, 
           OZW(10, umma::mbar_wait(&acc_full[ab], (gp >> 1) & 1));
           if (xf & 65536) spin_cycles(250);
           umma::fence_after();
-#pragma unroll
-          for (int j = 0; j < kSPW; ++j) {
-            // columns a = 0..7 of rhs slot w0 + j, six diagonals each, read in
-            // two halves of four a (24 registers at a time)
-            const uint32_t tc = tl_lane + (uint32_t)(ab * kAccCols + (w0 + j) * 8);
-            double sh = 0.0, sl_ = 0.0;
+#if NLD_GNM_PAIR
+          if (kSPW == 2) {
+            // both slots' columns in flight together (one wait per half), two
+            // independent combine chains per slot
+            const uint32_t tc0 = tl_lane + (uint32_t)(ab * kAccCols + w0 * 8);
+            double sh0 = 0.0, sl0 = 0.0, sh1 = 0.0, sl1 = 0.0;
 #pragma unroll
             for (int hf = 0; hf < 2; ++hf) {
-              uint32_t dv[kSl][4];
-              if (xf & 2) {
-#pragma unroll
-                for (int t = 0; t < kSl; ++t)
-#pragma unroll
-                  for (int i = 0; i < 4; ++i) dv[t][i] = (uint32_t)(lane * 7 + t + i + gp);
-              } else {
-                umma::tmem_ld4x6_wait(tc + 4 * hf, kPassRows, dv);
-              }
-              if (hf == 1 && j == kSPW - 1) {
-                // every column of this warp read: release the accumulator
+              uint32_t d0[kSl][4], d1[kSl][4];
+              umma::tmem_ld4x6x2_wait(tc0 + 4 * hf, tc0 + 8 + 4 * hf, kPassRows, d0, d1);
+              if (hf == 1) {
                 umma::fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&acc_empty[ab]);
               }
-              if (xf & 1) {
-                uint32_t f = 0;
-#pragma unroll
-                for (int t = 0; t < kSl; ++t)
-#pragma unroll
-                  for (int i = 0; i < 4; ++i) f ^= dv[t][i];
-                sh += (double)(f & 1);
-                continue;
-              }
-              // hi and lo parts accumulate in separate chains (combine6_parts)
               const double2 x0 = hf ? a45 : a01, x1 = hf ? a67 : a23;
               double h, l;
-              combine6_parts(dv, 0, h, l);
-              sh = fma(h, x0.x, sh);
-              sl_ = fma(l, x0.x, sl_);
-              combine6_parts(dv, 1, h, l);
-              sh = fma(h, x0.y, sh);
-              sl_ = fma(l, x0.y, sl_);
-              combine6_parts(dv, 2, h, l);
-              sh = fma(h, x1.x, sh);
-              sl_ = fma(l, x1.x, sl_);
-              combine6_parts(dv, 3, h, l);
-              sh = fma(h, x1.y, sh);
-              sl_ = fma(l, x1.y, sl_);
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const double av = i == 0 ? x0.x : i == 1 ? x0.y : i == 2 ? x1.x : x1.y;
+                combine6_parts(d0, i, h, l);
+                sh0 = fma(h, av, sh0);
+                sl0 = fma(l, av, sl0);
+                combine6_parts(d1, i, h, l);
+                sh1 = fma(h, av, sh1);
+                sl1 = fma(l, av, sl1);
+              }
             }
-            // rhs r0 + 4 j + ps
-            const int gx = ps == 0 ? ge[j].x : ps == 1 ? ge[j].y : ps == 2 ? ge[j].z : ge[j].w;
-            tv[j][ps] = fma(sh, 4294967296.0, sl_) * pow2(gx + eb);
+            const int gx0 = ps == 0 ? ge[0].x : ps == 1 ? ge[0].y : ps == 2 ? ge[0].z : ge[0].w;
+            const int gx1 = ps == 0 ? ge[kSPW - 1].x : ps == 1 ? ge[kSPW - 1].y
+                          : ps == 2 ? ge[kSPW - 1].z : ge[kSPW - 1].w;
+            tv[0][ps] = fma(sh0, 4294967296.0, sl0) * pow2(gx0 + eb);
+            tv[kSPW - 1][ps] = fma(sh1, 4294967296.0, sl1) * pow2(gx1 + eb);
+          } else
+#endif
+          {
+#pragma unroll
+            for (int j = 0; j < kSPW; ++j) {
+              // columns a = 0..7 of rhs slot w0 + j, six diagonals each, read in
+              // two halves of four a (24 registers at a time)
+              const uint32_t tc = tl_lane + (uint32_t)(ab * kAccCols + (w0 + j) * 8);
+              double sh = 0.0, sl_ = 0.0;
+  #pragma unroll
+              for (int hf = 0; hf < 2; ++hf) {
+                uint32_t dv[kSl][4];
+                if (xf & 2) {
+  #pragma unroll
+                  for (int t = 0; t < kSl; ++t)
+  #pragma unroll
+                    for (int i = 0; i < 4; ++i) dv[t][i] = (uint32_t)(lane * 7 + t + i + gp);
+                } else {
+                  umma::tmem_ld4x6_wait(tc + 4 * hf, kPassRows, dv);
+                }
+                if (hf == 1 && j == kSPW - 1) {
+                  // every column of this warp read: release the accumulator
+                  umma::fence_before();
+                  __syncwarp();
+                  if (lane == 0) mbar_arrive(&acc_empty[ab]);
+                }
+                if (xf & 1) {
+                  uint32_t f = 0;
+  #pragma unroll
+                  for (int t = 0; t < kSl; ++t)
+  #pragma unroll
+                    for (int i = 0; i < 4; ++i) f ^= dv[t][i];
+                  sh += (double)(f & 1);
+                  continue;
+                }
+                // hi and lo parts accumulate in separate chains (combine6_parts)
+                const double2 x0 = hf ? a45 : a01, x1 = hf ? a67 : a23;
+                double h, l;
+                combine6_parts(dv, 0, h, l);
+                sh = fma(h, x0.x, sh);
+                sl_ = fma(l, x0.x, sl_);
+                combine6_parts(dv, 1, h, l);
+                sh = fma(h, x0.y, sh);
+                sl_ = fma(l, x0.y, sl_);
+                combine6_parts(dv, 2, h, l);
+                sh = fma(h, x1.x, sh);
+                sl_ = fma(l, x1.x, sl_);
+                combine6_parts(dv, 3, h, l);
+                sh = fma(h, x1.y, sh);
+                sl_ = fma(l, x1.y, sl_);
+              }
+              // rhs r0 + 4 j + ps
+              const int gx = ps == 0 ? ge[j].x : ps == 1 ? ge[j].y : ps == 2 ? ge[j].z : ge[j].w;
+              tv[j][ps] = fma(sh, 4294967296.0, sl_) * pow2(gx + eb);
+            }
           }
-        }
+          }
         if (!ok || (xf & 128)) {
           if (xf & 128) {
             double f = 0.0;

@@ -163,6 +163,40 @@ __device__ __forceinline__ void tmem_ld4x6_wait(uint32_t taddr, uint32_t cs, uin
       : "r"(taddr), "r"(cs)
       : "memory");
 }
+// twelve x4 loads -- six per base address, column stride `cs` -- and one wait
+// in one asm (see above): two accumulator slots in flight together
+__device__ __forceinline__ void tmem_ld4x6x2_wait(uint32_t ta, uint32_t tb, uint32_t cs,
+                                                  uint32_t (&r)[6][4], uint32_t (&q)[6][4]) {
+  asm volatile(
+      "{\n\t.reg .b32 a1, a2, a3, a4, a5, b1, b2, b3, b4, b5;\n\t"
+      "add.u32 a1, %48, %50;\n\tadd.u32 a2, a1, %50;\n\tadd.u32 a3, a2, %50;\n\t"
+      "add.u32 a4, a3, %50;\n\tadd.u32 a5, a4, %50;\n\t"
+      "add.u32 b1, %49, %50;\n\tadd.u32 b2, b1, %50;\n\tadd.u32 b3, b2, %50;\n\t"
+      "add.u32 b4, b3, %50;\n\tadd.u32 b5, b4, %50;\n\t"
+      "tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%48];\n\t"
+      "tcgen05.ld.sync.aligned.32x32b.x4.b32 {%4,%5,%6,%7}, [a1];\n\t"
+      "tcgen05.ld.sync.aligned.32x32b.x4.b32 {%8,%9,%10,%11}, [a2];\n\t"
+      "tcgen05.ld.sync.aligned.32x32b.x4.b32 {%12,%13,%14,%15}, [a3];\n\t"
+      "tcgen05.ld.sync.aligned.32x32b.x4.b32 {%16,%17,%18,%19}, [a4];\n\t"
+      "tcgen05.ld.sync.aligned.32x32b.x4.b32 {%20,%21,%22,%23}, [a5];\n\t"
+      "tcgen05.ld.sync.aligned.32x32b.x4.b32 {%24,%25,%26,%27}, [%49];\n\t"
+      "tcgen05.ld.sync.aligned.32x32b.x4.b32 {%28,%29,%30,%31}, [b1];\n\t"
+      "tcgen05.ld.sync.aligned.32x32b.x4.b32 {%32,%33,%34,%35}, [b2];\n\t"
+      "tcgen05.ld.sync.aligned.32x32b.x4.b32 {%36,%37,%38,%39}, [b3];\n\t"
+      "tcgen05.ld.sync.aligned.32x32b.x4.b32 {%40,%41,%42,%43}, [b4];\n\t"
+      "tcgen05.ld.sync.aligned.32x32b.x4.b32 {%44,%45,%46,%47}, [b5];\n\t"
+      "tcgen05.wait::ld.sync.aligned;\n\t}\n"
+      : "=r"(r[0][0]), "=r"(r[0][1]), "=r"(r[0][2]), "=r"(r[0][3]), "=r"(r[1][0]), "=r"(r[1][1]),
+        "=r"(r[1][2]), "=r"(r[1][3]), "=r"(r[2][0]), "=r"(r[2][1]), "=r"(r[2][2]), "=r"(r[2][3]),
+        "=r"(r[3][0]), "=r"(r[3][1]), "=r"(r[3][2]), "=r"(r[3][3]), "=r"(r[4][0]), "=r"(r[4][1]),
+        "=r"(r[4][2]), "=r"(r[4][3]), "=r"(r[5][0]), "=r"(r[5][1]), "=r"(r[5][2]), "=r"(r[5][3]),
+        "=r"(q[0][0]), "=r"(q[0][1]), "=r"(q[0][2]), "=r"(q[0][3]), "=r"(q[1][0]), "=r"(q[1][1]),
+        "=r"(q[1][2]), "=r"(q[1][3]), "=r"(q[2][0]), "=r"(q[2][1]), "=r"(q[2][2]), "=r"(q[2][3]),
+        "=r"(q[3][0]), "=r"(q[3][1]), "=r"(q[3][2]), "=r"(q[3][3]), "=r"(q[4][0]), "=r"(q[4][1]),
+        "=r"(q[4][2]), "=r"(q[4][3]), "=r"(q[5][0]), "=r"(q[5][1]), "=r"(q[5][2]), "=r"(q[5][3])
+      : "r"(ta), "r"(tb), "r"(cs)
+      : "memory");
+}
 // six x8 loads (column stride `cs`) and the wait in one asm (see above)
 __device__ __forceinline__ void tmem_ld8x6_wait(uint32_t taddr, uint32_t cs, uint32_t (&r)[6][8]) {
   asm volatile(
