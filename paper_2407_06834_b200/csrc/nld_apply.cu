@@ -1036,6 +1036,15 @@ void spread_window_fast(const PlanSet& ps, const Workspace& ws, int w, const dou
   }
 }
 
+// window w's gather runs on the integer-sliced tcgen05 kernel (3-D, m = 4,
+// 16k rhs; the caller checks the cutoff)
+static bool sliced_gather(const PlanSet& ps, const Workspace& ws, int w, int nrhs) {
+  const WinPlan& wp = ps.win[w];
+  return ps.wdev_h[w].fast && wp.d == 3 && wp.n_subs > 0 && use_ozaki() && nrhs % 16 == 0 &&
+         nrhs <= 256 && ps.oz_ok && ws.gdig && !ab_switch("NLD_OZAKI_NO_GATHER", 0) &&
+         w < (int)ps.gcell_n.size() && ps.gcell_n[w] > 0;
+}
+
 template <int MC>
 void gather_window_fast(const PlanSet& ps, const Workspace& ws, int w, int64_t N, int nrhs,
                         cudaStream_t st, const mma::GatherEpi& ep, double* out) {
@@ -1049,13 +1058,11 @@ void gather_window_fast(const PlanSet& ps, const Workspace& ws, int w, int64_t N
   const int acc = ep.mode == mma::kGatherFirst ? 0 : 1;
   if (wp.d == 1) launch_gather<1, MC>(subs, nsub, ps, ws, N, nrhs, st, fout, acc);
   else if (wp.d == 2) launch_gather<2, MC>(subs, nsub, ps, ws, N, nrhs, st, fout, acc);
-  else if (MC == 4 && use_ozaki() && nrhs % 16 == 0 && nrhs <= 256 && ps.oz_ok && ws.gdig &&
-           !ab_switch("NLD_OZAKI_NO_GATHER", 0) &&
-           w < (int)ps.gcell_n.size() && ps.gcell_n[w] > 0)
+  else if (MC == 4 && sliced_gather(ps, ws, w, nrhs))
     launch_gather_nm(ps, subs, ps.sub_exp + wp.sub_off * 24, ps.sub_order + wp.sub_off,
                      nsub, ws.grid_out, ps.grid_total,
                      ep.mode == mma::kGatherStore ? ws.wout + (int64_t)w * N * nrhs : out, nrhs,
-                     ep, st, ws.gdig, ps.gcell_lo[w], ps.gcell_n[w]);
+                     ep, st, ws.gdig, ps.gcell_lo[w], ps.gcell_n[w], ws.gdig_on_aux);
   else if (MC == 4 && use_mma()) launch_gather_mma(subs, nsub, ps, ws, N, nrhs, st, ep, out);
   else launch_gather<3, MC>(subs, nsub, ps, ws, N, nrhs, st);
 }
@@ -1407,6 +1414,11 @@ void apply_op(nld_operator* op, int which, int kind, const double* v, double* ou
                       kind, L, v, eta, coef_dev};
     gather_window(op, ps, w, nrhs, st, &ep, out);
   };
+#ifndef NLD_GDIG_AUX
+#define NLD_GDIG_AUX 1
+#endif
+  const bool gdig_aux = NLD_GDIG_AUX && overlap && op->params.cutoff == 4;
+  ws.gdig_on_aux = gdig_aux;
   if (overlap) {
     // window w's assemble + convolution (latency / L2 bound) run on the aux
     // stream while the main stream spreads window w+1 and, later, gathers
@@ -1419,6 +1431,11 @@ void apply_op(nld_operator* op, int which, int kind, const double* v, double* ou
       assemble_window(op, ps, w, vt, nrhs, op->aux);
       comm_window(op, ps, w, nrhs, sliced && w == L - 1, op->aux);
       conv_window(op, ps, w, nrhs, op->aux);
+      // the window's G digits too (they depend only on its convolved grid):
+      // off the main stream, which spreads and gathers meanwhile
+      if (gdig_aux && sliced_gather(ps, ws, w, nrhs))
+        launch_gdig_nm(ps, ws.grid_out, ps.grid_total, nrhs, ws.gdig, ps.gcell_lo[w],
+                       ps.gcell_n[w], op->aux);
       NLD_CUDA(cudaEventRecord(op->ev_conv[w], op->aux));
     }
     ev.mark();
@@ -1475,6 +1492,7 @@ void apply_op(nld_operator* op, int which, int kind, const double* v, double* ou
     ++launches;
   }
   ev.mark();
+  ws.gdig_on_aux = false;
   op->stats.launches = launches;
 }
 

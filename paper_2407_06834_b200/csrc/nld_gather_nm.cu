@@ -652,6 +652,14 @@ k_gather_nm(const SubDev* __restrict__ subs, const int32_t* __restrict__ order, 
 
 int64_t gather_gdig_bytes() { return oz::nm::kGItem; }
 
+// G digits of one window's cells (grid_out of that window must be final)
+void launch_gdig_nm(const PlanSet& ps, const double* grid, int64_t grid_ld, int nrhs,
+                    uint8_t* gdig, int64_t cell_lo, int64_t ncell, cudaStream_t st) {
+  oz::nm::k_gdig_nm<<<dim3((unsigned)ncell, (unsigned)(nrhs / 16)), oz::kRows, 0, st>>>(
+      ps.cells, ps.wdev, grid, grid_ld, cell_lo, nrhs / 16, gdig);
+  NLD_CUDA(cudaGetLastError());
+}
+
 template <int MODE>
 static void launch_nm(unsigned grid_n, const PlanSet& ps, const SubDev* subs, const int32_t* order,
                       unsigned nsub, const int16_t* ex, const uint8_t* gdig, double* out, int nrhs,
@@ -671,16 +679,14 @@ static void launch_nm(unsigned grid_n, const PlanSet& ps, const SubDev* subs, co
 void launch_gather_nm(const PlanSet& ps, const SubDev* subs, const int16_t* ex,
                       const int32_t* order, unsigned nsub, const double* grid, int64_t grid_ld,
                       double* out, int nrhs, const mma::GatherEpi& ep, cudaStream_t st,
-                      uint8_t* gdig, int64_t cell_lo, int64_t ncell) {
+                      uint8_t* gdig, int64_t cell_lo, int64_t ncell, bool gdig_ready) {
   static int sms = 0;
   if (!sms) {
     int dev = 0;
     NLD_CUDA(cudaGetDevice(&dev));
     NLD_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   }
-  oz::nm::k_gdig_nm<<<dim3((unsigned)ncell, (unsigned)(nrhs / 16)), oz::kRows, 0, st>>>(
-      ps.cells, ps.wdev, grid, grid_ld, cell_lo, nrhs / 16, gdig);
-  NLD_CUDA(cudaGetLastError());
+  if (!gdig_ready) launch_gdig_nm(ps, grid, grid_ld, nrhs, gdig, cell_lo, ncell, st);
   const unsigned grid_n = std::min<unsigned>(nsub, (unsigned)sms);
   switch (ep.mode) {
     case mma::kGatherStore:

@@ -157,6 +157,7 @@ struct Workspace {
   unsigned long long* vmax = nullptr;   // [nrhs_cap] sliced spread: max |v| bits
   uint8_t* gdig = nullptr;       // sliced gather: per (cell, 16-rhs group) G digits + exponents
   int64_t gdig_cells = 0;
+  bool gdig_on_aux = false;      // this product's G digits were cut on the aux stream
   // persistent CG vectors (x, r, p, q, b, t): [6][cg_cap]
   double* cg = nullptr;
   int64_t cg_cap = 0;
@@ -217,7 +218,9 @@ namespace mma { struct GatherEpi; }
 void launch_gather_nm(const PlanSet& ps, const SubDev* subs, const int16_t* ex,
                       const int32_t* order, unsigned nsub, const double* grid, int64_t grid_ld,
                       double* out, int nrhs, const mma::GatherEpi& ep, cudaStream_t st,
-                      uint8_t* gdig, int64_t cell_lo, int64_t ncell);
+                      uint8_t* gdig, int64_t cell_lo, int64_t ncell, bool gdig_ready = false);
+void launch_gdig_nm(const PlanSet& ps, const double* grid, int64_t grid_ld, int nrhs,
+                    uint8_t* gdig, int64_t cell_lo, int64_t ncell, cudaStream_t st);
 // bytes per (cell, 16-rhs group) of precomputed gather G digits
 int64_t gather_gdig_bytes();
 void free_planset(PlanSet& ps);
