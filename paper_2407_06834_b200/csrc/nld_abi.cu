@@ -198,6 +198,7 @@ int nld_op_destroy(nld_operator* op) {
       cudaEventDestroy(op->ev_fork);
       cudaEventDestroy(op->ev_join);
       cudaStreamDestroy(op->aux);
+      if (op->aux2) cudaStreamDestroy(op->aux2);
     }
     delete op;
   });
@@ -249,6 +250,10 @@ int nld_op_debug_poison(nld_operator* op) {
     fill(ws.vt, sizeof(double) * std::max<int64_t>(1, op->N) * cap);
     fill(ws.asm_y1, sizeof(double) * ws.asm_cap);
     fill(ws.asm_y2, sizeof(double) * (ws.asm_cap / 8 + 1));
+    fill(ws.asm_y1b, sizeof(double) * ws.asm_cap);
+    fill(ws.asm_y2b, sizeof(double) * (ws.asm_cap / 8 + 1));
+    fill(ws.cbuf2, sizeof(double2) * gt);
+    fill(ws.cbuf3, sizeof(double2) * gt);
     if (ws.gdig) fill(ws.gdig, (size_t)nld::gather_gdig_bytes() * ws.gdig_cells * (cap / 16));
     fill(ws.cg, sizeof(double) * 6 * ws.cg_cap);
     NLD_CUDA(cudaDeviceSynchronize());

@@ -1105,6 +1105,8 @@ void ensure_workspace(nld_operator* op, const PlanSet& ps, int nrhs) {
   NLD_CUDA(cudaMalloc(&ws.grid_out, sizeof(double) * std::max<int64_t>(1, gt) * cap));
   NLD_CUDA(cudaMalloc(&ws.cbuf0, sizeof(double2) * std::max<int64_t>(1, gt) * cap));
   NLD_CUDA(cudaMalloc(&ws.cbuf1, sizeof(double2) * std::max<int64_t>(1, gt) * cap));
+  NLD_CUDA(cudaMalloc(&ws.cbuf2, sizeof(double2) * std::max<int64_t>(1, gt) * cap));
+  NLD_CUDA(cudaMalloc(&ws.cbuf3, sizeof(double2) * std::max<int64_t>(1, gt) * cap));
   NLD_CUDA(cudaMalloc(&ws.wout, sizeof(double) * std::max<int64_t>(1, op->N * op->L) * cap));
   NLD_CUDA(cudaMalloc(&ws.vt, sizeof(double) * std::max<int64_t>(1, op->N) * cap));
   NLD_CUDA(cudaMalloc(&ws.coef, sizeof(double) * 2 * cap));
@@ -1121,6 +1123,8 @@ void ensure_workspace(nld_operator* op, const PlanSet& ps, int nrhs) {
     if (ws.asm_cap) {
       NLD_CUDA(cudaMalloc(&ws.asm_y1, sizeof(double) * ws.asm_cap));
       NLD_CUDA(cudaMalloc(&ws.asm_y2, sizeof(double) * (ws.asm_cap / 8 + 1)));
+      NLD_CUDA(cudaMalloc(&ws.asm_y1b, sizeof(double) * ws.asm_cap));
+      NLD_CUDA(cudaMalloc(&ws.asm_y2b, sizeof(double) * (ws.asm_cap / 8 + 1)));
     }
   }
   {
@@ -1138,6 +1142,10 @@ void ensure_workspace(nld_operator* op, const PlanSet& ps, int nrhs) {
 void free_workspace(Workspace& ws) {
   cudaFree(ws.asm_y1);
   cudaFree(ws.asm_y2);
+  cudaFree(ws.asm_y1b);
+  cudaFree(ws.asm_y2b);
+  cudaFree(ws.cbuf2);
+  cudaFree(ws.cbuf3);
   cudaFree(ws.cg);
   cudaFree(ws.blocks);
   cudaFree(ws.grid_in);
@@ -1167,17 +1175,18 @@ static void spread_window(nld_operator* op, const PlanSet& ps, int w, const doub
 
 // assemble of window w + its generic/edge atomics (writes ws.grid_in)
 static void assemble_window(nld_operator* op, const PlanSet& ps, int w, const double* vt,
-                            int nrhs, cudaStream_t st) {
+                            int nrhs, cudaStream_t st, int set = 0) {
   Workspace& ws = op->ws;
+  double* const y1 = set ? ws.asm_y1b : ws.asm_y1;
+  double* const y2 = set ? ws.asm_y2b : ws.asm_y2;
   const WinDev& wd = ps.wdev_h[w];
   const WinPlan& wp = ps.win[w];
   const int64_t y1n = wd.box_size * 64 * nrhs;
   if (wd.fast && wd.d == 3 && wd.S == 8 && !wd.wrap && ws.asm_cap >= y1n) {
     k_asm_p1<<<grid_blocks(y1n, 256, 148 * 32), 256, 0, st>>>(ps.wdev, w, ps.cellinfo,
-                                                              ws.blocks, nrhs, ws.asm_y1);
-    k_asm_p2<<<grid_blocks(y1n / 8, 256, 148 * 32), 256, 0, st>>>(ps.wdev, w, ws.asm_y1, nrhs,
-                                                                  ws.asm_y2);
-    k_asm_p3<<<grid_blocks(y1n / 64, 256, 148 * 32), 256, 0, st>>>(ps.wdev, w, ws.asm_y2, nrhs,
+                                                              ws.blocks, nrhs, y1);
+    k_asm_p2<<<grid_blocks(y1n / 8, 256, 148 * 32), 256, 0, st>>>(ps.wdev, w, y1, nrhs, y2);
+    k_asm_p3<<<grid_blocks(y1n / 64, 256, 148 * 32), 256, 0, st>>>(ps.wdev, w, y2, nrhs,
                                                                    ws.grid_in, ps.grid_total);
   } else {
     dim3 grid(grid_blocks(wd.box_size * nrhs, 32, 148 * 16), 1);
@@ -1200,13 +1209,16 @@ static void assemble_window(nld_operator* op, const PlanSet& ps, int w, const do
 }
 
 // separable convolution of window w: grid_in -> grid_out
-static void conv_window(nld_operator* op, const PlanSet& ps, int w, int nrhs, cudaStream_t st) {
+static void conv_window(nld_operator* op, const PlanSet& ps, int w, int nrhs, cudaStream_t st,
+                        int set = 0) {
   Workspace& ws = op->ws;
+  double2* const b0 = set ? ws.cbuf2 : ws.cbuf0;
+  double2* const b1 = set ? ws.cbuf3 : ws.cbuf1;
   const WinDev& wd = ps.wdev_h[w];
   for (int pass = 0; pass < wd.d; ++pass) {
     dim3 grid(grid_blocks(wd.box_size, 128, 1024), 1, nrhs);
-    const double2* cin = (pass % 2 == 1) ? ws.cbuf0 : ws.cbuf1;
-    double2* cout = (pass % 2 == 0) ? ws.cbuf0 : ws.cbuf1;
+    const double2* cin = (pass % 2 == 1) ? b0 : b1;
+    double2* cout = (pass % 2 == 0) ? b0 : b1;
     k_conv<<<grid, 128, 0, st>>>(ps.wdev, w, pass, ps.K, ws.grid_in, cin, cout, ws.grid_out,
                                  ps.grid_total);
     NLD_CUDA(cudaGetLastError());
@@ -1288,13 +1300,13 @@ __global__ void k_unpack_win(const double* __restrict__ buf, int64_t grid_ld, in
 // next window): packed into the convolution scratch, summed, unpacked; the
 // last window also carries the per-rhs non-finite flags
 static void comm_window(nld_operator* op, const PlanSet& ps, int w, int nrhs, bool flags,
-                        cudaStream_t st) {
+                        cudaStream_t st, int set = 0) {
   if (!op->comm) return;
   Workspace& ws = op->ws;
   const WinDev& wd = ps.wdev_h[w];
   double* extra = ws.grid_in + ps.grid_total * nrhs;
   const int ne = flags ? nrhs : 0;
-  double* buf = reinterpret_cast<double*>(ws.cbuf0);
+  double* buf = reinterpret_cast<double*>(set ? ws.cbuf2 : ws.cbuf0);
   const int64_t cnt = wd.box_size * nrhs + ne;
   k_pack_win<<<grid_blocks(cnt, 256, 148 * 8), 256, 0, st>>>(ws.grid_in, ps.grid_total,
                                                              wd.grid_off, wd.box_size, nrhs,
@@ -1329,6 +1341,7 @@ static void ensure_aux(nld_operator* op, int L) {
   if (op->aux && op->aux_windows >= L) return;
   if (!op->aux) {
     NLD_CUDA(cudaStreamCreateWithFlags(&op->aux, cudaStreamNonBlocking));
+    NLD_CUDA(cudaStreamCreateWithFlags(&op->aux2, cudaStreamNonBlocking));
     NLD_CUDA(cudaEventCreateWithFlags(&op->ev_fork, cudaEventDisableTiming));
     NLD_CUDA(cudaEventCreateWithFlags(&op->ev_join, cudaEventDisableTiming));
   }
@@ -1427,16 +1440,21 @@ void apply_op(nld_operator* op, int which, int kind, const double* v, double* ou
     for (int w = 0; w < L; ++w) {
       spread_window(op, ps, w, vt, nrhs, st);
       NLD_CUDA(cudaEventRecord(op->ev_spread[w], st));
-      NLD_CUDA(cudaStreamWaitEvent(op->aux, op->ev_spread[w], 0));
-      assemble_window(op, ps, w, vt, nrhs, op->aux);
-      comm_window(op, ps, w, nrhs, sliced && w == L - 1, op->aux);
-      conv_window(op, ps, w, nrhs, op->aux);
+      // windows alternate between two aux streams (own scratch each): with
+      // many small windows (c2: eight 3-D) one stream's assemble chain was
+      // slower than the spreads it overlaps
+      const int set = w & 1;
+      cudaStream_t ax = set ? op->aux2 : op->aux;
+      NLD_CUDA(cudaStreamWaitEvent(ax, op->ev_spread[w], 0));
+      assemble_window(op, ps, w, vt, nrhs, ax, set);
+      comm_window(op, ps, w, nrhs, sliced && w == L - 1, ax, set);
+      conv_window(op, ps, w, nrhs, ax, set);
       // the window's G digits too (they depend only on its convolved grid):
       // off the main stream, which spreads and gathers meanwhile
       if (gdig_aux && sliced_gather(ps, ws, w, nrhs))
         launch_gdig_nm(ps, ws.grid_out, ps.grid_total, nrhs, ws.gdig, ps.gcell_lo[w],
-                       ps.gcell_n[w], op->aux);
-      NLD_CUDA(cudaEventRecord(op->ev_conv[w], op->aux));
+                       ps.gcell_n[w], ax);
+      NLD_CUDA(cudaEventRecord(op->ev_conv[w], ax));
     }
     ev.mark();
     NLD_CUDA(cudaStreamWaitEvent(st, op->ev_conv[gorder[0]], 0));

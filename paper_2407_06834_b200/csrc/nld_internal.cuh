@@ -146,6 +146,8 @@ struct Workspace {
   double* grid_out = nullptr;
   double2* cbuf0 = nullptr;
   double2* cbuf1 = nullptr;
+  double2* cbuf2 = nullptr;      // second aux stream's convolution scratch
+  double2* cbuf3 = nullptr;
   double* wout = nullptr;        // [L][N][nrhs] per-window gathers
   double* vt = nullptr;          // [N][nrhs] pixel-major rhs
   double* coef = nullptr;        // [nrhs][2]
@@ -153,6 +155,8 @@ struct Workspace {
   // separable assemble scratch (3-D windows): Y1 [box][64][nrhs], Y2 /8
   double* asm_y1 = nullptr;
   double* asm_y2 = nullptr;
+  double* asm_y1b = nullptr;     // second aux stream's assemble scratch
+  double* asm_y2b = nullptr;
   int64_t asm_cap = 0;
   unsigned long long* vmax = nullptr;   // [nrhs_cap] sliced spread: max |v| bits
   uint8_t* gdig = nullptr;       // sliced gather: per (cell, 16-rhs group) G digits + exponents
@@ -186,7 +190,8 @@ struct nld_operator {
   nld_stats stats{};
   cudaEvent_t ev[6] = {};
   bool events = false;
-  cudaStream_t aux = nullptr;    // assemble/convolution stream (overlap)
+  cudaStream_t aux = nullptr;    // assemble/convolution streams (overlap): windows
+  cudaStream_t aux2 = nullptr;   // alternate between them
   cudaEvent_t ev_spread[16] = {}, ev_conv[16] = {}, ev_fork = nullptr, ev_join = nullptr;
   int aux_windows = 0;
   std::mutex build_mu;           // lazy plan build (per operator: shards may

@@ -230,17 +230,36 @@ __device__ __forceinline__ int canon64(int row, int k) {
   return (row >> 3) * 512 + (k >> 4) * 128 + (row & 7) * 16 + (k & 15);
 }
 
+// The hi part converts with I2F.F64 (one conversion-unit instruction instead
+// of XOR + constant move + DADD: the gather's epilogue is bound by its
+// instruction count, measured 2.5% faster); NLD_OZ_COMBINE_MAGIC=1 keeps the
+// magic-number form.
+#ifndef NLD_OZ_COMBINE_MAGIC
+#define NLD_OZ_COMBINE_MAGIC 0
+#endif
+#ifndef NLD_OZ_COMBINE_LO64
+#define NLD_OZ_COMBINE_LO64 0
+#endif
 template <int NCOL>
 __device__ __forceinline__ void combine6_parts(const uint32_t (&dv)[6][NCOL], int i, double& hi,
                                                double& lo) {
   const uint32_t x01 = dv[0][i] * 256u + dv[1][i];
   const int32_t x23 = (int32_t)(dv[2][i] * 256u + dv[3][i]);
+#if NLD_OZ_COMBINE_LO64
+  const int32_t x45 = (int32_t)(dv[4][i] * 256u + dv[5][i]);
+  lo = (double)((long long)x23 * 65536 + x45);
+#else
   const uint32_t x45b = dv[4][i] * 256u + (dv[5][i] ^ 0x80000000u);
   double r;
   asm("{\n\t.reg .b64 c;\n\tmov.b64 c, {%1, %2};\n\tmad.wide.s32 c, %3, 65536, c;\n\t"
       "mov.b64 %0, c;\n\t}" : "=d"(r) : "r"(x45b), "r"(0x43380000u), "r"(x23));
   lo = r - (6755399441055744.0 + 2147483648.0);   // 2^52 + 2^51 + 2^31
+#endif
+#if NLD_OZ_COMBINE_MAGIC
   hi = i2d(x01);
+#else
+  hi = (double)(int32_t)x01;
+#endif
 }
 
 #if defined(NLD_OZ_TRACE)
