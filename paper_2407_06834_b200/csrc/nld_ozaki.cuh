@@ -245,9 +245,12 @@ __device__ __forceinline__ void combine6_parts(const uint32_t (&dv)[6][NCOL], in
                                                double& lo) {
   const uint32_t x01 = dv[0][i] * 256u + dv[1][i];
   const int32_t x23 = (int32_t)(dv[2][i] * 256u + dv[3][i]);
-#if NLD_OZ_COMBINE_LO64
+#if NLD_OZ_COMBINE_LO64 == 1
   const int32_t x45 = (int32_t)(dv[4][i] * 256u + dv[5][i]);
   lo = (double)((long long)x23 * 65536 + x45);
+#elif NLD_OZ_COMBINE_LO64 == 2
+  const int32_t x45 = (int32_t)(dv[4][i] * 256u + dv[5][i]);
+  lo = fma((double)x23, 65536.0, (double)x45);    // exact: |x23 2^16 + x45| < 2^46
 #else
   const uint32_t x45b = dv[4][i] * 256u + (dv[5][i] ^ 0x80000000u);
   double r;
