@@ -99,6 +99,8 @@ def cpu_sample(cfg_name, steps=2, warmup=1):
         "sample_seconds": best,
         "host_cpus": os.cpu_count(),
         "times_s": times,
+        "n_full": n_full,
+        "windows": [len(w) for w in wins],
     }
 
 
@@ -156,6 +158,23 @@ def reference_numba_sample(cfg_name, nodes=REF_SAMPLE_NODES):
                        f"a JIT warm-up, scaled by {ns}/{n_full}")}
 
 
+def workload_config(cfg_name, nrhs, n_global, n_rank, windows, world, kernels, setup_s=None):
+    """The `config` object of both arms' lines (same workload, same keys)."""
+    import synth
+    cfg = {"workload": (f"{cfg_name}: batched fused system matvec "
+                        f"y = v + a_k(eta v - Gamma v), {nrhs} rhs "
+                        "(pixel-major batch)"),
+           "n_nodes": int(n_global), "nodes_per_rank": int(n_rank),
+           "windows": list(windows), "nrhs": int(nrhs),
+           "bandwidth": synth.N_EXPANSION, "cutoff": synth.CUTOFF, "grid": 64,
+           "parallelism": (f"pixel-sharded x{world} (grid allreduce over NCCL)"
+                           if world > 1 else "single"),
+           "l2": "inputs larger than L2 (no flush)", "kernels": kernels}
+    if setup_s is not None:
+        cfg["setup_s"] = setup_s
+    return cfg
+
+
 def run_reference(args, world, rank):
     if rank != 0:
         return
@@ -170,8 +189,12 @@ def run_reference(args, world, rank):
         "warmup": args.warmup, "ms_per_step": 1e3 * res["sample_seconds"],
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{args.config} fused system matvec (cpu sample)",
-                   "n_nodes": int(4096 * 4096 if args.config == "c4" else 0)},
+        # the same workload and metric as our arm (matvecs per rhs): the
+        # sample (cpu_baseline.sample) is a bounded slice of it, scaled
+        "config": workload_config(args.config, args.nrhs or 16, res["n_full"],
+                                  res["n_full"], res["windows"], world,
+                                  "reference algorithm on the host CPU: C restatement of "
+                                  "_kernels.py spread/gather + numpy FFT (all host threads)"),
         "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind",
                                              "sample")},
         "host_cpus": os.cpu_count(),
@@ -287,11 +310,12 @@ def run_ours(args, world, rank, local):
     nrhs = args.nrhs or 16
     feats, wins, f_img = synth.make_problem(args.config)
     n_global = feats.shape[0]
-    # pixel sharding (strong scaling): this rank's contiguous slice
-    lo, hi = sharding.shard_range(n_global, rank, world)
-    feats = np.ascontiguousarray(feats[lo:hi])
-    f_img = np.ascontiguousarray(f_img[lo:hi])
-    n = hi - lo
+    # pixel sharding (strong scaling): this rank's pixels, partitioned by
+    # window-0 stencil-cell ownership (sharding.partition)
+    ix = sharding.partition(feats, wins, world)[rank] if world > 1 else np.arange(n_global)
+    feats = np.ascontiguousarray(feats[ix])
+    f_img = np.ascontiguousarray(f_img[ix])
+    n = len(ix)
     feat_t = torch.from_numpy(feats).to(dev)
     t_setup = time.perf_counter()
     op = nld.AnovaOperator(feat_t, wins, synth.SIGMA,
@@ -547,20 +571,10 @@ def run_ours(args, world, rank, local):
             "higher_is_better": True,
             "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": (f"{args.config}: batched fused system matvec "
-                                    f"y = v + a_k(eta v - Gamma v), {nrhs} rhs "
-                                    "(pixel-major batch)"),
-                       "n_nodes": n_global, "nodes_per_rank": n,
-                       "windows": [len(w) for w in wins],
-                       "nrhs": nrhs, "bandwidth": synth.N_EXPANSION,
-                       "cutoff": synth.CUTOFF, "grid": 64,
-                       "parallelism": (f"pixel-sharded x{world} (grid allreduce over NCCL)"
-                                       if world > 1 else "single"),
-                       "l2": "inputs larger than L2 (no flush)",
-                       "kernels": ("integer-sliced tcgen05 spread/gather (exact s8 x s8 -> s32 "
-                                   "digit products, fp64 combine)" if sliced
-                                   else "fp64 DMMA spread/gather"),
-                       "setup_s": t_setup},
+            "config": workload_config(
+                args.config, nrhs, n_global, n, [len(w) for w in wins], world,
+                ("integer-sliced tcgen05 spread/gather (exact s8 x s8 -> s32 digit products, "
+                 "fp64 combine)" if sliced else "fp64 DMMA spread/gather"), t_setup),
             "roofline": roofline, "cpu_baseline": cpu, "host_cpus": os.cpu_count(),
             "e2e": {"value": e2e_val, "unit": UNIT,
                     "h2d_bytes_per_step": int(nrhs * n_global * 8),
