@@ -163,9 +163,18 @@ constexpr int kLoaders = NLD_SPR_LD;
 // item is the TMEM drain (the accumulator is single-buffered: 384 of 512
 // columns).  Scales are per-thread registers (no per-item shared state).
 //   warps 0..S-1  slicers (X digits -> TMEM, Y digits -> shared memory)
-//   warp S        UMMA issuer     then kLoaders loader warps, 4 epilogue warps
+//   warp S        UMMA issuer     then kLoaders loader warps, kSPEpiN epilogue warps
+#ifndef NLD_SPR_EPI
+#define NLD_SPR_EPI 8
+#endif
+// epilogue warps: 4 (one per lane quarter, all 64 column groups) or 8 (two
+// per lane quarter, 32 columns each) -- the accumulator is single-buffered,
+// so the issuer waits for its drain at every item boundary
+constexpr int kSPEpiN = NLD_SPR_EPI;
+constexpr int kSPEpiCols = 64 * 4 / kSPEpiN;     // columns (b, c) per epilogue warp
 constexpr int kSPEpi0 = kLoaderWarp + kLoaders;
-constexpr int kSPThreads = 32 * (kSPEpi0 + 4);
+constexpr int kSPThreads = 32 * (kSPEpi0 + kSPEpiN);
+static_assert(kSPEpiN == 4 || kSPEpiN == 8, "spread epilogue warps");
 
 __global__ void __launch_bounds__(kSPThreads, 1)
 k_spread_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order, int nsub,
@@ -206,7 +215,7 @@ k_spread_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
       umma::mbar_init(&op_free[k], 1);
     }
     umma::mbar_init(&acc_full, 1);
-    umma::mbar_init(&acc_empty, 4);                       // epilogue warps
+    umma::mbar_init(&acc_empty, kSPEpiN);                 // epilogue warps
     umma::mbar_fence_init();
   }
   umma::fence_before();
@@ -399,6 +408,7 @@ k_spread_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
     const int m = lg * 32 + lane;
     const int a = m >> 4, r = m & 15;
     const uint32_t tl = tmem + ((uint32_t)(lg * 32) << 16);
+    const int cb = ((warp - kSPEpi0) >> 2) * kSPEpiCols;   // this warp's first column (b, c)
     for (int k = 0; k < nitems; ++k) {
       const int si = item_sub(k);
       const SubDev sd = subs[si];
@@ -416,10 +426,10 @@ k_spread_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
       umma::fence_after();
       double* bo = blocks + (sd.block + a * 64) * nrhs + rg + r;
 #pragma unroll 1
-      for (int c0 = 0; c0 < 64; c0 += 8) {
+      for (int c0 = cb; c0 < cb + kSPEpiCols; c0 += 8) {
         uint32_t dv[kSl][8];
         if (xf & 4) {
-          if (c0 == 56) {
+          if (c0 == cb + kSPEpiCols - 8) {
             umma::fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&acc_empty);
@@ -427,7 +437,7 @@ k_spread_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
           continue;
         }
         umma::tmem_ld8x6_wait(tl + (uint32_t)c0, 64, dv);
-        if (c0 == 56) {
+        if (c0 == cb + kSPEpiCols - 8) {
           // every column read: the next item's UMMAs may overwrite the accumulator
           umma::fence_before();
           __syncwarp();

@@ -424,6 +424,22 @@ def test_fused_gather_epilogue(case, nrhs):
         assert err < 1e-14, (kind, err)
     if case == "edges":
         assert op.window_info(0)["n_edge"] > 0 and op.window_info(1)["n_edge"] > 0
+        # not only self-consistent: the fused sliced product (edge nodes'
+        # extra stencil slices included) against the CPU oracle, every column
+        ref = O.AnovaOracle(feats, wins, 0.1, **PIN)
+        Vh = V.cpu().numpy()
+        g = op.apply_device(V.T.contiguous(), _lib.APPLY_GAMMA, nrhs, pixel_major=True)
+        g = g.cpu().numpy()
+        for k in range(nrhs):
+            want = ref.apply(Vh[k])
+            assert rel(g[:, k], want) < 1e-10, (k, rel(g[:, k], want))
+        y = op.apply_device(V.T.contiguous(), _lib.APPLY_SYSTEM, nrhs, coef,
+                            pixel_major=True).cpu().numpy()
+        eta = ref.degree()
+        for k in (0, nrhs - 1):
+            lam, mu = coef[2 * k], coef[2 * k + 1]
+            want = lam * Vh[k] + mu * (eta * Vh[k] - ref.apply(Vh[k]))
+            assert rel(y[:, k], want) < 1e-10
 
 
 # ------------------------------ integer-sliced tensor-core path (16k rhs)
