@@ -165,7 +165,7 @@ constexpr int kLoaders = NLD_SPR_LD;
 //   warps 0..S-1  slicers (X digits -> TMEM, Y digits -> shared memory)
 //   warp S        UMMA issuer     then kLoaders loader warps, kSPEpiN epilogue warps
 #ifndef NLD_SPR_EPI
-#define NLD_SPR_EPI 8
+#define NLD_SPR_EPI 4
 #endif
 // epilogue warps: 4 (one per lane quarter, all 64 column groups) or 8 (two
 // per lane quarter, 32 columns each) -- the accumulator is single-buffered,
@@ -310,14 +310,15 @@ k_spread_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
   } else if (warp < kIssuerWarp) {
     // --------------------------------------------------------------- slicers
     // X: thread = TMEM lane m = (a, r) of its warp's lane quarter, kXNodes
-    // nodes h kXNodes .. ; Y: a warp covers 8 rows (b, c) x 16 nodes, a lane
-    // one row and 4 nodes (its 4-byte digit words of a quarter-warp fill a
-    // 128-byte line: conflict-free stores)
+    // nodes h kXNodes .. ; Y with 8 slicer warps: a warp covers 32 rows (b, c)
+    // x 8 nodes, a lane one row and 8 nodes (the node of each load is
+    // warp-uniform: conflict-free loads, 8-byte digit stores); with 16: a warp
+    // covers 8 rows x 16 nodes, a lane one row and 4 nodes (conflict-free
+    // 4-byte stores)
     const int m = (warp & 3) * 32 + lane, h = warp >> 2;
     const int a = m >> 4, r = m & 15;
-    const int yn = (warp & 7) * 8 + (lane & 7);             // Y row (b, c)
+    const int yn = kSlcWarps == 16 ? (warp & 7) * 8 + (lane & 7) : tid & 63;   // Y row (b, c)
     const int yb = yn >> 3, yc = yn & 7;
-    constexpr int kYReps = kSlcWarps == 16 ? 1 : 2;         // 8 warps: both node halves
     int g = 0;
     for (int k = 0; k < nitems; ++k) {
       const int si = item_sub(k);
@@ -347,10 +348,9 @@ k_spread_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
           }
           continue;
         }
-#pragma unroll
-        for (int yr = 0; yr < kYReps; ++yr) {
+        if (kSlcWarps == 16) {
           // Y digits of 4 nodes for row (b, c): K-major canonical, zero past cn
-          const int kn = (kSlcWarps == 16 ? (warp >> 3) : yr) * 16 + (lane >> 3) * 4;
+          const int kn = (warp >> 3) * 16 + (lane >> 3) * 4;
           uint32_t lo[4], hi[4];
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
@@ -367,6 +367,21 @@ k_spread_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
           uint8_t* yd = sYop + st * kYOpBytes + canon32(yn, kn);
 #pragma unroll
           for (int p = 0; p < kSl; ++p) *reinterpret_cast<uint32_t*>(yd + p * kBBytes) = w6[p];
+        } else {
+          // Y digits of 8 nodes for row (b, c)
+          const int yq = tid >> 6;
+          uint32_t lo[8], hi[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int j = yq * 8 + i;
+            double x = 0.0, y = 0.0;
+            if (j < cn) {
+              x = R[j * 24 + 8 + yb] * sy;
+              y = R[j * 24 + 16 + yc];
+            }
+            slice1(x, y, lo[i], hi[i]);
+          }
+          store8(lo, hi, sYop + st * kYOpBytes + canon32(yn, yq * 8), kBBytes);
         }
         uint32_t lo[kXNodes], hi[kXNodes];
 #pragma unroll
@@ -445,14 +460,20 @@ k_spread_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
         }
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-          // sum_t D_t 256^-t: here K is up to 2048 nodes, |D_t| < 6 2^25, so the
-          // int32 pairs of combine6 would overflow -- each diagonal converts on
-          // its own (exact int32 -> fp64 magic, no I2F)
-          double acc = 0.0;
-#pragma unroll
-          for (int t = kSl - 1; t >= 0; --t) acc = fma(acc, 0.00390625, i2d(dv[t][i]));
+          // sum_t D_t 256^-t: K is up to 2048 nodes here, |D_t| < 6 2^25, so
+          // the int32 pairs of the gather's combine would overflow; the two
+          // triples D0 2^16 + D1 2^8 + D2 and D3 2^16 + ... (|.| < 2^43) are
+          // formed exactly in int64 and convert by the magic number (2 DADD
+          // instead of 6 conversions), then one FMA: acc = (hi + lo 2^-24) 2^-16
+          const long long h3 = (long long)(int32_t)dv[0][i] * 65536 +
+                               (long long)(int32_t)dv[1][i] * 256 + (long long)(int32_t)dv[2][i];
+          const long long l3 = (long long)(int32_t)dv[3][i] * 65536 +
+                               (long long)(int32_t)dv[4][i] * 256 + (long long)(int32_t)dv[5][i];
+          const double hd = __longlong_as_double(h3 + 0x4338000000000000LL) - 6755399441055744.0;
+          const double ld = __longlong_as_double(l3 + 0x4338000000000000LL) - 6755399441055744.0;
+          const double acc = fma(ld, 5.9604644775390625e-08, hd);   // x 2^-16 in the scale
           const int bc = c0 + i;
-          bo[(int64_t)bc * nrhs] = acc * rs * pow2(eb[bc >> 3] + ec[bc & 7] + 34);
+          bo[(int64_t)bc * nrhs] = acc * rs * pow2(eb[bc >> 3] + ec[bc & 7] + 34 - 16);
         }
       }
     }
