@@ -383,6 +383,7 @@ k_spread_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
           }
           store8(lo, hi, sYop + st * kYOpBytes + canon32(yn, yq * 8), kBBytes);
         }
+        OZW(25, (void)0);   // Y digits cut
         uint32_t lo[kXNodes], hi[kXNodes];
 #pragma unroll
         for (int i = 0; i < kXNodes; ++i) {
@@ -407,7 +408,8 @@ k_spread_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
           else
             umma::tmem_st2(xt + (uint32_t)(p * 8), w4[0][p], w4[1 % (kXNodes / 4)][p]);
         }
-        umma::tmem_wait_st();
+        OZW(26, (void)0);   // X digits issued to TMEM
+        OZW(27, umma::tmem_wait_st());
         umma::fence_before();
         umma::fence_async_smem();
         __syncwarp();
