@@ -112,7 +112,7 @@ static_assert(kSl == 6, "six digit slices");
 // successor prefetched into L2) and two Y stages (the slicers cut tile t+1
 // while tile t's copy is still in use)
 #ifndef NLD_GNM_GBUF
-#define NLD_GNM_GBUF 1
+#define NLD_GNM_GBUF 2
 #endif
 constexpr int kGBuf = NLD_GNM_GBUF;
 constexpr int kYBuf = kGBuf == 1 ? 2 : 1;
