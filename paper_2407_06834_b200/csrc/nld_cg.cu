@@ -180,13 +180,17 @@ k_cg_reduce(CgPtr c, const RhsScal* __restrict__ sc, const double* __restrict__ 
 }
 
 __global__ void k_final(const double* __restrict__ part, int nblk, double* __restrict__ out) {
-  // one thread per (rhs, k): sequential sum over blocks -> deterministic
+  // one warp per (rhs, k): lane l sums blocks l, l + 32, ... in order, then a
+  // fixed shuffle tree -- deterministic, and 32 loads in flight instead of a
+  // chain of nblk dependent ones
   const int rhs = blockIdx.x;
-  const int k = threadIdx.x;
+  const int k = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (k >= kMaxK) return;
   double s = 0.0;
-  for (int b = 0; b < nblk; ++b) s += part[((int64_t)rhs * nblk + b) * kMaxK + k];
-  out[rhs * kMaxK + k] = s;
+  for (int b = lane; b < nblk; b += 32) s += part[((int64_t)rhs * nblk + b) * kMaxK + k];
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+  if (lane == 0) out[rhs * kMaxK + k] = s;
 }
 
 // elementwise kernels over the N * nrhs pixel-major elements
@@ -300,7 +304,7 @@ struct Reducer {
                                  const double* vecA = nullptr) {
     k_cg_reduce<MODE><<<nblk, kRT, 0, st>>>(c, sc, vecA, part);
     NLD_CUDA(cudaGetLastError());
-    k_final<<<nrhs, 32, 0, st>>>(part, nblk, out);
+    k_final<<<nrhs, 32 * kMaxK, 0, st>>>(part, nblk, out);
     // sharded: the per-rank partial scalars are summed on the device, on the
     // stream (NCCL), before the one host read the solver's decisions need
     comm_device(op, out, (int64_t)nrhs * kMaxK, st);
@@ -432,7 +436,7 @@ double dev_dot(const double* x, const double* y, int64_t n, cudaStream_t st) {
   NLD_CUDA(cudaMallocAsync(&part, sizeof(double) * nblk * kMaxK, st));
   NLD_CUDA(cudaMallocAsync(&out, sizeof(double) * kMaxK, st));
   k_dot_part<<<nblk, kRT, 0, st>>>(x, y, n, part);
-  k_final<<<1, 32, 0, st>>>(part, nblk, out);
+  k_final<<<1, 32 * kMaxK, 0, st>>>(part, nblk, out);
   double h[kMaxK];
   NLD_CUDA(cudaMemcpyAsync(h, out, sizeof(double) * kMaxK, cudaMemcpyDeviceToHost, st));
   cudaFreeAsync(part, st);
