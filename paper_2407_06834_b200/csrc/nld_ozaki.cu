@@ -147,6 +147,11 @@ constexpr int kSlcWarps = NLD_SPR_SLC;
 constexpr int kSlicers = 32 * kSlcWarps;
 constexpr int kXNodes = 32 * 128 / kSlicers;     // X: nodes per thread (16 or 8)
 static_assert(kSlcWarps == 8 || kSlcWarps == 16, "slicer warps");
+#ifndef NLD_SPR_Y16
+#define NLD_SPR_Y16 1
+#endif
+// 8 slicer warps: Y on warps 0-3 with 16-byte stores, X split 8 / 24 nodes
+constexpr bool kY16 = NLD_SPR_Y16 != 0;
 constexpr int kIssuerWarp = kSlcWarps;
 constexpr int kLoaderWarp = kSlcWarps + 1;       // first of kLoaders loader warps
 constexpr int kLoaders = NLD_SPR_LD;
@@ -348,65 +353,125 @@ k_spread_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
           }
           continue;
         }
-        if (kSlcWarps == 16) {
-          // Y digits of 4 nodes for row (b, c): K-major canonical, zero past cn
-          const int kn = (warp >> 3) * 16 + (lane >> 3) * 4;
-          uint32_t lo[4], hi[4];
+        if (kSlcWarps == 8 && kY16) {
+          // Y on warps 0-3: thread = row (b, c) x 16 nodes, one 16-byte store
+          // per digit slice -- a warp's 32 rows fill whole 128-byte lines
+          // (conflict-free; 8-node 8-byte stores were 4-way conflicted)
+          if (warp < 4) {
+            const int kn = (warp >> 1) * 16;
+            uint32_t lo[16], hi[16];
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const int j = kn + i;
-            double x = 0.0, y = 0.0;
-            if (j < cn) {
-              x = R[j * 24 + 8 + yb] * sy;
-              y = R[j * 24 + 16 + yc];
+            for (int i = 0; i < 16; ++i) {
+              const int j = kn + i;
+              double x = 0.0, y = 0.0;
+              if (j < cn) {
+                x = R[j * 24 + 8 + yb] * sy;
+                y = R[j * 24 + 16 + yc];
+              }
+              slice1(x, y, lo[i], hi[i]);
             }
-            slice1(x, y, lo[i], hi[i]);
+            store16(lo, hi, sYop + st * kYOpBytes + canon32(yn, kn), kBBytes);
           }
-          uint32_t w6[6];
-          pack4(lo, hi, w6);
-          uint8_t* yd = sYop + st * kYOpBytes + canon32(yn, kn);
+          OZW(25, (void)0);   // Y digits cut
+          // X: warps 0-3 nodes 0..7, warps 4-7 nodes 8..31 (24 values per
+          // thread on every slicer warp), in blocks of 8 nodes
+          const int nb0 = warp < 4 ? 0 : 8, nblk = warp < 4 ? 1 : 3;
+          const uint32_t xt = tmem + ((uint32_t)((m >> 5) * 32) << 16) +
+                              (uint32_t)(kXTmem0 + st * kSl * 8);
 #pragma unroll
-          for (int p = 0; p < kSl; ++p) *reinterpret_cast<uint32_t*>(yd + p * kBBytes) = w6[p];
+          for (int bk = 0; bk < 3; ++bk) {
+            if (bk >= nblk) break;
+            const int n0 = nb0 + bk * 8;
+            uint32_t lo[8], hi[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const int j = n0 + i;
+              double x = 0.0, y = 0.0;
+              if (j < cn) {
+                x = Vr[j * 16 + r];
+                y = R[j * 24 + a] * sx;
+              }
+              slice1(x, y, lo[i], hi[i]);
+            }
+            uint32_t w0[6], w1[6];
+            pack4(lo, hi, w0);
+            pack4(lo + 4, hi + 4, w1);
+#pragma unroll
+            for (int p = 0; p < kSl; ++p)
+              umma::tmem_st2(xt + (uint32_t)(p * 8 + n0 / 4), w0[p], w1[p]);
+          }
         } else {
-          // Y digits of 8 nodes for row (b, c)
-          const int yq = tid >> 6;
-          uint32_t lo[8], hi[8];
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const int j = yq * 8 + i;
+          if (kSlcWarps == 16) {
+            // Y digits of 4 nodes for row (b, c): K-major canonical, zero past cn
+            const int kn = (warp >> 3) * 16 + (lane >> 3) * 4;
+            uint32_t lo[4], hi[4];
+  #pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const int j = kn + i;
+              double x = 0.0, y = 0.0;
+              if (j < cn) {
+                x = R[j * 24 + 8 + yb] * sy;
+                y = R[j * 24 + 16 + yc];
+              }
+              slice1(x, y, lo[i], hi[i]);
+            }
+            uint32_t w6[6];
+            pack4(lo, hi, w6);
+            uint8_t* yd = sYop + st * kYOpBytes + canon32(yn, kn);
+  #pragma unroll
+            for (int p = 0; p < kSl; ++p) *reinterpret_cast<uint32_t*>(yd + p * kBBytes) = w6[p];
+          } else {
+            // Y digits of 8 nodes for row (b, c)
+            const int yq = tid >> 6;
+            uint32_t lo[8], hi[8];
+  #pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const int j = yq * 8 + i;
+              double x = 0.0, y = 0.0;
+              if (j < cn) {
+  #ifdef NLD_EXP_SPR_NODMUL
+                x = R[j * 24 + 8 + yb];
+  #else
+                x = R[j * 24 + 8 + yb] * sy;
+  #endif
+                y = R[j * 24 + 16 + yc];
+              }
+              slice1(x, y, lo[i], hi[i]);
+            }
+  #ifdef NLD_EXP_SPR_NOYSTS
+            if (lo[0] == 0x12345u && hi[7] == 0x777u)
+  #endif
+            store8(lo, hi, sYop + st * kYOpBytes + canon32(yn, yq * 8), kBBytes);
+          }
+          OZW(25, (void)0);   // Y digits cut
+          uint32_t lo[kXNodes], hi[kXNodes];
+  #pragma unroll
+          for (int i = 0; i < kXNodes; ++i) {
+            const int j = h * kXNodes + i;
             double x = 0.0, y = 0.0;
             if (j < cn) {
-              x = R[j * 24 + 8 + yb] * sy;
-              y = R[j * 24 + 16 + yc];
+              x = Vr[j * 16 + r];
+  #ifdef NLD_EXP_SPR_NODMUL
+              y = R[j * 24 + a];
+  #else
+              y = R[j * 24 + a] * sx;
+  #endif
             }
             slice1(x, y, lo[i], hi[i]);
           }
-          store8(lo, hi, sYop + st * kYOpBytes + canon32(yn, yq * 8), kBBytes);
-        }
-        OZW(25, (void)0);   // Y digits cut
-        uint32_t lo[kXNodes], hi[kXNodes];
-#pragma unroll
-        for (int i = 0; i < kXNodes; ++i) {
-          const int j = h * kXNodes + i;
-          double x = 0.0, y = 0.0;
-          if (j < cn) {
-            x = Vr[j * 16 + r];
-            y = R[j * 24 + a] * sx;
+          uint32_t w4[kXNodes / 4][6];
+  #pragma unroll
+          for (int g4 = 0; g4 < kXNodes / 4; ++g4) pack4(lo + 4 * g4, hi + 4 * g4, w4[g4]);
+          const uint32_t xt = tmem + ((uint32_t)((m >> 5) * 32) << 16) +
+                              (uint32_t)(kXTmem0 + st * kSl * 8 + h * (kXNodes / 4));
+  #pragma unroll
+          for (int p = 0; p < kSl; ++p) {
+            if (kXNodes == 16)
+              umma::tmem_st4(xt + (uint32_t)(p * 8), w4[0][p], w4[1 % (kXNodes / 4)][p],
+                             w4[2 % (kXNodes / 4)][p], w4[3 % (kXNodes / 4)][p]);
+            else
+              umma::tmem_st2(xt + (uint32_t)(p * 8), w4[0][p], w4[1 % (kXNodes / 4)][p]);
           }
-          slice1(x, y, lo[i], hi[i]);
-        }
-        uint32_t w4[kXNodes / 4][6];
-#pragma unroll
-        for (int g4 = 0; g4 < kXNodes / 4; ++g4) pack4(lo + 4 * g4, hi + 4 * g4, w4[g4]);
-        const uint32_t xt = tmem + ((uint32_t)((m >> 5) * 32) << 16) +
-                            (uint32_t)(kXTmem0 + st * kSl * 8 + h * (kXNodes / 4));
-#pragma unroll
-        for (int p = 0; p < kSl; ++p) {
-          if (kXNodes == 16)
-            umma::tmem_st4(xt + (uint32_t)(p * 8), w4[0][p], w4[1 % (kXNodes / 4)][p],
-                           w4[2 % (kXNodes / 4)][p], w4[3 % (kXNodes / 4)][p]);
-          else
-            umma::tmem_st2(xt + (uint32_t)(p * 8), w4[0][p], w4[1 % (kXNodes / 4)][p]);
         }
         OZW(26, (void)0);   // X digits issued to TMEM
         OZW(27, umma::tmem_wait_st());

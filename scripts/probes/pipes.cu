@@ -22,6 +22,8 @@ __global__ void k_probe(const int* in, double* out) {
       if (K == 4) { acc[i] += __hiloint2double(0x43300000, x[i] ^ 0x80000000) - 4503601774854144.0; x[i] += 3; }
       if (K == 5) { x[i] = x[i] * 257 + 3; }                               // IMAD
       if (K == 6) { acc[i] += (double)(float)x[i]; x[i] += 3; }           // I2F.F32 + F2F.F64
+      if (K == 7) acc[i] = acc[i] * 1.0000001;                            // DMUL
+      if (K == 8) { x[i] = __byte_perm(x[i], x[i + 1 & 7], 0x5140) ^ 0x80808080; }  // PRMT+LOP
     }
   }
   double s = 0.0;
@@ -59,5 +61,7 @@ int main() {
   run<4>("magic i2d (LOP,MOV,DADD x2)", 1);
   run<5>("IMAD", 1);
   run<6>("I2F.F32+F2F.F64 (+DADD)", 1);
+  run<7>("DMUL", 1);
+  run<8>("PRMT+LOP", 2);
   return 0;
 }
