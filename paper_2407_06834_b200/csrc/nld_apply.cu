@@ -1368,7 +1368,8 @@ void to_rhs_major(const double* vt, int64_t n, int nrhs, double* out, int64_t ld
 
 void apply_op(nld_operator* op, int which, int kind, const double* v, double* out,
               int nrhs, int64_t ld, const double* coef_dev, const double* eta,
-              cudaStream_t st, int pixel_major) {
+              cudaStream_t st, int pixel_major, const unsigned long long* vmax_pre,
+              const double* flag_pre) {
   const PlanSet& ps = op->sets[which];
   ensure_workspace(op, ps, nrhs);
   if (use_ozaki() && op->params.cutoff == 4)
@@ -1388,7 +1389,14 @@ void apply_op(nld_operator* op, int which, int kind, const double* v, double* ou
   }
   const bool sliced = use_ozaki() && op->params.cutoff == 4 && nrhs % 16 == 0;
   double* const flags = ws.grid_in + ps.grid_total * nrhs;
-  if (sliced) {
+  if (sliced && vmax_pre && vt == v) {
+    // the caller's kernel that wrote v also took its per-rhs max |v| and
+    // non-finite flags (CG: the direction update), saving k_vmax's pass
+    NLD_CUDA(cudaMemcpyAsync(ws.vmax, vmax_pre, sizeof(unsigned long long) * nrhs,
+                             cudaMemcpyDeviceToDevice, st));
+    NLD_CUDA(cudaMemcpyAsync(flags, flag_pre, sizeof(double) * nrhs, cudaMemcpyDeviceToDevice,
+                             st));
+  } else if (sliced) {
     ozaki_vmax(vt, N, nrhs, ws.vmax, flags, st);
     launches += 1;   // k_vmax (its resets are memsets, not kernels)
   }

@@ -58,6 +58,8 @@ struct CgPtr {
   int L;
   int prec;
   int deflate;
+  unsigned long long* pmax;   // per-rhs max |p| bit pattern (direction update), or null
+  double* pflag;              // per-rhs non-finite flag of p
 };
 
 __device__ __forceinline__ double dinv_at(const CgPtr& c, const RhsScal& s, int64_t i) {
@@ -214,39 +216,63 @@ __global__ void k_cg_resid0(CgPtr c, const RhsScal* __restrict__ sc, int warm) {
     c.r[e] = warm ? c.b[e] - (c.q[e] - sc[e % c.nrhs].mq) : c.b[e];
 }
 
-__global__ void k_cg_direction(CgPtr c, const RhsScal* __restrict__ sc, int first) {
+__global__ void __launch_bounds__(256) k_cg_direction(CgPtr c, const RhsScal* __restrict__ sc,
+                                                      int first) {
   // z = Pi(D^-1 r) (or r), p = z + beta p.  Thread layout as in k_cg_reduce:
   // a fixed rhs per thread (its scalars in registers), pixels strided, four
-  // pixels' loads in flight per step
+  // pixels' loads in flight per step.  With c.pmax the kernel also takes the
+  // per-rhs max |p| (bit patterns: NaN > Inf > finite, as k_vmax) of the
+  // whole new p -- inactive rhs keep their p and only read it -- so the next
+  // product skips its own pass over p.
   const int nr = c.nrhs;
   const int grp = blockDim.x / nr;
-  if ((int)threadIdx.x >= grp * nr) return;
-  const int r = threadIdx.x % nr, g = threadIdx.x / nr;
+  const bool live = (int)threadIdx.x < grp * nr;
+  const int r = live ? threadIdx.x % nr : 0, g = threadIdx.x / nr;
   const RhsScal s = sc[r];
-  if (!s.active) return;
-  const int64_t stride = (int64_t)gridDim.x * grp;
-  const bool jac = c.prec == NLD_PREC_JACOBI;
-  auto one = [&](int64_t i, double rv, double pv, double ev) {
-    const double di = jac ? __drcp_rn(s.lam + s.mu * ev) : dinv_at(c, s, i);
-    const double z = (c.prec == NLD_PREC_NONE) ? rv : di * rv - s.mz;
-    c.p[i * nr + r] = first ? z : z + s.beta * pv;
-  };
-  int64_t i = blockIdx.x * (int64_t)grp + g;
-  for (; i + 3 * stride < c.N; i += 4 * stride) {
-    double rv[4], pv[4], ev[4];
+  const bool act = live && s.active;
+  const bool want_max = c.pmax != nullptr;
+  unsigned long long mx = 0ull;
+  if (act || (live && want_max)) {
+    const int64_t stride = (int64_t)gridDim.x * grp;
+    const bool jac = c.prec == NLD_PREC_JACOBI;
+    auto one = [&](int64_t i, double rv, double pv, double ev) {
+      double pn = pv;
+      if (act) {
+        const double di = jac ? __drcp_rn(s.lam + s.mu * ev) : dinv_at(c, s, i);
+        const double z = (c.prec == NLD_PREC_NONE) ? rv : di * rv - s.mz;
+        pn = first ? z : z + s.beta * pv;
+        c.p[i * nr + r] = pn;
+      }
+      mx = max(mx, (unsigned long long)__double_as_longlong(pn) & 0x7fffffffffffffffull);
+    };
+    const bool rd_p = !act || !first;
+    int64_t i = blockIdx.x * (int64_t)grp + g;
+    for (; i + 3 * stride < c.N; i += 4 * stride) {
+      double rv[4], pv[4], ev[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int64_t e = (i + u * stride) * nr + r;
-      rv[u] = c.r[e];
-      pv[u] = first ? 0.0 : c.p[e];
-      ev[u] = jac ? c.eta[i + u * stride] : 0.0;
+      for (int u = 0; u < 4; ++u) {
+        const int64_t e = (i + u * stride) * nr + r;
+        rv[u] = act ? c.r[e] : 0.0;
+        pv[u] = rd_p ? c.p[e] : 0.0;
+        ev[u] = (act && jac) ? c.eta[i + u * stride] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) one(i + u * stride, rv[u], pv[u], ev[u]);
     }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) one(i + u * stride, rv[u], pv[u], ev[u]);
+    for (; i < c.N; i += stride) {
+      const int64_t e = i * nr + r;
+      one(i, act ? c.r[e] : 0.0, rd_p ? c.p[e] : 0.0, (act && jac) ? c.eta[i] : 0.0);
+    }
   }
-  for (; i < c.N; i += stride) {
-    const int64_t e = i * nr + r;
-    one(i, c.r[e], first ? 0.0 : c.p[e], jac ? c.eta[i] : 0.0);
+  if (!want_max) return;
+  __shared__ unsigned long long shm[256];
+  shm[threadIdx.x] = mx;
+  __syncthreads();
+  if ((int)threadIdx.x < nr) {
+    unsigned long long m = 0ull;
+    for (int j = 0; j < grp; ++j) m = max(m, shm[j * nr + threadIdx.x]);
+    if (m) atomicMax(&c.pmax[threadIdx.x], m);
+    if (m >= 0x7ff0000000000000ull) c.pflag[threadIdx.x] = 1.0;
   }
 }
 
@@ -588,15 +614,31 @@ void cg_solve(nld_operator* op, const double* f, double* u, int nrhs, int64_t ld
     NLD_CUDA(cudaMemcpyAsync(scd, sc.data(), sizeof(RhsScal) * nrhs, cudaMemcpyHostToDevice,
                              st));
   };
-  auto matvec = [&](const double* in, double* out) {   // pixel-major in/out
+  // per-rhs max |p| and non-finite flags, taken by the direction update for
+  // the next product (which then skips its own pass over p)
+  if (nrhs % 16 == 0 && op->params.mode != 1 && op->params.cutoff == 4) {
+    c.pmax = scratch.alloc<unsigned long long>(nrhs);
+    c.pflag = scratch.alloc<double>(nrhs);
+  }
+  auto matvec = [&](const double* in, double* out, bool p_max = false) {   // pixel-major in/out
     if (op->params.mode == 1)
       dense_apply(op, 0, NLD_APPLY_SYSTEM, in, out, nrhs, N, coef, eta, st, 1);
+    else if (p_max && c.pmax)
+      apply_op(op, 0, NLD_APPLY_SYSTEM, in, out, nrhs, N, coef, eta, st, 1, c.pmax, c.pflag);
     else
       apply_op(op, 0, NLD_APPLY_SYSTEM, in, out, nrhs, N, coef, eta, st, 1);
   };
   const double dN = (double)op->N_global;
   Reducer red(op, nrhs, N, st);
   const int eg = eblocks(N * nrhs);
+  auto direction = [&](int first) {
+    if (c.pmax) {
+      NLD_CUDA(cudaMemsetAsync(c.pmax, 0, sizeof(unsigned long long) * nrhs, st));
+      NLD_CUDA(cudaMemsetAsync(c.pflag, 0, sizeof(double) * nrhs, st));
+    }
+    k_cg_direction<<<eg, 256, 0, st>>>(c, scd, first);
+    NLD_CUDA(cudaGetLastError());
+  };
 
   std::vector<std::vector<double>> H(nrhs);
   std::vector<double> bnorm(nrhs, 0.0), rz(nrhs, 0.0);
@@ -664,8 +706,7 @@ void cg_solve(nld_operator* op, const double* f, double* u, int nrhs, int64_t ld
   }
   for (int r = 0; r < nrhs; ++r) sc[r].active = done[r] ? 0 : 1;
   push();
-  k_cg_direction<<<eg, 256, 0, st>>>(c, scd, 1);
-  NLD_CUDA(cudaGetLastError());
+  direction(1);
 
   auto any_active = [&]() {
     for (int r = 0; r < nrhs; ++r)
@@ -711,7 +752,7 @@ void cg_solve(nld_operator* op, const double* f, double* u, int nrhs, int64_t ld
       NLD_CUDA(cudaGetLastError());
       matvec(c.t, c.q);
     } else {
-      matvec(c.p, c.q);
+      matvec(c.p, c.q, true);
     }
     auto hpq = red.run<RED_PQ>(c, scd);
     if (pend) {
@@ -758,9 +799,8 @@ void cg_solve(nld_operator* op, const double* f, double* u, int nrhs, int64_t ld
           sc[r].sel = 2;
         }
         push();
-        k_cg_direction<<<eg, 256, 0, st>>>(c, scd, 0);
-        NLD_CUDA(cudaGetLastError());
-        matvec(c.p, c.t);
+        direction(0);
+        matvec(c.p, c.t, true);
         k_cg_colsel<<<kRB, kRT, 0, st>>>(c, scd, 1);
         NLD_CUDA(cudaGetLastError());
         for (int r = 0; r < nrhs; ++r) sc[r].active = keep[r];
@@ -812,8 +852,7 @@ void cg_solve(nld_operator* op, const double* f, double* u, int nrhs, int64_t ld
       if (it[r] >= maxit) hit_max[r] = 1;
     }
     push();
-    k_cg_direction<<<eg, 256, 0, st>>>(c, scd, 0);
-    NLD_CUDA(cudaGetLastError());
+    direction(0);
     bool any_max = false;
     for (int r = 0; r < nrhs; ++r) any_max |= hit_max[r] != 0;
     if (any_max) {
@@ -854,8 +893,7 @@ void cg_solve(nld_operator* op, const double* f, double* u, int nrhs, int64_t ld
       if (rel_dir) {
         for (int r = 0; r < nrhs; ++r) sc[r].active = (sc[r].sel == 3) ? 1 : 0;
         push();
-        k_cg_direction<<<eg, 256, 0, st>>>(c, scd, 0);
-        NLD_CUDA(cudaGetLastError());
+        direction(0);
         for (int r = 0; r < nrhs; ++r) {
           sc[r].active = keep[r];
           sc[r].sel = 0;

@@ -235,7 +235,8 @@ void free_workspace(Workspace& ws);
 // one fused operator application (all windows, nrhs right-hand sides)
 void apply_op(nld_operator* op, int which, int kind, const double* v,
               double* out, int nrhs, int64_t ld, const double* coef_dev,
-              const double* eta, cudaStream_t st, int pixel_major = 0);
+              const double* eta, cudaStream_t st, int pixel_major = 0,
+              const unsigned long long* vmax_pre = nullptr, const double* flag_pre = nullptr);
 
 // the two halves of a product, reused by the NFFT transform API
 int spread_stage(nld_operator* op, const PlanSet& ps, const double* vt, int nrhs,
