@@ -1405,7 +1405,11 @@ void apply_op(nld_operator* op, int which, int kind, const double* v, double* ou
   // fused gather epilogue (see gather_window): every window on the DMMA
   // gather, pixel-major in/out, out not aliasing v
   const int no_fuse = ab_switch("NLD_NO_FUSED_EPILOGUE", 0);
-  bool fused = !no_fuse && pixel_major && nrhs >= 8 && L >= 2 && out != v &&
+  // (the sliced gather reads and writes the caller's v / out lines with
+  // 32-byte accesses: unaligned buffers take the unfused path through the
+  // aligned workspace)
+  const bool al32 = ((reinterpret_cast<uintptr_t>(out) | reinterpret_cast<uintptr_t>(v)) & 31) == 0;
+  bool fused = !no_fuse && pixel_major && nrhs >= 8 && L >= 2 && out != v && al32 &&
                op->params.cutoff == 4 && use_mma();
   // gather order: 1-/2-D windows first, then the 3-D ones (the last of which
   // applies the epilogue); every window on a fast path with subproblems

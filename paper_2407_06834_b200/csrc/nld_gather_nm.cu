@@ -407,28 +407,30 @@ k_gather_nm(const SubDev* __restrict__ subs, const int32_t* __restrict__ order, 
         eBm = max(eBm, (int)ex[8 + q]);
         eCm = max(eCm, (int)ex[16 + q]);
       }
-      const double syB = pow2(46 - eBm), syC = pow2(-eCm);
+      // the scale 2^(46 - eBm - eCm) rides in the slicing constant (slice1m)
+      const double mgy = kMagic * (pow2(eBm - 46) * pow2(eCm));
       const int ntile = (cnt + kT - 1) / kT;
       for (int tl = 0; tl < ntile; ++tl, ++gt) {
         const int s = gt % kRawStages;
         OZW(16, umma::mbar_wait(&raw_full[s], (gt / kRawStages) & 1));
-        const bool ok = tl * kT + m < cnt;
         const double* R = reinterpret_cast<const double*>(sRaw + s * kRawBytes + m * kRowBytes);
-        // this thread's b = b0 .. b0 + 2 kKqPer - 1 and all eight c
+        // this thread's b = b0 .. b0 + 2 kKqPer - 1 and all eight c.  Rows past
+        // the subproblem's end hold stale rows: their digits only reach their
+        // own accumulator lanes, which the epilogue drops (px < 0).
         double bb[2 * kKqPer], cc[8];
 #pragma unroll
         for (int i = 0; i < kKqPer; ++i) {
-          const double2 x = (ok && !(xf & 2048)) ? reinterpret_cast<const double2*>(R + 8 + b0)[i]
-                                                 : make_double2(1.0, 0.0);
-          bb[2 * i] = x.x * syB;
-          bb[2 * i + 1] = x.y * syB;
+          const double2 x = !(xf & 2048) ? reinterpret_cast<const double2*>(R + 8 + b0)[i]
+                                         : make_double2(1.0, 0.0);
+          bb[2 * i] = x.x;
+          bb[2 * i + 1] = x.y;
         }
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-          const double2 y = (ok && !(xf & 2048)) ? reinterpret_cast<const double2*>(R + 16)[i]
-                                                 : make_double2(0.5, 0.0);
-          cc[2 * i] = y.x * syC;
-          cc[2 * i + 1] = y.y * syC;
+          const double2 y = !(xf & 2048) ? reinterpret_cast<const double2*>(R + 16)[i]
+                                         : make_double2(0.5, 0.0);
+          cc[2 * i] = y.x;
+          cc[2 * i + 1] = y.y;
         }
         release_after_loads(&raw_empty[s], lane, 0, make_double2(bb[0], cc[7]),
                             make_double2(bb[2 * kKqPer - 1], cc[0]), make_double2(bb[1], cc[3]),
@@ -442,7 +444,7 @@ k_gather_nm(const SubDev* __restrict__ subs, const int32_t* __restrict__ order, 
           if (xf & 4) break;
           uint32_t lo[16], hi[16];
 #pragma unroll
-          for (int i = 0; i < 16; ++i) slice1(bb[2 * kk + (i >> 3)], cc[i & 7], lo[i], hi[i]);
+          for (int i = 0; i < 16; ++i) slice1m(bb[2 * kk + (i >> 3)], cc[i & 7], mgy, lo[i], hi[i]);
           store16(lo, hi, sY + ys * kYBytes + canon64(m, (kq0 + kk) * 16), kYSlice);
         }
         umma::fence_async_smem();
@@ -509,11 +511,7 @@ k_gather_nm(const SubDev* __restrict__ subs, const int32_t* __restrict__ order, 
 #pragma unroll
         for (int j = 0; j < kSPW; ++j) {
           s01[j] = s23[j] = v01[j] = v23[j] = make_double2(0.0, 0.0);
-          if (ok && MODE >= mma::kGatherAccum && !(xf & 128)) {
-            const double2* o2 = reinterpret_cast<const double2*>(out + e + 4 * j);
-            s01[j] = o2[0];
-            s23[j] = o2[1];
-          }
+          if (ok && MODE >= mma::kGatherAccum && !(xf & 128)) ldg256(out + e + 4 * j, s01[j], s23[j]);
         }
         double et = 0.0;
 #pragma unroll
@@ -522,9 +520,7 @@ k_gather_nm(const SubDev* __restrict__ subs, const int32_t* __restrict__ order, 
           if (MODE == mma::kGatherFinal && ps == 2 && ok && !(xf & 128)) {
 #pragma unroll
             for (int j = 0; j < kSPW; ++j) {
-              const double2* vv = reinterpret_cast<const double2*>(ep.v + e + 4 * j);
-              v01[j] = vv[0];
-              v23[j] = vv[1];
+              ldg256(ep.v + e + 4 * j, v01[j], v23[j]);
             }
             if (need_eta) et = ep.eta[px];
           }
@@ -650,9 +646,7 @@ k_gather_nm(const SubDev* __restrict__ subs, const int32_t* __restrict__ order, 
               res[i] = mma::epi_value_r(ep.kind, (double)ep.L, inv_L, sv[i], vx[i], et, lm.x, lm.y);
             }
           }
-          double2* o2 = reinterpret_cast<double2*>(out + e + 4 * j);
-          o2[0] = make_double2(res[0], res[1]);
-          o2[1] = make_double2(res[2], res[3]);
+          stg256(out + e + 4 * j, make_double2(res[0], res[1]), make_double2(res[2], res[3]));
         }
         OZW(21, (void)0);
       }

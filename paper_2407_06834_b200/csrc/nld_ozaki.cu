@@ -133,25 +133,16 @@ constexpr int kYOpBytes = kSl * kBBytes;         // 12 KB of Y digits per chunk
 __host__ __device__ constexpr int spread_oz_py_smem() {
   return kPyRawStages * kPyRawBytes + kOpStages * kYOpBytes;
 }
-#ifndef NLD_SPR_SLC
-#define NLD_SPR_SLC 8
-#endif
 #ifndef NLD_SPR_LD
 #define NLD_SPR_LD 4
 #endif
 // Slicer warps: cutting a chunk's X = v A (4096 values) and Y = B C (2048)
-// digits is a latency-bound chain (LDS, DMUL, DFMA, byte transposes, TMEM /
-// shared stores) and was the spread's critical path with 8 warps (~2k cycles
-// per chunk against ~0.7k of UMMA work): 16 warps cut 12 values per thread.
-constexpr int kSlcWarps = NLD_SPR_SLC;
+// digits is a latency-bound chain (LDS, DFMA, byte transposes, TMEM / shared
+// stores) and the spread's critical path: 8 warps, 24 values per thread --
+// warps 0-3 cut Y (16 nodes of one (b, c) row each) and X of nodes 0..7,
+// warps 4-7 X of nodes 8..31.
+constexpr int kSlcWarps = 8;
 constexpr int kSlicers = 32 * kSlcWarps;
-constexpr int kXNodes = 32 * 128 / kSlicers;     // X: nodes per thread (16 or 8)
-static_assert(kSlcWarps == 8 || kSlcWarps == 16, "slicer warps");
-#ifndef NLD_SPR_Y16
-#define NLD_SPR_Y16 1
-#endif
-// 8 slicer warps: Y on warps 0-3 with 16-byte stores, X split 8 / 24 nodes
-constexpr bool kY16 = NLD_SPR_Y16 != 0;
 constexpr int kIssuerWarp = kSlcWarps;
 constexpr int kLoaderWarp = kSlcWarps + 1;       // first of kLoaders loader warps
 constexpr int kLoaders = NLD_SPR_LD;
@@ -210,6 +201,12 @@ k_spread_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
   };
 
   if (warp == 0) umma::tmem_alloc<kTmemCols>(&taddr_s);
+  // the raw stages start zeroed: the slicers cut whole 32-node chunks without
+  // tail predicates, so a row slot no copy has written yet must hold finite
+  // values (later ones hold an earlier chunk's rows)
+  for (int i = tid; i < RS * RB / 16; i += kSPThreads)
+    reinterpret_cast<uint4*>(raw)[i] = make_uint4(0u, 0u, 0u, 0u);
+  umma::fence_async_smem();
   if (tid == 32) {
     for (int k = 0; k < RS; ++k) {
       umma::mbar_init(&raw_full[k], 33);                  // 32 noinc cp.async + the bulk copy
@@ -271,10 +268,12 @@ k_spread_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
         for (int q = 0; q < 8; ++q) {
           const int nd = q * 4 + (lane >> 3), pc = lane & 7;
           const int32_t pxn = __shfl_sync(0xffffffffu, px, nd);
-          if (nd < cn)
-            cp_async16(dst + kPyA + nd * 128 + pc * 16,
-                       vt + (int64_t)(uint32_t)((xf & 8) ? (sd.start + j0 + nd) & ((1 << 24) - 1) : pxn) *
-                                nrhs + rg + 2 * pc);
+          // past the tail (nd >= cn: px = 0 above) the line is zero-filled: X = v A
+          // of a missing node is then exactly zero whatever stale row it meets
+          cp_async16_zfill(dst + kPyA + nd * 128 + pc * 16,
+                           vt + (int64_t)(uint32_t)((xf & 8) ? (sd.start + j0 + nd) & ((1 << 24) - 1) : pxn) *
+                                    nrhs + rg + 2 * pc,
+                           nd < cn ? 16u : 0u);
         }
         cp_async_mbar_arrive(&raw_full[s]);
         px = px_next;
@@ -314,15 +313,12 @@ k_spread_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
     }
   } else if (warp < kIssuerWarp) {
     // --------------------------------------------------------------- slicers
-    // X: thread = TMEM lane m = (a, r) of its warp's lane quarter, kXNodes
-    // nodes h kXNodes .. ; Y with 8 slicer warps: a warp covers 32 rows (b, c)
-    // x 8 nodes, a lane one row and 8 nodes (the node of each load is
-    // warp-uniform: conflict-free loads, 8-byte digit stores); with 16: a warp
-    // covers 8 rows x 16 nodes, a lane one row and 4 nodes (conflict-free
-    // 4-byte stores)
-    const int m = (warp & 3) * 32 + lane, h = warp >> 2;
+    // X: thread = TMEM lane m = (a, r) of its warp's lane quarter; Y (warps
+    // 0-3): thread = row (b, c), the node of each load warp-uniform
+    // (conflict-free loads, 16-byte digit stores)
+    const int m = (warp & 3) * 32 + lane;
     const int a = m >> 4, r = m & 15;
-    const int yn = kSlcWarps == 16 ? (warp & 7) * 8 + (lane & 7) : tid & 63;   // Y row (b, c)
+    const int yn = tid & 63;   // Y row (b, c)
     const int yb = yn >> 3, yc = yn & 7;
     int g = 0;
     for (int k = 0; k < nitems; ++k) {
@@ -330,12 +326,13 @@ k_spread_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
       const SubDev sd = subs[si];
       const int rg = (k % ngroups) * 16;
       const int nchunk = (sd.count + kChunk - 1) / kChunk;
-      // X row scale: the rhs's max |v| times the subproblem's max |A_a|
+      // X row scale 2^(46 - ev - eA_a): the rhs's max |v| times the subproblem's
+      // max |A_a|; Y column scale 2^(46 - eB_b - eC_c).  Both are folded into
+      // the slicing constant (slice1m), not multiplied into the values.
       const int ev = max(-900, exp_bound(__longlong_as_double((long long)vmax[rg + r])));
-      const double sx = pow2(46 - ev) * pow2(-(int)sub_exp[(int64_t)si * kExpPerSub + a]);
-      // Y column scale 2^(46 - eB_b - eC_c) of the subproblem
-      const double sy = pow2(46 - (int)sub_exp[(int64_t)si * kExpPerSub + 8 + yb]) *
-                        pow2(-(int)sub_exp[(int64_t)si * kExpPerSub + 16 + yc]);
+      const double mgx = kMagic * (pow2(ev - 46) * pow2((int)sub_exp[(int64_t)si * kExpPerSub + a]));
+      const double mgy = kMagic * (pow2((int)sub_exp[(int64_t)si * kExpPerSub + 8 + yb] - 46) *
+                                   pow2((int)sub_exp[(int64_t)si * kExpPerSub + 16 + yc]));
       for (int c = 0; c < nchunk; ++c, ++g) {
         const int st = g % kOpStages, s = g % RS;
         OZW(16, umma::mbar_wait(&raw_full[s], (g / RS) & 1));
@@ -343,7 +340,6 @@ k_spread_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
         if (g >= kOpStages) OZW(17, umma::mbar_wait(&op_free[st], ((g / kOpStages) - 1) & 1));
         const double* R = reinterpret_cast<const double*>(raw + s * RB);
         const double* Vr = reinterpret_cast<const double*>(raw + s * RB + kPyA);
-        const int cn = min(kChunk, sd.count - c * kChunk);
         if (xf & 1) {
           umma::fence_before();
           __syncwarp();
@@ -353,125 +349,41 @@ k_spread_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
           }
           continue;
         }
-        if (kSlcWarps == 8 && kY16) {
+        // No tail predicates: a missing node's v line is zero (the loader
+        // zero-fills it), so its X digits are zero and whatever its stale --
+        // but finite: the stages start zeroed -- weight row cuts into Y never
+        // reaches the accumulator.
+        const uint32_t xt = tmem + ((uint32_t)((m >> 5) * 32) << 16) +
+                            (uint32_t)(kXTmem0 + st * kSl * 8);
+        auto cut_x = [&](int n0) {   // X digits of nodes n0 .. n0 + 7 -> TMEM
+          uint32_t lo[8], hi[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            slice1m(Vr[(n0 + i) * 16 + r], R[(n0 + i) * 24 + a], mgx, lo[i], hi[i]);
+          uint32_t w0[6], w1[6];
+          pack4(lo, hi, w0);
+          pack4(lo + 4, hi + 4, w1);
+#pragma unroll
+          for (int p = 0; p < kSl; ++p)
+            umma::tmem_st2(xt + (uint32_t)(p * 8 + n0 / 4), w0[p], w1[p]);
+        };
+        if (warp < 4) {
           // Y on warps 0-3: thread = row (b, c) x 16 nodes, one 16-byte store
           // per digit slice -- a warp's 32 rows fill whole 128-byte lines
           // (conflict-free; 8-node 8-byte stores were 4-way conflicted)
-          if (warp < 4) {
-            const int kn = (warp >> 1) * 16;
-            uint32_t lo[16], hi[16];
+          const int kn = (warp >> 1) * 16;
+          uint32_t lo[16], hi[16];
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              const int j = kn + i;
-              double x = 0.0, y = 0.0;
-              if (j < cn) {
-                x = R[j * 24 + 8 + yb] * sy;
-                y = R[j * 24 + 16 + yc];
-              }
-              slice1(x, y, lo[i], hi[i]);
-            }
-            store16(lo, hi, sYop + st * kYOpBytes + canon32(yn, kn), kBBytes);
-          }
+          for (int i = 0; i < 16; ++i)
+            slice1m(R[(kn + i) * 24 + 8 + yb], R[(kn + i) * 24 + 16 + yc], mgy, lo[i], hi[i]);
+          store16(lo, hi, sYop + st * kYOpBytes + canon32(yn, kn), kBBytes);
           OZW(25, (void)0);   // Y digits cut
-          // X: warps 0-3 nodes 0..7, warps 4-7 nodes 8..31 (24 values per
-          // thread on every slicer warp), in blocks of 8 nodes
-          const int nb0 = warp < 4 ? 0 : 8, nblk = warp < 4 ? 1 : 3;
-          const uint32_t xt = tmem + ((uint32_t)((m >> 5) * 32) << 16) +
-                              (uint32_t)(kXTmem0 + st * kSl * 8);
-#pragma unroll
-          for (int bk = 0; bk < 3; ++bk) {
-            if (bk >= nblk) break;
-            const int n0 = nb0 + bk * 8;
-            uint32_t lo[8], hi[8];
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              const int j = n0 + i;
-              double x = 0.0, y = 0.0;
-              if (j < cn) {
-                x = Vr[j * 16 + r];
-                y = R[j * 24 + a] * sx;
-              }
-              slice1(x, y, lo[i], hi[i]);
-            }
-            uint32_t w0[6], w1[6];
-            pack4(lo, hi, w0);
-            pack4(lo + 4, hi + 4, w1);
-#pragma unroll
-            for (int p = 0; p < kSl; ++p)
-              umma::tmem_st2(xt + (uint32_t)(p * 8 + n0 / 4), w0[p], w1[p]);
-          }
+          cut_x(0);           // and X of nodes 0..7
         } else {
-          if (kSlcWarps == 16) {
-            // Y digits of 4 nodes for row (b, c): K-major canonical, zero past cn
-            const int kn = (warp >> 3) * 16 + (lane >> 3) * 4;
-            uint32_t lo[4], hi[4];
-  #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const int j = kn + i;
-              double x = 0.0, y = 0.0;
-              if (j < cn) {
-                x = R[j * 24 + 8 + yb] * sy;
-                y = R[j * 24 + 16 + yc];
-              }
-              slice1(x, y, lo[i], hi[i]);
-            }
-            uint32_t w6[6];
-            pack4(lo, hi, w6);
-            uint8_t* yd = sYop + st * kYOpBytes + canon32(yn, kn);
-  #pragma unroll
-            for (int p = 0; p < kSl; ++p) *reinterpret_cast<uint32_t*>(yd + p * kBBytes) = w6[p];
-          } else {
-            // Y digits of 8 nodes for row (b, c)
-            const int yq = tid >> 6;
-            uint32_t lo[8], hi[8];
-  #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              const int j = yq * 8 + i;
-              double x = 0.0, y = 0.0;
-              if (j < cn) {
-  #ifdef NLD_EXP_SPR_NODMUL
-                x = R[j * 24 + 8 + yb];
-  #else
-                x = R[j * 24 + 8 + yb] * sy;
-  #endif
-                y = R[j * 24 + 16 + yc];
-              }
-              slice1(x, y, lo[i], hi[i]);
-            }
-  #ifdef NLD_EXP_SPR_NOYSTS
-            if (lo[0] == 0x12345u && hi[7] == 0x777u)
-  #endif
-            store8(lo, hi, sYop + st * kYOpBytes + canon32(yn, yq * 8), kBBytes);
-          }
-          OZW(25, (void)0);   // Y digits cut
-          uint32_t lo[kXNodes], hi[kXNodes];
-  #pragma unroll
-          for (int i = 0; i < kXNodes; ++i) {
-            const int j = h * kXNodes + i;
-            double x = 0.0, y = 0.0;
-            if (j < cn) {
-              x = Vr[j * 16 + r];
-  #ifdef NLD_EXP_SPR_NODMUL
-              y = R[j * 24 + a];
-  #else
-              y = R[j * 24 + a] * sx;
-  #endif
-            }
-            slice1(x, y, lo[i], hi[i]);
-          }
-          uint32_t w4[kXNodes / 4][6];
-  #pragma unroll
-          for (int g4 = 0; g4 < kXNodes / 4; ++g4) pack4(lo + 4 * g4, hi + 4 * g4, w4[g4]);
-          const uint32_t xt = tmem + ((uint32_t)((m >> 5) * 32) << 16) +
-                              (uint32_t)(kXTmem0 + st * kSl * 8 + h * (kXNodes / 4));
-  #pragma unroll
-          for (int p = 0; p < kSl; ++p) {
-            if (kXNodes == 16)
-              umma::tmem_st4(xt + (uint32_t)(p * 8), w4[0][p], w4[1 % (kXNodes / 4)][p],
-                             w4[2 % (kXNodes / 4)][p], w4[3 % (kXNodes / 4)][p]);
-            else
-              umma::tmem_st2(xt + (uint32_t)(p * 8), w4[0][p], w4[1 % (kXNodes / 4)][p]);
-          }
+          // X of nodes 8..31: every slicer warp cuts 24 values per thread
+          cut_x(8);
+          cut_x(16);
+          cut_x(24);
         }
         OZW(26, (void)0);   // X digits issued to TMEM
         OZW(27, umma::tmem_wait_st());

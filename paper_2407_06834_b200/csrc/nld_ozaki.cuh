@@ -151,8 +151,37 @@ __device__ __forceinline__ void slice1(double x, double y, uint32_t& lo, uint32_
   hi = (uint32_t)(u >> 32);
 }
 
+// digits of x * y * 2^k without the scaling multiply: `mg` = kMagic 2^-k puts
+// the same integer round(x y 2^k) into the low mantissa bits (only the
+// result's exponent field differs), so the caller folds its per-item scale
+// into the constant once instead of a DMUL per value
+__device__ __forceinline__ void slice1m(double x, double y, double mg, uint32_t& lo, uint32_t& hi) {
+  const long long u = __double_as_longlong(fma(x, y, mg));
+  lo = (uint32_t)u;
+  hi = (uint32_t)(u >> 32);
+}
+
+// 32-byte global accesses (sm_100: LDG/STG.E.ENL2.256): one request per
+// thread and 32-byte sector instead of two 16-byte ones -- the gather
+// epilogue's per-node lines are random, so its LSU cost is per request
+__device__ __forceinline__ void ldg256(const double* p, double2& a, double2& b) {
+  asm volatile("ld.global.v4.f64 {%0, %1, %2, %3}, [%4];\n"
+               : "=d"(a.x), "=d"(a.y), "=d"(b.x), "=d"(b.y)
+               : "l"(p));
+}
+__device__ __forceinline__ void stg256(double* p, double2 a, double2 b) {
+  asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};\n" ::"l"(p), "d"(a.x), "d"(a.y), "d"(b.x),
+               "d"(b.y)
+               : "memory");
+}
+
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(umma::smem_u32(dst)), "l"(src));
+}
+// 16-byte cp.async that copies `bytes` (0 or 16) and zero-fills the rest
+__device__ __forceinline__ void cp_async16_zfill(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(umma::smem_u32(dst)), "l"(src),
+               "r"(bytes));
 }
 __device__ __forceinline__ void cp_async4(void* dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(umma::smem_u32(dst)), "l"(src));
