@@ -533,7 +533,8 @@ k_gather_nm(const SubDev* __restrict__ subs, const int32_t* __restrict__ order, 
             // both slots' columns in flight together (one wait per half), two
             // independent combine chains per slot
             const uint32_t tc0 = tl_lane + (uint32_t)(ab * kAccCols + w0 * 8);
-            double sh0 = 0.0, sl0 = 0.0, sh1 = 0.0, sl1 = 0.0;
+            // two accumulation chains per slot (even / odd a)
+            double s0a = 0.0, s0b = 0.0, s1a = 0.0, s1b = 0.0;
 #pragma unroll
             for (int hf = 0; hf < 2; ++hf) {
               uint32_t d0[kSl][4], d1[kSl][4];
@@ -544,23 +545,20 @@ k_gather_nm(const SubDev* __restrict__ subs, const int32_t* __restrict__ order, 
                 if (lane == 0) mbar_arrive(&acc_empty[ab]);
               }
               const double2 x0 = hf ? a45 : a01, x1 = hf ? a67 : a23;
-              double h, l;
-#pragma unroll
-              for (int i = 0; i < 4; ++i) {
-                const double av = i == 0 ? x0.x : i == 1 ? x0.y : i == 2 ? x1.x : x1.y;
-                combine6_parts(d0, i, h, l);
-                sh0 = fma(h, av, sh0);
-                sl0 = fma(l, av, sl0);
-                combine6_parts(d1, i, h, l);
-                sh1 = fma(h, av, sh1);
-                sl1 = fma(l, av, sl1);
-              }
+              s0a = fma(combine6_i64(d0, 0), x0.x, s0a);
+              s1a = fma(combine6_i64(d1, 0), x0.x, s1a);
+              s0b = fma(combine6_i64(d0, 1), x0.y, s0b);
+              s1b = fma(combine6_i64(d1, 1), x0.y, s1b);
+              s0a = fma(combine6_i64(d0, 2), x1.x, s0a);
+              s1a = fma(combine6_i64(d1, 2), x1.x, s1a);
+              s0b = fma(combine6_i64(d0, 3), x1.y, s0b);
+              s1b = fma(combine6_i64(d1, 3), x1.y, s1b);
             }
             const int gx0 = ps == 0 ? ge[0].x : ps == 1 ? ge[0].y : ps == 2 ? ge[0].z : ge[0].w;
             const int gx1 = ps == 0 ? ge[kSPW - 1].x : ps == 1 ? ge[kSPW - 1].y
                           : ps == 2 ? ge[kSPW - 1].z : ge[kSPW - 1].w;
-            tv[0][ps] = fma(sh0, 4294967296.0, sl0) * pow2(gx0 + eb);
-            tv[kSPW - 1][ps] = fma(sh1, 4294967296.0, sl1) * pow2(gx1 + eb);
+            tv[0][ps] = (s0a + s0b) * pow2(gx0 + eb);
+            tv[kSPW - 1][ps] = (s1a + s1b) * pow2(gx1 + eb);
 #ifdef NLD_OZ_TRACE
             if (tv[0][ps] == 1.2345e-300) out[0] = 0.0;   // keep the marker after the math
 #endif
@@ -600,25 +598,15 @@ k_gather_nm(const SubDev* __restrict__ subs, const int32_t* __restrict__ order, 
                   sh += (double)(f & 1);
                   continue;
                 }
-                // hi and lo parts accumulate in separate chains (combine6_parts)
                 const double2 x0 = hf ? a45 : a01, x1 = hf ? a67 : a23;
-                double h, l;
-                combine6_parts(dv, 0, h, l);
-                sh = fma(h, x0.x, sh);
-                sl_ = fma(l, x0.x, sl_);
-                combine6_parts(dv, 1, h, l);
-                sh = fma(h, x0.y, sh);
-                sl_ = fma(l, x0.y, sl_);
-                combine6_parts(dv, 2, h, l);
-                sh = fma(h, x1.x, sh);
-                sl_ = fma(l, x1.x, sl_);
-                combine6_parts(dv, 3, h, l);
-                sh = fma(h, x1.y, sh);
-                sl_ = fma(l, x1.y, sl_);
+                sh = fma(combine6_i64(dv, 0), x0.x, sh);
+                sl_ = fma(combine6_i64(dv, 1), x0.y, sl_);
+                sh = fma(combine6_i64(dv, 2), x1.x, sh);
+                sl_ = fma(combine6_i64(dv, 3), x1.y, sl_);
               }
               // rhs r0 + 4 j + ps
               const int gx = ps == 0 ? ge[j].x : ps == 1 ? ge[j].y : ps == 2 ? ge[j].z : ge[j].w;
-              tv[j][ps] = fma(sh, 4294967296.0, sl_) * pow2(gx + eb);
+              tv[j][ps] = (sh + sl_) * pow2(gx + eb);
             }
           }
           }

@@ -294,6 +294,29 @@ __device__ __forceinline__ void combine6_parts(const uint32_t (&dv)[6][NCOL], in
 #endif
 }
 
+// The six diagonals as ONE exact int64, T = x01 2^32 + x23 2^16 + x45
+// (|T| < 2^61), rounded once by I2F.F64.S64.  Measured on B200
+// (scripts/probes/fp64issue.cu): I2F.F64 occupies the fp64 pipe for ~8 cycles
+// per warp and DADD / DFMA for 2, so the hi/lo form above (I2F + DADD + 2
+// DFMA = 14 pipe cycles, ~12 instructions) is pipe-bound at ~15 cycles per
+// value and sub-partition; this form needs I2F + 1 DFMA (10 cycles) and ~8
+// instructions.  The single rounding is 2^-53 relative, as the fp64
+// reference's own product.
+template <int NCOL>
+__device__ __forceinline__ double combine6_i64(const uint32_t (&dv)[6][NCOL], int i) {
+  const int32_t x01 = (int32_t)(dv[0][i] * 256u + dv[1][i]);
+  const int32_t x23 = (int32_t)(dv[2][i] * 256u + dv[3][i]);
+  const int32_t x45 = (int32_t)(dv[4][i] * 256u + dv[5][i]);
+  // x01 2^32 only touches the high word: one 32-bit add, no 64-bit carry chain
+  const long long lo = (long long)x23 * 65536 + (long long)x45;
+  long long t;
+  asm("{\n\t.reg .b32 l, h;\n\tmov.b64 {l, h}, %1;\n\tadd.s32 h, h, %2;\n\t"
+      "mov.b64 %0, {l, h};\n\t}"
+      : "=l"(t)
+      : "l"(lo), "r"(x01));
+  return (double)t;
+}
+
 #if defined(NLD_OZ_TRACE)
 // host: write the last launch's wait log of this file's kernels to
 // $NLD_TRACE_DIR/<tag>_<n>.txt (one "site warp start end" line per wait)
