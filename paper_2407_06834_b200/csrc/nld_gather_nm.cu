@@ -534,30 +534,26 @@ k_gather_nm(const SubDev* __restrict__ subs, const int32_t* __restrict__ order, 
           umma::fence_after();
 #if NLD_GNM_PAIR
           if (kSPW == 2) {
-            // both slots' columns in flight together (one wait per half), two
-            // independent combine chains per slot
+            // Four chunks per pass -- (slot 0 | slot 1) x (a = 0..3 | a = 4..7),
+            // six diagonals x four columns each -- software-pipelined: every
+            // chunk's TMEM loads are in flight while the previous chunk is
+            // combined (tmem_ld4x6_combine4), so only the first load's
+            // latency is exposed; two accumulation chains per slot.
             const uint32_t tc0 = tl_lane + (uint32_t)(ab * kAccCols + w0 * 8);
-            // two accumulation chains per slot (even / odd a)
             double s0a = 0.0, s0b = 0.0, s1a = 0.0, s1b = 0.0;
-#pragma unroll
-            for (int hf = 0; hf < 2; ++hf) {
-              uint32_t d0[kSl][4], d1[kSl][4];
-              OZW(23, umma::tmem_ld4x6x2_wait(tc0 + 4 * hf, tc0 + 8 + 4 * hf, kPassRows, d0, d1));
-              if (hf == 1) {
-                umma::fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&acc_empty[ab]);
-              }
-              const double2 x0 = hf ? a45 : a01, x1 = hf ? a67 : a23;
-              s0a = fma(combine6_i64(d0, 0), x0.x, s0a);
-              s1a = fma(combine6_i64(d1, 0), x0.x, s1a);
-              s0b = fma(combine6_i64(d0, 1), x0.y, s0b);
-              s1b = fma(combine6_i64(d1, 1), x0.y, s1b);
-              s0a = fma(combine6_i64(d0, 2), x1.x, s0a);
-              s1a = fma(combine6_i64(d1, 2), x1.x, s1a);
-              s0b = fma(combine6_i64(d0, 3), x1.y, s0b);
-              s1b = fma(combine6_i64(d1, 3), x1.y, s1b);
-            }
+            uint32_t c0[kSl][4], c1[kSl][4];
+            OZW(23, umma::tmem_ld4x6_wait(tc0, kPassRows, c0));                      // slot 0, a 0..3
+            tmem_ld4x6_combine4(c1, c0, tc0 + 8, kPassRows, a01.x, a01.y, a23.x, a23.y, s0a, s0b);
+            tmem_ld4x6_combine4(c0, c1, tc0 + 4, kPassRows, a01.x, a01.y, a23.x, a23.y, s1a, s1b);
+            tmem_ld4x6_combine4(c1, c0, tc0 + 12, kPassRows, a45.x, a45.y, a67.x, a67.y, s0a, s0b);
+            // every column of this warp read: release the accumulator
+            umma::fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&acc_empty[ab]);
+            s1a = fma(combine6_i64(c1, 0), a45.x, s1a);
+            s1b = fma(combine6_i64(c1, 1), a45.y, s1b);
+            s1a = fma(combine6_i64(c1, 2), a67.x, s1a);
+            s1b = fma(combine6_i64(c1, 3), a67.y, s1b);
             const int gx0 = ps == 0 ? ge[0].x : ps == 1 ? ge[0].y : ps == 2 ? ge[0].z : ge[0].w;
             const int gx1 = ps == 0 ? ge[kSPW - 1].x : ps == 1 ? ge[kSPW - 1].y
                           : ps == 2 ? ge[kSPW - 1].z : ge[kSPW - 1].w;

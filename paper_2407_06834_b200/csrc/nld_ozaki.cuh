@@ -317,6 +317,86 @@ __device__ __forceinline__ double combine6_i64(const uint32_t (&dv)[6][NCOL], in
   return (double)t;
 }
 
+// Software-pipelined epilogue step: issue the TMEM loads of the NEXT chunk
+// (six diagonals x four columns), combine the CURRENT chunk's four values
+// (combine6_i64's arithmetic) into two accumulation chains while they are in
+// flight, then wait for them -- all in one asm statement, so the compiler
+// never sees the next chunk's registers before their data exists (they are
+// early-clobber outputs: written while the current chunk is still read).
+// Operands: %0-23 next, %24 / %25 the even / odd accumulators, %26-49
+// current, %50 next address, %51 column stride, %52-55 the four weights.
+__device__ __forceinline__ void tmem_ld4x6_combine4(uint32_t (&nx)[6][4], const uint32_t (&cu)[6][4],
+                                                    uint32_t taddr, uint32_t cs, double w0,
+                                                    double w1, double w2, double w3, double& sa,
+                                                    double& sb) {
+  asm volatile(
+      "{\n\t.reg .b32 a1, a2, a3, a4, a5, x01, x23, x45, l, h;\n\t.reg .b64 t;\n\t.reg .f64 f;\n\t"
+      "add.u32 a1, %50, %51;\n\tadd.u32 a2, a1, %51;\n\tadd.u32 a3, a2, %51;\n\t"
+      "add.u32 a4, a3, %51;\n\tadd.u32 a5, a4, %51;\n\t"
+      "tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%50];\n\t"
+      "tcgen05.ld.sync.aligned.32x32b.x4.b32 {%4,%5,%6,%7}, [a1];\n\t"
+      "tcgen05.ld.sync.aligned.32x32b.x4.b32 {%8,%9,%10,%11}, [a2];\n\t"
+      "tcgen05.ld.sync.aligned.32x32b.x4.b32 {%12,%13,%14,%15}, [a3];\n\t"
+      "tcgen05.ld.sync.aligned.32x32b.x4.b32 {%16,%17,%18,%19}, [a4];\n\t"
+      "tcgen05.ld.sync.aligned.32x32b.x4.b32 {%20,%21,%22,%23}, [a5];\n\t"
+      "mad.lo.s32 x01, %26, 256, %30;\n\t"
+      "mad.lo.s32 x23, %34, 256, %38;\n\t"
+      "mad.lo.s32 x45, %42, 256, %46;\n\t"
+      "cvt.s64.s32 t, x45;\n\t"
+      "mad.wide.s32 t, x23, 65536, t;\n\t"
+      "mov.b64 {l, h}, t;\n\t"
+      "add.s32 h, h, x01;\n\t"
+      "mov.b64 t, {l, h};\n\t"
+      "cvt.rn.f64.s64 f, t;\n\t"
+      "fma.rn.f64 %24, f, %52, %24;\n\t"
+      "mad.lo.s32 x01, %27, 256, %31;\n\t"
+      "mad.lo.s32 x23, %35, 256, %39;\n\t"
+      "mad.lo.s32 x45, %43, 256, %47;\n\t"
+      "cvt.s64.s32 t, x45;\n\t"
+      "mad.wide.s32 t, x23, 65536, t;\n\t"
+      "mov.b64 {l, h}, t;\n\t"
+      "add.s32 h, h, x01;\n\t"
+      "mov.b64 t, {l, h};\n\t"
+      "cvt.rn.f64.s64 f, t;\n\t"
+      "fma.rn.f64 %25, f, %53, %25;\n\t"
+      "mad.lo.s32 x01, %28, 256, %32;\n\t"
+      "mad.lo.s32 x23, %36, 256, %40;\n\t"
+      "mad.lo.s32 x45, %44, 256, %48;\n\t"
+      "cvt.s64.s32 t, x45;\n\t"
+      "mad.wide.s32 t, x23, 65536, t;\n\t"
+      "mov.b64 {l, h}, t;\n\t"
+      "add.s32 h, h, x01;\n\t"
+      "mov.b64 t, {l, h};\n\t"
+      "cvt.rn.f64.s64 f, t;\n\t"
+      "fma.rn.f64 %24, f, %54, %24;\n\t"
+      "mad.lo.s32 x01, %29, 256, %33;\n\t"
+      "mad.lo.s32 x23, %37, 256, %41;\n\t"
+      "mad.lo.s32 x45, %45, 256, %49;\n\t"
+      "cvt.s64.s32 t, x45;\n\t"
+      "mad.wide.s32 t, x23, 65536, t;\n\t"
+      "mov.b64 {l, h}, t;\n\t"
+      "add.s32 h, h, x01;\n\t"
+      "mov.b64 t, {l, h};\n\t"
+      "cvt.rn.f64.s64 f, t;\n\t"
+      "fma.rn.f64 %25, f, %55, %25;\n\t"
+      "tcgen05.wait::ld.sync.aligned;\n\t}\n"
+      : "=&r"(nx[0][0]), "=&r"(nx[0][1]), "=&r"(nx[0][2]), "=&r"(nx[0][3]),
+        "=&r"(nx[1][0]), "=&r"(nx[1][1]), "=&r"(nx[1][2]), "=&r"(nx[1][3]),
+        "=&r"(nx[2][0]), "=&r"(nx[2][1]), "=&r"(nx[2][2]), "=&r"(nx[2][3]),
+        "=&r"(nx[3][0]), "=&r"(nx[3][1]), "=&r"(nx[3][2]), "=&r"(nx[3][3]),
+        "=&r"(nx[4][0]), "=&r"(nx[4][1]), "=&r"(nx[4][2]), "=&r"(nx[4][3]),
+        "=&r"(nx[5][0]), "=&r"(nx[5][1]), "=&r"(nx[5][2]), "=&r"(nx[5][3]),
+        "+d"(sa), "+d"(sb)
+      : "r"(cu[0][0]), "r"(cu[0][1]), "r"(cu[0][2]), "r"(cu[0][3]),
+        "r"(cu[1][0]), "r"(cu[1][1]), "r"(cu[1][2]), "r"(cu[1][3]),
+        "r"(cu[2][0]), "r"(cu[2][1]), "r"(cu[2][2]), "r"(cu[2][3]),
+        "r"(cu[3][0]), "r"(cu[3][1]), "r"(cu[3][2]), "r"(cu[3][3]),
+        "r"(cu[4][0]), "r"(cu[4][1]), "r"(cu[4][2]), "r"(cu[4][3]),
+        "r"(cu[5][0]), "r"(cu[5][1]), "r"(cu[5][2]), "r"(cu[5][3]),
+        "r"(taddr), "r"(cs), "d"(w0), "d"(w1), "d"(w2), "d"(w3)
+      : "memory");
+}
+
 #if defined(NLD_OZ_TRACE)
 // host: write the last launch's wait log of this file's kernels to
 // $NLD_TRACE_DIR/<tag>_<n>.txt (one "site warp start end" line per wait)

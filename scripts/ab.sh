@@ -13,6 +13,6 @@ for tag in $tags; do
   cp paper_2407_06834_b200/libnld_b200_$tag.so $SCR/repo/paper_2407_06834_b200/libnld_b200.so
   (cd $SCR/repo && env NLD_ALLOW_AB_BUILD=1 $ENV timeout 600 python bench.py --config $CFG --nrhs 16 --steps 8 --warmup 2 --no-cpu --no-cg --e2e-steps 2) > gpurun_out/ab_$tag.json 2>gpurun_out/ab_$tag.err
   python -c "
-import json; d=json.load(open('gpurun_out/ab_$tag.json')); ms=d['ms_per_step']; print('$tag', round(d['value'],1), round(ms,2), {k:round(v*ms,2) for k,v in d['roofline']['stage_share'].items()})" || tail -3 gpurun_out/ab_$tag.err
+import json; d=json.load(open('gpurun_out/ab_$tag.json')); ms=d['ms_per_step']; print('$tag', round(d['value'],1), round(ms,2), {k:round(v*ms,2) for k,v in d['roofline']['stage_share'].items()}, 'MHz', d['clocks']['sm_mhz'], 'Mcycles', round(ms*d['clocks']['sm_mhz']/1e3,2))" || tail -3 gpurun_out/ab_$tag.err
 done
 rm -rf $SCR
