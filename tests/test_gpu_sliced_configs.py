@@ -109,6 +109,30 @@ def c1_operator():
     return _C1["op"], _C1["f"]
 
 
+def test_unaligned_batch_buffers():
+    """The sliced gather's fused epilogue reads and writes the caller's
+    pixel-major lines with 32-byte accesses; buffers that are only 16-byte
+    aligned must take the unfused path through the aligned workspace and give
+    the same product (apply_op, nld_apply.cu: `al32`)."""
+    op, _ = c1_operator()
+    n = op.n
+    rng = np.random.default_rng(5)
+    V = rng.standard_normal((n, 16))
+    coef = np.tile([1.0, 0.37], 16)
+    Vd = torch.from_numpy(V).cuda()
+    want = op.apply_device(Vd, _lib.APPLY_SYSTEM, 16, coef, pixel_major=True)
+    flat_in = torch.empty(n * 16 + 2, dtype=torch.float64, device="cuda")
+    flat_out = torch.empty(n * 16 + 2, dtype=torch.float64, device="cuda")
+    vin = flat_in[2:].view(n, 16)      # data pointer 16 bytes past a 256-byte boundary
+    vout = flat_out[2:].view(n, 16)
+    assert vin.data_ptr() % 32 == 16 and vout.data_ptr() % 32 == 16
+    vin.copy_(Vd)
+    for x, y in ((vin, vout), (Vd, vout), (vin, None)):
+        got = op.apply_device(x, _lib.APPLY_SYSTEM, 16, coef, out=y, pixel_major=True)
+        err = rel(got.cpu().numpy(), want.cpu().numpy())
+        assert err < 1e-12, err
+
+
 @pytest.mark.parametrize("layout", ["pixel", "rhs"])
 @pytest.mark.parametrize("nrhs", [16, 32])
 def test_nonfinite_columns(layout, nrhs):
