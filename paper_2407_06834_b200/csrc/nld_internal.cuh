@@ -26,7 +26,31 @@
 
 namespace nld {
 
-constexpr int kSubMax = 2048;  // nodes per subproblem
+// Nodes per subproblem: between kSubMin and kSubMax, chosen per window so that
+// every SM still gets several items (sub_cap).  Upper bound: the sliced spread
+// sums K products of magnitude <= 2^14 per digit pair, six pairs per
+// diagonal, in int32 (K <= 16384).  Large items amortise the per-item costs
+// (spread accumulator drain, G digit load); small windows keep 2048 so the
+// persistent kernels' snake deal stays balanced.
+constexpr int kSubMin = 2048;
+#ifndef NLD_SUB_MAX
+#define NLD_SUB_MAX 8192
+#endif
+constexpr int kSubMax = NLD_SUB_MAX;
+static_assert(kSubMax <= 16384 && kSubMax >= kSubMin, "subproblem size cap");
+inline int sub_cap(long long nodes, int sms) {
+  const long long per = nodes / ((long long)sms * 8);     // >= ~8 full items per SM
+  long long cap = per < kSubMin ? kSubMin : (per > kSubMax ? kSubMax : per);
+  return (int)((cap + 127) & ~127LL);
+}
+// A cell's subproblems: nsub = ceil(cnt / kSubMax) near-equal parts, sized in
+// whole 128-node gather tiles -- no small remainder item paying the per-item
+// costs (spread accumulator drain, G digit load) for a few nodes.
+__host__ __device__ inline int sub_size(int cnt, int nsub) {
+  const int per = (cnt + nsub - 1) / nsub;
+  const int per128 = (per + 127) & ~127;
+  return ((int64_t)(nsub - 1) * per128 < cnt) ? per128 : per;
+}
 constexpr int kMaxDim = 3;
 
 struct Status {

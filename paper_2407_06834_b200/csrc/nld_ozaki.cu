@@ -10,7 +10,7 @@
 // 46-bit integers and cut into S = 6 signed 8-bit digits,
 //     x = sum_p d_p 256^(5-p),   y = sum_q e_q 256^(5-q),   d, e in [-128, 127],
 // so that  x y = sum_t 256^(10-t) sum_{p+q=t} d_p e_q.  The integer products
-// are exact (s8 x s8 -> s32, |sum| < 2^28 for <= 2048 nodes); the diagonals
+// are exact (s8 x s8 -> s32, |sum| < 2^31 for <= 16384 nodes); the diagonals
 // t = 0..S-1 are kept (the dropped ones are below 2^-46 of the operand
 // bounds), accumulated in TMEM by issuing A_p against the stacked slices
 // [e_0 | e_1 | ...] with the D window shifted by 64 p columns, and combined in
@@ -467,9 +467,9 @@ k_spread_ozp(const SubDev* __restrict__ subs, const int32_t* __restrict__ order,
         }
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-          // sum_t D_t 256^-t: K is up to 2048 nodes here, |D_t| < 6 2^25, so
+          // sum_t D_t 256^-t: K is up to kSubMax = 8192 nodes here, |D_t| < 6 2^27, so
           // the int32 pairs of the gather's combine would overflow; the two
-          // triples D0 2^16 + D1 2^8 + D2 and D3 2^16 + ... (|.| < 2^43) are
+          // triples D0 2^16 + D1 2^8 + D2 and D3 2^16 + ... (|.| < 2^47) are
           // formed exactly in int64 and convert by the magic number (2 DADD
           // instead of 6 conversions), then one FMA: acc = (hi + lo 2^-24) 2^-16
           const long long h3 = (long long)(int32_t)dv[0][i] * 65536 +

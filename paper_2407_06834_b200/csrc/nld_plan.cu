@@ -271,13 +271,16 @@ __global__ void k_edges(const double* __restrict__ F, int64_t N, int D,
   }
 }
 
+#ifndef NLD_SUB_BALANCED
+#define NLD_SUB_BALANCED 1
+#endif
 // cells and their subproblems
 __global__ void k_cells(const int32_t* __restrict__ ukeys,
                         const int32_t* __restrict__ counts,
                         const int32_t* __restrict__ starts,
                         const int32_t* __restrict__ sub_first, int ncell,
                         BoxDev bx, int win, int64_t node_off, int cell_off,
-                        int64_t block_base, int blk, CellDev* __restrict__ cells,
+                        int64_t block_base, int blk, int sub_max, CellDev* __restrict__ cells,
                         SubDev* __restrict__ subs, int32_t* __restrict__ cellmap) {
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < ncell;
        k += gridDim.x * blockDim.x) {
@@ -291,18 +294,23 @@ __global__ void k_cells(const int32_t* __restrict__ ukeys,
     }
     int first = sub_first[k];
     int cnt = counts[k];
-    int nsub = (cnt + kSubMax - 1) / kSubMax;
+    int nsub = (cnt + sub_max - 1) / sub_max;
     cd.win = win;
     cd.block0 = block_base + (int64_t)first * blk;
     cd.nsub = nsub;
     cd.blk = blk;
     cells[k] = cd;
     cellmap[key] = cell_off + k;
+#if NLD_SUB_BALANCED
+    const int per = sub_size(cnt, max(nsub, 1));
+#else
+    const int per = sub_max;
+#endif
     for (int q = 0; q < nsub; ++q) {
       SubDev sd;
-      sd.start = node_off + starts[k] + (int64_t)q * kSubMax;
+      sd.start = node_off + starts[k] + (int64_t)q * per;
       sd.block = cd.block0 + (int64_t)q * blk;
-      sd.count = min(kSubMax, cnt - q * kSubMax);
+      sd.count = min(per, cnt - q * per);
       sd.cell = cell_off + k;
       sd.win = win;
       sd.pad = 0;
@@ -320,11 +328,11 @@ __global__ void k_cellinfo(const int32_t* __restrict__ cellmap, const CellDev* _
   }
 }
 
-__global__ void k_nsub(const int32_t* __restrict__ counts, int ncell,
+__global__ void k_nsub(const int32_t* __restrict__ counts, int ncell, int sub_max,
                        int32_t* __restrict__ nsub) {
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < ncell;
        k += gridDim.x * blockDim.x)
-    nsub[k] = (counts[k] + kSubMax - 1) / kSubMax;
+    nsub[k] = (counts[k] + sub_max - 1) / sub_max;
 }
 
 __global__ void k_iota(int32_t* p, int64_t n) {
@@ -692,7 +700,15 @@ void build_planset(nld_operator* op, int which, cudaStream_t st) {
       NLD_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tbytes, counts.as<int32_t>(),
                                              starts.as<int32_t>(), ncell, st));
     }
-    k_nsub<<<blocks_for(ncell), 256, 0, st>>>(counts.as<int32_t>(), ncell,
+    // nodes per subproblem of this window (nld_internal.cuh: sub_cap)
+    static int sms = 0;
+    if (!sms) {
+      int dev = 0;
+      NLD_CUDA(cudaGetDevice(&dev));
+      NLD_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    }
+    const int sub_max = sub_cap(N, sms);
+    k_nsub<<<blocks_for(ncell), 256, 0, st>>>(counts.as<int32_t>(), ncell, sub_max,
                                               nsubs.as<int32_t>());
     tbytes = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, tbytes, nsubs.as<int32_t>(),
@@ -724,7 +740,7 @@ void build_planset(nld_operator* op, int which, cudaStream_t st) {
     k_cells<<<blocks_for(ncell), 256, 0, st>>>(
         ukeys.as<int32_t>(), counts.as<int32_t>(), starts.as<int32_t>(),
         subfirst.as<int32_t>(), ncell, bx, w, (int64_t)w * N, (int)cells_so_far,
-        fast ? block_total : 0, blk, wc[w].cells, wc[w].subs, cellmaps[w]);
+        fast ? block_total : 0, blk, sub_max, wc[w].cells, wc[w].subs, cellmaps[w]);
     NLD_CUDA(cudaGetLastError());
     if (fast) {
       block_total += nsub * blk;
