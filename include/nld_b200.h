@@ -99,7 +99,7 @@ typedef struct {
   int32_t box_lo[3];      /* support box of the spread grid        */
   int32_t box_w[3];
   int64_t n_cells;        /* occupied stencil cells                */
-  int64_t n_subproblems;  /* work items of <= P nodes of one cell  */
+  int64_t n_subproblems;  /* work items: parts of one cell, <= 2048..8192 nodes */
   int64_t n_edge;         /* nodes with 2m+1 nonzero weights       */
 } nld_window_info;
 
@@ -138,7 +138,12 @@ NLD_API int nld_op_set_comm(nld_operator* op, nld_allreduce_fn fn, void* ctx,
 
 /* One fused product per right-hand side (kernel.py:79-93, linops.py:43-50).
  * coef: per-rhs (lam, mu) pairs for NLD_APPLY_SYSTEM, ignored otherwise.
- * NLD_APPLY_SYSTEM/LAPLACIAN use the cached degree (nld_op_degree). */
+ * NLD_APPLY_SYSTEM/LAPLACIAN use the cached degree (nld_op_degree).
+ * Pixel-major batches (kind | NLD_LAYOUT_PIXEL_MAJOR, v/out = [n][nrhs]) are
+ * the kernels' native layout; with v and out 32-byte aligned (any cudaMalloc'd
+ * or torch-allocated buffer) the window sum and the degree/shift terms are
+ * fused into the last window's gather, otherwise the product goes through
+ * the library's aligned workspace (same result, one more pass). */
 NLD_API int nld_op_apply(nld_operator* op, int32_t kind, const double* v, double* out,
                  int32_t nrhs, int64_t ld, const double* coef_host,
                  void* stream);
