@@ -248,9 +248,7 @@ int nld_op_debug_poison(nld_operator* op) {
     fill(ws.cbuf1, sizeof(double2) * gt);
     fill(ws.wout, sizeof(double) * std::max<int64_t>(1, op->N * op->L) * cap);
     fill(ws.vt, sizeof(double) * std::max<int64_t>(1, op->N) * cap);
-    fill(ws.asm_y1, sizeof(double) * ws.asm_cap);
     fill(ws.asm_y2, sizeof(double) * (ws.asm_cap / 8 + 1));
-    fill(ws.asm_y1b, sizeof(double) * ws.asm_cap);
     fill(ws.asm_y2b, sizeof(double) * (ws.asm_cap / 8 + 1));
     fill(ws.cbuf2, sizeof(double2) * gt);
     fill(ws.cbuf3, sizeof(double2) * gt);

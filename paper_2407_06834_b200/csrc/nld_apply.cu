@@ -308,64 +308,59 @@ k_assemble(const WinDev* __restrict__ wins, int w0, const int2* __restrict__ cel
 //   Y2[c0][p1][p2][o0]     = sum_o1 Y1[c0][p1-o1][p2][o0][o1]
 //   G[p0][p1][p2]          = sum_o0 Y2[p0-o0][p1][p2][o0]
 // (all with the rhs index innermost: [..][nrhs]).
-__global__ void __launch_bounds__(256)
-k_asm_p1(const WinDev* __restrict__ wins, int w, const int2* __restrict__ cellinfo,
-         const double* __restrict__ blocks, int nrhs, double* __restrict__ y1) {
+__global__ void __launch_bounds__(128)
+k_asm_p12(const WinDev* __restrict__ wins, int w, const int2* __restrict__ cellinfo,
+          const double* __restrict__ blocks, int nrhs, double* __restrict__ y2) {
+  // Passes 1 and 2 in one kernel (Y1 never reaches memory): one CTA per
+  // (c0, p1, p2) line of 8 nrhs values (o0, r).  The line's 64 source cells
+  // (o1, o2) are looked up once per CTA, and lines whose cells are all empty
+  // -- most of the box -- are only zero-filled.  Each value keeps the two
+  // passes' summation order: Y1 terms over o2 (first blocks, then the extra
+  // blocks of cells split into several subproblems), then those over o1.
   const WinDev wd = wins[w];
-  const int B0 = wd.box_w[0], B1 = wd.box_w[1], B2 = wd.box_w[2];
+  const int B1 = wd.box_w[1], B2 = wd.box_w[2];
+  const int nline = wd.box_w[0] * B1 * B2;
   const int2* __restrict__ ci = cellinfo + wd.cellmap_off;
-  const int64_t total = (int64_t)B0 * B1 * B2 * 64 * nrhs;
-  for (int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; id < total;
-       id += (int64_t)gridDim.x * blockDim.x) {
-    const int r = (int)(id % nrhs);
-    int64_t rest = id / nrhs;
-    const int o01 = (int)(rest & 63);
-    rest >>= 6;
-    const int p2 = (int)(rest % B2);
-    const int64_t row = rest / B2;            // c0 * B1 + c1
-    // the eight cells' (first block, count) first, all loads independent --
-    // most cells of the box are empty, so a chain of dependent index -> block
-    // loads per o2 left this pass latency bound
-    int2 cs[8];
-#pragma unroll
-    for (int o2 = 0; o2 < 8; ++o2)
-      cs[o2] = p2 - o2 >= 0 ? __ldg(ci + row * B2 + p2 - o2) : make_int2(0, 0);
-    double sum = 0.0;
-#pragma unroll
-    for (int o2 = 0; o2 < 8; ++o2)
-      if (cs[o2].y > 0) sum += __ldg(blocks + ((int64_t)cs[o2].x + o01 * 8 + o2) * nrhs + r);
-#pragma unroll
-    for (int o2 = 0; o2 < 8; ++o2)   // cells split into several subproblems
-      for (int q = 1; q < cs[o2].y; ++q)
-        sum += __ldg(blocks + ((int64_t)cs[o2].x + (int64_t)q * 512 + o01 * 8 + o2) * nrhs + r);
-    y1[id] = sum;
-  }
-}
-
-__global__ void __launch_bounds__(256)
-k_asm_p2(const WinDev* __restrict__ wins, int w, const double* __restrict__ y1, int nrhs,
-         double* __restrict__ y2) {
-  const WinDev wd = wins[w];
-  const int B0 = wd.box_w[0], B1 = wd.box_w[1], B2 = wd.box_w[2];
-  const int64_t total = (int64_t)B0 * B1 * B2 * 8 * nrhs;
-  for (int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; id < total;
-       id += (int64_t)gridDim.x * blockDim.x) {
-    const int r = (int)(id % nrhs);
-    int64_t rest = id / nrhs;
-    const int o0 = (int)(rest & 7);
-    rest >>= 3;
-    const int p2 = (int)(rest % B2);
-    rest /= B2;
-    const int p1 = (int)(rest % B1);
-    const int c0 = (int)(rest / B1);
-    double sum = 0.0;
-#pragma unroll
-    for (int o1 = 0; o1 < 8; ++o1) {
-      const int c1 = p1 - o1;
-      if (c1 < 0) break;
-      sum += y1[(((((int64_t)c0 * B1 + c1) * B2 + p2) * 64) + o0 * 8 + o1) * nrhs + r];
+  const int per = 8 * nrhs;
+  __shared__ int2 cs[64];   // [o1][o2]: (first block, number of blocks)
+  for (int ln = blockIdx.x; ln < nline; ln += gridDim.x) {
+    const int p2 = ln % B2, p1 = (ln / B2) % B1;
+    __syncthreads();
+    int mine = 0;
+    if (threadIdx.x < 64) {
+      const int o1 = threadIdx.x >> 3, o2 = threadIdx.x & 7;
+      const int2 c = (p1 - o1 >= 0 && p2 - o2 >= 0) ? __ldg(ci + ln - o1 * B2 - o2) : make_int2(0, 0);
+      cs[threadIdx.x] = c;
+      mine = c.y > 0;
     }
-    y2[id] = sum;
+    const int any = __syncthreads_or(mine);
+    double* __restrict__ dst = y2 + (int64_t)ln * per;
+    if (!any) {
+      for (int e = threadIdx.x; e < per; e += 128) dst[e] = 0.0;
+      continue;
+    }
+    for (int e = threadIdx.x; e < per; e += 128) {
+      const int o0 = e / nrhs, r = e - o0 * nrhs;
+      const double* __restrict__ src = blocks + (int64_t)o0 * 64 * nrhs + r;
+      double sum = 0.0;
+#pragma unroll 2
+      for (int o1 = 0; o1 < 8; ++o1) {
+        double inner = 0.0;
+#pragma unroll
+        for (int o2 = 0; o2 < 8; ++o2) {
+          const int2 c = cs[o1 * 8 + o2];
+          if (c.y > 0) inner += __ldg(src + ((int64_t)c.x + o1 * 8 + o2) * nrhs);
+        }
+#pragma unroll
+        for (int o2 = 0; o2 < 8; ++o2) {
+          const int2 c = cs[o1 * 8 + o2];
+          for (int q = 1; q < c.y; ++q)
+            inner += __ldg(src + ((int64_t)c.x + (int64_t)q * 512 + o1 * 8 + o2) * nrhs);
+        }
+        sum += inner;
+      }
+      dst[e] = sum;
+    }
   }
 }
 
@@ -1121,9 +1116,7 @@ void ensure_workspace(nld_operator* op, const PlanSet& ps, int nrhs) {
       if (w.d == 3) mb = std::max(mb, w.box_size);
     ws.asm_cap = mb * 64 * cap;
     if (ws.asm_cap) {
-      NLD_CUDA(cudaMalloc(&ws.asm_y1, sizeof(double) * ws.asm_cap));
       NLD_CUDA(cudaMalloc(&ws.asm_y2, sizeof(double) * (ws.asm_cap / 8 + 1)));
-      NLD_CUDA(cudaMalloc(&ws.asm_y1b, sizeof(double) * ws.asm_cap));
       NLD_CUDA(cudaMalloc(&ws.asm_y2b, sizeof(double) * (ws.asm_cap / 8 + 1)));
     }
   }
@@ -1140,9 +1133,7 @@ void ensure_workspace(nld_operator* op, const PlanSet& ps, int nrhs) {
 }
 
 void free_workspace(Workspace& ws) {
-  cudaFree(ws.asm_y1);
   cudaFree(ws.asm_y2);
-  cudaFree(ws.asm_y1b);
   cudaFree(ws.asm_y2b);
   cudaFree(ws.cbuf2);
   cudaFree(ws.cbuf3);
@@ -1177,15 +1168,13 @@ static void spread_window(nld_operator* op, const PlanSet& ps, int w, const doub
 static void assemble_window(nld_operator* op, const PlanSet& ps, int w, const double* vt,
                             int nrhs, cudaStream_t st, int set = 0) {
   Workspace& ws = op->ws;
-  double* const y1 = set ? ws.asm_y1b : ws.asm_y1;
   double* const y2 = set ? ws.asm_y2b : ws.asm_y2;
   const WinDev& wd = ps.wdev_h[w];
   const WinPlan& wp = ps.win[w];
   const int64_t y1n = wd.box_size * 64 * nrhs;
   if (wd.fast && wd.d == 3 && wd.S == 8 && !wd.wrap && ws.asm_cap >= y1n) {
-    k_asm_p1<<<grid_blocks(y1n, 256, 148 * 32), 256, 0, st>>>(ps.wdev, w, ps.cellinfo,
-                                                              ws.blocks, nrhs, y1);
-    k_asm_p2<<<grid_blocks(y1n / 8, 256, 148 * 32), 256, 0, st>>>(ps.wdev, w, y1, nrhs, y2);
+    k_asm_p12<<<(int)std::min<int64_t>(wd.box_size, 148 * 64), 128, 0, st>>>(ps.wdev, w, ps.cellinfo,
+                                                                            ws.blocks, nrhs, y2);
     k_asm_p3<<<grid_blocks(y1n / 64, 256, 148 * 32), 256, 0, st>>>(ps.wdev, w, y2, nrhs,
                                                                    ws.grid_in, ps.grid_total);
   } else {

@@ -176,11 +176,9 @@ struct Workspace {
   double* vt = nullptr;          // [N][nrhs] pixel-major rhs
   double* coef = nullptr;        // [nrhs][2]
   int64_t grid_total = 0, blocks_total = 0;
-  // separable assemble scratch (3-D windows): Y1 [box][64][nrhs], Y2 /8
-  double* asm_y1 = nullptr;
+  // separable assemble scratch (3-D windows): Y2 [box][8][nrhs] = asm_cap / 8
   double* asm_y2 = nullptr;
-  double* asm_y1b = nullptr;     // second aux stream's assemble scratch
-  double* asm_y2b = nullptr;
+  double* asm_y2b = nullptr;     // second aux stream's assemble scratch
   int64_t asm_cap = 0;
   unsigned long long* vmax = nullptr;   // [nrhs_cap] sliced spread: max |v| bits
   uint8_t* gdig = nullptr;       // sliced gather: per (cell, 16-rhs group) G digits + exponents
