@@ -314,7 +314,8 @@ k_asm_p12(const WinDev* __restrict__ wins, int w, const int2* __restrict__ celli
   // Passes 1 and 2 in one kernel (Y1 never reaches memory): one CTA per
   // (c0, p1, p2) line of 8 nrhs values (o0, r).  The line's 64 source cells
   // (o1, o2) are looked up once per CTA, and lines whose cells are all empty
-  // -- most of the box -- are only zero-filled.  Each value keeps the two
+  // -- most of the box -- are only zero-filled (per CTA pass: small batches
+  // take several lines at once).  Each value keeps the two
   // passes' summation order: Y1 terms over o2 (first blocks, then the extra
   // blocks of cells split into several subproblems), then those over o1.
   const WinDev wd = wins[w];
@@ -322,24 +323,33 @@ k_asm_p12(const WinDev* __restrict__ wins, int w, const int2* __restrict__ celli
   const int nline = wd.box_w[0] * B1 * B2;
   const int2* __restrict__ ci = cellinfo + wd.cellmap_off;
   const int per = 8 * nrhs;
-  __shared__ int2 cs[64];   // [o1][o2]: (first block, number of blocks)
-  for (int ln = blockIdx.x; ln < nline; ln += gridDim.x) {
-    const int p2 = ln % B2, p1 = (ln / B2) % B1;
+  // small batches: several consecutive lines per CTA pass, so that a single
+  // right-hand side still fills the CTA (per >= 8: at most 16 lines)
+  const int L = per >= 128 ? 1 : 128 / per;
+  __shared__ int2 cs[16 * 64];   // [line][o1][o2]: (first block, number of blocks)
+  for (int l0 = blockIdx.x * L; l0 < nline; l0 += gridDim.x * L) {
     __syncthreads();
     int mine = 0;
-    if (threadIdx.x < 64) {
-      const int o1 = threadIdx.x >> 3, o2 = threadIdx.x & 7;
-      const int2 c = (p1 - o1 >= 0 && p2 - o2 >= 0) ? __ldg(ci + ln - o1 * B2 - o2) : make_int2(0, 0);
-      cs[threadIdx.x] = c;
-      mine = c.y > 0;
+    for (int k = threadIdx.x; k < L * 64; k += 128) {
+      const int ln = l0 + (k >> 6), o1 = (k >> 3) & 7, o2 = k & 7;
+      int2 c = make_int2(0, 0);
+      if (ln < nline) {
+        const int p2 = ln % B2, p1 = (ln / B2) % B1;
+        if (p1 - o1 >= 0 && p2 - o2 >= 0) c = __ldg(ci + ln - o1 * B2 - o2);
+      }
+      cs[k] = c;
+      mine |= c.y > 0;
     }
     const int any = __syncthreads_or(mine);
-    double* __restrict__ dst = y2 + (int64_t)ln * per;
+    const int nval = min(L, nline - l0) * per;
+    double* __restrict__ dst = y2 + (int64_t)l0 * per;
     if (!any) {
-      for (int e = threadIdx.x; e < per; e += 128) dst[e] = 0.0;
+      for (int k = threadIdx.x; k < nval; k += 128) dst[k] = 0.0;
       continue;
     }
-    for (int e = threadIdx.x; e < per; e += 128) {
+    for (int k = threadIdx.x; k < nval; k += 128) {
+      const int li = k / per, e = k - li * per;
+      const int2* __restrict__ cl = cs + li * 64;
       const int o0 = e / nrhs, r = e - o0 * nrhs;
       const double* __restrict__ src = blocks + (int64_t)o0 * 64 * nrhs + r;
       double sum = 0.0;
@@ -348,18 +358,18 @@ k_asm_p12(const WinDev* __restrict__ wins, int w, const int2* __restrict__ celli
         double inner = 0.0;
 #pragma unroll
         for (int o2 = 0; o2 < 8; ++o2) {
-          const int2 c = cs[o1 * 8 + o2];
+          const int2 c = cl[o1 * 8 + o2];
           if (c.y > 0) inner += __ldg(src + ((int64_t)c.x + o1 * 8 + o2) * nrhs);
         }
 #pragma unroll
         for (int o2 = 0; o2 < 8; ++o2) {
-          const int2 c = cs[o1 * 8 + o2];
+          const int2 c = cl[o1 * 8 + o2];
           for (int q = 1; q < c.y; ++q)
             inner += __ldg(src + ((int64_t)c.x + (int64_t)q * 512 + o1 * 8 + o2) * nrhs);
         }
         sum += inner;
       }
-      dst[e] = sum;
+      dst[k] = sum;
     }
   }
 }
@@ -1173,8 +1183,9 @@ static void assemble_window(nld_operator* op, const PlanSet& ps, int w, const do
   const WinPlan& wp = ps.win[w];
   const int64_t y1n = wd.box_size * 64 * nrhs;
   if (wd.fast && wd.d == 3 && wd.S == 8 && !wd.wrap && ws.asm_cap >= y1n) {
-    k_asm_p12<<<(int)std::min<int64_t>(wd.box_size, 148 * 64), 128, 0, st>>>(ps.wdev, w, ps.cellinfo,
-                                                                            ws.blocks, nrhs, y2);
+    const int lines_per_cta = 8 * nrhs >= 128 ? 1 : 128 / (8 * nrhs);
+    k_asm_p12<<<(int)std::min<int64_t>((wd.box_size + lines_per_cta - 1) / lines_per_cta, 148 * 64), 128,
+                0, st>>>(ps.wdev, w, ps.cellinfo, ws.blocks, nrhs, y2);
     k_asm_p3<<<grid_blocks(y1n / 64, 256, 148 * 32), 256, 0, st>>>(ps.wdev, w, y2, nrhs,
                                                                    ws.grid_in, ps.grid_total);
   } else {
