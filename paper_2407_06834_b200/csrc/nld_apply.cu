@@ -1486,13 +1486,13 @@ void apply_op(nld_operator* op, int which, int kind, const double* v, double* ou
   }
   for (int w = 0; w < L; ++w) {
     // spread + gather (+ the sliced gather's per-cell G digits), assemble
-    // (three separable passes for 3-D m = 4 boxes), d convolution passes,
+    // (two kernels for 3-D m = 4 boxes: k_asm_p12, k_asm_p3), d convolution passes,
     // generic-path and edge-node kernels
     const WinDev& wd = ps.wdev_h[w];
     const bool fastw = wd.fast && ps.win[w].n_subs;
     const bool asm3 = wd.fast && wd.d == 3 && wd.S == 8 && !wd.wrap;
     launches += (fastw ? 2 : 0) + (fastw && sliced && wd.d == 3 && ws.gdig ? 1 : 0) +
-                (asm3 ? 3 : 1) + wd.d + (wd.fast ? 0 : 2) + (ps.win[w].n_edge ? 2 : 0);
+                (asm3 ? 2 : 1) + wd.d + (wd.fast ? 0 : 2) + (ps.win[w].n_edge ? 2 : 0);
   }
   ev.mark();
   // 5. epilogue
