@@ -596,6 +596,63 @@ __global__ void k_conv(const WinDev* __restrict__ wins, int w0, int pass,
   }
 }
 
+// Passes 0 and 1 of a 3-D window (axes 2 and 1) in one kernel: one CTA per
+// (p0 slab, rhs) keeps the slab and the axis-2 result in shared memory, so the
+// per-window convolution is two launches instead of three and the first
+// intermediate never reaches L2.  Same terms, order and FMAs per value as two
+// k_conv passes (bit-identical).  Writes the complex slab for pass 2.
+__host__ __device__ inline size_t conv01_smem(int B1, int B2) {
+  return (size_t)B1 * B2 * (sizeof(double) + sizeof(double2)) +
+         (size_t)(2 * (B1 > B2 ? B1 : B2)) * sizeof(double2);
+}
+__global__ void __launch_bounds__(256)
+k_conv01(const WinDev* __restrict__ wins, int w, const double2* __restrict__ K,
+         const double* __restrict__ gin, double2* __restrict__ cout, int64_t grid_ld) {
+  extern __shared__ double2 cv_smem[];
+  const WinDev wd = wins[w];
+  const int B1 = wd.box_w[1], B2 = wd.box_w[2], n = wd.n;
+  const int slab = B1 * B2, wm = B1 > B2 ? B1 : B2;
+  double2* const ta = cv_smem;                       // [B1][B2] axis-2 result
+  double2* const ks = ta + slab;                     // kernel at offsets -(wm-1) .. wm-1
+  double* const g = reinterpret_cast<double*>(ks + 2 * wm);   // [B1][B2] input slab
+  const double2* __restrict__ kw = K + wd.kern_off;
+  const int64_t base = (int64_t)blockIdx.y * grid_ld + wd.grid_off + (int64_t)blockIdx.x * slab;
+  for (int i = threadIdx.x; i < slab; i += blockDim.x) g[i] = gin[base + i];
+  for (int j = threadIdx.x; j < 2 * wm - 1; j += blockDim.x) {
+    int dl = (j - (wm - 1)) % n;
+    if (dl < 0) dl += n;
+    ks[j] = kw[dl];
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < slab; i += blockDim.x) {
+    const int t = i % B2;
+    const double* __restrict__ line = g + (i - t);
+    const double2* __restrict__ kk = ks + (wm - 1 - t);      // kk[s] = kw[(s - t) mod n]
+    double re = 0.0, im = 0.0;
+    for (int s = 0; s < B2; ++s) {
+      const double2 k = kk[s];
+      re = fma(k.x, line[s], re);
+      im = fma(k.y, line[s], im);
+    }
+    ta[i] = make_double2(re, im);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < slab; i += blockDim.x) {
+    const int p2 = i % B2, t = i / B2;
+    const double2* __restrict__ kk = ks + (wm - 1 - t);
+    double re = 0.0, im = 0.0;
+    for (int s = 0; s < B1; ++s) {
+      const double2 k = kk[s];
+      const double2 x = ta[s * B2 + p2];
+      re = fma(k.x, x.x, re);
+      re = fma(-k.y, x.y, re);
+      im = fma(k.x, x.y, im);
+      im = fma(k.y, x.x, im);
+    }
+    cout[base + i] = make_double2(re, im);
+  }
+}
+
 // ---- gather -------------------------------------------------------------
 //
 // CTA = one subproblem, all rhs.  The (2m)^D grid blocks of its cell for a
@@ -1208,6 +1265,12 @@ static void assemble_window(nld_operator* op, const PlanSet& ps, int w, const do
   }
 }
 
+// 3-D windows whose slab fits the default shared-memory limit take the fused
+// first two passes (k_conv01)
+static bool conv_fused01(const WinDev& wd) {
+  return wd.d == 3 && conv01_smem(wd.box_w[1], wd.box_w[2]) <= 48 * 1024 && wd.box_w[0] <= 65535;
+}
+
 // separable convolution of window w: grid_in -> grid_out
 static void conv_window(nld_operator* op, const PlanSet& ps, int w, int nrhs, cudaStream_t st,
                         int set = 0) {
@@ -1215,7 +1278,15 @@ static void conv_window(nld_operator* op, const PlanSet& ps, int w, int nrhs, cu
   double2* const b0 = set ? ws.cbuf2 : ws.cbuf0;
   double2* const b1 = set ? ws.cbuf3 : ws.cbuf1;
   const WinDev& wd = ps.wdev_h[w];
-  for (int pass = 0; pass < wd.d; ++pass) {
+  int pass0 = 0;
+  if (conv_fused01(wd)) {
+    // axes 2 and 1 in one kernel (writes the buffer pass 2 reads)
+    k_conv01<<<dim3(wd.box_w[0], nrhs), 256, conv01_smem(wd.box_w[1], wd.box_w[2]), st>>>(
+        ps.wdev, w, ps.K, ws.grid_in, b1, ps.grid_total);
+    NLD_CUDA(cudaGetLastError());
+    pass0 = 2;
+  }
+  for (int pass = pass0; pass < wd.d; ++pass) {
     dim3 grid(grid_blocks(wd.box_size, 128, 1024), 1, nrhs);
     const double2* cin = (pass % 2 == 1) ? b0 : b1;
     double2* cout = (pass % 2 == 0) ? b0 : b1;
@@ -1486,13 +1557,14 @@ void apply_op(nld_operator* op, int which, int kind, const double* v, double* ou
   }
   for (int w = 0; w < L; ++w) {
     // spread + gather (+ the sliced gather's per-cell G digits), assemble
-    // (two kernels for 3-D m = 4 boxes: k_asm_p12, k_asm_p3), d convolution passes,
+    // (two kernels for 3-D m = 4 boxes: k_asm_p12, k_asm_p3), d convolution passes
+    // (two kernels for 3-D windows: k_conv01 + the axis-0 pass),
     // generic-path and edge-node kernels
     const WinDev& wd = ps.wdev_h[w];
     const bool fastw = wd.fast && ps.win[w].n_subs;
     const bool asm3 = wd.fast && wd.d == 3 && wd.S == 8 && !wd.wrap;
     launches += (fastw ? 2 : 0) + (fastw && sliced && wd.d == 3 && ws.gdig ? 1 : 0) +
-                (asm3 ? 2 : 1) + wd.d + (wd.fast ? 0 : 2) + (ps.win[w].n_edge ? 2 : 0);
+                (asm3 ? 2 : 1) + (conv_fused01(wd) ? 2 : wd.d) + (wd.fast ? 0 : 2) + (ps.win[w].n_edge ? 2 : 0);
   }
   ev.mark();
   // 5. epilogue
