@@ -327,6 +327,7 @@ k_asm_p12(const WinDev* __restrict__ wins, int w, const int2* __restrict__ celli
   // right-hand side still fills the CTA (per >= 8: at most 16 lines)
   const int L = per >= 128 ? 1 : 128 / per;
   __shared__ int2 cs[16 * 64];   // [line][o1][o2]: (first block, number of blocks)
+  __shared__ uchar2 rowm[16 * 8];  // [line][o1]: o2 masks (occupied, several blocks)
   for (int l0 = blockIdx.x * L; l0 < nline; l0 += gridDim.x * L) {
     __syncthreads();
     int mine = 0;
@@ -339,6 +340,14 @@ k_asm_p12(const WinDev* __restrict__ wins, int w, const int2* __restrict__ celli
       }
       cs[k] = c;
       mine |= c.y > 0;
+      // per (line, o1) row of eight cells: which are occupied / split (a warp
+      // holds four whole rows; L * 64 is a multiple of 32, so it votes whole)
+      const unsigned occ = __ballot_sync(0xffffffffu, c.y > 0);
+      const unsigned ext = __ballot_sync(0xffffffffu, c.y > 1);
+      if ((k & 7) == 0) {
+        const int sh = k & 31;
+        rowm[k >> 3] = make_uchar2((occ >> sh) & 0xffu, (ext >> sh) & 0xffu);
+      }
     }
     const int any = __syncthreads_or(mine);
     const int nval = min(L, nline - l0) * per;
@@ -355,17 +364,21 @@ k_asm_p12(const WinDev* __restrict__ wins, int w, const int2* __restrict__ celli
       double sum = 0.0;
 #pragma unroll 2
       for (int o1 = 0; o1 < 8; ++o1) {
+        const uchar2 rm = rowm[li * 8 + o1];
+        if (rm.x == 0) continue;   // an empty row adds +0.0
         double inner = 0.0;
 #pragma unroll
         for (int o2 = 0; o2 < 8; ++o2) {
           const int2 c = cl[o1 * 8 + o2];
           if (c.y > 0) inner += __ldg(src + ((int64_t)c.x + o1 * 8 + o2) * nrhs);
         }
+        if (rm.y != 0) {
 #pragma unroll
-        for (int o2 = 0; o2 < 8; ++o2) {
-          const int2 c = cl[o1 * 8 + o2];
-          for (int q = 1; q < c.y; ++q)
-            inner += __ldg(src + ((int64_t)c.x + (int64_t)q * 512 + o1 * 8 + o2) * nrhs);
+          for (int o2 = 0; o2 < 8; ++o2) {
+            const int2 c = cl[o1 * 8 + o2];
+            for (int q = 1; q < c.y; ++q)
+              inner += __ldg(src + ((int64_t)c.x + (int64_t)q * 512 + o1 * 8 + o2) * nrhs);
+          }
         }
         sum += inner;
       }
